@@ -1,0 +1,469 @@
+"""ctypes binding of the CPU oracle (oracle/_build/libcpcag_oracle.so).
+
+TEST INFRASTRUCTURE ONLY.  The oracle is the checker for the CUDA product
+path: only tests/, ``__graft_entry__.smoke()`` and bench.py's
+``cpu_baseline`` / ``--impl reference`` legs may import this module.  The
+product package (paper_1602_02070_b200) never imports it.
+
+Every function restates a reference routine (see oracle/cpcag_oracle.cpp for
+the file:line each follows) and raises the reference's exception type with
+the reference's message.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "libcpcag_oracle.so")
+_lib = None
+
+i64 = C.c_int64
+dp = C.POINTER(C.c_double)
+ip = C.POINTER(C.c_int64)
+vp = C.c_void_p
+
+
+class FrpcagCfg(C.Structure):
+    _fields_ = [
+        ("gamma_r", C.c_double),
+        ("gamma_c", C.c_double),
+        ("loss_l2", C.c_int),
+        ("tol", C.c_double),
+        ("max_iter", C.c_int64),
+        ("step", C.c_double),
+    ]
+
+
+def build() -> str:
+    """Compile the oracle (make in oracle/); returns the .so path."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = C.CDLL(_LIB_PATH)
+        L.ora_last_error.restype = C.c_char_p
+        L.ora_csr_rows.restype = i64
+        L.ora_csr_cols.restype = i64
+        L.ora_csr_nnz.restype = i64
+        L.ora_rng_mix.restype = C.c_uint64
+        L.ora_rng_mix.argtypes = [C.c_uint64]
+        L.ora_rng_derive_seed.restype = C.c_uint64
+        L.ora_rng_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.ora_rng_u64.argtypes = [C.c_uint64, i64, C.POINTER(C.c_uint64)]
+        L.ora_rng_gaussian.argtypes = [C.c_uint64, i64, dp]
+        L.ora_power_iteration_norm.argtypes = [vp, C.c_double, C.c_uint64, i64, dp]
+        L.ora_draw_plan.argtypes = [i64, i64, i64, i64, C.c_uint64, ip, ip]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().ora_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)
+    if rc == 3:
+        raise IndexError(msg)
+    raise RuntimeError(msg)
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(dp)
+
+
+def _i(a: np.ndarray):
+    return a.ctypes.data_as(ip)
+
+
+def _f64(a) -> np.ndarray:
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _idx(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int64))
+
+
+def set_threads(n: int) -> None:
+    lib().ora_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().ora_get_threads())
+
+
+class Csr:
+    """Owning handle of an oracle CSR matrix (sparse.hpp:18-66 layout)."""
+
+    def __init__(self, handle):
+        self._h = handle if isinstance(handle, vp) else vp(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.ora_csr_free(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def rows(self) -> int:
+        return int(lib().ora_csr_rows(self._h))
+
+    @property
+    def cols(self) -> int:
+        return int(lib().ora_csr_cols(self._h))
+
+    @property
+    def nnz(self) -> int:
+        return int(lib().ora_csr_nnz(self._h))
+
+    def arrays(self):
+        rp = np.empty(self.rows + 1, np.int64)
+        ci = np.empty(self.nnz, np.int64)
+        v = np.empty(self.nnz, np.float64)
+        lib().ora_csr_export(self._h, _i(rp), _i(ci), _d(v))
+        return rp, ci, v
+
+    def to_dense(self) -> np.ndarray:
+        rp, ci, v = self.arrays()
+        D = np.zeros((self.rows, self.cols))
+        for r in range(self.rows):
+            D[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
+        return D
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+
+        rp, ci, v = self.arrays()
+        return sp.csr_matrix((v, ci, rp), shape=(self.rows, self.cols))
+
+    @staticmethod
+    def from_triplets(rows, cols, ti, tj, tv, drop_below=0.0) -> "Csr":
+        ti, tj, tv = _idx(ti), _idx(tj), np.ascontiguousarray(tv, np.float64)
+        out = vp()
+        _check(lib().ora_csr_from_triplets(i64(rows), i64(cols), i64(len(tv)), _i(ti), _i(tj),
+                                           _d(tv), C.c_double(drop_below), C.byref(out)))
+        return Csr(out)
+
+    @staticmethod
+    def from_csr(rows, cols, rp, ci, v) -> "Csr":
+        rp, ci, v = _idx(rp), _idx(ci), np.ascontiguousarray(v, np.float64)
+        out = vp()
+        _check(lib().ora_csr_from_csr(i64(rows), i64(cols), _i(rp), _i(ci), _d(v), C.byref(out)))
+        return Csr(out)
+
+    @staticmethod
+    def from_dense(D, drop_below=0.0) -> "Csr":
+        D = _f64(D)
+        out = vp()
+        _check(lib().ora_csr_from_dense(_d(D), i64(D.shape[0]), i64(D.shape[1]),
+                                        C.c_double(drop_below), C.byref(out)))
+        return Csr(out)
+
+    @staticmethod
+    def from_scipy(S) -> "Csr":
+        S = S.tocsr()
+        S.sort_indices()
+        return Csr.from_csr(S.shape[0], S.shape[1], S.indptr, S.indices, S.data)
+
+    def submatrix(self, rows, cols) -> "Csr":
+        rows, cols = _idx(rows), _idx(cols)
+        out = vp()
+        _check(lib().ora_csr_submatrix(self._h, _i(rows), i64(len(rows)), _i(cols),
+                                       i64(len(cols)), C.byref(out)))
+        return Csr(out)
+
+    def row_sums(self) -> np.ndarray:
+        out = np.empty(self.rows)
+        lib().ora_csr_row_sums(self._h, _d(out))
+        return out
+
+    def components(self):
+        lab = np.empty(self.rows, np.int64)
+        nc = i64()
+        _check(lib().ora_csr_components(self._h, _i(lab), C.byref(nc)))
+        return lab, int(nc.value)
+
+    def spmv(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.empty(self.rows)
+        _check(lib().ora_spmv(self._h, _d(x), i64(len(x)), _d(y)))
+        return y
+
+    def multiply(self, X) -> np.ndarray:
+        X = _f64(X)
+        if X.ndim == 1:
+            return self.spmv(X)
+        Y = np.empty((self.rows, X.shape[1]), order="F")
+        _check(lib().ora_spmm_left(self._h, _d(X), i64(X.shape[0]), i64(X.shape[1]), _d(Y)))
+        return Y
+
+    def right_multiply(self, X) -> np.ndarray:
+        X = _f64(X)
+        Y = np.empty((X.shape[0], self.cols), order="F")
+        _check(lib().ora_spmm_right(self._h, _d(X), i64(X.shape[0]), i64(X.shape[1]), _d(Y)))
+        return Y
+
+
+# ----------------------------------------------------------------- RNG
+def rng_mix(z: int) -> int:
+    return int(lib().ora_rng_mix(C.c_uint64(z & 0xFFFFFFFFFFFFFFFF)))
+
+
+def rng_derive_seed(seed: int, stream: int) -> int:
+    return int(lib().ora_rng_derive_seed(C.c_uint64(seed), C.c_uint64(stream)))
+
+
+def rng_u64(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count, np.uint64)
+    lib().ora_rng_u64(C.c_uint64(seed), i64(count), out.ctypes.data_as(C.POINTER(C.c_uint64)))
+    return out
+
+
+def rng_gaussian(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count)
+    lib().ora_rng_gaussian(C.c_uint64(seed), i64(count), _d(out))
+    return out
+
+
+def gaussian_matrix(rows: int, cols: int, seed: int) -> np.ndarray:
+    """oracles.hpp:26-32: CounterRng(mix(seed)), column-major fill."""
+    v = rng_gaussian(rng_mix(seed), rows * cols)
+    return v.reshape((rows, cols), order="F")
+
+
+# ----------------------------------------------------------------- solvers
+@dataclass
+class PcgResult:
+    iterations: int
+    converged: bool
+    relative_residual: float
+
+
+def pcg_solve(A: Csr, b, x=None, tol=1e-10, max_iter=5000, jacobi=True):
+    b = np.ascontiguousarray(b, np.float64)
+    x = np.zeros_like(b) if x is None else np.ascontiguousarray(x, np.float64).copy()
+    it, cv, rr = i64(), C.c_int(), C.c_double()
+    _check(lib().ora_pcg_solve(A.handle, _d(b), _d(x), i64(len(b)), C.c_double(tol),
+                               i64(max_iter), C.c_int(1 if jacobi else 0), C.byref(it),
+                               C.byref(cv), C.byref(rr)))
+    return x, PcgResult(int(it.value), bool(cv.value), float(rr.value))
+
+
+def power_iteration_norm(A: Csr, tol=1e-9, seed=0, max_iter=50000) -> float:
+    out = C.c_double()
+    _check(lib().ora_power_iteration_norm(A.handle, C.c_double(tol), C.c_uint64(seed),
+                                          i64(max_iter), C.byref(out)))
+    return float(out.value)
+
+
+# ----------------------------------------------------------------- graphs
+@dataclass
+class GraphModel:
+    n_nodes: int
+    K: int
+    sigma2: float
+    adjacency: Csr
+    degrees: np.ndarray
+    laplacian: Csr
+    normalized: bool = False
+
+
+def build_knn_graph(X, axis_rows: bool, K: int, normalized=False, sigma2_override=0.0):
+    X = _f64(X)
+    n = X.shape[0] if axis_rows else X.shape[1]
+    W, L = vp(), vp()
+    deg = np.empty(max(n, 0))
+    s2 = C.c_double()
+    _check(lib().ora_knn_graph(_d(X), i64(X.shape[0]), i64(X.shape[1]), C.c_int(int(axis_rows)),
+                               i64(K), C.c_int(int(normalized)), C.c_double(sigma2_override),
+                               C.byref(W), C.byref(L), _d(deg), C.byref(s2)))
+    return GraphModel(n, K, float(s2.value), Csr(W), deg, Csr(L), normalized)
+
+
+def knn_neighbors(X, axis_rows: bool, K: int):
+    X = _f64(X)
+    n = X.shape[0] if axis_rows else X.shape[1]
+    nbr = np.empty((n, K), np.int64)
+    d2 = np.empty((n, K))
+    _check(lib().ora_knn_neighbors(_d(X), i64(X.shape[0]), i64(X.shape[1]),
+                                   C.c_int(int(axis_rows)), i64(K), _i(nbr), _d(d2)))
+    return nbr, d2
+
+
+def graph_from_adjacency(W: Csr, normalized=False) -> GraphModel:
+    L = vp()
+    deg = np.empty(W.rows)
+    _check(lib().ora_graph_from_adjacency(W.handle, C.c_int(int(normalized)), C.byref(L), _d(deg)))
+    return GraphModel(W.rows, 0, 0.0, W, deg, Csr(L), normalized)
+
+
+def kron_reduce(L: Csr, keep, pcg_tol=1e-12, prune_tol=1e-12) -> Csr:
+    keep = _idx(keep)
+    out = vp()
+    _check(lib().ora_kron_reduce(L.handle, _i(keep), i64(len(keep)), C.c_double(pcg_tol),
+                                 C.c_double(prune_tol), C.byref(out)))
+    return Csr(out)
+
+
+# ----------------------------------------------------------------- sampling
+@dataclass
+class SamplingPlan:
+    omega_r: np.ndarray
+    omega_c: np.ndarray
+    p: int
+    n: int
+    delta: float = 0.0
+    epsilon: float = 0.0
+    seed: int = 0
+
+    @property
+    def rho_r(self):
+        return len(self.omega_r)
+
+    @property
+    def rho_c(self):
+        return len(self.omega_c)
+
+    def norm_const(self):
+        return (float(self.n) * float(self.p)) / (float(self.rho_r) * float(self.rho_c))
+
+
+def draw_plan(p, n, rho_r, rho_c, delta=0.0, epsilon=0.0, seed=0) -> SamplingPlan:
+    om_r = np.empty(max(rho_r, 0), np.int64)
+    om_c = np.empty(max(rho_c, 0), np.int64)
+    _check(lib().ora_draw_plan(i64(p), i64(n), i64(rho_r), i64(rho_c), C.c_uint64(seed),
+                               _i(om_r), _i(om_c)))
+    return SamplingPlan(om_r, om_c, p, n, delta, epsilon, seed)
+
+
+def subsample(Y, plan: SamplingPlan) -> np.ndarray:
+    Y = _f64(Y)
+    if Y.shape != (plan.p, plan.n):
+        raise ValueError("subsample: plan does not match matrix dimensions")
+    out = np.empty((plan.rho_r, plan.rho_c), order="F")
+    _check(lib().ora_subsample(_d(Y), i64(plan.p), i64(plan.n), _i(_idx(plan.omega_r)),
+                               i64(plan.rho_r), _i(_idx(plan.omega_c)), i64(plan.rho_c), _d(out)))
+    return out
+
+
+# ----------------------------------------------------------------- FRPCAG
+@dataclass
+class FrpcagConfig:
+    gamma_r: float = 1.0
+    gamma_c: float = 1.0
+    loss: str = "l1"
+    tol: float = 1e-10
+    max_iter: int = 500
+    step: float = 0.0
+
+    def c(self) -> FrpcagCfg:
+        return FrpcagCfg(self.gamma_r, self.gamma_c, 1 if self.loss == "l2" else 0, self.tol,
+                         self.max_iter, self.step)
+
+
+@dataclass
+class SolveTrace:
+    objective: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    final_rel_change: float = 0.0
+    step: float = 0.0
+
+
+def objective(X, Y, Lr: Csr, Lc: Csr, cfg: FrpcagConfig) -> float:
+    X, Y = _f64(X), _f64(Y)
+    if X.shape != Y.shape:
+        raise ValueError("frpcag: X and Y dimensions differ")
+    out = C.c_double()
+    c = cfg.c()
+    _check(lib().ora_objective(_d(X), _d(Y), i64(X.shape[0]), i64(X.shape[1]), Lr.handle,
+                               Lc.handle, C.byref(c), C.byref(out)))
+    return float(out.value)
+
+
+def prox_l1(Z, Y, lam) -> np.ndarray:
+    Z, Y = _f64(Z), _f64(Y)
+    if Z.shape != Y.shape:
+        raise ValueError("prox: Z and Y dimensions differ")
+    out = np.empty_like(Z, order="F")
+    _check(lib().ora_prox_l1(_d(Z), _d(Y), i64(Z.size), C.c_double(lam), _d(out)))
+    return out
+
+
+def prox_l2(Z, Y, lam) -> np.ndarray:
+    Z, Y = _f64(Z), _f64(Y)
+    if Z.shape != Y.shape:
+        raise ValueError("prox: Z and Y dimensions differ")
+    out = np.empty_like(Z, order="F")
+    _check(lib().ora_prox_l2(_d(Z), _d(Y), i64(Z.size), C.c_double(lam), _d(out)))
+    return out
+
+
+def grad_g(Z, Lr: Csr, Lc: Csr, cfg: FrpcagConfig) -> np.ndarray:
+    Z = _f64(Z)
+    G = np.empty_like(Z, order="F")
+    c = cfg.c()
+    _check(lib().ora_grad_g(_d(Z), i64(Z.shape[0]), i64(Z.shape[1]), Lr.handle, Lc.handle,
+                            C.byref(c), _d(G)))
+    return G
+
+
+def fista_solve(Y, Lr: Csr, Lc: Csr, cfg: FrpcagConfig):
+    Y = _f64(Y)
+    X = np.empty_like(Y, order="F")
+    obj = np.zeros(max(cfg.max_iter, 1))
+    it, cv, frc, st = i64(), C.c_int(), C.c_double(), C.c_double()
+    c = cfg.c()
+    _check(lib().ora_fista_solve(_d(Y), i64(Y.shape[0]), i64(Y.shape[1]), Lr.handle, Lc.handle,
+                                 C.byref(c), _d(X), _d(obj), C.byref(it), C.byref(cv),
+                                 C.byref(frc), C.byref(st)))
+    n = int(it.value)
+    return X, SolveTrace(list(obj[:n]), n, bool(cv.value), float(frc.value), float(st.value))
+
+
+# ----------------------------------------------------------------- decoder
+@dataclass
+class AlternateDecodeResult:
+    X: np.ndarray
+    converged: bool
+    iterations: int
+
+
+def alternate_decode(Xt, plan: SamplingPlan, Lr: Csr, Lc: Csr, lambda_k1_r: float,
+                     lambda_k1_c: float, gamma=1.0, pcg_tol=1e-10, pcg_max_iter=5000):
+    Xt = _f64(Xt)
+    X = np.empty((plan.p, plan.n), order="F")
+    cv, it = C.c_int(), i64()
+    if Xt.shape != (plan.rho_r, plan.rho_c):
+        raise ValueError("alternate decoder: Xt does not match plan")
+    _check(lib().ora_alternate_decode(_d(Xt), i64(plan.rho_r), i64(plan.rho_c),
+                                      _i(_idx(plan.omega_r)), _i(_idx(plan.omega_c)),
+                                      i64(plan.p), i64(plan.n), Lr.handle, Lc.handle,
+                                      C.c_double(lambda_k1_r), C.c_double(lambda_k1_c),
+                                      C.c_double(gamma), C.c_double(pcg_tol), i64(pcg_max_iter),
+                                      _d(X), C.byref(cv), C.byref(it)))
+    return AlternateDecodeResult(X, bool(cv.value), int(it.value))
+
+
+def decoder_apply(X, plan: SamplingPlan, Lr: Csr, Lc: Csr, gbar_r: float, gbar_c: float):
+    X = _f64(X)
+    out = np.empty_like(X, order="F")
+    _check(lib().ora_decoder_apply(_d(X), i64(plan.p), i64(plan.n), _i(_idx(plan.omega_r)),
+                                   i64(plan.rho_r), _i(_idx(plan.omega_c)), i64(plan.rho_c),
+                                   Lr.handle, Lc.handle, C.c_double(gbar_r), C.c_double(gbar_c),
+                                   _d(out)))
+    return out
