@@ -1,0 +1,241 @@
+/*
+ * cpcag_cuda.h -- C-ABI of the B200 (sm_100a) implementation of the CPCA hot
+ * path (Compressive PCA on graphs, arXiv 1602.02070).
+ *
+ * This is the drop-in boundary: every entry point replaces one public
+ * function of the reference library `cpcag` (proj/core/include/cpcag/*.hpp,
+ * cited per function) with the same argument meaning, the same defaults
+ * (documented per argument) and the same error behaviour: a nonzero status
+ * maps back to the reference exception type and cpcag_cuda_last_error()
+ * returns the reference's message text.
+ *
+ * Conventions
+ *   - Dense matrices are column-major (types.hpp:12-13).  Element type is
+ *     double for CPCAG_F64 and float for CPCAG_F32 (`precision` argument).
+ *   - Every array argument may be host memory (pageable or pinned) or
+ *     device memory of the context's device; the library detects which
+ *     (cudaPointerGetAttributes) and stages host arrays through HBM inside
+ *     the call.  Device arrays are used in place (no copies).
+ *   - Index lists are int64 (types.hpp:10,16).
+ *   - Sparse matrices live on the device as cpcag_csr handles (CSR with
+ *     int64 row pointers, sorted int32 column indices, fp64 values; the
+ *     invariants of sparse.hpp:15-17).  Handles are created from host or
+ *     device CSR arrays or returned by the graph routines, and are
+ *     immutable.
+ *   - Calls on one context are serialised on its stream; contexts are
+ *     independent, so distinct threads may use distinct contexts
+ *     concurrently.  The last-error text is thread-local.
+ *   - No CPU fallback: without a usable sm_100 device every call returns
+ *     CPCAG_ERR_CUDA.
+ */
+#ifndef CPCAG_CUDA_H
+#define CPCAG_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum cpcag_status {
+  CPCAG_OK = 0,
+  CPCAG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+  CPCAG_ERR_RUNTIME = 2,          /* std::runtime_error */
+  CPCAG_ERR_OUT_OF_RANGE = 3,     /* std::out_of_range */
+  CPCAG_ERR_CUDA = 4              /* device/driver failure (no reference analogue) */
+};
+
+enum cpcag_precision { CPCAG_F64 = 0, CPCAG_F32 = 1 };
+enum cpcag_axis { CPCAG_AXIS_ROWS = 0, CPCAG_AXIS_COLS = 1 };           /* graph.hpp:11 */
+enum cpcag_laplacian_kind { CPCAG_COMBINATORIAL = 0, CPCAG_NORMALIZED = 1 }; /* graph.hpp:10 */
+enum cpcag_loss { CPCAG_LOSS_L1 = 0, CPCAG_LOSS_L2 = 1 };                 /* frpcag.hpp:11 */
+enum cpcag_spmm_side { CPCAG_LEFT = 0 /* Y = A X */, CPCAG_RIGHT = 1 /* Y = X A */ };
+
+typedef struct cpcag_ctx_s* cpcag_ctx;
+typedef struct cpcag_csr_s* cpcag_csr;
+
+/* Thread-local text of the last failure (the reference's exception message). */
+const char* cpcag_cuda_last_error(void);
+/* Library version string and the compiled device architecture ("sm_100a"). */
+const char* cpcag_cuda_version(void);
+
+/* ------------------------------------------------------------------ context */
+/* device < 0 selects the current device.  The context owns a non-blocking
+ * stream, a workspace cache and pinned staging buffers. */
+int cpcag_ctx_create(int device, cpcag_ctx* out);
+int cpcag_ctx_destroy(cpcag_ctx ctx);
+/* Use an external stream (e.g. torch.cuda.current_stream()); NULL restores
+ * the context's own stream. */
+int cpcag_ctx_set_stream(cpcag_ctx ctx, void* cuda_stream);
+void* cpcag_ctx_stream(cpcag_ctx ctx);
+int cpcag_ctx_synchronize(cpcag_ctx ctx);
+/* Number of kernels this context has launched since creation (or reset). */
+int64_t cpcag_ctx_launch_count(cpcag_ctx ctx);
+void cpcag_ctx_reset_launch_count(cpcag_ctx ctx);
+
+/* ------------------------------------------------------------------ sparse */
+/* SparseMatrix from CSR arrays (sparse.hpp:18-66).  The arrays must already
+ * satisfy the CSR invariants (monotone row_ptr, strictly increasing columns
+ * per row, finite values); violations return CPCAG_ERR_INVALID_ARGUMENT.
+ * Exact zeros are dropped as SparseMatrix::from_triplets does. */
+int cpcag_csr_create(cpcag_ctx ctx, int64_t rows, int64_t cols, int64_t nnz,
+                     const int64_t* row_ptr, const int64_t* col_idx, const double* values,
+                     cpcag_csr* out);
+int cpcag_csr_destroy(cpcag_csr a);
+int cpcag_csr_info(cpcag_csr a, int64_t* rows, int64_t* cols, int64_t* nnz);
+/* Copy the CSR out (host or device destinations; any may be NULL). */
+int cpcag_csr_export(cpcag_ctx ctx, cpcag_csr a, int64_t* row_ptr, int64_t* col_idx,
+                     double* values);
+/* 1 when A == A^T bit for bit (what every Laplacian built here satisfies). */
+int cpcag_csr_is_symmetric(cpcag_csr a);
+
+/* SparseMatrix::multiply(Matrix) / right_multiply(Matrix)
+ * (sparse.hpp:41-45, sparse.cpp:87-111).  side = CPCAG_LEFT: Y = A X with X
+ * (A.cols x m); CPCAG_RIGHT: Y = X A with X (m x A.rows).  Per output entry
+ * the accumulation order is the reference's (CSR order, starting from 0), so
+ * CPCAG_F64 results are bit-identical to the reference loop. */
+int cpcag_cuda_spmm(cpcag_ctx ctx, cpcag_csr A, int side, int precision, int64_t x_rows,
+                    int64_t x_cols, const void* X, void* Y);
+/* SparseMatrix::multiply(Vector) (sparse.cpp:73-85). */
+int cpcag_cuda_spmv(cpcag_ctx ctx, cpcag_csr A, int precision, int64_t n, const void* x, void* y);
+
+/* power_iteration_norm (solvers.hpp:90-91, solvers.cpp:29-53); defaults in
+ * the reference: tol 1e-9, seed 0, max_iter 50000. */
+int cpcag_cuda_power_norm(cpcag_ctx ctx, cpcag_csr A, double tol, uint64_t seed,
+                          int64_t max_iter, double* out);
+
+/* pcg_solve(const SparseMatrix&, b, x, opt, jacobi) (solvers.hpp:82-86,
+ * solvers.cpp:19-27): x is the start iterate and receives the solution. */
+int cpcag_cuda_pcg_solve(cpcag_ctx ctx, cpcag_csr A, const double* b, double* x, int64_t n,
+                         double tol, int64_t max_iter, int jacobi, int64_t* iterations,
+                         int* converged, double* relative_residual);
+
+/* ------------------------------------------------------------------ graphs */
+/* build_knn_graph (graph.hpp:29-31, graph.cpp:47-135).  X is x_rows x x_cols;
+ * axis selects whether points are rows or columns.  Defaults in the
+ * reference: kind = combinatorial, sigma2_override = 0 (automatic).
+ * Outputs: adjacency W and Laplacian L handles, degrees (length n, host or
+ * device), sigma2.  The neighbour sets follow the reference's canonical fp64
+ * distance d2 = max(0, g_ii + g_jj - 2 g_ij) with ties toward the lower
+ * index, bit-exactly. */
+int cpcag_cuda_knn_graph(cpcag_ctx ctx, int precision, const void* X, int64_t x_rows,
+                         int64_t x_cols, int axis, int64_t K, int kind, double sigma2_override,
+                         cpcag_csr* adjacency, cpcag_csr* laplacian, double* degrees,
+                         double* sigma2);
+/* The K nearest neighbours per point (ascending (d2, index)) without the
+ * graph assembly; nbr and nbr_d2 are n x K row-major. */
+int cpcag_cuda_knn(cpcag_ctx ctx, int precision, const void* X, int64_t x_rows, int64_t x_cols,
+                   int axis, int64_t K, int64_t* nbr, double* nbr_d2);
+
+/* graph_from_adjacency (graph.hpp:35-36, graph.cpp:137-154). */
+int cpcag_cuda_graph_from_adjacency(cpcag_ctx ctx, cpcag_csr W, int kind, cpcag_csr* laplacian,
+                                    double* degrees);
+
+/* kron_reduce (graph.hpp:50-51, graph.cpp:170-235).  Reference defaults:
+ * pcg_tol 1e-12, prune_tol 1e-12 (run_pipeline passes 1e-11). */
+int cpcag_cuda_kron_reduce(cpcag_ctx ctx, cpcag_csr L, const int64_t* keep, int64_t n_keep,
+                           double pcg_tol, double prune_tol, cpcag_csr* out);
+
+/* ------------------------------------------------------------------ sampling */
+/* draw_plan (sampling.hpp:39-40, sampling.cpp:48-64).  Host-side by design:
+ * it is O(rho) integer work on the reference's counter RNG and its output
+ * must be bit-identical; omega_r/omega_c receive the draw order. */
+int cpcag_cuda_draw_plan(int64_t p, int64_t n, int64_t rho_r, int64_t rho_c, uint64_t seed,
+                         int64_t* omega_r, int64_t* omega_c);
+/* subsample (sampling.hpp:43, sampling.cpp:66-75): out(i,j) = Y(om_r[i], om_c[j]). */
+int cpcag_cuda_subsample(cpcag_ctx ctx, int precision, const void* Y, int64_t p, int64_t n,
+                         const int64_t* omega_r, int64_t rho_r, const int64_t* omega_c,
+                         int64_t rho_c, void* out);
+
+/* ------------------------------------------------------------------ FRPCAG */
+typedef struct cpcag_frpcag_config { /* FrpcagConfig, frpcag.hpp:15-22 */
+  double gamma_r;   /* default 1 */
+  double gamma_c;   /* default 1 */
+  int loss;         /* CPCAG_LOSS_L1 (default) or CPCAG_LOSS_L2 */
+  double tol;       /* default 1e-10: stop when ||Z+ - Z||^2 < tol ||Z||^2 */
+  int64_t max_iter; /* default 500 */
+  double step;      /* 0 = auto: 1 / (2 gc ||Lc|| + 2 gr ||Lr||) */
+} cpcag_frpcag_config;
+
+typedef struct cpcag_solve_trace { /* SolveTrace, frpcag.hpp:24-30 (objective separate) */
+  int64_t iterations;
+  int converged;
+  double final_rel_change;
+  double step;
+} cpcag_solve_trace;
+
+/* objective / prox_l1 / prox_l2 / grad_g (frpcag.hpp:32-43). */
+int cpcag_cuda_objective(cpcag_ctx ctx, int precision, const void* X, const void* Y,
+                         int64_t rows, int64_t cols, cpcag_csr Lr, cpcag_csr Lc,
+                         const cpcag_frpcag_config* cfg, double* out);
+int cpcag_cuda_prox(cpcag_ctx ctx, int precision, int loss, const void* Z, const void* Y,
+                    int64_t count, double lam, void* out);
+int cpcag_cuda_grad_g(cpcag_ctx ctx, int precision, const void* Z, int64_t rows, int64_t cols,
+                      cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg, void* G);
+
+/* fista_solve (frpcag.hpp:46-47, frpcag.cpp:62-112).  Y is rows x cols; X
+ * receives the last prox output; objective (may be NULL) receives one value
+ * per iteration (capacity cfg->max_iter). */
+int cpcag_cuda_fista(cpcag_ctx ctx, int precision, const void* Y, int64_t rows, int64_t cols,
+                     cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg, void* X,
+                     double* objective, cpcag_solve_trace* trace);
+
+/* ------------------------------------------------------------------ decoder */
+typedef struct cpcag_decoder_config { /* DecoderConfig fields used by alternate_decode */
+  double gamma;         /* default 1; scaled by 1/lambda_{k+1} per side */
+  double pcg_tol;       /* default 1e-10 */
+  int64_t pcg_max_iter; /* default 5000 */
+} cpcag_decoder_config;
+
+/* alternate_decode (decoders.hpp:59-62, decoders.cpp:145-186): CG on
+ * M o X + gbar_c X Lc + gbar_r Lr X = scatter(Xt), X0 = 0, no
+ * preconditioner, gbar = gamma / lambda_k1 (SpectralGap::lambda_k1).
+ * Xt is rho_r x rho_c; X receives the p x n solution.  Non-convergence is a
+ * flag, not an error (decoders.cpp:185). */
+int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, int64_t rho_r,
+                                int64_t rho_c, const int64_t* omega_r, const int64_t* omega_c,
+                                int64_t p, int64_t n, cpcag_csr Lr, cpcag_csr Lc,
+                                double lambda_k1_r, double lambda_k1_c,
+                                const cpcag_decoder_config* cfg, void* X, int* converged,
+                                int64_t* iterations);
+
+/* ------------------------------------------------------------------ pipeline */
+typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36-63 */
+  int64_t knn;               /* default 10 */
+  int laplacian;             /* default combinatorial */
+  double sigma2;             /* 0 = automatic */
+  int64_t a, b;              /* downsampling: rho_c = ceil(n/a), rho_r = ceil(p/b) */
+  int64_t rho_r_override, rho_c_override;
+  double kron_pcg_tol;       /* default 1e-11 */
+  cpcag_frpcag_config frpcag;
+  cpcag_decoder_config decoder;
+  double lambda_k1_r, lambda_k1_c; /* SpectralGap::lambda_k1 supplied by the caller */
+  uint64_t seed;
+} cpcag_pipeline_config;
+
+typedef struct cpcag_pipeline_report { /* PipelineReport subset, pipeline.hpp:73-94 */
+  int64_t p, n, rho_r, rho_c;
+  cpcag_solve_trace trace;
+  int decoder_converged;
+  int64_t decoder_iterations;
+  /* Stage timings in ms (device events), in the reference's stage order:
+   * graphs, plan, subsample, kron, solve, decode (pipeline.cpp:273-350). */
+  double stage_ms[6];
+} cpcag_pipeline_report;
+
+/* run_pipeline, low-rank task with the alternate decoder (pipeline.cpp:228-
+ * 350): graphs (row graph from W_r when given, else kNN over rows; column
+ * graph from W_c when given, else kNN over columns) -> plan -> subsample ->
+ * Kron -> FISTA -> alternate decode.  Y is p x n.  Xt (rho_r x rho_c) and X
+ * (p x n) receive the compressed and decoded solutions; omega_r/omega_c
+ * (may be NULL) receive the plan; objective (may be NULL) the FISTA trace. */
+int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void* Y, int64_t p, int64_t n,
+                            cpcag_csr W_r, cpcag_csr W_c, const cpcag_pipeline_config* cfg,
+                            void* Xt, void* X, int64_t* omega_r, int64_t* omega_c,
+                            double* objective, cpcag_pipeline_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPCAG_CUDA_H */

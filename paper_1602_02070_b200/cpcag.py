@@ -1,0 +1,681 @@
+"""Python mirror of the reference `cpcag` API for the CPCA hot path.
+
+Same names, argument meaning, defaults and exceptions as the C++ reference
+(proj/core/include/cpcag/*.hpp; file:line per function below), executed by
+libcpcag_cuda.so on the GPU through the C-ABI in include/cpcag_cuda.h.
+
+Arrays: numpy arrays (host) or torch tensors (host or CUDA) are accepted;
+dense matrices are column-major as in the reference (types.hpp:12-13).
+Results come back as numpy arrays for host inputs and as CUDA tensors
+(column-major strides) for CUDA inputs, so a caller that keeps its data in
+HBM never round-trips through the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+
+__all__ = [
+    "Context", "SparseMatrix", "GraphModel", "SamplingPlan", "FrpcagConfig", "SolveTrace",
+    "DecoderConfig", "SpectralGap", "AlternateDecodeResult", "PcgOptions", "PcgResult",
+    "PipelineConfig", "PipelineReport", "build_knn_graph", "knn", "graph_from_adjacency",
+    "kron_reduce", "draw_plan", "subsample", "objective", "prox_l1", "prox_l2", "grad_g",
+    "fista_solve", "alternate_decode", "power_iteration_norm", "pcg_solve", "run_pipeline",
+    "default_context",
+]
+
+
+# ------------------------------------------------------------------ arrays
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _is_cuda(x) -> bool:
+    return _is_torch(x) and x.is_cuda
+
+
+def _np_dtype(precision: int):
+    return np.float64 if precision == N.F64 else np.float32
+
+
+class _In:
+    """Pointer to a caller array in the requested precision, column-major."""
+
+    def __init__(self, x, precision: int, shape=None, kind="float"):
+        self.keep = None
+        if _is_torch(x):
+            torch = _torch()
+            dt = torch.int64 if kind == "index" else (torch.float64 if precision == N.F64 else torch.float32)
+            t = x.detach()
+            if t.dtype != dt:
+                t = t.to(dt)
+            if t.dim() == 2 and not (t.stride(0) == 1 and t.stride(1) == max(t.shape[0], 1)):
+                t = t.t().contiguous().t()
+            elif t.dim() != 2 and not t.is_contiguous():
+                t = t.contiguous()
+            if not t.is_cuda:
+                t = t.numpy()
+                self._from_numpy(t, precision, kind)
+            else:
+                self.keep = t
+                self.ptr = t.data_ptr()
+                self.shape = tuple(t.shape)
+        else:
+            self._from_numpy(x, precision, kind)
+        if shape is not None and tuple(self.shape) != tuple(shape):
+            raise ValueError(f"array shape {self.shape} does not match the expected {shape}")
+
+    def _from_numpy(self, x, precision, kind):
+        dt = np.int64 if kind == "index" else _np_dtype(precision)
+        a = np.asarray(x, dtype=dt)
+        a = np.asfortranarray(a) if a.ndim == 2 else np.ascontiguousarray(a)
+        self.keep = a
+        self.ptr = a.ctypes.data if a.size else None
+        self.shape = a.shape
+
+
+def _out(like_cuda, device, shape, precision: int, kind="float"):
+    """Column-major output buffer: CUDA tensor when inputs are CUDA, else numpy."""
+    if like_cuda:
+        torch = _torch()
+        dt = torch.int64 if kind == "index" else (torch.float64 if precision == N.F64 else torch.float32)
+        if len(shape) == 2:
+            t = torch.empty((shape[1], shape[0]), dtype=dt, device=device).t()
+        else:
+            t = torch.empty(shape, dtype=dt, device=device)
+        return t, t.data_ptr()
+    dt = np.int64 if kind == "index" else _np_dtype(precision)
+    a = np.empty(shape, dtype=dt, order="F")
+    return a, (a.ctypes.data if a.size else None)
+
+
+def _precision(x, precision):
+    if precision is not None:
+        return N.F32 if precision in (N.F32, "f32", "float32", np.float32) else N.F64
+    if _is_torch(x):
+        return N.F32 if x.dtype == _torch().float32 else N.F64
+    if isinstance(x, np.ndarray) and x.dtype == np.float32:
+        return N.F32
+    return N.F64
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """A device, a CUDA stream and a workspace (cpcag_ctx)."""
+
+    def __init__(self, device: int = -1):
+        L = N.lib()
+        h = N.vp()
+        N.check(L.cpcag_ctx_create(int(device), C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: Optional[int]):
+        N.check(N.lib().cpcag_ctx_set_stream(self._h, stream_ptr))
+
+    def synchronize(self):
+        N.check(N.lib().cpcag_ctx_synchronize(self._h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(N.lib().cpcag_ctx_launch_count(self._h))
+
+    def reset_launch_count(self):
+        N.lib().cpcag_ctx_reset_launch_count(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            N.lib().cpcag_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(-1)
+    return _default_ctx
+
+
+def _ctx(ctx):
+    return (ctx or default_context()).handle
+
+
+def _torch_device(x):
+    return x.device if _is_cuda(x) else None
+
+
+# ------------------------------------------------------------------ sparse
+class SparseMatrix:
+    """Device CSR (sparse.hpp:18-66): int64 row pointers, sorted columns, fp64
+    values, no stored zeros.  Immutable."""
+
+    def __init__(self, handle, ctx: Optional[Context] = None):
+        self._h = handle if isinstance(handle, N.vp) else N.vp(handle)
+        self._ctx = ctx or default_context()
+
+    def __del__(self):
+        try:
+            if self._h is not None and self._h.value:
+                N.lib().cpcag_csr_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        r, c, z = N.i64(), N.i64(), N.i64()
+        N.check(N.lib().cpcag_csr_info(self._h, C.byref(r), C.byref(c), C.byref(z)))
+        return int(r.value), int(c.value), int(z.value)
+
+    def rows(self) -> int:
+        return self._info()[0]
+
+    def cols(self) -> int:
+        return self._info()[1]
+
+    def nonzeros(self) -> int:
+        return self._info()[2]
+
+    @property
+    def shape(self):
+        r, c, _ = self._info()
+        return (r, c)
+
+    # sparse.cpp:10-46 (host-side construction utility; the CSR is then
+    # uploaded once and every product runs on the device).
+    @staticmethod
+    def from_triplets(rows, cols, ti, tj, tv, drop_below=0.0, ctx=None) -> "SparseMatrix":
+        ti = np.asarray(ti, np.int64).ravel()
+        tj = np.asarray(tj, np.int64).ravel()
+        tv = np.asarray(tv, np.float64).ravel()
+        if rows < 0 or cols < 0:
+            raise ValueError("sparse: negative dimensions")
+        if ti.size and (ti.min() < 0 or ti.max() >= rows or tj.min() < 0 or tj.max() >= cols):
+            raise ValueError("sparse: triplet index out of range")
+        if not np.all(np.isfinite(tv)):
+            raise ValueError("sparse: non-finite entry")
+        order = np.lexsort((tj, ti))
+        ti, tj, tv = ti[order], tj[order], tv[order]
+        if ti.size:
+            key = ti * max(cols, 1) + tj
+            start = np.concatenate(([True], key[1:] != key[:-1]))
+            grp = np.cumsum(start) - 1
+            vals = np.zeros(int(grp[-1]) + 1)
+            # sequential per-group sums in input order (np.add.at is unbuffered)
+            np.add.at(vals, grp, tv)
+            ui, uj = ti[start], tj[start]
+            keep = (vals != 0.0) & (np.abs(vals) > drop_below)
+            ui, uj, vals = ui[keep], uj[keep], vals[keep]
+        else:
+            ui, uj, vals = ti, tj, tv
+        rp = np.zeros(rows + 1, np.int64)
+        np.add.at(rp, ui + 1, 1)
+        rp = np.cumsum(rp)
+        return SparseMatrix.from_csr(rows, cols, rp, uj, vals, ctx=ctx)
+
+    @staticmethod
+    def from_csr(rows, cols, row_ptr, col_idx, values, ctx=None) -> "SparseMatrix":
+        ctx = ctx or default_context()
+        rp = _In(row_ptr, N.F64, kind="index")
+        ci = _In(col_idx, N.F64, kind="index")
+        v = _In(values, N.F64)
+        nnz = int(row_ptr[-1]) if len(row_ptr) else 0
+        h = N.vp()
+        N.check(N.lib().cpcag_csr_create(ctx.handle, int(rows), int(cols), nnz, rp.ptr, ci.ptr, v.ptr,
+                                         C.byref(h)))
+        return SparseMatrix(h, ctx)
+
+    @staticmethod
+    def from_scipy(S, ctx=None) -> "SparseMatrix":
+        S = S.tocsr().copy()
+        S.sort_indices()
+        S.sum_duplicates()
+        return SparseMatrix.from_csr(S.shape[0], S.shape[1], S.indptr.astype(np.int64),
+                                     S.indices.astype(np.int64), S.data.astype(np.float64), ctx=ctx)
+
+    @staticmethod
+    def from_dense(D, drop_below=0.0, ctx=None) -> "SparseMatrix":
+        D = np.asarray(D, np.float64)
+        i, j = np.nonzero(D)
+        return SparseMatrix.from_triplets(D.shape[0], D.shape[1], i, j, D[i, j], drop_below, ctx)
+
+    def arrays(self):
+        r, c, z = self._info()
+        rp = np.empty(r + 1, np.int64)
+        ci = np.empty(z, np.int64)
+        v = np.empty(z, np.float64)
+        N.check(N.lib().cpcag_csr_export(self._ctx.handle, self._h, rp.ctypes.data,
+                                         ci.ctypes.data if z else None, v.ctypes.data if z else None))
+        return rp, ci, v
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+
+        rp, ci, v = self.arrays()
+        return sp.csr_matrix((v, ci, rp), shape=self.shape)
+
+    def to_dense(self) -> np.ndarray:
+        return self.to_scipy().toarray()
+
+    def is_symmetric(self) -> bool:
+        return bool(N.lib().cpcag_csr_is_symmetric(self._h))
+
+    # sparse.cpp:73-98
+    def multiply(self, X, precision=None):
+        prec = _precision(X, precision)
+        if (X.ndim if hasattr(X, "ndim") else np.ndim(X)) == 1:
+            x = _In(X, prec)
+            r, c, _ = self._info()
+            y, yp = _out(_is_cuda(X), _torch_device(X), (r,), prec)
+            N.check(N.lib().cpcag_cuda_spmv(self._ctx.handle, self._h, prec, x.shape[0], x.ptr, yp))
+            return y
+        x = _In(X, prec)
+        r, c, _ = self._info()
+        y, yp = _out(_is_cuda(X), _torch_device(X), (r, x.shape[1]), prec)
+        N.check(N.lib().cpcag_cuda_spmm(self._ctx.handle, self._h, N.LEFT, prec, x.shape[0],
+                                        x.shape[1], x.ptr, yp))
+        return y
+
+    # sparse.cpp:100-111
+    def right_multiply(self, X, precision=None):
+        prec = _precision(X, precision)
+        x = _In(X, prec)
+        r, c, _ = self._info()
+        y, yp = _out(_is_cuda(X), _torch_device(X), (x.shape[0], c), prec)
+        N.check(N.lib().cpcag_cuda_spmm(self._ctx.handle, self._h, N.RIGHT, prec, x.shape[0],
+                                        x.shape[1], x.ptr, yp))
+        return y
+
+
+# ------------------------------------------------------------------ solvers
+@dataclass
+class PcgOptions:  # solvers.hpp:13-16
+    tol: float = 1e-10
+    max_iter: int = 5000
+
+
+@dataclass
+class PcgResult:  # solvers.hpp:18-22
+    iterations: int = 0
+    converged: bool = False
+    relative_residual: float = 0.0
+
+
+def power_iteration_norm(A: SparseMatrix, tol=1e-9, seed=0, max_iter=50000, ctx=None) -> float:
+    """solvers.hpp:90-91 / solvers.cpp:29-53."""
+    out = N.dbl()
+    N.check(N.lib().cpcag_cuda_power_norm(_ctx(ctx), A.handle, float(tol), int(seed) & (2**64 - 1),
+                                          int(max_iter), C.byref(out)))
+    return float(out.value)
+
+
+def pcg_solve(A: SparseMatrix, b, x=None, opt: PcgOptions = PcgOptions(), jacobi=True, ctx=None):
+    """solvers.hpp:85-86 / solvers.cpp:19-27.  Returns (x, PcgResult)."""
+    b = np.ascontiguousarray(b, np.float64)
+    xv = np.zeros_like(b) if x is None or np.size(x) != b.size else np.array(x, np.float64)
+    it, cv, rr = N.i64(), C.c_int(), N.dbl()
+    N.check(N.lib().cpcag_cuda_pcg_solve(_ctx(ctx), A.handle, b.ctypes.data, xv.ctypes.data, b.size,
+                                         float(opt.tol), int(opt.max_iter), int(bool(jacobi)),
+                                         C.byref(it), C.byref(cv), C.byref(rr)))
+    return xv, PcgResult(int(it.value), bool(cv.value), float(rr.value))
+
+
+# ------------------------------------------------------------------ graphs
+@dataclass
+class GraphModel:  # graph.hpp:13-21
+    n_nodes: int
+    K: int
+    sigma2: float
+    adjacency: SparseMatrix
+    degrees: np.ndarray
+    laplacian: SparseMatrix
+    kind: int = N.COMBINATORIAL
+
+
+def _axis(axis) -> int:
+    if axis in ("rows", N.AXIS_ROWS):
+        return N.AXIS_ROWS
+    if axis in ("cols", N.AXIS_COLS):
+        return N.AXIS_COLS
+    raise ValueError("axis must be 'rows' or 'cols'")
+
+
+def _kind(kind) -> int:
+    if kind in ("combinatorial", N.COMBINATORIAL):
+        return N.COMBINATORIAL
+    if kind in ("normalized", N.NORMALIZED):
+        return N.NORMALIZED
+    raise ValueError("unknown laplacian kind")
+
+
+def build_knn_graph(X, axis, K: int, kind="combinatorial", sigma2_override=0.0, precision=None,
+                    ctx=None) -> GraphModel:
+    """graph.hpp:29-31 / graph.cpp:47-135."""
+    prec = _precision(X, precision)
+    x = _In(X, prec)
+    if len(x.shape) != 2:
+        raise ValueError("knn graph: X must be a matrix")
+    ax = _axis(axis)
+    n = x.shape[0] if ax == N.AXIS_ROWS else x.shape[1]
+    W, L = N.vp(), N.vp()
+    deg = np.empty(max(n, 0))
+    s2 = N.dbl()
+    N.check(N.lib().cpcag_cuda_knn_graph(_ctx(ctx), prec, x.ptr, x.shape[0], x.shape[1], ax, int(K),
+                                         _kind(kind), float(sigma2_override), C.byref(W), C.byref(L),
+                                         deg.ctypes.data if n > 0 else None, C.byref(s2)))
+    c = ctx or default_context()
+    return GraphModel(n, int(K), float(s2.value), SparseMatrix(W, c), deg, SparseMatrix(L, c), _kind(kind))
+
+
+def knn(X, axis, K: int, precision=None, ctx=None):
+    """Neighbour lists of build_knn_graph (graph.cpp:86-105): (n x K indices, n x K d2)."""
+    prec = _precision(X, precision)
+    x = _In(X, prec)
+    ax = _axis(axis)
+    n = x.shape[0] if ax == N.AXIS_ROWS else x.shape[1]
+    nbr = np.empty((n, K), np.int64)
+    d2 = np.empty((n, K), np.float64)
+    N.check(N.lib().cpcag_cuda_knn(_ctx(ctx), prec, x.ptr, x.shape[0], x.shape[1], ax, int(K),
+                                   nbr.ctypes.data, d2.ctypes.data))
+    return nbr, d2
+
+
+def graph_from_adjacency(W: SparseMatrix, kind="combinatorial", ctx=None) -> GraphModel:
+    """graph.hpp:35-36 / graph.cpp:137-154."""
+    L = N.vp()
+    n = W.rows()
+    deg = np.empty(n)
+    N.check(N.lib().cpcag_cuda_graph_from_adjacency(_ctx(ctx), W.handle, _kind(kind), C.byref(L),
+                                                    deg.ctypes.data if n else None))
+    return GraphModel(n, 0, 0.0, W, deg, SparseMatrix(L, ctx or default_context()), _kind(kind))
+
+
+def kron_reduce(L: SparseMatrix, keep, pcg_tol=1e-12, prune_tol=1e-12, ctx=None) -> SparseMatrix:
+    """graph.hpp:50-51 / graph.cpp:170-235."""
+    k = _In(keep, N.F64, kind="index")
+    out = N.vp()
+    N.check(N.lib().cpcag_cuda_kron_reduce(_ctx(ctx), L.handle, k.ptr, int(k.shape[0]), float(pcg_tol),
+                                           float(prune_tol), C.byref(out)))
+    return SparseMatrix(out, ctx or default_context())
+
+
+# ------------------------------------------------------------------ sampling
+@dataclass
+class SamplingPlan:  # sampling.hpp:13-26
+    omega_r: np.ndarray
+    omega_c: np.ndarray
+    p: int = 0
+    n: int = 0
+    delta: float = 0.0
+    epsilon: float = 0.0
+    seed: int = 0
+
+    def rho_r(self) -> int:
+        return len(self.omega_r)
+
+    def rho_c(self) -> int:
+        return len(self.omega_c)
+
+    def norm_const(self) -> float:
+        return (float(self.n) * float(self.p)) / (float(self.rho_r()) * float(self.rho_c()))
+
+
+def draw_plan(p, n, rho_r, rho_c, delta=0.0, epsilon=0.0, seed=0) -> SamplingPlan:
+    """sampling.hpp:39-40 / sampling.cpp:48-64 (host: bit-exact counter RNG)."""
+    om_r = np.empty(max(int(rho_r), 0), np.int64)
+    om_c = np.empty(max(int(rho_c), 0), np.int64)
+    N.check(N.lib().cpcag_cuda_draw_plan(int(p), int(n), int(rho_r), int(rho_c),
+                                         int(seed) & (2**64 - 1),
+                                         om_r.ctypes.data if om_r.size else None,
+                                         om_c.ctypes.data if om_c.size else None))
+    return SamplingPlan(om_r, om_c, int(p), int(n), float(delta), float(epsilon), int(seed))
+
+
+def subsample(Y, plan: SamplingPlan, precision=None, ctx=None):
+    """sampling.hpp:43 / sampling.cpp:66-75."""
+    prec = _precision(Y, precision)
+    y = _In(Y, prec)
+    if tuple(y.shape) != (plan.p, plan.n):
+        raise ValueError("subsample: plan does not match matrix dimensions")
+    om_r = np.ascontiguousarray(plan.omega_r, np.int64)
+    om_c = np.ascontiguousarray(plan.omega_c, np.int64)
+    out, op = _out(_is_cuda(Y), _torch_device(Y), (plan.rho_r(), plan.rho_c()), prec)
+    N.check(N.lib().cpcag_cuda_subsample(_ctx(ctx), prec, y.ptr, plan.p, plan.n, om_r.ctypes.data,
+                                         plan.rho_r(), om_c.ctypes.data, plan.rho_c(), op))
+    return out
+
+
+# ------------------------------------------------------------------ FRPCAG
+@dataclass
+class FrpcagConfig:  # frpcag.hpp:15-22
+    gamma_r: float = 1.0
+    gamma_c: float = 1.0
+    loss: str = "l1"
+    tol: float = 1e-10
+    max_iter: int = 500
+    step: float = 0.0
+
+    def c(self) -> N.FrpcagConfigC:
+        return N.FrpcagConfigC(self.gamma_r, self.gamma_c, N.LOSS_L2 if self.loss == "l2" else N.LOSS_L1,
+                               self.tol, int(self.max_iter), self.step)
+
+
+@dataclass
+class SolveTrace:  # frpcag.hpp:24-30
+    objective: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    final_rel_change: float = 0.0
+    step: float = 0.0
+
+
+def objective(X, Y, Lr: SparseMatrix, Lc: SparseMatrix, cfg: FrpcagConfig, precision=None, ctx=None) -> float:
+    """frpcag.hpp:32-33 / frpcag.cpp:23-35."""
+    prec = _precision(X, precision)
+    x, y = _In(X, prec), _In(Y, prec)
+    if x.shape != y.shape:
+        raise ValueError("frpcag: X and Y dimensions differ")
+    out = N.dbl()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_objective(_ctx(ctx), prec, x.ptr, y.ptr, x.shape[0], x.shape[1], Lr.handle,
+                                         Lc.handle, C.byref(c), C.byref(out)))
+    return float(out.value)
+
+
+def _prox(loss, Z, Y, lam, precision, ctx):
+    prec = _precision(Z, precision)
+    z, y = _In(Z, prec), _In(Y, prec)
+    if z.shape != y.shape:
+        raise ValueError("prox: Z and Y dimensions differ")
+    out, op = _out(_is_cuda(Z), _torch_device(Z), z.shape, prec)
+    N.check(N.lib().cpcag_cuda_prox(_ctx(ctx), prec, loss, z.ptr, y.ptr, int(np.prod(z.shape)), float(lam), op))
+    return out
+
+
+def prox_l1(Z, Y, lam, precision=None, ctx=None):
+    """frpcag.hpp:36 / frpcag.cpp:37-44."""
+    return _prox(N.LOSS_L1, Z, Y, lam, precision, ctx)
+
+
+def prox_l2(Z, Y, lam, precision=None, ctx=None):
+    """frpcag.hpp:39 / frpcag.cpp:46-51."""
+    return _prox(N.LOSS_L2, Z, Y, lam, precision, ctx)
+
+
+def grad_g(Z, Lr: SparseMatrix, Lc: SparseMatrix, cfg: FrpcagConfig, precision=None, ctx=None):
+    """frpcag.hpp:42-43 / frpcag.cpp:53-60."""
+    prec = _precision(Z, precision)
+    z = _In(Z, prec)
+    out, op = _out(_is_cuda(Z), _torch_device(Z), z.shape, prec)
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_grad_g(_ctx(ctx), prec, z.ptr, z.shape[0], z.shape[1], Lr.handle, Lc.handle,
+                                      C.byref(c), op))
+    return out
+
+
+def fista_solve(Y, Lr: SparseMatrix, Lc: SparseMatrix, cfg: FrpcagConfig, precision=None, ctx=None):
+    """frpcag.hpp:46-47 / frpcag.cpp:62-112.  Returns (X, SolveTrace)."""
+    prec = _precision(Y, precision)
+    y = _In(Y, prec)
+    if len(y.shape) != 2:
+        raise ValueError("fista: Y must be a matrix")
+    out, op = _out(_is_cuda(Y), _torch_device(Y), y.shape, prec)
+    obj = np.zeros(max(int(cfg.max_iter), 1))
+    tr = N.SolveTraceC()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_fista(_ctx(ctx), prec, y.ptr, y.shape[0], y.shape[1], Lr.handle, Lc.handle,
+                                     C.byref(c), op, obj.ctypes.data, C.byref(tr)))
+    n = int(tr.iterations)
+    return out, SolveTrace(list(obj[:n]), n, bool(tr.converged), float(tr.final_rel_change), float(tr.step))
+
+
+# ------------------------------------------------------------------ decoder
+@dataclass
+class DecoderConfig:  # decoders.hpp:13-22 (fields used by the alternate decoder)
+    gamma: float = 1.0
+    pcg_tol: float = 1e-10
+    pcg_max_iter: int = 5000
+
+    def c(self) -> N.DecoderConfigC:
+        return N.DecoderConfigC(self.gamma, self.pcg_tol, int(self.pcg_max_iter))
+
+
+@dataclass
+class SpectralGap:  # graph.hpp:53-58
+    k: int = 0
+    lambda_k: float = 0.0
+    lambda_k1: float = 0.0
+    ratio: float = 0.0
+
+
+@dataclass
+class AlternateDecodeResult:  # decoders.hpp:50-54
+    X: object
+    converged: bool
+    iterations: int
+
+
+def alternate_decode(Xt, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix, gap_r: SpectralGap,
+                     gap_c: SpectralGap, cfg: DecoderConfig = DecoderConfig(), precision=None,
+                     ctx=None) -> AlternateDecodeResult:
+    """decoders.hpp:59-62 / decoders.cpp:145-186."""
+    prec = _precision(Xt, precision)
+    xt = _In(Xt, prec)
+    if tuple(xt.shape) != (plan.rho_r(), plan.rho_c()):
+        raise ValueError("alternate decoder: Xt does not match plan")
+    om_r = np.ascontiguousarray(plan.omega_r, np.int64)
+    om_c = np.ascontiguousarray(plan.omega_c, np.int64)
+    out, op = _out(_is_cuda(Xt), _torch_device(Xt), (plan.p, plan.n), prec)
+    cv, it = C.c_int(), N.i64()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_alternate_decode(_ctx(ctx), prec, xt.ptr, plan.rho_r(), plan.rho_c(),
+                                                om_r.ctypes.data if om_r.size else None,
+                                                om_c.ctypes.data if om_c.size else None, plan.p, plan.n,
+                                                Lr.handle, Lc.handle, float(gap_r.lambda_k1),
+                                                float(gap_c.lambda_k1), C.byref(c), op, C.byref(cv),
+                                                C.byref(it)))
+    return AlternateDecodeResult(out, bool(cv.value), int(it.value))
+
+
+# ------------------------------------------------------------------ pipeline
+STAGES = ("graphs", "plan", "subsample", "kron", "solve", "decode")
+
+
+@dataclass
+class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
+    knn: int = 10
+    laplacian: str = "combinatorial"
+    sigma2: float = 0.0
+    a: int = 1
+    b: int = 1
+    rho_r_override: int = 0
+    rho_c_override: int = 0
+    kron_pcg_tol: float = 1e-11
+    frpcag: FrpcagConfig = field(default_factory=FrpcagConfig)
+    decoder: DecoderConfig = field(default_factory=DecoderConfig)
+    lambda_k1_r: float = 1.0
+    lambda_k1_c: float = 1.0
+    seed: int = 0
+
+    def c(self) -> N.PipelineConfigC:
+        return N.PipelineConfigC(int(self.knn), _kind(self.laplacian), float(self.sigma2), int(self.a),
+                                 int(self.b), int(self.rho_r_override), int(self.rho_c_override),
+                                 float(self.kron_pcg_tol), self.frpcag.c(), self.decoder.c(),
+                                 float(self.lambda_k1_r), float(self.lambda_k1_c),
+                                 int(self.seed) & (2**64 - 1))
+
+
+@dataclass
+class PipelineReport:  # pipeline.hpp:73-94 (subset)
+    p: int
+    n: int
+    rho_r: int
+    rho_c: int
+    trace: SolveTrace
+    plan: SamplingPlan
+    Xt: object
+    X: object
+    decoder_converged: bool
+    decoder_iterations: int
+    stages: dict
+
+    def stage_ms(self, name: str) -> float:
+        return self.stages.get(name, 0.0)
+
+
+def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
+                 W_c: Optional[SparseMatrix] = None, precision=None, ctx=None) -> PipelineReport:
+    """pipeline.hpp:100 / pipeline.cpp:228-350 on a resident data matrix Y (p x n)."""
+    prec = _precision(Y, precision)
+    y = _In(Y, prec)
+    p, n = y.shape
+    rho_r = cfg.rho_r_override if cfg.rho_r_override > 0 else -(-p // max(cfg.b, 1))
+    rho_c = cfg.rho_c_override if cfg.rho_c_override > 0 else -(-n // max(cfg.a, 1))
+    rho_r, rho_c = min(rho_r, p), min(rho_c, n)
+    cuda = _is_cuda(Y)
+    xt, xtp = _out(cuda, _torch_device(Y), (rho_r, rho_c), prec)
+    x, xp = _out(cuda, _torch_device(Y), (p, n), prec)
+    om_r = np.empty(max(rho_r, 1), np.int64)
+    om_c = np.empty(max(rho_c, 1), np.int64)
+    obj = np.zeros(max(int(cfg.frpcag.max_iter), 1))
+    rep = N.PipelineReportC()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_run_pipeline(_ctx(ctx), prec, y.ptr, p, n, W_r.handle if W_r else None,
+                                            W_c.handle if W_c else None, C.byref(c), xtp, xp,
+                                            om_r.ctypes.data, om_c.ctypes.data, obj.ctypes.data,
+                                            C.byref(rep)))
+    it = int(rep.trace.iterations)
+    trace = SolveTrace(list(obj[:it]), it, bool(rep.trace.converged), float(rep.trace.final_rel_change),
+                       float(rep.trace.step))
+    plan = SamplingPlan(om_r[:rep.rho_r].copy(), om_c[:rep.rho_c].copy(), p, n, seed=cfg.seed)
+    stages = {name: float(rep.stage_ms[k]) for k, name in enumerate(STAGES)}
+    return PipelineReport(int(rep.p), int(rep.n), int(rep.rho_r), int(rep.rho_c), trace, plan, xt, x,
+                          bool(rep.decoder_converged), int(rep.decoder_iterations), stages)

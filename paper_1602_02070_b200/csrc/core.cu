@@ -1,0 +1,842 @@
+// core.cu -- context, device CSR operator, SpMM/SpMV, power iteration,
+// sampling plan + gather, and the element-wise FRPCAG operators.
+//
+// Reference: proj/core/src/sparse.cpp (CSR, SpMV/SpMM), solvers.cpp:29-53
+// (power iteration), sampling.cpp:35-75 (plan, subsample), frpcag.cpp:23-60
+// (objective, prox, gradient).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <numeric>
+
+#include "common.cuh"
+#include "frpcag.cuh"
+
+namespace cpcag_cuda {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+double HostRng::gaussian() {
+  if (has_spare) {
+    has_spare = false;
+    return spare;
+  }
+  double a = uniform();
+  while (a <= 0.0) a = uniform();
+  const double b = uniform();
+  const double rad = std::sqrt(-2.0 * std::log(a));
+  const double tau = 6.283185307179586476925286766559;
+  spare = rad * std::sin(tau * b);
+  has_spare = true;
+  return rad * std::cos(tau * b);
+}
+
+// ------------------------------------------------------------------ CSR
+Csr::~Csr() {
+  cudaFree(rp);
+  cudaFree(ci);
+  cudaFree(v);
+  cudaFree(v32);
+  cudaFree(t_rp);
+  cudaFree(t_ci);
+  cudaFree(t_v);
+  cudaFree(t_v32);
+}
+
+Csr* csr_alloc(Ctx* c, i64 rows, i64 cols, i64 nnz) {
+  Csr* a = new Csr();
+  a->rows = rows;
+  a->cols = cols;
+  a->nnz = nnz;
+  a->device = c->device;
+  try {
+    CUDA_OK(cudaMalloc(&a->rp, sizeof(i64) * (rows + 1)));
+    CUDA_OK(cudaMemsetAsync(a->rp, 0, sizeof(i64) * (rows + 1), c->stream));
+    if (nnz) {
+      CUDA_OK(cudaMalloc(&a->ci, sizeof(int) * nnz));
+      CUDA_OK(cudaMalloc(&a->v, sizeof(double) * nnz));
+    }
+  } catch (...) {
+    delete a;
+    throw;
+  }
+  return a;
+}
+
+__global__ void to_f32_k(const double* __restrict__ a, float* __restrict__ b, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    b[i] = static_cast<float>(a[i]);
+}
+
+template <>
+const double* csr_values<double>(Ctx*, Csr* a) {
+  return a->v;
+}
+template <>
+const float* csr_values<float>(Ctx* c, Csr* a) {
+  if (!a->v32 && a->nnz) {
+    CUDA_OK(cudaMalloc(&a->v32, sizeof(float) * a->nnz));
+    to_f32_k<<<stride_blocks(c, a->nnz), kBlock, 0, c->stream>>>(a->v, a->v32, a->nnz);
+    launched(c);
+  }
+  return a->v32;
+}
+
+// Exact symmetry: every (r, c, v) has (c, r, v) with the same bits.
+__global__ void sym_check_k(i64 rows, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, int* asym) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) {
+    const int c = ci[k];
+    i64 lo = rp[c], hi = rp[c + 1];
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (ci[mid] < r) lo = mid + 1; else hi = mid;
+    }
+    if (lo == rp[c + 1] || ci[lo] != r ||
+        __double_as_longlong(v[lo]) != __double_as_longlong(v[k])) {
+      *asym = 1;
+      return;
+    }
+  }
+}
+
+int csr_symmetric(Ctx* c, Csr* a) {
+  if (a->sym >= 0) return a->sym;
+  if (a->rows != a->cols) return a->sym = 0;
+  DevBuf<int> flag(c, 1);
+  flag.zero(c);
+  if (a->rows) {
+    sym_check_k<<<blocks_for(a->rows), kBlock, 0, c->stream>>>(a->rows, a->rp, a->ci, a->v, flag.p);
+    launched(c);
+  }
+  const int asym = read_back(c, flag.p);
+  return a->sym = asym ? 0 : 1;
+}
+
+__global__ void expand_rows_k(i64 rows, const i64* __restrict__ rp, int* __restrict__ row_of) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) row_of[k] = static_cast<int>(r);
+}
+
+__global__ void gather_perm_k(i64 nnz, const int* __restrict__ perm, const int* __restrict__ row_of,
+                              const double* __restrict__ v, int* __restrict__ t_ci,
+                              double* __restrict__ t_v) {
+  const i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (k >= nnz) return;
+  const int src = perm[k];
+  t_ci[k] = row_of[src];
+  t_v[k] = v[src];
+}
+
+__global__ void count_cols_k(i64 nnz, const int* __restrict__ sorted_cols, i64 cols, i64* t_rp) {
+  // t_rp[c+1] = number of entries with column <= c, via upper bounds on the
+  // sorted column list (one thread per column).
+  const i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (c > cols) return;
+  if (c == 0) {
+    t_rp[0] = 0;
+    return;
+  }
+  i64 lo = 0, hi = nnz;
+  const int key = static_cast<int>(c - 1);
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (sorted_cols[mid] <= key) lo = mid + 1; else hi = mid;
+  }
+  t_rp[c] = lo;
+}
+
+__global__ void iota_k(i64 n, int* out) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<int>(i);
+}
+
+// A^T as CSR (stable radix sort of entries by column keeps rows ascending
+// within each column: the order sparse.cpp:100-111 accumulates in).
+void csr_build_transpose(Ctx* c, Csr* a) {
+  if (a->t_rp) return;
+  const i64 nnz = a->nnz;
+  CUDA_OK(cudaMalloc(&a->t_rp, sizeof(i64) * (a->cols + 1)));
+  if (nnz == 0) {
+    CUDA_OK(cudaMemsetAsync(a->t_rp, 0, sizeof(i64) * (a->cols + 1), c->stream));
+    return;
+  }
+  CUDA_OK(cudaMalloc(&a->t_ci, sizeof(int) * nnz));
+  CUDA_OK(cudaMalloc(&a->t_v, sizeof(double) * nnz));
+  DevBuf<int> keys_out(c, nnz), idx(c, nnz), idx_out(c, nnz), row_of(c, nnz);
+  iota_k<<<blocks_for(nnz), kBlock, 0, c->stream>>>(nnz, idx.p);
+  launched(c);
+  expand_rows_k<<<blocks_for(a->rows), kBlock, 0, c->stream>>>(a->rows, a->rp, row_of.p);
+  launched(c);
+  size_t tmp = 0;
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, a->ci, keys_out.p, idx.p, idx_out.p,
+                                          static_cast<int>(nnz), 0, 32, c->stream));
+  DevBuf<char> ws(c, tmp);
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(ws.p, tmp, a->ci, keys_out.p, idx.p, idx_out.p,
+                                          static_cast<int>(nnz), 0, 32, c->stream));
+  launched(c);
+  gather_perm_k<<<blocks_for(nnz), kBlock, 0, c->stream>>>(nnz, idx_out.p, row_of.p, a->v,
+                                                           a->t_ci, a->t_v);
+  launched(c);
+  count_cols_k<<<blocks_for(a->cols + 1), kBlock, 0, c->stream>>>(nnz, keys_out.p, a->cols, a->t_rp);
+  launched(c);
+}
+
+template <>
+const double* csr_t_values<double>(Ctx* c, Csr* a) {
+  csr_build_transpose(c, a);
+  return a->t_v;
+}
+template <>
+const float* csr_t_values<float>(Ctx* c, Csr* a) {
+  csr_build_transpose(c, a);
+  if (!a->t_v32 && a->nnz) {
+    CUDA_OK(cudaMalloc(&a->t_v32, sizeof(float) * a->nnz));
+    to_f32_k<<<stride_blocks(c, a->nnz), kBlock, 0, c->stream>>>(a->t_v, a->t_v32, a->nnz);
+    launched(c);
+  }
+  return a->t_v32;
+}
+
+// Column-pull view of A for X*A: A itself when exactly symmetric, else A^T.
+template <typename T>
+struct PullView {
+  const i64* rp;
+  const int* ci;
+  const T* v;
+};
+template <typename T>
+PullView<T> pull_view(Ctx* c, Csr* a) {
+  if (csr_symmetric(c, a)) return {a->rp, a->ci, csr_values<T>(c, a)};
+  const T* tv = csr_t_values<T>(c, a);
+  return {a->t_rp, a->t_ci, tv};
+}
+
+// ------------------------------------------------------------------ SpMM
+// Y(r, j) = sum_k v_k X(c_k, j), CSR order, explicit mul then add
+// (sparse.cpp:87-98).  Threads run down a column of Y (coalesced stores).
+template <typename T>
+__global__ void spmm_left_k(i64 rows, i64 m, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const T* __restrict__ v, const T* __restrict__ X, i64 ldx,
+                            T* __restrict__ Y) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const i64 k0 = rp[r], k1 = rp[r + 1];
+  for (i64 j = blockIdx.y; j < m; j += gridDim.y) {
+    Y[r + j * rows] = pull_left(k0, k1, ci, v, X + j * ldx);
+  }
+}
+
+// Y(i, c) = sum over rows r of A holding column c (ascending) of A(r,c) X(i,r)
+// (sparse.cpp:100-111), pulled over row c of A^T.
+template <typename T>
+__global__ void spmm_right_k(i64 xr, i64 cols, const i64* __restrict__ rp, const int* __restrict__ ci,
+                             const T* __restrict__ v, const T* __restrict__ X, T* __restrict__ Y) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= xr) return;
+  for (i64 c = blockIdx.y; c < cols; c += gridDim.y) {
+    Y[i + c * xr] = pull_right(rp[c], rp[c + 1], ci, v, X, xr, i);
+  }
+}
+
+template <typename T>
+void spmm_left(Ctx* c, Csr* A, const T* X, i64 m, T* Y) {
+  if (A->rows == 0 || m == 0) return;
+  dim3 g(blocks_for(A->rows), static_cast<unsigned>(std::min<i64>(m, 65535)));
+  spmm_left_k<T><<<g, kBlock, 0, c->stream>>>(A->rows, m, A->rp, A->ci, csr_values<T>(c, A), X,
+                                              A->cols, Y);
+  launched(c);
+}
+
+template <typename T>
+void spmm_right(Ctx* c, Csr* A, const T* X, i64 m, T* Y) {
+  if (A->cols == 0 || m == 0) return;
+  const PullView<T> pv = pull_view<T>(c, A);
+  dim3 g(blocks_for(m), static_cast<unsigned>(std::min<i64>(A->cols, 65535)));
+  spmm_right_k<T><<<g, kBlock, 0, c->stream>>>(m, A->cols, pv.rp, pv.ci, pv.v, X, Y);
+  launched(c);
+}
+
+template void spmm_left<double>(Ctx*, Csr*, const double*, i64, double*);
+template void spmm_left<float>(Ctx*, Csr*, const float*, i64, float*);
+template void spmm_right<double>(Ctx*, Csr*, const double*, i64, double*);
+template void spmm_right<float>(Ctx*, Csr*, const float*, i64, float*);
+
+// ------------------------------------------------------------------ dots
+template <typename T>
+__global__ void dot_k(const T* __restrict__ a, const T* __restrict__ b, i64 n, double* partials,
+                      unsigned* counter, double* out) {
+  double s[1] = {0.0};
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    s[0] += static_cast<double>(a[i]) * static_cast<double>(b[i]);
+  double t[1];
+  if (grid_sum_last<1>(s, partials, counter, t) && threadIdx.x == 0) *out = t[0];
+}
+
+template <typename T>
+void dot_device(Ctx* c, const T* a, const T* b, i64 n, double* out_dev) {
+  const unsigned nb = stride_blocks(c, n);
+  DevBuf<double> part(c, nb);
+  DevBuf<unsigned> cnt(c, 1);
+  cnt.zero(c);
+  dot_k<T><<<nb, kBlock, 0, c->stream>>>(a, b, n, part.p, cnt.p, out_dev);
+  launched(c);
+}
+template void dot_device<double>(Ctx*, const double*, const double*, i64, double*);
+template void dot_device<float>(Ctx*, const float*, const float*, i64, double*);
+
+// ------------------------------------------------------------------ power iteration
+// solvers.cpp:29-53 as one cooperative kernel: w = A v (CSR order), ||w|| by
+// a fixed-order grid reduction every block evaluates identically, v = w/||w||,
+// stop when |est - prev| <= tol est.  v0 comes from the reference RNG on the
+// host (bit-identical).
+struct PowerState {
+  double est;
+  i64 iterations;
+  unsigned bar_count, bar_gen;
+};
+
+__global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                             const double* __restrict__ val, double* v, double* w, double* partials,
+                             double tol, i64 max_iter, PowerState* st) {
+  const i64 gtid = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  const i64 gstride = (i64)gridDim.x * blockDim.x;
+  const unsigned nb = gridDim.x;
+  double est = 0.0;
+  i64 it = 0;
+  for (; it < max_iter; ++it) {
+    double s[1] = {0.0};
+    for (i64 r = gtid; r < n; r += gstride) {
+      double acc = 0.0;
+      for (i64 k = rp[r]; k < rp[r + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(val[k], __ldcg(v + ci[k])));
+      w[r] = acc;
+      s[0] += acc * acc;
+    }
+    block_sum<1>(s);
+    if (threadIdx.x == 0) partials[(it & 1) * nb + blockIdx.x] = s[0];
+    grid_barrier(&st->bar_count, &st->bar_gen);
+    double t[1] = {0.0};
+    for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) t[0] += __ldcg(partials + (it & 1) * nb + i);
+    block_sum<1>(t);
+    const double nw = sqrt(t[0]);
+    if (nw == 0.0) {
+      est = 0.0;
+      break;
+    }
+    const double prev = est;
+    est = nw;
+    for (i64 r = gtid; r < n; r += gstride) v[r] = __ddiv_rn(w[r], nw);
+    if (it > 0 && fabs(est - prev) <= tol * est) {
+      ++it;
+      break;
+    }
+    grid_barrier(&st->bar_count, &st->bar_gen);
+  }
+  if (gtid == 0) {
+    st->est = est;
+    st->iterations = it;
+  }
+}
+
+double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
+  if (A->rows != A->cols) invalid("power iteration: square matrix required");
+  const i64 n = A->rows;
+  if (n == 0) return 0.0;
+  HostRng rng(HostRng::mix(seed ^ 0x5ca1ab1eULL));
+  std::vector<double> v0(static_cast<size_t>(n));
+  for (i64 i = 0; i < n; ++i) v0[i] = rng.gaussian();
+  double nv = 0.0;
+  for (i64 i = 0; i < n; ++i) nv += v0[i] * v0[i];
+  nv = std::sqrt(nv);
+  if (nv == 0.0) return 0.0;
+  for (double& x : v0) x /= nv;
+  if (max_iter <= 0) return 0.0;
+  DevBuf<double> v(c, n), w(c, n);
+  CUDA_OK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_k, kBlock, 0));
+  const i64 want = (n + kBlock - 1) / kBlock;
+  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(want, (i64)per_sm * c->num_sms)));
+  DevBuf<double> part(c, 2 * nb);
+  DevBuf<PowerState> st(c, 1);
+  st.zero(c);
+  const i64* rp = A->rp;
+  const int* ci = A->ci;
+  const double* val = A->v;
+  double* vp = v.p;
+  double* wp = w.p;
+  double* pp = part.p;
+  PowerState* sp = st.p;
+  void* args[] = {(void*)&n, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp,
+                  (void*)&pp, (void*)&tol, (void*)&max_iter, (void*)&sp};
+  CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_k, dim3(nb), dim3(kBlock), args, 0, c->stream));
+  launched(c);
+  const PowerState out = read_back(c, st.p);
+  return out.est;
+}
+
+// ------------------------------------------------------------------ gather / prox / grad / objective
+template <typename T>
+__global__ void subsample_k(const T* __restrict__ Y, i64 p, const i64* __restrict__ om_r, i64 rho_r,
+                            const i64* __restrict__ om_c, i64 rho_c, T* __restrict__ out) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= rho_r) return;
+  const i64 r = om_r[i];
+  for (i64 j = blockIdx.y; j < rho_c; j += gridDim.y) out[i + j * rho_r] = Y[r + om_c[j] * p];
+}
+
+template <typename T>
+void subsample_device(Ctx* c, const T* Y, i64 p, const i64* om_r, i64 rho_r, const i64* om_c,
+                      i64 rho_c, T* out) {
+  if (rho_r == 0 || rho_c == 0) return;
+  dim3 g(blocks_for(rho_r), static_cast<unsigned>(std::min<i64>(rho_c, 65535)));
+  subsample_k<T><<<g, kBlock, 0, c->stream>>>(Y, p, om_r, rho_r, om_c, rho_c, out);
+  launched(c);
+}
+template void subsample_device<double>(Ctx*, const double*, i64, const i64*, i64, const i64*, i64, double*);
+template void subsample_device<float>(Ctx*, const float*, i64, const i64*, i64, const i64*, i64, float*);
+
+template <typename T>
+__global__ void prox_k(int loss, const T* __restrict__ Z, const T* __restrict__ Y, i64 n, T lam,
+                       T* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(Z[i], Y[i], lam) : prox_l1_elem(Z[i], Y[i], lam);
+}
+
+template <typename T>
+__global__ void grad_k(i64 rows, i64 cols, Pull<T> Lr, Pull<T> Lc, T s_r, T s_c, int use_r,
+                       int use_c, const T* __restrict__ Z, T* __restrict__ G) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (i64 c = blockIdx.y; c < cols; c += gridDim.y)
+    G[i + c * rows] = grad_elem(Lr, Lc, s_r, s_c, use_r, use_c, Z, rows, i, c);
+}
+
+// Partial sums for objective(): phi(Y - X), sum (X Lc) o X, sum (Lr X) o X.
+template <typename T>
+__global__ void objective_k(i64 rows, i64 cols, Pull<T> Lr, Pull<T> Lc, int loss, int use_r,
+                            int use_c, const T* __restrict__ X, const T* __restrict__ Y,
+                            double* partials, unsigned* counter, double3* out) {
+  double s[3] = {0.0, 0.0, 0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < rows) {
+    for (i64 c = blockIdx.y; c < cols; c += gridDim.y) {
+      const i64 at = i + c * rows;
+      const double e = static_cast<double>(Y[at]) - static_cast<double>(X[at]);
+      s[0] += loss == CPCAG_LOSS_L2 ? e * e : fabs(e);
+      const double x = static_cast<double>(X[at]);
+      if (use_c) s[1] += static_cast<double>(pull_right(Lc.rp[c], Lc.rp[c + 1], Lc.ci, Lc.v, X, rows, i)) * x;
+      if (use_r) s[2] += static_cast<double>(pull_left(Lr.rp[i], Lr.rp[i + 1], Lr.ci, Lr.v, X + c * rows)) * x;
+    }
+  }
+  double t[3];
+  if (grid_sum_last<3>(s, partials, counter, t) && threadIdx.x == 0) *out = make_double3(t[0], t[1], t[2]);
+}
+
+template <typename T>
+Pull<T> make_pull(Ctx* c, Csr* A, bool right) {
+  if (!right) return Pull<T>{A->rp, A->ci, csr_values<T>(c, A)};
+  const PullView<T> pv = pull_view<T>(c, A);
+  return Pull<T>{pv.rp, pv.ci, pv.v};
+}
+template Pull<double> make_pull<double>(Ctx*, Csr*, bool);
+template Pull<float> make_pull<float>(Ctx*, Csr*, bool);
+
+void frpcag_check_dims(i64 rows, i64 cols, Csr* Lr, Csr* Lc) {
+  if (Lr->rows != Lr->cols || Lr->rows != rows) invalid("frpcag: row Laplacian does not match X");
+  if (Lc->rows != Lc->cols || Lc->rows != cols) invalid("frpcag: column Laplacian does not match X");
+}
+
+template <typename T>
+double objective_device(Ctx* c, const T* X, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
+                        const cpcag_frpcag_config& cfg) {
+  frpcag_check_dims(rows, cols, Lr, Lc);
+  const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
+  dim3 g(blocks_for(rows), static_cast<unsigned>(std::min<i64>(std::max<i64>(cols, 1), 65535)));
+  const unsigned nb = g.x * g.y;
+  DevBuf<double> part(c, 3 * nb);
+  DevBuf<unsigned> cnt(c, 1);
+  cnt.zero(c);
+  DevBuf<double3> out(c, 1);
+  CUDA_OK(cudaMemsetAsync(out.p, 0, sizeof(double3), c->stream));
+  if (rows > 0 && cols > 0) {
+    objective_k<T><<<g, kBlock, 0, c->stream>>>(rows, cols, pr, pc, cfg.loss, cfg.gamma_r != 0.0,
+                                                cfg.gamma_c != 0.0, X, Y, part.p, cnt.p, out.p);
+    launched(c);
+  }
+  const double3 s = read_back(c, out.p);
+  double val = s.x;
+  if (cfg.gamma_c != 0.0) val += cfg.gamma_c * s.y;
+  if (cfg.gamma_r != 0.0) val += cfg.gamma_r * s.z;
+  return val;
+}
+
+std::vector<i64> draw_indices(i64 n, i64 take, HostRng rng) {
+  std::vector<i64> pool(static_cast<size_t>(n));
+  std::iota(pool.begin(), pool.end(), i64{0});
+  for (i64 i = 0; i < take; ++i) {
+    const i64 j = i + static_cast<i64>(rng.below(static_cast<uint64_t>(n - i)));
+    std::swap(pool[static_cast<size_t>(i)], pool[static_cast<size_t>(j)]);
+  }
+  pool.resize(static_cast<size_t>(take));
+  return pool;
+}
+
+template <typename T>
+size_t esize() {
+  return sizeof(T);
+}
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+namespace {
+template <class F>
+int dispatch(int precision, F&& f) {
+  if (precision == CPCAG_F64) return f(double{});
+  if (precision == CPCAG_F32) return f(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}
+
+std::vector<i64> host_list(Ctx* c, const int64_t* p, int64_t n) {
+  std::vector<i64> out(static_cast<size_t>(n > 0 ? n : 0));
+  if (n <= 0) return out;
+  if (is_device_ptr(p)) {
+    CUDA_OK(cudaMemcpyAsync(out.data(), p, sizeof(i64) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  } else {
+    std::memcpy(out.data(), p, sizeof(i64) * n);
+  }
+  return out;
+}
+}  // namespace
+
+extern "C" {
+
+const char* cpcag_cuda_last_error(void) { return g_last_error.c_str(); }
+
+const char* cpcag_cuda_version(void) { return "cpcag-b200 0.1 sm_100a"; }
+
+int cpcag_ctx_create(int device, cpcag_ctx* out) {
+  return guard([&] {
+    if (!out) invalid("null output pointer");
+    int dev = device;
+    if (dev < 0) CUDA_OK(cudaGetDevice(&dev));
+    CUDA_OK(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    CUDA_OK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+      fail(CPCAG_ERR_CUDA, "cpcag_cuda: device " + std::to_string(dev) + " is sm_" +
+                               std::to_string(prop.major) + std::to_string(prop.minor) +
+                               "; this library is built for sm_100a only");
+    Ctx* c = new Ctx();
+    c->device = dev;
+    c->num_sms = prop.multiProcessorCount;
+    CUDA_OK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    c->stream = c->own;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = reinterpret_cast<cpcag_ctx>(c);
+  });
+}
+
+int cpcag_ctx_destroy(cpcag_ctx ctx) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    cudaStreamSynchronize(c->stream);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    cudaStreamDestroy(c->own);
+    delete c;
+  });
+}
+
+int cpcag_ctx_set_stream(cpcag_ctx ctx, void* s) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    c->stream = s ? reinterpret_cast<cudaStream_t>(s) : c->own;
+  });
+}
+
+void* cpcag_ctx_stream(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->stream : nullptr; }
+
+int cpcag_ctx_synchronize(cpcag_ctx ctx) {
+  return guard([&] { sync(as_ctx(ctx)); });
+}
+
+int64_t cpcag_ctx_launch_count(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->launches : 0; }
+void cpcag_ctx_reset_launch_count(cpcag_ctx ctx) {
+  if (ctx) reinterpret_cast<Ctx*>(ctx)->launches = 0;
+}
+
+int cpcag_csr_create(cpcag_ctx ctx, int64_t rows, int64_t cols, int64_t nnz, const int64_t* row_ptr,
+                     const int64_t* col_idx, const double* values, cpcag_csr* out) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (!out) invalid("null output pointer");
+    if (rows < 0 || cols < 0) invalid("sparse: negative dimensions");
+    if (cols > INT32_MAX) invalid("sparse: more than 2^31-1 columns are not supported");
+    // Validation of the CSR invariants (sparse.hpp:15-17) on the host copy:
+    // one pass over the index arrays, done once per handle.
+    std::vector<i64> rp(static_cast<size_t>(rows) + 1);
+    std::vector<i64> ci(static_cast<size_t>(nnz));
+    std::vector<double> v(static_cast<size_t>(nnz));
+    auto fetch = [&](void* dst, const void* src, size_t bytes) {
+      if (!bytes) return;
+      if (is_device_ptr(src))
+        CUDA_OK(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(dst, src, bytes);
+    };
+    fetch(rp.data(), row_ptr, sizeof(i64) * (rows + 1));
+    fetch(ci.data(), col_idx, sizeof(i64) * nnz);
+    fetch(v.data(), values, sizeof(double) * nnz);
+    if (rp[0] != 0 || rp[rows] != nnz) invalid("sparse: row pointers do not span the entries");
+    std::vector<i64> rp2(static_cast<size_t>(rows) + 1, 0);
+    std::vector<int> ci2;
+    std::vector<double> v2;
+    ci2.reserve(static_cast<size_t>(nnz));
+    v2.reserve(static_cast<size_t>(nnz));
+    for (i64 r = 0; r < rows; ++r) {
+      if (rp[r + 1] < rp[r]) invalid("sparse: row pointers must be nondecreasing");
+      for (i64 k = rp[r]; k < rp[r + 1]; ++k) {
+        if (ci[k] < 0 || ci[k] >= cols) invalid("sparse: triplet index out of range");
+        if (k > rp[r] && ci[k] <= ci[k - 1]) invalid("sparse: column indices must be strictly increasing");
+        if (!std::isfinite(v[k])) invalid("sparse: non-finite entry");
+        if (v[k] != 0.0) {
+          ci2.push_back(static_cast<int>(ci[k]));
+          v2.push_back(v[k]);
+        }
+      }
+      rp2[r + 1] = static_cast<i64>(v2.size());
+    }
+    Csr* a = csr_alloc(c, rows, cols, static_cast<i64>(v2.size()));
+    CUDA_OK(cudaMemcpyAsync(a->rp, rp2.data(), sizeof(i64) * (rows + 1), cudaMemcpyHostToDevice, c->stream));
+    if (a->nnz) {
+      CUDA_OK(cudaMemcpyAsync(a->ci, ci2.data(), sizeof(int) * a->nnz, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(a->v, v2.data(), sizeof(double) * a->nnz, cudaMemcpyHostToDevice, c->stream));
+    }
+    sync(c);
+    *out = reinterpret_cast<cpcag_csr>(a);
+  });
+}
+
+int cpcag_csr_destroy(cpcag_csr a) {
+  return guard([&] { delete as_csr(a); });
+}
+
+int cpcag_csr_info(cpcag_csr h, int64_t* rows, int64_t* cols, int64_t* nnz) {
+  return guard([&] {
+    Csr* a = as_csr(h);
+    if (rows) *rows = a->rows;
+    if (cols) *cols = a->cols;
+    if (nnz) *nnz = a->nnz;
+  });
+}
+
+__global__ void widen_k(const int* __restrict__ a, int64_t* __restrict__ b, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+int cpcag_csr_export(cpcag_ctx ctx, cpcag_csr h, int64_t* row_ptr, int64_t* col_idx, double* values) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    Csr* a = as_csr(h);
+    if (row_ptr) {
+      OutView<i64> o(c, row_ptr, a->rows + 1);
+      CUDA_OK(cudaMemcpyAsync(o.d, a->rp, sizeof(i64) * (a->rows + 1), cudaMemcpyDeviceToDevice, c->stream));
+      o.flush(c);
+      sync(c);
+    }
+    if (col_idx && a->nnz) {
+      OutView<i64> o(c, col_idx, a->nnz);
+      widen_k<<<stride_blocks(c, a->nnz), kBlock, 0, c->stream>>>(a->ci, o.d, a->nnz);
+      launched(c);
+      o.flush(c);
+      sync(c);
+    }
+    if (values && a->nnz) {
+      OutView<double> o(c, values, a->nnz);
+      CUDA_OK(cudaMemcpyAsync(o.d, a->v, sizeof(double) * a->nnz, cudaMemcpyDeviceToDevice, c->stream));
+      o.flush(c);
+      sync(c);
+    }
+  });
+}
+
+int cpcag_csr_is_symmetric(cpcag_csr h) {
+  Csr* a = reinterpret_cast<Csr*>(h);
+  if (!a) return 0;
+  return a->sym == 1 ? 1 : 0;
+}
+
+int cpcag_cuda_spmm(cpcag_ctx ctx, cpcag_csr Ah, int side, int precision, int64_t x_rows,
+                    int64_t x_cols, const void* X, void* Y) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      Csr* A = as_csr(Ah);
+      if (side == CPCAG_LEFT) {
+        if (x_rows != A->cols) invalid("sparse multiply: dimension mismatch");
+        InView<T> xin(c, static_cast<const T*>(X), static_cast<size_t>(x_rows * x_cols));
+        OutView<T> yout(c, static_cast<T*>(Y), static_cast<size_t>(A->rows * x_cols));
+        spmm_left<T>(c, A, xin.d, x_cols, yout.d);
+        yout.flush(c);
+        if (yout.host || xin.staged.p) sync(c);
+      } else if (side == CPCAG_RIGHT) {
+        if (x_cols != A->rows) invalid("sparse right_multiply: dimension mismatch");
+        InView<T> xin(c, static_cast<const T*>(X), static_cast<size_t>(x_rows * x_cols));
+        OutView<T> yout(c, static_cast<T*>(Y), static_cast<size_t>(x_rows * A->cols));
+        spmm_right<T>(c, A, xin.d, x_rows, yout.d);
+        yout.flush(c);
+        if (yout.host || xin.staged.p) sync(c);
+      } else {
+        invalid("spmm: side must be CPCAG_LEFT or CPCAG_RIGHT");
+      }
+    });
+  });
+}
+
+int cpcag_cuda_spmv(cpcag_ctx ctx, cpcag_csr Ah, int precision, int64_t n, const void* x, void* y) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      Csr* A = as_csr(Ah);
+      if (n != A->cols)
+        invalid("spmv: dimension mismatch (" + std::to_string(A->cols) + " vs " + std::to_string(n) + ")");
+      InView<T> xin(c, static_cast<const T*>(x), static_cast<size_t>(n));
+      OutView<T> yout(c, static_cast<T*>(y), static_cast<size_t>(A->rows));
+      spmm_left<T>(c, A, xin.d, 1, yout.d);
+      yout.flush(c);
+      if (yout.host || xin.staged.p) sync(c);
+    });
+  });
+}
+
+int cpcag_cuda_power_norm(cpcag_ctx ctx, cpcag_csr A, double tol, uint64_t seed, int64_t max_iter,
+                          double* out) {
+  return guard([&] {
+    if (!out) invalid("null output pointer");
+    *out = power_norm(as_ctx(ctx), as_csr(A), tol, seed, max_iter);
+  });
+}
+
+int cpcag_cuda_draw_plan(int64_t p, int64_t n, int64_t rho_r, int64_t rho_c, uint64_t seed,
+                         int64_t* omega_r, int64_t* omega_c) {
+  return guard([&] {
+    if (rho_r < 1 || rho_r > p) invalid("draw_plan: rho_r out of range [1, " + std::to_string(p) + "]");
+    if (rho_c < 1 || rho_c > n) invalid("draw_plan: rho_c out of range [1, " + std::to_string(n) + "]");
+    const auto r = draw_indices(p, rho_r, HostRng::derive(seed, 0x726f7773ULL));
+    const auto cc = draw_indices(n, rho_c, HostRng::derive(seed, 0x636f6c73ULL));
+    std::copy(r.begin(), r.end(), omega_r);
+    std::copy(cc.begin(), cc.end(), omega_c);
+  });
+}
+
+int cpcag_cuda_subsample(cpcag_ctx ctx, int precision, const void* Y, int64_t p, int64_t n,
+                         const int64_t* omega_r, int64_t rho_r, const int64_t* omega_c, int64_t rho_c,
+                         void* out) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      const auto hr = host_list(c, omega_r, rho_r);
+      const auto hc = host_list(c, omega_c, rho_c);
+      for (i64 r : hr)
+        if (r < 0 || r >= p) invalid("subsample: plan does not match matrix dimensions");
+      for (i64 q : hc)
+        if (q < 0 || q >= n) invalid("subsample: plan does not match matrix dimensions");
+      InView<T> yin(c, static_cast<const T*>(Y), static_cast<size_t>(p * n));
+      InView<i64> rin(c, omega_r, static_cast<size_t>(rho_r));
+      InView<i64> cin(c, omega_c, static_cast<size_t>(rho_c));
+      OutView<T> o(c, static_cast<T*>(out), static_cast<size_t>(rho_r * rho_c));
+      subsample_device<T>(c, yin.d, p, rin.d, rho_r, cin.d, rho_c, o.d);
+      o.flush(c);
+      sync(c);
+    });
+  });
+}
+
+int cpcag_cuda_prox(cpcag_ctx ctx, int precision, int loss, const void* Z, const void* Y, int64_t count,
+                    double lam, void* out) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (lam < 0.0) invalid("prox: negative threshold");
+      InView<T> z(c, static_cast<const T*>(Z), static_cast<size_t>(count));
+      InView<T> y(c, static_cast<const T*>(Y), static_cast<size_t>(count));
+      OutView<T> o(c, static_cast<T*>(out), static_cast<size_t>(count));
+      if (count > 0) {
+        prox_k<T><<<stride_blocks(c, count), kBlock, 0, c->stream>>>(loss, z.d, y.d, count, static_cast<T>(lam), o.d);
+        launched(c);
+      }
+      o.flush(c);
+      sync(c);
+    });
+  });
+}
+
+int cpcag_cuda_grad_g(cpcag_ctx ctx, int precision, const void* Z, int64_t rows, int64_t cols,
+                      cpcag_csr Lrh, cpcag_csr Lch, const cpcag_frpcag_config* cfg, void* G) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      Csr* Lr = as_csr(Lrh);
+      Csr* Lc = as_csr(Lch);
+      if (!cfg) invalid("null config");
+      frpcag_check_dims(rows, cols, Lr, Lc);
+      InView<T> z(c, static_cast<const T*>(Z), static_cast<size_t>(rows * cols));
+      OutView<T> g(c, static_cast<T*>(G), static_cast<size_t>(rows * cols));
+      if (rows > 0 && cols > 0) {
+        dim3 gr(blocks_for(rows), static_cast<unsigned>(std::min<i64>(cols, 65535)));
+        grad_k<T><<<gr, kBlock, 0, c->stream>>>(rows, cols, make_pull<T>(c, Lr, false), make_pull<T>(c, Lc, true),
+                                                 static_cast<T>(2.0 * cfg->gamma_r), static_cast<T>(2.0 * cfg->gamma_c),
+                                                 cfg->gamma_r != 0.0, cfg->gamma_c != 0.0, z.d, g.d);
+        launched(c);
+      }
+      g.flush(c);
+      sync(c);
+    });
+  });
+}
+
+int cpcag_cuda_objective(cpcag_ctx ctx, int precision, const void* X, const void* Y, int64_t rows,
+                         int64_t cols, cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg,
+                         double* out) {
+  return dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (!cfg || !out) invalid("null argument");
+      InView<T> x(c, static_cast<const T*>(X), static_cast<size_t>(rows * cols));
+      InView<T> y(c, static_cast<const T*>(Y), static_cast<size_t>(rows * cols));
+      *out = objective_device<T>(c, x.d, y.d, rows, cols, as_csr(Lr), as_csr(Lc), *cfg);
+    });
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,328 @@
+// decoder.cu -- the graph-regularised alternate decoder (decoders.cpp:145-186):
+// conjugate gradient on the normal operator
+//     A(X) = gbar_c X Lc + gbar_r Lr X + M o X,   b = scatter(Xt),  X0 = 0,
+// with the reference recurrence of detail::pcg_core (solvers.hpp:33-74,
+// identity preconditioner: z = r, rho = <r, r>).
+//
+// HBM layout: X, R, P, AP are p x n column-major in the working precision;
+// the mask and b are never materialised: rsel[i] / csel[c] give the position
+// of row i / column c in the plan (or -1), so M(i,c) and b(i,c) are O(1)
+// look-ups.  One CG iteration is three kernels:
+//   A  apply+dot   AP = A(P), <P, AP>          -> alpha (last block)
+//   B  residual    R -= alpha AP, <R, R>        -> beta
+//   C  update      X += alpha P, P = R + beta P -> stop test
+// Every scalar lives on the device; the host polls the done flag once per
+// chunk of iterations.
+#include <algorithm>
+
+#include "common.cuh"
+#include "frpcag.cuh"
+
+namespace cpcag_cuda {
+
+struct CgState {
+  double rho, rho_next, curv, alpha, beta;
+  double norm_b, target, rel_res;
+  i64 it;
+  int done, err, zero_rhs, pad;
+  i64 err_it;
+  unsigned cnt[4];
+};
+
+struct Plan {
+  const int* rsel;   // p: index into omega_r or -1
+  const int* csel;   // n: index into omega_c or -1
+  i64 rho_r;
+};
+
+template <typename T>
+__device__ __forceinline__ T rhs_at(const Plan& pl, const T* __restrict__ Xt, i64 i, i64 c) {
+  const int a = pl.rsel[i], b = pl.csel[c];
+  return (a >= 0 && b >= 0) ? Xt[a + static_cast<i64>(b) * pl.rho_r] : T(0);
+}
+
+// decoders.cpp:160-170 for one entry: (gbar_c (X Lc))(i,c) + (gbar_r (Lr X))(i,c),
+// then + X(i,c) on the sampled grid.
+template <typename T>
+__device__ __forceinline__ T apply_elem(const Pull<T>& Lr, const Pull<T>& Lc, T gr, T gc,
+                                        const Plan& pl, const T* __restrict__ V, i64 p, i64 i,
+                                        i64 c) {
+  const T a1 = pull_right(Lc.rp[c], Lc.rp[c + 1], Lc.ci, Lc.v, V, p, i);
+  const T a2 = pull_left(Lr.rp[i], Lr.rp[i + 1], Lr.ci, Lr.v, V + c * p);
+  T out = add_rn(mul_rn(gc, a1), mul_rn(gr, a2));
+  if (pl.rsel[i] >= 0 && pl.csel[c] >= 0) out = add_rn(out, V[i + c * p]);
+  return out;
+}
+
+// x = 0, r = b, p = r; rho = <b, b>.
+template <typename T>
+__global__ void cg_init_k(i64 p, i64 n, Plan pl, const T* __restrict__ Xt, T* __restrict__ X,
+                          T* __restrict__ R, T* __restrict__ P, double tol, double* partials,
+                          CgState* st) {
+  double s[1] = {0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p) {
+    for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+      const i64 at = i + c * p;
+      const T b = rhs_at(pl, Xt, i, c);
+      X[at] = T(0);
+      R[at] = b;
+      P[at] = b;
+      s[0] += static_cast<double>(b) * static_cast<double>(b);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0) {
+    const double nb = sqrt(tot[0]);
+    st->norm_b = nb;
+    st->rho = tot[0];
+    st->it = 0;
+    if (nb == 0.0) {
+      st->zero_rhs = 1;
+      st->done = 1;
+      return;
+    }
+    st->target = tol * nb;
+    if (sqrt(tot[0]) <= st->target) st->done = 1;
+  }
+}
+
+template <typename T>
+__global__ void cg_apply_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                           const T* __restrict__ P, T* __restrict__ AP, double* partials,
+                           CgState* st) {
+  if (st->done) return;
+  double s[1] = {0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p) {
+    for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+      const T ap = apply_elem(Lr, Lc, gr, gc, pl, P, p, i, c);
+      AP[i + c * p] = ap;
+      s[0] += static_cast<double>(P[i + c * p]) * static_cast<double>(ap);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
+template <typename T>
+__global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
+                              CgState* st) {
+  if (st->done) return;
+  const T alpha = static_cast<T>(st->alpha);
+  double s[1] = {0.0};
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const T r = sub_rn(R[q], mul_rn(alpha, AP[q]));
+    R[q] = r;
+    s[0] += static_cast<double>(r) * static_cast<double>(r);
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[2], tot) && threadIdx.x == 0) {
+    st->rho_next = tot[0];
+    st->beta = tot[0] / st->rho;
+  }
+}
+
+template <typename T>
+__global__ void cg_update_k(i64 N, T* __restrict__ X, T* __restrict__ P, const T* __restrict__ R,
+                            i64 max_iter, CgState* st) {
+  if (st->done) return;
+  const T alpha = static_cast<T>(st->alpha), beta = static_cast<T>(st->beta);
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const T pv = P[q];
+    X[q] = add_rn(X[q], mul_rn(alpha, pv));
+    P[q] = add_rn(R[q], mul_rn(beta, pv));
+  }
+  // Scalar step: a second tiny reduction is not needed, the last block to
+  // finish (counted) advances the iteration.
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->cnt[3], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    st->cnt[3] = 0u;
+    st->rho = st->rho_next;
+    st->it += 1;
+    if (sqrt(st->rho) <= st->target || st->it >= max_iter) st->done = 1;
+  }
+}
+
+// ||b - A(x)||^2 for the exit test (solvers.hpp:69-72).
+template <typename T>
+__global__ void cg_true_residual_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                   const T* __restrict__ Xt, const T* __restrict__ X,
+                                   double* partials, CgState* st) {
+  double s[1] = {0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p) {
+    for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+      const T ax = apply_elem(Lr, Lc, gr, gc, pl, X, p, i, c);
+      const double e = static_cast<double>(sub_rn(rhs_at(pl, Xt, i, c), ax));
+      s[0] += e * e;
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0)
+    st->rel_res = sqrt(tot[0]) / st->norm_b;
+}
+
+__global__ void fill_sel_k(i64 len, int* sel) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < len) sel[i] = -1;
+}
+__global__ void scatter_sel_k(const i64* __restrict__ om, i64 rho, int* sel) {
+  const i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (k < rho) sel[om[k]] = static_cast<int>(k);
+}
+
+template <typename T>
+void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i64* om_r_host,
+                             const i64* om_c_host, i64 p, i64 n, Csr* Lr, Csr* Lc, double lk1_r,
+                             double lk1_c, const cpcag_decoder_config& cfg, T* X, int* converged,
+                             i64* iterations) {
+  if (Lr->rows != p || Lc->rows != n || Lr->cols != p || Lc->cols != n)
+    invalid("alternate decoder: Laplacians do not match plan");
+  if (cfg.gamma <= 0.0) invalid("alternate decoder: gamma must be positive");
+  {
+    std::vector<char> seen_r(static_cast<size_t>(p), 0), seen_c(static_cast<size_t>(n), 0);
+    for (i64 k = 0; k < rho_r; ++k) {
+      const i64 r = om_r_host[k];
+      if (r < 0 || r >= p || seen_r[r]) invalid("alternate decoder: Xt does not match plan");
+      seen_r[r] = 1;
+    }
+    for (i64 k = 0; k < rho_c; ++k) {
+      const i64 q = om_c_host[k];
+      if (q < 0 || q >= n || seen_c[q]) invalid("alternate decoder: Xt does not match plan");
+      seen_c[q] = 1;
+    }
+  }
+  const double gbar_r = cfg.gamma / lk1_r;
+  const double gbar_c = cfg.gamma / lk1_c;
+  const i64 N = p * n;
+
+  DevBuf<i64> omr(c, rho_r), omc(c, rho_c);
+  if (rho_r) CUDA_OK(cudaMemcpyAsync(omr.p, om_r_host, sizeof(i64) * rho_r, cudaMemcpyHostToDevice, c->stream));
+  if (rho_c) CUDA_OK(cudaMemcpyAsync(omc.p, om_c_host, sizeof(i64) * rho_c, cudaMemcpyHostToDevice, c->stream));
+  DevBuf<int> rsel(c, p), csel(c, n);
+  if (p) {
+    fill_sel_k<<<blocks_for(p), kBlock, 0, c->stream>>>(p, rsel.p);
+    launched(c);
+  }
+  if (n) {
+    fill_sel_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, csel.p);
+    launched(c);
+  }
+  if (rho_r) {
+    scatter_sel_k<<<blocks_for(rho_r), kBlock, 0, c->stream>>>(omr.p, rho_r, rsel.p);
+    launched(c);
+  }
+  if (rho_c) {
+    scatter_sel_k<<<blocks_for(rho_c), kBlock, 0, c->stream>>>(omc.p, rho_c, csel.p);
+    launched(c);
+  }
+  const Plan pl{rsel.p, csel.p, rho_r};
+  const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
+  const T gr = static_cast<T>(gbar_r), gc = static_cast<T>(gbar_c);
+
+  DevBuf<T> R(c, N), P(c, N), AP(c, N);
+  DevBuf<CgState> st(c, 1);
+  st.zero(c);
+  if (N == 0) {
+    *converged = 1;
+    *iterations = 0;
+    return;
+  }
+  const unsigned gx = blocks_for(p);
+  const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx);
+  dim3 g2(gx, static_cast<unsigned>(std::max<i64>(1, std::min<i64>({n, ycap, 65535}))));
+  const unsigned nb1 = stride_blocks(c, N);
+  DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
+
+  cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
+  launched(c);
+  CgState host = read_back(c, st.p);
+  const i64 chunk = 32;
+  while (!host.done) {
+    for (i64 k = 0; k < chunk; ++k) {
+      cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
+      launched(c);
+      cg_residual_k<T><<<nb1, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+      launched(c);
+      cg_update_k<T><<<nb1, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
+      launched(c);
+    }
+    host = read_back(c, st.p);
+  }
+  if (host.err)
+    runtime("pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(host.err_it));
+  if (host.zero_rhs) {
+    *converged = 1;
+    *iterations = 0;
+    return;
+  }
+  cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, Xt, X, part.p, st.p);
+  launched(c);
+  host = read_back(c, st.p);
+  *converged = host.rel_res <= cfg.pcg_tol ? 1 : 0;
+  *iterations = host.it;
+}
+
+template void alternate_decode_device<double>(Ctx*, const double*, i64, i64, const i64*, const i64*, i64, i64,
+                                              Csr*, Csr*, double, double, const cpcag_decoder_config&,
+                                              double*, int*, i64*);
+template void alternate_decode_device<float>(Ctx*, const float*, i64, i64, const i64*, const i64*, i64, i64,
+                                             Csr*, Csr*, double, double, const cpcag_decoder_config&,
+                                             float*, int*, i64*);
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+extern "C" int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, int64_t rho_r,
+                                           int64_t rho_c, const int64_t* omega_r, const int64_t* omega_c,
+                                           int64_t p, int64_t n, cpcag_csr Lr, cpcag_csr Lc,
+                                           double lambda_k1_r, double lambda_k1_c,
+                                           const cpcag_decoder_config* cfg, void* X, int* converged,
+                                           int64_t* iterations) {
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (!cfg || !converged || !iterations) invalid("null argument");
+      std::vector<i64> omr(static_cast<size_t>(std::max<int64_t>(rho_r, 0)));
+      std::vector<i64> omc(static_cast<size_t>(std::max<int64_t>(rho_c, 0)));
+      auto fetch = [&](std::vector<i64>& dst, const int64_t* src) {
+        if (dst.empty()) return;
+        if (is_device_ptr(src))
+          CUDA_OK(cudaMemcpy(dst.data(), src, sizeof(i64) * dst.size(), cudaMemcpyDeviceToHost));
+        else
+          std::copy(src, src + dst.size(), dst.begin());
+      };
+      fetch(omr, omega_r);
+      fetch(omc, omega_c);
+      InView<T> xt(c, static_cast<const T*>(Xt), static_cast<size_t>(rho_r * rho_c));
+      OutView<T> x(c, static_cast<T*>(X), static_cast<size_t>(p * n));
+      alternate_decode_device<T>(c, xt.d, rho_r, rho_c, omr.data(), omc.data(), p, n, as_csr(Lr), as_csr(Lc),
+                                 lambda_k1_r, lambda_k1_c, *cfg, x.d, converged, iterations);
+      x.flush(c);
+      sync(c);
+    });
+  };
+  if (precision == CPCAG_F64) return run(double{});
+  if (precision == CPCAG_F32) return run(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}

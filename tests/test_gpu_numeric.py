@@ -1,0 +1,233 @@
+"""GPU parity: SpMM/SpMV, power iteration, sampling, FRPCAG operators, FISTA
+and the alternate decoder through the C-ABI, against the CPU oracle.
+
+Tolerances: fp64 SpMM/SpMV/gather are bit-exact (same per-entry operation
+order); fp64 solvers within 1e-9 relative (only full-array reduction order
+differs); fp32 device runs within the north_star 1e-4 relative Frobenius
+error of the fp64 oracle.
+"""
+import numpy as np
+import pytest
+
+from helpers import knn_laplacian, random_laplacian, rel, to_device
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1602_02070_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    return P.Context(0)
+
+
+def test_spmm_left_right_fp64_bit_exact(P, ctx):
+    L = knn_laplacian(300, 5, 10, 3)
+    A = to_device(ctx, L)
+    X = np.random.default_rng(0).standard_normal((300, 17))
+    assert np.array_equal(A.multiply(X), L.multiply(X))
+    Xr = np.random.default_rng(1).standard_normal((23, 300))
+    assert np.array_equal(A.right_multiply(Xr), L.right_multiply(Xr))
+    x = X[:, 0].copy()
+    assert np.array_equal(A.multiply(x), L.spmv(x))
+
+
+def test_spmm_nonsymmetric_uses_transpose_order(P, ctx):
+    rs = np.random.default_rng(5)
+    D = rs.standard_normal((40, 30)) * (rs.random((40, 30)) < 0.2)
+    L = O.Csr.from_dense(D)
+    A = to_device(ctx, L)
+    X = rs.standard_normal((11, 40))
+    assert np.array_equal(A.right_multiply(X), L.right_multiply(X))
+    X2 = rs.standard_normal((30, 4))
+    assert np.array_equal(A.multiply(X2), L.multiply(X2))
+    assert not A.is_symmetric()
+
+
+def test_spmm_fp32_and_device_tensors(P, ctx):
+    import torch
+
+    L = random_laplacian(200, 0.05, 7)
+    A = to_device(ctx, L)
+    X = np.random.default_rng(2).standard_normal((200, 9))
+    Xd = torch.tensor(X, dtype=torch.float32, device="cuda")
+    Y = A.multiply(Xd)
+    assert Y.is_cuda and Y.dtype == torch.float32
+    assert rel(Y.cpu().numpy(), L.multiply(X)) <= 1e-6
+
+
+def test_spmm_dimension_mismatch(P, ctx):
+    A = to_device(ctx, random_laplacian(10, 0.3, 1))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        A.multiply(np.zeros((9, 2)))
+    with pytest.raises(ValueError, match="dimension mismatch"):
+        A.multiply(np.zeros(4))
+
+
+def test_power_iteration_known_answers(P, ctx):
+    # test_numeric.cpp:179-199
+    A = P.SparseMatrix.from_triplets(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 5.0, 3.0], ctx=ctx)
+    assert P.power_iteration_norm(A, 1e-12, 3, ctx=ctx) == pytest.approx(5.0, rel=1e-9)
+    ti, tj, tv = [], [], []
+    for i in range(4):
+        for j in range(4):
+            ti.append(i), tj.append(j), tv.append(3.0 if i == j else -1.0)
+    K4 = P.SparseMatrix.from_triplets(4, 4, ti, tj, tv, ctx=ctx)
+    assert P.power_iteration_norm(K4, 1e-12, 5, ctx=ctx) == pytest.approx(4.0, rel=1e-9)
+    Z = P.SparseMatrix.from_triplets(4, 4, [], [], [], ctx=ctx)
+    assert P.power_iteration_norm(Z, 1e-10, 9, ctx=ctx) == 0.0
+
+
+def test_power_iteration_matches_oracle(P, ctx):
+    for seed, n in [(1, 50), (2, 700), (3, 3000)]:
+        L = knn_laplacian(n, 4, 8, seed)
+        got = P.power_iteration_norm(to_device(ctx, L), 1e-7, 42, ctx=ctx)
+        want = O.power_iteration_norm(L, 1e-7, 42)
+        assert got == pytest.approx(want, rel=1e-6)
+
+
+def test_plan_and_subsample_bit_exact(P, ctx):
+    plan = P.draw_plan(1000, 777, 101, 93, seed=1602)
+    plan_o = O.draw_plan(1000, 777, 101, 93, seed=1602)
+    assert np.array_equal(plan.omega_r, plan_o.omega_r)
+    assert np.array_equal(plan.omega_c, plan_o.omega_c)
+    Y = np.random.default_rng(3).standard_normal((1000, 777))
+    assert np.array_equal(P.subsample(Y, plan, ctx=ctx), O.subsample(Y, plan_o))
+    with pytest.raises(ValueError, match="does not match"):
+        P.subsample(Y[:, :10], plan, ctx=ctx)
+
+
+def test_prox_grad_objective_match_oracle(P, ctx):
+    rs = np.random.default_rng(9)
+    r, c = 37, 29
+    Lr, Lc = random_laplacian(r, 0.2, 1), random_laplacian(c, 0.3, 2)
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    Z, Y = rs.standard_normal((r, c)), rs.standard_normal((r, c))
+    assert np.array_equal(P.prox_l1(Z, Y, 0.3, ctx=ctx), O.prox_l1(Z, Y, 0.3))
+    assert np.array_equal(P.prox_l2(Z, Y, 0.3, ctx=ctx), O.prox_l2(Z, Y, 0.3))
+    cfg = P.FrpcagConfig(gamma_r=1.5, gamma_c=0.7)
+    ocfg = O.FrpcagConfig(gamma_r=1.5, gamma_c=0.7)
+    assert np.array_equal(P.grad_g(Z, dLr, dLc, cfg, ctx=ctx), O.grad_g(Z, Lr, Lc, ocfg))
+    assert P.objective(Z, Y, dLr, dLc, cfg, ctx=ctx) == pytest.approx(O.objective(Z, Y, Lr, Lc, ocfg), rel=1e-12)
+    with pytest.raises(ValueError, match="negative threshold"):
+        P.prox_l1(Z, Y, -1.0, ctx=ctx)
+
+
+@pytest.mark.parametrize("loss", ["l1", "l2"])
+def test_fista_fp64_matches_oracle(P, ctx, loss):
+    rs = np.random.default_rng(11)
+    r, c = 60, 45
+    Lr, Lc = knn_laplacian(r, 3, 6, 4), knn_laplacian(c, 3, 6, 5)
+    Y = rs.standard_normal((r, c))
+    cfg = P.FrpcagConfig(gamma_r=3.0, gamma_c=2.0, loss=loss, tol=1e-300, max_iter=120)
+    X, tr = P.fista_solve(Y, to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+    Xo, tro = O.fista_solve(Y, Lr, Lc, O.FrpcagConfig(3.0, 2.0, loss, 1e-300, 120))
+    assert tr.iterations == tro.iterations == 120 and not tr.converged
+    assert tr.step == pytest.approx(tro.step, rel=1e-6)
+    assert rel(X, Xo) <= 1e-9
+    assert np.allclose(tr.objective, tro.objective, rtol=1e-9)
+
+
+def test_fista_stops_on_tolerance_like_oracle(P, ctx):
+    rs = np.random.default_rng(12)
+    Lr, Lc = knn_laplacian(30, 3, 5, 6), knn_laplacian(25, 3, 5, 7)
+    Y = rs.standard_normal((30, 25))
+    cfg = P.FrpcagConfig(gamma_r=0.5, gamma_c=0.5, loss="l2", tol=1e-8, max_iter=5000)
+    X, tr = P.fista_solve(Y, to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+    Xo, tro = O.fista_solve(Y, Lr, Lc, O.FrpcagConfig(0.5, 0.5, "l2", 1e-8, 5000))
+    assert tr.converged and tro.converged
+    assert abs(tr.iterations - tro.iterations) <= 1
+    assert rel(X, Xo) <= 1e-7
+
+
+def test_fista_fp32_within_north_star_tolerance(P, ctx):
+    rs = np.random.default_rng(13)
+    Lr, Lc = knn_laplacian(120, 3, 8, 8), knn_laplacian(90, 3, 8, 9)
+    Y = rs.standard_normal((120, 90))
+    cfg = P.FrpcagConfig(gamma_r=2.0, gamma_c=2.0, tol=1e-300, max_iter=200)
+    X, tr = P.fista_solve(Y.astype(np.float32), to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+    Xo, _ = O.fista_solve(Y.astype(np.float32).astype(np.float64), Lr, Lc,
+                          O.FrpcagConfig(2.0, 2.0, "l1", 1e-300, 200))
+    assert X.dtype == np.float32
+    assert rel(X, Xo) <= 1e-4
+
+
+def test_fista_errors(P, ctx):
+    Lr, Lc = random_laplacian(6, 0.5, 1), random_laplacian(5, 0.5, 2)
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    Y = np.ones((6, 5))
+    with pytest.raises(ValueError, match="negative regularization"):
+        P.fista_solve(Y, dLr, dLc, P.FrpcagConfig(gamma_r=-1.0), ctx=ctx)
+    with pytest.raises(ValueError, match="column Laplacian"):
+        P.fista_solve(Y, dLr, dLr, P.FrpcagConfig(), ctx=ctx)
+    with pytest.raises(RuntimeError, match=r"diverged \(non-finite objective at iteration"):
+        P.fista_solve(Y * 1e300, dLr, dLc, P.FrpcagConfig(step=10.0, tol=1e-300, max_iter=20), ctx=ctx)
+
+
+def _decoder_case(p=150, n=120, rr=40, rc=30, seed=21):
+    Lr, Lc = knn_laplacian(p, 3, 7, seed), knn_laplacian(n, 3, 7, seed + 1)
+    plan = O.draw_plan(p, n, rr, rc, seed=seed)
+    Xt = np.random.default_rng(seed).standard_normal((rr, rc))
+    return Lr, Lc, plan, Xt
+
+
+def test_alternate_decode_fp64_matches_oracle(P, ctx):
+    Lr, Lc, plan_o, Xt = _decoder_case()
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    res = P.alternate_decode(Xt, plan, to_device(ctx, Lr), to_device(ctx, Lc), P.SpectralGap(lambda_k1=0.3),
+                             P.SpectralGap(lambda_k1=0.4), P.DecoderConfig(1.0, 1e-10, 400), ctx=ctx)
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 400)
+    assert res.converged == ro.converged
+    assert abs(res.iterations - ro.iterations) <= 1
+    assert rel(res.X, ro.X) <= 1e-9
+
+
+def test_alternate_decode_fixed_iterations_fp32(P, ctx):
+    Lr, Lc, plan_o, Xt = _decoder_case(400, 300, 100, 75, 23)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    res = P.alternate_decode(Xt.astype(np.float32), plan, to_device(ctx, Lr), to_device(ctx, Lc),
+                             P.SpectralGap(lambda_k1=1.0), P.SpectralGap(lambda_k1=1.0),
+                             P.DecoderConfig(1.0, 1e-8, 100), ctx=ctx)
+    ro = O.alternate_decode(Xt.astype(np.float32).astype(np.float64), plan_o, Lr, Lc, 1.0, 1.0, 1.0, 1e-8, 100)
+    assert res.iterations == ro.iterations
+    assert rel(res.X, ro.X) <= 1e-4
+
+
+def test_alternate_decode_zero_rhs_and_validation(P, ctx):
+    Lr, Lc, plan_o, Xt = _decoder_case(20, 15, 5, 4, 3)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    g = P.SpectralGap(lambda_k1=1.0)
+    res = P.alternate_decode(np.zeros_like(Xt), plan, dLr, dLc, g, g, ctx=ctx)
+    assert res.converged and res.iterations == 0 and np.all(res.X == 0)
+    with pytest.raises(ValueError, match="gamma must be positive"):
+        P.alternate_decode(Xt, plan, dLr, dLc, g, g, P.DecoderConfig(gamma=0.0), ctx=ctx)
+    with pytest.raises(ValueError, match="Laplacians do not match"):
+        P.alternate_decode(Xt, plan, dLc, dLc, g, g, ctx=ctx)
+    with pytest.raises(ValueError, match="Xt does not match"):
+        P.alternate_decode(Xt[:, :2], plan, dLr, dLc, g, g, ctx=ctx)
+
+
+def test_decoder_breakdown_names_iteration(P, ctx):
+    # A zero operator (no graph, no samples on the support) breaks down at 0:
+    # mask empty rows/cols are impossible with a plan, so use negative weights.
+    p, n = 6, 5
+    Lr = P.SparseMatrix.from_triplets(p, p, range(p), range(p), [-1.0] * p, ctx=ctx)
+    Lc = P.SparseMatrix.from_triplets(n, n, range(n), range(n), [-1.0] * n, ctx=ctx)
+    plan = P.draw_plan(p, n, 2, 2, seed=1)
+    g = P.SpectralGap(lambda_k1=1.0)
+    with pytest.raises(RuntimeError, match="pcg: breakdown .* at iteration 0"):
+        P.alternate_decode(np.ones((2, 2)), plan, Lr, Lc, g, g, ctx=ctx)
+
+
+def test_launches_are_counted(P, ctx):
+    ctx.reset_launch_count()
+    L = random_laplacian(50, 0.1, 3)
+    to_device(ctx, L).multiply(np.ones((50, 3)))
+    assert ctx.launch_count >= 1
