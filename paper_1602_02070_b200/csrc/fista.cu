@@ -201,7 +201,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   const i64 J = host.iterations;
   CUDA_OK(cudaMemcpyAsync(X, Sb[J & 1].p, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
   if (objective_host && J > 0)
-    CUDA_OK(cudaMemcpyAsync(objective_host, tr.p, sizeof(double) * J, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(cudaMemcpyAsync(objective_host, tr.p, sizeof(double) * J, cudaMemcpyDefault, c->stream));
   sync(c);
   trace->iterations = J;
   trace->converged = host.converged;

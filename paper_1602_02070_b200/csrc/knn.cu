@@ -1,0 +1,599 @@
+// knn.cu -- kNN graph construction (graph.cpp:47-135), graph_from_adjacency
+// (graph.cpp:137-154) and the Laplacian assembly (graph.cpp:16-43).
+//
+// Neighbour selection is exact with respect to the reference's canonical
+// fp64 distance d2(i,j) = max(0, (g_ii + g_jj) - 2 g_ij) where every Gram
+// entry is the k-ascending sum of products with separate rounding (no FMA):
+// the tiled Gram kernel keeps one accumulator per pair and walks k in order,
+// so the value is bit-identical to the oracle's (and symmetric in i, j
+// because products commute).  Per-row top-K is kept under the lexicographic
+// (d2, j) order, i.e. ties go to the lower index (graph.cpp:93-96).
+//
+// Layout: points are gathered point-major (n x d fp64, each point
+// contiguous) so a 64-point x 16-k tile is 64 coalesced 128-byte reads.  A
+// CTA owns 64 query points and sweeps a range of 64-point candidate tiles;
+// the candidate range is split across CTAs when n/64 alone cannot fill the
+// 148 SMs, and the per-split top-K lists are merged afterwards.
+//
+// Graph assembly: 2nK directed (row, col, d2) records -> one radix sort on
+// (row << 32 | col) -> duplicates dropped (union symmetrisation) ->
+// Gaussian weights (w == 0 dropped) -> CSR W -> degrees -> CSR L.
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <math_constants.h>
+
+#include <memory>
+
+#include "common.cuh"
+
+namespace cpcag_cuda {
+
+constexpr int kTile = 64;   // points per tile side
+constexpr int kKc = 16;     // k-chunk staged in shared memory
+constexpr int kMaxK = 64;   // largest supported neighbour count
+constexpr size_t kKnnSmem = (2 * kKc + kTile) * (kTile + 1) * sizeof(double) +
+                            kTile * (kMaxK + 1) * (sizeof(double) + sizeof(int));
+
+template <typename T>
+__global__ void gather_points_k(const T* __restrict__ X, i64 x_rows, i64 n, i64 d, int axis_rows,
+                                double* __restrict__ Pm) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= n * d) return;
+  const i64 i = t / d, k = t % d;
+  Pm[t] = static_cast<double>(axis_rows ? X[i + k * x_rows] : X[k + i * x_rows]);
+}
+
+__global__ void sqnorm_k(const double* __restrict__ Pm, i64 n, i64 d, double* __restrict__ sq) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* a = Pm + i * d;
+  double s = 0.0;
+  for (i64 k = 0; k < d; ++k) s = __dadd_rn(s, __dmul_rn(a[k], a[k]));
+  sq[i] = s;
+}
+
+__device__ __forceinline__ bool lex_less(double da, int ja, double db, int jb) {
+  return da < db || (da == db && ja < jb);
+}
+
+// One CTA: 64 query points x candidate tiles [jt0, jt1).  Output: per query
+// point the K best (d2, j) of the range, ascending, into cand[split].
+__global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm, const double* __restrict__ sq,
+                                                  i64 n, i64 d, int K, int tiles_per_split,
+                                                  double* __restrict__ cand_d, int* __restrict__ cand_j,
+                                                  int* __restrict__ dup) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double(*As)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(smem);
+  double(*Bs)[kTile + 1] = As + kKc;
+  double(*Dt)[kTile + 1] = Bs + kKc;
+  double(*best_d)[kMaxK + 1] = reinterpret_cast<double(*)[kMaxK + 1]>(Dt + kTile);
+  int(*best_j)[kMaxK + 1] = reinterpret_cast<int(*)[kMaxK + 1]>(best_d + kTile);
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kTile;
+  const int split = blockIdx.y;
+  const i64 n_tiles = (n + kTile - 1) / kTile;
+  const i64 jt0 = static_cast<i64>(split) * tiles_per_split;
+  const i64 jt1 = min(n_tiles, jt0 + tiles_per_split);
+
+  if (tid < kTile)
+    for (int q = 0; q < K; ++q) {
+      best_d[tid][q] = CUDART_INF;
+      best_j[tid][q] = INT32_MAX;
+    }
+  __syncthreads();
+
+  for (i64 jt = jt0; jt < jt1; ++jt) {
+    const i64 j0 = jt * kTile;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
+
+    for (i64 k0 = 0; k0 < d; k0 += kKc) {
+      // Stage 64 x 16 of A (queries) and B (candidates), transposed.
+#pragma unroll
+      for (int q = 0; q < (kTile * kKc) / 256; ++q) {
+        const int idx = tid + 256 * q;
+        const int pt = idx / kKc, kk = idx % kKc;
+        const i64 k = k0 + kk;
+        const i64 ia = i0 + pt, jb = j0 + pt;
+        As[kk][pt] = (ia < n && k < d) ? Pm[ia * d + k] : 0.0;
+        Bs[kk][pt] = (jb < n && k < d) ? Pm[jb * d + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kKc; ++kk) {
+        double a[4], b[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) b[s] = Bs[kk][tx + 16 * s];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int s = 0; s < 4; ++s) acc[r][s] = __dadd_rn(acc[r][s], __dmul_rn(a[r], b[s]));
+      }
+      __syncthreads();
+    }
+    // d2 tile (graph.cpp:63), masked outside the matrix and on the diagonal.
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int li = ty + 16 * r, lj = tx + 16 * s;
+        const i64 gi = i0 + li, gj = j0 + lj;
+        double v = CUDART_INF;
+        if (gi < n && gj < n && gi != gj) {
+          const double t = __dsub_rn(__dadd_rn(sq[gi], sq[gj]), __dmul_rn(2.0, acc[r][s]));
+          v = t > 0.0 ? t : 0.0;
+        }
+        Dt[li][lj] = v;
+      }
+    __syncthreads();
+    if (tid < kTile) {
+      const i64 gi = i0 + tid;
+      if (gi < n) {
+        for (int lj = 0; lj < kTile; ++lj) {
+          const double v = Dt[tid][lj];
+          const int gj = static_cast<int>(j0 + lj);
+          if (v == 0.0 && gj < gi && gj < n && !dup[gi]) {
+            // Coincident candidate: exact coordinate test (graph.cpp:68-84).
+            const double* a = Pm + gi * d;
+            const double* b = Pm + static_cast<i64>(gj) * d;
+            bool same = true;
+            for (i64 k = 0; k < d && same; ++k) same = a[k] == b[k];
+            if (same) dup[gi] = 1;
+          }
+          if (!lex_less(v, gj, best_d[tid][K - 1], best_j[tid][K - 1])) continue;
+          int q = K - 1;
+          while (q > 0 && lex_less(v, gj, best_d[tid][q - 1], best_j[tid][q - 1])) {
+            best_d[tid][q] = best_d[tid][q - 1];
+            best_j[tid][q] = best_j[tid][q - 1];
+            --q;
+          }
+          best_d[tid][q] = v;
+          best_j[tid][q] = gj;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < kTile) {
+    const i64 gi = i0 + tid;
+    if (gi < n) {
+      double* od = cand_d + (static_cast<i64>(split) * n + gi) * K;
+      int* oj = cand_j + (static_cast<i64>(split) * n + gi) * K;
+      for (int q = 0; q < K; ++q) {
+        od[q] = best_d[tid][q];
+        oj[q] = best_j[tid][q];
+      }
+    }
+  }
+}
+
+// Merge the per-split sorted lists of each point; mean d2 in ascending order.
+__global__ void knn_merge_k(i64 n, int K, int splits, const double* __restrict__ cand_d,
+                            const int* __restrict__ cand_j, int64_t* __restrict__ nbr,
+                            double* __restrict__ nbr_d2, double* __restrict__ mean_d2) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int pos[64];
+  const int S = splits < 64 ? splits : 64;
+  for (int s = 0; s < S; ++s) pos[s] = 0;
+  double m = 0.0;
+  for (int q = 0; q < K; ++q) {
+    int bs = -1;
+    double bd = CUDART_INF;
+    int bj = INT32_MAX;
+    for (int s = 0; s < S; ++s) {
+      if (pos[s] >= K) continue;
+      const i64 at = (static_cast<i64>(s) * n + i) * K + pos[s];
+      const double dv = cand_d[at];
+      const int jv = cand_j[at];
+      if (bs < 0 || lex_less(dv, jv, bd, bj)) {
+        bs = s;
+        bd = dv;
+        bj = jv;
+      }
+    }
+    pos[bs]++;
+    nbr[i * K + q] = bj;
+    nbr_d2[i * K + q] = bd;
+    m = __dadd_rn(m, bd);
+  }
+  mean_d2[i] = m;
+}
+
+// sigma2 = sum_i (mean_i / K) / n, summed in point order (graph.cpp:104-107).
+__global__ void sigma2_k(i64 n, int K, const double* __restrict__ mean_d2, double override_, double* out) {
+  if (blockIdx.x || threadIdx.x) return;
+  double s = 0.0;
+  for (i64 i = 0; i < n; ++i) s = __dadd_rn(s, __ddiv_rn(mean_d2[i], static_cast<double>(K)));
+  *out = override_ > 0.0 ? override_ : __ddiv_rn(s, static_cast<double>(n));
+}
+
+__global__ void count_dup_k(i64 n, const int* __restrict__ dup, unsigned long long* cnt) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n && dup[i]) atomicAdd(cnt, 1ull);
+}
+
+// 2nK directed records keyed (row << 32 | col).
+__global__ void edge_records_k(i64 n, int K, const int64_t* __restrict__ nbr, const double* __restrict__ nbr_d2,
+                               unsigned long long* __restrict__ keys, double* __restrict__ vals) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= n * K) return;
+  const unsigned long long i = static_cast<unsigned long long>(t / K);
+  const unsigned long long j = static_cast<unsigned long long>(nbr[t]);
+  keys[2 * t] = (i << 32) | j;
+  keys[2 * t + 1] = (j << 32) | i;
+  vals[2 * t] = nbr_d2[t];
+  vals[2 * t + 1] = nbr_d2[t];
+}
+
+// Unique edges with a nonzero Gaussian weight (graph.cpp:116-124).
+__global__ void edge_weight_k(i64 m, const unsigned long long* __restrict__ keys, const double* __restrict__ d2,
+                              const double* __restrict__ sigma2, double* __restrict__ w, i64* __restrict__ keep) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const bool first = t == 0 || keys[t] != keys[t - 1];
+  const double dv = d2[t];
+  const double wv = dv == 0.0 ? 1.0 : exp(__ddiv_rn(-dv, *sigma2));
+  w[t] = wv;
+  keep[t] = (first && wv != 0.0) ? 1 : 0;
+}
+
+__global__ void edge_rowptr_k(i64 n, i64 m, const unsigned long long* __restrict__ keys,
+                              const i64* __restrict__ incl, i64* __restrict__ rp) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r > n) return;
+  // first record with row >= r
+  i64 lo = 0, hi = m;
+  const unsigned long long key = static_cast<unsigned long long>(r) << 32;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (keys[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  rp[r] = lo == 0 ? 0 : incl[lo - 1];
+}
+
+__global__ void edge_fill_k(i64 m, const unsigned long long* __restrict__ keys, const double* __restrict__ w,
+                            const i64* __restrict__ keep, const i64* __restrict__ incl, int* __restrict__ ci,
+                            double* __restrict__ v) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= m || !keep[t]) return;
+  const i64 o = incl[t] - 1;
+  ci[o] = static_cast<int>(keys[t] & 0xffffffffull);
+  v[o] = w[t];
+}
+
+// Row sums in CSR order (sparse.cpp:159-168).
+__global__ void row_sums_k(i64 n, const i64* __restrict__ rp, const double* __restrict__ v, double* __restrict__ out) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) s = __dadd_rn(s, v[k]);
+  out[r] = s;
+}
+
+// Laplacian rows (graph.cpp:16-43): combinatorial D - W (diagonal iff
+// deg != 0) or normalised I - D^-1/2 W D^-1/2 (entries -w dis_r dis_c,
+// exact zeros dropped).
+__device__ __forceinline__ double lap_off(int kind, double w, const double* dis, i64 r, int c) {
+  return kind == CPCAG_COMBINATORIAL ? -w : __dmul_rn(__dmul_rn(-w, dis[r]), dis[c]);
+}
+
+__global__ void dis_k(i64 n, const double* __restrict__ deg, double* __restrict__ dis) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) dis[i] = deg[i] > 0.0 ? __ddiv_rn(1.0, __dsqrt_rn(deg[i])) : 0.0;
+}
+
+__global__ void lap_count_k(i64 n, int kind, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ deg,
+                            const double* __restrict__ dis, i64* __restrict__ cnt) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  i64 c = (kind == CPCAG_COMBINATORIAL ? deg[r] != 0.0 : deg[r] > 0.0) ? 1 : 0;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) c += lap_off(kind, v[k], dis, r, ci[k]) != 0.0;
+  cnt[r] = c;
+}
+
+__global__ void lap_fill_k(i64 n, int kind, const i64* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ deg,
+                           const double* __restrict__ dis, const i64* __restrict__ orp, int* __restrict__ oci,
+                           double* __restrict__ ov) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const bool has_diag = kind == CPCAG_COMBINATORIAL ? deg[r] != 0.0 : deg[r] > 0.0;
+  const double dval = kind == CPCAG_COMBINATORIAL ? deg[r] : 1.0;
+  i64 o = orp[r];
+  bool placed = !has_diag;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) {
+    const int c = ci[k];
+    if (!placed && c > r) {
+      oci[o] = static_cast<int>(r);
+      ov[o] = dval;
+      ++o;
+      placed = true;
+    }
+    const double x = lap_off(kind, v[k], dis, r, c);
+    if (x != 0.0) {
+      oci[o] = c;
+      ov[o] = x;
+      ++o;
+    }
+  }
+  if (!placed) {
+    oci[o] = static_cast<int>(r);
+    ov[o] = dval;
+  }
+}
+
+i64 scan_counts(Ctx* c, const i64* cnt, i64 rows, i64* rp);  // kron.cu
+
+Csr* build_laplacian(Ctx* c, Csr* W, const double* deg, int kind) {
+  const i64 n = W->rows;
+  Csr* L = csr_alloc(c, n, n, 0);
+  std::unique_ptr<Csr> own(L);
+  DevBuf<double> dis(c, std::max<i64>(n, 1));
+  DevBuf<i64> cnt(c, std::max<i64>(n, 1));
+  if (n) {
+    dis_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, deg, dis.p);
+    launched(c);
+    lap_count_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, kind, W->rp, W->ci, W->v, deg, dis.p, cnt.p);
+    launched(c);
+  }
+  L->nnz = scan_counts(c, cnt.p, n, L->rp);
+  if (L->nnz) {
+    CUDA_OK(cudaMalloc(&L->ci, sizeof(int) * L->nnz));
+    CUDA_OK(cudaMalloc(&L->v, sizeof(double) * L->nnz));
+    lap_fill_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, kind, W->rp, W->ci, W->v, deg, dis.p, L->rp, L->ci, L->v);
+    launched(c);
+  }
+  L->sym = W->sym == 1 ? 1 : -1;
+  return own.release();
+}
+
+// ------------------------------------------------------------------ kNN
+struct KnnLists {
+  DevBuf<int64_t> nbr;
+  DevBuf<double> d2, mean;
+  i64 n = 0, d = 0;
+  DevBuf<double> Pm;
+};
+
+template <typename T>
+void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K, KnnLists* out) {
+  if (K < 1) invalid("knn graph: K must be >= 1");
+  const i64 n = axis_rows ? x_rows : x_cols;
+  const i64 d = axis_rows ? x_cols : x_rows;
+  if (n < K + 1) invalid("knn graph: need at least K+1 points, got " + std::to_string(n));
+  if (K > kMaxK) invalid("knn graph: K above " + std::to_string(kMaxK) + " is not supported on the device");
+  if (n > INT32_MAX) invalid("knn graph: more than 2^31-1 points are not supported");
+  out->n = n;
+  out->d = d;
+  out->Pm.alloc(c, std::max<i64>(n * d, 1));
+  DevBuf<double> sq(c, n);
+  if (n * d) {
+    gather_points_k<T><<<blocks_for(n * d), kBlock, 0, c->stream>>>(X, x_rows, n, d, axis_rows ? 1 : 0, out->Pm.p);
+    launched(c);
+  } else {
+    out->Pm.zero(c);
+  }
+  sqnorm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(out->Pm.p, n, d, sq.p);
+  launched(c);
+
+  const i64 n_tiles = (n + kTile - 1) / kTile;
+  // Split the candidate range so the grid covers >= 2 waves of 148 SMs.
+  i64 splits = std::max<i64>(1, (2 * static_cast<i64>(c->num_sms) + n_tiles - 1) / n_tiles);
+  splits = std::min<i64>({splits, n_tiles, 64});
+  const i64 tps = (n_tiles + splits - 1) / splits;
+  splits = (n_tiles + tps - 1) / tps;
+  DevBuf<double> cand_d(c, splits * n * K);
+  DevBuf<int> cand_j(c, splits * n * K);
+  DevBuf<int> dup(c, n);
+  dup.zero(c);
+  dim3 g(static_cast<unsigned>(n_tiles), static_cast<unsigned>(splits));
+  CUDA_OK(cudaFuncSetAttribute(knn_tile_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kKnnSmem)));
+  knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,
+                                       cand_j.p, dup.p);
+  launched(c);
+  DevBuf<unsigned long long> ndup(c, 1);
+  ndup.zero(c);
+  count_dup_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, dup.p, ndup.p);
+  launched(c);
+  const unsigned long long nd = read_back(c, ndup.p);
+  const i64 distinct = n - static_cast<i64>(nd);
+  if (distinct < K)
+    invalid("knn graph: fewer distinct points (" + std::to_string(distinct) + ") than K (" + std::to_string(K) + ")");
+  out->nbr.alloc(c, n * K);
+  out->d2.alloc(c, n * K);
+  out->mean.alloc(c, n);
+  knn_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(K), static_cast<int>(splits), cand_d.p,
+                                                          cand_j.p, out->nbr.p, out->d2.p, out->mean.p);
+  launched(c);
+}
+
+template <typename T>
+void knn_graph_device(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K, int kind,
+                      double sigma2_override, Csr** Wout, Csr** Lout, double* degrees_dev, double* sigma2) {
+  KnnLists kl;
+  knn_lists<T>(c, X, x_rows, x_cols, axis_rows, K, &kl);
+  const i64 n = kl.n;
+  DevBuf<double> s2(c, 1);
+  sigma2_k<<<1, 1, 0, c->stream>>>(n, static_cast<int>(K), kl.mean.p, sigma2_override, s2.p);
+  launched(c);
+
+  const i64 m = 2 * n * K;
+  DevBuf<unsigned long long> keys(c, m), keys_s(c, m);
+  DevBuf<double> vals(c, m), vals_s(c, m);
+  edge_records_k<<<blocks_for(n * K), kBlock, 0, c->stream>>>(n, static_cast<int>(K), kl.nbr.p, kl.d2.p, keys.p, vals.p);
+  launched(c);
+  int end_bit = 32;
+  while ((1ll << (end_bit - 32)) < n && end_bit < 64) ++end_bit;
+  size_t tmp = 0;
+  CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys.p, keys_s.p, vals.p, vals_s.p, static_cast<int>(m), 0,
+                                          end_bit, c->stream));
+  {
+    DevBuf<char> ws(c, tmp);
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(ws.p, tmp, keys.p, keys_s.p, vals.p, vals_s.p, static_cast<int>(m), 0,
+                                            end_bit, c->stream));
+    launched(c);
+  }
+  DevBuf<double> w(c, m);
+  DevBuf<i64> keep(c, m), incl(c, m);
+  edge_weight_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keys_s.p, vals_s.p, s2.p, w.p, keep.p);
+  launched(c);
+  {
+    size_t t2 = 0;
+    CUDA_OK(cub::DeviceScan::InclusiveSum(nullptr, t2, keep.p, incl.p, static_cast<int>(m), c->stream));
+    DevBuf<char> ws(c, t2);
+    CUDA_OK(cub::DeviceScan::InclusiveSum(ws.p, t2, keep.p, incl.p, static_cast<int>(m), c->stream));
+    launched(c);
+  }
+  i64 nnz = 0;
+  CUDA_OK(cudaMemcpyAsync(&nnz, incl.p + (m - 1), sizeof(i64), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  Csr* W = csr_alloc(c, n, n, nnz);
+  std::unique_ptr<Csr> ownW(W);
+  edge_rowptr_k<<<blocks_for(n + 1), kBlock, 0, c->stream>>>(n, m, keys_s.p, incl.p, W->rp);
+  launched(c);
+  if (nnz) {
+    edge_fill_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keys_s.p, w.p, keep.p, incl.p, W->ci, W->v);
+    launched(c);
+  }
+  W->sym = 1;
+  row_sums_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, W->rp, W->v, degrees_dev);
+  launched(c);
+  Csr* L = build_laplacian(c, W, degrees_dev, kind);
+  L->sym = 1;
+  *sigma2 = read_back(c, s2.p);
+  *Wout = ownW.release();
+  *Lout = L;
+}
+
+template void knn_graph_device<double>(Ctx*, const double*, i64, i64, bool, i64, int, double, Csr**, Csr**, double*,
+                                       double*);
+template void knn_graph_device<float>(Ctx*, const float*, i64, i64, bool, i64, int, double, Csr**, Csr**, double*,
+                                      double*);
+
+// ------------------------------------------------------------------ adjacency
+__global__ void adj_check_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, int* flags) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) {
+    if (ci[k] == r) atomicOr(flags, 1);  // nonzero diagonal (stored entries are nonzero)
+    if (v[k] < 0.0) atomicOr(flags, 2);
+  }
+}
+
+void graph_from_adjacency_device(Ctx* c, Csr* W, int kind, Csr** Lout, double* degrees_dev) {
+  if (W->rows != W->cols) invalid("adjacency must be square");
+  if (!csr_symmetric(c, W)) invalid("adjacency must be symmetric");
+  const i64 n = W->rows;
+  if (n) {
+    DevBuf<int> flags(c, 1);
+    flags.zero(c);
+    adj_check_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, W->rp, W->ci, W->v, flags.p);
+    launched(c);
+    const int f = read_back(c, flags.p);
+    if (f & 1) invalid("adjacency must have zero diagonal");
+    if (f & 2) invalid("adjacency weights must be nonnegative");
+    row_sums_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, W->rp, W->v, degrees_dev);
+    launched(c);
+  }
+  *Lout = build_laplacian(c, W, degrees_dev, kind);
+  (*Lout)->sym = 1;
+}
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+extern "C" int cpcag_cuda_knn_graph(cpcag_ctx ctx, int precision, const void* X, int64_t x_rows, int64_t x_cols,
+                                    int axis, int64_t K, int kind, double sigma2_override, cpcag_csr* adjacency,
+                                    cpcag_csr* laplacian, double* degrees, double* sigma2) {
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (!adjacency || !laplacian || !sigma2) invalid("null output pointer");
+      if (axis != CPCAG_AXIS_ROWS && axis != CPCAG_AXIS_COLS) invalid("knn graph: unknown axis");
+      if (kind != CPCAG_COMBINATORIAL && kind != CPCAG_NORMALIZED) invalid("knn graph: unknown laplacian kind");
+      const bool rows = axis == CPCAG_AXIS_ROWS;
+      if (K < 1) invalid("knn graph: K must be >= 1");
+      const i64 n = rows ? x_rows : x_cols;
+      InView<T> xin(c, static_cast<const T*>(X), static_cast<size_t>(x_rows * x_cols));
+      DevBuf<double> deg_scratch;
+      double* deg_d = nullptr;
+      const bool dev_deg = degrees && is_device_ptr(degrees);
+      if (dev_deg) {
+        deg_d = degrees;
+      } else {
+        deg_scratch.alloc(c, std::max<i64>(n, 1));
+        deg_d = deg_scratch.p;
+      }
+      Csr *W = nullptr, *L = nullptr;
+      knn_graph_device<T>(c, xin.d, x_rows, x_cols, rows, K, kind, sigma2_override, &W, &L, deg_d, sigma2);
+      if (degrees && !dev_deg && n)
+        CUDA_OK(cudaMemcpyAsync(degrees, deg_d, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      *adjacency = reinterpret_cast<cpcag_csr>(W);
+      *laplacian = reinterpret_cast<cpcag_csr>(L);
+    });
+  };
+  if (precision == CPCAG_F64) return run(double{});
+  if (precision == CPCAG_F32) return run(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int cpcag_cuda_knn(cpcag_ctx ctx, int precision, const void* X, int64_t x_rows, int64_t x_cols, int axis,
+                              int64_t K, int64_t* nbr, double* nbr_d2) {
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (axis != CPCAG_AXIS_ROWS && axis != CPCAG_AXIS_COLS) invalid("knn graph: unknown axis");
+      const bool rows = axis == CPCAG_AXIS_ROWS;
+      InView<T> xin(c, static_cast<const T*>(X), static_cast<size_t>(x_rows * x_cols));
+      KnnLists kl;
+      knn_lists<T>(c, xin.d, x_rows, x_cols, rows, K, &kl);
+      OutView<int64_t> on(c, nbr, static_cast<size_t>(kl.n * K));
+      OutView<double> od(c, nbr_d2, static_cast<size_t>(kl.n * K));
+      if (on.d) CUDA_OK(cudaMemcpyAsync(on.d, kl.nbr.p, sizeof(int64_t) * kl.n * K, cudaMemcpyDeviceToDevice, c->stream));
+      if (od.d) CUDA_OK(cudaMemcpyAsync(od.d, kl.d2.p, sizeof(double) * kl.n * K, cudaMemcpyDeviceToDevice, c->stream));
+      on.flush(c);
+      od.flush(c);
+      sync(c);
+    });
+  };
+  if (precision == CPCAG_F64) return run(double{});
+  if (precision == CPCAG_F32) return run(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int cpcag_cuda_graph_from_adjacency(cpcag_ctx ctx, cpcag_csr W, int kind, cpcag_csr* laplacian,
+                                               double* degrees) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (!laplacian) invalid("null output pointer");
+    Csr* Wc = as_csr(W);
+    OutView<double> deg(c, degrees, static_cast<size_t>(Wc->rows));
+    DevBuf<double> scratch;
+    double* dd = deg.d;
+    if (!dd) {
+      scratch.alloc(c, std::max<i64>(Wc->rows, 1));
+      dd = scratch.p;
+    }
+    Csr* L = nullptr;
+    graph_from_adjacency_device(c, Wc, kind, &L, dd);
+    deg.flush(c);
+    sync(c);
+    *laplacian = reinterpret_cast<cpcag_csr>(L);
+  });
+}

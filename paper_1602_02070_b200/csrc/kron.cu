@@ -1,0 +1,681 @@
+// kron.cu -- Kron reduction of a Laplacian onto the kept node set
+// (graph.cpp:170-235) and the Jacobi-preconditioned CG it runs per kept node
+// (solvers.cpp:7-27, solvers.hpp:33-74).
+//
+// Device plan:
+//   1. connected components of the pattern by lock-free union-find (roots =
+//      smallest node, the node the reference's error message names);
+//   2. interior / kept index maps, L_aa and L_ba gathered as device CSR,
+//      L_bb scattered into the dense Schur matrix S (keep order);
+//   3. every kept node j with a nonempty row of L_ba is one column of a
+//      batched, per-column-independent Jacobi PCG on L_aa (each column runs
+//      the reference recurrence with its own alpha/beta and its own stop
+//      test; finished columns freeze);
+//   4. S(:, j) -= L_ba z_j, S <- (S + S^T)/2, prune |v| <= prune_tol,
+//      CSR in keep order.
+// RHS blocks are sized to the free HBM so 50 000-column reductions run in
+// slices.
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <memory>
+#include <numeric>
+
+#include "common.cuh"
+#include "frpcag.cuh"
+
+namespace cpcag_cuda {
+
+// ------------------------------------------------------------------ components
+__device__ __forceinline__ int uf_root(volatile int* parent, int x) {
+  int p = parent[x];
+  while (p != x) {
+    x = p;
+    p = parent[x];
+  }
+  return x;
+}
+
+__global__ void uf_init_k(i64 n, int* parent) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) parent[i] = static_cast<int>(i);
+}
+
+__global__ void uf_hook_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci, int* parent) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+    int a = static_cast<int>(i), b = ci[k];
+    while (true) {
+      a = uf_root(parent, a);
+      b = uf_root(parent, b);
+      if (a == b) break;
+      if (a < b) {
+        const int t = a;
+        a = b;
+        b = t;
+      }
+      // link the larger root under the smaller one: the surviving root of a
+      // component is its smallest node.
+      const int old = atomicCAS(parent + a, a, b);
+      if (old == a) break;
+      a = old;
+    }
+  }
+}
+
+__global__ void uf_flatten_k(i64 n, int* parent) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) parent[i] = uf_root(parent, static_cast<int>(i));
+}
+
+__global__ void ground_k(i64 m, const i64* __restrict__ keep, const int* __restrict__ parent, int* grounded) {
+  const i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (j < m) grounded[parent[keep[j]]] = 1;
+}
+
+__global__ void ungrounded_k(i64 n, const int* __restrict__ parent, const int* __restrict__ grounded, int* first) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n && parent[i] == i && !grounded[i]) atomicMin(first, static_cast<int>(i));
+}
+
+// ------------------------------------------------------------------ gathers
+// Count / fill of a row-gathered, column-filtered submatrix: rows rsrc[r],
+// columns kept when cmap[col] >= 0 (cmap monotone, so columns stay sorted).
+__global__ void sub_count_k(i64 nr, const i64* __restrict__ rsrc, const i64* __restrict__ rp,
+                            const int* __restrict__ ci, const int* __restrict__ cmap, i64* __restrict__ cnt) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  const i64 u = rsrc[r];
+  i64 c = 0;
+  for (i64 k = rp[u]; k < rp[u + 1]; ++k) c += cmap[ci[k]] >= 0;
+  cnt[r] = c;
+}
+
+__global__ void sub_fill_k(i64 nr, const i64* __restrict__ rsrc, const i64* __restrict__ rp,
+                           const int* __restrict__ ci, const double* __restrict__ v,
+                           const int* __restrict__ cmap, const i64* __restrict__ orp,
+                           int* __restrict__ oci, double* __restrict__ ov) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  const i64 u = rsrc[r];
+  i64 o = orp[r];
+  for (i64 k = rp[u]; k < rp[u + 1]; ++k) {
+    const int m = cmap[ci[k]];
+    if (m >= 0) {
+      oci[o] = m;
+      ov[o] = v[k];
+      ++o;
+    }
+  }
+}
+
+// S(j, kpos[col]) = L(keep[j], col) for kept columns (dense m x m, col-major).
+__global__ void scatter_bb_k(i64 m, const i64* __restrict__ keep, const i64* __restrict__ rp,
+                             const int* __restrict__ ci, const double* __restrict__ v,
+                             const int* __restrict__ kpos, double* __restrict__ S) {
+  const i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const i64 u = keep[j];
+  for (i64 k = rp[u]; k < rp[u + 1]; ++k) {
+    const int q = kpos[ci[k]];
+    if (q >= 0) S[j + static_cast<i64>(q) * m] = v[k];
+  }
+}
+
+// Jacobi inverse of the diagonal (solvers.cpp:14-15: d > 0 ? 1/d : 1).
+__global__ void jacobi_inv_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                             const double* __restrict__ v, double* __restrict__ inv) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double d = 0.0;
+  for (i64 k = rp[i]; k < rp[i + 1]; ++k)
+    if (ci[k] == i) d = v[k];
+  inv[i] = d > 0.0 ? 1.0 / d : 1.0;
+}
+
+__global__ void ones_k(i64 n, double* a) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = 1.0;
+}
+
+// ------------------------------------------------------------------ batched PCG
+// Column c of the batch is one independent PCG (solvers.hpp:33-74).  Per
+// column scalars live in ColState; per-column reductions go through
+// partials[c][rb] and the last row-block of the column (per-column arrival
+// counter) finalises them in a fixed order.
+struct ColState {
+  double rho, rho_next, rr, curv, alpha, beta, norm_b, target, rel_res;
+  i64 it;
+  int done, err;  // err: 1 breakdown
+  unsigned cnt;
+  int pad;
+};
+
+constexpr int kPcgBlock = 256;
+
+__device__ __forceinline__ bool col_last_block(ColState* s, unsigned nrb) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&s->cnt, 1u) == nrb - 1;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+template <int NV>
+__device__ __forceinline__ void col_partial(double (&v)[NV], double* partials, i64 c, unsigned rb, unsigned nrb) {
+  block_sum<NV>(v);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) partials[(c * NV + q) * nrb + rb] = v[q];
+  }
+}
+
+template <int NV>
+__device__ __forceinline__ void col_total(double (&t)[NV], const double* partials, i64 c, unsigned nrb) {
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < nrb; i += blockDim.x) s += __ldcg(partials + (c * NV + q) * nrb + i);
+    t[q] = s;
+  }
+  block_sum<NV>(t);
+}
+
+// r = b - A x, z = inv o r, p = z; rho = <r, z>, ||b||^2, ||r||^2.
+__global__ void pcg_init_k(i64 n, i64 nb, const i64* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ inv,
+                           const double* __restrict__ B, const double* __restrict__ X, double* __restrict__ R,
+                           double* __restrict__ Z, double* __restrict__ P, double tol, i64 max_iter,
+                           double* partials, ColState* st, unsigned* ndone) {
+  const unsigned rb = blockIdx.x, nrb = gridDim.x;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    double s[3] = {0.0, 0.0, 0.0};
+    const i64 i = rb * (i64)blockDim.x + threadIdx.x;
+    if (i < n) {
+      const i64 at = i + c * n;
+      const double ax = pull_left(rp[i], rp[i + 1], ci, v, X + c * n);
+      const double b = B[at];
+      const double r = __dsub_rn(b, ax);
+      const double z = __dmul_rn(inv[i], r);
+      R[at] = r;
+      Z[at] = z;
+      P[at] = z;
+      s[0] = b * b;
+      s[1] = r * z;
+      s[2] = r * r;
+    }
+    col_partial<3>(s, partials, c, rb, nrb);
+    if (col_last_block(st + c, nrb)) {
+      double t[3];
+      col_total<3>(t, partials, c, nrb);
+      if (threadIdx.x == 0) {
+        ColState& S = st[c];
+        S.cnt = 0u;
+        S.norm_b = sqrt(t[0]);
+        S.rho = t[1];
+        S.rr = t[2];
+        S.it = 0;
+        S.target = tol * S.norm_b;
+        if (S.norm_b == 0.0) {
+          S.done = 2;  // zero rhs: x = b, converged, no true-residual pass
+          atomicAdd(ndone, 1u);
+        } else if (sqrt(S.rr) <= S.target || max_iter <= 0) {
+          S.done = 1;
+          atomicAdd(ndone, 1u);
+        }
+      }
+    }
+  }
+}
+
+__global__ void pcg_apply_k(i64 n, i64 nb, const i64* __restrict__ rp, const int* __restrict__ ci,
+                            const double* __restrict__ v, const double* __restrict__ P,
+                            double* __restrict__ AP, double* partials, ColState* st) {
+  const unsigned rb = blockIdx.x, nrb = gridDim.x;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    if (st[c].done) continue;
+    double s[1] = {0.0};
+    const i64 i = rb * (i64)blockDim.x + threadIdx.x;
+    if (i < n) {
+      const double ap = pull_left(rp[i], rp[i + 1], ci, v, P + c * n);
+      AP[i + c * n] = ap;
+      s[0] = P[i + c * n] * ap;
+    }
+    col_partial<1>(s, partials, c, rb, nrb);
+  }
+}
+
+__global__ void pcg_update_k(i64 n, i64 nb, const double* __restrict__ inv, double* __restrict__ X,
+                             double* __restrict__ R, double* __restrict__ Z, const double* __restrict__ P,
+                             const double* __restrict__ AP, double* partials, double* partials2,
+                             ColState* st, unsigned* ndone) {
+  const unsigned rb = blockIdx.x, nrb = gridDim.x;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    if (st[c].done) continue;
+    double t[1];
+    col_total<1>(t, partials, c, nrb);
+    const double curv = t[0];
+    const bool bad = !isfinite(curv) || curv <= 0.0;
+    double s[2] = {0.0, 0.0};
+    if (!bad) {
+      const double alpha = st[c].rho / curv;
+      const i64 i = rb * (i64)blockDim.x + threadIdx.x;
+      if (i < n) {
+        const i64 at = i + c * n;
+        X[at] = __dadd_rn(X[at], __dmul_rn(alpha, P[at]));
+        const double r = __dsub_rn(R[at], __dmul_rn(alpha, AP[at]));
+        const double z = __dmul_rn(inv[i], r);
+        R[at] = r;
+        Z[at] = z;
+        s[0] = r * z;
+        s[1] = r * r;
+      }
+    }
+    col_partial<2>(s, partials2, c, rb, nrb);
+    if (col_last_block(st + c, nrb) && threadIdx.x == 0) {
+      ColState& S = st[c];
+      S.cnt = 0u;
+      S.curv = curv;
+      if (bad) {
+        S.err = 1;
+        S.done = 1;
+        atomicAdd(ndone, 1u);
+      } else {
+        S.alpha = S.rho / curv;
+      }
+    }
+  }
+}
+
+__global__ void pcg_direction_k(i64 n, i64 nb, i64 max_iter, const double* __restrict__ Z,
+                                double* __restrict__ P, const double* partials2, ColState* st,
+                                unsigned* ndone) {
+  const unsigned rb = blockIdx.x, nrb = gridDim.x;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    if (st[c].done) continue;
+    double t[2];
+    col_total<2>(t, partials2, c, nrb);
+    const double beta = t[0] / st[c].rho;
+    const i64 i = rb * (i64)blockDim.x + threadIdx.x;
+    if (i < n) {
+      const i64 at = i + c * n;
+      P[at] = __dadd_rn(Z[at], __dmul_rn(beta, P[at]));
+    }
+    if (col_last_block(st + c, nrb) && threadIdx.x == 0) {
+      ColState& S = st[c];
+      S.cnt = 0u;
+      S.rho = t[0];
+      S.rr = t[1];
+      S.it += 1;
+      if (sqrt(S.rr) <= S.target || S.it >= max_iter) {
+        S.done = 1;
+        atomicAdd(ndone, 1u);
+      }
+    }
+  }
+}
+
+// True residual ||b - A x|| / ||b|| per column (solvers.hpp:69-72).
+__global__ void pcg_true_k(i64 n, i64 nb, const i64* __restrict__ rp, const int* __restrict__ ci,
+                           const double* __restrict__ v, const double* __restrict__ B,
+                           const double* __restrict__ X, double* partials, ColState* st) {
+  const unsigned rb = blockIdx.x, nrb = gridDim.x;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    if (st[c].done == 2) continue;
+    double s[1] = {0.0};
+    const i64 i = rb * (i64)blockDim.x + threadIdx.x;
+    if (i < n) {
+      const double e = __dsub_rn(B[i + c * n], pull_left(rp[i], rp[i + 1], ci, v, X + c * n));
+      s[0] = e * e;
+    }
+    col_partial<1>(s, partials, c, rb, nrb);
+    if (col_last_block(st + c, nrb)) {
+      double t[1];
+      col_total<1>(t, partials, c, nrb);
+      if (threadIdx.x == 0) {
+        st[c].cnt = 0u;
+        st[c].rel_res = sqrt(t[0]) / st[c].norm_b;
+      }
+    }
+  }
+}
+
+struct PcgBatchOut {
+  std::vector<ColState> cols;
+};
+
+// Solves A X(:,c) = B(:,c) for every column c (A square device CSR, inv the
+// Jacobi inverse or all ones).  X holds the start iterates and receives the
+// solutions.
+void pcg_batched(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb,
+                 double tol, i64 max_iter, PcgBatchOut* out) {
+  out->cols.assign(static_cast<size_t>(nb), ColState{});
+  if (nb == 0) return;
+  DevBuf<double> R(c, n * nb), Z(c, n * nb), P(c, n * nb), AP(c, n * nb);
+  const unsigned nrb = blocks_for(std::max<i64>(n, 1), kPcgBlock);
+  const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 32) / nrb);
+  dim3 g(nrb, static_cast<unsigned>(std::max<i64>(1, std::min<i64>({nb, ycap, 65535}))));
+  DevBuf<double> part(c, 3 * nb * nrb), part2(c, 2 * nb * nrb);
+  DevBuf<ColState> st(c, nb);
+  st.zero(c);
+  DevBuf<unsigned> ndone(c, 1);
+  ndone.zero(c);
+  pcg_init_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, Z.p, P.p, tol, max_iter,
+                                             part.p, st.p, ndone.p);
+  launched(c);
+  unsigned done = read_back(c, ndone.p);
+  const i64 chunk = 16;
+  while (done < nb) {
+    for (i64 k = 0; k < chunk; ++k) {
+      pcg_apply_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, P.p, AP.p, part.p, st.p);
+      launched(c);
+      pcg_update_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, inv, X, R.p, Z.p, P.p, AP.p, part.p, part2.p, st.p,
+                                                   ndone.p);
+      launched(c);
+      pcg_direction_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, max_iter, Z.p, P.p, part2.p, st.p, ndone.p);
+      launched(c);
+    }
+    done = read_back(c, ndone.p);
+  }
+  pcg_true_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, B, X, part.p, st.p);
+  launched(c);
+  CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+// ------------------------------------------------------------------ Schur assembly
+__global__ void rhs_fill_k(i64 ni, i64 nb, const i64* __restrict__ rows, const i64* __restrict__ rp,
+                           const int* __restrict__ ci, const double* __restrict__ v, double* __restrict__ B) {
+  const i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  const i64 j = rows[c];
+  for (i64 k = rp[j]; k < rp[j + 1]; ++k) B[ci[k] + c * ni] = v[k];
+}
+
+// S(i, j_c) -= (L_ba z_c)(i), CSR order per row (graph.cpp:230).
+__global__ void schur_update_k(i64 m, i64 ni, i64 nb, const i64* __restrict__ cols, const i64* __restrict__ rp,
+                               const int* __restrict__ ci, const double* __restrict__ v,
+                               const double* __restrict__ Zs, double* __restrict__ S) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    const double y = pull_left(rp[i], rp[i + 1], ci, v, Zs + c * ni);
+    const i64 at = i + cols[c] * m;
+    S[at] = __dsub_rn(S[at], y);
+  }
+}
+
+// Symmetrise (0.5 (S + S^T)) and prune (v != 0 and |v| > tol) row by row.
+__global__ void sym_count_k(i64 m, const double* __restrict__ S, double prune, bool symmetrize, i64* cnt) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  i64 k = 0;
+  for (i64 j = 0; j < m; ++j) {
+    const double x = symmetrize ? __dmul_rn(0.5, __dadd_rn(S[i + j * m], S[j + i * m])) : S[i + j * m];
+    k += (x != 0.0 && fabs(x) > prune);
+  }
+  cnt[i] = k;
+}
+
+__global__ void sym_fill_k(i64 m, const double* __restrict__ S, double prune, bool symmetrize,
+                           const i64* __restrict__ rp, int* __restrict__ ci, double* __restrict__ v) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  i64 o = rp[i];
+  for (i64 j = 0; j < m; ++j) {
+    const double x = symmetrize ? __dmul_rn(0.5, __dadd_rn(S[i + j * m], S[j + i * m])) : S[i + j * m];
+    if (x != 0.0 && fabs(x) > prune) {
+      ci[o] = static_cast<int>(j);
+      v[o] = x;
+      ++o;
+    }
+  }
+}
+
+// Exclusive scan of per-row counts into row pointers (rp[0] = 0); returns nnz.
+i64 scan_counts(Ctx* c, const i64* cnt, i64 rows, i64* rp) {
+  CUDA_OK(cudaMemsetAsync(rp, 0, sizeof(i64), c->stream));
+  if (rows == 0) return 0;
+  size_t tmp = 0;
+  CUDA_OK(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt, rp + 1, static_cast<int>(rows), c->stream));
+  DevBuf<char> ws(c, tmp);
+  CUDA_OK(cub::DeviceScan::InclusiveSum(ws.p, tmp, cnt, rp + 1, static_cast<int>(rows), c->stream));
+  launched(c);
+  i64 nnz = 0;
+  CUDA_OK(cudaMemcpyAsync(&nnz, rp + rows, sizeof(i64), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  return nnz;
+}
+
+// Dense (m x m, col-major) to CSR with the from_dense / prune rules.
+Csr* dense_to_csr(Ctx* c, const double* S, i64 m, double prune, bool symmetrize) {
+  DevBuf<i64> cnt(c, std::max<i64>(m, 1));
+  Csr* out = csr_alloc(c, m, m, 0);
+  if (m) {
+    sym_count_k<<<blocks_for(m, 128), 128, 0, c->stream>>>(m, S, prune, symmetrize, cnt.p);
+    launched(c);
+  }
+  const i64 nnz = scan_counts(c, cnt.p, m, out->rp);
+  out->nnz = nnz;
+  if (nnz) {
+    CUDA_OK(cudaMalloc(&out->ci, sizeof(int) * nnz));
+    CUDA_OK(cudaMalloc(&out->v, sizeof(double) * nnz));
+    sym_fill_k<<<blocks_for(m, 128), 128, 0, c->stream>>>(m, S, prune, symmetrize, out->rp, out->ci, out->v);
+    launched(c);
+  }
+  return out;
+}
+
+// Row-gathered, column-filtered submatrix as a new device CSR.
+Csr* gather_sub(Ctx* c, Csr* L, const i64* rsrc_dev, i64 nr, const int* cmap_dev, i64 ncols) {
+  Csr* out = csr_alloc(c, nr, ncols, 0);
+  DevBuf<i64> cnt(c, std::max<i64>(nr, 1));
+  if (nr) {
+    sub_count_k<<<blocks_for(nr), kBlock, 0, c->stream>>>(nr, rsrc_dev, L->rp, L->ci, cmap_dev, cnt.p);
+    launched(c);
+  }
+  const i64 nnz = scan_counts(c, cnt.p, nr, out->rp);
+  out->nnz = nnz;
+  if (nnz) {
+    CUDA_OK(cudaMalloc(&out->ci, sizeof(int) * nnz));
+    CUDA_OK(cudaMalloc(&out->v, sizeof(double) * nnz));
+    sub_fill_k<<<blocks_for(nr), kBlock, 0, c->stream>>>(nr, rsrc_dev, L->rp, L->ci, L->v, cmap_dev, out->rp,
+                                                         out->ci, out->v);
+    launched(c);
+  }
+  return out;
+}
+
+Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg_tol, double prune_tol) {
+  const i64 n = L->rows;
+  if (L->cols != n) invalid("kron reduction: square Laplacian required");
+  if (n > INT32_MAX) invalid("kron reduction: graphs above 2^31 nodes are not supported");
+  std::vector<int> kpos(static_cast<size_t>(n), -1);
+  for (size_t j = 0; j < keep.size(); ++j) {
+    const i64 u = keep[j];
+    if (u < 0 || u >= n) invalid("kron reduction: index out of range");
+    if (kpos[u] != -1) invalid("kron reduction: duplicate index");
+    kpos[u] = static_cast<int>(j);
+  }
+  const i64 m = static_cast<i64>(keep.size());
+
+  // graph.cpp:183-193: every component must hold a kept node.
+  DevBuf<i64> keep_d(c, std::max<i64>(m, 1));
+  if (m) CUDA_OK(cudaMemcpyAsync(keep_d.p, keep.data(), sizeof(i64) * m, cudaMemcpyHostToDevice, c->stream));
+  if (n) {
+    DevBuf<int> parent(c, n), grounded(c, n), first(c, 1);
+    grounded.zero(c);
+    const int big = INT32_MAX;
+    CUDA_OK(cudaMemcpyAsync(first.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    uf_init_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
+    launched(c);
+    uf_hook_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, L->rp, L->ci, parent.p);
+    launched(c);
+    uf_flatten_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
+    launched(c);
+    if (m) {
+      ground_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keep_d.p, parent.p, grounded.p);
+      launched(c);
+    }
+    ungrounded_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p, grounded.p, first.p);
+    launched(c);
+    const int bad = read_back(c, first.p);
+    if (bad != INT32_MAX)
+      runtime("kron reduction: connected component containing node " + std::to_string(bad) + " has no kept node");
+  }
+
+  std::vector<i64> interior;
+  interior.reserve(static_cast<size_t>(n - m));
+  std::vector<int> ipos(static_cast<size_t>(n), -1);
+  for (i64 u = 0; u < n; ++u)
+    if (kpos[u] < 0) {
+      ipos[u] = static_cast<int>(interior.size());
+      interior.push_back(u);
+    }
+  const i64 ni = static_cast<i64>(interior.size());
+
+  DevBuf<int> kpos_d(c, std::max<i64>(n, 1)), ipos_d(c, std::max<i64>(n, 1));
+  if (n) {
+    CUDA_OK(cudaMemcpyAsync(kpos_d.p, kpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ipos_d.p, ipos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+  }
+  // Dense Schur matrix initialised with L_bb (graph.cpp:208).
+  DevBuf<double> S(c, std::max<i64>(m * m, 1));
+  S.zero(c);
+  if (m) {
+    scatter_bb_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keep_d.p, L->rp, L->ci, L->v, kpos_d.p, S.p);
+    launched(c);
+  }
+  if (ni == 0) return dense_to_csr(c, S.p, m, 0.0, false);  // graph.cpp:201: L_bb as is
+
+  DevBuf<i64> int_d(c, ni);
+  CUDA_OK(cudaMemcpyAsync(int_d.p, interior.data(), sizeof(i64) * ni, cudaMemcpyHostToDevice, c->stream));
+  Csr* Laa = gather_sub(c, L, int_d.p, ni, ipos_d.p, ni);
+  Csr* Lba = gather_sub(c, L, keep_d.p, m, ipos_d.p, ni);
+  std::unique_ptr<Csr> own_aa(Laa), own_ba(Lba);
+  DevBuf<double> inv(c, ni);
+  jacobi_inv_k<<<blocks_for(ni), kBlock, 0, c->stream>>>(ni, Laa->rp, Laa->ci, Laa->v, inv.p);
+  launched(c);
+
+  // Kept nodes with a nonempty row of L_ba get a solve (graph.cpp:213-220).
+  std::vector<i64> rp_ba(static_cast<size_t>(m) + 1);
+  CUDA_OK(cudaMemcpyAsync(rp_ba.data(), Lba->rp, sizeof(i64) * (m + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  std::vector<i64> active;
+  for (i64 j = 0; j < m; ++j)
+    if (rp_ba[j + 1] > rp_ba[j]) active.push_back(j);
+
+  // Columns per slice: 6 dense |int| x b fp64 vectors within ~40% of free HBM.
+  size_t free_b = 0, total_b = 0;
+  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  const double per_col = 6.0 * 8.0 * static_cast<double>(ni) + 64.0;
+  i64 slice = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
+  slice = std::max<i64>(1, std::min<i64>(slice, static_cast<i64>(active.size())));
+  const i64 max_iter = 20 * ni + 100;
+
+  i64 fail_j = -1;
+  std::string fail_msg;
+  for (size_t s0 = 0; s0 < active.size(); s0 += static_cast<size_t>(slice)) {
+    const i64 nb = std::min<i64>(slice, static_cast<i64>(active.size() - s0));
+    std::vector<i64> cols(active.begin() + s0, active.begin() + s0 + nb);
+    DevBuf<i64> cols_d(c, nb);
+    CUDA_OK(cudaMemcpyAsync(cols_d.p, cols.data(), sizeof(i64) * nb, cudaMemcpyHostToDevice, c->stream));
+    DevBuf<double> B(c, ni * nb), X(c, ni * nb);
+    B.zero(c);
+    X.zero(c);
+    rhs_fill_k<<<blocks_for(nb), kBlock, 0, c->stream>>>(ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, B.p);
+    launched(c);
+    PcgBatchOut res;
+    pcg_batched(c, Laa, inv.p, B.p, X.p, ni, nb, pcg_tol, max_iter, &res);
+    for (i64 q = 0; q < nb; ++q) {
+      const ColState& cs = res.cols[q];
+      const i64 j = cols[q];
+      std::string msg;
+      if (cs.err)
+        msg = "pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(cs.it);
+      else if (cs.done != 2 && !(cs.rel_res <= pcg_tol))
+        msg = "kron reduction: interior solve failed to converge for kept node " + std::to_string(keep[j]);
+      if (!msg.empty() && (fail_j < 0 || j < fail_j)) {
+        fail_j = j;
+        fail_msg = msg;
+      }
+    }
+    if (fail_j >= 0) break;
+    dim3 g(blocks_for(m), static_cast<unsigned>(std::min<i64>(nb, 65535)));
+    schur_update_k<<<g, kBlock, 0, c->stream>>>(m, ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, X.p, S.p);
+    launched(c);
+  }
+  if (fail_j >= 0) runtime(fail_msg);
+  return dense_to_csr(c, S.p, m, prune_tol, true);
+}
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+extern "C" int cpcag_cuda_kron_reduce(cpcag_ctx ctx, cpcag_csr Lh, const int64_t* keep, int64_t n_keep,
+                                      double pcg_tol, double prune_tol, cpcag_csr* out) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (!out) invalid("null output pointer");
+    std::vector<i64> k(static_cast<size_t>(std::max<int64_t>(n_keep, 0)));
+    if (!k.empty()) {
+      if (is_device_ptr(keep))
+        CUDA_OK(cudaMemcpy(k.data(), keep, sizeof(i64) * k.size(), cudaMemcpyDeviceToHost));
+      else
+        std::copy(keep, keep + k.size(), k.begin());
+    }
+    Csr* r = kron_reduce_device(c, as_csr(Lh), k, pcg_tol, prune_tol);
+    r->sym = 1;
+    *out = reinterpret_cast<cpcag_csr>(r);
+  });
+}
+
+extern "C" int cpcag_cuda_pcg_solve(cpcag_ctx ctx, cpcag_csr Ah, const double* b, double* x, int64_t n,
+                                    double tol, int64_t max_iter, int jacobi, int64_t* iterations,
+                                    int* converged, double* relative_residual) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    Csr* A = as_csr(Ah);
+    if (A->rows != A->cols || A->cols != n) invalid("pcg: dimension mismatch");
+    InView<double> bin(c, b, static_cast<size_t>(n));
+    DevBuf<double> X(c, std::max<i64>(n, 1)), inv(c, std::max<i64>(n, 1));
+    if (n) {
+      if (is_device_ptr(x))
+        CUDA_OK(cudaMemcpyAsync(X.p, x, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      else
+        CUDA_OK(cudaMemcpyAsync(X.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+      if (jacobi)
+        jacobi_inv_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, A->rp, A->ci, A->v, inv.p);
+      else
+        ones_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, inv.p);
+      launched(c);
+    }
+    PcgBatchOut res;
+    pcg_batched(c, A, inv.p, bin.d, X.p, n, n ? 1 : 0, tol, max_iter, &res);
+    if (n == 0) {
+      *iterations = 0;
+      *converged = 1;
+      *relative_residual = 0.0;
+      return;
+    }
+    const ColState& cs = res.cols[0];
+    if (cs.err) runtime("pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(cs.it));
+    if (cs.done == 2) {
+      // Zero right-hand side: x = b (solvers.hpp:38-42).
+      CUDA_OK(cudaMemcpyAsync(X.p, bin.d, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (is_device_ptr(x))
+      CUDA_OK(cudaMemcpyAsync(x, X.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    else
+      CUDA_OK(cudaMemcpyAsync(x, X.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    *iterations = cs.it;
+    *converged = cs.done == 2 ? 1 : (cs.rel_res <= tol ? 1 : 0);
+    *relative_residual = cs.done == 2 ? 0.0 : cs.rel_res;
+  });
+}

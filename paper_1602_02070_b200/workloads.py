@@ -1,0 +1,171 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+The reference measures nothing on public data for this path; the paper's
+datasets (MNIST/USPS/ORL/videos) are not available, so these generators
+stand in with the configs' shapes, ranks and corruption levels
+(SURVEY.md Appendix A records each interpretation):
+
+  config 0  200 x 300, rank 10 on two 3-D noisy-circle kNN graphs, 5 %
+            additive outliers +-U(0, 5 max|X0|), a = b = 4.
+  config 1  10 304 x 1 000 (112 x 92 pixels x samples), rank 10 on the
+            8-neighbour pixel grid and a latent 1 000-node circle kNN graph,
+            10 % additive outliers U(-255, 255), X0 scaled to max|X0| = 255,
+            a = b = 10.
+  config 3  decoder only: kNN graphs (K=10) over N(0, I_64) points, p = 4 096,
+            n = 200 000, rank 20 low-pass basis, 1/8 x 1/8 sampling.
+
+Generation uses numpy/scipy only (LAPACK for the small eigenproblems); it is
+harness code, never timed.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def circle_points(n: int, rs: np.random.Generator, noise: float = 0.05) -> np.ndarray:
+    th = rs.uniform(0.0, 2.0 * math.pi, n)
+    pts = np.stack([np.cos(th), np.sin(th), np.zeros(n)])
+    return pts + noise * rs.standard_normal((3, n))
+
+
+def knn_laplacian_dense(pts: np.ndarray, K: int) -> np.ndarray:
+    """Dense combinatorial Laplacian of the reference kNN rule (graph.cpp:47-135)
+    for small generator graphs: union symmetrisation, sigma2 = mean of the
+    per-point mean squared kNN distance, w = exp(-d2 / sigma2)."""
+    P = pts.T
+    g = P @ P.T
+    sq = np.diag(g)
+    d2 = np.maximum(0.0, sq[:, None] + sq[None, :] - 2.0 * g)
+    n = d2.shape[0]
+    np.fill_diagonal(d2, np.inf)
+    idx = np.argsort(d2, axis=1, kind="stable")[:, :K]
+    near = np.take_along_axis(d2, idx, axis=1)
+    sigma2 = float(np.mean(near.mean(axis=1)))
+    A = np.zeros((n, n), bool)
+    A[np.repeat(np.arange(n), K), idx.ravel()] = True
+    A |= A.T
+    np.fill_diagonal(d2, 0.0)
+    W = np.where(A, np.exp(-d2 / sigma2), 0.0)
+    return np.diag(W.sum(axis=1)) - W
+
+
+def grid_adjacency(h: int, w: int):
+    """8-neighbour unit-weight pixel grid (scipy CSR), pixels column-major
+    within the image like a vectorised face."""
+    import scipy.sparse as sp
+
+    rows, cols = [], []
+    for dr, dc in [(0, 1), (1, -1), (1, 0), (1, 1)]:
+        r = np.arange(h)[:, None]
+        c = np.arange(w)[None, :]
+        r2, c2 = r + dr, c + dc
+        ok = (r2 >= 0) & (r2 < h) & (c2 >= 0) & (c2 < w)
+        a = np.broadcast_to(r + c * h, ok.shape)[ok]
+        b = np.broadcast_to(r2 + c2 * h, ok.shape)[ok]
+        rows += [a, b]
+        cols += [b, a]
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    W = sp.csr_matrix((np.ones(rows.size), (rows, cols)), shape=(h * w, h * w))
+    W.sum_duplicates()
+    W.sort_indices()
+    return W
+
+
+def smallest_eigvecs_dense(L: np.ndarray, k: int):
+    ev, V = np.linalg.eigh(0.5 * (L + L.T))
+    return ev[:k], V[:, :k]
+
+
+def smallest_eigvecs_sparse(L, k: int):
+    import scipy.sparse.linalg as sla
+
+    ev, V = sla.eigsh(L.tocsc(), k=k, sigma=-1e-3, which="LM")
+    order = np.argsort(ev)
+    return ev[order], V[:, order]
+
+
+def add_outliers(X0: np.ndarray, frac: float, rs: np.random.Generator, amp: float | None = None,
+                 symmetric_uniform: float | None = None) -> np.ndarray:
+    Y = X0.copy()
+    N = Y.size
+    m = int(round(frac * N))
+    pos = rs.choice(N, size=m, replace=False)
+    if symmetric_uniform is not None:
+        vals = rs.uniform(-symmetric_uniform, symmetric_uniform, m)
+    else:
+        vals = rs.choice([-1.0, 1.0], m) * rs.uniform(0.0, amp, m)
+    Yf = Y.reshape(-1, order="F")
+    Yf[pos] += vals
+    return Yf.reshape(Y.shape, order="F")
+
+
+@dataclass
+class Workload:
+    name: str
+    Y: np.ndarray          # p x n, column-major
+    X0: np.ndarray         # low-rank truth
+    a: int
+    b: int
+    gamma: float           # gamma_r = gamma_c (gamma' = 1/lambda)
+    fista_iters: int
+    cg_iters: int
+    cg_tol: float
+    lambda_k1_r: float = 1.0
+    lambda_k1_c: float = 1.0
+    W_r: object = None     # optional row adjacency (scipy CSR)
+    rank: int = 10
+
+
+def config0(seed: int = 1602, small: bool = False) -> tuple[np.ndarray, np.ndarray]:
+    """Config 0 data (Y, X0).  small=True shrinks to 60 x 80 for quick tests."""
+    rs = np.random.default_rng(seed)
+    p, n, k = (60, 80, 5) if small else (200, 300, 10)
+    Lr = knn_laplacian_dense(circle_points(p, rs), 10)
+    Lc = knn_laplacian_dense(circle_points(n, rs), 10)
+    _, U = smallest_eigvecs_dense(Lr, k)
+    _, V = smallest_eigvecs_dense(Lc, k)
+    A = rs.standard_normal((k, k))
+    X0 = np.asfortranarray(U @ A @ V.T)
+    Y = add_outliers(X0, 0.05, rs, amp=5.0 * np.abs(X0).max())
+    return np.asfortranarray(Y), X0
+
+
+def config0_workload(seed: int = 1602) -> Workload:
+    Y, X0 = config0(seed)
+    p, n = Y.shape
+    lr = _lambda_k1_of_knn(Y, True, 10, 10)
+    lc = _lambda_k1_of_knn(Y, False, 10, 10)
+    return Workload("cfg0 CPCA 200x300 fp64", Y, X0, 4, 4, math.sqrt(max(p, n)), 200, 100, 1e-8, lr, lc)
+
+
+def _lambda_k1_of_knn(Y, axis_rows, K, k):
+    pts = Y if axis_rows else Y.T
+    L = knn_laplacian_dense(np.ascontiguousarray(pts.T), K)
+    ev = np.linalg.eigvalsh(0.5 * (L + L.T))
+    return float(max(ev[k], 1e-12))
+
+
+def config1(seed: int = 1603) -> Workload:
+    """Config 1: face-image-sized CPCA (10 304 x 1 000)."""
+    rs = np.random.default_rng(seed)
+    h, w, n, k = 112, 92, 1000, 10
+    Wr = grid_adjacency(h, w)
+    deg = np.asarray(Wr.sum(axis=1)).ravel()
+    import scipy.sparse as sp
+
+    Lr = sp.diags(deg) - Wr
+    ev_r, U = smallest_eigvecs_sparse(Lr, k + 1)
+    Lc_lat = knn_laplacian_dense(circle_points(n, rs), 10)
+    _, V = smallest_eigvecs_dense(Lc_lat, k)
+    A = rs.standard_normal((k, k))
+    X0 = U[:, :k] @ A @ V.T
+    X0 *= 255.0 / np.abs(X0).max()
+    Y = add_outliers(np.asfortranarray(X0), 0.10, rs, symmetric_uniform=255.0)
+    p = h * w
+    lc = _lambda_k1_of_knn(Y, False, 10, k)
+    return Workload("cfg1 CPCA 10304x1000 fp32", np.asfortranarray(Y), np.asfortranarray(X0), 10, 10,
+                    math.sqrt(max(p, n)), 300, 200, 1e-8, float(ev_r[k]), lc, Wr, k)
