@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""Benchmark of the CPCA hot path on B200 (BASELINE.json metric, config 1).
+
+One step = one full CPCA run on config 1 (10 304 x 1 000, fp32): graphs (row
+graph from the 8-neighbour pixel-grid adjacency, column kNN graph K = 10 over
+the samples), sampling plan (a = b = 10), subsample, Kron reduction of both
+Laplacians, FRPCAG FISTA (300 iterations) and the alternate CG decoder
+(200 iterations), all through libcpcag_cuda.so.
+
+  value   seconds per CPCA run with the inputs resident in HBM (device
+          events on the launching stream; L2 flushed between steps).
+  e2e     the same run through the C-ABI with host (pinned) buffers: the
+          data matrix and the row adjacency go host->device and the decoded
+          and compressed matrices come back every step.
+  roofline  the dominant kernel (by device time in the timed region) against
+          the measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline  the oracle port (CPU restatement of the reference, all host
+          threads) on a bounded sample of the same run, extrapolated per
+          iteration (rank 0, N = 1 only).
+
+`--impl reference` times the oracle port alone (the reference itself cannot
+be built: Eigen3 is absent).  Under torchrun every rank runs
+an independent replica (config 1 is a one-GPU configuration); value is the
+max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CPCA end-to-end s; FRPCAG+decoder iters/s; achieved HBM GB/s vs B200 peak"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--fp64", action="store_true", help="compute in fp64 (config 1 is fp32)")
+    ap.add_argument("--json-out", default=None)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peaks():
+    for path in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(path):
+            with open(path) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        hi = max(sm)
+        loaded = [x for x in sm if x >= 0.5 * hi] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def make_workload():
+    from paper_1602_02070_b200 import workloads
+
+    return workloads.config1()
+
+
+def pipeline_config(P, wl):
+    return P.PipelineConfig(
+        knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
+        frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
+                              max_iter=wl.fista_iters),
+        decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-30, pcg_max_iter=wl.cg_iters),
+        lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1603)
+
+
+KERNEL_BYTES_DOC = {
+    "cg_apply": "read P + write AP (2 N w) + one read of L_r and L_c (nnz (w+4) + 8 (rows+1))",
+    "cg_residual": "read R, AP + write R (3 N w)",
+    "cg_update": "read X, P, R + write X, P (5 N w)",
+    "fista_grad_prox": "read Z, Y + write S (3 m w) + L~_r, L~_c once",
+    "fista_objective": "read S, Y (2 m w) + L~_r, L~_c once",
+    "fista_momentum": "read S, S_prev, Z + write Z_next (4 m w)",
+    "pcg_apply": "read P + write AP (2 |int| b 8) + L_aa once",
+    "pcg_update": "read X, R, P, AP + write X, R, Z (7 |int| b 8)",
+    "pcg_direction": "read Z, P + write P (3 |int| b 8)",
+}
+
+
+def kernel_bytes(tag, dims, w):
+    N, m, nnz_r, nnz_c, nnz_rt, nnz_ct, p, n, rr, rc = (dims[k] for k in (
+        "N", "m", "nnz_r", "nnz_c", "nnz_rt", "nnz_ct", "p", "n", "rho_r", "rho_c"))
+    if tag == "cg_apply":
+        return 2 * N * w + (nnz_r + nnz_c) * (w + 4) + 8 * (p + n + 2)
+    if tag == "cg_residual":
+        return 3 * N * w
+    if tag == "cg_update":
+        return 5 * N * w
+    if tag == "fista_grad_prox":
+        return 3 * m * w + (nnz_rt + nnz_ct) * (w + 4) + 8 * (rr + rc + 2)
+    if tag == "fista_objective":
+        return 2 * m * w + (nnz_rt + nnz_ct) * (w + 4) + 8 * (rr + rc + 2)
+    if tag == "fista_momentum":
+        return 4 * m * w
+    return None
+
+
+def run_ours(args, rank, local_rank, world):
+    import torch
+
+    import paper_1602_02070_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    wl = make_workload()
+    p, n = wl.Y.shape
+    prec_np = np.float64 if args.fp64 else np.float32
+    tdt = torch.float64 if args.fp64 else torch.float32
+    w = 8 if args.fp64 else 4
+    ctx = P.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=tdt, device="cuda").t()  # col-major p x n
+    Wr_sp = wl.W_r
+    Wr_dev = P.SparseMatrix.from_scipy(Wr_sp, ctx=ctx)
+    cfg = pipeline_config(P, wl)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    # operator sizes for the roofline accounting (untimed setup)
+    gc = P.build_knn_graph(Yd, "cols", 10, ctx=ctx)
+    nnz_c = gc.laplacian.nonzeros()
+    nnz_r = Wr_sp.nnz + p
+    rep = P.run_pipeline(Yd, cfg, W_r=Wr_dev, ctx=ctx)  # first (warm) run
+    plan = rep.plan
+    Lr_t = P.kron_reduce(P.graph_from_adjacency(Wr_dev, ctx=ctx).laplacian, plan.omega_r, 1e-11, ctx=ctx)
+    Lc_t = P.kron_reduce(gc.laplacian, plan.omega_c, 1e-11, ctx=ctx)
+    dims = dict(N=p * n, m=rep.rho_r * rep.rho_c, nnz_r=nnz_r, nnz_c=nnz_c, nnz_rt=Lr_t.nonzeros(),
+                nnz_ct=Lc_t.nonzeros(), p=p, n=n, rho_r=rep.rho_r, rho_c=rep.rho_c)
+    del Lr_t, Lc_t
+
+    for _ in range(max(args.warmup - 1, 0)):
+        P.run_pipeline(Yd, cfg, W_r=Wr_dev, ctx=ctx)
+    torch.cuda.synchronize()
+
+    # one profiled step (untimed) picks the dominant kernel
+    ctx.reset_kernel_timing()
+    ctx.kernel_timing_filter(None)
+    ctx.enable_kernel_timing(True)
+    P.run_pipeline(Yd, cfg, W_r=Wr_dev, ctx=ctx)
+    ctx.enable_kernel_timing(False)
+    prof = ctx.kernel_times()
+    top = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    ctx.reset_kernel_timing()
+    if top:
+        ctx.kernel_timing_filter([top])
+        ctx.enable_kernel_timing(True)
+
+    # ---------------- timed region (device events, L2 flushed between steps)
+    clocks = ClockSampler(local_rank)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ctx.reset_launch_count()
+    wall0 = time.perf_counter()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    reports = []
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        reports.append(P.run_pipeline(Yd, cfg, W_r=Wr_dev, ctx=ctx))
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    wall1 = time.perf_counter()
+    launches = ctx.launch_count
+    clk = clocks.stop()
+    ctx.enable_kernel_timing(False)
+    live = ctx.kernel_times()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = sum(step_ms) / len(step_ms)
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    last = reports[-1]
+    stages = last.stages
+    it_f, it_c = last.trace.iterations, last.decoder_iterations
+    iters = {
+        "fista_iters": it_f, "decoder_iters": it_c,
+        "fista_iters_per_s": it_f / (stages["solve"] / 1e3) if stages["solve"] > 0 else None,
+        "decoder_iters_per_s": it_c / (stages["decode"] / 1e3) if stages["decode"] > 0 else None,
+        "frpcag_plus_decoder_iters_per_s": (it_f + it_c) / ((stages["solve"] + stages["decode"]) / 1e3),
+    }
+
+    # ---------------- roofline of the dominant kernel
+    peak, peak_src = measured_peaks()
+    roof = None
+    if top and top in live:
+        nl, tot = live[top]
+        avg_ms = tot / nl
+        by = kernel_bytes(top, dims, w)
+        prof_total = sum(v[1] for v in prof.values())
+        share = prof[top][1] / prof_total if prof_total else None
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(top)
+            except Exception:
+                traffic = None
+        if by is not None:
+            achieved = by / (avg_ms / 1e3) / 1e9
+            roof = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(achieved / peak, 4), "traffic": traffic,
+                    "algorithmic_bytes_per_launch": by, "bytes_model": KERNEL_BYTES_DOC.get(top),
+                    "avg_launch_ms": round(avg_ms, 5), "launches_timed": nl, "share_of_step": share,
+                    "peak_source": peak_src}
+    # CG iteration as a whole (survey B_iter = 6 N w + (nnz_r + nnz_c)(w + 4))
+    cg_iter_bytes = 6 * p * n * w + (nnz_r + nnz_c) * (w + 4)
+    kernel_share = {k: round(v[1] / sum(x[1] for x in prof.values()), 4) for k, v in prof.items()} if prof else {}
+
+    # ---------------- e2e through the C-ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Yh_t = torch.empty((n, p), dtype=tdt, pin_memory=True)
+        Yh_t.copy_(torch.from_numpy(np.ascontiguousarray(wl.Y.T.astype(prec_np))))
+        Yh = Yh_t.numpy().T  # Fortran-ordered p x n view of pinned memory
+        rp, ci, vv = (Wr_sp.indptr.astype(np.int64), Wr_sp.indices.astype(np.int64), Wr_sp.data.astype(np.float64))
+        for _ in range(1):
+            P.run_pipeline(Yh, cfg, W_r=P.SparseMatrix.from_csr(p, p, rp, ci, vv, ctx=ctx), ctx=ctx)
+        ts = []
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            W = P.SparseMatrix.from_csr(p, p, rp, ci, vv, ctx=ctx)
+            r = P.run_pipeline(Yh, cfg, W_r=W, ctx=ctx)
+            t1 = time.perf_counter()
+            ts.append(t1 - t0)
+            h2d = Yh.nbytes + rp.nbytes + ci.nbytes + vv.nbytes
+            d2h = r.X.nbytes + r.Xt.nbytes + 8 * (r.rho_r + r.rho_c) + 8 * r.trace.iterations
+            del W
+        e_val = sum(ts) / len(ts)
+        if dist:
+            t = torch.tensor([e_val], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_val = float(t.item())
+        e2e = {"value": round(e_val, 5), "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "note": "wall clock around SparseMatrix.from_csr(host CSR) + run_pipeline(host pinned Y) -> host X, Xt"}
+
+    # ---------------- CPU baseline (oracle port, bounded sample)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(wl)
+
+    out = {
+        "metric": METRIC, "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",
+        "data": "synthetic: seeded config-1 generator (paper_1602_02070_b200/workloads.py), "
+                "rank-10 on pixel-grid and latent kNN graphs + 10% U(-255,255) outliers",
+        "config": {"workload": "cfg1: CPCA 10304x1000, pixel-grid W_r + kNN(K=10) L_c, a=b=10 "
+                               "(rho 1031x100), FRPCAG 300 it, alternate CG decoder 200 it",
+                   "global_batch": 1, "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "flushed between steps (512 MiB write outside the events)",
+                   "gamma": wl.gamma, "lambda_k1": [wl.lambda_k1_r, wl.lambda_k1_c]},
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
+        "clocks": clk, "stage_ms": {k: round(v, 3) for k, v in stages.items()}, "iters": iters,
+        "cg_iteration": {"bytes_B_iter": cg_iter_bytes,
+                         "achieved_GBps": round(cg_iter_bytes * it_c / (stages["decode"] / 1e3) / 1e9, 1)
+                         if stages["decode"] > 0 else None},
+        "kernel_share": kernel_share, "wall_s_timed_region": round(wall1 - wall0, 3),
+    }
+    if rank == 0:
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                f.write(line + "\n")
+    if dist:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_sample_times(wl, fista_iters=4, cg_iters=3):
+    """Time the oracle port on config 1: every stage in full except FISTA and
+    the decoder, which run a few iterations and are extrapolated linearly."""
+    from oracle import pyoracle as O
+
+    Y = np.asfortranarray(wl.Y.astype(np.float32).astype(np.float64))
+    p, n = Y.shape
+    t = {}
+    t0 = time.perf_counter()
+    gc = O.build_knn_graph(Y, False, 10)
+    Wr = O.Csr.from_scipy(wl.W_r)
+    gr = O.graph_from_adjacency(Wr)
+    t["graphs"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan = O.draw_plan(p, n, -(-p // wl.b), -(-n // wl.a), seed=1603)
+    t["plan"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Yt = O.subsample(Y, plan)
+    t["subsample"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Lrt = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
+    Lct = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
+    t["kron"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Xt, tr = O.fista_solve(Yt, Lrt, Lct, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, fista_iters))
+    t["solve_sample"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, cg_iters)
+    t["decode_sample"] = time.perf_counter() - t0
+    # the power iterations for the FISTA step are included once in solve_sample
+    full = (t["graphs"] + t["plan"] + t["subsample"] + t["kron"] + t["solve_sample"] / fista_iters * wl.fista_iters
+            + t["decode_sample"] / cg_iters * wl.cg_iters)
+    return full, t
+
+
+def cpu_baseline(wl):
+    from oracle import pyoracle as O
+
+    cores = O.get_threads()
+    full, t = cpu_sample_times(wl)
+    return {"value": round(full, 3), "unit": "s", "cores": cores, "kind": "port",
+            "sample": "oracle port on config 1: graphs, plan, subsample and Kron in full; FRPCAG 4 of 300 and "
+                      "decoder 3 of 200 iterations timed and extrapolated linearly "
+                      f"(stage seconds {json.dumps({k: round(v, 3) for k, v in t.items()})})"}
+
+
+def run_reference(args, rank, world):
+    if world > 1 and rank != 0:
+        return
+    from oracle import pyoracle as O
+
+    O.lib()
+    wl = make_workload()
+    cores = O.get_threads()
+    for _ in range(args.warmup):
+        cpu_sample_times(wl, 1, 1)
+    vals = []
+    t_all0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        full, t = cpu_sample_times(wl)
+        vals.append(full)
+        last = t
+    t_all1 = time.perf_counter()
+    v = sum(vals) / len(vals)
+    sample = ("oracle port (CPU restatement of the reference; the reference needs Eigen3, absent) on config 1: "
+              "graphs, plan, subsample, Kron in full; FRPCAG 4/300 and decoder 3/200 iterations per step, "
+              "extrapolated linearly to the full run")
+    out = {"metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded config-1 generator",
+           "config": {"workload": "cfg1: CPCA 10304x1000, pixel-grid W_r + kNN(K=10) L_c, a=b=10, "
+                                  "FRPCAG 300 it, alternate CG decoder 200 it", "parallelism": "cpu threads"},
+           "impl": "reference",
+           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": cores, "kind": "port", "sample": sample,
+                            "last_step_stage_s": {k: round(x, 3) for k, x in last.items()}},
+           "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s_timed_region": round(t_all1 - t_all0, 3)}
+    print(json.dumps(out), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            f.write(json.dumps(out) + "\n")
+
+
+def main():
+    args = parse()
+    rank, local_rank, world = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, local_rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -74,6 +74,18 @@ int cpcag_ctx_synchronize(cpcag_ctx ctx);
 int64_t cpcag_ctx_launch_count(cpcag_ctx ctx);
 void cpcag_ctx_reset_launch_count(cpcag_ctx ctx);
 
+/* Per-kernel device timing (CUDA events around every launch of the hot
+ * kernels, on the context stream).  Used by bench.py for live roofline
+ * figures; off by default. */
+int cpcag_ctx_enable_kernel_timing(cpcag_ctx ctx, int enable);
+/* Restrict timing to a comma-separated list of kernel tags (NULL/"" = all). */
+int cpcag_ctx_kernel_timing_filter(cpcag_ctx ctx, const char* tags_csv);
+int cpcag_ctx_reset_kernel_timing(cpcag_ctx ctx);
+int cpcag_ctx_kernel_timing_count(cpcag_ctx ctx);
+/* Entry `index` (0 <= index < count): kernel tag, launches, summed ms. */
+int cpcag_ctx_kernel_timing(cpcag_ctx ctx, int index, char* tag, int64_t tag_cap, int64_t* launches,
+                            double* total_ms);
+
 /* ------------------------------------------------------------------ sparse */
 /* SparseMatrix from CSR arrays (sparse.hpp:18-66).  The arrays must already
  * satisfy the CSR invariants (monotone row_ptr, strictly increasing columns

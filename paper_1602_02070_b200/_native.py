@@ -66,6 +66,11 @@ SIGNATURES = {
     "cpcag_ctx_synchronize": (C.c_int, [vp]),
     "cpcag_ctx_launch_count": (i64, [vp]),
     "cpcag_ctx_reset_launch_count": (None, [vp]),
+    "cpcag_ctx_enable_kernel_timing": (C.c_int, [vp, C.c_int]),
+    "cpcag_ctx_reset_kernel_timing": (C.c_int, [vp]),
+    "cpcag_ctx_kernel_timing_filter": (C.c_int, [vp, C.c_char_p]),
+    "cpcag_ctx_kernel_timing_count": (C.c_int, [vp]),
+    "cpcag_ctx_kernel_timing": (C.c_int, [vp, C.c_int, C.c_char_p, i64, ip, dp]),
     "cpcag_csr_create": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, C.POINTER(vp)]),
     "cpcag_csr_destroy": (C.c_int, [vp]),
     "cpcag_csr_info": (C.c_int, [vp, ip, ip, ip]),

@@ -139,6 +139,29 @@ class Context:
     def reset_launch_count(self):
         N.lib().cpcag_ctx_reset_launch_count(self._h)
 
+    def enable_kernel_timing(self, on: bool = True):
+        """CUDA-event timing of every hot-kernel launch (for roofline figures)."""
+        N.check(N.lib().cpcag_ctx_enable_kernel_timing(self._h, int(bool(on))))
+
+    def kernel_timing_filter(self, tags=None):
+        """Time only these kernel tags (None = all)."""
+        csv = ",".join(tags) if tags else ""
+        N.check(N.lib().cpcag_ctx_kernel_timing_filter(self._h, csv.encode()))
+
+    def reset_kernel_timing(self):
+        N.check(N.lib().cpcag_ctx_reset_kernel_timing(self._h))
+
+    def kernel_times(self) -> dict:
+        """{kernel tag: (launches, total device ms)} since the last reset."""
+        L = N.lib()
+        out = {}
+        for k in range(int(L.cpcag_ctx_kernel_timing_count(self._h))):
+            buf = C.create_string_buffer(64)
+            n, ms = N.i64(), N.dbl()
+            N.check(L.cpcag_ctx_kernel_timing(self._h, k, buf, 64, C.byref(n), C.byref(ms)))
+            out[buf.value.decode()] = (int(n.value), float(ms.value))
+        return out
+
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
             N.lib().cpcag_ctx_destroy(self._h)

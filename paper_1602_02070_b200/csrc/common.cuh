@@ -60,6 +60,18 @@ int guard(F&& body) {
 }
 
 // ------------------------------------------------------------------ context
+// Per-kernel device timing (CUDA events on the launching stream), enabled
+// on demand by the caller (bench.py) for the roofline figures.
+struct KernelTimes {
+  struct Rec {
+    std::string tag;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;        // in flight since the last harvest
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<std::string, std::pair<i64, double>>> totals;  // tag -> (launches, ms)
+};
+
 struct Ctx {
   int device = 0;
   int num_sms = 148;
@@ -68,6 +80,18 @@ struct Ctx {
   i64 launches = 0;
   void* pinned = nullptr;  // small pinned staging area for scalar read-back
   size_t pinned_bytes = 0;
+  bool timing = false;
+  std::string timing_filter;  // comma-separated tags; empty = all
+  KernelTimes kt;
+};
+
+// RAII scope timing one kernel launch under `tag` when timing is enabled.
+struct KScope {
+  Ctx* c;
+  const char* tag;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KScope(Ctx* ctx, const char* t);
+  ~KScope();
 };
 
 inline Ctx* as_ctx(cpcag_ctx c) {

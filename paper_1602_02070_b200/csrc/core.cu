@@ -44,6 +44,56 @@ double HostRng::gaussian() {
   return rad * std::cos(tau * b);
 }
 
+// ------------------------------------------------------------------ kernel timing
+static cudaEvent_t take_event(Ctx* c) {
+  if (!c->kt.pool.empty()) {
+    cudaEvent_t e = c->kt.pool.back();
+    c->kt.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_OK(cudaEventCreate(&e));
+  return e;
+}
+
+KScope::KScope(Ctx* ctx, const char* t) : c(ctx), tag(t) {
+  if (!c->timing) return;
+  if (!c->timing_filter.empty()) {
+    const std::string f = "," + c->timing_filter + ",";
+    if (f.find("," + std::string(t) + ",") == std::string::npos) return;
+  }
+  a = take_event(c);
+  b = take_event(c);
+  cudaEventRecord(a, c->stream);
+}
+
+KScope::~KScope() {
+  if (!a) return;
+  cudaEventRecord(b, c->stream);
+  c->kt.recs.push_back({tag, a, b});
+}
+
+static void harvest(Ctx* c) {
+  if (c->kt.recs.empty()) return;
+  CUDA_OK(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->kt.recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    bool found = false;
+    for (auto& t : c->kt.totals)
+      if (t.first == r.tag) {
+        t.second.first += 1;
+        t.second.second += ms;
+        found = true;
+        break;
+      }
+    if (!found) c->kt.totals.push_back({r.tag, {1, static_cast<double>(ms)}});
+    c->kt.pool.push_back(r.a);
+    c->kt.pool.push_back(r.b);
+  }
+  c->kt.recs.clear();
+}
+
 // ------------------------------------------------------------------ CSR
 Csr::~Csr() {
   cudaFree(rp);
@@ -565,6 +615,11 @@ int cpcag_ctx_destroy(cpcag_ctx ctx) {
   return guard([&] {
     Ctx* c = as_ctx(ctx);
     cudaStreamSynchronize(c->stream);
+    for (auto& r : c->kt.recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    for (auto e : c->kt.pool) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
     cudaStreamDestroy(c->own);
     delete c;
@@ -582,6 +637,56 @@ void* cpcag_ctx_stream(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)
 
 int cpcag_ctx_synchronize(cpcag_ctx ctx) {
   return guard([&] { sync(as_ctx(ctx)); });
+}
+
+int cpcag_ctx_enable_kernel_timing(cpcag_ctx ctx, int enable) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    harvest(c);
+    c->timing = enable != 0;
+  });
+}
+
+int cpcag_ctx_kernel_timing_filter(cpcag_ctx ctx, const char* tags_csv) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    c->timing_filter = tags_csv ? tags_csv : "";
+  });
+}
+
+int cpcag_ctx_reset_kernel_timing(cpcag_ctx ctx) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    harvest(c);
+    c->kt.totals.clear();
+  });
+}
+
+int cpcag_ctx_kernel_timing(cpcag_ctx ctx, int index, char* tag, int64_t tag_cap, int64_t* launches,
+                            double* total_ms) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    harvest(c);
+    if (index < 0 || index >= static_cast<int>(c->kt.totals.size())) fail(CPCAG_ERR_OUT_OF_RANGE, "kernel timing index out of range");
+    const auto& t = c->kt.totals[static_cast<size_t>(index)];
+    if (tag && tag_cap > 0) {
+      std::strncpy(tag, t.first.c_str(), static_cast<size_t>(tag_cap - 1));
+      tag[tag_cap - 1] = 0;
+    }
+    if (launches) *launches = t.second.first;
+    if (total_ms) *total_ms = t.second.second;
+  });
+}
+
+int cpcag_ctx_kernel_timing_count(cpcag_ctx ctx) {
+  if (!ctx) return 0;
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  try {
+    harvest(c);
+  } catch (...) {
+    return 0;
+  }
+  return static_cast<int>(c->kt.totals.size());
 }
 
 int64_t cpcag_ctx_launch_count(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->launches : 0; }

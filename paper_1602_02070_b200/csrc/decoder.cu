@@ -257,12 +257,21 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const i64 chunk = 32;
   while (!host.done) {
     for (i64 k = 0; k < chunk; ++k) {
-      cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
-      launched(c);
-      cg_residual_k<T><<<nb1, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
-      launched(c);
-      cg_update_k<T><<<nb1, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
-      launched(c);
+      {
+        KScope ks_(c, "cg_apply");
+        cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "cg_residual");
+        cg_residual_k<T><<<nb1, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "cg_update");
+        cg_update_k<T><<<nb1, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
+        launched(c);
+      }
     }
     host = read_back(c, st.p);
   }

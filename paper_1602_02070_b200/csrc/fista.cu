@@ -168,15 +168,24 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       T* Sj = Sb[j & 1].p;
       const T* Sprev = Sb[(j - 1) & 1].p;
       T* Znext = Zb[(j + 1) & 1].p;
-      fista_grad_prox_k<T><<<g2, kBlock, 0, c->stream>>>(rows, cols, pr, pc, s_r, s_c, use_r, use_c,
-                                                         cfg.loss, stepT, Zj, Y, Sj, st.p);
-      launched(c);
-      fista_objective_k<T><<<g2, kBlock, 0, c->stream>>>(rows, cols, pr, pc, cfg.gamma_r, cfg.gamma_c,
-                                                         cfg.loss, Sj, Y, part.p, tr.p, st.p);
-      launched(c);
-      fista_momentum_k<T><<<nb1, kBlock, 0, c->stream>>>(N, Sj, Sprev, Zj, Znext, cfg.tol,
-                                                         cfg.max_iter, part.p, st.p);
-      launched(c);
+      {
+        KScope ks_(c, "fista_grad_prox");
+        fista_grad_prox_k<T><<<g2, kBlock, 0, c->stream>>>(rows, cols, pr, pc, s_r, s_c, use_r, use_c,
+                                                           cfg.loss, stepT, Zj, Y, Sj, st.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "fista_objective");
+        fista_objective_k<T><<<g2, kBlock, 0, c->stream>>>(rows, cols, pr, pc, cfg.gamma_r, cfg.gamma_c,
+                                                           cfg.loss, Sj, Y, part.p, tr.p, st.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "fista_momentum");
+        fista_momentum_k<T><<<nb1, kBlock, 0, c->stream>>>(N, Sj, Sprev, Zj, Znext, cfg.tol,
+                                                           cfg.max_iter, part.p, st.p);
+        launched(c);
+      }
     }
     host = read_back(c, st.p);
     if (host.done) break;

@@ -397,9 +397,12 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   dup.zero(c);
   dim3 g(static_cast<unsigned>(n_tiles), static_cast<unsigned>(splits));
   CUDA_OK(cudaFuncSetAttribute(knn_tile_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kKnnSmem)));
-  knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,
-                                       cand_j.p, dup.p);
-  launched(c);
+  {
+    KScope ks_(c, "knn_tile");
+    knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,
+                                         cand_j.p, dup.p);
+    launched(c);
+  }
   DevBuf<unsigned long long> ndup(c, 1);
   ndup.zero(c);
   count_dup_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, dup.p, ndup.p);

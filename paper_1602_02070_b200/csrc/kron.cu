@@ -371,13 +371,22 @@ void pcg_batched(Ctx* c, Csr* A, const double* inv, const double* B, double* X, 
   const i64 chunk = 16;
   while (done < nb) {
     for (i64 k = 0; k < chunk; ++k) {
-      pcg_apply_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, P.p, AP.p, part.p, st.p);
-      launched(c);
-      pcg_update_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, inv, X, R.p, Z.p, P.p, AP.p, part.p, part2.p, st.p,
-                                                   ndone.p);
-      launched(c);
-      pcg_direction_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, max_iter, Z.p, P.p, part2.p, st.p, ndone.p);
-      launched(c);
+      {
+        KScope ks_(c, "pcg_apply");
+        pcg_apply_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, P.p, AP.p, part.p, st.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "pcg_update");
+        pcg_update_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, inv, X, R.p, Z.p, P.p, AP.p, part.p, part2.p, st.p,
+                                                     ndone.p);
+        launched(c);
+      }
+      {
+        KScope ks_(c, "pcg_direction");
+        pcg_direction_k<<<g, kPcgBlock, 0, c->stream>>>(n, nb, max_iter, Z.p, P.p, part2.p, st.p, ndone.p);
+        launched(c);
+      }
     }
     done = read_back(c, ndone.p);
   }
