@@ -352,19 +352,79 @@ template void dot_device<double>(Ctx*, const double*, const double*, i64, double
 template void dot_device<float>(Ctx*, const float*, const float*, i64, double*);
 
 // ------------------------------------------------------------------ power iteration
-// solvers.cpp:29-53 as one cooperative kernel: w = A v (CSR order), ||w|| by
-// a fixed-order grid reduction every block evaluates identically, v = w/||w||,
-// stop when |est - prev| <= tol est.  v0 comes from the reference RNG on the
-// host (bit-identical).
+// solvers.cpp:29-53: w = A v, est = ||w||, v = w / est, stop when
+// |est - prev| <= tol est.  v0 comes from the reference RNG on the host
+// (bit-identical).  The SpMV is warp-per-row (lanes stride the row, fixed
+// shuffle tree), so rows of the near-dense Kron-reduced Laplacians (~600
+// nnz/row at config 1) read coalesced.
 struct PowerState {
   double est;
   i64 iterations;
   unsigned bar_count, bar_gen;
 };
 
+__device__ __forceinline__ double warp_row_dot(i64 k0, i64 k1, const int* __restrict__ ci,
+                                               const double* __restrict__ val, const double* x, int lane) {
+  double acc = 0.0;
+  for (i64 k = k0 + lane; k < k1; k += 32) acc += val[k] * x[ci[k]];
+  return warp_sum(acc);
+}
+
+// Small operators: the whole iteration in one CTA, v and w in shared memory.
+__global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __restrict__ rp,
+                                                           const int* __restrict__ ci,
+                                                           const double* __restrict__ val,
+                                                           const double* __restrict__ v0, double tol,
+                                                           i64 max_iter, PowerState* st) {
+  extern __shared__ double sm[];
+  double* vs = sm;
+  double* ws = sm + n;
+  __shared__ double warp_part[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
+  __syncthreads();
+  double est = 0.0;
+  i64 it = 0;
+  for (; it < max_iter; ++it) {
+    double part = 0.0;
+    for (i64 r = wid; r < n; r += nw) {
+      const double acc = warp_row_dot(rp[r], rp[r + 1], ci, val, vs, lane);
+      if (lane == 0) {
+        ws[r] = acc;
+        part += acc * acc;
+      }
+    }
+    if (lane == 0) warp_part[wid] = part;
+    __syncthreads();
+    double tot = lane < nw ? warp_part[lane] : 0.0;
+    tot = warp_sum(tot);  // every warp computes the same total
+    const double nrm = sqrt(tot);
+    if (nrm == 0.0) {
+      est = 0.0;
+      break;
+    }
+    const double prev = est;
+    est = nrm;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(ws[i], nrm);
+    __syncthreads();
+    if (it > 0 && fabs(est - prev) <= tol * est) {
+      ++it;
+      break;
+    }
+  }
+  if (threadIdx.x == 0) {
+    st->est = est;
+    st->iterations = it;
+  }
+}
+
+// Large operators: cooperative grid, one warp per row, fixed-order grid sum.
 __global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
                              const double* __restrict__ val, double* v, double* w, double* partials,
                              double tol, i64 max_iter, PowerState* st) {
+  const int lane = threadIdx.x & 31;
+  const i64 gwarp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
   const i64 gtid = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   const i64 gstride = (i64)gridDim.x * blockDim.x;
   const unsigned nb = gridDim.x;
@@ -372,11 +432,14 @@ __global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __res
   i64 it = 0;
   for (; it < max_iter; ++it) {
     double s[1] = {0.0};
-    for (i64 r = gtid; r < n; r += gstride) {
+    for (i64 r = gwarp; r < n; r += nwarps) {
       double acc = 0.0;
-      for (i64 k = rp[r]; k < rp[r + 1]; ++k) acc = __dadd_rn(acc, __dmul_rn(val[k], __ldcg(v + ci[k])));
-      w[r] = acc;
-      s[0] += acc * acc;
+      for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) acc += val[k] * __ldcg(v + ci[k]);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        w[r] = acc;
+        s[0] += acc * acc;
+      }
     }
     block_sum<1>(s);
     if (threadIdx.x == 0) partials[(it & 1) * nb + blockIdx.x] = s[0];
@@ -384,14 +447,14 @@ __global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __res
     double t[1] = {0.0};
     for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) t[0] += __ldcg(partials + (it & 1) * nb + i);
     block_sum<1>(t);
-    const double nw = sqrt(t[0]);
-    if (nw == 0.0) {
+    const double nrm = sqrt(t[0]);
+    if (nrm == 0.0) {
       est = 0.0;
       break;
     }
     const double prev = est;
-    est = nw;
-    for (i64 r = gtid; r < n; r += gstride) v[r] = __ddiv_rn(w[r], nw);
+    est = nrm;
+    for (i64 r = gtid; r < n; r += gstride) v[r] = __ddiv_rn(__ldcg(w + r), nrm);
     if (it > 0 && fabs(est - prev) <= tol * est) {
       ++it;
       break;
@@ -419,13 +482,24 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   if (max_iter <= 0) return 0.0;
   DevBuf<double> v(c, n), w(c, n);
   CUDA_OK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_k, kBlock, 0));
-  const i64 want = (n + kBlock - 1) / kBlock;
-  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(want, (i64)per_sm * c->num_sms)));
-  DevBuf<double> part(c, 2 * nb);
   DevBuf<PowerState> st(c, 1);
   st.zero(c);
+  const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
+  if (small_smem <= 200 * 1024) {
+    CUDA_OK(cudaFuncSetAttribute(power_iter_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(small_smem)));
+    {
+      KScope ks_(c, "power_iter");
+      power_iter_small_k<<<1, 512, small_smem, c->stream>>>(n, A->rp, A->ci, A->v, v.p, tol, max_iter, st.p);
+      launched(c);
+    }
+    return read_back(c, st.p).est;
+  }
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_k, kBlock, 0));
+  const i64 want = (n * 32 + kBlock - 1) / kBlock;
+  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(want, (i64)per_sm * c->num_sms)));
+  DevBuf<double> part(c, 2 * nb);
   const i64* rp = A->rp;
   const int* ci = A->ci;
   const double* val = A->v;
@@ -435,10 +509,12 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   PowerState* sp = st.p;
   void* args[] = {(void*)&n, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp,
                   (void*)&pp, (void*)&tol, (void*)&max_iter, (void*)&sp};
-  CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_k, dim3(nb), dim3(kBlock), args, 0, c->stream));
-  launched(c);
-  const PowerState out = read_back(c, st.p);
-  return out.est;
+  {
+    KScope ks_(c, "power_iter");
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_k, dim3(nb), dim3(kBlock), args, 0, c->stream));
+    launched(c);
+  }
+  return read_back(c, st.p).est;
 }
 
 // ------------------------------------------------------------------ gather / prox / grad / objective

@@ -231,3 +231,19 @@ def test_launches_are_counted(P, ctx):
     L = random_laplacian(50, 0.1, 3)
     to_device(ctx, L).multiply(np.ones((50, 3)))
     assert ctx.launch_count >= 1
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_fista_dense_operator_path(P, ctx, prec):
+    """Kron-reduced Laplacians are near dense: the dense tiled-GEMM path."""
+    Lr_full, Lc_full = knn_laplacian(300, 3, 10, 31), knn_laplacian(240, 3, 10, 32)
+    plan = O.draw_plan(300, 240, 75, 60, seed=5)
+    Lr, Lc = O.kron_reduce(Lr_full, plan.omega_r, 1e-11), O.kron_reduce(Lc_full, plan.omega_c, 1e-11)
+    assert Lr.nnz >= 0.25 * 75 * 75 and Lc.nnz >= 0.25 * 60 * 60
+    Y = np.random.default_rng(4).standard_normal((75, 60)) * 3.0
+    dt = np.float64 if prec == "f64" else np.float32
+    cfg = P.FrpcagConfig(gamma_r=8.0, gamma_c=8.0, tol=1e-300, max_iter=150)
+    X, tr = P.fista_solve(Y.astype(dt), to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+    Xo, tro = O.fista_solve(Y.astype(dt).astype(np.float64), Lr, Lc, O.FrpcagConfig(8.0, 8.0, "l1", 1e-300, 150))
+    assert rel(X, Xo) <= (1e-9 if prec == "f64" else 1e-4)
+    assert np.allclose(tr.objective, tro.objective, rtol=1e-9 if prec == "f64" else 1e-4)
