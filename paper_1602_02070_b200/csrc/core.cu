@@ -418,31 +418,62 @@ __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __re
   }
 }
 
-// Large operators: cooperative grid, one warp per row, fixed-order grid sum.
-__global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
-                             const double* __restrict__ val, double* v, double* w, double* partials,
-                             double tol, i64 max_iter, PowerState* st) {
-  const int lane = threadIdx.x & 31;
-  const i64 gwarp = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
-  const i64 nwarps = ((i64)gridDim.x * blockDim.x) >> 5;
-  const i64 gtid = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  const i64 gstride = (i64)gridDim.x * blockDim.x;
+// Large operators: cooperative grid, one CTA per SM, each CTA owning a
+// contiguous slice of rows whose CSR entries stay resident in its shared
+// memory for the whole iteration (when they fit), a private shared-memory copy
+// of v, and ONE grid barrier per iteration: every CTA publishes its slice of
+// w (double-buffered by iteration parity) and its partial ||w||^2, then every
+// CTA sums the partials in the same fixed order and renormalises the whole of
+// v into its own shared copy.
+__global__ void __launch_bounds__(256) power_iter_coop_k(i64 n, const i64* __restrict__ rp,
+                                                         const int* __restrict__ ci,
+                                                         const double* __restrict__ val,
+                                                         const double* __restrict__ v0, double* wbuf,
+                                                         double* partials, double tol, i64 max_iter,
+                                                         int slice_in_smem, int v_in_smem, PowerState* st) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned nb = gridDim.x;
+  const i64 r0 = (n * blockIdx.x) / nb, r1 = (n * (blockIdx.x + 1)) / nb;
+  const i64 k0 = rp[r0], k1 = rp[r1];
+  double* vs = sm;                                   // n doubles (if v_in_smem)
+  double* sval = sm + (v_in_smem ? n : 0);           // slice values
+  int* sci = reinterpret_cast<int*>(sval + (slice_in_smem ? (k1 - k0) : 0));
+  if (slice_in_smem)
+    for (i64 k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      sval[k - k0] = val[k];
+      sci[k - k0] = ci[k];
+    }
+  if (v_in_smem)
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
+  __shared__ double warp_part[32];
+  __syncthreads();
+  const double* vsrc = v_in_smem ? vs : v0;
   double est = 0.0;
   i64 it = 0;
   for (; it < max_iter; ++it) {
-    double s[1] = {0.0};
-    for (i64 r = gwarp; r < n; r += nwarps) {
+    double* w = wbuf + (it & 1) * n;
+    double part = 0.0;
+    for (i64 r = r0 + wid; r < r1; r += nw) {
       double acc = 0.0;
-      for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) acc += val[k] * __ldcg(v + ci[k]);
+      if (slice_in_smem) {
+        for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) acc += sval[k - k0] * vsrc[sci[k - k0]];
+      } else {
+        for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) acc += val[k] * vsrc[ci[k]];
+      }
       acc = warp_sum(acc);
       if (lane == 0) {
         w[r] = acc;
-        s[0] += acc * acc;
+        part += acc * acc;
       }
     }
-    block_sum<1>(s);
-    if (threadIdx.x == 0) partials[(it & 1) * nb + blockIdx.x] = s[0];
+    if (lane == 0) warp_part[wid] = part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+      for (int q = 0; q < nw; ++q) b += warp_part[q];
+      partials[(it & 1) * nb + blockIdx.x] = b;
+    }
     grid_barrier(&st->bar_count, &st->bar_gen);
     double t[1] = {0.0};
     for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) t[0] += __ldcg(partials + (it & 1) * nb + i);
@@ -454,14 +485,22 @@ __global__ void power_iter_k(i64 n, const i64* __restrict__ rp, const int* __res
     }
     const double prev = est;
     est = nrm;
-    for (i64 r = gtid; r < n; r += gstride) v[r] = __ddiv_rn(__ldcg(w + r), nrm);
+    if (v_in_smem) {
+      for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(__ldcg(w + i), nrm);
+      __syncthreads();
+    } else {
+      // v lives in global memory: the grid renormalises its own rows and
+      // needs a second barrier before the next product reads them.
+      double* vg = const_cast<double*>(v0);
+      for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(w[i], nrm);
+    }
     if (it > 0 && fabs(est - prev) <= tol * est) {
       ++it;
       break;
     }
-    grid_barrier(&st->bar_count, &st->bar_gen);
+    if (!v_in_smem) grid_barrier(&st->bar_count, &st->bar_gen);
   }
-  if (gtid == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->est = est;
     st->iterations = it;
   }
@@ -485,7 +524,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   DevBuf<PowerState> st(c, 1);
   st.zero(c);
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
-  if (small_smem <= 200 * 1024) {
+  if (small_smem <= 200 * 1024 && A->nnz <= 4096) {
     CUDA_OK(cudaFuncSetAttribute(power_iter_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(small_smem)));
     {
@@ -495,23 +534,38 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
     }
     return read_back(c, st.p).est;
   }
+  // One CTA per SM; slice CSR and v in shared memory when they fit.
+  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(c->num_sms, (n + 3) / 4)));
+  std::vector<i64> rph(static_cast<size_t>(n) + 1);
+  CUDA_OK(cudaMemcpyAsync(rph.data(), A->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  i64 max_slice = 0;
+  for (unsigned b = 0; b < nb; ++b) {
+    const i64 r0 = (n * b) / nb, r1 = (n * (b + 1)) / nb;
+    max_slice = std::max(max_slice, rph[r1] - rph[r0]);
+  }
+  const size_t budget = 200 * 1024;
+  int v_in_smem = static_cast<size_t>(n) * 8 <= budget / 2 ? 1 : 0;
+  size_t smem = v_in_smem ? static_cast<size_t>(n) * 8 : 0;
+  int slice_in_smem = smem + static_cast<size_t>(max_slice) * 12 + 16 <= budget ? 1 : 0;
+  if (slice_in_smem) smem += static_cast<size_t>(max_slice) * 12 + 16;
+  CUDA_OK(cudaFuncSetAttribute(power_iter_coop_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_k, kBlock, 0));
-  const i64 want = (n * 32 + kBlock - 1) / kBlock;
-  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(want, (i64)per_sm * c->num_sms)));
-  DevBuf<double> part(c, 2 * nb);
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 256, smem));
+  if (per_sm < 1) invalid("power iteration: kernel does not fit on an SM");
+  DevBuf<double> part(c, 2 * nb), wb(c, 2 * n);
   const i64* rp = A->rp;
   const int* ci = A->ci;
   const double* val = A->v;
-  double* vp = v.p;
-  double* wp = w.p;
+  const double* vp = v.p;
+  double* wp = wb.p;
   double* pp = part.p;
   PowerState* sp = st.p;
-  void* args[] = {(void*)&n, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp,
-                  (void*)&pp, (void*)&tol, (void*)&max_iter, (void*)&sp};
+  void* args[] = {(void*)&n, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp, (void*)&pp,
+                  (void*)&tol, (void*)&max_iter, (void*)&slice_in_smem, (void*)&v_in_smem, (void*)&sp};
   {
     KScope ks_(c, "power_iter");
-    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_k, dim3(nb), dim3(kBlock), args, 0, c->stream));
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(256), args, smem, c->stream));
     launched(c);
   }
   return read_back(c, st.p).est;

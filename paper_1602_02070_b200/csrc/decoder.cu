@@ -115,6 +115,69 @@ __global__ void cg_apply_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Pla
   }
 }
 
+// Staged variant of cg_apply_k: a CTA owns rows [i0, i0 + 256) and a
+// contiguous chunk of columns [cb, ce).  The CSR rows of L_r for its rows and
+// of L_c for its columns are copied into shared memory once, so the inner
+// loops only issue the P gathers (coalesced along i for the X L_c part).  The
+// per-entry operation order is unchanged (bit-identical to cg_apply_k).
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
+                                                         Plan pl, i64 cols_per_cta, const T* __restrict__ P,
+                                                         T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
+  const i64 i1 = min(p, i0 + static_cast<i64>(blockDim.x));
+  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
+  const i64 ce = min(n, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0], er = Lr.rp[i1] - kr_base;
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
+  T* vr = reinterpret_cast<T*>(smraw);
+  T* vc = vr + er;
+  int* cir = reinterpret_cast<int*>(vc + ec);
+  int* cic = cir + er;
+  for (i64 k = threadIdx.x; k < er; k += blockDim.x) {
+    vr[k] = Lr.v[kr_base + k];
+    cir[k] = Lr.ci[kr_base + k];
+  }
+  for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
+    vc[k] = Lc.v[kc_base + k];
+    cic[k] = Lc.ci[kc_base + k];
+  }
+  __syncthreads();
+  double s[1] = {0.0};
+  const i64 i = i0 + threadIdx.x;
+  if (i < p) {
+    const i64 a0 = Lr.rp[i] - kr_base, a1 = Lr.rp[i + 1] - kr_base;
+    const bool row_sampled = pl.rsel[i] >= 0;
+    for (i64 c = cb; c < ce; ++c) {
+      const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
+      T x1 = T(0);
+      for (i64 k = b0; k < b1; ++k) x1 = add_rn(x1, mul_rn(vc[k], P[i + static_cast<i64>(cic[k]) * p]));
+      const T* pc = P + c * p;
+      T x2 = T(0);
+      for (i64 k = a0; k < a1; ++k) x2 = add_rn(x2, mul_rn(vr[k], pc[cir[k]]));
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = pc[i];
+      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + c * p] = out;
+      s[0] += static_cast<double>(pv) * static_cast<double>(out);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 template <typename T>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
@@ -251,6 +314,30 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned nb1 = stride_blocks(c, N);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
+  // Staged apply: per-CTA operator slices in shared memory when they fit.
+  std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
+  CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  const i64 cols_per_cta = (n + g2.y - 1) / g2.y;
+  const dim3 gs(gx, static_cast<unsigned>((n + cols_per_cta - 1) / cols_per_cta));
+  i64 max_er = 0, max_ec = 0;
+  for (unsigned b = 0; b < gx; ++b) {
+    const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);
+    max_er = std::max(max_er, rpr[e] - rpr[a]);
+  }
+  for (unsigned b = 0; b < gs.y; ++b) {
+    const i64 a = static_cast<i64>(b) * cols_per_cta, e = std::min<i64>(n, a + cols_per_cta);
+    max_ec = std::max(max_ec, rpc[e] - rpc[a]);
+  }
+  const size_t staged_smem = static_cast<size_t>(max_er + max_ec) * (sizeof(T) + sizeof(int)) + 16;
+  const bool staged = staged_smem <= 96 * 1024;
+  if (staged) {
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(staged_smem)));
+    if (part.n < static_cast<size_t>(gs.x) * gs.y) part.alloc(c, static_cast<size_t>(gs.x) * gs.y);
+  }
+
   cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
   launched(c);
   CgState host = read_back(c, st.p);
@@ -259,7 +346,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     for (i64 k = 0; k < chunk; ++k) {
       {
         KScope ks_(c, "cg_apply");
-        cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
+        if (staged)
+          cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
+                                                                      AP.p, part.p, st.p);
+        else
+          cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         launched(c);
       }
       {

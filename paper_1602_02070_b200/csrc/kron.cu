@@ -344,6 +344,200 @@ __global__ void pcg_true_k(i64 n, i64 nb, const i64* __restrict__ rp, const int*
   }
 }
 
+// ------------------------------------------------------------------ persistent batched PCG
+// Each CTA owns kCpb complete RHS columns, stored as a row-interleaved slab
+// (element (i, c) at ((c / kCpb) * n + i) * kCpb + c % kCpb), so one
+// 32-byte load fetches a row of all its columns and every per-column dot
+// product is a block reduction.  The CTA runs its columns' PCG iterations to
+// completion in one launch (columns are independent; no grid-wide sync), in
+// the reference recurrence with z = inv o r recomputed instead of stored.
+constexpr int kCpb = 4;
+
+__device__ __forceinline__ i64 slab_at(i64 n, i64 i, i64 c) { return ((c / kCpb) * n + i) * kCpb + (c % kCpb); }
+
+__global__ void __launch_bounds__(256) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
+                                                        const int* __restrict__ ci, const double* __restrict__ v,
+                                                        const double* __restrict__ inv, const double* __restrict__ B,
+                                                        double* __restrict__ X, double* __restrict__ R,
+                                                        double* __restrict__ P, double* __restrict__ AP, double tol,
+                                                        i64 max_iter, ColState* st) {
+  const i64 c0 = static_cast<i64>(blockIdx.x) * kCpb;
+  const i64 base = static_cast<i64>(blockIdx.x) * n * kCpb;
+  __shared__ int done_s[kCpb];
+  __shared__ double rho_s[kCpb], target_s[kCpb];
+  __shared__ i64 it_s[kCpb];
+  // r = b - A x, z = inv o r, p = z
+  double s3[3 * kCpb];
+#pragma unroll
+  for (int q = 0; q < 3 * kCpb; ++q) s3[q] = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+    double ax[kCpb];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) ax[q] = 0.0;
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+      const double a = v[k];
+      const double* xr = X + base + static_cast<i64>(ci[k]) * kCpb;
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) ax[q] = __dadd_rn(ax[q], __dmul_rn(a, xr[q]));
+    }
+    const double iv = inv[i];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) {
+      const i64 at = base + i * kCpb + q;
+      const double b = B[at];
+      const double r = __dsub_rn(b, ax[q]);
+      const double z = __dmul_rn(iv, r);
+      R[at] = r;
+      P[at] = z;
+      s3[q] += b * b;
+      s3[kCpb + q] += r * z;
+      s3[2 * kCpb + q] += r * r;
+    }
+  }
+  block_sum<3 * kCpb>(s3);
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < kCpb; ++q) {
+      const i64 c = c0 + q;
+      it_s[q] = 0;
+      if (c >= nb) {
+        done_s[q] = 3;
+        continue;
+      }
+      ColState& S = st[c];
+      S.norm_b = sqrt(s3[q]);
+      S.target = tol * S.norm_b;
+      rho_s[q] = s3[kCpb + q];
+      target_s[q] = S.target;
+      S.it = 0;
+      if (S.norm_b == 0.0)
+        done_s[q] = 2;
+      else if (sqrt(s3[2 * kCpb + q]) <= S.target || max_iter <= 0)
+        done_s[q] = 1;
+      else
+        done_s[q] = 0;
+      S.done = done_s[q];
+    }
+  }
+  __syncthreads();
+  while (true) {
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) any |= done_s[q] == 0;
+    if (!any) break;
+    // ap = A p, curvature
+    double cv[kCpb];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) cv[q] = 0.0;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+      double ap[kCpb];
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) ap[q] = 0.0;
+      for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+        const double a = v[k];
+        const double* pr = P + base + static_cast<i64>(ci[k]) * kCpb;
+#pragma unroll
+        for (int q = 0; q < kCpb; ++q) ap[q] = __dadd_rn(ap[q], __dmul_rn(a, pr[q]));
+      }
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) {
+        const i64 at = base + i * kCpb + q;
+        AP[at] = ap[q];
+        cv[q] += P[at] * ap[q];
+      }
+    }
+    block_sum<kCpb>(cv);
+    // alpha, breakdown
+    double alpha[kCpb];
+    bool live[kCpb];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) {
+      live[q] = done_s[q] == 0;
+      const bool bad = !isfinite(cv[q]) || cv[q] <= 0.0;
+      alpha[q] = rho_s[q] / cv[q];
+      if (live[q] && bad) live[q] = false;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kCpb; ++q)
+        if (done_s[q] == 0 && (!isfinite(cv[q]) || cv[q] <= 0.0)) {
+          st[c0 + q].err = 1;
+          st[c0 + q].curv = cv[q];
+          done_s[q] = 1;
+        }
+    // x += alpha p, r -= alpha ap, <r, z>, <r, r>
+    double s2[2 * kCpb];
+#pragma unroll
+    for (int q = 0; q < 2 * kCpb; ++q) s2[q] = 0.0;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+      const double iv = inv[i];
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) {
+        if (!live[q]) continue;
+        const i64 at = base + i * kCpb + q;
+        X[at] = __dadd_rn(X[at], __dmul_rn(alpha[q], P[at]));
+        const double r = __dsub_rn(R[at], __dmul_rn(alpha[q], AP[at]));
+        R[at] = r;
+        const double z = __dmul_rn(iv, r);
+        s2[q] += r * z;
+        s2[kCpb + q] += r * r;
+      }
+    }
+    block_sum<2 * kCpb>(s2);
+    // p = z + beta p
+    double beta[kCpb];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) beta[q] = s2[q] / rho_s[q];
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+      const double iv = inv[i];
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) {
+        if (!live[q]) continue;
+        const i64 at = base + i * kCpb + q;
+        P[at] = __dadd_rn(__dmul_rn(iv, R[at]), __dmul_rn(beta[q], P[at]));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kCpb; ++q) {
+        if (!live[q]) continue;
+        rho_s[q] = s2[q];
+        it_s[q] += 1;
+        if (sqrt(s2[kCpb + q]) <= target_s[q] || it_s[q] >= max_iter) done_s[q] = 1;
+      }
+    __syncthreads();
+  }
+  // true residual
+  double sr[kCpb];
+#pragma unroll
+  for (int q = 0; q < kCpb; ++q) sr[q] = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+    double ax[kCpb];
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) ax[q] = 0.0;
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+      const double a = v[k];
+      const double* xr = X + base + static_cast<i64>(ci[k]) * kCpb;
+#pragma unroll
+      for (int q = 0; q < kCpb; ++q) ax[q] = __dadd_rn(ax[q], __dmul_rn(a, xr[q]));
+    }
+#pragma unroll
+    for (int q = 0; q < kCpb; ++q) {
+      const double e = __dsub_rn(B[base + i * kCpb + q], ax[q]);
+      sr[q] += e * e;
+    }
+  }
+  block_sum<kCpb>(sr);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < kCpb; ++q) {
+      const i64 c = c0 + q;
+      if (c >= nb) continue;
+      ColState& S = st[c];
+      S.it = it_s[q];
+      S.done = done_s[q] == 2 ? 2 : 1;
+      S.rel_res = sqrt(sr[q]) / S.norm_b;
+    }
+}
+
 struct PcgBatchOut {
   std::vector<ColState> cols;
 };
@@ -396,7 +590,47 @@ void pcg_batched(Ctx* c, Csr* A, const double* inv, const double* B, double* X, 
   sync(c);
 }
 
+// Slab-layout batched PCG (B, X in slab layout with nb padded to kCpb).
+void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb, double tol,
+              i64 max_iter, PcgBatchOut* out) {
+  out->cols.assign(static_cast<size_t>(nb), ColState{});
+  if (nb == 0) return;
+  const i64 nbp = (nb + kCpb - 1) / kCpb * kCpb;
+  DevBuf<double> R(c, n * nbp), P(c, n * nbp), AP(c, n * nbp);
+  DevBuf<ColState> st(c, nb);
+  st.zero(c);
+  {
+    KScope ks_(c, "pcg_persistent");
+    pcg_persistent_k<<<static_cast<unsigned>(nbp / kCpb), 256, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
+                                                                              R.p, P.p, AP.p, tol, max_iter, st.p);
+    launched(c);
+  }
+  CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
 // ------------------------------------------------------------------ Schur assembly
+__global__ void rhs_fill_slab_k(i64 ni, i64 nb, const i64* __restrict__ rows, const i64* __restrict__ rp,
+                                const int* __restrict__ ci, const double* __restrict__ v, double* __restrict__ B) {
+  const i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (c >= nb) return;
+  const i64 j = rows[c];
+  for (i64 k = rp[j]; k < rp[j + 1]; ++k) B[slab_at(ni, ci[k], c)] = v[k];
+}
+
+__global__ void schur_update_slab_k(i64 m, i64 ni, i64 nb, const i64* __restrict__ cols, const i64* __restrict__ rp,
+                                    const int* __restrict__ ci, const double* __restrict__ v,
+                                    const double* __restrict__ Zs, double* __restrict__ S) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (i64 c = blockIdx.y; c < nb; c += gridDim.y) {
+    double y = 0.0;
+    for (i64 k = rp[i]; k < rp[i + 1]; ++k) y = __dadd_rn(y, __dmul_rn(v[k], Zs[slab_at(ni, ci[k], c)]));
+    const i64 at = i + cols[c] * m;
+    S[at] = __dsub_rn(S[at], y);
+  }
+}
+
 __global__ void rhs_fill_k(i64 ni, i64 nb, const i64* __restrict__ rows, const i64* __restrict__ rp,
                            const int* __restrict__ ci, const double* __restrict__ v, double* __restrict__ B) {
   const i64 c = blockIdx.x * (i64)blockDim.x + threadIdx.x;
@@ -593,13 +827,14 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     std::vector<i64> cols(active.begin() + s0, active.begin() + s0 + nb);
     DevBuf<i64> cols_d(c, nb);
     CUDA_OK(cudaMemcpyAsync(cols_d.p, cols.data(), sizeof(i64) * nb, cudaMemcpyHostToDevice, c->stream));
-    DevBuf<double> B(c, ni * nb), X(c, ni * nb);
+    const i64 nbp = (nb + kCpb - 1) / kCpb * kCpb;
+    DevBuf<double> B(c, ni * nbp), X(c, ni * nbp);
     B.zero(c);
     X.zero(c);
-    rhs_fill_k<<<blocks_for(nb), kBlock, 0, c->stream>>>(ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, B.p);
+    rhs_fill_slab_k<<<blocks_for(nb), kBlock, 0, c->stream>>>(ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, B.p);
     launched(c);
     PcgBatchOut res;
-    pcg_batched(c, Laa, inv.p, B.p, X.p, ni, nb, pcg_tol, max_iter, &res);
+    pcg_slab(c, Laa, inv.p, B.p, X.p, ni, nb, pcg_tol, max_iter, &res);
     for (i64 q = 0; q < nb; ++q) {
       const ColState& cs = res.cols[q];
       const i64 j = cols[q];
@@ -615,7 +850,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     }
     if (fail_j >= 0) break;
     dim3 g(blocks_for(m), static_cast<unsigned>(std::min<i64>(nb, 65535)));
-    schur_update_k<<<g, kBlock, 0, c->stream>>>(m, ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, X.p, S.p);
+    schur_update_slab_k<<<g, kBlock, 0, c->stream>>>(m, ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, X.p, S.p);
     launched(c);
   }
   if (fail_j >= 0) runtime(fail_msg);
