@@ -115,48 +115,74 @@ __global__ void cg_apply_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Pla
   }
 }
 
-// Staged variant of cg_apply_k: a CTA owns rows [i0, i0 + 256) and a
-// contiguous chunk of columns [cb, ce).  The CSR rows of L_r for its rows and
-// of L_c for its columns are copied into shared memory once, so the inner
-// loops only issue the P gathers (coalesced along i for the X L_c part).  The
-// per-entry operation order is unchanged (bit-identical to cg_apply_k).
+// Register-resident variant of cg_apply_k.  A CTA owns rows [i0, i0 + 256)
+// and a contiguous chunk of columns [cb, ce):
+//  - each thread keeps the CSR row of L_r for its row i in registers
+//    (kRmax entries, predicated, CSR order) for the whole column chunk, so
+//    the L_r part issues only its P gathers;
+//  - the CSR rows of L_c for the chunk are staged once in shared memory as
+//    packed (value, column) pairs: one broadcast load per entry.
+// The per-entry operation order is unchanged (bit-identical to cg_apply_k).
+constexpr int kRmax = 16;
+
 template <typename T>
-__global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
-                                                         Plan pl, i64 cols_per_cta, const T* __restrict__ P,
-                                                         T* __restrict__ AP, double* partials, CgState* st) {
+struct alignas(sizeof(T) == 8 ? 16 : 8) LcEnt {
+  T v;
+  int ci;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_reg_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                      i64 cols_per_cta, const T* __restrict__ P,
+                                                      T* __restrict__ AP, double* partials, CgState* st) {
   if (st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
+  LcEnt<T>* ent = reinterpret_cast<LcEnt<T>*>(smraw);
   const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
-  const i64 i1 = min(p, i0 + static_cast<i64>(blockDim.x));
   const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
   const i64 ce = min(n, cb + cols_per_cta);
-  const i64 kr_base = Lr.rp[i0], er = Lr.rp[i1] - kr_base;
   const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
-  T* vr = reinterpret_cast<T*>(smraw);
-  T* vc = vr + er;
-  int* cir = reinterpret_cast<int*>(vc + ec);
-  int* cic = cir + er;
-  for (i64 k = threadIdx.x; k < er; k += blockDim.x) {
-    vr[k] = Lr.v[kr_base + k];
-    cir[k] = Lr.ci[kr_base + k];
-  }
   for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
-    vc[k] = Lc.v[kc_base + k];
-    cic[k] = Lc.ci[kc_base + k];
+    LcEnt<T> e;
+    e.v = Lc.v[kc_base + k];
+    e.ci = Lc.ci[kc_base + k];
+    ent[k] = e;
+  }
+  const i64 i = i0 + threadIdx.x;
+  T rv[kRmax];
+  int rc[kRmax];
+  int rlen = 0;
+  i64 ra = 0;
+  bool row_sampled = false;
+  if (i < p) {
+    ra = Lr.rp[i];
+    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
+#pragma unroll
+    for (int k = 0; k < kRmax; ++k) {
+      rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
+      rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
+    }
+    row_sampled = pl.rsel[i] >= 0;
   }
   __syncthreads();
   double s[1] = {0.0};
-  const i64 i = i0 + threadIdx.x;
   if (i < p) {
-    const i64 a0 = Lr.rp[i] - kr_base, a1 = Lr.rp[i + 1] - kr_base;
-    const bool row_sampled = pl.rsel[i] >= 0;
     for (i64 c = cb; c < ce; ++c) {
       const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
       T x1 = T(0);
-      for (i64 k = b0; k < b1; ++k) x1 = add_rn(x1, mul_rn(vc[k], P[i + static_cast<i64>(cic[k]) * p]));
+      for (i64 k = b0; k < b1; ++k) {
+        const LcEnt<T> e = ent[k];
+        x1 = add_rn(x1, mul_rn(e.v, P[i + static_cast<i64>(e.ci) * p]));
+      }
       const T* pc = P + c * p;
       T x2 = T(0);
-      for (i64 k = a0; k < a1; ++k) x2 = add_rn(x2, mul_rn(vr[k], pc[cir[k]]));
+      if (rlen <= kRmax) {
+#pragma unroll
+        for (int k = 0; k < kRmax; ++k)
+          if (k < rlen) x2 = add_rn(x2, mul_rn(rv[k], pc[rc[k]]));
+      } else {
+        for (i64 k = ra; k < ra + rlen; ++k) x2 = add_rn(x2, mul_rn(Lr.v[k], pc[Lr.ci[k]]));
+      }
       T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
       const T pv = pc[i];
       if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
@@ -330,10 +356,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     const i64 a = static_cast<i64>(b) * cols_per_cta, e = std::min<i64>(n, a + cols_per_cta);
     max_ec = std::max(max_ec, rpc[e] - rpc[a]);
   }
-  const size_t staged_smem = static_cast<size_t>(max_er + max_ec) * (sizeof(T) + sizeof(int)) + 16;
+  (void)max_er;
+  const size_t staged_smem = static_cast<size_t>(max_ec) * sizeof(LcEnt<T>) + 16;
   const bool staged = staged_smem <= 96 * 1024;
   if (staged) {
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_reg_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(staged_smem)));
     if (part.n < static_cast<size_t>(gs.x) * gs.y) part.alloc(c, static_cast<size_t>(gs.x) * gs.y);
   }
@@ -347,8 +374,8 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       {
         KScope ks_(c, "cg_apply");
         if (staged)
-          cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
-                                                                      AP.p, part.p, st.p);
+          cg_apply_reg_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
+                                                                   AP.p, part.p, st.p);
         else
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         launched(c);

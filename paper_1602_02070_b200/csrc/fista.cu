@@ -273,6 +273,248 @@ __global__ void __launch_bounds__(256) fista_dense_objective_k(i64 rr, i64 rc, c
   }
 }
 
+// ---- fp32 split-K: the concatenated k-space [0, rr) u [rr, rr + rc) of the
+// two products is cut into S ranges; CTA (tile, s) writes its partial tile,
+// and the last CTA of the tile (per-tile arrival counter) sums the S partials
+// in s order (deterministic) and runs the epilogue.
+struct SplitWs {
+  float* part1;        // S x m partial (Lr Z)
+  float* part2;        // S x m partial (Z Lc)
+  unsigned* tile_cnt;  // tiles
+  unsigned* done_cnt;  // 1
+  double* tile_sums;   // 3 x tiles (objective)
+};
+
+__device__ __forceinline__ void splitk_partial(const float* __restrict__ Lr, const float* __restrict__ Lc,
+                                               const float* __restrict__ Z, i64 rr, i64 rc, int use_r,
+                                               int use_c, i64 i0, i64 c0, i64 ka, i64 kb, float (&acc1)[2][2],
+                                               float (&acc2)[2][2]) {
+  __shared__ float As[kDK][kDT + 1];
+  __shared__ float Bs[kDK][kDT + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc1[a][b] = acc2[a][b] = 0.f;
+  // part 1: k in [ka, min(kb, rr))
+  if (use_r)
+    for (i64 k0 = ka; k0 < min(kb, rr); k0 += kDK) {
+      const i64 kend = min(min(kb, rr), k0 + kDK);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
+        const i64 gi = i0 + ii, gk = k0 + kk;
+        As[kk][ii] = (gi < rr && gk < kend) ? Lr[gk * rr + gi] : 0.f;
+        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
+        const i64 gk2 = k0 + kk2, gc = c0 + cc;
+        Bs[kk2][cc] = (gk2 < kend && gc < rc) ? Z[gc * rr + gk2] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < kDK; ++kk) {
+        const float a0 = As[kk][ty], a1 = As[kk][ty + 16];
+        const float b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+        acc1[0][0] = fmaf(a0, b0, acc1[0][0]);
+        acc1[0][1] = fmaf(a0, b1, acc1[0][1]);
+        acc1[1][0] = fmaf(a1, b0, acc1[1][0]);
+        acc1[1][1] = fmaf(a1, b1, acc1[1][1]);
+      }
+      __syncthreads();
+    }
+  // part 2: k - rr in [max(ka, rr) - rr, kb - rr)
+  if (use_c)
+    for (i64 k0 = max(ka, rr) - rr; k0 < kb - rr; k0 += kDK) {
+      const i64 kend = kb - rr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
+        const i64 gi = i0 + ii, gk = k0 + kk;
+        As[kk][ii] = (gi < rr && gk < kend) ? Z[gk * rr + gi] : 0.f;
+        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
+        const i64 gk2 = k0 + kk2, gc = c0 + cc;
+        Bs[kk2][cc] = (gk2 < kend && gc < rc) ? Lc[gc * rc + gk2] : 0.f;
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int kk = 0; kk < kDK; ++kk) {
+        const float a0 = As[kk][ty], a1 = As[kk][ty + 16];
+        const float b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+        acc2[0][0] = fmaf(a0, b0, acc2[0][0]);
+        acc2[0][1] = fmaf(a0, b1, acc2[0][1]);
+        acc2[1][0] = fmaf(a1, b0, acc2[1][0]);
+        acc2[1][1] = fmaf(a1, b1, acc2[1][1]);
+      }
+      __syncthreads();
+    }
+}
+
+// Writes the partial, returns true in the CTA that must finish the tile
+// (with acc1/acc2 holding the full sums).
+__device__ __forceinline__ bool splitk_finish(const SplitWs& ws, i64 rr, i64 rc, i64 i0, i64 c0, int S,
+                                              float (&acc1)[2][2], float (&acc2)[2][2]) {
+  const i64 m = rr * rc;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4, s = blockIdx.z;
+  const unsigned tile = blockIdx.x + gridDim.x * blockIdx.y;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      if (i < rr && c < rc) {
+        ws.part1[static_cast<i64>(s) * m + i + c * rr] = acc1[a][b];
+        ws.part2[static_cast<i64>(s) * m + i + c * rr] = acc2[a][b];
+      }
+    }
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ws.tile_cnt + tile, 1u) == static_cast<unsigned>(S - 1);
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      float x1 = 0.f, x2 = 0.f;
+      if (i < rr && c < rc)
+        for (int q = 0; q < S; ++q) {
+          x1 += __ldcg(ws.part1 + static_cast<i64>(q) * m + i + c * rr);
+          x2 += __ldcg(ws.part2 + static_cast<i64>(q) * m + i + c * rr);
+        }
+      acc1[a][b] = x1;
+      acc2[a][b] = x2;
+    }
+  if (threadIdx.x == 0) ws.tile_cnt[tile] = 0u;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) fista_splitk_grad_prox_k(i64 rr, i64 rc, const float* __restrict__ Lr,
+                                                                const float* __restrict__ Lc, float s_r, float s_c,
+                                                                int use_r, int use_c, int loss, float step,
+                                                                const float* __restrict__ Z,
+                                                                const float* __restrict__ Y, float* __restrict__ S,
+                                                                SplitWs ws, const FistaState* st) {
+  if (st->done) return;
+  const int Sn = gridDim.z;
+  const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = static_cast<i64>(blockIdx.y) * kDT;
+  float acc1[2][2], acc2[2][2];
+  splitk_partial(Lr, Lc, Z, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
+  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      if (i >= rr || c >= rc) continue;
+      const i64 at = i + c * rr;
+      float g = 0.f;
+      if (use_c) g = __fadd_rn(g, __fmul_rn(s_c, acc2[a][b]));
+      if (use_r) g = __fadd_rn(g, __fmul_rn(s_r, acc1[a][b]));
+      const float arg = __fsub_rn(Z[at], __fmul_rn(step, g));
+      S[at] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[at], step) : prox_l1_elem(arg, Y[at], step);
+    }
+}
+
+__global__ void __launch_bounds__(256) fista_splitk_objective_k(i64 rr, i64 rc, const float* __restrict__ Lr,
+                                                                const float* __restrict__ Lc, double gamma_r,
+                                                                double gamma_c, int loss, const float* __restrict__ S,
+                                                                const float* __restrict__ Y, SplitWs ws,
+                                                                double* trace, FistaState* st) {
+  if (st->done) return;
+  const int use_r = gamma_r != 0.0, use_c = gamma_c != 0.0;
+  const int Sn = gridDim.z;
+  const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = static_cast<i64>(blockIdx.y) * kDT;
+  float acc1[2][2], acc2[2][2];
+  splitk_partial(Lr, Lc, S, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
+  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double sm3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      if (i >= rr || c >= rc) continue;
+      const i64 at = i + c * rr;
+      const double x = static_cast<double>(S[at]);
+      const double e = static_cast<double>(Y[at]) - x;
+      sm3[0] += loss == CPCAG_LOSS_L2 ? e * e : fabs(e);
+      sm3[1] += static_cast<double>(acc2[a][b]) * x;
+      sm3[2] += static_cast<double>(acc1[a][b]) * x;
+    }
+  block_sum<3>(sm3);
+  const unsigned tiles = gridDim.x * gridDim.y, tile = blockIdx.x + gridDim.x * blockIdx.y;
+  __shared__ bool last_tile;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 3; ++q) ws.tile_sums[q * tiles + tile] = sm3[q];
+    __threadfence();
+    last_tile = atomicAdd(ws.done_cnt, 1u) == tiles - 1;
+  }
+  __syncthreads();
+  if (!last_tile) return;
+  __threadfence();
+  double tot[3];
+  for (int q = 0; q < 3; ++q) {
+    double x = 0.0;
+    for (unsigned t = threadIdx.x; t < tiles; t += blockDim.x) x += __ldcg(ws.tile_sums + q * tiles + t);
+    tot[q] = x;
+  }
+  block_sum<3>(tot);
+  if (threadIdx.x == 0) {
+    *ws.done_cnt = 0u;
+    double val = tot[0];
+    if (use_c) val += gamma_c * tot[1];
+    if (use_r) val += gamma_r * tot[2];
+    const i64 j = st->j;
+    if (!isfinite(val)) {
+      st->err = 1;
+      st->err_j = j;
+      st->done = 1;
+      return;
+    }
+    trace[j - 1] = val;
+    st->iterations = j;
+    const double t = st->t;
+    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    st->t_next = tn;
+    st->coef = (t - 1.0) / tn;
+  }
+}
+
+template <typename T>
+struct SplitLauncher {
+  static bool run_grad(Ctx*, dim3, i64, i64, const T*, const T*, T, T, int, int, int, T, const T*, const T*, T*,
+                       const SplitWs&, FistaState*) {
+    return false;
+  }
+  static bool run_obj(Ctx*, dim3, i64, i64, const T*, const T*, double, double, int, const T*, const T*,
+                      const SplitWs&, double*, FistaState*) {
+    return false;
+  }
+};
+template <>
+struct SplitLauncher<float> {
+  static bool run_grad(Ctx* c, dim3 g, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r, float s_c,
+                       int use_r, int use_c, int loss, float step, const float* Z, const float* Y, float* S,
+                       const SplitWs& ws, FistaState* st) {
+    fista_splitk_grad_prox_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, s_r, s_c, use_r, use_c, loss, step, Z, Y, S,
+                                                        ws, st);
+    launched(c);
+    return true;
+  }
+  static bool run_obj(Ctx* c, dim3 g, i64 rr, i64 rc, const float* Lr, const float* Lc, double gr, double gc,
+                      int loss, const float* S, const float* Y, const SplitWs& ws, double* trace, FistaState* st) {
+    fista_splitk_objective_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, gr, gc, loss, S, Y, ws, trace, st);
+    launched(c);
+    return true;
+  }
+};
+
 template <typename T>
 __global__ void densify_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
                           const double* __restrict__ v, T* __restrict__ D) {
@@ -348,8 +590,26 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     densify<T>(c, Lr, Dr);
     densify<T>(c, Lc, Dc);
   }
-  const dim3 gd(static_cast<unsigned>((rows + kDT - 1) / kDT), static_cast<unsigned>((cols + kDT - 1) / kDT));
+  dim3 gd(static_cast<unsigned>((rows + kDT - 1) / kDT), static_cast<unsigned>((cols + kDT - 1) / kDT));
   if (dense) part.alloc(c, 3 * static_cast<size_t>(std::max<unsigned>(gd.x * gd.y, nb1)));
+  // fp32: split the k-space so the grid covers ~6 CTAs per SM.
+  const bool splitk = dense && sizeof(T) == 4;
+  DevBuf<float> sp1, sp2;
+  DevBuf<unsigned> scnt;
+  DevBuf<double> ssum;
+  SplitWs ws{};
+  if (splitk) {
+    const unsigned tiles = gd.x * gd.y;
+    unsigned S = static_cast<unsigned>(std::max<i64>(1, (6 * static_cast<i64>(c->num_sms)) / tiles));
+    S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / kDK + 1, 32}));
+    gd.z = S;
+    sp1.alloc(c, static_cast<size_t>(S) * N);
+    sp2.alloc(c, static_cast<size_t>(S) * N);
+    scnt.alloc(c, tiles + 1);
+    scnt.zero(c);
+    ssum.alloc(c, 3 * static_cast<size_t>(tiles));
+    ws = SplitWs{sp1.p, sp2.p, scnt.p, scnt.p + tiles, ssum.p};
+  }
 
   i64 j = 1;
   FistaState host{};
@@ -361,7 +621,18 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       T* Sj = Sb[j & 1].p;
       const T* Sprev = Sb[(j - 1) & 1].p;
       T* Znext = Zb[(j + 1) & 1].p;
-      if (dense) {
+      if (splitk) {
+        {
+          KScope ks_(c, "fista_grad_prox");
+          SplitLauncher<T>::run_grad(c, gd, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg.loss, stepT, Zj, Y, Sj,
+                                     ws, st.p);
+        }
+        {
+          KScope ks_(c, "fista_objective");
+          SplitLauncher<T>::run_obj(c, gd, rows, cols, Dr.p, Dc.p, cfg.gamma_r, cfg.gamma_c, cfg.loss, Sj, Y, ws, tr.p,
+                                    st.p);
+        }
+      } else if (dense) {
         {
           KScope ks_(c, "fista_grad_prox");
           fista_dense_grad_prox_k<T><<<gd, 256, 0, c->stream>>>(rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c,
