@@ -115,78 +115,95 @@ __global__ void cg_apply_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Pla
   }
 }
 
-// Register-resident variant of cg_apply_k.  A CTA owns rows [i0, i0 + 256)
-// and a contiguous chunk of columns [cb, ce):
-//  - each thread keeps the CSR row of L_r for its row i in registers
-//    (kRmax entries, predicated, CSR order) for the whole column chunk, so
-//    the L_r part issues only its P gathers;
-//  - the CSR rows of L_c for the chunk are staged once in shared memory as
-//    packed (value, column) pairs: one broadcast load per entry.
-// The per-entry operation order is unchanged (bit-identical to cg_apply_k).
-constexpr int kRmax = 16;
-
 template <typename T>
 struct alignas(sizeof(T) == 8 ? 16 : 8) LcEnt {
   T v;
   int ci;
 };
 
+// Two-kernel apply (HBM-friendly; used when the panels fit in shared memory):
+//  cg_apply_lr_k  Yr = L_r P      CTA = kLrCols columns x all p rows; the
+//                                 columns are staged in shared memory, so the
+//                                 L_r gathers are shared-memory loads and each
+//                                 CSR entry is read once for kLrCols columns.
+//  cg_apply_lc_k  AP = gc (P L_c) + gr Yr (+ P on the sampled grid), <P, AP>
+//                 CTA = a 32-row panel x all n columns staged in shared memory
+//                 (row-major, padded), lane = row, warp = column; the L_c
+//                 row of each column is read with one coalesced load per 32
+//                 entries and broadcast from shared memory.
+// Per-entry operation order is the reference's (bit-identical to cg_apply_k).
+constexpr int kLrCols = 4;
+constexpr int kPanel = 32;
+
 template <typename T>
-__global__ void __launch_bounds__(256) cg_apply_reg_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
-                                                      i64 cols_per_cta, const T* __restrict__ P,
-                                                      T* __restrict__ AP, double* partials, CgState* st) {
+__global__ void __launch_bounds__(512) cg_apply_lr_k(i64 p, i64 n, Pull<T> Lr, const T* __restrict__ P,
+                                                     T* __restrict__ Yr, const CgState* st) {
   if (st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
-  LcEnt<T>* ent = reinterpret_cast<LcEnt<T>*>(smraw);
-  const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
-  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
-  const i64 ce = min(n, cb + cols_per_cta);
-  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
-  for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
-    LcEnt<T> e;
-    e.v = Lc.v[kc_base + k];
-    e.ci = Lc.ci[kc_base + k];
-    ent[k] = e;
-  }
-  const i64 i = i0 + threadIdx.x;
-  T rv[kRmax];
-  int rc[kRmax];
-  int rlen = 0;
-  i64 ra = 0;
-  bool row_sampled = false;
-  if (i < p) {
-    ra = Lr.rp[i];
-    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
-#pragma unroll
-    for (int k = 0; k < kRmax; ++k) {
-      rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
-      rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
-    }
-    row_sampled = pl.rsel[i] >= 0;
-  }
+  T* Ps = reinterpret_cast<T*>(smraw);  // kLrCols x p
+  const i64 c0 = static_cast<i64>(blockIdx.x) * kLrCols;
+  const int nc = static_cast<int>(min(static_cast<i64>(kLrCols), n - c0));
+  for (int q = 0; q < nc; ++q)
+    for (i64 i = threadIdx.x; i < p; i += blockDim.x) Ps[q * p + i] = P[i + (c0 + q) * p];
   __syncthreads();
-  double s[1] = {0.0};
-  if (i < p) {
-    for (i64 c = cb; c < ce; ++c) {
-      const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
-      T x1 = T(0);
-      for (i64 k = b0; k < b1; ++k) {
-        const LcEnt<T> e = ent[k];
-        x1 = add_rn(x1, mul_rn(e.v, P[i + static_cast<i64>(e.ci) * p]));
-      }
-      const T* pc = P + c * p;
-      T x2 = T(0);
-      if (rlen <= kRmax) {
+  for (i64 i = threadIdx.x; i < p; i += blockDim.x) {
+    T acc[kLrCols];
 #pragma unroll
-        for (int k = 0; k < kRmax; ++k)
-          if (k < rlen) x2 = add_rn(x2, mul_rn(rv[k], pc[rc[k]]));
-      } else {
-        for (i64 k = ra; k < ra + rlen; ++k) x2 = add_rn(x2, mul_rn(Lr.v[k], pc[Lr.ci[k]]));
+    for (int q = 0; q < kLrCols; ++q) acc[q] = T(0);
+    for (i64 k = Lr.rp[i]; k < Lr.rp[i + 1]; ++k) {
+      const T v = Lr.v[k];
+      const int j = Lr.ci[k];
+#pragma unroll
+      for (int q = 0; q < kLrCols; ++q)
+        if (q < nc) acc[q] = add_rn(acc[q], mul_rn(v, Ps[q * p + j]));
+    }
+#pragma unroll
+    for (int q = 0; q < kLrCols; ++q)
+      if (q < nc) Yr[i + (c0 + q) * p] = acc[q];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_lc_k(i64 p, i64 n, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                     const T* __restrict__ P, const T* __restrict__ Yr,
+                                                     T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  LcEnt<T>* ents = reinterpret_cast<LcEnt<T>*>(smraw);     // nw x 32 staging of L_c rows
+  T* Ps = reinterpret_cast<T*>(ents + nw * 32);             // n x (kPanel + 1)
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kPanel;
+  const i64 i = i0 + lane;
+  const bool in = i < p;
+  for (i64 c = wid; c < n; c += nw) Ps[c * (kPanel + 1) + lane] = in ? P[i + c * p] : T(0);
+  __syncthreads();
+  const bool row_sampled = in && pl.rsel[i] >= 0;
+  double s[1] = {0.0};
+  LcEnt<T>* mine = ents + wid * 32;
+  for (i64 c = wid; c < n; c += nw) {
+    const i64 k0 = Lc.rp[c], k1 = Lc.rp[c + 1];
+    T x1 = T(0);
+    for (i64 kb = k0; kb < k1; kb += 32) {
+      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - kb));
+      if (lane < cnt) {
+        LcEnt<T> e;
+        e.v = Lc.v[kb + lane];
+        e.ci = Lc.ci[kb + lane];
+        mine[lane] = e;
       }
-      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
-      const T pv = pc[i];
+      __syncwarp();
+      for (int k = 0; k < cnt; ++k) {
+        const LcEnt<T> e = mine[k];
+        x1 = add_rn(x1, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanel + 1) + lane]));
+      }
+      __syncwarp();
+    }
+    if (in) {
+      const i64 at = i + c * p;
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, Yr[at]));
+      const T pv = Ps[c * (kPanel + 1) + lane];
       if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
-      AP[i + c * p] = out;
+      AP[at] = out;
       s[0] += static_cast<double>(pv) * static_cast<double>(out);
     }
   }
@@ -340,29 +357,18 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned nb1 = stride_blocks(c, N);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
-  // Staged apply: per-CTA operator slices in shared memory when they fit.
-  std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
-  CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  const i64 cols_per_cta = (n + g2.y - 1) / g2.y;
-  const dim3 gs(gx, static_cast<unsigned>((n + cols_per_cta - 1) / cols_per_cta));
-  i64 max_er = 0, max_ec = 0;
-  for (unsigned b = 0; b < gx; ++b) {
-    const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);
-    max_er = std::max(max_er, rpr[e] - rpr[a]);
-  }
-  for (unsigned b = 0; b < gs.y; ++b) {
-    const i64 a = static_cast<i64>(b) * cols_per_cta, e = std::min<i64>(n, a + cols_per_cta);
-    max_ec = std::max(max_ec, rpc[e] - rpc[a]);
-  }
-  (void)max_er;
-  const size_t staged_smem = static_cast<size_t>(max_ec) * sizeof(LcEnt<T>) + 16;
-  const bool staged = staged_smem <= 96 * 1024;
-  if (staged) {
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_reg_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(staged_smem)));
-    if (part.n < static_cast<size_t>(gs.x) * gs.y) part.alloc(c, static_cast<size_t>(gs.x) * gs.y);
+  // Split apply when the staged panels fit in shared memory.
+  const size_t lr_smem = static_cast<size_t>(kLrCols) * p * sizeof(T);
+  const size_t lc_smem = 8 * 32 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanel + 1) * sizeof(T);
+  const bool split = lr_smem <= 200 * 1024 && lc_smem <= 200 * 1024;
+  DevBuf<T> Yr;
+  const unsigned lr_blocks = static_cast<unsigned>((n + kLrCols - 1) / kLrCols);
+  const unsigned lc_blocks = static_cast<unsigned>((p + kPanel - 1) / kPanel);
+  if (split) {
+    Yr.alloc(c, N);
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_lr_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lr_smem)));
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_lc_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lc_smem)));
+    if (part.n < lc_blocks) part.alloc(c, lc_blocks);
   }
 
   cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
@@ -373,11 +379,14 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     for (i64 k = 0; k < chunk; ++k) {
       {
         KScope ks_(c, "cg_apply");
-        if (staged)
-          cg_apply_reg_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
-                                                                   AP.p, part.p, st.p);
-        else
+        if (split) {
+          cg_apply_lr_k<T><<<lr_blocks, 512, lr_smem, c->stream>>>(p, n, pr, P.p, Yr.p, st.p);
+          launched(c);
+          cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
+                                                                  st.p);
+        } else {
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
+        }
         launched(c);
       }
       {
