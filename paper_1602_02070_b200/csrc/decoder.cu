@@ -14,6 +14,9 @@
 // Every scalar lives on the device; the host polls the done flag once per
 // chunk of iterations.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "frpcag.cuh"
@@ -221,6 +224,144 @@ __global__ void __launch_bounds__(256) cg_apply_lc_k(i64 p, i64 n, Pull<T> Lc, T
   }
 }
 
+// Staged variant of cg_apply_k: a CTA owns rows [i0, i0 + 256) and a
+// contiguous chunk of columns [cb, ce).  The CSR rows of L_r for its rows and
+// of L_c for its columns are copied into shared memory once, so the inner
+// loops only issue the P gathers (coalesced along i for the X L_c part).  The
+// per-entry operation order is unchanged (bit-identical to cg_apply_k).
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
+                                                         Plan pl, i64 cols_per_cta, const T* __restrict__ P,
+                                                         T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
+  const i64 i1 = min(p, i0 + static_cast<i64>(blockDim.x));
+  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
+  const i64 ce = min(n, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0], er = Lr.rp[i1] - kr_base;
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
+  T* vr = reinterpret_cast<T*>(smraw);
+  T* vc = vr + er;
+  int* cir = reinterpret_cast<int*>(vc + ec);
+  int* cic = cir + er;
+  for (i64 k = threadIdx.x; k < er; k += blockDim.x) {
+    vr[k] = Lr.v[kr_base + k];
+    cir[k] = Lr.ci[kr_base + k];
+  }
+  for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
+    vc[k] = Lc.v[kc_base + k];
+    cic[k] = Lc.ci[kc_base + k];
+  }
+  __syncthreads();
+  double s[1] = {0.0};
+  const i64 i = i0 + threadIdx.x;
+  if (i < p) {
+    const i64 a0 = Lr.rp[i] - kr_base, a1 = Lr.rp[i + 1] - kr_base;
+    const bool row_sampled = pl.rsel[i] >= 0;
+    for (i64 c = cb; c < ce; ++c) {
+      const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
+      T x1 = T(0);
+      for (i64 k = b0; k < b1; ++k) x1 = add_rn(x1, mul_rn(vc[k], P[i + static_cast<i64>(cic[k]) * p]));
+      const T* pc = P + c * p;
+      T x2 = T(0);
+      for (i64 k = a0; k < a1; ++k) x2 = add_rn(x2, mul_rn(vr[k], pc[cir[k]]));
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = pc[i];
+      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + c * p] = out;
+      s[0] += static_cast<double>(pv) * static_cast<double>(out);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
+
+
+template <typename T, int kRmax>
+__global__ void __launch_bounds__(256, 2) cg_apply_reg_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                      i64 cols_per_cta, const T* __restrict__ P,
+                                                      T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  LcEnt<T>* ent = reinterpret_cast<LcEnt<T>*>(smraw);
+  const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
+  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
+  const i64 ce = min(n, cb + cols_per_cta);
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
+  for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
+    LcEnt<T> e;
+    e.v = Lc.v[kc_base + k];
+    e.ci = Lc.ci[kc_base + k];
+    ent[k] = e;
+  }
+  const i64 i = i0 + threadIdx.x;
+  T rv[kRmax];
+  int rc[kRmax];
+  int rlen = 0;
+  i64 ra = 0;
+  bool row_sampled = false;
+  if (i < p) {
+    ra = Lr.rp[i];
+    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
+#pragma unroll
+    for (int k = 0; k < kRmax; ++k) {
+      rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
+      rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
+    }
+    row_sampled = pl.rsel[i] >= 0;
+  }
+  __syncthreads();
+  double s[1] = {0.0};
+  if (i < p) {
+    for (i64 c = cb; c < ce; ++c) {
+      const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
+      T x1 = T(0);
+      for (i64 k = b0; k < b1; ++k) {
+        const LcEnt<T> e = ent[k];
+        x1 = add_rn(x1, mul_rn(e.v, P[i + static_cast<i64>(e.ci) * p]));
+      }
+      const T* pc = P + c * p;
+      T x2 = T(0);
+      if (rlen <= kRmax) {
+#pragma unroll
+        for (int k = 0; k < kRmax; ++k)
+          if (k < rlen) x2 = add_rn(x2, mul_rn(rv[k], pc[rc[k]]));
+      } else {
+        for (i64 k = ra; k < ra + rlen; ++k) x2 = add_rn(x2, mul_rn(Lr.v[k], pc[Lr.ci[k]]));
+      }
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = pc[i];
+      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + c * p] = out;
+      s[0] += static_cast<double>(pv) * static_cast<double>(out);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 template <typename T>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
@@ -357,10 +498,34 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned nb1 = stride_blocks(c, N);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
-  // Split apply when the staged panels fit in shared memory.
+  // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
+  // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
+  std::string variant = "staged";
+  if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
+  std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
+  CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  const i64 cols_per_cta = (n + g2.y - 1) / g2.y;
+  const dim3 gs(gx, static_cast<unsigned>((n + cols_per_cta - 1) / cols_per_cta));
+  i64 max_er = 0, max_ec = 0, max_row = 0;
+  for (unsigned b = 0; b < gx; ++b) {
+    const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);
+    max_er = std::max(max_er, rpr[e] - rpr[a]);
+  }
+  for (i64 r = 0; r < p; ++r) max_row = std::max(max_row, rpr[r + 1] - rpr[r]);
+  for (unsigned b = 0; b < gs.y; ++b) {
+    const i64 a = static_cast<i64>(b) * cols_per_cta, e = std::min<i64>(n, a + cols_per_cta);
+    max_ec = std::max(max_ec, rpc[e] - rpc[a]);
+  }
+  const size_t staged_smem = static_cast<size_t>(max_er + max_ec) * (sizeof(T) + sizeof(int)) + 16;
+  const size_t reg_smem = static_cast<size_t>(max_ec) * sizeof(LcEnt<T>) + 16;
   const size_t lr_smem = static_cast<size_t>(kLrCols) * p * sizeof(T);
   const size_t lc_smem = 8 * 32 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanel + 1) * sizeof(T);
-  const bool split = lr_smem <= 200 * 1024 && lc_smem <= 200 * 1024;
+  if (variant == "split" && !(lr_smem <= 200 * 1024 && lc_smem <= 200 * 1024)) variant = "staged";
+  if (variant == "reg" && !(max_row <= 32 && reg_smem <= 96 * 1024)) variant = "staged";
+  if (variant == "staged" && !(staged_smem <= 96 * 1024)) variant = "plain";
+  const bool split = variant == "split";
   DevBuf<T> Yr;
   const unsigned lr_blocks = static_cast<unsigned>((n + kLrCols - 1) / kLrCols);
   const unsigned lc_blocks = static_cast<unsigned>((p + kPanel - 1) / kPanel);
@@ -369,7 +534,17 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     CUDA_OK(cudaFuncSetAttribute(cg_apply_lr_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lr_smem)));
     CUDA_OK(cudaFuncSetAttribute(cg_apply_lc_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lc_smem)));
     if (part.n < lc_blocks) part.alloc(c, lc_blocks);
+  } else if (variant == "staged") {
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(staged_smem)));
   }
+  auto launch_reg = [&](auto rmax_tag) {
+    constexpr int R = decltype(rmax_tag)::value;
+    CUDA_OK(cudaFuncSetAttribute(cg_apply_reg_k<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(reg_smem)));
+    cg_apply_reg_k<T, R><<<gs, kBlock, reg_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p, AP.p,
+                                                              part.p, st.p);
+  };
 
   cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
   launched(c);
@@ -384,6 +559,18 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           launched(c);
           cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
                                                                   st.p);
+        } else if (variant == "staged") {
+          cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
+                                                                      AP.p, part.p, st.p);
+        } else if (variant == "reg") {
+          if (max_row <= 8)
+            launch_reg(std::integral_constant<int, 8>{});
+          else if (max_row <= 12)
+            launch_reg(std::integral_constant<int, 12>{});
+          else if (max_row <= 20)
+            launch_reg(std::integral_constant<int, 20>{});
+          else
+            launch_reg(std::integral_constant<int, 32>{});
         } else {
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         }

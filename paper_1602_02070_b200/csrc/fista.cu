@@ -285,80 +285,70 @@ struct SplitWs {
   double* tile_sums;   // 3 x tiles (objective)
 };
 
+constexpr int kST = 64;  // split-K output tile side
+constexpr int kSK = 16;  // k chunk
+
+// 64 x 64 output tile per CTA, 4 x 4 outputs per thread (rows ty + 16 a,
+// columns tx + 16 b), k staged through shared memory 16 at a time.
+template <bool kLeft>
+__device__ __forceinline__ void splitk_gemm(const float* __restrict__ A, i64 lda, i64 arows,
+                                            const float* __restrict__ B, i64 ldb, i64 bcols, i64 ka, i64 kb,
+                                            i64 i0, i64 c0, float (&acc)[4][4]) {
+  // kLeft:  acc += Lr[i, k] * Z[k, c]   (A = Lr dense col-major rr x rr, B = Z)
+  // !kLeft: acc += Z[i, k] * Lc[k, c]   (A = Z, B = Lc dense col-major)
+  __shared__ float As[kSK][kST + 1];
+  __shared__ float Bs[kSK][kST + 1];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (i64 k0 = ka; k0 < kb; k0 += kSK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int ii = tid & 63, kk = (tid >> 6) + 4 * q;
+      const i64 gi = i0 + ii, gk = k0 + kk;
+      As[kk][ii] = (gi < arows && gk < kb) ? A[gk * lda + gi] : 0.f;
+      const int kk2 = tid & 15, cc = (tid >> 4) + 16 * q;
+      const i64 gk2 = k0 + kk2, gc = c0 + cc;
+      Bs[kk2][cc] = (gk2 < kb && gc < bcols) ? B[gc * ldb + gk2] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kSK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = As[kk][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void splitk_partial(const float* __restrict__ Lr, const float* __restrict__ Lc,
                                                const float* __restrict__ Z, i64 rr, i64 rc, int use_r,
-                                               int use_c, i64 i0, i64 c0, i64 ka, i64 kb, float (&acc1)[2][2],
-                                               float (&acc2)[2][2]) {
-  __shared__ float As[kDK][kDT + 1];
-  __shared__ float Bs[kDK][kDT + 1];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+                                               int use_c, i64 i0, i64 c0, i64 ka, i64 kb, float (&acc1)[4][4],
+                                               float (&acc2)[4][4]) {
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) acc1[a][b] = acc2[a][b] = 0.f;
-  // part 1: k in [ka, min(kb, rr))
-  if (use_r)
-    for (i64 k0 = ka; k0 < min(kb, rr); k0 += kDK) {
-      const i64 kend = min(min(kb, rr), k0 + kDK);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
-        const i64 gi = i0 + ii, gk = k0 + kk;
-        As[kk][ii] = (gi < rr && gk < kend) ? Lr[gk * rr + gi] : 0.f;
-        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
-        const i64 gk2 = k0 + kk2, gc = c0 + cc;
-        Bs[kk2][cc] = (gk2 < kend && gc < rc) ? Z[gc * rr + gk2] : 0.f;
-      }
-      __syncthreads();
-#pragma unroll 8
-      for (int kk = 0; kk < kDK; ++kk) {
-        const float a0 = As[kk][ty], a1 = As[kk][ty + 16];
-        const float b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
-        acc1[0][0] = fmaf(a0, b0, acc1[0][0]);
-        acc1[0][1] = fmaf(a0, b1, acc1[0][1]);
-        acc1[1][0] = fmaf(a1, b0, acc1[1][0]);
-        acc1[1][1] = fmaf(a1, b1, acc1[1][1]);
-      }
-      __syncthreads();
-    }
-  // part 2: k - rr in [max(ka, rr) - rr, kb - rr)
-  if (use_c)
-    for (i64 k0 = max(ka, rr) - rr; k0 < kb - rr; k0 += kDK) {
-      const i64 kend = kb - rr;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
-        const i64 gi = i0 + ii, gk = k0 + kk;
-        As[kk][ii] = (gi < rr && gk < kend) ? Z[gk * rr + gi] : 0.f;
-        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
-        const i64 gk2 = k0 + kk2, gc = c0 + cc;
-        Bs[kk2][cc] = (gk2 < kend && gc < rc) ? Lc[gc * rc + gk2] : 0.f;
-      }
-      __syncthreads();
-#pragma unroll 8
-      for (int kk = 0; kk < kDK; ++kk) {
-        const float a0 = As[kk][ty], a1 = As[kk][ty + 16];
-        const float b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
-        acc2[0][0] = fmaf(a0, b0, acc2[0][0]);
-        acc2[0][1] = fmaf(a0, b1, acc2[0][1]);
-        acc2[1][0] = fmaf(a1, b0, acc2[1][0]);
-        acc2[1][1] = fmaf(a1, b1, acc2[1][1]);
-      }
-      __syncthreads();
-    }
+    for (int b = 0; b < 4; ++b) acc1[a][b] = acc2[a][b] = 0.f;
+  if (use_r && ka < rr) splitk_gemm<true>(Lr, rr, rr, Z, rr, rc, ka, min(kb, rr), i0, c0, acc1);
+  if (use_c && kb > rr) splitk_gemm<false>(Z, rr, rr, Lc, rc, rc, max(ka, rr) - rr, kb - rr, i0, c0, acc2);
 }
 
 // Writes the partial, returns true in the CTA that must finish the tile
-// (with acc1/acc2 holding the full sums).
+// (with acc1/acc2 holding the full sums, added in split order).
 __device__ __forceinline__ bool splitk_finish(const SplitWs& ws, i64 rr, i64 rc, i64 i0, i64 c0, int S,
-                                              float (&acc1)[2][2], float (&acc2)[2][2]) {
+                                              float (&acc1)[4][4], float (&acc2)[4][4]) {
   const i64 m = rr * rc;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4, s = blockIdx.z;
   const unsigned tile = blockIdx.x + gridDim.x * blockIdx.y;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
       if (i < rr && c < rc) {
         ws.part1[static_cast<i64>(s) * m + i + c * rr] = acc1[a][b];
@@ -373,9 +363,9 @@ __device__ __forceinline__ bool splitk_finish(const SplitWs& ws, i64 rr, i64 rc,
   if (!last) return false;
   __threadfence();
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
       float x1 = 0.f, x2 = 0.f;
       if (i < rr && c < rc)
@@ -399,15 +389,15 @@ __global__ void __launch_bounds__(256) fista_splitk_grad_prox_k(i64 rr, i64 rc, 
   if (st->done) return;
   const int Sn = gridDim.z;
   const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = static_cast<i64>(blockIdx.y) * kDT;
-  float acc1[2][2], acc2[2][2];
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kST, c0 = static_cast<i64>(blockIdx.y) * kST;
+  float acc1[4][4], acc2[4][4];
   splitk_partial(Lr, Lc, Z, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
-  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;
+  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;    
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
       if (i >= rr || c >= rc) continue;
       const i64 at = i + c * rr;
@@ -428,16 +418,16 @@ __global__ void __launch_bounds__(256) fista_splitk_objective_k(i64 rr, i64 rc, 
   const int use_r = gamma_r != 0.0, use_c = gamma_c != 0.0;
   const int Sn = gridDim.z;
   const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = static_cast<i64>(blockIdx.y) * kDT;
-  float acc1[2][2], acc2[2][2];
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kST, c0 = static_cast<i64>(blockIdx.y) * kST;
+  float acc1[4][4], acc2[4][4];
   splitk_partial(Lr, Lc, S, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
   if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double sm3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
       if (i >= rr || c >= rc) continue;
       const i64 at = i + c * rr;
@@ -598,11 +588,12 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   DevBuf<unsigned> scnt;
   DevBuf<double> ssum;
   SplitWs ws{};
+  dim3 gk(static_cast<unsigned>((rows + kST - 1) / kST), static_cast<unsigned>((cols + kST - 1) / kST));
   if (splitk) {
-    const unsigned tiles = gd.x * gd.y;
-    unsigned S = static_cast<unsigned>(std::max<i64>(1, (6 * static_cast<i64>(c->num_sms)) / tiles));
-    S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / kDK + 1, 32}));
-    gd.z = S;
+    const unsigned tiles = gk.x * gk.y;
+    unsigned S = static_cast<unsigned>(std::max<i64>(1, (4 * static_cast<i64>(c->num_sms)) / tiles));
+    S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / (2 * kSK) + 1, 64}));
+    gk.z = S;
     sp1.alloc(c, static_cast<size_t>(S) * N);
     sp2.alloc(c, static_cast<size_t>(S) * N);
     scnt.alloc(c, tiles + 1);
@@ -624,12 +615,12 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       if (splitk) {
         {
           KScope ks_(c, "fista_grad_prox");
-          SplitLauncher<T>::run_grad(c, gd, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg.loss, stepT, Zj, Y, Sj,
+          SplitLauncher<T>::run_grad(c, gk, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg.loss, stepT, Zj, Y, Sj,
                                      ws, st.p);
         }
         {
           KScope ks_(c, "fista_objective");
-          SplitLauncher<T>::run_obj(c, gd, rows, cols, Dr.p, Dc.p, cfg.gamma_r, cfg.gamma_c, cfg.loss, Sj, Y, ws, tr.p,
+          SplitLauncher<T>::run_obj(c, gk, rows, cols, Dr.p, Dc.p, cfg.gamma_r, cfg.gamma_c, cfg.loss, Sj, Y, ws, tr.p,
                                     st.p);
         }
       } else if (dense) {
