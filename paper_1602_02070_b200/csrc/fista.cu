@@ -338,125 +338,76 @@ __device__ __forceinline__ void splitk_partial(const float* __restrict__ Lr, con
   if (use_c && kb > rr) splitk_gemm<false>(Z, rr, rr, Lc, rc, rc, max(ka, rr) - rr, kb - rr, i0, c0, acc2);
 }
 
-// Writes the partial, returns true in the CTA that must finish the tile
-// (with acc1/acc2 holding the full sums, added in split order).
-__device__ __forceinline__ bool splitk_finish(const SplitWs& ws, i64 rr, i64 rc, i64 i0, i64 c0, int S,
-                                              float (&acc1)[4][4], float (&acc2)[4][4]) {
-  const i64 m = rr * rc;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4, s = blockIdx.z;
-  const unsigned tile = blockIdx.x + gridDim.x * blockIdx.y;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
-      if (i < rr && c < rc) {
-        ws.part1[static_cast<i64>(s) * m + i + c * rr] = acc1[a][b];
-        ws.part2[static_cast<i64>(s) * m + i + c * rr] = acc2[a][b];
-      }
-    }
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(ws.tile_cnt + tile, 1u) == static_cast<unsigned>(S - 1);
-  __syncthreads();
-  if (!last) return false;
-  __threadfence();
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
-      float x1 = 0.f, x2 = 0.f;
-      if (i < rr && c < rc)
-        for (int q = 0; q < S; ++q) {
-          x1 += __ldcg(ws.part1 + static_cast<i64>(q) * m + i + c * rr);
-          x2 += __ldcg(ws.part2 + static_cast<i64>(q) * m + i + c * rr);
-        }
-      acc1[a][b] = x1;
-      acc2[a][b] = x2;
-    }
-  if (threadIdx.x == 0) ws.tile_cnt[tile] = 0u;
-  return true;
-}
-
-__global__ void __launch_bounds__(256) fista_splitk_grad_prox_k(i64 rr, i64 rc, const float* __restrict__ Lr,
-                                                                const float* __restrict__ Lc, float s_r, float s_c,
-                                                                int use_r, int use_c, int loss, float step,
-                                                                const float* __restrict__ Z,
-                                                                const float* __restrict__ Y, float* __restrict__ S,
-                                                                SplitWs ws, const FistaState* st) {
+// Partial products of split s into ws.part1/part2[s] (no reduction here).
+__global__ void __launch_bounds__(256) fista_splitk_partial_k(i64 rr, i64 rc, const float* __restrict__ Lr,
+                                                              const float* __restrict__ Lc, int use_r, int use_c,
+                                                              const float* __restrict__ Z, SplitWs ws,
+                                                              const FistaState* st) {
   if (st->done) return;
   const int Sn = gridDim.z;
   const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
   const i64 i0 = static_cast<i64>(blockIdx.x) * kST, c0 = static_cast<i64>(blockIdx.y) * kST;
   float acc1[4][4], acc2[4][4];
   splitk_partial(Lr, Lc, Z, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
-  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;    
+  const i64 m = rr * rc;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  float* p1 = ws.part1 + static_cast<i64>(blockIdx.z) * m;
+  float* p2 = ws.part2 + static_cast<i64>(blockIdx.z) * m;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
-      if (i >= rr || c >= rc) continue;
-      const i64 at = i + c * rr;
-      float g = 0.f;
-      if (use_c) g = __fadd_rn(g, __fmul_rn(s_c, acc2[a][b]));
-      if (use_r) g = __fadd_rn(g, __fmul_rn(s_r, acc1[a][b]));
-      const float arg = __fsub_rn(Z[at], __fmul_rn(step, g));
-      S[at] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[at], step) : prox_l1_elem(arg, Y[at], step);
+      if (i < rr && c < rc) {
+        p1[i + c * rr] = acc1[a][b];
+        p2[i + c * rr] = acc2[a][b];
+      }
     }
 }
 
-__global__ void __launch_bounds__(256) fista_splitk_objective_k(i64 rr, i64 rc, const float* __restrict__ Lr,
-                                                                const float* __restrict__ Lc, double gamma_r,
-                                                                double gamma_c, int loss, const float* __restrict__ S,
-                                                                const float* __restrict__ Y, SplitWs ws,
-                                                                double* trace, FistaState* st) {
+__device__ __forceinline__ void splitk_sum(const SplitWs& ws, i64 m, int S, i64 e, float& x1, float& x2) {
+  x1 = 0.f;
+  x2 = 0.f;
+  for (int q = 0; q < S; ++q) {
+    x1 += ws.part1[static_cast<i64>(q) * m + e];
+    x2 += ws.part2[static_cast<i64>(q) * m + e];
+  }
+}
+
+__global__ void fista_splitk_grad_prox_k(i64 rr, i64 rc, int S, float s_r, float s_c, int use_r, int use_c, int loss,
+                                         float step, const float* __restrict__ Z, const float* __restrict__ Y,
+                                         float* __restrict__ Sout, SplitWs ws, const FistaState* st) {
+  if (st->done) return;
+  const i64 m = rr * rc;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < m; e += (i64)gridDim.x * blockDim.x) {
+    float x1, x2;
+    splitk_sum(ws, m, S, e, x1, x2);
+    float g = 0.f;
+    if (use_c) g = __fadd_rn(g, __fmul_rn(s_c, x2));
+    if (use_r) g = __fadd_rn(g, __fmul_rn(s_r, x1));
+    const float arg = __fsub_rn(Z[e], __fmul_rn(step, g));
+    Sout[e] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[e], step) : prox_l1_elem(arg, Y[e], step);
+  }
+}
+
+__global__ void fista_splitk_objective_k(i64 rr, i64 rc, int S, double gamma_r, double gamma_c, int loss,
+                                         const float* __restrict__ Sv, const float* __restrict__ Y, SplitWs ws,
+                                         double* partials, double* trace, FistaState* st) {
   if (st->done) return;
   const int use_r = gamma_r != 0.0, use_c = gamma_c != 0.0;
-  const int Sn = gridDim.z;
-  const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kST, c0 = static_cast<i64>(blockIdx.y) * kST;
-  float acc1[4][4], acc2[4][4];
-  splitk_partial(Lr, Lc, S, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
-  if (!splitk_finish(ws, rr, rc, i0, c0, Sn, acc1, acc2)) return;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const i64 m = rr * rc;
   double sm3[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
-      if (i >= rr || c >= rc) continue;
-      const i64 at = i + c * rr;
-      const double x = static_cast<double>(S[at]);
-      const double e = static_cast<double>(Y[at]) - x;
-      sm3[0] += loss == CPCAG_LOSS_L2 ? e * e : fabs(e);
-      sm3[1] += static_cast<double>(acc2[a][b]) * x;
-      sm3[2] += static_cast<double>(acc1[a][b]) * x;
-    }
-  block_sum<3>(sm3);
-  const unsigned tiles = gridDim.x * gridDim.y, tile = blockIdx.x + gridDim.x * blockIdx.y;
-  __shared__ bool last_tile;
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < 3; ++q) ws.tile_sums[q * tiles + tile] = sm3[q];
-    __threadfence();
-    last_tile = atomicAdd(ws.done_cnt, 1u) == tiles - 1;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < m; e += (i64)gridDim.x * blockDim.x) {
+    float x1, x2;
+    splitk_sum(ws, m, S, e, x1, x2);
+    const double x = static_cast<double>(Sv[e]);
+    const double d = static_cast<double>(Y[e]) - x;
+    sm3[0] += loss == CPCAG_LOSS_L2 ? d * d : fabs(d);
+    sm3[1] += static_cast<double>(x2) * x;
+    sm3[2] += static_cast<double>(x1) * x;
   }
-  __syncthreads();
-  if (!last_tile) return;
-  __threadfence();
   double tot[3];
-  for (int q = 0; q < 3; ++q) {
-    double x = 0.0;
-    for (unsigned t = threadIdx.x; t < tiles; t += blockDim.x) x += __ldcg(ws.tile_sums + q * tiles + t);
-    tot[q] = x;
-  }
-  block_sum<3>(tot);
-  if (threadIdx.x == 0) {
-    *ws.done_cnt = 0u;
+  if (grid_sum_last<3>(sm3, partials, &st->cnt[0], tot) && threadIdx.x == 0) {
     double val = tot[0];
     if (use_c) val += gamma_c * tot[1];
     if (use_r) val += gamma_r * tot[2];
@@ -478,30 +429,30 @@ __global__ void __launch_bounds__(256) fista_splitk_objective_k(i64 rr, i64 rc, 
 
 template <typename T>
 struct SplitLauncher {
-  static bool run_grad(Ctx*, dim3, i64, i64, const T*, const T*, T, T, int, int, int, T, const T*, const T*, T*,
-                       const SplitWs&, FistaState*) {
-    return false;
-  }
-  static bool run_obj(Ctx*, dim3, i64, i64, const T*, const T*, double, double, int, const T*, const T*,
-                      const SplitWs&, double*, FistaState*) {
-    return false;
-  }
+  static void grad(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, T, T, int, int, int, T, const T*, const T*, T*,
+                   const SplitWs&, FistaState*) {}
+  static void obj(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, double, double, int, const T*, const T*,
+                  const SplitWs&, double*, double*, FistaState*) {}
 };
 template <>
 struct SplitLauncher<float> {
-  static bool run_grad(Ctx* c, dim3 g, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r, float s_c,
-                       int use_r, int use_c, int loss, float step, const float* Z, const float* Y, float* S,
-                       const SplitWs& ws, FistaState* st) {
-    fista_splitk_grad_prox_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, s_r, s_c, use_r, use_c, loss, step, Z, Y, S,
-                                                        ws, st);
+  static void grad(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r,
+                   float s_c, int use_r, int use_c, int loss, float step, const float* Z, const float* Y, float* S,
+                   const SplitWs& ws, FistaState* st) {
+    fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, use_r, use_c, Z, ws, st);
     launched(c);
-    return true;
+    fista_splitk_grad_prox_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), s_r, s_c, use_r, use_c, loss,
+                                                        step, Z, Y, S, ws, st);
+    launched(c);
   }
-  static bool run_obj(Ctx* c, dim3 g, i64 rr, i64 rc, const float* Lr, const float* Lc, double gr, double gc,
-                      int loss, const float* S, const float* Y, const SplitWs& ws, double* trace, FistaState* st) {
-    fista_splitk_objective_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, gr, gc, loss, S, Y, ws, trace, st);
+  static void obj(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, double gr, double gc,
+                  int loss, const float* S, const float* Y, const SplitWs& ws, double* partials, double* trace,
+                  FistaState* st) {
+    fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, gr != 0.0, gc != 0.0, S, ws, st);
     launched(c);
-    return true;
+    fista_splitk_objective_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), gr, gc, loss, S, Y, ws,
+                                                        partials, trace, st);
+    launched(c);
   }
 };
 
@@ -591,8 +542,8 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   dim3 gk(static_cast<unsigned>((rows + kST - 1) / kST), static_cast<unsigned>((cols + kST - 1) / kST));
   if (splitk) {
     const unsigned tiles = gk.x * gk.y;
-    unsigned S = static_cast<unsigned>(std::max<i64>(1, (4 * static_cast<i64>(c->num_sms)) / tiles));
-    S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / (2 * kSK) + 1, 64}));
+    unsigned S = static_cast<unsigned>(std::max<i64>(1, (2 * static_cast<i64>(c->num_sms)) / tiles));
+    S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / (4 * kSK) + 1, 32}));
     gk.z = S;
     sp1.alloc(c, static_cast<size_t>(S) * N);
     sp2.alloc(c, static_cast<size_t>(S) * N);
@@ -615,13 +566,13 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       if (splitk) {
         {
           KScope ks_(c, "fista_grad_prox");
-          SplitLauncher<T>::run_grad(c, gk, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg.loss, stepT, Zj, Y, Sj,
-                                     ws, st.p);
+          SplitLauncher<T>::grad(c, gk, nb1, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg.loss, stepT, Zj, Y,
+                                 Sj, ws, st.p);
         }
         {
           KScope ks_(c, "fista_objective");
-          SplitLauncher<T>::run_obj(c, gk, rows, cols, Dr.p, Dc.p, cfg.gamma_r, cfg.gamma_c, cfg.loss, Sj, Y, ws, tr.p,
-                                    st.p);
+          SplitLauncher<T>::obj(c, gk, nb1, rows, cols, Dr.p, Dc.p, cfg.gamma_r, cfg.gamma_c, cfg.loss, Sj, Y, ws,
+                                part.p, tr.p, st.p);
         }
       } else if (dense) {
         {
