@@ -190,6 +190,10 @@ struct OutView {
 
 inline void sync(Ctx* c) { CUDA_OK(cudaStreamSynchronize(c->stream)); }
 
+// Host-side phase tracing (CPCAG_TRACE=1): synchronises and prints wall time
+// since the previous mark.  Off by default; used to find host overheads.
+void trace_mark(Ctx* c, const char* what);
+
 // Copies a small device struct back through pinned memory (synchronises).
 template <typename T>
 T read_back(Ctx* c, const T* dptr) {

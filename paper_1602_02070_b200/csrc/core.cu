@@ -7,6 +7,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <numeric>
 
@@ -42,6 +45,17 @@ double HostRng::gaussian() {
   spare = rad * std::sin(tau * b);
   has_spare = true;
   return rad * std::cos(tau * b);
+}
+
+void trace_mark(Ctx* c, const char* what) {
+  static const bool on = std::getenv("CPCAG_TRACE") != nullptr;
+  if (!on) return;
+  static thread_local std::chrono::steady_clock::time_point last = std::chrono::steady_clock::now();
+  cudaStreamSynchronize(c->stream);
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[cpcag trace] %-28s %9.3f ms\n", what,
+               std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
 }
 
 // ------------------------------------------------------------------ kernel timing

@@ -745,6 +745,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     kpos[u] = static_cast<int>(j);
   }
   const i64 m = static_cast<i64>(keep.size());
+  trace_mark(c, "kron: enter");
 
   // graph.cpp:183-193: every component must hold a kept node.
   DevBuf<i64> keep_d(c, std::max<i64>(m, 1));
@@ -771,6 +772,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
       runtime("kron reduction: connected component containing node " + std::to_string(bad) + " has no kept node");
   }
 
+  trace_mark(c, "kron: components");
   std::vector<i64> interior;
   interior.reserve(static_cast<size_t>(n - m));
   std::vector<int> ipos(static_cast<size_t>(n), -1);
@@ -797,6 +799,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
 
   DevBuf<i64> int_d(c, ni);
   CUDA_OK(cudaMemcpyAsync(int_d.p, interior.data(), sizeof(i64) * ni, cudaMemcpyHostToDevice, c->stream));
+  trace_mark(c, "kron: maps+Lbb");
   Csr* Laa = gather_sub(c, L, int_d.p, ni, ipos_d.p, ni);
   Csr* Lba = gather_sub(c, L, keep_d.p, m, ipos_d.p, ni);
   std::unique_ptr<Csr> own_aa(Laa), own_ba(Lba);
@@ -804,6 +807,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   jacobi_inv_k<<<blocks_for(ni), kBlock, 0, c->stream>>>(ni, Laa->rp, Laa->ci, Laa->v, inv.p);
   launched(c);
 
+  trace_mark(c, "kron: gathers");
   // Kept nodes with a nonempty row of L_ba get a solve (graph.cpp:213-220).
   std::vector<i64> rp_ba(static_cast<size_t>(m) + 1);
   CUDA_OK(cudaMemcpyAsync(rp_ba.data(), Lba->rp, sizeof(i64) * (m + 1), cudaMemcpyDeviceToHost, c->stream));
@@ -833,6 +837,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     X.zero(c);
     rhs_fill_slab_k<<<blocks_for(nb), kBlock, 0, c->stream>>>(ni, nb, cols_d.p, Lba->rp, Lba->ci, Lba->v, B.p);
     launched(c);
+    trace_mark(c, "kron: slice setup");
     PcgBatchOut res;
     pcg_slab(c, Laa, inv.p, B.p, X.p, ni, nb, pcg_tol, max_iter, &res);
     for (i64 q = 0; q < nb; ++q) {
@@ -854,7 +859,10 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     launched(c);
   }
   if (fail_j >= 0) runtime(fail_msg);
-  return dense_to_csr(c, S.p, m, prune_tol, true);
+  trace_mark(c, "kron: solves+schur");
+  Csr* out = dense_to_csr(c, S.p, m, prune_tol, true);
+  trace_mark(c, "kron: to csr");
+  return out;
 }
 
 }  // namespace cpcag_cuda
