@@ -212,6 +212,30 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
                                 const cpcag_decoder_config* cfg, void* X, int* converged,
                                 int64_t* iterations);
 
+/* ------------------------------------------------------------------ column-sharded decoder */
+/* Local primitives of the alternate decoder for one column block
+ * [c_begin, c_end) of a column-sharded multi-GPU solve: the
+ * caller all-gathers the search direction P between ranks (NCCL over
+ * NVLink) and all-reduces the partial dot products; these functions do the
+ * GPU-local work.  All matrices are device memory; P_full is p x n, blocks
+ * are p x (c_end - c_begin), column-major.  gbar = gamma / lambda_k1. */
+typedef struct cpcag_decoder_block_s* cpcag_decoder_block;
+int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int64_t p, int64_t n, int64_t c_begin,
+                                    int64_t c_end, cpcag_csr Lr, cpcag_csr Lc, const int64_t* omega_r,
+                                    int64_t rho_r, const int64_t* omega_c, int64_t rho_c, double gbar_r,
+                                    double gbar_c, cpcag_decoder_block* out);
+int cpcag_cuda_decoder_block_destroy(cpcag_decoder_block b);
+/* B_block = scatter(Xt) restricted to the block; *sq_norm = ||B_block||^2. */
+int cpcag_cuda_decoder_block_rhs(cpcag_decoder_block b, const void* Xt, void* B_block, double* sq_norm);
+/* AP_block = (gbar_c P L_c + gbar_r L_r P + M o P)(:, block); *dot = <P_block, AP_block>. */
+int cpcag_cuda_decoder_block_apply(cpcag_decoder_block b, const void* P_full, void* AP_block, double* dot);
+/* R -= alpha AP over count entries; *rr = ||R||^2 (solvers.hpp:60-62). */
+int cpcag_cuda_cg_residual(cpcag_ctx ctx, int precision, int64_t count, double alpha, void* R, const void* AP,
+                           double* rr);
+/* X += alpha P; P = R + beta P (solvers.hpp:59,63). */
+int cpcag_cuda_cg_update(cpcag_ctx ctx, int precision, int64_t count, double alpha, double beta, void* X, void* P,
+                         const void* R);
+
 /* ------------------------------------------------------------------ pipeline */
 typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36-63 */
   int64_t knn;               /* default 10 */

@@ -98,6 +98,13 @@ SIGNATURES = {
     "cpcag_cuda_alternate_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                               dbl, dbl, C.POINTER(DecoderConfigC), vp,
                                               C.POINTER(C.c_int), ip]),
+    "cpcag_cuda_decoder_block_create": (C.c_int, [vp, C.c_int, i64, i64, i64, i64, vp, vp, vp, i64, vp, i64,
+                                                  dbl, dbl, C.POINTER(vp)]),
+    "cpcag_cuda_decoder_block_destroy": (C.c_int, [vp]),
+    "cpcag_cuda_decoder_block_rhs": (C.c_int, [vp, vp, vp, dp]),
+    "cpcag_cuda_decoder_block_apply": (C.c_int, [vp, vp, vp, dp]),
+    "cpcag_cuda_cg_residual": (C.c_int, [vp, C.c_int, i64, dbl, vp, vp, dp]),
+    "cpcag_cuda_cg_update": (C.c_int, [vp, C.c_int, i64, dbl, dbl, vp, vp, vp]),
     "cpcag_cuda_run_pipeline": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp,
                                           C.POINTER(PipelineConfigC), vp, vp, vp, vp, vp,
                                           C.POINTER(PipelineReportC)]),

@@ -14,6 +14,7 @@
 // Every scalar lives on the device; the host polls the done flag once per
 // chunk of iterations.
 #include <algorithm>
+#include <memory>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -229,16 +230,19 @@ __global__ void __launch_bounds__(256) cg_apply_lc_k(i64 p, i64 n, Pull<T> Lc, T
 // of L_c for its columns are copied into shared memory once, so the inner
 // loops only issue the P gathers (coalesced along i for the X L_c part).  The
 // per-entry operation order is unchanged (bit-identical to cg_apply_k).
+// Columns [c_lo, c_hi) are computed (the whole matrix for the one-GPU
+// solver, one column block for the sharded decoder); AP is indexed by the
+// global column (AP + c * p), P holds every column.
 template <typename T>
-__global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
-                                                         Plan pl, i64 cols_per_cta, const T* __restrict__ P,
+__global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 c_lo, i64 c_hi, Pull<T> Lr, Pull<T> Lc, T gr,
+                                                         T gc, Plan pl, i64 cols_per_cta, const T* __restrict__ P,
                                                          T* __restrict__ AP, double* partials, CgState* st) {
   if (st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
   const i64 i1 = min(p, i0 + static_cast<i64>(blockDim.x));
-  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
-  const i64 ce = min(n, cb + cols_per_cta);
+  const i64 cb = c_lo + static_cast<i64>(blockIdx.y) * cols_per_cta;
+  const i64 ce = min(c_hi, cb + cols_per_cta);
   const i64 kr_base = Lr.rp[i0], er = Lr.rp[i1] - kr_base;
   const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
   T* vr = reinterpret_cast<T*>(smraw);
@@ -560,7 +564,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
                                                                   st.p);
         } else if (variant == "staged") {
-          cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
+          cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, 0, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
                                                                       AP.p, part.p, st.p);
         } else if (variant == "reg") {
           if (max_row <= 8)
@@ -610,6 +614,254 @@ template void alternate_decode_device<float>(Ctx*, const float*, i64, i64, const
                                              Csr*, Csr*, double, double, const cpcag_decoder_config&,
                                              float*, int*, i64*);
 
+// ------------------------------------------------------------------ column-block primitives
+// The decoder's local work for one column block [c0, c1) of a column-sharded
+// solve: the caller all-gathers P between ranks and
+// all-reduces the partial dots; everything here touches only this GPU.
+struct DecBlock {
+  Ctx* c;
+  int prec;
+  i64 p, n, c0, c1, rho_r;
+  Csr *Lr, *Lc;
+  double gr, gc;
+  DevBuf<int> rsel, csel;
+  DevBuf<double> part;
+  DevBuf<CgState> st;
+  size_t smem = 0;
+  i64 cols_per_cta = 1;
+  dim3 grid;
+};
+
+template <typename T>
+__global__ void block_rhs_k(i64 p, i64 c0, i64 c1, Plan pl, const T* __restrict__ Xt, T* __restrict__ B,
+                            double* partials, CgState* st) {
+  double s[1] = {0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p)
+    for (i64 c = c0 + blockIdx.y; c < c1; c += gridDim.y) {
+      const T b = rhs_at(pl, Xt, i, c);
+      B[i + (c - c0) * p] = b;
+      s[0] += static_cast<double>(b) * static_cast<double>(b);
+    }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0) st->norm_b = tot[0];
+}
+
+template <typename T>
+__global__ void block_residual_k(i64 N, T alpha, T* __restrict__ R, const T* __restrict__ AP, double* partials,
+                                 CgState* st) {
+  double s[1] = {0.0};
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const T r = sub_rn(R[q], mul_rn(alpha, AP[q]));
+    R[q] = r;
+    s[0] += static_cast<double>(r) * static_cast<double>(r);
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[2], tot) && threadIdx.x == 0) st->rho_next = tot[0];
+}
+
+template <typename T>
+__global__ void block_update_k(i64 N, T alpha, T beta, T* __restrict__ X, T* __restrict__ P, const T* __restrict__ R) {
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const T pv = P[q];
+    X[q] = add_rn(X[q], mul_rn(alpha, pv));
+    P[q] = add_rn(R[q], mul_rn(beta, pv));
+  }
+}
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+namespace {
+DecBlock* as_block(cpcag_decoder_block b) {
+  if (!b) invalid("null decoder block");
+  return reinterpret_cast<DecBlock*>(b);
+}
+
+template <typename T>
+void block_apply(DecBlock* b, const T* Pfull, T* APblk, double* dot) {
+  Ctx* c = b->c;
+  const Pull<T> pr = make_pull<T>(c, b->Lr, false), pc = make_pull<T>(c, b->Lc, true);
+  const Plan pl{b->rsel.p, b->csel.p, b->rho_r};
+  b->st.zero(c);
+  // AP indexed by global column: shift the block pointer back by c0 columns.
+  T* base = APblk - b->c0 * b->p;
+  {
+    KScope ks_(c, "cg_apply");
+    cg_apply_staged_k<T><<<b->grid, kBlock, b->smem, c->stream>>>(b->p, b->c0, b->c1, pr, pc, static_cast<T>(b->gr),
+                                                                  static_cast<T>(b->gc), pl, b->cols_per_cta, Pfull,
+                                                                  base, b->part.p, b->st.p);
+    launched(c);
+  }
+  *dot = read_back(c, b->st.p).curv;
+}
+}  // namespace
+
+extern "C" int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int64_t p, int64_t n, int64_t c_begin,
+                                               int64_t c_end, cpcag_csr Lr, cpcag_csr Lc, const int64_t* omega_r,
+                                               int64_t rho_r, const int64_t* omega_c, int64_t rho_c, double gbar_r,
+                                               double gbar_c, cpcag_decoder_block* out) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (!out) invalid("null output pointer");
+    if (precision != CPCAG_F64 && precision != CPCAG_F32) invalid("unknown precision flag");
+    Csr* A = as_csr(Lr);
+    Csr* B = as_csr(Lc);
+    if (A->rows != p || A->cols != p || B->rows != n || B->cols != n)
+      invalid("alternate decoder: Laplacians do not match plan");
+    if (c_begin < 0 || c_end > n || c_begin > c_end) invalid("decoder block: column range out of bounds");
+    auto blk = std::make_unique<DecBlock>();
+    blk->c = c;
+    blk->prec = precision;
+    blk->p = p;
+    blk->n = n;
+    blk->c0 = c_begin;
+    blk->c1 = c_end;
+    blk->rho_r = rho_r;
+    blk->Lr = A;
+    blk->Lc = B;
+    blk->gr = gbar_r;
+    blk->gc = gbar_c;
+    std::vector<int> rs(static_cast<size_t>(p), -1), cs(static_cast<size_t>(n), -1);
+    std::vector<i64> omr(static_cast<size_t>(rho_r)), omc(static_cast<size_t>(rho_c));
+    auto fetch = [&](std::vector<i64>& dst, const int64_t* src) {
+      if (dst.empty()) return;
+      if (is_device_ptr(src))
+        CUDA_OK(cudaMemcpy(dst.data(), src, sizeof(i64) * dst.size(), cudaMemcpyDeviceToHost));
+      else
+        std::copy(src, src + dst.size(), dst.begin());
+    };
+    fetch(omr, omega_r);
+    fetch(omc, omega_c);
+    for (i64 k = 0; k < rho_r; ++k) {
+      if (omr[k] < 0 || omr[k] >= p || rs[omr[k]] >= 0) invalid("alternate decoder: Xt does not match plan");
+      rs[omr[k]] = static_cast<int>(k);
+    }
+    for (i64 k = 0; k < rho_c; ++k) {
+      if (omc[k] < 0 || omc[k] >= n || cs[omc[k]] >= 0) invalid("alternate decoder: Xt does not match plan");
+      cs[omc[k]] = static_cast<int>(k);
+    }
+    blk->rsel.alloc(c, std::max<i64>(p, 1));
+    blk->csel.alloc(c, std::max<i64>(n, 1));
+    if (p) CUDA_OK(cudaMemcpyAsync(blk->rsel.p, rs.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
+    if (n) CUDA_OK(cudaMemcpyAsync(blk->csel.p, cs.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    // launch geometry of the staged apply over the block's columns
+    const i64 nb_cols = std::max<i64>(c_end - c_begin, 1);
+    const unsigned gx = blocks_for(std::max<i64>(p, 1));
+    const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx);
+    const i64 gy = std::max<i64>(1, std::min<i64>({nb_cols, ycap, 65535}));
+    blk->cols_per_cta = (nb_cols + gy - 1) / gy;
+    blk->grid = dim3(gx, static_cast<unsigned>((nb_cols + blk->cols_per_cta - 1) / blk->cols_per_cta));
+    std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
+    CUDA_OK(cudaMemcpy(rpr.data(), A->rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(rpc.data(), B->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost));
+    i64 max_er = 0, max_ec = 0;
+    for (unsigned b = 0; b < gx; ++b) {
+      const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);
+      max_er = std::max(max_er, rpr[e] - rpr[a]);
+    }
+    for (unsigned b = 0; b < blk->grid.y; ++b) {
+      const i64 a = std::min<i64>(n, c_begin + static_cast<i64>(b) * blk->cols_per_cta);
+      const i64 e = std::min<i64>(c_end, a + blk->cols_per_cta);
+      max_ec = std::max(max_ec, rpc[e] - rpc[a]);
+    }
+    const size_t es = precision == CPCAG_F64 ? sizeof(double) : sizeof(float);
+    blk->smem = static_cast<size_t>(max_er + max_ec) * (es + sizeof(int)) + 16;
+    if (blk->smem > 200 * 1024) invalid("decoder block: operator slice exceeds shared memory");
+    if (precision == CPCAG_F64)
+      CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(blk->smem)));
+    else
+      CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(blk->smem)));
+    const size_t nparts = std::max<size_t>(static_cast<size_t>(blk->grid.x) * blk->grid.y,
+                                           stride_blocks(c, std::max<i64>(p * nb_cols, 1)));
+    blk->part.alloc(c, nparts);
+    blk->st.alloc(c, 1);
+    blk->st.zero(c);
+    sync(c);
+    *out = reinterpret_cast<cpcag_decoder_block>(blk.release());
+  });
+}
+
+extern "C" int cpcag_cuda_decoder_block_destroy(cpcag_decoder_block b) {
+  return guard([&] { delete as_block(b); });
+}
+
+extern "C" int cpcag_cuda_decoder_block_rhs(cpcag_decoder_block bh, const void* Xt, void* B, double* sq_norm) {
+  return guard([&] {
+    DecBlock* b = as_block(bh);
+    Ctx* c = b->c;
+    if (!Xt || !B || !sq_norm) invalid("null argument");
+    const Plan pl{b->rsel.p, b->csel.p, b->rho_r};
+    b->st.zero(c);
+    const i64 ncol = b->c1 - b->c0;
+    dim3 g(blocks_for(std::max<i64>(b->p, 1)), static_cast<unsigned>(std::max<i64>(1, std::min<i64>(ncol, 65535))));
+    if (b->prec == CPCAG_F64)
+      block_rhs_k<double><<<g, kBlock, 0, c->stream>>>(b->p, b->c0, b->c1, pl, static_cast<const double*>(Xt),
+                                                       static_cast<double*>(B), b->part.p, b->st.p);
+    else
+      block_rhs_k<float><<<g, kBlock, 0, c->stream>>>(b->p, b->c0, b->c1, pl, static_cast<const float*>(Xt),
+                                                      static_cast<float*>(B), b->part.p, b->st.p);
+    launched(c);
+    *sq_norm = read_back(c, b->st.p).norm_b;
+  });
+}
+
+extern "C" int cpcag_cuda_decoder_block_apply(cpcag_decoder_block bh, const void* P_full, void* AP_block,
+                                              double* dot) {
+  return guard([&] {
+    DecBlock* b = as_block(bh);
+    if (!P_full || !AP_block || !dot) invalid("null argument");
+    if (b->prec == CPCAG_F64)
+      block_apply<double>(b, static_cast<const double*>(P_full), static_cast<double*>(AP_block), dot);
+    else
+      block_apply<float>(b, static_cast<const float*>(P_full), static_cast<float*>(AP_block), dot);
+  });
+}
+
+extern "C" int cpcag_cuda_cg_residual(cpcag_ctx ctx, int precision, int64_t count, double alpha, void* R,
+                                      const void* AP, double* rr) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (!rr) invalid("null argument");
+    const unsigned nb = stride_blocks(c, std::max<int64_t>(count, 1));
+    DevBuf<double> part(c, nb);
+    DevBuf<CgState> st(c, 1);
+    st.zero(c);
+    if (precision == CPCAG_F64)
+      block_residual_k<double><<<nb, kBlock, 0, c->stream>>>(count, alpha, static_cast<double*>(R),
+                                                             static_cast<const double*>(AP), part.p, st.p);
+    else if (precision == CPCAG_F32)
+      block_residual_k<float><<<nb, kBlock, 0, c->stream>>>(count, static_cast<float>(alpha), static_cast<float*>(R),
+                                                            static_cast<const float*>(AP), part.p, st.p);
+    else
+      invalid("unknown precision flag");
+    launched(c);
+    *rr = read_back(c, st.p).rho_next;
+  });
+}
+
+extern "C" int cpcag_cuda_cg_update(cpcag_ctx ctx, int precision, int64_t count, double alpha, double beta, void* X,
+                                    void* P, const void* R) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    const unsigned nb = stride_blocks(c, std::max<int64_t>(count, 1));
+    if (precision == CPCAG_F64)
+      block_update_k<double><<<nb, kBlock, 0, c->stream>>>(count, alpha, beta, static_cast<double*>(X),
+                                                           static_cast<double*>(P), static_cast<const double*>(R));
+    else if (precision == CPCAG_F32)
+      block_update_k<float><<<nb, kBlock, 0, c->stream>>>(count, static_cast<float>(alpha), static_cast<float>(beta),
+                                                          static_cast<float*>(X), static_cast<float*>(P),
+                                                          static_cast<const float*>(R));
+    else
+      invalid("unknown precision flag");
+    launched(c);
+  });
+}
+
+namespace cpcag_cuda {
 }  // namespace cpcag_cuda
 
 using namespace cpcag_cuda;

@@ -1,0 +1,178 @@
+"""Column-sharded alternate decoder across the GPUs of one node.
+
+X (p x n) is split into contiguous column blocks, one per rank.  Per CG
+iteration (the reference recurrence of detail::pcg_core, solvers.hpp:33-74,
+identity preconditioner):
+
+  1. all-gather the search-direction blocks P_g into the full P (NCCL over
+     NVLink): the X·L_c term of a block needs P's halo columns, and for kNN
+     graphs over high-dimensional points the halo is nearly every column
+     (SURVEY §0.5), so a full all-gather is the exchange;
+  2. AP_g = (γ̄_c P L_c + γ̄_r L_r P + M∘P)(:, block g) on the local GPU;
+     L_r·P is block-local;
+  3. all-reduce ⟨P_g, AP_g⟩ -> α;  R_g -= α AP_g;  all-reduce ‖R_g‖² -> β;
+  4. X_g += α P_g;  P_g = R_g + β P_g.
+
+The local work runs in libcpcag_cuda.so (`CudaBlockBackend`, the
+cpcag_cuda_decoder_block_* / cpcag_cuda_cg_* entry points); the
+communication is torch.distributed (`TorchCollectives`).  Both are plain
+objects handed to `alternate_decode_sharded`, which holds only the
+algorithm, so the distributed logic is testable on CPU (gloo) with a test
+double standing in for the GPU backend.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+
+
+def column_blocks(n: int, world: int):
+    """Equal-width blocks (the last one may be short or empty) so all-gather
+    buffers have one size: block g is [g * w, min(n, (g + 1) * w))."""
+    w = -(-n // world) if world > 0 else n
+    return w, [(min(n, g * w), min(n, (g + 1) * w)) for g in range(world)]
+
+
+class TorchCollectives:
+    """all-gather / all-reduce on torch.distributed (NCCL for CUDA tensors)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_blocks(self, full_padded, block_padded):
+        """full_padded: 1-D tensor of world * len(block_padded) elements."""
+        if self.dist.get_backend(self.group) == "nccl":
+            self.dist.all_gather_into_tensor(full_padded, block_padded, group=self.group)
+        else:
+            parts = list(full_padded.chunk(self.world))
+            self.dist.all_gather(parts, block_padded, group=self.group)
+
+    def allreduce_sum(self, value: float, like) -> float:
+        import torch
+
+        t = torch.tensor([value], dtype=torch.float64, device=like.device)
+        self.dist.all_reduce(t, group=self.group)
+        return float(t.item())
+
+
+class CudaBlockBackend:
+    """GPU-local primitives through the C-ABI (device tensors, column-major)."""
+
+    def __init__(self, ctx, precision, plan, Lr, Lc, gbar_r, gbar_c, c0, c1, stream=None):
+        import torch
+
+        # The collectives (NCCL) and the tensor copies run on torch's stream;
+        # the block kernels must be ordered with them.
+        ctx.set_stream(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        self.ctx = ctx
+        self.prec = precision
+        self.p, self.n = plan.p, plan.n
+        self.c0, self.c1 = c0, c1
+        om_r = np.ascontiguousarray(plan.omega_r, np.int64)
+        om_c = np.ascontiguousarray(plan.omega_c, np.int64)
+        h = N.vp()
+        N.check(N.lib().cpcag_cuda_decoder_block_create(
+            ctx.handle, precision, self.p, self.n, c0, c1, Lr.handle, Lc.handle, om_r.ctypes.data, len(om_r),
+            om_c.ctypes.data, len(om_c), float(gbar_r), float(gbar_c), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            N.lib().cpcag_cuda_decoder_block_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def rhs(self, Xt, B) -> float:
+        out = N.dbl()
+        N.check(N.lib().cpcag_cuda_decoder_block_rhs(self.h, Xt.data_ptr(), B.data_ptr(), C.byref(out)))
+        return float(out.value)
+
+    def apply(self, P_full, AP) -> float:
+        out = N.dbl()
+        N.check(N.lib().cpcag_cuda_decoder_block_apply(self.h, P_full.data_ptr(), AP.data_ptr(), C.byref(out)))
+        return float(out.value)
+
+    def residual(self, alpha, R, AP) -> float:
+        out = N.dbl()
+        N.check(N.lib().cpcag_cuda_cg_residual(self.ctx.handle, self.prec, R.numel(), float(alpha), R.data_ptr(),
+                                               AP.data_ptr(), C.byref(out)))
+        return float(out.value)
+
+    def update(self, alpha, beta, X, P, R):
+        N.check(N.lib().cpcag_cuda_cg_update(self.ctx.handle, self.prec, X.numel(), float(alpha), float(beta),
+                                             X.data_ptr(), P.data_ptr(), R.data_ptr()))
+
+
+@dataclass
+class ShardedResult:
+    X_block: object      # p x (c1 - c0) solution block of this rank
+    c0: int
+    c1: int
+    converged: bool
+    iterations: int
+
+
+def alternate_decode_sharded(Xt, plan, backend, coll, zeros, tol=1e-10, max_iter=5000) -> ShardedResult:
+    """The CG of decoders.cpp:145-186 over column blocks.
+
+    backend: local primitives (rhs/apply/residual/update) of this rank's block.
+    coll:    rank/world + all_gather_blocks + allreduce_sum.
+    zeros:   allocator zeros(count) -> 1-D array/tensor on the backend's device.
+    Blocks are p x w with w = ceil(n / world) columns (zero-padded).
+    """
+    p, n = plan.p, plan.n
+    w, blocks = column_blocks(n, coll.world)
+    c0, c1 = blocks[coll.rank]
+    nloc = c1 - c0
+    B = zeros(p * w)
+    X = zeros(p * w)
+    R = zeros(p * w)
+    P = zeros(p * w)
+    AP = zeros(p * w)
+    Pfull = zeros(p * w * coll.world)
+    view = lambda a: a[: p * nloc]
+    bb = coll.allreduce_sum(backend.rhs(Xt, view(B)), B)
+    norm_b = math.sqrt(bb)
+    if norm_b == 0.0:  # solvers.hpp:38-42
+        return ShardedResult(view(X), c0, c1, True, 0)
+    target = tol * norm_b
+    R[:] = B  # r = b - A x with x = 0
+    P[:] = R  # z = r
+    rho = bb
+    it = 0
+    while it < max_iter:
+        if math.sqrt(rho) <= target:
+            break
+        coll.all_gather_blocks(Pfull, P)
+        curv = coll.allreduce_sum(backend.apply(Pfull, view(AP)), AP)
+        if not math.isfinite(curv) or curv <= 0.0:
+            raise RuntimeError(f"pcg: breakdown (nonpositive curvature) at iteration {it}")
+        alpha = rho / curv
+        rho_next = coll.allreduce_sum(backend.residual(alpha, view(R), view(AP)), R)
+        beta = rho_next / rho
+        backend.update(alpha, beta, view(X), view(P), view(R))
+        rho = rho_next
+        it += 1
+    # true residual (solvers.hpp:69-72)
+    coll.all_gather_blocks(Pfull, X)
+    backend.apply(Pfull, view(AP))
+    E = B.clone() if hasattr(B, "clone") else B.copy()
+    rt = coll.allreduce_sum(backend.residual(1.0, view(E), view(AP)), E)
+    rel = math.sqrt(rt) / norm_b
+    return ShardedResult(view(X), c0, c1, rel <= tol, it)

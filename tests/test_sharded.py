@@ -1,0 +1,131 @@
+"""Column-sharded alternate decoder: the distributed algorithm
+against the single-process oracle.  CPU: world size 2 over gloo with the
+NumPy block double.  GPU: three in-process ranks on one device (separate
+contexts, thread collectives) through the CUDA block primitives."""
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+
+from helpers import knn_laplacian, rel
+from oracle import pyoracle as O
+
+
+def _case(p=48, n=37, rr=12, rc=9, seed=5):
+    Lr, Lc = knn_laplacian(p, 3, 6, seed), knn_laplacian(n, 3, 6, seed + 1)
+    plan = O.draw_plan(p, n, rr, rc, seed=seed)
+    Xt = np.random.default_rng(seed).standard_normal((rr, rc))
+    return Lr, Lc, plan, Xt
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1602_02070_b200.sharded import TorchCollectives, alternate_decode_sharded, column_blocks
+    from shard_double import NumpyBlockBackend
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    Lr, Lc, plan, Xt = _case()
+    _, blocks = column_blocks(plan.n, world)
+    c0, c1 = blocks[rank]
+    be = NumpyBlockBackend(plan, Lr, Lc, 1.0 / 0.3, 1.0 / 0.4, c0, c1)
+    coll = TorchCollectives()
+    res = alternate_decode_sharded(Xt, plan, be, coll, lambda k: torch.zeros(k, dtype=torch.float64),
+                                   tol=1e-10, max_iter=400)
+    out[rank] = (c0, c1, res.X_block.numpy().copy(), res.iterations, res.converged)
+    dist.destroy_process_group()
+
+
+def test_sharded_decoder_gloo_world2_matches_oracle():
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, out)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+        assert pr.exitcode == 0
+    Lr, Lc, plan, Xt = _case()
+    ro = O.alternate_decode(Xt, plan, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 400)
+    X = np.zeros((plan.p, plan.n))
+    for r in range(2):
+        c0, c1, blk, it, conv = out[r]
+        X[:, c0:c1] = blk.reshape((plan.p, c1 - c0), order="F")
+        assert abs(it - ro.iterations) <= 1 and conv == ro.converged
+    assert rel(X, ro.X) <= 1e-9
+
+
+def test_column_blocks_cover_and_pad():
+    from paper_1602_02070_b200.sharded import column_blocks
+
+    for n, g in [(37, 2), (10, 4), (8, 8), (5, 8)]:
+        w, blocks = column_blocks(n, g)
+        assert len(blocks) == g and w * g >= n
+        cols = [c for a, b in blocks for c in range(a, b)]
+        assert cols == list(range(n))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_sharded_decoder_cuda_three_ranks_one_gpu(prec):
+    import torch
+
+    import paper_1602_02070_b200 as P
+    from helpers import to_device
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200.sharded import CudaBlockBackend, alternate_decode_sharded, column_blocks
+    from shard_double import ThreadCollectives
+
+    Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
+    world = 3
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    code = N.F64 if prec == "f64" else N.F32
+    shared = ThreadCollectives.Shared(world)
+    _, blocks = column_blocks(plan.n, world)
+    out, errs = {}, []
+
+    def worker(rank):
+        try:
+            ctx = P.Context(0)
+            dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+            c0, c1 = blocks[rank]
+            be = CudaBlockBackend(ctx, code, plan, dLr, dLc, 1.0 / 0.3, 1.0 / 0.4, c0, c1)
+            Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), dtype=dt, device="cuda").t()
+            res = alternate_decode_sharded(Xt_d, plan, be, ThreadCollectives(shared, rank),
+                                           lambda k: torch.zeros(k, dtype=dt, device="cuda"), tol=1e-10, max_iter=300)
+            torch.cuda.synchronize()
+            out[rank] = (c0, c1, res.X_block.cpu().numpy().astype(np.float64), res.iterations)
+            be.close()
+        except Exception as e:  # surface in the main thread
+            errs.append(e)
+            shared.barrier.abort()
+
+    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(300)
+    assert not errs, errs
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
+    X = np.zeros((plan.p, plan.n))
+    for r in range(world):
+        c0, c1, blk, it = out[r]
+        X[:, c0:c1] = blk.reshape((plan.p, c1 - c0), order="F")
+        assert abs(it - ro.iterations) <= (1 if prec == "f64" else 300)
+    assert rel(X, ro.X) <= (1e-9 if prec == "f64" else 1e-4)
