@@ -212,6 +212,11 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
                                 const cpcag_decoder_config* cfg, void* X, int* converged,
                                 int64_t* iterations);
 
+/* 3xTF32 tensor-core Gram matrix (tcgen05.mma kind::tf32) of n points given
+ * as the rows of the n x d row-major fp64 array P; G is n x n row-major fp32.
+ * The kNN filter stage's arithmetic, exposed for verification. */
+int cpcag_cuda_gram_tf32x3(cpcag_ctx ctx, const double* P, int64_t n, int64_t d, float* G);
+
 /* ------------------------------------------------------------------ column-sharded decoder */
 /* Local primitives of the alternate decoder for one column block
  * [c_begin, c_end) of a column-sharded multi-GPU solve: the

@@ -105,6 +105,7 @@ SIGNATURES = {
     "cpcag_cuda_decoder_block_apply": (C.c_int, [vp, vp, vp, dp]),
     "cpcag_cuda_cg_residual": (C.c_int, [vp, C.c_int, i64, dbl, vp, vp, dp]),
     "cpcag_cuda_cg_update": (C.c_int, [vp, C.c_int, i64, dbl, dbl, vp, vp, vp]),
+    "cpcag_cuda_gram_tf32x3": (C.c_int, [vp, vp, i64, i64, vp]),
     "cpcag_cuda_run_pipeline": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp,
                                           C.POINTER(PipelineConfigC), vp, vp, vp, vp, vp,
                                           C.POINTER(PipelineReportC)]),

@@ -190,6 +190,15 @@ struct OutView {
 
 inline void sync(Ctx* c) { CUDA_OK(cudaStreamSynchronize(c->stream)); }
 
+// Raises (never lowers) a kernel's dynamic shared-memory limit.  The limit is
+// process-wide state, so concurrent contexts must not shrink it under each
+// other's launches.
+void ensure_smem_impl(const void* func, size_t bytes);
+template <class F>
+inline void ensure_smem(F* func, size_t bytes) {
+  ensure_smem_impl(reinterpret_cast<const void*>(func), bytes);
+}
+
 // Host-side phase tracing (CPCAG_TRACE=1): synchronises and prints wall time
 // since the previous mark.  Off by default; used to find host overheads.
 void trace_mark(Ctx* c, const char* what);

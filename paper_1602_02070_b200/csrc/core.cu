@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -45,6 +46,21 @@ double HostRng::gaussian() {
   spare = rad * std::sin(tau * b);
   has_spare = true;
   return rad * std::cos(tau * b);
+}
+
+void ensure_smem_impl(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> seen;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : seen)
+    if (e.first == func) {
+      if (e.second >= bytes) return;
+      ensure_smem(func, bytes);
+      e.second = bytes;
+      return;
+    }
+  ensure_smem(func, bytes);
+  seen.push_back({func, bytes});
 }
 
 void trace_mark(Ctx* c, const char* what) {
@@ -539,8 +555,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   st.zero(c);
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
   if (small_smem <= 200 * 1024 && A->nnz <= 4096) {
-    CUDA_OK(cudaFuncSetAttribute(power_iter_small_k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(small_smem)));
+    ensure_smem(power_iter_small_k, small_smem);
     {
       KScope ks_(c, "power_iter");
       power_iter_small_k<<<1, 512, small_smem, c->stream>>>(n, A->rp, A->ci, A->v, v.p, tol, max_iter, st.p);
@@ -563,7 +578,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   size_t smem = v_in_smem ? static_cast<size_t>(n) * 8 : 0;
   int slice_in_smem = smem + static_cast<size_t>(max_slice) * 12 + 16 <= budget ? 1 : 0;
   if (slice_in_smem) smem += static_cast<size_t>(max_slice) * 12 + 16;
-  CUDA_OK(cudaFuncSetAttribute(power_iter_coop_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  ensure_smem(power_iter_coop_k, smem);
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 256, smem));
   if (per_sm < 1) invalid("power iteration: kernel does not fit on an SM");

@@ -535,17 +535,15 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned lc_blocks = static_cast<unsigned>((p + kPanel - 1) / kPanel);
   if (split) {
     Yr.alloc(c, N);
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_lr_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lr_smem)));
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_lc_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lc_smem)));
+    ensure_smem(cg_apply_lr_k<T>, lr_smem);
+    ensure_smem(cg_apply_lc_k<T>, lc_smem);
     if (part.n < lc_blocks) part.alloc(c, lc_blocks);
   } else if (variant == "staged") {
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(staged_smem)));
+    ensure_smem(cg_apply_staged_k<T>, staged_smem);
   }
   auto launch_reg = [&](auto rmax_tag) {
     constexpr int R = decltype(rmax_tag)::value;
-    CUDA_OK(cudaFuncSetAttribute(cg_apply_reg_k<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(reg_smem)));
+    ensure_smem(cg_apply_reg_k<T, R>, reg_smem);
     cg_apply_reg_k<T, R><<<gs, kBlock, reg_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p, AP.p,
                                                               part.p, st.p);
   };
@@ -770,11 +768,9 @@ extern "C" int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int
     blk->smem = static_cast<size_t>(max_er + max_ec) * (es + sizeof(int)) + 16;
     if (blk->smem > 200 * 1024) invalid("decoder block: operator slice exceeds shared memory");
     if (precision == CPCAG_F64)
-      CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(blk->smem)));
+      ensure_smem(cg_apply_staged_k<double>, blk->smem);
     else
-      CUDA_OK(cudaFuncSetAttribute(cg_apply_staged_k<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(blk->smem)));
+      ensure_smem(cg_apply_staged_k<float>, blk->smem);
     const size_t nparts = std::max<size_t>(static_cast<size_t>(blk->grid.x) * blk->grid.y,
                                            stride_blocks(c, std::max<i64>(p * nb_cols, 1)));
     blk->part.alloc(c, nparts);

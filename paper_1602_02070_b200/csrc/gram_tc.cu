@@ -1,0 +1,254 @@
+// gram_tc.cu -- 3xTF32 Gram tiles on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM), the filter stage of the
+// certified kNN search (knn.cu).
+//
+// Each point x is split as x = hi + lo with hi = tf32(x), lo = tf32(x - hi);
+// g_ij ~ hi_i.hi_j + hi_i.lo_j + lo_i.hi_j (three MMAs into one fp32
+// accumulator), which carries ~fp32 accuracy.  The approximation only
+// filters candidates: the neighbour lists are re-ranked with the canonical
+// fp64 distance, so results stay bit-exact (see knn.cu).
+//
+// Tile: 128 query rows x 128 candidate rows per CTA, K staged 32 at a time.
+// Shared memory holds K-major operand tiles in the canonical SWIZZLE_NONE
+// "core matrix" layout: an 8-row x 16-byte core matrix is 128 contiguous
+// bytes; the 8 core matrices of a 32-wide k chunk follow each other (LBO =
+// 128 B) and 8-row groups are 1024 B apart (SBO).  One elected thread issues
+// the MMAs; tcgen05.commit arrives on an mbarrier that every thread waits on
+// before the shared-memory stage is refilled.
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace cpcag_cuda {
+
+namespace tc {
+
+constexpr int kM = 128;                 // query rows per tile (UMMA M)
+constexpr int kN = 128;                 // candidate rows per tile (UMMA N)
+constexpr int kKc = 32;                 // k per stage (one 128-byte row per point)
+constexpr int kTileBytes = kM * kKc * 4;  // 16 KiB per operand tile
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_NONE.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm100)
+  // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// 32 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+// Copies rows [row0, row0 + 128) x k [k0, k0 + 32) of a point-major fp32
+// matrix (leading dimension ld, rows >= nrows read as zero) into the core
+// matrix layout at dst.  128 threads, 16-byte chunks.
+__device__ __forceinline__ void stage_tile(unsigned char* dst, const float* __restrict__ src, i64 ld, i64 nrows,
+                                           i64 row0, i64 k0) {
+#pragma unroll
+  for (int q = 0; q < (kM * 8) / 128; ++q) {
+    const int id = threadIdx.x + 128 * q;
+    const int r = id >> 3, kc = id & 7;
+    const i64 gr = row0 + r;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (gr < nrows) v = *reinterpret_cast<const float4*>(src + gr * ld + k0 + kc * 4);
+    *reinterpret_cast<float4*>(dst + ((r >> 3) * 8 + kc) * 128 + (r & 7) * 16) = v;
+  }
+}
+
+}  // namespace tc
+
+// G(i, j) for a 128 x 128 tile: 3xTF32 Gram of points i (rows of H/L) and j.
+// H, L: n x dp fp32 point-major (dp multiple of 32).  G row-major n x n.
+__global__ void __launch_bounds__(128) gram_tf32x3_k(const float* __restrict__ H, const float* __restrict__ L, i64 n,
+                                                     i64 dp, float* __restrict__ G) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* Ah = smem;
+  unsigned char* Al = smem + kTileBytes;
+  unsigned char* Bh = smem + 2 * kTileBytes;
+  unsigned char* Bl = smem + 3 * kTileBytes;
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kM, j0 = static_cast<i64>(blockIdx.y) * kN;
+  if (warp == 0) tmem_alloc(&tmem_base, kN);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t idesc = idesc_tf32(kM, kN);
+  uint32_t phase = 0;
+  for (i64 k0 = 0; k0 < dp; k0 += kKc) {
+    stage_tile(Ah, H, dp, n, i0, k0);
+    stage_tile(Al, L, dp, n, i0, k0);
+    stage_tile(Bh, H, dp, n, j0, k0);
+    stage_tile(Bl, L, dp, n, j0, k0);
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_after();
+      const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
+#pragma unroll
+      for (int kk = 0; kk < kKc / 8; ++kk) {
+        const uint32_t off = kk * 256;  // two core matrices (8 tf32) per MMA
+        const uint32_t acc = (k0 > 0 || kk > 0) ? 1u : 0u;
+        mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, acc);
+        mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bl + off, 128, 1024), idesc, 1u);
+        mma_tf32(tmem, umma_desc(al + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, 1u);
+      }
+      mma_commit(&mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1u;
+    fence_after();
+  }
+  // Epilogue: warp w owns TMEM lanes [32w, 32w + 32) = rows i0 + 32w + lane.
+  const i64 gi = i0 + 32 * warp + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < kN; c0 += 32) {
+    float v[32];
+    tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
+    if (gi < n)
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const i64 gj = j0 + c0 + q;
+        if (gj < n) G[gi * n + gj] = v[q];
+      }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kN);
+}
+
+// hi = tf32(x) (round to nearest), lo = tf32(x - hi); rows padded to dp.
+__global__ void split_tf32_k(const double* __restrict__ Pm, i64 n, i64 d, i64 dp, float* __restrict__ H,
+                             float* __restrict__ L) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= n * dp) return;
+  const i64 i = t / dp, k = t % dp;
+  float h = 0.f, l = 0.f;
+  if (k < d) {
+    const float x = static_cast<float>(Pm[i * d + k]);
+    uint32_t hb, lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+    h = __uint_as_float(hb);
+    const float r = x - h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(r));
+    l = __uint_as_float(lb);
+  }
+  H[t] = h;
+  L[t] = l;
+}
+
+size_t gram_tc_smem() { return 4 * static_cast<size_t>(tc::kTileBytes); }
+
+// H/L split of point-major fp64 points (n x d) into padded fp32 arrays.
+void split_points(Ctx* c, const double* Pm, i64 n, i64 d, i64 dp, float* H, float* L) {
+  split_tf32_k<<<blocks_for(std::max<i64>(n * dp, 1)), kBlock, 0, c->stream>>>(Pm, n, d, dp, H, L);
+  launched(c);
+}
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+// Test/diagnostic primitive: the full 3xTF32 Gram matrix of n points (point
+// i = row i of the n x d row-major fp64 array P), row-major fp32 n x n.
+extern "C" int cpcag_cuda_gram_tf32x3(cpcag_ctx ctx, const double* P, int64_t n, int64_t d, float* G) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (n < 0 || d < 0) invalid("gram: negative size");
+    InView<double> pin(c, P, static_cast<size_t>(n * d));
+    OutView<float> gout(c, G, static_cast<size_t>(n * n));
+    const i64 dp = std::max<i64>(32, (d + 31) / 32 * 32);
+    DevBuf<float> H(c, std::max<i64>(n * dp, 1)), L(c, std::max<i64>(n * dp, 1));
+    if (n) {
+      split_points(c, pin.d, n, d, dp, H.p, L.p);
+      const size_t smem = gram_tc_smem();
+      ensure_smem(gram_tf32x3_k, smem);
+      dim3 g(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>((n + 127) / 128));
+      {
+        KScope ks_(c, "gram_tf32x3");
+        gram_tf32x3_k<<<g, 128, smem, c->stream>>>(H.p, L.p, n, dp, gout.d);
+        launched(c);
+      }
+    }
+    gout.flush(c);
+    sync(c);
+  });
+}

@@ -396,7 +396,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   DevBuf<int> dup(c, n);
   dup.zero(c);
   dim3 g(static_cast<unsigned>(n_tiles), static_cast<unsigned>(splits));
-  CUDA_OK(cudaFuncSetAttribute(knn_tile_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kKnnSmem)));
+  ensure_smem(knn_tile_k, kKnnSmem);
   {
     KScope ks_(c, "knn_tile");
     knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,

@@ -262,3 +262,24 @@ def test_pipeline_stage_error_is_tagged(P, ctx):
     cfg = P.PipelineConfig(knn=50, a=2, b=2)
     with pytest.raises(RuntimeError, match="stage graphs: knn graph: need at least K\\+1 points"):
         P.run_pipeline(Y, cfg, ctx=ctx)
+
+
+# ------------------------------------------------------------------ tensor-core Gram
+@pytest.mark.parametrize("n,d", [(128, 32), (300, 70), (517, 512)])
+def test_gram_tf32x3_tensor_cores(P, ctx, n, d):
+    """tcgen05 kind::tf32 3xTF32 Gram: error within the filter's bound."""
+    import ctypes
+
+    from paper_1602_02070_b200 import _native as N
+
+    X = np.random.default_rng(n + d).standard_normal((n, d))
+    G = np.empty((n, n), np.float32)
+    Xc = np.ascontiguousarray(X)
+    N.check(N.lib().cpcag_cuda_gram_tf32x3(ctx.handle, Xc.ctypes.data, n, d, G.ctypes.data))
+    ref = X @ X.T
+    nrm = np.linalg.norm(X, axis=1)
+    bound = (d * 2.0 ** -23 + 2.0 ** -19) * np.outer(nrm, nrm)
+    err = np.abs(G.astype(np.float64) - ref)
+    assert np.all(err <= bound), float((err / bound).max())
+    # and far better than plain TF32 would be
+    assert err.max() <= 1e-4 * np.abs(ref).max()
