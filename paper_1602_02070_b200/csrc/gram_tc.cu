@@ -15,6 +15,8 @@
 // 128 B) and 8-row groups are 1024 B apart (SBO).  One elected thread issues
 // the MMAs; tcgen05.commit arrives on an mbarrier that every thread waits on
 // before the shared-memory stage is refilled.
+#include <math_constants.h>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -194,6 +196,126 @@ __global__ void __launch_bounds__(128) gram_tf32x3_k(const float* __restrict__ H
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, kN);
 }
+
+// ------------------------------------------------------------------ certified kNN filter
+// One CTA = 128 query points (one TMEM lane each) x a range of 128-point
+// candidate tiles.  For every candidate tile the three MMAs of each k chunk
+// accumulate G~ in TMEM; the epilogue turns row i's 128 values into
+// approximate distances d~ = (sq_i + sq_j) - 2 G~ (fp64, sq canonical) and
+// keeps the kKc smallest (d~, j) per point in shared memory.  knn.cu merges
+// the lists, applies the rigorous error window and re-ranks exactly.
+constexpr int kCand = 32;  // candidates kept per point per split
+
+__global__ void __launch_bounds__(128) knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
+                                                       const double* __restrict__ sq, i64 n, i64 dp,
+                                                       int tiles_per_split, float* __restrict__ cand_d,
+                                                       int* __restrict__ cand_j) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  unsigned char* Ah = smem;
+  unsigned char* Al = smem + kTileBytes;
+  unsigned char* Bh = smem + 2 * kTileBytes;
+  unsigned char* Bl = smem + 3 * kTileBytes;
+  float* lst_d = reinterpret_cast<float*>(smem + 4 * kTileBytes);  // [kCand][128]
+  int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);          // [kCand][128]
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kM;
+  const i64 n_tiles = (n + kN - 1) / kN;
+  const i64 jt0 = static_cast<i64>(blockIdx.y) * tiles_per_split;
+  const i64 jt1 = min(n_tiles, jt0 + tiles_per_split);
+  if (warp == 0) tmem_alloc(&tmem_base, kN);
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  const int r = threadIdx.x;  // this thread's query row (TMEM lane r)
+  for (int q = 0; q < kCand; ++q) {
+    lst_d[q * kM + r] = CUDART_INF_F;
+    lst_j[q * kM + r] = INT32_MAX;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t idesc = idesc_tf32(kM, kN);
+  const i64 gi = i0 + r;
+  const double sqi = gi < n ? sq[gi] : 0.0;
+  float thr = CUDART_INF_F;  // current kCand-th best
+  uint32_t phase = 0;
+  for (i64 jt = jt0; jt < jt1; ++jt) {
+    const i64 j0 = jt * kN;
+    for (i64 k0 = 0; k0 < dp; k0 += kKc) {
+      stage_tile(Ah, H, dp, n, i0, k0);
+      stage_tile(Al, L, dp, n, i0, k0);
+      stage_tile(Bh, H, dp, n, j0, k0);
+      stage_tile(Bl, L, dp, n, j0, k0);
+      fence_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        fence_after();
+        const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
+#pragma unroll
+        for (int kk = 0; kk < kKc / 8; ++kk) {
+          const uint32_t off = kk * 256;
+          const uint32_t acc = (k0 > 0 || kk > 0) ? 1u : 0u;
+          mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, acc);
+          mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bl + off, 128, 1024), idesc, 1u);
+          mma_tf32(tmem, umma_desc(al + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, 1u);
+        }
+        mma_commit(&mbar);
+      }
+      mbar_wait(&mbar, phase);
+      phase ^= 1u;
+      fence_after();
+    }
+    // epilogue for this candidate tile
+#pragma unroll 1
+    for (int c0 = 0; c0 < kN; c0 += 32) {
+      float v[32];
+      tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
+      if (gi < n) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const i64 gj = j0 + c0 + q;
+          if (gj >= n || gj == gi) continue;
+          const double dd = (sqi + sq[gj]) - 2.0 * static_cast<double>(v[q]);
+          const float df = static_cast<float>(dd);
+          if (!(df < thr)) continue;
+          // insert (df, gj) into the sorted list (ties: lower index first)
+          int pos = kCand - 1;
+          while (pos > 0) {
+            const float pd = lst_d[(pos - 1) * kM + r];
+            if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
+            lst_d[pos * kM + r] = pd;
+            lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
+            --pos;
+          }
+          lst_d[pos * kM + r] = df;
+          lst_j[pos * kM + r] = static_cast<int>(gj);
+          thr = lst_d[(kCand - 1) * kM + r];
+        }
+      }
+    }
+    fence_before();
+    __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
+    fence_after();
+  }
+  if (gi < n) {
+    float* od = cand_d + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
+    int* oj = cand_j + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
+    for (int q = 0; q < kCand; ++q) {
+      od[q] = lst_d[q * kM + r];
+      oj[q] = lst_j[q * kM + r];
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, kN);
+}
+
+size_t knn_tc_smem() { return 4 * static_cast<size_t>(tc::kTileBytes) + kCand * tc::kM * (sizeof(float) + sizeof(int)); }
 
 // hi = tf32(x) (round to nearest), lo = tf32(x - hi); rows padded to dp.
 __global__ void split_tf32_k(const double* __restrict__ Pm, i64 n, i64 d, i64 dp, float* __restrict__ H,

@@ -22,7 +22,9 @@
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
+#include <cstdlib>
 #include <memory>
+#include <string>
 
 #include "common.cuh"
 
@@ -58,10 +60,13 @@ __device__ __forceinline__ bool lex_less(double da, int ja, double db, int jb) {
 
 // One CTA: 64 query points x candidate tiles [jt0, jt1).  Output: per query
 // point the K best (d2, j) of the range, ascending, into cand[split].
+// qidx (optional): the query points are qidx[0..nq) instead of 0..n-1 (used
+// for the rows the tensor-core filter could not certify); outputs are indexed
+// by query position.
 __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm, const double* __restrict__ sq,
                                                   i64 n, i64 d, int K, int tiles_per_split,
                                                   double* __restrict__ cand_d, int* __restrict__ cand_j,
-                                                  int* __restrict__ dup) {
+                                                  int* __restrict__ dup, const int* __restrict__ qidx, i64 nq) {
   extern __shared__ __align__(16) unsigned char smem[];
   double(*As)[kTile + 1] = reinterpret_cast<double(*)[kTile + 1]>(smem);
   double(*Bs)[kTile + 1] = As + kKc;
@@ -99,7 +104,8 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
         const int idx = tid + 256 * q;
         const int pt = idx / kKc, kk = idx % kKc;
         const i64 k = k0 + kk;
-        const i64 ia = i0 + pt, jb = j0 + pt;
+        const i64 qa = i0 + pt, jb = j0 + pt;
+        const i64 ia = qa < nq ? (qidx ? qidx[qa] : qa) : n;
         As[kk][pt] = (ia < n && k < d) ? Pm[ia * d + k] : 0.0;
         Bs[kk][pt] = (jb < n && k < d) ? Pm[jb * d + k] : 0.0;
       }
@@ -124,7 +130,8 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const int li = ty + 16 * r, lj = tx + 16 * s;
-        const i64 gi = i0 + li, gj = j0 + lj;
+        const i64 qi = i0 + li, gj = j0 + lj;
+        const i64 gi = qi < nq ? (qidx ? qidx[qi] : qi) : n;
         double v = CUDART_INF;
         if (gi < n && gj < n && gi != gj) {
           const double t = __dsub_rn(__dadd_rn(sq[gi], sq[gj]), __dmul_rn(2.0, acc[r][s]));
@@ -134,7 +141,8 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
       }
     __syncthreads();
     if (tid < kTile) {
-      const i64 gi = i0 + tid;
+      const i64 qi = i0 + tid;
+      const i64 gi = qi < nq ? (qidx ? qidx[qi] : qi) : n;
       if (gi < n) {
         for (int lj = 0; lj < kTile; ++lj) {
           const double v = Dt[tid][lj];
@@ -162,10 +170,10 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
     __syncthreads();
   }
   if (tid < kTile) {
-    const i64 gi = i0 + tid;
-    if (gi < n) {
-      double* od = cand_d + (static_cast<i64>(split) * n + gi) * K;
-      int* oj = cand_j + (static_cast<i64>(split) * n + gi) * K;
+    const i64 qi = i0 + tid;
+    if (qi < nq) {
+      double* od = cand_d + (static_cast<i64>(split) * nq + qi) * K;
+      int* oj = cand_j + (static_cast<i64>(split) * nq + qi) * K;
       for (int q = 0; q < K; ++q) {
         od[q] = best_d[tid][q];
         oj[q] = best_j[tid][q];
@@ -177,9 +185,12 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
 // Merge the per-split sorted lists of each point; mean d2 in ascending order.
 __global__ void knn_merge_k(i64 n, int K, int splits, const double* __restrict__ cand_d,
                             const int* __restrict__ cand_j, int64_t* __restrict__ nbr,
-                            double* __restrict__ nbr_d2, double* __restrict__ mean_d2) {
-  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+                            double* __restrict__ nbr_d2, double* __restrict__ mean_d2,
+                            const int* __restrict__ qidx) {
+  const i64 qq = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (qq >= n) return;
+  const i64 i = qq;                         // position in the candidate arrays
+  const i64 o = qidx ? qidx[qq] : qq;       // output row
   int pos[64];
   const int S = splits < 64 ? splits : 64;
   for (int s = 0; s < S; ++s) pos[s] = 0;
@@ -200,11 +211,11 @@ __global__ void knn_merge_k(i64 n, int K, int splits, const double* __restrict__
       }
     }
     pos[bs]++;
-    nbr[i * K + q] = bj;
-    nbr_d2[i * K + q] = bd;
+    nbr[o * K + q] = bj;
+    nbr_d2[o * K + q] = bd;
     m = __dadd_rn(m, bd);
   }
-  mean_d2[i] = m;
+  mean_d2[o] = m;
 }
 
 // sigma2 = sum_i (mean_i / K) / n, summed in point order (graph.cpp:104-107).
@@ -362,7 +373,154 @@ struct KnnLists {
   DevBuf<double> d2, mean;
   i64 n = 0, d = 0;
   DevBuf<double> Pm;
+  i64 tc_rows = 0;  // points certified by the tensor-core filter
 };
+
+// ---- tensor-core filter + certified exact re-rank ------------------------
+constexpr int kCandTc = 32;  // == kCand in gram_tc.cu
+
+void split_points(Ctx* c, const double* Pm, i64 n, i64 d, i64 dp, float* H, float* L);  // gram_tc.cu
+size_t knn_tc_smem();
+__global__ void knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
+                                const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split,
+                                float* __restrict__ cand_d, int* __restrict__ cand_j);
+
+__global__ void max_norm_k(const double* __restrict__ sq, i64 n, unsigned long long* out) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(sqrt(sq[i]))));
+}
+
+// Merge the per-split sorted approximate lists of each point (first kCandTc).
+__global__ void tc_merge_k(i64 n, int splits, const float* __restrict__ cd, const int* __restrict__ cj,
+                           float* __restrict__ md, int* __restrict__ mj) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int pos[64];
+  for (int s = 0; s < splits; ++s) pos[s] = 0;
+  for (int q = 0; q < kCandTc; ++q) {
+    int bs = -1;
+    float bd = CUDART_INF_F;
+    int bj = INT32_MAX;
+    for (int s = 0; s < splits; ++s) {
+      if (pos[s] >= kCandTc) continue;
+      const i64 at = (static_cast<i64>(s) * n + i) * kCandTc + pos[s];
+      const float dv = cd[at];
+      const int jv = cj[at];
+      if (bs < 0 || dv < bd || (dv == bd && jv < bj)) {
+        bs = s;
+        bd = dv;
+        bj = jv;
+      }
+    }
+    pos[bs]++;
+    md[i * kCandTc + q] = bd;
+    mj[i * kCandTc + q] = bj;
+  }
+}
+
+// One warp per point, lane q = q-th approximate candidate.  The window
+// [.., D_K + 2E] with E a rigorous bound of the 3xTF32 distance error
+// contains every true top-K neighbour; if the whole list lies inside the
+// window some candidate may be missing and the point is deferred to the
+// exact path (overflow[i] = 1).  Otherwise the candidates inside the window
+// get the canonical fp64 distance (sequential k, no FMA) and the K smallest
+// (d2, j) are selected exactly.
+__global__ void tc_rerank_k(const double* __restrict__ Pm, const double* __restrict__ sq, i64 n, i64 d, int K,
+                            double cg, const unsigned long long* __restrict__ maxnorm_bits,
+                            const float* __restrict__ md, const int* __restrict__ mj, int64_t* __restrict__ nbr,
+                            double* __restrict__ nbr_d2, double* __restrict__ mean_d2, int* __restrict__ overflow,
+                            int* __restrict__ dup) {
+  const i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const double maxnorm = __longlong_as_double(static_cast<long long>(*maxnorm_bits));
+  const float dq = md[i * kCandTc + lane];
+  const int jq = mj[i * kCandTc + lane];
+  const double DK = static_cast<double>(__shfl_sync(0xffffffffu, dq, K - 1));
+  const double last = static_cast<double>(__shfl_sync(0xffffffffu, dq, kCandTc - 1));
+  const double E = 2.0 * cg * sqrt(sq[i]) * maxnorm;
+  const double W = DK + fabs(DK) * 0x1.0p-22 + 2.0 * E;  // + float rounding of the stored d~
+  const bool ovf = last - fabs(last) * 0x1.0p-22 <= W;
+  if (ovf) {
+    if (lane == 0) overflow[i] = 1;
+    return;
+  }
+  const double dql = static_cast<double>(dq) - fabs(static_cast<double>(dq)) * 0x1.0p-22;
+  double ex = CUDART_INF;
+  if (jq != INT32_MAX && dql <= W) {
+    const double* a = Pm + i * d;
+    const double* b = Pm + static_cast<i64>(jq) * d;
+    double g = 0.0;
+    for (i64 k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(a[k], b[k]));
+    const double t = __dsub_rn(__dadd_rn(sq[i], sq[jq]), __dmul_rn(2.0, g));
+    ex = t > 0.0 ? t : 0.0;
+    if (ex == 0.0 && jq < i) {
+      bool same = true;
+      for (i64 k = 0; k < d && same; ++k) same = a[k] == b[k];
+      if (same) dup[i] = 1;
+    }
+  }
+  // K rounds of a lexicographic warp argmin.
+  double m = 0.0;
+  int jcur = ex < CUDART_INF ? jq : INT32_MAX;
+  for (int q = 0; q < K; ++q) {
+    double bv = ex;
+    int bj = jcur;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov < bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    if (lane == 0) {
+      nbr[i * K + q] = bj;
+      nbr_d2[i * K + q] = bv;
+    }
+    m = __dadd_rn(m, bv);
+    if (jcur == bj) {
+      ex = CUDART_INF;
+      jcur = INT32_MAX;
+    }
+  }
+  if (lane == 0) mean_d2[i] = m;
+}
+
+// Exact fp64 tiled search for the queries qidx[0..nq) (all points when qidx
+// is null), writing their rows of nbr / nbr_d2 / mean.
+void knn_exact_rows(Ctx* c, const double* Pm, const double* sq, i64 n, i64 d, i64 K, const int* qidx, i64 nq,
+                    int* dup, int64_t* nbr, double* nbr_d2, double* mean) {
+  if (nq == 0) return;
+  const i64 q_tiles = (nq + kTile - 1) / kTile;
+  const i64 n_tiles = (n + kTile - 1) / kTile;
+  i64 splits = std::max<i64>(1, (2 * static_cast<i64>(c->num_sms) + q_tiles - 1) / q_tiles);
+  splits = std::min<i64>({splits, n_tiles, 64});
+  const i64 tps = (n_tiles + splits - 1) / splits;
+  splits = (n_tiles + tps - 1) / tps;
+  DevBuf<double> cand_d(c, splits * nq * K);
+  DevBuf<int> cand_j(c, splits * nq * K);
+  dim3 g(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits));
+  ensure_smem(knn_tile_k, kKnnSmem);
+  {
+    KScope ks_(c, "knn_tile");
+    knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(Pm, sq, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,
+                                                cand_j.p, dup, qidx, nq);
+    launched(c);
+  }
+  knn_merge_k<<<blocks_for(nq, 128), 128, 0, c->stream>>>(nq, static_cast<int>(K), static_cast<int>(splits),
+                                                           cand_d.p, cand_j.p, nbr, nbr_d2, mean, qidx);
+  launched(c);
+}
+
+static bool tc_knn_enabled(i64 n, i64 d, i64 K) {
+  const char* e = std::getenv("CPCAG_KNN");
+  if (e && std::string(e) == "exact") return false;
+  const bool forced = e && std::string(e) == "tc";
+  if (K + 4 > kCandTc || d < 1) return false;
+  return forced || (n >= 4096 && d <= 1024);
+}
 
 template <typename T>
 void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K, KnnLists* out) {
@@ -384,24 +542,66 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   }
   sqnorm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(out->Pm.p, n, d, sq.p);
   launched(c);
-
-  const i64 n_tiles = (n + kTile - 1) / kTile;
-  // Split the candidate range so the grid covers >= 2 waves of 148 SMs.
-  i64 splits = std::max<i64>(1, (2 * static_cast<i64>(c->num_sms) + n_tiles - 1) / n_tiles);
-  splits = std::min<i64>({splits, n_tiles, 64});
-  const i64 tps = (n_tiles + splits - 1) / splits;
-  splits = (n_tiles + tps - 1) / tps;
-  DevBuf<double> cand_d(c, splits * n * K);
-  DevBuf<int> cand_j(c, splits * n * K);
+  out->nbr.alloc(c, n * K);
+  out->d2.alloc(c, n * K);
+  out->mean.alloc(c, n);
   DevBuf<int> dup(c, n);
   dup.zero(c);
-  dim3 g(static_cast<unsigned>(n_tiles), static_cast<unsigned>(splits));
-  ensure_smem(knn_tile_k, kKnnSmem);
-  {
-    KScope ks_(c, "knn_tile");
-    knn_tile_k<<<g, 256, kKnnSmem, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), static_cast<int>(tps), cand_d.p,
-                                         cand_j.p, dup.p);
+  out->tc_rows = 0;
+  if (tc_knn_enabled(n, d, K)) {
+    // Filter on the tensor cores, certify, re-rank exactly.
+    const i64 dp = std::max<i64>(32, (d + 31) / 32 * 32);
+    DevBuf<float> H(c, n * dp), L(c, n * dp);
+    split_points(c, out->Pm.p, n, d, dp, H.p, L.p);
+    const i64 q_tiles = (n + 127) / 128, n_tiles = (n + 127) / 128;
+    i64 splits = std::max<i64>(1, (2 * static_cast<i64>(c->num_sms) + q_tiles - 1) / q_tiles);
+    splits = std::min<i64>({splits, n_tiles, 64});
+    const i64 tps = (n_tiles + splits - 1) / splits;
+    splits = (n_tiles + tps - 1) / tps;
+    DevBuf<float> cd(c, splits * n * kCandTc), md(c, n * kCandTc);
+    DevBuf<int> cj(c, splits * n * kCandTc), mj(c, n * kCandTc), ovf(c, n);
+    ovf.zero(c);
+    const size_t smem = knn_tc_smem();
+    ensure_smem(knn_tc_filter_k, smem);
+    {
+      KScope ks_(c, "knn_tc_filter");
+      knn_tc_filter_k<<<dim3(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits)), 128, smem, c->stream>>>(
+          H.p, L.p, sq.p, n, dp, static_cast<int>(tps), cd.p, cj.p);
+      launched(c);
+    }
+    tc_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(splits), cd.p, cj.p, md.p, mj.p);
     launched(c);
+    DevBuf<unsigned long long> mxn(c, 1);
+    mxn.zero(c);
+    max_norm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(sq.p, n, mxn.p);
+    launched(c);
+    // Rigorous bound on |G~ - G| / (|x_i| |x_j|): split error 3 * 2^-22 plus
+    // fp32 accumulation of 3 d exact tf32 products, 2^-23 per addition
+    // (truncating accumulation), doubled for margin.
+    const double cg = 2.0 * (3.0 + 3.0 * static_cast<double>(d)) * 0x1.0p-23;
+    {
+      KScope ks_(c, "knn_tc_rerank");
+      tc_rerank_k<<<blocks_for(n * 32, 256), 256, 0, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), cg,
+                                                                 mxn.p, md.p, mj.p, out->nbr.p, out->d2.p,
+                                                                 out->mean.p, ovf.p, dup.p);
+      launched(c);
+    }
+    std::vector<int> of(static_cast<size_t>(n));
+    CUDA_OK(cudaMemcpyAsync(of.data(), ovf.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    std::vector<int> rows;
+    for (i64 i = 0; i < n; ++i)
+      if (of[i]) rows.push_back(static_cast<int>(i));
+    out->tc_rows = n - static_cast<i64>(rows.size());
+    if (!rows.empty()) {
+      DevBuf<int> qd(c, rows.size());
+      CUDA_OK(cudaMemcpyAsync(qd.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice, c->stream));
+      knn_exact_rows(c, out->Pm.p, sq.p, n, d, K, qd.p, static_cast<i64>(rows.size()), dup.p, out->nbr.p,
+                     out->d2.p, out->mean.p);
+      sync(c);
+    }
+  } else {
+    knn_exact_rows(c, out->Pm.p, sq.p, n, d, K, nullptr, n, dup.p, out->nbr.p, out->d2.p, out->mean.p);
   }
   DevBuf<unsigned long long> ndup(c, 1);
   ndup.zero(c);
@@ -411,12 +611,6 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   const i64 distinct = n - static_cast<i64>(nd);
   if (distinct < K)
     invalid("knn graph: fewer distinct points (" + std::to_string(distinct) + ") than K (" + std::to_string(K) + ")");
-  out->nbr.alloc(c, n * K);
-  out->d2.alloc(c, n * K);
-  out->mean.alloc(c, n);
-  knn_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(K), static_cast<int>(splits), cand_d.p,
-                                                          cand_j.p, out->nbr.p, out->d2.p, out->mean.p);
-  launched(c);
 }
 
 template <typename T>

@@ -283,3 +283,18 @@ def test_gram_tf32x3_tensor_cores(P, ctx, n, d):
     assert np.all(err <= bound), float((err / bound).max())
     # and far better than plain TF32 would be
     assert err.max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("n,d,K", [(4500, 64, 10), (5000, 16, 12), (4200, 200, 10)])
+def test_knn_tensor_core_filter_bit_exact(P, ctx, n, d, K, monkeypatch):
+    """3xTF32 tcgen05 filter + certified fp64 re-rank: neighbour sets and
+    distances bit-identical to the oracle's canonical fp64 search."""
+    monkeypatch.setenv("CPCAG_KNN", "tc")
+    rs = np.random.default_rng(n + d)
+    centres = rs.standard_normal((d, 8)) * 2.0
+    X = centres[:, rs.integers(0, 8, n)] + 0.5 * rs.standard_normal((d, n))
+    X[:, 100:110] = X[:, 0:10]  # coincident points
+    nbr, d2 = P.knn(X, "cols", K, ctx=ctx)
+    nbr_o, d2_o = O.knn_neighbors(X, False, K)
+    assert np.array_equal(nbr, nbr_o)
+    assert np.array_equal(d2, d2_o)
