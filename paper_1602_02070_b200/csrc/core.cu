@@ -55,11 +55,11 @@ void ensure_smem_impl(const void* func, size_t bytes) {
   for (auto& e : seen)
     if (e.first == func) {
       if (e.second >= bytes) return;
-      ensure_smem(func, bytes);
+      CUDA_OK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
       e.second = bytes;
       return;
     }
-  ensure_smem(func, bytes);
+  CUDA_OK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
   seen.push_back({func, bytes});
 }
 
