@@ -366,6 +366,132 @@ __global__ void __launch_bounds__(256, 2) cg_apply_reg_k(i64 p, i64 n, Pull<T> L
   }
 }
 
+// Fused row-panel apply ("panel"): a CTA owns 32 consecutive rows and every
+// column.  P(i0:i0+32, :) is staged in shared memory (row-major per column,
+// padded), lane = row, warp = column; each warp handles two columns at a
+// time for ILP.  X L_c reads its neighbour columns from the panel (one
+// conflict-free shared load per entry); L_r P reads the lane's L_r row from
+// registers (loaded once) and gathers P(j, c) from global memory (coalesced
+// along the lane's consecutive rows for stencil-like graphs).
+constexpr int kPanelRows = 32;
+constexpr int kPanelRmax = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(512, 1) cg_apply_panel_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
+                                                            Plan pl, const T* __restrict__ P, T* __restrict__ AP,
+                                                            double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  LcEnt<T>* ents = reinterpret_cast<LcEnt<T>*>(smraw);  // nw x 2 x 32
+  T* Ps = reinterpret_cast<T*>(ents + nw * 64);          // n x (32 + 1)
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kPanelRows;
+  const i64 i = i0 + lane;
+  const bool in = i < p;
+  for (i64 c = wid; c < n; c += nw) Ps[c * (kPanelRows + 1) + lane] = in ? P[i + c * p] : T(0);
+  T rv[kPanelRmax];
+  int rc[kPanelRmax];
+  int rlen = 0;
+  i64 ra = 0;
+  if (in) {
+    ra = Lr.rp[i];
+    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
+  }
+#pragma unroll
+  for (int k = 0; k < kPanelRmax; ++k) {
+    rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
+    rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
+  }
+  __syncthreads();
+  const bool row_sampled = in && pl.rsel[i] >= 0;
+  LcEnt<T>* mine = ents + wid * 64;
+  double s[1] = {0.0};
+  for (i64 cA = wid; cA < n; cA += 2 * nw) {
+    const i64 cB = cA + nw;
+    const bool hasB = cB < n;
+    const i64 a0 = Lc.rp[cA], a1 = Lc.rp[cA + 1];
+    const i64 b0 = hasB ? Lc.rp[cB] : 0, b1 = hasB ? Lc.rp[cB + 1] : 0;
+    T xA = T(0), xB = T(0);
+    i64 ka = a0, kb = b0;
+    while (ka < a1 || kb < b1) {
+      const int cntA = static_cast<int>(min(static_cast<i64>(32), a1 - ka));
+      const int cntB = static_cast<int>(min(static_cast<i64>(32), b1 - kb));
+      if (lane < cntA) {
+        LcEnt<T> e;
+        e.v = Lc.v[ka + lane];
+        e.ci = Lc.ci[ka + lane];
+        mine[lane] = e;
+      }
+      if (lane < cntB) {
+        LcEnt<T> e;
+        e.v = Lc.v[kb + lane];
+        e.ci = Lc.ci[kb + lane];
+        mine[32 + lane] = e;
+      }
+      __syncwarp();
+      const int cmax = cntA > cntB ? cntA : cntB;
+      for (int k = 0; k < cmax; ++k) {
+        if (k < cntA) {
+          const LcEnt<T> e = mine[k];
+          xA = add_rn(xA, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanelRows + 1) + lane]));
+        }
+        if (k < cntB) {
+          const LcEnt<T> e = mine[32 + k];
+          xB = add_rn(xB, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanelRows + 1) + lane]));
+        }
+      }
+      __syncwarp();
+      ka += cntA > 0 ? cntA : 0;
+      kb += cntB > 0 ? cntB : 0;
+    }
+    if (in) {
+      // L_r P for both columns, CSR order per row
+      const T* pA = P + cA * p;
+      const T* pB = P + (hasB ? cB : cA) * p;
+      T yA = T(0), yB = T(0);
+      if (rlen <= kPanelRmax) {
+#pragma unroll
+        for (int k = 0; k < kPanelRmax; ++k)
+          if (k < rlen) {
+            yA = add_rn(yA, mul_rn(rv[k], pA[rc[k]]));
+            yB = add_rn(yB, mul_rn(rv[k], pB[rc[k]]));
+          }
+      } else {
+        for (i64 k = ra; k < ra + rlen; ++k) {
+          yA = add_rn(yA, mul_rn(Lr.v[k], pA[Lr.ci[k]]));
+          yB = add_rn(yB, mul_rn(Lr.v[k], pB[Lr.ci[k]]));
+        }
+      }
+      {
+        T out = add_rn(mul_rn(gc, xA), mul_rn(gr, yA));
+        const T pv = Ps[cA * (kPanelRows + 1) + lane];
+        if (row_sampled && pl.csel[cA] >= 0) out = add_rn(out, pv);
+        AP[i + cA * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+      if (hasB) {
+        T out = add_rn(mul_rn(gc, xB), mul_rn(gr, yB));
+        const T pv = Ps[cB * (kPanelRows + 1) + lane];
+        if (row_sampled && pl.csel[cB] >= 0) out = add_rn(out, pv);
+        AP[i + cB * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 template <typename T>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
@@ -526,6 +652,13 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const size_t reg_smem = static_cast<size_t>(max_ec) * sizeof(LcEnt<T>) + 16;
   const size_t lr_smem = static_cast<size_t>(kLrCols) * p * sizeof(T);
   const size_t lc_smem = 8 * 32 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanel + 1) * sizeof(T);
+  const size_t panel_smem = 16 * 64 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanelRows + 1) * sizeof(T);
+  const unsigned panel_blocks = static_cast<unsigned>((p + kPanelRows - 1) / kPanelRows);
+  if (variant == "panel" && !(panel_smem <= 220 * 1024)) variant = "staged";
+  if (variant == "panel") {
+    ensure_smem(cg_apply_panel_k<T>, panel_smem);
+    if (part.n < panel_blocks) part.alloc(c, panel_blocks);
+  }
   if (variant == "split" && !(lr_smem <= 200 * 1024 && lc_smem <= 200 * 1024)) variant = "staged";
   if (variant == "reg" && !(max_row <= 32 && reg_smem <= 96 * 1024)) variant = "staged";
   if (variant == "staged" && !(staged_smem <= 96 * 1024)) variant = "plain";
@@ -561,6 +694,9 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           launched(c);
           cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
                                                                   st.p);
+        } else if (variant == "panel") {
+          cg_apply_panel_k<T><<<panel_blocks, 512, panel_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p,
+                                                                            part.p, st.p);
         } else if (variant == "staged") {
           cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, 0, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
                                                                       AP.p, part.p, st.p);
