@@ -492,6 +492,98 @@ __global__ void __launch_bounds__(512, 1) cg_apply_panel_k(i64 p, i64 n, Pull<T>
   }
 }
 
+// Lean variant of the staged apply (default when p * n < 2^31): the staged
+// entries carry 32-bit element offsets (L_c: ci * p, L_r: ci), so a gather
+// is one shared load of the (value, offset) pair, one wide address add, one
+// global load and one fused multiply-add (fp32) / exact multiply + add
+// (fp64, so fp64 stays bit-identical to the reference order).
+template <typename T>
+struct alignas(sizeof(T) == 8 ? 16 : 8) OffEnt {
+  T v;
+  int off;
+};
+
+template <typename T>
+__device__ __forceinline__ T madd_entry(T acc, T v, T x) {
+  if constexpr (sizeof(T) == 8)
+    return __dadd_rn(acc, __dmul_rn(v, x));
+  else
+    return fmaf(v, x, acc);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_fast_k(int p, int c_lo, int c_hi, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
+                                                       Plan pl, int cols_per_cta, const T* __restrict__ P,
+                                                       T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int i0 = blockIdx.x * blockDim.x;
+  const int i1 = min(p, i0 + static_cast<int>(blockDim.x));
+  const int cb = c_lo + blockIdx.y * cols_per_cta;
+  const int ce = min(c_hi, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0];
+  const int er = static_cast<int>(Lr.rp[i1] - kr_base);
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0;
+  const int ec = cb < ce ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  OffEnt<T>* Er = reinterpret_cast<OffEnt<T>*>(smraw);
+  OffEnt<T>* Ec = Er + er;
+  int* crp = reinterpret_cast<int*>(Ec + ec);  // chunk row pointers of L_c (ce - cb + 1)
+  for (int k = threadIdx.x; k < er; k += blockDim.x) {
+    OffEnt<T> e;
+    e.v = Lr.v[kr_base + k];
+    e.off = Lr.ci[kr_base + k];
+    Er[k] = e;
+  }
+  for (int k = threadIdx.x; k < ec; k += blockDim.x) {
+    OffEnt<T> e;
+    e.v = Lc.v[kc_base + k];
+    e.off = Lc.ci[kc_base + k] * p;
+    Ec[k] = e;
+  }
+  for (int q = threadIdx.x; q <= ce - cb; q += blockDim.x) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  __syncthreads();
+  double s[1] = {0.0};
+  const int i = i0 + threadIdx.x;
+  if (i < p) {
+    const int a0 = static_cast<int>(Lr.rp[i] - kr_base), a1 = static_cast<int>(Lr.rp[i + 1] - kr_base);
+    const bool row_sampled = pl.rsel[i] >= 0;
+    const T* Pi = P + i;
+    for (int c = cb; c < ce; ++c) {
+      const int b0 = crp[c - cb], b1 = crp[c - cb + 1];
+      T x1 = T(0);
+#pragma unroll 4
+      for (int k = b0; k < b1; ++k) {
+        const OffEnt<T> e = Ec[k];
+        x1 = madd_entry(x1, e.v, Pi[e.off]);
+      }
+      const T* pc = P + static_cast<i64>(c) * p;
+      T x2 = T(0);
+#pragma unroll 4
+      for (int k = a0; k < a1; ++k) {
+        const OffEnt<T> e = Er[k];
+        x2 = madd_entry(x2, e.v, pc[e.off]);
+      }
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = pc[i];
+      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + static_cast<i64>(c) * p] = out;
+      s[0] += static_cast<double>(pv) * static_cast<double>(out);
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 template <typename T>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
@@ -630,7 +722,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 
   // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
   // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
-  std::string variant = "staged";
+  std::string variant = p * n < (i64{1} << 31) ? "fast" : "staged";
   if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
   std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
   CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
@@ -655,6 +747,9 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const size_t panel_smem = 16 * 64 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanelRows + 1) * sizeof(T);
   const unsigned panel_blocks = static_cast<unsigned>((p + kPanelRows - 1) / kPanelRows);
   if (variant == "panel" && !(panel_smem <= 220 * 1024)) variant = "staged";
+  const size_t fast_smem = static_cast<size_t>(max_er + max_ec) * sizeof(OffEnt<T>) + sizeof(int) * (cols_per_cta + 2) + 16;
+  if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
+  if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
   if (variant == "panel") {
     ensure_smem(cg_apply_panel_k<T>, panel_smem);
     if (part.n < panel_blocks) part.alloc(c, panel_blocks);
@@ -694,6 +789,10 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           launched(c);
           cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
                                                                   st.p);
+        } else if (variant == "fast") {
+          cg_apply_fast_k<T><<<gs, kBlock, fast_smem, c->stream>>>(static_cast<int>(p), 0, static_cast<int>(n), pr, pc,
+                                                                  gr, gc, pl, static_cast<int>(cols_per_cta), P.p, AP.p,
+                                                                  part.p, st.p);
         } else if (variant == "panel") {
           cg_apply_panel_k<T><<<panel_blocks, 512, panel_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p,
                                                                             part.p, st.p);
