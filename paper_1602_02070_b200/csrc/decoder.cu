@@ -548,47 +548,26 @@ __global__ void __launch_bounds__(256) cg_apply_fast_k(int p, int c_lo, int c_hi
     const int a0 = static_cast<int>(Lr.rp[i] - kr_base), a1 = static_cast<int>(Lr.rp[i + 1] - kr_base);
     const bool row_sampled = pl.rsel[i] >= 0;
     const T* Pi = P + i;
-    // two columns in flight per thread (independent load streams)
-    for (int c = cb; c < ce; c += 2) {
-      const bool two = c + 1 < ce;
+    for (int c = cb; c < ce; ++c) {
       const int b0 = crp[c - cb], b1 = crp[c - cb + 1];
-      const int d0 = two ? b1 : 0, d1 = two ? crp[c - cb + 2] : 0;
-      T xa = T(0), xb = T(0);
-      const int la = b1 - b0, lb = d1 - d0, lm = la > lb ? la : lb;
+      T x1 = T(0);
 #pragma unroll 4
-      for (int t = 0; t < lm; ++t) {
-        if (t < la) {
-          const OffEnt<T> e = Ec[b0 + t];
-          xa = madd_entry(xa, e.v, Pi[e.off]);
-        }
-        if (t < lb) {
-          const OffEnt<T> e = Ec[d0 + t];
-          xb = madd_entry(xb, e.v, Pi[e.off]);
-        }
+      for (int k = b0; k < b1; ++k) {
+        const OffEnt<T> e = Ec[k];
+        x1 = madd_entry(x1, e.v, Pi[e.off]);
       }
-      const T* pa = P + static_cast<i64>(c) * p;
-      const T* pb = two ? pa + p : pa;
-      T ya = T(0), yb = T(0);
+      const T* pc = P + static_cast<i64>(c) * p;
+      T x2 = T(0);
 #pragma unroll 4
       for (int k = a0; k < a1; ++k) {
         const OffEnt<T> e = Er[k];
-        ya = madd_entry(ya, e.v, pa[e.off]);
-        yb = madd_entry(yb, e.v, pb[e.off]);
+        x2 = madd_entry(x2, e.v, pc[e.off]);
       }
-      {
-        T out = add_rn(mul_rn(gc, xa), mul_rn(gr, ya));
-        const T pv = pa[i];
-        if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
-        AP[i + static_cast<i64>(c) * p] = out;
-        s[0] += static_cast<double>(pv) * static_cast<double>(out);
-      }
-      if (two) {
-        T out = add_rn(mul_rn(gc, xb), mul_rn(gr, yb));
-        const T pv = pb[i];
-        if (row_sampled && pl.csel[c + 1] >= 0) out = add_rn(out, pv);
-        AP[i + static_cast<i64>(c + 1) * p] = out;
-        s[0] += static_cast<double>(pv) * static_cast<double>(out);
-      }
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = pc[i];
+      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + static_cast<i64>(c) * p] = out;
+      s[0] += static_cast<double>(pv) * static_cast<double>(out);
     }
   }
   double tot[1];
