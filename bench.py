@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="compute in fp64 (config 1 is fp32)")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--config", choices=["cfg1", "cfg2", "cfg3"], default="cfg1",
+                    help="cfg1 (default, the headline): full CPCA; cfg2: kNN graph alone; cfg3: decoder at scale")
     return ap.parse_args()
 
 
@@ -444,9 +446,127 @@ def run_reference(args, rank, world):
             f.write(json.dumps(out) + "\n")
 
 
+# ------------------------------------------------------------------ cfg2 / cfg3
+def timed_steps(fn, steps, warmup, stream):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+
+
+def run_cfg2(args):
+    """kNN graph construction alone (BASELINE config 2)."""
+    import torch
+
+    import paper_1602_02070_b200 as P
+    from paper_1602_02070_b200 import workloads
+
+    X = workloads.config2_points()
+    d, n = X.shape
+    ctx = P.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda").t()
+    ctx.reset_kernel_timing()
+    ctx.enable_kernel_timing(True)
+    ms = timed_steps(lambda: P.build_knn_graph(Xd, "cols", 10, ctx=ctx), args.steps, args.warmup, stream)
+    ctx.enable_kernel_timing(False)
+    kt = ctx.kernel_times()
+    flops = 2.0 * n * n * d
+    tc = kt.get("knn_tc_filter")
+    out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32 in, 3xTF32 filter + fp64 exact re-rank",
+           "data": "synthetic: seeded config-2 generator (50/50 N(0,I) + 20 clusters)",
+           "config": {"workload": "cfg2: kNN graph, n=100000, d=512, K=10, CSR combinatorial Laplacian"},
+           "kernel_ms": {k: round(v[1] / max(v[0], 1) * v[0] / (args.steps + args.warmup), 3) for k, v in kt.items()},
+           "gram_useful_tflops": round(flops / (ms / 1e3) / 1e12, 2)}
+    if tc:
+        t_tc = tc[1] / tc[0]
+        out["roofline"] = {"bound": "tensor", "kernel": "knn_tc_filter", "achieved": round(3 * flops / (t_tc / 1e3) / 1e12, 1),
+                           "peak": 1100.0, "unit": "TFLOP/s", "frac": round(3 * flops / (t_tc / 1e3) / 1e12 / 1100.0, 4),
+                           "peak_source": "nominal dense TF32 (B200_PROFILING.md), 3 MMAs per product counted"}
+    print(json.dumps(out), flush=True)
+
+
+def run_cfg3(args):
+    """Decoder-only CG at scale (BASELINE config 3), one GPU."""
+    import torch
+
+    import paper_1602_02070_b200 as P
+    from paper_1602_02070_b200 import workloads
+
+    Pr, Pc = workloads.config3_points()
+    p, n = Pr.shape[1], Pc.shape[1]
+    ctx = P.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    t0 = time.perf_counter()
+    gr = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    gc = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    t_graphs = time.perf_counter() - t0
+    rs = np.random.default_rng(1606)
+
+    def lowpass(L, m, k=20, sweeps=20):
+        nrm = P.power_iteration_norm(L, 1e-7, 42, ctx=ctx)
+        B = torch.tensor(rs.standard_normal((m, k)), device="cuda")
+        for _ in range(sweeps):
+            B = B - L.multiply(B) / nrm
+        q, _ = torch.linalg.qr(B)
+        return q
+
+    Br, Bc = lowpass(gr.laplacian, p), lowpass(gc.laplacian, n)
+    plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
+    A = torch.tensor(rs.standard_normal((20, 20)), device="cuda")
+    Xt = (Br[torch.tensor(plan.omega_r, device="cuda")] @ A @ Bc[torch.tensor(plan.omega_c, device="cuda")].T)
+    Xt = Xt.float().t().contiguous().t()
+    g1 = P.SpectralGap(lambda_k1=1.0)
+    dcfg = P.DecoderConfig(1.0, 1e-30, 100)
+    ctx.reset_kernel_timing()
+    ctx.enable_kernel_timing(True)
+    res = {}
+
+    def step():
+        res["r"] = P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, ctx=ctx)
+
+    ms = timed_steps(step, args.steps, max(args.warmup, 1), stream)
+    ctx.enable_kernel_timing(False)
+    kt = ctx.kernel_times()
+    N = p * n
+    nnz_r, nnz_c = gr.laplacian.nonzeros(), gc.laplacian.nonzeros()
+    it = res["r"].iterations
+    b_iter = 6 * N * 4 + (nnz_r + nnz_c) * 8
+    peak, src = measured_peaks()
+    out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic: seeded config-3 generator (N(0,I_64) points, rank-20 low-pass basis)",
+           "config": {"workload": f"cfg3: alternate CG decoder, p={p}, n={n}, 1/8 x 1/8 sampling, {it} iterations",
+                      "graphs_s_untimed": round(t_graphs, 3)},
+           "iters_per_s": round(it / (ms / 1e3), 1),
+           "cg_iteration": {"bytes_B_iter": b_iter, "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
+                            "frac_of_hbm": round(b_iter * it / (ms / 1e3) / 1e9 / peak, 4), "peak_source": src},
+           "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()}}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
+    if args.config == "cfg2" and args.impl == "ours":
+        return run_cfg2(args)
+    if args.config == "cfg3" and args.impl == "ours":
+        return run_cfg3(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

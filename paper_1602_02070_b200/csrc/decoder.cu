@@ -728,8 +728,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
-  const i64 cols_per_cta = (n + g2.y - 1) / g2.y;
-  const dim3 gs(gx, static_cast<unsigned>((n + cols_per_cta - 1) / cols_per_cta));
+  // Column chunk per CTA: enough CTAs for ~16 per SM, and a chunk small
+  // enough that its L_c rows stage in shared memory (<= 128 columns).
+  const i64 cols_per_cta = std::max<i64>({i64{1}, std::min<i64>((n + g2.y - 1) / g2.y, 128), (n + 65534) / 65535});
+  const dim3 gs(gx, static_cast<unsigned>(std::min<i64>((n + cols_per_cta - 1) / cols_per_cta, 65535)));
+  if (part.n < static_cast<size_t>(gs.x) * gs.y) part.alloc(c, static_cast<size_t>(gs.x) * gs.y);
   i64 max_er = 0, max_ec = 0, max_row = 0;
   for (unsigned b = 0; b < gx; ++b) {
     const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);

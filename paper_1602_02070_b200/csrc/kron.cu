@@ -355,7 +355,7 @@ constexpr int kCpb = 4;
 
 __device__ __forceinline__ i64 slab_at(i64 n, i64 i, i64 c) { return ((c / kCpb) * n + i) * kCpb + (c % kCpb); }
 
-__global__ void __launch_bounds__(256) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
+__global__ void __launch_bounds__(1024, 1) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
                                                         const int* __restrict__ ci, const double* __restrict__ v,
                                                         const double* __restrict__ inv, const double* __restrict__ B,
                                                         double* __restrict__ X, double* __restrict__ R,
@@ -601,7 +601,7 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   st.zero(c);
   {
     KScope ks_(c, "pcg_persistent");
-    pcg_persistent_k<<<static_cast<unsigned>(nbp / kCpb), 256, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
+    pcg_persistent_k<<<static_cast<unsigned>(nbp / kCpb), 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
                                                                               R.p, P.p, AP.p, tol, max_iter, st.p);
     launched(c);
   }

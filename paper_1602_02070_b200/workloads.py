@@ -169,3 +169,22 @@ def config1(seed: int = 1603) -> Workload:
     lc = _lambda_k1_of_knn(Y, False, 10, k)
     return Workload("cfg1 CPCA 10304x1000 fp32", np.asfortranarray(Y), np.asfortranarray(X0), 10, 10,
                     math.sqrt(max(p, n)), 300, 200, 1e-8, float(ev_r[k]), lc, Wr, k)
+
+
+def config2_points(seed: int = 1604, n: int = 100_000, d: int = 512, clusters: int = 20) -> np.ndarray:
+    """Config 2: n points in R^d (columns of a d x n fp32 matrix), a 50/50
+    mixture of N(0, I) background and `clusters` Gaussian clusters (centres
+    N(0, 4 I), std 0.5).  The mixture weight is an assumption."""
+    rs = np.random.default_rng(seed)
+    X = rs.standard_normal((d, n), dtype=np.float32)
+    m = n // 2
+    centres = (2.0 * rs.standard_normal((d, clusters))).astype(np.float32)
+    lab = rs.integers(0, clusters, m)
+    X[:, :m] = centres[:, lab] + 0.5 * rs.standard_normal((d, m), dtype=np.float32)
+    return np.asfortranarray(X)
+
+
+def config3_points(seed: int = 1605, p: int = 4096, n: int = 200_000, dim: int = 64):
+    """Config 3: row points (p x dim) and column points (n x dim), N(0, I)."""
+    rs = np.random.default_rng(seed)
+    return (rs.standard_normal((dim, p), dtype=np.float32), rs.standard_normal((dim, n), dtype=np.float32))
