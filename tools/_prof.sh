@@ -1,3 +1,4 @@
-timeout -s KILL 300 python bench.py --steps 5 --warmup 3 --json-out gpurun_out/bench23.json > gpurun_out/bench23.log 2>&1; tail -1 gpurun_out/bench23.log | cut -c1-300
-timeout -s KILL 120 python tools/profile_step.py > gpurun_out/p23.log 2>&1 && timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_r1_final.csv python tools/profile_step.py > gpurun_out/ncu23a.log 2>&1
-timeout -s KILL 400 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"cg_apply_fast|fista_splitk_partial|pcg_persistent|knn_tile|power_iter_coop|cg_update|cg_residual" -c 7 -o gpurun_out/full_r1 python tools/profile_step.py > gpurun_out/ncu23b.log 2>&1; tail -1 gpurun_out/ncu23b.log
+timeout -s KILL 300 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/t24.log 2>&1; tail -2 gpurun_out/t24.log
+timeout -s KILL 200 python tools/bench_stages.py > gpurun_out/stages24.log 2>&1; cat gpurun_out/stages24.log | cut -c1-200
+timeout -s KILL 300 python bench.py --config cfg2 --steps 2 --warmup 1 > gpurun_out/bench24_cfg2.log 2>&1; tail -1 gpurun_out/bench24_cfg2.log
+timeout -s KILL 400 python bench.py --config cfg3 --steps 2 --warmup 1 > gpurun_out/bench24_cfg3.log 2>&1; tail -1 gpurun_out/bench24_cfg3.log

@@ -51,7 +51,10 @@ def main(rep, json_out=None):
             if key not in d or d[key] in ("", "n/a"):
                 vals.append("-")
                 continue
-            if scale is None:
+            if key == "gpu__time_duration.sum":
+                f = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u[key], 1.0)
+                vals.append(f"{float(d[key]) * f:.1f}")
+            elif scale is None:
                 vals.append(f"{to_mb(d[key], u[key]):.1f}")
             else:
                 try:
