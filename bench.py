@@ -547,8 +547,16 @@ def run_cfg3(args):
     N = p * n
     nnz_r, nnz_c = gr.laplacian.nonzeros(), gc.laplacian.nonzeros()
     it = res["r"].iterations
-    b_iter = 6 * N * 4 + (nnz_r + nnz_c) * 8
+    # Algorithmic HBM bytes per CG iteration: apply reads P and writes AP
+    # (2N), residual reads R, AP and writes R (3N), update reads X, P, R and
+    # writes X, P (5N); plus one pass over both Laplacians.
+    b_iter = 10 * N * 4 + (nnz_r + nnz_c) * 8
     peak, src = measured_peaks()
+    kbytes = {"cg_apply": 2 * N * 4 + (nnz_r + nnz_c) * 8,
+              "cg_apply_band": 2 * N * 4 + nnz_c * 8,      # P read once, U written
+              "cg_apply_col": 3 * N * 4 + nnz_r * 8,       # P, U read; AP written
+              "cg_residual": 3 * N * 4, "cg_update": 5 * N * 4}
+    kgbps = {k: round(kbytes[k] / (v[1] / v[0] / 1e3) / 1e9, 1) for k, v in kt.items() if k in kbytes}
     out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32",
@@ -558,7 +566,8 @@ def run_cfg3(args):
            "iters_per_s": round(it / (ms / 1e3), 1),
            "cg_iteration": {"bytes_B_iter": b_iter, "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
                             "frac_of_hbm": round(b_iter * it / (ms / 1e3) / 1e9 / peak, 4), "peak_source": src},
-           "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()}}
+           "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()},
+           "kernel_algorithmic_GBps": kgbps}
     print(json.dumps(out), flush=True)
 
 

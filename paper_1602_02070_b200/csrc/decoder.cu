@@ -657,6 +657,284 @@ __global__ void scatter_sel_k(const i64* __restrict__ om, i64 rho, int* sel) {
   if (k < rho) sel[om[k]] = static_cast<int>(k);
 }
 
+// ------------------------------------------------------------------ band apply
+// For iterates that do not fit in L2 (cfg3: P is 4096 x 200000 fp32 =
+// 3.3 GB) the single-pass applies above fetch every gathered column of P
+// from HBM again, about 19 times the matrix per apply.  The band apply splits
+// A(P) into two sweeps.  Each sweep keeps the data it gathers on chip:
+//   cg_apply_band_k  U = gc (P L_c).  Rows go in bands of 32*RPL; the grid is
+//                    band-major (blockIdx.x = column chunk), so one band of
+//                    32*RPL rows x all n columns (<= ~56 MB) stays resident
+//                    in L2 while each column gathers its L_c neighbours from
+//                    it.  One warp per column, lane = row: 128-byte gathers.
+//   cg_apply_col_k   AP = U + gr (L_r P) (+ P on the sampled grid), <P, AP>.
+//                    A CTA stages Q full columns in shared memory as one
+//                    16/32-byte record per row (swizzled halves, so random
+//                    record reads spread over all bank groups).  L_r is read
+//                    in a warp-interleaved ELL layout: one coalesced load per
+//                    warp per entry slot, reused for Q columns.
+// U = mul_rn(gc, x1) rounds exactly like apply_elem, so the split result is
+// bit-identical to cg_apply_k in fp64 (same per-entry order).
+template <typename T>
+__global__ void pack_ent_k(i64 nnz, const int* __restrict__ ci, const T* __restrict__ v, OffEnt<T>* __restrict__ out) {
+  const i64 k = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (k < nnz) {
+    OffEnt<T> e;
+    e.v = v[k];
+    e.off = ci[k];
+    out[k] = e;
+  }
+}
+
+template <typename T>
+__global__ void ell_fill_k(i64 p, const i64* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
+                           const int* __restrict__ base, OffEnt<T>* __restrict__ ell, int* __restrict__ deg) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  const i64 k0 = rp[i], d = rp[i + 1] - k0;
+  OffEnt<T>* dst = ell + static_cast<i64>(base[i >> 5]) * 32 + (i & 31);
+  for (i64 k = 0; k < d; ++k) {
+    OffEnt<T> e;
+    e.v = v[k0 + k];
+    e.off = ci[k0 + k];
+    dst[k * 32] = e;
+  }
+  deg[i] = static_cast<int>(d);
+}
+
+template <typename T, int RPL>
+__global__ void __launch_bounds__(256) cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp,
+                                                       const OffEnt<T>* __restrict__ ent, T gc, i64 cols_per_cta,
+                                                       const T* __restrict__ P, T* __restrict__ U,
+                                                       const CgState* st, int force) {
+  if (!force && st->done) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const i64 r0 = static_cast<i64>(blockIdx.y) * (32 * RPL) + lane;
+  const i64 cb = c_lo + static_cast<i64>(blockIdx.x) * cols_per_cta;
+  const i64 ce = min(c_hi, cb + cols_per_cta);
+  bool ok[RPL];
+#pragma unroll
+  for (int t = 0; t < RPL; ++t) ok[t] = r0 + 32 * t < p;
+  for (i64 c = cb + warp; c < ce; c += nw) {
+    const i64 k0 = rp[c], k1 = rp[c + 1];
+    T acc[RPL];
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) acc[t] = T(0);
+#pragma unroll 4
+    for (i64 k = k0; k < k1; ++k) {
+      const OffEnt<T> e = ent[k];
+      const T* col = P + static_cast<i64>(e.off) * p + r0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t)
+        if (ok[t]) acc[t] = madd_entry(acc[t], e.v, col[32 * t]);
+    }
+    T* out = U + c * p + r0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+      if (ok[t]) out[32 * t] = mul_rn(gc, acc[t]);
+  }
+}
+
+template <int H>
+__device__ __forceinline__ int rec_chunk(int j, int h) {
+  if constexpr (H == 2)
+    return 2 * j + (h ^ ((j >> 2) & 1));
+  else
+    return j;
+}
+
+template <typename T, int RB>
+__global__ void __launch_bounds__(1024, 1) cg_apply_col_k(int p, i64 c_lo, i64 c_hi, const int* __restrict__ ell_base,
+                                                          const int* __restrict__ deg,
+                                                          const OffEnt<T>* __restrict__ ell, T gr, Plan pl,
+                                                          const T* __restrict__ P, T* __restrict__ AP,
+                                                          double* partials, CgState* st, int force) {
+  if (!force && st->done) return;
+  constexpr int Q = RB / static_cast<int>(sizeof(T));
+  constexpr int H = RB / 16;
+  union Rec {
+    uint4 u[H];
+    T v[Q];
+  };
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint4* S = reinterpret_cast<uint4*>(smraw);
+  const i64 c0 = c_lo + static_cast<i64>(blockIdx.x) * Q;
+  const int qn = static_cast<int>(min(static_cast<i64>(Q), c_hi - c0));
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    Rec r;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) r.v[q] = q < qn ? P[j + (c0 + q) * static_cast<i64>(p)] : T(0);
+#pragma unroll
+    for (int h = 0; h < H; ++h) S[rec_chunk<H>(j, h)] = r.u[h];
+  }
+  __syncthreads();
+  double s = 0.0;
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < p; i += blockDim.x) {
+    const int d = deg[i];
+    const OffEnt<T>* e = ell + static_cast<i64>(ell_base[i >> 5]) * 32 + lane;
+    T acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = T(0);
+#pragma unroll 2
+    for (int k = 0; k < d; ++k) {
+      const OffEnt<T> en = e[k * 32];
+      Rec x;
+#pragma unroll
+      for (int h = 0; h < H; ++h) x.u[h] = S[rec_chunk<H>(en.off, h)];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = madd_entry(acc[q], en.v, x.v[q]);
+    }
+    Rec own;
+#pragma unroll
+    for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
+    const bool rs = pl.rsel[i] >= 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (q < qn) {
+        const i64 c = c0 + q;
+        const i64 at = i + c * p;
+        T out = add_rn(AP[at], mul_rn(gr, acc[q]));
+        if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
+        AP[at] = out;
+        s += static_cast<double>(own.v[q]) * static_cast<double>(out);
+      }
+    }
+  }
+  if (force) return;
+  double sv[1] = {s}, tot[1];
+  if (grid_sum_last<1>(sv, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
+// ||b - AX||^2 with AX already applied (band path of the exit test).
+template <typename T>
+__global__ void cg_true_res_ap_k(i64 p, i64 n, Plan pl, const T* __restrict__ Xt, const T* __restrict__ AX,
+                                 double* partials, CgState* st) {
+  double s[1] = {0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p) {
+    for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+      const double e = static_cast<double>(sub_rn(rhs_at(pl, Xt, i, c), AX[i + c * p]));
+      s[0] += e * e;
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0)
+    st->rel_res = sqrt(tot[0]) / st->norm_b;
+}
+
+// Host side of the band apply: packed L_c entries, the L_r ELL layout and the
+// launch geometry, built once per solve (or per decoder block).
+template <typename T>
+struct BandApply {
+  static constexpr i64 kBandBytes = i64{56} << 20;  // L2-resident band budget
+  static constexpr int kColsPerCta = 64;
+  i64 p = 0, n = 0;
+  int rpl = 1, rb = 32;
+  size_t col_smem = 0;
+  DevBuf<OffEnt<T>> ent, ell;
+  DevBuf<int> base, deg;
+  const i64* rpc = nullptr;
+
+  // Feasible when a Q-column group of P fits in shared memory.
+  static bool feasible(i64 p) { return p > 0 && p * 16 <= 200 * 1024 && p < (i64{1} << 31); }
+  // Auto choice: the iterate does not fit in L2.
+  static bool preferred(i64 p, i64 n) { return static_cast<double>(p) * n * sizeof(T) > 96e6 && feasible(p); }
+
+  void build(Ctx* c, Csr* Lr, Csr* Lc, const std::vector<i64>& rpr) {
+    p = Lr->rows;
+    n = Lc->rows;
+    if (!feasible(p)) invalid("band apply: row count too large for the column-group kernel");
+    rb = p * 32 <= 200 * 1024 ? 32 : 16;
+    col_smem = static_cast<size_t>(p) * rb;
+    rpl = 1;
+    for (int r : {4, 2}) {
+      if (32 * r * n * static_cast<i64>(sizeof(T)) <= kBandBytes && 32 * r <= ((p + 31) / 32) * 32) {
+        rpl = r;
+        break;
+      }
+    }
+    const Pull<T> pc = make_pull<T>(c, Lc, true), pr = make_pull<T>(c, Lr, false);
+    rpc = pc.rp;
+    const i64 nnz_c = Lc->nnz;
+    ent.alloc(c, std::max<i64>(nnz_c, 1));
+    if (nnz_c) {
+      pack_ent_k<T><<<blocks_for(nnz_c), kBlock, 0, c->stream>>>(nnz_c, pc.ci, pc.v, ent.p);
+      launched(c);
+    }
+    const i64 groups = (p + 31) / 32;
+    std::vector<int> hb(static_cast<size_t>(groups));
+    i64 slots = 0;
+    for (i64 g = 0; g < groups; ++g) {
+      i64 md = 0;
+      for (i64 i = g * 32; i < std::min<i64>(p, g * 32 + 32); ++i) md = std::max(md, rpr[i + 1] - rpr[i]);
+      hb[g] = static_cast<int>(slots);
+      slots += md;
+    }
+    if (slots * 32 >= (i64{1} << 31)) invalid("band apply: L_r too dense for the ELL layout");
+    base.alloc(c, groups);
+    deg.alloc(c, p);
+    ell.alloc(c, std::max<i64>(slots * 32, 1));
+    CUDA_OK(cudaMemcpyAsync(base.p, hb.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
+    ell_fill_k<T><<<blocks_for(p), kBlock, 0, c->stream>>>(p, pr.rp, pr.ci, pr.v, base.p, ell.p, deg.p);
+    launched(c);
+    if (rb == 32)
+      ensure_smem(cg_apply_col_k<T, 32>, col_smem);
+    else
+      ensure_smem(cg_apply_col_k<T, 16>, col_smem);
+    sync(c);  // hb must outlive the copy
+  }
+
+  unsigned col_blocks(i64 c_lo, i64 c_hi) const {
+    const i64 q = rb / static_cast<i64>(sizeof(T));
+    return static_cast<unsigned>(std::max<i64>(1, (c_hi - c_lo + q - 1) / q));
+  }
+
+  // AP[:, c_lo:c_hi] (AP indexed by global column) = A(P) on those columns;
+  // P holds every column.  force = 1 ignores the CG done flag and skips the
+  // <P, AP> reduction (true-residual apply).
+  void apply(Ctx* c, const T* P, T* AP, i64 c_lo, i64 c_hi, const Plan& pl, T gr, T gc, double* part, CgState* st,
+             int force) const {
+    if (c_hi <= c_lo) return;
+    const i64 band_rows = 32 * rpl;
+    const dim3 gb(static_cast<unsigned>((c_hi - c_lo + kColsPerCta - 1) / kColsPerCta),
+                  static_cast<unsigned>((p + band_rows - 1) / band_rows));
+    {
+    KScope ks_(c, "cg_apply_band");
+    switch (rpl) {
+      case 4:
+        cg_apply_band_k<T, 4><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
+        break;
+      case 2:
+        cg_apply_band_k<T, 2><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
+        break;
+      default:
+        cg_apply_band_k<T, 1><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
+    }
+    launched(c);
+    }
+    KScope ks_(c, "cg_apply_col");
+    const unsigned gcb = col_blocks(c_lo, c_hi);
+    if (rb == 32)
+      cg_apply_col_k<T, 32><<<gcb, 1024, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
+                                                                ell.p, gr, pl, P, AP, part, st, force);
+    else
+      cg_apply_col_k<T, 16><<<gcb, 1024, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
+                                                                ell.p, gr, pl, P, AP, part, st, force);
+    launched(c);
+  }
+};
+
 template <typename T>
 void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i64* om_r_host,
                              const i64* om_c_host, i64 p, i64 n, Csr* Lr, Csr* Lc, double lk1_r,
@@ -723,7 +1001,9 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
   // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
   std::string variant = p * n < (i64{1} << 31) ? "fast" : "staged";
+  if (BandApply<T>::preferred(p, n)) variant = "band";
   if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
+  if (variant == "band" && !BandApply<T>::feasible(p)) variant = "staged";
   std::vector<i64> rpr(static_cast<size_t>(p) + 1), rpc(static_cast<size_t>(n) + 1);
   CUDA_OK(cudaMemcpyAsync(rpr.data(), pr.rp, sizeof(i64) * (p + 1), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
@@ -752,6 +1032,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "panel" && !(panel_smem <= 220 * 1024)) variant = "staged";
   const size_t fast_smem = static_cast<size_t>(max_er + max_ec) * sizeof(OffEnt<T>) + sizeof(int) * (cols_per_cta + 2) + 16;
   if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
+  BandApply<T> band;
+  if (variant == "band") {
+    band.build(c, Lr, Lc, rpr);
+    if (part.n < band.col_blocks(0, n)) part.alloc(c, band.col_blocks(0, n));
+  }
   if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
   if (variant == "panel") {
     ensure_smem(cg_apply_panel_k<T>, panel_smem);
@@ -792,6 +1077,8 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           launched(c);
           cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
                                                                   st.p);
+        } else if (variant == "band") {
+          band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
         } else if (variant == "fast") {
           cg_apply_fast_k<T><<<gs, kBlock, fast_smem, c->stream>>>(static_cast<int>(p), 0, static_cast<int>(n), pr, pc,
                                                                   gr, gc, pl, static_cast<int>(cols_per_cta), P.p, AP.p,
@@ -814,7 +1101,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
         } else {
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         }
-        launched(c);
+        if (variant != "band") launched(c);
       }
       {
         KScope ks_(c, "cg_residual");
@@ -836,7 +1123,12 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     *iterations = 0;
     return;
   }
-  cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, Xt, X, part.p, st.p);
+  if (variant == "band") {
+    band.apply(c, X, AP.p, 0, n, pl, gr, gc, part.p, st.p, 1);
+    cg_true_res_ap_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, AP.p, part.p, st.p);
+  } else {
+    cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, Xt, X, part.p, st.p);
+  }
   launched(c);
   host = read_back(c, st.p);
   *converged = host.rel_res <= cfg.pcg_tol ? 1 : 0;
@@ -866,6 +1158,11 @@ struct DecBlock {
   size_t smem = 0;
   i64 cols_per_cta = 1;
   dim3 grid;
+  // Band apply (iterate larger than L2); null when the staged apply is used.
+  std::unique_ptr<BandApply<float>> band32;
+  std::unique_ptr<BandApply<double>> band64;
+  BandApply<float>* band(float*) { return band32.get(); }
+  BandApply<double>* band(double*) { return band64.get(); }
 };
 
 template <typename T>
@@ -923,7 +1220,10 @@ void block_apply(DecBlock* b, const T* Pfull, T* APblk, double* dot) {
   b->st.zero(c);
   // AP indexed by global column: shift the block pointer back by c0 columns.
   T* base = APblk - b->c0 * b->p;
-  {
+  if (BandApply<T>* band = b->band(static_cast<T*>(nullptr))) {
+    KScope ks_(c, "cg_apply");
+    band->apply(c, Pfull, base, b->c0, b->c1, pl, static_cast<T>(b->gr), static_cast<T>(b->gc), b->part.p, b->st.p, 0);
+  } else {
     KScope ks_(c, "cg_apply");
     cg_apply_staged_k<T><<<b->grid, kBlock, b->smem, c->stream>>>(b->p, b->c0, b->c1, pr, pc, static_cast<T>(b->gr),
                                                                   static_cast<T>(b->gc), pl, b->cols_per_cta, Pfull,
@@ -1004,13 +1304,30 @@ extern "C" int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int
     }
     const size_t es = precision == CPCAG_F64 ? sizeof(double) : sizeof(float);
     blk->smem = static_cast<size_t>(max_er + max_ec) * (es + sizeof(int)) + 16;
-    if (blk->smem > 200 * 1024) invalid("decoder block: operator slice exceeds shared memory");
-    if (precision == CPCAG_F64)
-      ensure_smem(cg_apply_staged_k<double>, blk->smem);
-    else
-      ensure_smem(cg_apply_staged_k<float>, blk->smem);
-    const size_t nparts = std::max<size_t>(static_cast<size_t>(blk->grid.x) * blk->grid.y,
-                                           stride_blocks(c, std::max<i64>(p * nb_cols, 1)));
+    std::string variant = "staged";
+    if (precision == CPCAG_F64 ? BandApply<double>::preferred(p, n) : BandApply<float>::preferred(p, n))
+      variant = "band";
+    if (const char* e = std::getenv("CPCAG_APPLY")) variant = std::string(e) == "band" ? "band" : "staged";
+    if (variant == "band" && !BandApply<float>::feasible(p)) variant = "staged";
+    size_t nparts = std::max<size_t>(static_cast<size_t>(blk->grid.x) * blk->grid.y,
+                                     stride_blocks(c, std::max<i64>(p * nb_cols, 1)));
+    if (variant == "band") {
+      if (precision == CPCAG_F64) {
+        blk->band64 = std::make_unique<BandApply<double>>();
+        blk->band64->build(c, A, B, rpr);
+        nparts = std::max<size_t>(nparts, blk->band64->col_blocks(c_begin, c_end));
+      } else {
+        blk->band32 = std::make_unique<BandApply<float>>();
+        blk->band32->build(c, A, B, rpr);
+        nparts = std::max<size_t>(nparts, blk->band32->col_blocks(c_begin, c_end));
+      }
+    } else {
+      if (blk->smem > 200 * 1024) invalid("decoder block: operator slice exceeds shared memory");
+      if (precision == CPCAG_F64)
+        ensure_smem(cg_apply_staged_k<double>, blk->smem);
+      else
+        ensure_smem(cg_apply_staged_k<float>, blk->smem);
+    }
     blk->part.alloc(c, nparts);
     blk->st.alloc(c, 1);
     blk->st.zero(c);
