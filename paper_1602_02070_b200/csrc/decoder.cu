@@ -702,8 +702,17 @@ __global__ void ell_fill_k(i64 p, const i64* __restrict__ rp, const int* __restr
   deg[i] = static_cast<int>(d);
 }
 
+template <typename T>
+__device__ __forceinline__ void store_stream(T* p, T v) {
+  __stcs(p, v);
+}
+
+// Warp per column: the column's L_c entries are loaded with one coalesced
+// load (lane t holds entry t of the chunk) and broadcast by shuffle, so the
+// gathers of 8 entries are in flight at once; U is stored evict-first so it
+// does not push the band out of L2.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256) cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp,
+__global__ void __launch_bounds__(256, 4) cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp,
                                                        const OffEnt<T>* __restrict__ ent, T gc, i64 cols_per_cta,
                                                        const T* __restrict__ P, T* __restrict__ U,
                                                        const CgState* st, int force) {
@@ -715,23 +724,36 @@ __global__ void __launch_bounds__(256) cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi
   bool ok[RPL];
 #pragma unroll
   for (int t = 0; t < RPL; ++t) ok[t] = r0 + 32 * t < p;
-  for (i64 c = cb + warp; c < ce; c += nw) {
-    const i64 k0 = rp[c], k1 = rp[c + 1];
+  // Row pointers of this warp's columns (lane m holds column cb + warp + m*nw).
+  const i64 cm = cb + warp + static_cast<i64>(lane) * nw;
+  const i64 my_k0 = cm < ce ? rp[cm] : 0, my_k1 = cm < ce ? rp[cm + 1] : 0;
+  for (int m = 0;; ++m) {
+    const i64 c = cb + warp + static_cast<i64>(m) * nw;
+    if (c >= ce) break;
+    const i64 k0 = __shfl_sync(0xffffffffu, my_k0, m & 31), k1 = __shfl_sync(0xffffffffu, my_k1, m & 31);
     T acc[RPL];
 #pragma unroll
     for (int t = 0; t < RPL; ++t) acc[t] = T(0);
-#pragma unroll 4
-    for (i64 k = k0; k < k1; ++k) {
-      const OffEnt<T> e = ent[k];
-      const T* col = P + static_cast<i64>(e.off) * p + r0;
+    for (i64 kb = k0; kb < k1; kb += 32) {
+      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - kb));
+      OffEnt<T> mine;
+      mine.v = T(0);
+      mine.off = 0;
+      if (lane < cnt) mine = ent[kb + lane];
+#pragma unroll 8
+      for (int q = 0; q < cnt; ++q) {
+        const int j = __shfl_sync(0xffffffffu, mine.off, q);
+        const T v = __shfl_sync(0xffffffffu, mine.v, q);
+        const T* col = P + static_cast<i64>(j) * p + r0;
 #pragma unroll
-      for (int t = 0; t < RPL; ++t)
-        if (ok[t]) acc[t] = madd_entry(acc[t], e.v, col[32 * t]);
+        for (int t = 0; t < RPL; ++t)
+          if (ok[t]) acc[t] = madd_entry(acc[t], v, col[32 * t]);
+      }
     }
     T* out = U + c * p + r0;
 #pragma unroll
     for (int t = 0; t < RPL; ++t)
-      if (ok[t]) out[32 * t] = mul_rn(gc, acc[t]);
+      if (ok[t]) store_stream(out + 32 * t, mul_rn(gc, acc[t]));
   }
 }
 
@@ -743,23 +765,32 @@ __device__ __forceinline__ int rec_chunk(int j, int h) {
     return j;
 }
 
+// Row groups (32 rows = one warp's lanes) are handed to warps dynamically,
+// heaviest (largest padded degree) first, from a shared counter; each lane
+// keeps a batch of 8 L_r entries in registers so their loads overlap.
+constexpr int kColThreads = 512;
 template <typename T, int RB>
-__global__ void __launch_bounds__(1024, 1) cg_apply_col_k(int p, i64 c_lo, i64 c_hi, const int* __restrict__ ell_base,
-                                                          const int* __restrict__ deg,
-                                                          const OffEnt<T>* __restrict__ ell, T gr, Plan pl,
-                                                          const T* __restrict__ P, T* __restrict__ AP,
-                                                          double* partials, CgState* st, int force) {
+__global__ void __launch_bounds__(kColThreads, 1) cg_apply_col_k(int p, i64 c_lo, i64 c_hi,
+                                                                 const int* __restrict__ ell_base,
+                                                                 const int* __restrict__ deg,
+                                                                 const int* __restrict__ order,
+                                                                 const OffEnt<T>* __restrict__ ell, T gr, Plan pl,
+                                                                 const T* __restrict__ P, T* __restrict__ AP,
+                                                                 double* partials, CgState* st, int force) {
   if (!force && st->done) return;
   constexpr int Q = RB / static_cast<int>(sizeof(T));
   constexpr int H = RB / 16;
+  constexpr int KB = 8;
   union Rec {
     uint4 u[H];
     T v[Q];
   };
   extern __shared__ __align__(16) unsigned char smraw[];
   uint4* S = reinterpret_cast<uint4*>(smraw);
+  __shared__ int next_group;
   const i64 c0 = c_lo + static_cast<i64>(blockIdx.x) * Q;
   const int qn = static_cast<int>(min(static_cast<i64>(Q), c_hi - c0));
+  if (threadIdx.x == 0) next_group = blockDim.x >> 5;
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
     Rec r;
 #pragma unroll
@@ -770,36 +801,52 @@ __global__ void __launch_bounds__(1024, 1) cg_apply_col_k(int p, i64 c_lo, i64 c
   __syncthreads();
   double s = 0.0;
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < p; i += blockDim.x) {
-    const int d = deg[i];
-    const OffEnt<T>* e = ell + static_cast<i64>(ell_base[i >> 5]) * 32 + lane;
+  const int groups = (p + 31) >> 5;
+  int gi = threadIdx.x >> 5;
+  while (gi < groups) {
+    const int g = order[gi];
+    const int i = g * 32 + lane;
+    const bool row = i < p;
+    const int d = row ? deg[i] : 0;
+    const OffEnt<T>* e = ell + static_cast<i64>(ell_base[g]) * 32 + lane;
     T acc[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = T(0);
-#pragma unroll 2
-    for (int k = 0; k < d; ++k) {
-      const OffEnt<T> en = e[k * 32];
-      Rec x;
+    for (int k0 = 0; k0 < d; k0 += KB) {
+      OffEnt<T> en[KB];
 #pragma unroll
-      for (int h = 0; h < H; ++h) x.u[h] = S[rec_chunk<H>(en.off, h)];
+      for (int u = 0; u < KB; ++u)
+        if (k0 + u < d) en[u] = e[(k0 + u) * 32];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = madd_entry(acc[q], en.v, x.v[q]);
-    }
-    Rec own;
+      for (int u = 0; u < KB; ++u) {
+        if (k0 + u < d) {
+          Rec x;
 #pragma unroll
-    for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
-    const bool rs = pl.rsel[i] >= 0;
+          for (int h = 0; h < H; ++h) x.u[h] = S[rec_chunk<H>(en[u].off, h)];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      if (q < qn) {
-        const i64 c = c0 + q;
-        const i64 at = i + c * p;
-        T out = add_rn(AP[at], mul_rn(gr, acc[q]));
-        if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
-        AP[at] = out;
-        s += static_cast<double>(own.v[q]) * static_cast<double>(out);
+          for (int q = 0; q < Q; ++q) acc[q] = madd_entry(acc[q], en[u].v, x.v[q]);
+        }
       }
     }
+    if (row) {
+      Rec own;
+#pragma unroll
+      for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
+      const bool rs = pl.rsel[i] >= 0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        if (q < qn) {
+          const i64 c = c0 + q;
+          const i64 at = i + c * p;
+          T out = add_rn(__ldcs(AP + at), mul_rn(gr, acc[q]));
+          if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
+          __stcs(AP + at, out);
+          s += static_cast<double>(own.v[q]) * static_cast<double>(out);
+        }
+      }
+    }
+    if (lane == 0) gi = atomicAdd(&next_group, 1);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
   }
   if (force) return;
   double sv[1] = {s}, tot[1];
@@ -843,7 +890,7 @@ struct BandApply {
   int rpl = 1, rb = 32;
   size_t col_smem = 0;
   DevBuf<OffEnt<T>> ent, ell;
-  DevBuf<int> base, deg;
+  DevBuf<int> base, deg, order;
   const i64* rpc = nullptr;
 
   // Feasible when a Q-column group of P fits in shared memory.
@@ -856,6 +903,7 @@ struct BandApply {
     n = Lc->rows;
     if (!feasible(p)) invalid("band apply: row count too large for the column-group kernel");
     rb = p * 32 <= 200 * 1024 ? 32 : 16;
+    if (const char* e = std::getenv("CPCAG_BAND_RB")) rb = std::atoi(e) == 16 ? 16 : rb;
     col_smem = static_cast<size_t>(p) * rb;
     rpl = 1;
     for (int r : {4, 2}) {
@@ -873,17 +921,23 @@ struct BandApply {
       launched(c);
     }
     const i64 groups = (p + 31) / 32;
-    std::vector<int> hb(static_cast<size_t>(groups));
+    std::vector<int> hb(static_cast<size_t>(groups)), hmd(static_cast<size_t>(groups)), ho(static_cast<size_t>(groups));
     i64 slots = 0;
     for (i64 g = 0; g < groups; ++g) {
       i64 md = 0;
       for (i64 i = g * 32; i < std::min<i64>(p, g * 32 + 32); ++i) md = std::max(md, rpr[i + 1] - rpr[i]);
       hb[g] = static_cast<int>(slots);
+      hmd[g] = static_cast<int>(md);
       slots += md;
     }
+    // Heaviest groups first (longest-processing-time order for the warps).
+    for (i64 g = 0; g < groups; ++g) ho[g] = static_cast<int>(g);
+    std::stable_sort(ho.begin(), ho.end(), [&](int a, int b) { return hmd[a] > hmd[b]; });
     if (slots * 32 >= (i64{1} << 31)) invalid("band apply: L_r too dense for the ELL layout");
     base.alloc(c, groups);
+    order.alloc(c, groups);
     deg.alloc(c, p);
+    CUDA_OK(cudaMemcpyAsync(order.p, ho.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
     ell.alloc(c, std::max<i64>(slots * 32, 1));
     CUDA_OK(cudaMemcpyAsync(base.p, hb.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
     ell_fill_k<T><<<blocks_for(p), kBlock, 0, c->stream>>>(p, pr.rp, pr.ci, pr.v, base.p, ell.p, deg.p);
@@ -926,11 +980,11 @@ struct BandApply {
     KScope ks_(c, "cg_apply_col");
     const unsigned gcb = col_blocks(c_lo, c_hi);
     if (rb == 32)
-      cg_apply_col_k<T, 32><<<gcb, 1024, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
-                                                                ell.p, gr, pl, P, AP, part, st, force);
+      cg_apply_col_k<T, 32><<<gcb, kColThreads, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
+                                                                       order.p, ell.p, gr, pl, P, AP, part, st, force);
     else
-      cg_apply_col_k<T, 16><<<gcb, 1024, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
-                                                                ell.p, gr, pl, P, AP, part, st, force);
+      cg_apply_col_k<T, 16><<<gcb, kColThreads, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
+                                                                       order.p, ell.p, gr, pl, P, AP, part, st, force);
     launched(c);
   }
 };

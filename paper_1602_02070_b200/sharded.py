@@ -76,6 +76,7 @@ class CudaBlockBackend:
         # the block kernels must be ordered with them.
         ctx.set_stream(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
         self.ctx = ctx
+        self._graphs = (Lr, Lc)  # the block keeps raw CSR handles: hold the owners
         self.prec = precision
         self.p, self.n = plan.p, plan.n
         self.c0, self.c1 = c0, c1
