@@ -707,15 +707,32 @@ __device__ __forceinline__ void store_stream(T* p, T v) {
   __stcs(p, v);
 }
 
-// Warp per column: the column's L_c entries are loaded with one coalesced
-// load (lane t holds entry t of the chunk) and broadcast by shuffle, so the
-// gathers of 8 entries are in flight at once; U is stored evict-first so it
-// does not push the band out of L2.
+// Warp per column, lane = row.  Two variants (CPCAG_BAND_V):
+//  1  entries read per step (warp-uniform loads), 4 steps unrolled;
+//     32 registers, full occupancy;
+//  2/3 the column's entries loaded with one coalesced load (lane t holds
+//     entry t) and broadcast by shuffle, the next column's entries
+//     prefetched while this column gathers; 8 steps in flight
+//     (2: 64 registers, 3: 40 registers).
+// U is stored evict-first so it does not push the band out of L2.
 template <typename T, int RPL>
-__global__ void __launch_bounds__(256, 4) cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp,
-                                                       const OffEnt<T>* __restrict__ ent, T gc, i64 cols_per_cta,
-                                                       const T* __restrict__ P, T* __restrict__ U,
-                                                       const CgState* st, int force) {
+__device__ __forceinline__ void band_column_simple(const OffEnt<T>* __restrict__ ent, i64 k0, i64 k1,
+                                                   const T* __restrict__ P, i64 p, i64 r0, const bool (&ok)[RPL],
+                                                   T (&acc)[RPL]) {
+#pragma unroll 4
+  for (i64 k = k0; k < k1; ++k) {
+    const OffEnt<T> e = ent[k];
+    const T* col = P + static_cast<i64>(e.off) * p + r0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+      if (ok[t]) acc[t] = madd_entry(acc[t], e.v, col[32 * t]);
+  }
+}
+
+template <typename T, int RPL, int V>
+__global__ void __launch_bounds__(256, V == 1 ? 8 : (V == 2 ? 4 : 6))
+    cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp, const OffEnt<T>* __restrict__ ent, T gc,
+                    i64 cols_per_cta, const T* __restrict__ P, T* __restrict__ U, const CgState* st, int force) {
   if (!force && st->done) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const i64 r0 = static_cast<i64>(blockIdx.y) * (32 * RPL) + lane;
@@ -727,6 +744,13 @@ __global__ void __launch_bounds__(256, 4) cg_apply_band_k(i64 p, i64 c_lo, i64 c
   // Row pointers of this warp's columns (lane m holds column cb + warp + m*nw).
   const i64 cm = cb + warp + static_cast<i64>(lane) * nw;
   const i64 my_k0 = cm < ce ? rp[cm] : 0, my_k1 = cm < ce ? rp[cm + 1] : 0;
+  OffEnt<T> nxt;
+  nxt.v = T(0);
+  nxt.off = 0;
+  if (V != 1) {
+    const i64 k0 = __shfl_sync(0xffffffffu, my_k0, 0), k1 = __shfl_sync(0xffffffffu, my_k1, 0);
+    if (k0 + lane < k1) nxt = ent[k0 + lane];
+  }
   for (int m = 0;; ++m) {
     const i64 c = cb + warp + static_cast<i64>(m) * nw;
     if (c >= ce) break;
@@ -734,12 +758,18 @@ __global__ void __launch_bounds__(256, 4) cg_apply_band_k(i64 p, i64 c_lo, i64 c
     T acc[RPL];
 #pragma unroll
     for (int t = 0; t < RPL; ++t) acc[t] = T(0);
-    for (i64 kb = k0; kb < k1; kb += 32) {
-      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - kb));
-      OffEnt<T> mine;
-      mine.v = T(0);
-      mine.off = 0;
-      if (lane < cnt) mine = ent[kb + lane];
+    if constexpr (V == 1) {
+      band_column_simple<T, RPL>(ent, k0, k1, P, p, r0, ok, acc);
+    } else {
+      const OffEnt<T> mine = nxt;
+      {  // prefetch the next column's first 32 entries
+        const i64 n0 = __shfl_sync(0xffffffffu, my_k0, (m + 1) & 31);
+        const i64 n1 = __shfl_sync(0xffffffffu, my_k1, (m + 1) & 31);
+        nxt.v = T(0);
+        nxt.off = 0;
+        if (c + nw < ce && n0 + lane < n1) nxt = ent[n0 + lane];
+      }
+      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - k0));
 #pragma unroll 8
       for (int q = 0; q < cnt; ++q) {
         const int j = __shfl_sync(0xffffffffu, mine.off, q);
@@ -749,11 +779,12 @@ __global__ void __launch_bounds__(256, 4) cg_apply_band_k(i64 p, i64 c_lo, i64 c
         for (int t = 0; t < RPL; ++t)
           if (ok[t]) acc[t] = madd_entry(acc[t], v, col[32 * t]);
       }
+      if (k1 - k0 > 32) band_column_simple<T, RPL>(ent, k0 + 32, k1, P, p, r0, ok, acc);
     }
     T* out = U + c * p + r0;
 #pragma unroll
     for (int t = 0; t < RPL; ++t)
-      if (ok[t]) store_stream(out + 32 * t, mul_rn(gc, acc[t]));
+      if (ok[t]) __stcs(out + 32 * t, mul_rn(gc, acc[t]));
   }
 }
 
@@ -768,9 +799,8 @@ __device__ __forceinline__ int rec_chunk(int j, int h) {
 // Row groups (32 rows = one warp's lanes) are handed to warps dynamically,
 // heaviest (largest padded degree) first, from a shared counter; each lane
 // keeps a batch of 8 L_r entries in registers so their loads overlap.
-constexpr int kColThreads = 512;
-template <typename T, int RB>
-__global__ void __launch_bounds__(kColThreads, 1) cg_apply_col_k(int p, i64 c_lo, i64 c_hi,
+template <typename T, int RB, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo, i64 c_hi,
                                                                  const int* __restrict__ ell_base,
                                                                  const int* __restrict__ deg,
                                                                  const int* __restrict__ order,
@@ -780,7 +810,7 @@ __global__ void __launch_bounds__(kColThreads, 1) cg_apply_col_k(int p, i64 c_lo
   if (!force && st->done) return;
   constexpr int Q = RB / static_cast<int>(sizeof(T));
   constexpr int H = RB / 16;
-  constexpr int KB = 8;
+  constexpr int KB = 4;
   union Rec {
     uint4 u[H];
     T v[Q];
@@ -887,8 +917,28 @@ struct BandApply {
   static constexpr i64 kBandBytes = i64{56} << 20;  // L2-resident band budget
   static constexpr int kColsPerCta = 64;
   i64 p = 0, n = 0;
-  int rpl = 1, rb = 32;
+  int rpl = 1, rb = 32, band_v = 1, col_nt = 1024;
   size_t col_smem = 0;
+
+  template <typename F>
+  void with_col_kernel(F&& f) const {
+    if (rb == 32 && col_nt == 1024) f(cg_apply_col_k<T, 32, 1024>);
+    else if (rb == 32) f(cg_apply_col_k<T, 32, 512>);
+    else if (col_nt == 1024) f(cg_apply_col_k<T, 16, 1024>);
+    else f(cg_apply_col_k<T, 16, 512>);
+  }
+  template <int RPL, int V>
+  void launch_band(Ctx* c, dim3 gb, const T* P, T* AP, i64 c_lo, i64 c_hi, T gc, const CgState* st, int force) const {
+    cg_apply_band_k<T, RPL, V><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st,
+                                                          force);
+  }
+  template <int RPL>
+  void launch_band_v(Ctx* c, dim3 gb, const T* P, T* AP, i64 c_lo, i64 c_hi, T gc, const CgState* st,
+                     int force) const {
+    if (band_v == 2) launch_band<RPL, 2>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else if (band_v == 3) launch_band<RPL, 3>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else launch_band<RPL, 1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+  }
   DevBuf<OffEnt<T>> ent, ell;
   DevBuf<int> base, deg, order;
   const i64* rpc = nullptr;
@@ -942,10 +992,9 @@ struct BandApply {
     CUDA_OK(cudaMemcpyAsync(base.p, hb.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
     ell_fill_k<T><<<blocks_for(p), kBlock, 0, c->stream>>>(p, pr.rp, pr.ci, pr.v, base.p, ell.p, deg.p);
     launched(c);
-    if (rb == 32)
-      ensure_smem(cg_apply_col_k<T, 32>, col_smem);
-    else
-      ensure_smem(cg_apply_col_k<T, 16>, col_smem);
+    if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(3, std::atoi(e)));
+    if (const char* e = std::getenv("CPCAG_BAND_NT")) col_nt = std::atoi(e) == 512 ? 512 : 1024;
+    with_col_kernel([&](auto kern) { ensure_smem(kern, col_smem); });
     sync(c);  // hb must outlive the copy
   }
 
@@ -965,26 +1014,17 @@ struct BandApply {
                   static_cast<unsigned>((p + band_rows - 1) / band_rows));
     {
     KScope ks_(c, "cg_apply_band");
-    switch (rpl) {
-      case 4:
-        cg_apply_band_k<T, 4><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
-        break;
-      case 2:
-        cg_apply_band_k<T, 2><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
-        break;
-      default:
-        cg_apply_band_k<T, 1><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
-    }
+    if (rpl == 4) launch_band_v<4>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else if (rpl == 2) launch_band_v<2>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else launch_band_v<1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     launched(c);
     }
     KScope ks_(c, "cg_apply_col");
     const unsigned gcb = col_blocks(c_lo, c_hi);
-    if (rb == 32)
-      cg_apply_col_k<T, 32><<<gcb, kColThreads, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
-                                                                       order.p, ell.p, gr, pl, P, AP, part, st, force);
-    else
-      cg_apply_col_k<T, 16><<<gcb, kColThreads, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p,
-                                                                       order.p, ell.p, gr, pl, P, AP, part, st, force);
+    with_col_kernel([&](auto kern) {
+      kern<<<gcb, col_nt, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p, order.p, ell.p, gr, pl,
+                                                P, AP, part, st, force);
+    });
     launched(c);
   }
 };

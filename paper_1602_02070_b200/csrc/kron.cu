@@ -26,13 +26,18 @@
 namespace cpcag_cuda {
 
 // ------------------------------------------------------------------ components
+// Find with path halving.  Roots only ever link under smaller roots, so
+// every parent pointer points to a smaller index and replacing parent[x] by
+// its grandparent (a plain store racing with other finds) keeps the forest
+// valid.
 __device__ __forceinline__ int uf_root(volatile int* parent, int x) {
-  int p = parent[x];
-  while (p != x) {
-    x = p;
-    p = parent[x];
+  while (true) {
+    const int p = parent[x];
+    if (p == x) return x;
+    const int gp = parent[p];
+    if (gp != p) parent[x] = gp;
+    x = gp;
   }
-  return x;
 }
 
 __global__ void uf_init_k(i64 n, int* parent) {
