@@ -686,20 +686,19 @@ __global__ void pack_ent_k(i64 nnz, const int* __restrict__ ci, const T* __restr
   }
 }
 
+// Row permutation of the band path (rows sorted by L_r degree, see BandApply).
+__global__ void permute_sel_k(i64 p, const int* __restrict__ pos, const int* __restrict__ sel, int* __restrict__ out) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < p) out[pos[i]] = sel[i];
+}
+
 template <typename T>
-__global__ void ell_fill_k(i64 p, const i64* __restrict__ rp, const int* __restrict__ ci, const T* __restrict__ v,
-                           const int* __restrict__ base, OffEnt<T>* __restrict__ ell, int* __restrict__ deg) {
+__global__ void unpermute_rows_k(i64 p, i64 n, const int* __restrict__ pos, const T* __restrict__ src,
+                                 T* __restrict__ dst) {
   const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   if (i >= p) return;
-  const i64 k0 = rp[i], d = rp[i + 1] - k0;
-  OffEnt<T>* dst = ell + static_cast<i64>(base[i >> 5]) * 32 + (i & 31);
-  for (i64 k = 0; k < d; ++k) {
-    OffEnt<T> e;
-    e.v = v[k0 + k];
-    e.off = ci[k0 + k];
-    dst[k * 32] = e;
-  }
-  deg[i] = static_cast<int>(d);
+  const i64 s = pos[i];
+  for (i64 c = blockIdx.y; c < n; c += gridDim.y) dst[i + c * p] = src[s + c * p];
 }
 
 template <typename T>
@@ -730,7 +729,7 @@ __device__ __forceinline__ void band_column_simple(const OffEnt<T>* __restrict__
 }
 
 template <typename T, int RPL, int V>
-__global__ void __launch_bounds__(256, V == 1 ? 8 : (V == 2 ? 4 : 6))
+__global__ void __launch_bounds__(256, (V == 1 || V == 4) ? 8 : (V == 2 ? 4 : (V == 3 ? 6 : 1)))
     cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp, const OffEnt<T>* __restrict__ ent, T gc,
                     i64 cols_per_cta, const T* __restrict__ P, T* __restrict__ U, const CgState* st, int force) {
   if (!force && st->done) return;
@@ -741,6 +740,19 @@ __global__ void __launch_bounds__(256, V == 1 ? 8 : (V == 2 ? 4 : 6))
   bool ok[RPL];
 #pragma unroll
   for (int t = 0; t < RPL; ++t) ok[t] = r0 + 32 * t < p;
+  if constexpr (V == 5) {  // plain: per-column row pointers, plain stores
+    for (i64 c = cb + warp; c < ce; c += nw) {
+      T acc[RPL];
+#pragma unroll
+      for (int t = 0; t < RPL; ++t) acc[t] = T(0);
+      band_column_simple<T, RPL>(ent, rp[c], rp[c + 1], P, p, r0, ok, acc);
+      T* out = U + c * p + r0;
+#pragma unroll
+      for (int t = 0; t < RPL; ++t)
+        if (ok[t]) out[32 * t] = mul_rn(gc, acc[t]);
+    }
+    return;
+  }
   // Row pointers of this warp's columns (lane m holds column cb + warp + m*nw).
   const i64 cm = cb + warp + static_cast<i64>(lane) * nw;
   const i64 my_k0 = cm < ce ? rp[cm] : 0, my_k1 = cm < ce ? rp[cm + 1] : 0;
@@ -758,7 +770,7 @@ __global__ void __launch_bounds__(256, V == 1 ? 8 : (V == 2 ? 4 : 6))
     T acc[RPL];
 #pragma unroll
     for (int t = 0; t < RPL; ++t) acc[t] = T(0);
-    if constexpr (V == 1) {
+    if constexpr (V == 1 || V == 4) {
       band_column_simple<T, RPL>(ent, k0, k1, P, p, r0, ok, acc);
     } else {
       const OffEnt<T> mine = nxt;
@@ -783,8 +795,14 @@ __global__ void __launch_bounds__(256, V == 1 ? 8 : (V == 2 ? 4 : 6))
     }
     T* out = U + c * p + r0;
 #pragma unroll
-    for (int t = 0; t < RPL; ++t)
-      if (ok[t]) __stcs(out + 32 * t, mul_rn(gc, acc[t]));
+    for (int t = 0; t < RPL; ++t) {
+      if (ok[t]) {
+        if constexpr (V == 4)
+          out[32 * t] = mul_rn(gc, acc[t]);
+        else
+          __stcs(out + 32 * t, mul_rn(gc, acc[t]));
+      }
+    }
   }
 }
 
@@ -937,10 +955,13 @@ struct BandApply {
                      int force) const {
     if (band_v == 2) launch_band<RPL, 2>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     else if (band_v == 3) launch_band<RPL, 3>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else if (band_v == 4) launch_band<RPL, 4>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else if (band_v == 5) launch_band<RPL, 5>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     else launch_band<RPL, 1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
   }
   DevBuf<OffEnt<T>> ent, ell;
-  DevBuf<int> base, deg, order;
+  DevBuf<int> base, deg, order, pos;
+  bool permuted = false;
   const i64* rpc = nullptr;
 
   // Feasible when a Q-column group of P fits in shared memory.
@@ -948,7 +969,12 @@ struct BandApply {
   // Auto choice: the iterate does not fit in L2.
   static bool preferred(i64 p, i64 n) { return static_cast<double>(p) * n * sizeof(T) > 96e6 && feasible(p); }
 
-  void build(Ctx* c, Csr* Lr, Csr* Lc, const std::vector<i64>& rpr) {
+  // permute: store rows in descending-degree order (pos[row] = stored row),
+  // so the 32-row ELL groups are nearly uniform: kNN graphs in high dimension
+  // have hubs (cfg3 row graph: mean degree 18, max 495), and natural-order
+  // groups pad to ~5x the entries.  Each row keeps its CSR entry order (only
+  // the column labels are mapped), so per-entry arithmetic is unchanged.
+  void build(Ctx* c, Csr* Lr, Csr* Lc, const std::vector<i64>& rpr, bool permute) {
     p = Lr->rows;
     n = Lc->rows;
     if (!feasible(p)) invalid("band apply: row count too large for the column-group kernel");
@@ -970,29 +996,64 @@ struct BandApply {
       pack_ent_k<T><<<blocks_for(nnz_c), kBlock, 0, c->stream>>>(nnz_c, pc.ci, pc.v, ent.p);
       launched(c);
     }
+    const i64 nnz_r = rpr[p];
+    std::vector<int> hci(static_cast<size_t>(nnz_r));
+    std::vector<T> hv(static_cast<size_t>(nnz_r));
+    if (nnz_r) {
+      CUDA_OK(cudaMemcpyAsync(hci.data(), pr.ci, sizeof(int) * nnz_r, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaMemcpyAsync(hv.data(), pr.v, sizeof(T) * nnz_r, cudaMemcpyDeviceToHost, c->stream));
+    }
+    sync(c);
+    std::vector<int> ord(static_cast<size_t>(p)), hpos(static_cast<size_t>(p));
+    for (i64 i = 0; i < p; ++i) ord[i] = static_cast<int>(i);
+    permuted = permute;
+    if (permute)
+      std::stable_sort(ord.begin(), ord.end(),
+                       [&](int a, int b) { return rpr[a + 1] - rpr[a] > rpr[b + 1] - rpr[b]; });
+    for (i64 r = 0; r < p; ++r) hpos[ord[r]] = static_cast<int>(r);
     const i64 groups = (p + 31) / 32;
     std::vector<int> hb(static_cast<size_t>(groups)), hmd(static_cast<size_t>(groups)), ho(static_cast<size_t>(groups));
+    std::vector<int> hdeg(static_cast<size_t>(p));
     i64 slots = 0;
     for (i64 g = 0; g < groups; ++g) {
       i64 md = 0;
-      for (i64 i = g * 32; i < std::min<i64>(p, g * 32 + 32); ++i) md = std::max(md, rpr[i + 1] - rpr[i]);
+      for (i64 r = g * 32; r < std::min<i64>(p, g * 32 + 32); ++r) {
+        const i64 d = rpr[ord[r] + 1] - rpr[ord[r]];
+        hdeg[r] = static_cast<int>(d);
+        md = std::max(md, d);
+      }
       hb[g] = static_cast<int>(slots);
       hmd[g] = static_cast<int>(md);
       slots += md;
     }
+    if (slots * 32 >= (i64{1} << 31)) invalid("band apply: L_r too dense for the ELL layout");
     // Heaviest groups first (longest-processing-time order for the warps).
     for (i64 g = 0; g < groups; ++g) ho[g] = static_cast<int>(g);
     std::stable_sort(ho.begin(), ho.end(), [&](int a, int b) { return hmd[a] > hmd[b]; });
-    if (slots * 32 >= (i64{1} << 31)) invalid("band apply: L_r too dense for the ELL layout");
+    std::vector<OffEnt<T>> hell(static_cast<size_t>(std::max<i64>(slots * 32, 1)));
+    for (auto& e : hell) {
+      e.v = T(0);
+      e.off = 0;
+    }
+    for (i64 r = 0; r < p; ++r) {
+      const i64 old = ord[r], k0 = rpr[old];
+      OffEnt<T>* dst = hell.data() + static_cast<i64>(hb[r >> 5]) * 32 + (r & 31);
+      for (i64 k = 0; k < hdeg[r]; ++k) {
+        dst[k * 32].v = hv[k0 + k];
+        dst[k * 32].off = hpos[hci[k0 + k]];
+      }
+    }
     base.alloc(c, groups);
     order.alloc(c, groups);
     deg.alloc(c, p);
-    CUDA_OK(cudaMemcpyAsync(order.p, ho.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
-    ell.alloc(c, std::max<i64>(slots * 32, 1));
+    pos.alloc(c, p);
+    ell.alloc(c, hell.size());
     CUDA_OK(cudaMemcpyAsync(base.p, hb.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
-    ell_fill_k<T><<<blocks_for(p), kBlock, 0, c->stream>>>(p, pr.rp, pr.ci, pr.v, base.p, ell.p, deg.p);
-    launched(c);
-    if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(3, std::atoi(e)));
+    CUDA_OK(cudaMemcpyAsync(order.p, ho.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(deg.p, hdeg.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ell.p, hell.data(), sizeof(OffEnt<T>) * hell.size(), cudaMemcpyHostToDevice, c->stream));
+    if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(5, std::atoi(e)));
     if (const char* e = std::getenv("CPCAG_BAND_NT")) col_nt = std::atoi(e) == 512 ? 512 : 1024;
     with_col_kernel([&](auto kern) { ensure_smem(kern, col_smem); });
     sync(c);  // hb must outlive the copy
@@ -1074,7 +1135,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     scatter_sel_k<<<blocks_for(rho_c), kBlock, 0, c->stream>>>(omc.p, rho_c, csel.p);
     launched(c);
   }
-  const Plan pl{rsel.p, csel.p, rho_r};
+  Plan pl{rsel.p, csel.p, rho_r};
   const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
   const T gr = static_cast<T>(gbar_r), gc = static_cast<T>(gbar_c);
 
@@ -1127,9 +1188,18 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const size_t fast_smem = static_cast<size_t>(max_er + max_ec) * sizeof(OffEnt<T>) + sizeof(int) * (cols_per_cta + 2) + 16;
   if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
   BandApply<T> band;
+  DevBuf<int> rsel_perm;
   if (variant == "band") {
-    band.build(c, Lr, Lc, rpr);
+    const char* pe = std::getenv("CPCAG_BAND_PERM");
+    band.build(c, Lr, Lc, rpr, !(pe && std::string(pe) == "0"));
     if (part.n < band.col_blocks(0, n)) part.alloc(c, band.col_blocks(0, n));
+    if (band.permuted && p) {
+      // Every p x n iterate is stored with rows in the band's order.
+      rsel_perm.alloc(c, p);
+      permute_sel_k<<<blocks_for(p), kBlock, 0, c->stream>>>(p, band.pos.p, rsel.p, rsel_perm.p);
+      launched(c);
+      pl.rsel = rsel_perm.p;
+    }
   }
   if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
   if (variant == "panel") {
@@ -1220,6 +1290,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "band") {
     band.apply(c, X, AP.p, 0, n, pl, gr, gc, part.p, st.p, 1);
     cg_true_res_ap_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, AP.p, part.p, st.p);
+    if (band.permuted) {  // back to the caller's row order
+      launched(c);
+      CUDA_OK(cudaMemcpyAsync(AP.p, X, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
+      unpermute_rows_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, band.pos.p, AP.p, X);
+    }
   } else {
     cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, Xt, X, part.p, st.p);
   }
@@ -1408,11 +1483,11 @@ extern "C" int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int
     if (variant == "band") {
       if (precision == CPCAG_F64) {
         blk->band64 = std::make_unique<BandApply<double>>();
-        blk->band64->build(c, A, B, rpr);
+        blk->band64->build(c, A, B, rpr, false);
         nparts = std::max<size_t>(nparts, blk->band64->col_blocks(c_begin, c_end));
       } else {
         blk->band32 = std::make_unique<BandApply<float>>();
-        blk->band32->build(c, A, B, rpr);
+        blk->band32->build(c, A, B, rpr, false);
         nparts = std::max<size_t>(nparts, blk->band32->col_blocks(c_begin, c_end));
       }
     } else {

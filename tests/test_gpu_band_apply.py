@@ -73,7 +73,10 @@ def test_band_apply_fp64_bit_exact(P, ctx, band, p, n, c0, c1):
     be.close()
 
 
-def test_band_decode_fp64_matches_oracle(P, ctx, band):
+@pytest.mark.parametrize("perm", ["1", "0"])
+def test_band_decode_fp64_matches_oracle(P, ctx, band, monkeypatch, perm):
+    # perm 1: iterates stored in descending-L_r-degree row order (the default)
+    monkeypatch.setenv("CPCAG_BAND_PERM", perm)
     Lr, Lc, plan_o, _ = _apply_case(150, 210, 3)
     Xt = np.random.default_rng(4).standard_normal((plan_o.rho_r, plan_o.rho_c))
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
