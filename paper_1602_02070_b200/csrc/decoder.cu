@@ -814,14 +814,26 @@ __device__ __forceinline__ int rec_chunk(int j, int h) {
     return j;
 }
 
-// Row groups (32 rows = one warp's lanes) are handed to warps dynamically,
-// heaviest (largest padded degree) first, from a shared counter; each lane
-// keeps a batch of 8 L_r entries in registers so their loads overlap.
+// The L_r sweep works on "virtual rows": a stored row, or (fp32 only) a
+// chunk of at most `split_cap` entries of a long row, so one hub row (degree
+// 495 in the cfg3 row graph) cannot hold the whole CTA on its sequential
+// chain.  32 virtual rows form an ELL group (lane = virtual row); groups are
+// dealt to warps round-robin in descending cost, a fixed assignment, so the
+// per-thread dot partials and hence <P, AP> are deterministic.  A chunk
+// writes its partial sums to shared memory; after the sweep warp 0 adds the
+// chunks of each split row in chunk order and finishes those rows.
+struct ColMeta {
+  const int* vrow;    // stored row of each virtual row (-1 = padding lane)
+  const int* vdeg;    // entries of each virtual row
+  const int* vslot;   // partial-sum slot, -1 = unsplit row (written directly)
+  const int* base;    // ELL slot base per group
+  const int* order;   // groups in descending cost
+  const int* split_row, *split_first, *split_n;
+  int groups, nsplit, nslots;
+};
+
 template <typename T, int RB, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo, i64 c_hi,
-                                                                 const int* __restrict__ ell_base,
-                                                                 const int* __restrict__ deg,
-                                                                 const int* __restrict__ order,
+__global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo, i64 c_hi, ColMeta cm,
                                                                  const OffEnt<T>* __restrict__ ell, T gr, Plan pl,
                                                                  const T* __restrict__ P, T* __restrict__ AP,
                                                                  double* partials, CgState* st, int force) {
@@ -835,10 +847,9 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
   };
   extern __shared__ __align__(16) unsigned char smraw[];
   uint4* S = reinterpret_cast<uint4*>(smraw);
-  __shared__ int next_group;
+  T* part_sm = reinterpret_cast<T*>(smraw + static_cast<size_t>(p) * RB);
   const i64 c0 = c_lo + static_cast<i64>(blockIdx.x) * Q;
   const int qn = static_cast<int>(min(static_cast<i64>(Q), c_hi - c0));
-  if (threadIdx.x == 0) next_group = blockDim.x >> 5;
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
     Rec r;
 #pragma unroll
@@ -848,15 +859,29 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
   }
   __syncthreads();
   double s = 0.0;
-  const int lane = threadIdx.x & 31;
-  const int groups = (p + 31) >> 5;
-  int gi = threadIdx.x >> 5;
-  while (gi < groups) {
-    const int g = order[gi];
-    const int i = g * 32 + lane;
-    const bool row = i < p;
-    const int d = row ? deg[i] : 0;
-    const OffEnt<T>* e = ell + static_cast<i64>(ell_base[g]) * 32 + lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto finish = [&](int i, const T (&acc)[Q]) {
+    Rec own;
+#pragma unroll
+    for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
+    const bool rs = pl.rsel[i] >= 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      if (q < qn) {
+        const i64 c = c0 + q;
+        const i64 at = i + c * p;
+        T out = add_rn(__ldcs(AP + at), mul_rn(gr, acc[q]));
+        if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
+        __stcs(AP + at, out);
+        s += static_cast<double>(own.v[q]) * static_cast<double>(out);
+      }
+    }
+  };
+  for (int it = warp; it < cm.groups; it += nw) {
+    const int g = cm.order[it];
+    const int v = g * 32 + lane;
+    const int i = cm.vrow[v], d = cm.vdeg[v];
+    const OffEnt<T>* e = ell + static_cast<i64>(cm.base[g]) * 32 + lane;
     T acc[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = T(0);
@@ -876,25 +901,31 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
         }
       }
     }
-    if (row) {
-      Rec own;
+    if (i >= 0) {
+      const int slot = cm.vslot[v];
+      if (slot < 0) {
+        finish(i, acc);
+      } else {
 #pragma unroll
-      for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
-      const bool rs = pl.rsel[i] >= 0;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        if (q < qn) {
-          const i64 c = c0 + q;
-          const i64 at = i + c * p;
-          T out = add_rn(__ldcs(AP + at), mul_rn(gr, acc[q]));
-          if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
-          __stcs(AP + at, out);
-          s += static_cast<double>(own.v[q]) * static_cast<double>(out);
-        }
+        for (int q = 0; q < Q; ++q) part_sm[slot * Q + q] = acc[q];
       }
     }
-    if (lane == 0) gi = atomicAdd(&next_group, 1);
-    gi = __shfl_sync(0xffffffffu, gi, 0);
+  }
+  if (cm.nsplit > 0) {
+    __syncthreads();
+    if (warp == 0) {
+      for (int t = lane; t < cm.nsplit; t += 32) {
+        const int f = cm.split_first[t], nc = cm.split_n[t];
+        T acc[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          T tot = T(0);
+          for (int ch = 0; ch < nc; ++ch) tot = add_rn(tot, part_sm[(f + ch) * Q + q]);
+          acc[q] = tot;
+        }
+        finish(cm.split_row[t], acc);
+      }
+    }
   }
   if (force) return;
   double sv[1] = {s}, tot[1];
@@ -960,7 +991,8 @@ struct BandApply {
     else launch_band<RPL, 1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
   }
   DevBuf<OffEnt<T>> ent, ell;
-  DevBuf<int> base, deg, order, pos;
+  DevBuf<int> base, order, pos, vrow, vdeg, vslot, split_row, split_first, split_n;
+  ColMeta meta{};
   bool permuted = false;
   const i64* rpc = nullptr;
 
@@ -1011,23 +1043,53 @@ struct BandApply {
       std::stable_sort(ord.begin(), ord.end(),
                        [&](int a, int b) { return rpr[a + 1] - rpr[a] > rpr[b + 1] - rpr[b]; });
     for (i64 r = 0; r < p; ++r) hpos[ord[r]] = static_cast<int>(r);
-    const i64 groups = (p + 31) / 32;
+    // Virtual rows: fp64 keeps whole rows (bit-exact per-entry order); fp32
+    // cuts rows longer than split_cap into chunks (their partial sums are
+    // added in chunk order, a different rounding within the fp32 tolerance).
+    i64 cap = sizeof(T) == 4 ? 64 : (i64{1} << 40);
+    if (const char* e = std::getenv("CPCAG_BAND_SPLIT")) cap = std::max<i64>(8, std::atoll(e));
+    if (sizeof(T) == 8) cap = i64{1} << 40;
+    struct VRow {
+      int row;
+      i64 k0, len;
+      int slot;
+    };
+    std::vector<VRow> vr;
+    std::vector<int> srow, sfirst, sn;
+    int nslots = 0;
+    vr.reserve(static_cast<size_t>(p));
+    for (i64 r = 0; r < p; ++r) {  // chunks of split rows first (longest first)
+      const i64 d = rpr[ord[r] + 1] - rpr[ord[r]];
+      if (d <= cap) continue;
+      srow.push_back(static_cast<int>(r));
+      sfirst.push_back(nslots);
+      sn.push_back(static_cast<int>((d + cap - 1) / cap));
+      for (i64 k = 0; k < d; k += cap) vr.push_back({static_cast<int>(r), k, std::min(cap, d - k), nslots++});
+    }
+    std::stable_sort(vr.begin(), vr.end(), [](const VRow& a, const VRow& b) { return a.len > b.len; });
+    for (i64 r = 0; r < p; ++r) {  // then whole rows in stored (descending-degree) order
+      const i64 d = rpr[ord[r] + 1] - rpr[ord[r]];
+      if (d <= cap) vr.push_back({static_cast<int>(r), 0, d, -1});
+    }
+    const i64 nv = static_cast<i64>(vr.size());
+    const i64 groups = (nv + 31) / 32;
     std::vector<int> hb(static_cast<size_t>(groups)), hmd(static_cast<size_t>(groups)), ho(static_cast<size_t>(groups));
-    std::vector<int> hdeg(static_cast<size_t>(p));
+    std::vector<int> hvrow(static_cast<size_t>(groups * 32), -1), hvdeg(static_cast<size_t>(groups * 32), 0),
+        hvslot(static_cast<size_t>(groups * 32), -1);
     i64 slots = 0;
     for (i64 g = 0; g < groups; ++g) {
       i64 md = 0;
-      for (i64 r = g * 32; r < std::min<i64>(p, g * 32 + 32); ++r) {
-        const i64 d = rpr[ord[r] + 1] - rpr[ord[r]];
-        hdeg[r] = static_cast<int>(d);
-        md = std::max(md, d);
+      for (i64 v = g * 32; v < std::min<i64>(nv, g * 32 + 32); ++v) {
+        hvrow[v] = vr[v].row;
+        hvdeg[v] = static_cast<int>(vr[v].len);
+        hvslot[v] = vr[v].slot;
+        md = std::max(md, vr[v].len);
       }
       hb[g] = static_cast<int>(slots);
       hmd[g] = static_cast<int>(md);
       slots += md;
     }
     if (slots * 32 >= (i64{1} << 31)) invalid("band apply: L_r too dense for the ELL layout");
-    // Heaviest groups first (longest-processing-time order for the warps).
     for (i64 g = 0; g < groups; ++g) ho[g] = static_cast<int>(g);
     std::stable_sort(ho.begin(), ho.end(), [&](int a, int b) { return hmd[a] > hmd[b]; });
     std::vector<OffEnt<T>> hell(static_cast<size_t>(std::max<i64>(slots * 32, 1)));
@@ -1035,24 +1097,35 @@ struct BandApply {
       e.v = T(0);
       e.off = 0;
     }
-    for (i64 r = 0; r < p; ++r) {
-      const i64 old = ord[r], k0 = rpr[old];
-      OffEnt<T>* dst = hell.data() + static_cast<i64>(hb[r >> 5]) * 32 + (r & 31);
-      for (i64 k = 0; k < hdeg[r]; ++k) {
+    for (i64 v = 0; v < nv; ++v) {
+      const i64 old = ord[vr[v].row], k0 = rpr[old] + vr[v].k0;
+      OffEnt<T>* dst = hell.data() + static_cast<i64>(hb[v >> 5]) * 32 + (v & 31);
+      for (i64 k = 0; k < vr[v].len; ++k) {
         dst[k * 32].v = hv[k0 + k];
         dst[k * 32].off = hpos[hci[k0 + k]];
       }
     }
-    base.alloc(c, groups);
-    order.alloc(c, groups);
-    deg.alloc(c, p);
-    pos.alloc(c, p);
+    const i64 ns = static_cast<i64>(srow.size());
+    auto up = [&](DevBuf<int>& d, const std::vector<int>& h) {
+      d.alloc(c, std::max<size_t>(h.size(), 1));
+      if (!h.empty())
+        CUDA_OK(cudaMemcpyAsync(d.p, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, c->stream));
+    };
+    up(base, hb);
+    up(order, ho);
+    up(vrow, hvrow);
+    up(vdeg, hvdeg);
+    up(vslot, hvslot);
+    up(split_row, srow);
+    up(split_first, sfirst);
+    up(split_n, sn);
+    up(pos, hpos);
     ell.alloc(c, hell.size());
-    CUDA_OK(cudaMemcpyAsync(base.p, hb.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(order.p, ho.data(), sizeof(int) * groups, cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(deg.p, hdeg.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
-    CUDA_OK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
     CUDA_OK(cudaMemcpyAsync(ell.p, hell.data(), sizeof(OffEnt<T>) * hell.size(), cudaMemcpyHostToDevice, c->stream));
+    meta = ColMeta{vrow.p, vdeg.p, vslot.p, base.p, order.p, split_row.p, split_first.p, split_n.p,
+                   static_cast<int>(groups), static_cast<int>(ns), nslots};
+    col_smem = static_cast<size_t>(p) * rb + static_cast<size_t>(nslots) * rb;
+    if (col_smem > 220 * 1024) invalid("band apply: column group and split partials exceed shared memory");
     if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(5, std::atoi(e)));
     if (const char* e = std::getenv("CPCAG_BAND_NT")) col_nt = std::atoi(e) == 512 ? 512 : 1024;
     with_col_kernel([&](auto kern) { ensure_smem(kern, col_smem); });
@@ -1083,8 +1156,8 @@ struct BandApply {
     KScope ks_(c, "cg_apply_col");
     const unsigned gcb = col_blocks(c_lo, c_hi);
     with_col_kernel([&](auto kern) {
-      kern<<<gcb, col_nt, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, base.p, deg.p, order.p, ell.p, gr, pl,
-                                                P, AP, part, st, force);
+      kern<<<gcb, col_nt, col_smem, c->stream>>>(static_cast<int>(p), c_lo, c_hi, meta, ell.p, gr, pl, P, AP, part,
+                                                st, force);
     });
     launched(c);
   }

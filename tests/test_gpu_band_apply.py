@@ -110,3 +110,21 @@ def test_band_kernels_are_the_ones_launched(P, ctx, band):
     names = set(ctx.kernel_times())
     ctx.enable_kernel_timing(False)
     assert {"cg_apply_band", "cg_apply_col"} <= names
+
+
+@pytest.mark.parametrize("split", ["8", "64"])
+def test_band_decode_fp32_split_rows_deterministic(P, ctx, band, monkeypatch, split):
+    # split 8 cuts most rows into chunks (partial sums combined in chunk order)
+    monkeypatch.setenv("CPCAG_BAND_SPLIT", split)
+    Lr, Lc, plan_o, _ = _apply_case(333, 260, 29, dim=3)
+    Xt = np.random.default_rng(7).standard_normal((plan_o.rho_r, plan_o.rho_c)).astype(np.float32)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    g = P.SpectralGap(lambda_k1=1.0)
+    cfg = P.DecoderConfig(1.0, 1e-8, 60)
+    r1 = P.alternate_decode(Xt, plan, dLr, dLc, g, g, cfg, ctx=ctx)
+    r2 = P.alternate_decode(Xt, plan, dLr, dLc, g, g, cfg, ctx=ctx)
+    assert np.array_equal(r1.X, r2.X)  # fixed warp assignment: deterministic dots
+    ro = O.alternate_decode(Xt.astype(np.float64), plan_o, Lr, Lc, 1.0, 1.0, 1.0, 1e-8, 60)
+    assert r1.iterations == ro.iterations
+    assert rel(r1.X, ro.X) <= 1e-4
