@@ -14,6 +14,7 @@
 // Every scalar lives on the device; the host polls the done flag once per
 // chunk of iterations.
 #include <algorithm>
+#include <cstdio>
 #include <memory>
 #include <cstdlib>
 #include <string>
@@ -830,7 +831,14 @@ struct ColMeta {
   const int* order;   // groups in descending cost
   const int* split_row, *split_first, *split_n;
   int groups, nsplit, nslots;
+  unsigned long long* prof;  // diagnostics (CPCAG_BAND_PROF): per-CTA phase times, else null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <typename T, int RB, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo, i64 c_hi, ColMeta cm,
@@ -848,8 +856,23 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
   extern __shared__ __align__(16) unsigned char smraw[];
   uint4* S = reinterpret_cast<uint4*>(smraw);
   T* part_sm = reinterpret_cast<T*>(smraw + static_cast<size_t>(p) * RB);
+  // per-group and per-split-row dot partials (summed in index order: the
+  // result does not depend on which warp took which group)
+  double* dot_sm = reinterpret_cast<double*>(smraw + static_cast<size_t>(p) * RB + static_cast<size_t>(cm.nslots) * RB);
+  __shared__ int next_item;
+  __shared__ unsigned long long pt[4];
   const i64 c0 = c_lo + static_cast<i64>(blockIdx.x) * Q;
   const int qn = static_cast<int>(min(static_cast<i64>(Q), c_hi - c0));
+  const bool prof = cm.prof != nullptr && blockIdx.x < 4096;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    next_item = nw;
+    if (prof) {
+      pt[0] = gtimer();
+      pt[2] = ~0ull;
+      pt[3] = 0;
+    }
+  }
   for (int j = threadIdx.x; j < p; j += blockDim.x) {
     Rec r;
 #pragma unroll
@@ -858,13 +881,15 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
     for (int h = 0; h < H; ++h) S[rec_chunk<H>(j, h)] = r.u[h];
   }
   __syncthreads();
-  double s = 0.0;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  auto finish = [&](int i, const T (&acc)[Q]) {
+  if (prof && threadIdx.x == 0) pt[1] = gtimer();
+  // Finishes stored row i: AP = U + gr x2 (+ P on the sampled grid); returns
+  // this row's contribution to <P, AP>.
+  auto finish = [&](int i, const T (&acc)[Q]) -> double {
     Rec own;
 #pragma unroll
     for (int h = 0; h < H; ++h) own.u[h] = S[rec_chunk<H>(i, h)];
     const bool rs = pl.rsel[i] >= 0;
+    double d = 0.0;
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       if (q < qn) {
@@ -873,11 +898,12 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
         T out = add_rn(__ldcs(AP + at), mul_rn(gr, acc[q]));
         if (rs && pl.csel[c] >= 0) out = add_rn(out, own.v[q]);
         __stcs(AP + at, out);
-        s += static_cast<double>(own.v[q]) * static_cast<double>(out);
+        d += static_cast<double>(own.v[q]) * static_cast<double>(out);
       }
     }
+    return d;
   };
-  for (int it = warp; it < cm.groups; it += nw) {
+  for (int it = warp; it < cm.groups;) {
     const int g = cm.order[it];
     const int v = g * 32 + lane;
     const int i = cm.vrow[v], d = cm.vdeg[v];
@@ -901,34 +927,54 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo,
         }
       }
     }
+    double dg = 0.0;
     if (i >= 0) {
       const int slot = cm.vslot[v];
       if (slot < 0) {
-        finish(i, acc);
+        dg = finish(i, acc);
       } else {
 #pragma unroll
         for (int q = 0; q < Q; ++q) part_sm[slot * Q + q] = acc[q];
       }
     }
+    dg = warp_sum(dg);
+    if (lane == 0) {
+      dot_sm[g] = dg;
+      it = atomicAdd(&next_item, 1);
+    }
+    it = __shfl_sync(0xffffffffu, it, 0);
+  }
+  if (prof && lane == 0) {
+    const unsigned long long t = gtimer();
+    atomicMin(&pt[2], t);
+    atomicMax(&pt[3], t);
   }
   if (cm.nsplit > 0) {
     __syncthreads();
-    if (warp == 0) {
-      for (int t = lane; t < cm.nsplit; t += 32) {
-        const int f = cm.split_first[t], nc = cm.split_n[t];
-        T acc[Q];
+    for (int t = threadIdx.x; t < cm.nsplit; t += blockDim.x) {
+      const int f = cm.split_first[t], nc = cm.split_n[t];
+      T acc[Q];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          T tot = T(0);
-          for (int ch = 0; ch < nc; ++ch) tot = add_rn(tot, part_sm[(f + ch) * Q + q]);
-          acc[q] = tot;
-        }
-        finish(cm.split_row[t], acc);
+      for (int q = 0; q < Q; ++q) {
+        T tot = T(0);
+        for (int ch = 0; ch < nc; ++ch) tot = add_rn(tot, part_sm[(f + ch) * Q + q]);
+        acc[q] = tot;
       }
+      dot_sm[cm.groups + t] = finish(cm.split_row[t], acc);
     }
   }
+  __syncthreads();
+  if (prof && threadIdx.x == 0) {
+    unsigned long long* o = cm.prof + static_cast<i64>(blockIdx.x) * 8;
+    o[0] = pt[0];
+    o[1] = pt[1];
+    o[2] = pt[2];
+    o[3] = pt[3];
+    o[4] = gtimer();
+  }
   if (force) return;
-  double sv[1] = {s}, tot[1];
+  double sv[1] = {0.0}, tot[1];
+  for (int t = threadIdx.x; t < cm.groups + cm.nsplit; t += blockDim.x) sv[0] += dot_sm[t];
   if (grid_sum_last<1>(sv, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
     const double curv = tot[0];
     st->curv = curv;
@@ -993,7 +1039,33 @@ struct BandApply {
   DevBuf<OffEnt<T>> ent, ell;
   DevBuf<int> base, order, pos, vrow, vdeg, vslot, split_row, split_first, split_n;
   ColMeta meta{};
+  DevBuf<unsigned long long> prof_buf;
   bool permuted = false;
+
+  // CPCAG_BAND_PROF: phase times of the first 4096 column-group CTAs of the
+  // last apply (staging, first/last warp done, CTA end), printed to stderr.
+  void report_prof(Ctx* c) const {
+    if (!meta.prof) return;
+    std::vector<unsigned long long> h(4096 * 8);
+    CUDA_OK(cudaMemcpy(h.data(), prof_buf.p, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+    double a = 0, b = 0, d = 0, e = 0, cnt = 0;
+    unsigned long long t_min = ~0ull, t_max = 0;
+    for (int k = 0; k < 4096; ++k) {
+      const unsigned long long* o = h.data() + k * 8;
+      if (!o[0] || !o[4]) continue;
+      a += o[1] - o[0];
+      b += o[2] - o[1];
+      d += o[3] - o[1];
+      e += o[4] - o[0];
+      cnt += 1;
+      t_min = std::min(t_min, o[0]);
+      t_max = std::max(t_max, o[4]);
+    }
+    if (cnt > 0)
+      std::fprintf(stderr, "[band prof] ctas %.0f  stage %.2f us  first-warp %.2f us  last-warp %.2f us  cta %.2f us  "
+                   "span %.1f us\n", cnt, a / cnt / 1e3, b / cnt / 1e3, d / cnt / 1e3, e / cnt / 1e3,
+                   static_cast<double>(t_max - t_min) / 1e3);
+  }
   const i64* rpc = nullptr;
 
   // Feasible when a Q-column group of P fits in shared memory.
@@ -1123,8 +1195,14 @@ struct BandApply {
     ell.alloc(c, hell.size());
     CUDA_OK(cudaMemcpyAsync(ell.p, hell.data(), sizeof(OffEnt<T>) * hell.size(), cudaMemcpyHostToDevice, c->stream));
     meta = ColMeta{vrow.p, vdeg.p, vslot.p, base.p, order.p, split_row.p, split_first.p, split_n.p,
-                   static_cast<int>(groups), static_cast<int>(ns), nslots};
-    col_smem = static_cast<size_t>(p) * rb + static_cast<size_t>(nslots) * rb;
+                   static_cast<int>(groups), static_cast<int>(ns), nslots, nullptr};
+    if (std::getenv("CPCAG_BAND_PROF")) {
+      prof_buf.alloc(c, 4096 * 8);
+      prof_buf.zero(c);
+      meta.prof = prof_buf.p;
+    }
+    col_smem = static_cast<size_t>(p) * rb + static_cast<size_t>(nslots) * rb +
+               sizeof(double) * static_cast<size_t>(groups + ns);
     if (col_smem > 220 * 1024) invalid("band apply: column group and split partials exceed shared memory");
     if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(5, std::atoi(e)));
     if (const char* e = std::getenv("CPCAG_BAND_NT")) col_nt = std::atoi(e) == 512 ? 512 : 1024;
@@ -1353,6 +1431,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     }
     host = read_back(c, st.p);
   }
+  if (variant == "band") band.report_prof(c);
   if (host.err)
     runtime("pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(host.err_it));
   if (host.zero_rhs) {
