@@ -212,6 +212,40 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
                                 const cpcag_decoder_config* cfg, void* X, int* converged,
                                 int64_t* iterations);
 
+/* DecoderConfig fields the approximate decoder reads (decoders.hpp:13-22). */
+typedef struct cpcag_approx_config {
+  double delta_for_scaling; /* default 0; sigma scale sqrt(np / (rho_r rho_c (1 - delta))) */
+  double rank_threshold;    /* default 0.1; k = #{sigma_i / sigma_1 >= threshold} */
+  double pcg_tol;           /* default 1e-10 (upsampling solves) */
+  int64_t pcg_max_iter;     /* default 5000 */
+} cpcag_approx_config;
+
+/* thin_svd (eigs.cpp:53-57): A (m x n, fp64 col-major) = U diag(sigma) V^T
+ * with q = min(m, n): U m x q, sigma q (descending), V n x q.  Column signs
+ * are the solver's (the reference's JacobiSVD leaves them unspecified too).
+ * Non-finite input -> CPCAG_ERR_INVALID_ARGUMENT "thin_svd: non-finite input". */
+int cpcag_cuda_thin_svd(cpcag_ctx ctx, const double* A, int64_t m, int64_t n, double* U, double* sigma,
+                        double* V);
+
+/* graph_upsample (decoders.hpp:37-38, decoders.cpp:72-121): S (n x r, fp64
+ * col-major) equals R (n_known x r) on the rows `known` and solves
+ * L_aa S_a = -L_ab R on the rest, one Jacobi PCG per column (batched).
+ * Errors as the reference: index out of range / duplicate index
+ * (invalid argument); a component without a known node, an interior solve
+ * that does not converge, PCG breakdown (runtime). */
+int cpcag_cuda_graph_upsample(cpcag_ctx ctx, cpcag_csr L, const int64_t* known, int64_t n_known, const double* R,
+                              int64_t r, double pcg_tol, int64_t pcg_max_iter, double* S);
+
+/* approx_decode (decoders.hpp:64-72, decoders.cpp:188-225): thin SVD of Xt,
+ * rank k at sigma_k / sigma_1 >= rank_threshold, graph_upsample of both
+ * factors, unit columns, sign alignment, sigma rescaling, X = U S V^T (p x n,
+ * `precision`).  *k receives the rank; when 0 < k <= k_cap the factors are
+ * also written (fp64: U p x k, sigma k, V n x k; each pointer may be NULL). */
+int cpcag_cuda_approx_decode(cpcag_ctx ctx, int precision, const void* Xt, int64_t rho_r, int64_t rho_c,
+                             const int64_t* omega_r, const int64_t* omega_c, int64_t p, int64_t n, cpcag_csr Lr,
+                             cpcag_csr Lc, const cpcag_approx_config* cfg, void* X, double* U, double* sigma,
+                             double* V, int64_t k_cap, int64_t* k);
+
 /* 3xTF32 tensor-core Gram matrix (tcgen05.mma kind::tf32) of n points given
  * as the rows of the n x d row-major fp64 array P; G is n x n row-major fp32.
  * The kNN filter stage's arithmetic, exposed for verification. */

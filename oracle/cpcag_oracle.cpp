@@ -649,6 +649,73 @@ Csr kron_reduce(const Csr& L, const std::vector<i64>& keep, double pcg_tol, doub
 }
 
 // ---------------------------------------------------------------- sampling
+// decoders.cpp:72-121 (graph_upsample): rows `known` of S equal R, the rest
+// solve L_aa S_a = -L_ab R, one Jacobi PCG per column (independent columns
+// in parallel; the first failing column in index order is reported).
+std::vector<double> graph_upsample(const Csr& L, const std::vector<i64>& known, const double* R, i64 r,
+                                   double pcg_tol, i64 pcg_max_iter) {
+  const i64 n = L.rows;
+  if (L.cols != n) throw std::invalid_argument("graph upsample: square Laplacian required");
+  std::vector<char> mask(static_cast<size_t>(n), 0);
+  for (const i64 i : known) {  // decoders.cpp:17-25
+    if (i < 0 || i >= n) throw std::invalid_argument("graph upsample: index out of range");
+    if (mask[static_cast<size_t>(i)]) throw std::invalid_argument("graph upsample: duplicate index");
+    mask[static_cast<size_t>(i)] = 1;
+  }
+  for (const auto& comp : components(L)) {
+    bool covered = false;
+    for (const i64 u : comp)
+      if (mask[static_cast<size_t>(u)]) {
+        covered = true;
+        break;
+      }
+    if (!covered)
+      throw std::runtime_error("graph upsample: connected component containing node " +
+                               std::to_string(comp.front()) + " has no sampled node");
+  }
+  const i64 m = static_cast<i64>(known.size());
+  std::vector<double> S(static_cast<size_t>(n * r), 0.0);
+  for (i64 i = 0; i < m; ++i)
+    for (i64 j = 0; j < r; ++j) S[known[i] + j * n] = R[i + j * m];
+  if (m == n) return S;
+  std::vector<i64> unknown;
+  for (i64 i = 0; i < n; ++i)
+    if (!mask[static_cast<size_t>(i)]) unknown.push_back(i);
+  const i64 ni = static_cast<i64>(unknown.size());
+  const Csr Laa = submatrix(L, unknown, unknown);
+  const Csr Lab = submatrix(L, unknown, known);
+  const Vec dg = diagonal(Laa);
+  std::vector<double> rhs(static_cast<size_t>(ni * r));
+  spmm_left(Lab, R, m, r, rhs.data());  // L_ab.multiply(R), then negated (decoders.cpp:107)
+  for (double& v : rhs) v = -v;
+  std::string failure;
+  i64 fail_j = -1;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (i64 j = 0; j < r; ++j) {
+    Vec b(rhs.begin() + j * ni, rhs.begin() + (j + 1) * ni);
+    Vec x(static_cast<size_t>(ni), 0.0);
+    PcgOut res;
+    std::string err;
+    try {
+      res = pcg_jacobi(Laa, dg, b, x, pcg_tol, pcg_max_iter);
+    } catch (const std::exception& e) {
+      err = e.what();
+    }
+    if (!err.empty() || !res.converged) {
+#pragma omp critical
+      if (fail_j < 0 || j < fail_j) {
+        fail_j = j;
+        failure = err.empty() ? "graph upsample: interior solve did not converge (column " + std::to_string(j) + ")"
+                              : err;
+      }
+      continue;
+    }
+    for (i64 i = 0; i < ni; ++i) S[unknown[i] + j * n] = x[i];
+  }
+  if (fail_j >= 0) throw std::runtime_error(failure);
+  return S;
+}
+
 // sampling.cpp:35-44
 std::vector<i64> partial_shuffle(i64 n, i64 take, Rng rng) {
   std::vector<i64> pool(static_cast<size_t>(n));
@@ -1056,6 +1123,14 @@ int ora_graph_from_adjacency(const ora_csr* W, int normalized, ora_csr** laplaci
 int ora_kron_reduce(const ora_csr* L, const int64_t* keep, int64_t nkeep, double pcg_tol,
                     double prune_tol, ora_csr** out) {
   return guard([&] { *out = box(kron_reduce(*L, to_list(keep, nkeep), pcg_tol, prune_tol)); });
+}
+
+int ora_graph_upsample(const ora_csr* L, const int64_t* known, int64_t n_known, const double* R, int64_t r,
+                       double pcg_tol, int64_t pcg_max_iter, double* S) {
+  return guard([&] {
+    const auto out = graph_upsample(*L, to_list(known, n_known), R, r, pcg_tol, pcg_max_iter);
+    std::copy(out.begin(), out.end(), S);
+  });
 }
 
 int ora_draw_plan(int64_t p, int64_t n, int64_t rho_r, int64_t rho_c, uint64_t seed,

@@ -76,6 +76,10 @@ int ora_knn_neighbors(const double* X, int64_t rows, int64_t cols, int axis_rows
                       int64_t* nbr, double* nbr_d2);
 int ora_graph_from_adjacency(const ora_csr* W, int normalized, ora_csr** laplacian,
                              double* degrees);
+/* decoders.cpp:72-121: S (n x r, col-major) = harmonic extension of the known
+ * rows R (n_known x r). */
+int ora_graph_upsample(const ora_csr* L, const int64_t* known, int64_t n_known, const double* R, int64_t r,
+                       double pcg_tol, int64_t pcg_max_iter, double* S);
 int ora_kron_reduce(const ora_csr* L, const int64_t* keep, int64_t nkeep, double pcg_tol,
                     double prune_tol, ora_csr** out);
 

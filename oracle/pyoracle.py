@@ -12,6 +12,7 @@ the reference's message.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 import subprocess
 from dataclasses import dataclass, field
@@ -467,3 +468,88 @@ def decoder_apply(X, plan: SamplingPlan, Lr: Csr, Lc: Csr, gbar_r: float, gbar_c
                                    Lr.handle, Lc.handle, C.c_double(gbar_r), C.c_double(gbar_c),
                                    _d(out)))
     return out
+
+
+# ----------------------------------------------------------------- approximate decoder
+def graph_upsample(L: Csr, known, R, pcg_tol=1e-10, pcg_max_iter=5000):
+    """decoders.cpp:72-121 (restated in cpcag_oracle.cpp)."""
+    known = _idx(known)
+    R = _f64(np.asarray(R).reshape(len(known), -1) if np.ndim(R) == 1 else R)
+    if R.shape[0] != len(known):
+        raise ValueError("graph upsample: known set and R row count differ")
+    r = R.shape[1]
+    S = np.empty((L.rows, r), order="F")
+    _check(lib().ora_graph_upsample(L.handle, _i(known), i64(len(known)), _d(R), i64(r), C.c_double(pcg_tol),
+                                    i64(pcg_max_iter), _d(S)))
+    return S
+
+
+def thin_svd(A):
+    """eigs.cpp:53-57.  The reference uses Eigen's JacobiSVD; Eigen is absent
+    here, so LAPACK (numpy gesdd) stands in: both return the exact SVD to
+    working precision, and every consumer below is invariant to the
+    per-column sign choice (align_factor_signs, U S V^T)."""
+    A = np.asarray(A, np.float64)
+    if not np.all(np.isfinite(A)):
+        raise ValueError("thin_svd: non-finite input")
+    U, s, Vt = np.linalg.svd(A, full_matrices=False)
+    return U, s, Vt.T
+
+
+def detect_rank(sigma, threshold):
+    """eigs.cpp:59-64."""
+    if len(sigma) == 0 or not sigma[0] > 0.0:
+        return 0
+    k = 0
+    while k < len(sigma) and sigma[k] / sigma[0] >= threshold:
+        k += 1
+    return k
+
+
+@dataclass
+class ApproxDecodeResult:
+    X: np.ndarray
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+    k: int
+
+
+def approx_decode(Xt, plan: SamplingPlan, Lr: Csr, Lc: Csr, delta_for_scaling=0.0, rank_threshold=0.1,
+                  pcg_tol=1e-10, pcg_max_iter=5000) -> ApproxDecodeResult:
+    """decoders.cpp:188-225 (Algorithm 2), loop for loop."""
+    Xt = _f64(Xt)
+    if Xt.shape != (plan.rho_r, plan.rho_c):
+        raise ValueError("approximate decoder: Xt does not match plan")
+    if Lr.rows != plan.p or Lc.rows != plan.n:
+        raise ValueError("approximate decoder: Laplacians do not match plan")
+    if not (0.0 < rank_threshold < 1.0):
+        raise ValueError("approximate decoder: rank threshold must be in (0,1)")
+    Ut, s, Vt = thin_svd(Xt)
+    k = detect_rank(s, rank_threshold)
+    if k == 0:
+        raise RuntimeError("approximate decoder: no singular value above the rank threshold")
+    U = graph_upsample(Lr, plan.omega_r, Ut[:, :k], pcg_tol, pcg_max_iter)
+    V = graph_upsample(Lc, plan.omega_c, Vt[:, :k], pcg_tol, pcg_max_iter)
+    for j in range(k):  # decoders.cpp:208-215
+        nu = math.sqrt(float(np.sum(U[:, j] * U[:, j])))
+        nv = math.sqrt(float(np.sum(V[:, j] * V[:, j])))
+        if nu <= 1e-14 or nv <= 1e-14:
+            raise RuntimeError(f"approximate decoder: zero column {j} after upsampling (rank overestimated)")
+        U[:, j] /= nu
+        V[:, j] /= nv
+    for j in range(k):  # align_factor_signs, decoders.cpp:33-50 (first largest |U(i,j)|)
+        arg, best = 0, -1.0
+        for i in range(U.shape[0]):
+            a = abs(U[i, j])
+            if a > best:
+                best, arg = a, i
+        if U[arg, j] < 0.0:
+            U[:, j] = -U[:, j]
+            V[:, j] = -V[:, j]
+    if not (0.0 <= delta_for_scaling < 1.0):
+        raise ValueError("decoder: delta_for_scaling must be in [0,1)")
+    norm_const = (float(plan.n) * float(plan.p)) / (float(plan.rho_r) * float(plan.rho_c))
+    sigma = math.sqrt(norm_const / (1.0 - delta_for_scaling)) * s[:k]
+    X = np.asfortranarray((U * sigma) @ V.T)
+    return ApproxDecodeResult(X, U, sigma, V, k)

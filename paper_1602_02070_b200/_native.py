@@ -42,6 +42,10 @@ class DecoderConfigC(C.Structure):
     _fields_ = [("gamma", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64)]
 
 
+class ApproxConfigC(C.Structure):
+    _fields_ = [("delta_for_scaling", dbl), ("rank_threshold", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64)]
+
+
 class PipelineConfigC(C.Structure):
     _fields_ = [("knn", i64), ("laplacian", C.c_int), ("sigma2", dbl), ("a", i64), ("b", i64),
                 ("rho_r_override", i64), ("rho_c_override", i64), ("kron_pcg_tol", dbl),
@@ -98,6 +102,10 @@ SIGNATURES = {
     "cpcag_cuda_alternate_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                               dbl, dbl, C.POINTER(DecoderConfigC), vp,
                                               C.POINTER(C.c_int), ip]),
+    "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
+    "cpcag_cuda_graph_upsample": (C.c_int, [vp, vp, vp, i64, vp, i64, dbl, i64, vp]),
+    "cpcag_cuda_approx_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
+                                           C.POINTER(ApproxConfigC), vp, vp, vp, vp, i64, ip]),
     "cpcag_cuda_decoder_block_create": (C.c_int, [vp, C.c_int, i64, i64, i64, i64, vp, vp, vp, i64, vp, i64,
                                                   dbl, dbl, C.POINTER(vp)]),
     "cpcag_cuda_decoder_block_destroy": (C.c_int, [vp]),

@@ -27,7 +27,8 @@ __all__ = [
     "PipelineConfig", "PipelineReport", "build_knn_graph", "knn", "graph_from_adjacency",
     "kron_reduce", "draw_plan", "subsample", "objective", "prox_l1", "prox_l2", "grad_g",
     "fista_solve", "alternate_decode", "power_iteration_norm", "pcg_solve", "run_pipeline",
-    "default_context",
+    "default_context", "SvdResult", "thin_svd", "detect_rank", "graph_upsample", "LowRankFactors",
+    "ApproxDecodeResult", "approx_decode",
 ]
 
 
@@ -582,13 +583,20 @@ def fista_solve(Y, Lr: SparseMatrix, Lc: SparseMatrix, cfg: FrpcagConfig, precis
 
 # ------------------------------------------------------------------ decoder
 @dataclass
-class DecoderConfig:  # decoders.hpp:13-22 (fields used by the alternate decoder)
+class DecoderConfig:  # decoders.hpp:13-22
     gamma: float = 1.0
     pcg_tol: float = 1e-10
     pcg_max_iter: int = 5000
+    variant: str = "approx"          # decoder of run_pipeline: "approx" (reference default) | "alternate"
+    delta_for_scaling: float = 0.0
+    rank_threshold: float = 0.1
 
     def c(self) -> N.DecoderConfigC:
         return N.DecoderConfigC(self.gamma, self.pcg_tol, int(self.pcg_max_iter))
+
+    def approx_c(self) -> N.ApproxConfigC:
+        return N.ApproxConfigC(float(self.delta_for_scaling), float(self.rank_threshold), float(self.pcg_tol),
+                               int(self.pcg_max_iter))
 
 
 @dataclass
@@ -626,6 +634,102 @@ def alternate_decode(Xt, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix,
                                                 float(gap_c.lambda_k1), C.byref(c), op, C.byref(cv),
                                                 C.byref(it)))
     return AlternateDecodeResult(out, bool(cv.value), int(it.value))
+
+
+# ------------------------------------------------------------------ approximate decoder
+@dataclass
+class SvdResult:  # eigs.hpp (thin_svd)
+    U: object
+    sigma: np.ndarray
+    V: object
+
+
+def thin_svd(A, ctx=None) -> SvdResult:
+    """eigs.cpp:53-57 on the device (fp64).  Column signs are unspecified, as
+    with the reference's JacobiSVD."""
+    a = _In(A, N.F64)
+    if len(a.shape) != 2:
+        raise ValueError("thin_svd: matrix required")
+    m, n = a.shape
+    q = min(m, n)
+    cuda = _is_cuda(A)
+    U, up = _out(cuda, _torch_device(A), (m, q), N.F64)
+    V, vp_ = _out(cuda, _torch_device(A), (n, q), N.F64)
+    s = np.empty(q, np.float64)
+    N.check(N.lib().cpcag_cuda_thin_svd(_ctx(ctx), a.ptr, m, n, up, s.ctypes.data if q else None, vp_))
+    return SvdResult(U, s, V)
+
+
+def detect_rank(sigma, threshold: float) -> int:
+    """eigs.cpp:59-64 (host logic on the singular values)."""
+    s = np.asarray(sigma, np.float64)
+    if s.size == 0 or not s[0] > 0.0:
+        return 0
+    k = 0
+    while k < s.size and s[k] / s[0] >= threshold:
+        k += 1
+    return k
+
+
+def graph_upsample(L: SparseMatrix, known, R, pcg_tol: float = 1e-10, pcg_max_iter: int = 5000, ctx=None):
+    """decoders.hpp:37-38 / decoders.cpp:72-121: rows `known` of the result
+    equal R, the others solve L_aa S_a = -L_ab R (batched Jacobi PCG)."""
+    if L.rows != L.cols:
+        raise ValueError("graph upsample: square Laplacian required")
+    kn = np.ascontiguousarray(known, np.int64).ravel()
+    r = _In(R, N.F64)
+    rr = r.shape[1] if len(r.shape) == 2 else 1
+    if r.shape[0] != kn.size:
+        raise ValueError("graph upsample: known set and R row count differ")
+    S, sp = _out(_is_cuda(R), _torch_device(R), (L.rows, rr), N.F64)
+    N.check(N.lib().cpcag_cuda_graph_upsample(_ctx(ctx), L.handle, kn.ctypes.data if kn.size else None, kn.size,
+                                              r.ptr, rr, float(pcg_tol), int(pcg_max_iter), sp))
+    return S
+
+
+@dataclass
+class LowRankFactors:  # decoders.hpp:26-32
+    U: object
+    sigma: np.ndarray
+    V: object
+    k: int = 0
+    scale_applied: bool = False
+
+
+@dataclass
+class ApproxDecodeResult:  # decoders.hpp:64-67
+    X: object
+    factors: LowRankFactors
+
+
+def approx_decode(Xt, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix, cfg: DecoderConfig = DecoderConfig(),
+                  precision=None, ctx=None) -> ApproxDecodeResult:
+    """decoders.hpp:69-72 / decoders.cpp:188-225 (Algorithm 2)."""
+    prec = _precision(Xt, precision)
+    xt = _In(Xt, prec)
+    if tuple(xt.shape) != (plan.rho_r(), plan.rho_c()):
+        raise ValueError("approximate decoder: Xt does not match plan")
+    om_r = np.ascontiguousarray(plan.omega_r, np.int64)
+    om_c = np.ascontiguousarray(plan.omega_c, np.int64)
+    cuda = _is_cuda(Xt)
+    X, xp = _out(cuda, _torch_device(Xt), (plan.p, plan.n), prec)
+    kcap = max(1, min(plan.rho_r(), plan.rho_c()))
+    U = np.empty((plan.p, kcap), np.float64, order="F")
+    V = np.empty((plan.n, kcap), np.float64, order="F")
+    s = np.empty(kcap, np.float64)
+    k = N.i64()
+    c = cfg.approx_c()
+    N.check(N.lib().cpcag_cuda_approx_decode(_ctx(ctx), prec, xt.ptr, plan.rho_r(), plan.rho_c(),
+                                             om_r.ctypes.data if om_r.size else None,
+                                             om_c.ctypes.data if om_c.size else None, plan.p, plan.n, Lr.handle,
+                                             Lc.handle, C.byref(c), xp, U.ctypes.data, s.ctypes.data,
+                                             V.ctypes.data, kcap, C.byref(k)))
+    kk = int(k.value)
+    f = LowRankFactors(np.asfortranarray(U.ravel(order="F")[: plan.p * kk].reshape((plan.p, kk), order="F")),
+                       s[:kk].copy(),
+                       np.asfortranarray(V.ravel(order="F")[: plan.n * kk].reshape((plan.n, kk), order="F")), kk,
+                       True)
+    return ApproxDecodeResult(X, f)
 
 
 # ------------------------------------------------------------------ pipeline

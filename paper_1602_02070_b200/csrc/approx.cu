@@ -1,0 +1,323 @@
+// approx.cu -- the approximate (subspace-upsampling) decoder, Algorithm 2 of
+// the paper as the reference implements it (decoders.cpp:188-225), with its
+// building blocks thin_svd (eigs.cpp:53-57) and detect_rank (eigs.cpp:59-64).
+//
+//   Xt = U~ S~ V~^T (thin SVD, fp64, cuSOLVER gesvdj on the small sampled
+//   matrix);  k = #{i : s_i / s_1 >= rank_threshold};
+//   U = graph_upsample(L_r, Omega_r, U~(:, :k)),  V = graph_upsample(L_c, ...)
+//   (multi-RHS Jacobi PCG on the interior block, kron.cu);
+//   unit-normalise the columns, make the largest-|.| entry of each U column
+//   positive (V flips with it), S = sqrt(np / (rho_r rho_c (1 - delta))) S~,
+//   X = U S V^T.
+// The factors are fp64; X is written in the working precision.
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace cpcag_cuda {
+
+namespace {
+
+void solver_ok(cusolverStatus_t st, const char* what) {
+  if (st != CUSOLVER_STATUS_SUCCESS)
+    fail(CPCAG_ERR_CUDA, std::string("cusolver ") + what + " failed (status " + std::to_string(static_cast<int>(st)) + ")");
+}
+
+// One cuSOLVER handle per (thread, device); the stream is set per call.
+cusolverDnHandle_t solver_handle(Ctx* c) {
+  thread_local std::unordered_map<int, cusolverDnHandle_t> handles;
+  auto it = handles.find(c->device);
+  if (it == handles.end()) {
+    cusolverDnHandle_t h = nullptr;
+    solver_ok(cusolverDnCreate(&h), "create");
+    it = handles.emplace(c->device, h).first;
+  }
+  solver_ok(cusolverDnSetStream(it->second, c->stream), "set stream");
+  return it->second;
+}
+
+}  // namespace
+
+__global__ void nonfinite_k(i64 n, const double* __restrict__ a, int* flag) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    if (!isfinite(a[i])) *flag = 1;
+}
+
+template <typename T>
+__global__ void to_f64_k(i64 n, const T* __restrict__ a, double* __restrict__ b) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    b[i] = static_cast<double>(a[i]);
+}
+
+// Column norms sqrt(sum x^2) of an m x k column-major matrix, one CTA per
+// column (fixed reduction tree).
+__global__ void col_norms_k(i64 m, const double* __restrict__ A, double* __restrict__ out) {
+  const i64 j = blockIdx.x;
+  double s[1] = {0.0};
+  for (i64 i = threadIdx.x; i < m; i += blockDim.x) {
+    const double x = A[i + j * m];
+    s[0] += x * x;
+  }
+  block_sum<1>(s);
+  if (threadIdx.x == 0) out[j] = sqrt(s[0]);
+}
+
+// A(:, j) /= nrm[j] (decoders.cpp:213-214).
+__global__ void col_div_k(i64 m, i64 k, double* __restrict__ A, const double* __restrict__ nrm) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (i64 j = blockIdx.y; j < k; j += gridDim.y) A[i + j * m] = __ddiv_rn(A[i + j * m], nrm[j]);
+}
+
+// Index of the first largest |U(i, j)| per column (decoders.cpp:35-49).
+__global__ void col_argmax_abs_k(i64 m, const double* __restrict__ U, i64* __restrict__ arg) {
+  __shared__ double bv[1024];
+  __shared__ i64 bi[1024];
+  const i64 j = blockIdx.x;
+  double best = -1.0;
+  i64 at = 0;
+  for (i64 i = threadIdx.x; i < m; i += blockDim.x) {
+    const double a = fabs(U[i + j * m]);
+    if (a > best) {
+      best = a;
+      at = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = at;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double ov = bv[threadIdx.x + s];
+      const i64 oi = bi[threadIdx.x + s];
+      if (ov > bv[threadIdx.x] || (ov == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = ov;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) arg[j] = bi[0];
+}
+
+__global__ void pivot_sign_k(i64 p, i64 k, const double* __restrict__ U, const i64* __restrict__ arg,
+                             int* __restrict__ flip) {
+  const i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (j < k) flip[j] = U[arg[j] + j * p] < 0.0 ? 1 : 0;
+}
+
+__global__ void flip_cols_k(i64 m, i64 k, double* __restrict__ A, const int* __restrict__ flip) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  for (i64 j = blockIdx.y; j < k; j += gridDim.y)
+    if (flip[j]) A[i + j * m] = -A[i + j * m];
+}
+
+// X(i, c) = sum_j (U(i, j) s_j) V(c, j), j ascending (decoders.cpp:220).
+template <typename T>
+__global__ void lowrank_k(i64 p, i64 n, i64 k, const double* __restrict__ U, const double* __restrict__ s,
+                          const double* __restrict__ V, T* __restrict__ X) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+    double x = 0.0;
+    for (i64 j = 0; j < k; ++j) x = __dadd_rn(x, __dmul_rn(__dmul_rn(U[i + j * p], s[j]), V[c + j * n]));
+    X[i + c * p] = static_cast<T>(x);
+  }
+}
+
+// eigs.cpp:53-57.  A is m x n (device, fp64, col-major); U m x q, sigma q
+// (descending), V n x q with q = min(m, n).  Column signs are the solver's.
+void thin_svd_device(Ctx* c, const double* A, i64 m, i64 n, double* U, double* sigma, double* V) {
+  const i64 mn = m * n;
+  if (mn) {
+    DevBuf<int> flag(c, 1);
+    flag.zero(c);
+    nonfinite_k<<<stride_blocks(c, mn), kBlock, 0, c->stream>>>(mn, A, flag.p);
+    launched(c);
+    if (read_back(c, flag.p)) invalid("thin_svd: non-finite input");
+  }
+  const i64 q = std::min(m, n);
+  if (q == 0) return;
+  if (m > INT32_MAX || n > INT32_MAX) invalid("thin_svd: matrix too large");
+  cusolverDnHandle_t h = solver_handle(c);
+  gesvdjInfo_t params = nullptr;
+  solver_ok(cusolverDnCreateGesvdjInfo(&params), "gesvdj info");
+  std::unique_ptr<std::remove_pointer<gesvdjInfo_t>::type, void (*)(gesvdjInfo_t)> own(
+      params, [](gesvdjInfo_t p) { cusolverDnDestroyGesvdjInfo(p); });
+  solver_ok(cusolverDnXgesvdjSetSortEig(params, 1), "gesvdj sort");
+  DevBuf<double> W(c, mn);  // gesvdj overwrites its input
+  CUDA_OK(cudaMemcpyAsync(W.p, A, sizeof(double) * mn, cudaMemcpyDeviceToDevice, c->stream));
+  const int mi = static_cast<int>(m), ni = static_cast<int>(n);
+  int lwork = 0;
+  solver_ok(cusolverDnDgesvdj_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, 1, mi, ni, W.p, mi, sigma, U, mi, V, ni,
+                                         &lwork, params),
+            "gesvdj buffer");
+  DevBuf<double> work(c, std::max(lwork, 1));
+  DevBuf<int> info(c, 1);
+  solver_ok(cusolverDnDgesvdj(h, CUSOLVER_EIG_MODE_VECTOR, 1, mi, ni, W.p, mi, sigma, U, mi, V, ni, work.p, lwork,
+                              info.p, params),
+            "gesvdj");
+  const int inf = read_back(c, info.p);
+  if (inf != 0) runtime("thin_svd: solver did not converge (info " + std::to_string(inf) + ")");
+}
+
+// eigs.cpp:59-64.
+i64 detect_rank_host(const std::vector<double>& s, double thr) {
+  if (s.empty() || !(s[0] > 0.0)) return 0;
+  i64 k = 0;
+  while (k < static_cast<i64>(s.size()) && s[k] / s[0] >= thr) ++k;
+  return k;
+}
+
+template <typename T>
+void approx_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const std::vector<i64>& om_r,
+                          const std::vector<i64>& om_c, i64 p, i64 n, Csr* Lr, Csr* Lc,
+                          const cpcag_approx_config& cfg, T* X, double* U_out, double* s_out, double* V_out,
+                          i64 k_cap, i64* k_out) {
+  if (Lr->rows != p || Lc->rows != n) invalid("approximate decoder: Laplacians do not match plan");
+  if (!(cfg.rank_threshold > 0.0 && cfg.rank_threshold < 1.0))
+    invalid("approximate decoder: rank threshold must be in (0,1)");
+  const i64 q = std::min(rho_r, rho_c);
+  DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), Ut(c, std::max<i64>(rho_r * q, 1)),
+      Vt(c, std::max<i64>(rho_c * q, 1)), st(c, std::max<i64>(q, 1));
+  if (rho_r * rho_c) {
+    to_f64_k<T><<<stride_blocks(c, rho_r * rho_c), kBlock, 0, c->stream>>>(rho_r * rho_c, Xt, A.p);
+    launched(c);
+  }
+  thin_svd_device(c, A.p, rho_r, rho_c, Ut.p, st.p, Vt.p);
+  std::vector<double> s(static_cast<size_t>(q));
+  if (q) CUDA_OK(cudaMemcpyAsync(s.data(), st.p, sizeof(double) * q, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  const i64 k = detect_rank_host(s, cfg.rank_threshold);
+  if (k == 0) runtime("approximate decoder: no singular value above the rank threshold");
+
+  DevBuf<double> U(c, p * k), V(c, n * k);
+  graph_upsample_device(c, Lr, om_r, Ut.p, k, cfg.pcg_tol, cfg.pcg_max_iter, U.p);
+  graph_upsample_device(c, Lc, om_c, Vt.p, k, cfg.pcg_tol, cfg.pcg_max_iter, V.p);
+
+  DevBuf<double> nu(c, k), nv(c, k);
+  col_norms_k<<<static_cast<unsigned>(k), kBlock, 0, c->stream>>>(p, U.p, nu.p);
+  launched(c);
+  col_norms_k<<<static_cast<unsigned>(k), kBlock, 0, c->stream>>>(n, V.p, nv.p);
+  launched(c);
+  std::vector<double> hnu(static_cast<size_t>(k)), hnv(static_cast<size_t>(k));
+  CUDA_OK(cudaMemcpyAsync(hnu.data(), nu.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(hnv.data(), nv.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  for (i64 j = 0; j < k; ++j)
+    if (hnu[j] <= 1e-14 || hnv[j] <= 1e-14)
+      runtime("approximate decoder: zero column " + std::to_string(j) + " after upsampling (rank overestimated)");
+  const unsigned ky = static_cast<unsigned>(std::min<i64>(k, 65535));
+  col_div_k<<<dim3(blocks_for(p), ky), kBlock, 0, c->stream>>>(p, k, U.p, nu.p);
+  launched(c);
+  col_div_k<<<dim3(blocks_for(n), ky), kBlock, 0, c->stream>>>(n, k, V.p, nv.p);
+  launched(c);
+  // align_factor_signs (decoders.cpp:33-50)
+  DevBuf<i64> arg(c, k);
+  DevBuf<int> flip(c, k);
+  col_argmax_abs_k<<<static_cast<unsigned>(k), 1024, 0, c->stream>>>(p, U.p, arg.p);
+  launched(c);
+  pivot_sign_k<<<blocks_for(k), kBlock, 0, c->stream>>>(p, k, U.p, arg.p, flip.p);
+  launched(c);
+  flip_cols_k<<<dim3(blocks_for(p), ky), kBlock, 0, c->stream>>>(p, k, U.p, flip.p);
+  launched(c);
+  flip_cols_k<<<dim3(blocks_for(n), ky), kBlock, 0, c->stream>>>(n, k, V.p, flip.p);
+  launched(c);
+  // scaling_constant (decoders.cpp:27-31, sampling.cpp:12-15)
+  const double delta = cfg.delta_for_scaling;
+  if (!(delta >= 0.0 && delta < 1.0)) invalid("decoder: delta_for_scaling must be in [0,1)");
+  const double norm_const = (static_cast<double>(n) * static_cast<double>(p)) /
+                            (static_cast<double>(rho_r) * static_cast<double>(rho_c));
+  const double scale = std::sqrt(norm_const / (1.0 - delta));
+  std::vector<double> sig(static_cast<size_t>(k));
+  for (i64 j = 0; j < k; ++j) sig[j] = scale * s[j];
+  DevBuf<double> sd(c, k);
+  CUDA_OK(cudaMemcpyAsync(sd.p, sig.data(), sizeof(double) * k, cudaMemcpyHostToDevice, c->stream));
+  if (p && n) {
+    dim3 g(blocks_for(p), static_cast<unsigned>(std::min<i64>(n, 65535)));
+    lowrank_k<T><<<g, kBlock, 0, c->stream>>>(p, n, k, U.p, sd.p, V.p, X);
+    launched(c);
+  }
+  *k_out = k;
+  if (k_cap > 0 && k <= k_cap) {
+    if (U_out) CUDA_OK(cudaMemcpyAsync(U_out, U.p, sizeof(double) * p * k, cudaMemcpyDefault, c->stream));
+    if (V_out) CUDA_OK(cudaMemcpyAsync(V_out, V.p, sizeof(double) * n * k, cudaMemcpyDefault, c->stream));
+    if (s_out) CUDA_OK(cudaMemcpyAsync(s_out, sd.p, sizeof(double) * k, cudaMemcpyDefault, c->stream));
+  }
+  sync(c);
+}
+
+template void approx_decode_device<double>(Ctx*, const double*, i64, i64, const std::vector<i64>&,
+                                           const std::vector<i64>&, i64, i64, Csr*, Csr*, const cpcag_approx_config&,
+                                           double*, double*, double*, double*, i64, i64*);
+template void approx_decode_device<float>(Ctx*, const float*, i64, i64, const std::vector<i64>&,
+                                          const std::vector<i64>&, i64, i64, Csr*, Csr*, const cpcag_approx_config&,
+                                          float*, double*, double*, double*, i64, i64*);
+
+}  // namespace cpcag_cuda
+
+using namespace cpcag_cuda;
+
+namespace {
+std::vector<i64> fetch_idx(const int64_t* src, i64 count) {
+  std::vector<i64> v(static_cast<size_t>(std::max<i64>(count, 0)));
+  if (v.empty()) return v;
+  if (!src) invalid("null argument");
+  if (is_device_ptr(src))
+    CUDA_OK(cudaMemcpy(v.data(), src, sizeof(i64) * v.size(), cudaMemcpyDeviceToHost));
+  else
+    std::copy(src, src + v.size(), v.begin());
+  return v;
+}
+}  // namespace
+
+extern "C" int cpcag_cuda_thin_svd(cpcag_ctx ctx, const double* A, int64_t m, int64_t n, double* U, double* sigma,
+                                   double* V) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (m < 0 || n < 0) invalid("thin_svd: negative size");
+    const i64 q = std::min(m, n);
+    if ((m * n && !A) || (q && (!U || !sigma || !V))) invalid("null argument");
+    InView<double> a(c, A, static_cast<size_t>(m * n));
+    OutView<double> u(c, U, static_cast<size_t>(m * q)), s(c, sigma, static_cast<size_t>(q)),
+        v(c, V, static_cast<size_t>(n * q));
+    thin_svd_device(c, a.d, m, n, u.d, s.d, v.d);
+    u.flush(c);
+    s.flush(c);
+    v.flush(c);
+    sync(c);
+  });
+}
+
+extern "C" int cpcag_cuda_approx_decode(cpcag_ctx ctx, int precision, const void* Xt, int64_t rho_r, int64_t rho_c,
+                                        const int64_t* omega_r, const int64_t* omega_c, int64_t p, int64_t n,
+                                        cpcag_csr Lr, cpcag_csr Lc, const cpcag_approx_config* cfg, void* X,
+                                        double* U, double* sigma, double* V, int64_t k_cap, int64_t* k) {
+  auto run = [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (!cfg || !k || (p * n && !X) || (rho_r * rho_c && !Xt)) invalid("null argument");
+      const std::vector<i64> omr = fetch_idx(omega_r, rho_r), omc = fetch_idx(omega_c, rho_c);
+      InView<T> xt(c, static_cast<const T*>(Xt), static_cast<size_t>(rho_r * rho_c));
+      OutView<T> x(c, static_cast<T*>(X), static_cast<size_t>(p * n));
+      approx_decode_device<T>(c, xt.d, rho_r, rho_c, omr, omc, p, n, as_csr(Lr), as_csr(Lc), *cfg, x.d, U, sigma, V,
+                              k_cap, k);
+      x.flush(c);
+      sync(c);
+    });
+  };
+  if (precision == CPCAG_F64) return run(double{});
+  if (precision == CPCAG_F32) return run(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}

@@ -416,6 +416,17 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
                         double prune_tol);
 
 template <typename T>
+void approx_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const std::vector<i64>& om_r,
+                          const std::vector<i64>& om_c, i64 p, i64 n, Csr* Lr, Csr* Lc,
+                          const cpcag_approx_config& cfg, T* X, double* U_out, double* s_out, double* V_out,
+                          i64 k_cap, i64* k_out);
+
+// decoders.cpp:72-121: S (n x r, fp64 col-major) = harmonic extension of the
+// known rows R (|known| x r, leading dimension |known|).
+void graph_upsample_device(Ctx* c, Csr* L, const std::vector<i64>& known, const double* R, i64 r,
+                           double pcg_tol, i64 pcg_max_iter, double* S);
+
+template <typename T>
 void knn_graph_device(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K,
                       int kind, double sigma2_override, Csr** W, Csr** L, double* degrees_dev,
                       double* sigma2);

@@ -1009,7 +1009,7 @@ __global__ void cg_true_res_ap_k(i64 p, i64 n, Plan pl, const T* __restrict__ Xt
 // launch geometry, built once per solve (or per decoder block).
 template <typename T>
 struct BandApply {
-  static constexpr i64 kBandBytes = i64{56} << 20;  // L2-resident band budget
+  static constexpr i64 kBandBytes = i64{128} << 20;  // band budget (measured: taller bands win even past L2)
   static constexpr int kColsPerCta = 64;
   i64 p = 0, n = 0;
   int rpl = 1, rb = 32, band_v = 1, col_nt = 1024;
@@ -1091,6 +1091,10 @@ struct BandApply {
         rpl = r;
         break;
       }
+    }
+    if (const char* e = std::getenv("CPCAG_BAND_RPL")) {
+      const int r = std::atoi(e);
+      if (r == 1 || r == 2 || r == 4 || r == 8) rpl = r;
     }
     const Pull<T> pc = make_pull<T>(c, Lc, true), pr = make_pull<T>(c, Lr, false);
     rpc = pc.rp;
@@ -1226,7 +1230,8 @@ struct BandApply {
                   static_cast<unsigned>((p + band_rows - 1) / band_rows));
     {
     KScope ks_(c, "cg_apply_band");
-    if (rpl == 4) launch_band_v<4>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    if (rpl == 8) launch_band_v<8>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    else if (rpl == 4) launch_band_v<4>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     else if (rpl == 2) launch_band_v<2>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     else launch_band_v<1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
     launched(c);

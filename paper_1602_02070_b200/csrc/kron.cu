@@ -738,6 +738,34 @@ Csr* gather_sub(Ctx* c, Csr* L, const i64* rsrc_dev, i64 nr, const int* cmap_dev
   return out;
 }
 
+// Every connected component of L must hold a node of keep (graph.cpp:183-193,
+// decoders.cpp:84-94); throws "<what>: connected component containing node X
+// has no <noun> node" naming the smallest node of the first such component.
+void check_components(Ctx* c, Csr* L, const i64* keep_d, i64 m, const char* what, const char* noun) {
+  const i64 n = L->rows;
+  if (!n) return;
+  DevBuf<int> parent(c, n), grounded(c, n), first(c, 1);
+  grounded.zero(c);
+  const int big = INT32_MAX;
+  CUDA_OK(cudaMemcpyAsync(first.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  uf_init_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
+  launched(c);
+  uf_hook_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, L->rp, L->ci, parent.p);
+  launched(c);
+  uf_flatten_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
+  launched(c);
+  if (m) {
+    ground_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keep_d, parent.p, grounded.p);
+    launched(c);
+  }
+  ungrounded_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p, grounded.p, first.p);
+  launched(c);
+  const int bad = read_back(c, first.p);
+  if (bad != INT32_MAX)
+    runtime(std::string(what) + ": connected component containing node " + std::to_string(bad) + " has no " + noun +
+            " node");
+}
+
 Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg_tol, double prune_tol) {
   const i64 n = L->rows;
   if (L->cols != n) invalid("kron reduction: square Laplacian required");
@@ -755,27 +783,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   // graph.cpp:183-193: every component must hold a kept node.
   DevBuf<i64> keep_d(c, std::max<i64>(m, 1));
   if (m) CUDA_OK(cudaMemcpyAsync(keep_d.p, keep.data(), sizeof(i64) * m, cudaMemcpyHostToDevice, c->stream));
-  if (n) {
-    DevBuf<int> parent(c, n), grounded(c, n), first(c, 1);
-    grounded.zero(c);
-    const int big = INT32_MAX;
-    CUDA_OK(cudaMemcpyAsync(first.p, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    uf_init_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
-    launched(c);
-    uf_hook_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, L->rp, L->ci, parent.p);
-    launched(c);
-    uf_flatten_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p);
-    launched(c);
-    if (m) {
-      ground_k<<<blocks_for(m), kBlock, 0, c->stream>>>(m, keep_d.p, parent.p, grounded.p);
-      launched(c);
-    }
-    ungrounded_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, parent.p, grounded.p, first.p);
-    launched(c);
-    const int bad = read_back(c, first.p);
-    if (bad != INT32_MAX)
-      runtime("kron reduction: connected component containing node " + std::to_string(bad) + " has no kept node");
-  }
+  check_components(c, L, keep_d.p, m, "kron reduction", "kept");
 
   trace_mark(c, "kron: components");
   std::vector<i64> interior;
@@ -870,9 +878,142 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   return out;
 }
 
+// ------------------------------------------------------------------ graph upsampling
+// Rows of a gathered submatrix re-sorted by (new) column: submatrix() goes
+// through from_triplets (sparse.cpp:122-141), so when the column map is not
+// monotone (known = Omega in draw order) the entries come out in map order.
+__global__ void sort_rows_k(i64 nr, const i64* __restrict__ rp, int* __restrict__ ci, double* __restrict__ v) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= nr) return;
+  for (i64 a = rp[r] + 1; a < rp[r + 1]; ++a) {
+    const int kc = ci[a];
+    const double kv = v[a];
+    i64 b = a - 1;
+    while (b >= rp[r] && ci[b] > kc) {
+      ci[b + 1] = ci[b];
+      v[b + 1] = v[b];
+      --b;
+    }
+    ci[b + 1] = kc;
+    v[b + 1] = kv;
+  }
+}
+
+// B(:, j) = -(L_ab R)(:, j) in slab layout (decoders.cpp:107, CSR order).
+__global__ void upsample_rhs_slab_k(i64 ni, i64 r, const i64* __restrict__ rp, const int* __restrict__ ci,
+                                    const double* __restrict__ v, const double* __restrict__ R, i64 ldr,
+                                    double* __restrict__ B) {
+  const i64 a = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (a >= ni) return;
+  for (i64 j = blockIdx.y; j < r; j += gridDim.y) {
+    const double y = pull_left(rp[a], rp[a + 1], ci, v, R + j * ldr);
+    B[slab_at(ni, a, j)] = -y;
+  }
+}
+
+// S(i, :) = R(kpos[i], :) on known rows, the interior solution elsewhere.
+__global__ void upsample_scatter_k(i64 n, i64 r, const int* __restrict__ kpos, const int* __restrict__ ipos,
+                                   const double* __restrict__ R, i64 ldr, const double* __restrict__ Xs, i64 ni,
+                                   double* __restrict__ S) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (i64 j = blockIdx.y; j < r; j += gridDim.y)
+    S[i + j * n] = kpos[i] >= 0 ? R[kpos[i] + j * ldr] : Xs[slab_at(ni, ipos[i], j)];
+}
+
+void graph_upsample_device(Ctx* c, Csr* L, const std::vector<i64>& known, const double* R, i64 r, double pcg_tol,
+                           i64 pcg_max_iter, double* S) {
+  const i64 n = L->rows;
+  if (L->cols != n) invalid("graph upsample: square Laplacian required");
+  if (n > INT32_MAX) invalid("graph upsample: graphs above 2^31 nodes are not supported");
+  const i64 m = static_cast<i64>(known.size());
+  std::vector<int> kpos(static_cast<size_t>(n), -1);
+  for (i64 j = 0; j < m; ++j) {  // decoders.cpp:17-25
+    const i64 u = known[j];
+    if (u < 0 || u >= n) invalid("graph upsample: index out of range");
+    if (kpos[u] != -1) invalid("graph upsample: duplicate index");
+    kpos[u] = static_cast<int>(j);
+  }
+  DevBuf<i64> known_d(c, std::max<i64>(m, 1));
+  if (m) CUDA_OK(cudaMemcpyAsync(known_d.p, known.data(), sizeof(i64) * m, cudaMemcpyHostToDevice, c->stream));
+  check_components(c, L, known_d.p, m, "graph upsample", "sampled");
+
+  std::vector<i64> interior;
+  std::vector<int> ipos(static_cast<size_t>(n), -1);
+  for (i64 u = 0; u < n; ++u)
+    if (kpos[u] < 0) {
+      ipos[u] = static_cast<int>(interior.size());
+      interior.push_back(u);
+    }
+  const i64 ni = static_cast<i64>(interior.size());
+  DevBuf<int> kpos_d(c, std::max<i64>(n, 1)), ipos_d(c, std::max<i64>(n, 1));
+  if (n) {
+    CUDA_OK(cudaMemcpyAsync(kpos_d.p, kpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ipos_d.p, ipos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+  }
+  const i64 nbp = std::max<i64>((r + kCpb - 1) / kCpb * kCpb, kCpb);
+  DevBuf<double> X(c, std::max<i64>(ni, 1) * nbp);
+  if (ni > 0 && r > 0) {
+    DevBuf<i64> int_d(c, ni);
+    CUDA_OK(cudaMemcpyAsync(int_d.p, interior.data(), sizeof(i64) * ni, cudaMemcpyHostToDevice, c->stream));
+    Csr* Laa = gather_sub(c, L, int_d.p, ni, ipos_d.p, ni);
+    Csr* Lab = gather_sub(c, L, int_d.p, ni, kpos_d.p, m);
+    std::unique_ptr<Csr> own_aa(Laa), own_ab(Lab);
+    if (Lab->nnz) {
+      sort_rows_k<<<blocks_for(ni), kBlock, 0, c->stream>>>(ni, Lab->rp, Lab->ci, Lab->v);
+      launched(c);
+    }
+    DevBuf<double> inv(c, ni), B(c, ni * nbp);
+    jacobi_inv_k<<<blocks_for(ni), kBlock, 0, c->stream>>>(ni, Laa->rp, Laa->ci, Laa->v, inv.p);
+    launched(c);
+    B.zero(c);
+    X.zero(c);
+    dim3 g(blocks_for(ni), static_cast<unsigned>(std::min<i64>(r, 65535)));
+    upsample_rhs_slab_k<<<g, kBlock, 0, c->stream>>>(ni, r, Lab->rp, Lab->ci, Lab->v, R, m, B.p);
+    launched(c);
+    PcgBatchOut res;
+    pcg_slab(c, Laa, inv.p, B.p, X.p, ni, r, pcg_tol, pcg_max_iter, &res);
+    for (i64 j = 0; j < r; ++j) {  // first failing column, as the reference's column loop
+      const ColState& cs = res.cols[j];
+      if (cs.err) runtime("pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(cs.it));
+      if (cs.done != 2 && !(cs.rel_res <= pcg_tol))
+        runtime("graph upsample: interior solve did not converge (column " + std::to_string(j) + ")");
+    }
+  }
+  if (n && r) {
+    dim3 g(blocks_for(n), static_cast<unsigned>(std::min<i64>(r, 65535)));
+    upsample_scatter_k<<<g, kBlock, 0, c->stream>>>(n, r, kpos_d.p, ipos_d.p, R, m, X.p, std::max<i64>(ni, 1), S);
+    launched(c);
+  }
+}
+
 }  // namespace cpcag_cuda
 
 using namespace cpcag_cuda;
+
+extern "C" int cpcag_cuda_graph_upsample(cpcag_ctx ctx, cpcag_csr Lh, const int64_t* known, int64_t n_known,
+                                         const double* R, int64_t r, double pcg_tol, int64_t pcg_max_iter,
+                                         double* S) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    Csr* L = as_csr(Lh);
+    if (r < 0 || n_known < 0) invalid("graph upsample: negative size");
+    if ((n_known * r && !R) || (L->rows * r && !S)) invalid("null argument");
+    std::vector<i64> k(static_cast<size_t>(n_known));
+    if (!k.empty()) {
+      if (!known) invalid("null argument");
+      if (is_device_ptr(known))
+        CUDA_OK(cudaMemcpy(k.data(), known, sizeof(i64) * k.size(), cudaMemcpyDeviceToHost));
+      else
+        std::copy(known, known + k.size(), k.begin());
+    }
+    InView<double> rv(c, R, static_cast<size_t>(n_known * r));
+    OutView<double> sv(c, S, static_cast<size_t>(L->rows * r));
+    graph_upsample_device(c, L, k, rv.d, r, pcg_tol, pcg_max_iter, sv.d);
+    sv.flush(c);
+    sync(c);
+  });
+}
 
 extern "C" int cpcag_cuda_kron_reduce(cpcag_ctx ctx, cpcag_csr Lh, const int64_t* keep, int64_t n_keep,
                                       double pcg_tol, double prune_tol, cpcag_csr* out) {
