@@ -142,7 +142,7 @@ def pipeline_config(P, wl):
         knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
         frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
                               max_iter=wl.fista_iters),
-        decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-30, pcg_max_iter=wl.cg_iters),
+        decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-30, pcg_max_iter=wl.cg_iters, variant="alternate"),
         lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1603)
 
 

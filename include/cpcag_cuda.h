@@ -287,28 +287,47 @@ typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36
   cpcag_decoder_config decoder;
   double lambda_k1_r, lambda_k1_c; /* SpectralGap::lambda_k1 supplied by the caller */
   uint64_t seed;
+  int decoder_variant;       /* DecoderVariant (decoders.hpp:11): CPCAG_DECODER_ALTERNATE or _APPROX */
+  cpcag_approx_config approx; /* the approximate decoder's DecoderConfig fields */
 } cpcag_pipeline_config;
+
+enum { CPCAG_DECODER_IDEAL = 0, CPCAG_DECODER_ALTERNATE = 1, CPCAG_DECODER_APPROX = 2 };
+
+/* Optional factor output of the approximate decoder (PipelineReport::factors,
+ * pipeline.hpp:91): fp64 U (p x k), sigma (k), V (n x k) when k <= k_cap. */
+typedef struct cpcag_pipeline_factors {
+  double* U;
+  double* sigma;
+  double* V;
+  int64_t k_cap;
+} cpcag_pipeline_factors;
 
 typedef struct cpcag_pipeline_report { /* PipelineReport subset, pipeline.hpp:73-94 */
   int64_t p, n, rho_r, rho_c;
   cpcag_solve_trace trace;
   int decoder_converged;
   int64_t decoder_iterations;
+  int64_t detected_rank;  /* detect_rank(thin_svd(Xt).sigma, rank_threshold), pipeline.cpp:319-320 */
+  int64_t factors_k;      /* approximate decoder: rank of the factors (0 otherwise) */
+  int has_factors;
   /* Stage timings in ms (device events), in the reference's stage order:
    * graphs, plan, subsample, kron, solve, decode (pipeline.cpp:273-350). */
   double stage_ms[6];
 } cpcag_pipeline_report;
 
-/* run_pipeline, low-rank task with the alternate decoder (pipeline.cpp:228-
- * 350): graphs (row graph from W_r when given, else kNN over rows; column
- * graph from W_c when given, else kNN over columns) -> plan -> subsample ->
- * Kron -> FISTA -> alternate decode.  Y is p x n.  Xt (rho_r x rho_c) and X
- * (p x n) receive the compressed and decoded solutions; omega_r/omega_c
- * (may be NULL) receive the plan; objective (may be NULL) the FISTA trace. */
+/* run_pipeline, low-rank task (pipeline.cpp:228-350): graphs (row graph
+ * from W_r when given, else kNN over rows; column graph from W_c when given,
+ * else kNN over columns) -> plan -> subsample -> Kron -> FISTA -> detected
+ * rank -> decode with the alternate or the approximate decoder.  Y is p x n.
+ * Xt (rho_r x rho_c) and X (p x n) receive the compressed and decoded
+ * solutions; omega_r/omega_c (may be NULL) receive the plan; objective (may
+ * be NULL) the FISTA trace; factors (may be NULL) the approximate decoder's
+ * factors. */
 int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void* Y, int64_t p, int64_t n,
                             cpcag_csr W_r, cpcag_csr W_c, const cpcag_pipeline_config* cfg,
                             void* Xt, void* X, int64_t* omega_r, int64_t* omega_c,
-                            double* objective, cpcag_pipeline_report* report);
+                            double* objective, cpcag_pipeline_report* report,
+                            const cpcag_pipeline_factors* factors);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,9 @@ class DecoderConfigC(C.Structure):
     _fields_ = [("gamma", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64)]
 
 
+DECODER_IDEAL, DECODER_ALTERNATE, DECODER_APPROX = 0, 1, 2
+
+
 class ApproxConfigC(C.Structure):
     _fields_ = [("delta_for_scaling", dbl), ("rank_threshold", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64)]
 
@@ -50,13 +53,17 @@ class PipelineConfigC(C.Structure):
     _fields_ = [("knn", i64), ("laplacian", C.c_int), ("sigma2", dbl), ("a", i64), ("b", i64),
                 ("rho_r_override", i64), ("rho_c_override", i64), ("kron_pcg_tol", dbl),
                 ("frpcag", FrpcagConfigC), ("decoder", DecoderConfigC), ("lambda_k1_r", dbl),
-                ("lambda_k1_c", dbl), ("seed", u64)]
+                ("lambda_k1_c", dbl), ("seed", u64), ("decoder_variant", C.c_int), ("approx", ApproxConfigC)]
+
+
+class PipelineFactorsC(C.Structure):
+    _fields_ = [("U", vp), ("sigma", vp), ("V", vp), ("k_cap", i64)]
 
 
 class PipelineReportC(C.Structure):
     _fields_ = [("p", i64), ("n", i64), ("rho_r", i64), ("rho_c", i64), ("trace", SolveTraceC),
-                ("decoder_converged", C.c_int), ("decoder_iterations", i64),
-                ("stage_ms", dbl * 6)]
+                ("decoder_converged", C.c_int), ("decoder_iterations", i64), ("detected_rank", i64),
+                ("factors_k", i64), ("has_factors", C.c_int), ("stage_ms", dbl * 6)]
 
 
 # (name, restype, argtypes) of every exported symbol.
@@ -116,7 +123,7 @@ SIGNATURES = {
     "cpcag_cuda_gram_tf32x3": (C.c_int, [vp, vp, i64, i64, vp]),
     "cpcag_cuda_run_pipeline": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp,
                                           C.POINTER(PipelineConfigC), vp, vp, vp, vp, vp,
-                                          C.POINTER(PipelineReportC)]),
+                                          C.POINTER(PipelineReportC), C.POINTER(PipelineFactorsC)]),
 }
 
 _lib = None

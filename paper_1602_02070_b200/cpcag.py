@@ -674,14 +674,14 @@ def detect_rank(sigma, threshold: float) -> int:
 def graph_upsample(L: SparseMatrix, known, R, pcg_tol: float = 1e-10, pcg_max_iter: int = 5000, ctx=None):
     """decoders.hpp:37-38 / decoders.cpp:72-121: rows `known` of the result
     equal R, the others solve L_aa S_a = -L_ab R (batched Jacobi PCG)."""
-    if L.rows != L.cols:
+    if L.rows() != L.cols():
         raise ValueError("graph upsample: square Laplacian required")
     kn = np.ascontiguousarray(known, np.int64).ravel()
     r = _In(R, N.F64)
     rr = r.shape[1] if len(r.shape) == 2 else 1
     if r.shape[0] != kn.size:
         raise ValueError("graph upsample: known set and R row count differ")
-    S, sp = _out(_is_cuda(R), _torch_device(R), (L.rows, rr), N.F64)
+    S, sp = _out(_is_cuda(R), _torch_device(R), (L.rows(), rr), N.F64)
     N.check(N.lib().cpcag_cuda_graph_upsample(_ctx(ctx), L.handle, kn.ctypes.data if kn.size else None, kn.size,
                                               r.ptr, rr, float(pcg_tol), int(pcg_max_iter), sp))
     return S
@@ -757,7 +757,17 @@ class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
                                  int(self.b), int(self.rho_r_override), int(self.rho_c_override),
                                  float(self.kron_pcg_tol), self.frpcag.c(), self.decoder.c(),
                                  float(self.lambda_k1_r), float(self.lambda_k1_c),
-                                 int(self.seed) & (2**64 - 1))
+                                 int(self.seed) & (2**64 - 1), _variant(self.decoder.variant),
+                                 self.decoder.approx_c())
+
+
+def _variant(v) -> int:
+    table = {"ideal": N.DECODER_IDEAL, "alternate": N.DECODER_ALTERNATE, "approx": N.DECODER_APPROX}
+    if v in table:
+        return table[v]
+    if v in table.values():
+        return int(v)
+    raise ValueError(f"unknown decoder variant {v!r}")
 
 
 @dataclass
@@ -773,6 +783,9 @@ class PipelineReport:  # pipeline.hpp:73-94 (subset)
     decoder_converged: bool
     decoder_iterations: int
     stages: dict
+    detected_rank: int = 0
+    factors: Optional[LowRankFactors] = None  # approximate decoder only
+    has_factors: bool = False
 
     def stage_ms(self, name: str) -> float:
         return self.stages.get(name, 0.0)
@@ -795,14 +808,25 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
     obj = np.zeros(max(int(cfg.frpcag.max_iter), 1))
     rep = N.PipelineReportC()
     c = cfg.c()
+    kcap = max(1, min(rho_r, rho_c)) if _variant(cfg.decoder.variant) == N.DECODER_APPROX else 0
+    fU = np.empty((p, kcap), np.float64, order="F")
+    fV = np.empty((n, kcap), np.float64, order="F")
+    fs = np.empty(max(kcap, 1), np.float64)
+    fac = N.PipelineFactorsC(fU.ctypes.data if kcap else None, fs.ctypes.data if kcap else None,
+                             fV.ctypes.data if kcap else None, kcap)
     N.check(N.lib().cpcag_cuda_run_pipeline(_ctx(ctx), prec, y.ptr, p, n, W_r.handle if W_r else None,
                                             W_c.handle if W_c else None, C.byref(c), xtp, xp,
                                             om_r.ctypes.data, om_c.ctypes.data, obj.ctypes.data,
-                                            C.byref(rep)))
+                                            C.byref(rep), C.byref(fac)))
     it = int(rep.trace.iterations)
     trace = SolveTrace(list(obj[:it]), it, bool(rep.trace.converged), float(rep.trace.final_rel_change),
                        float(rep.trace.step))
     plan = SamplingPlan(om_r[:rep.rho_r].copy(), om_c[:rep.rho_c].copy(), p, n, seed=cfg.seed)
     stages = {name: float(rep.stage_ms[k]) for k, name in enumerate(STAGES)}
+    factors = None
+    if rep.has_factors:
+        k = int(rep.factors_k)
+        factors = LowRankFactors(np.asfortranarray(fU[:, :k]), fs[:k].copy(), np.asfortranarray(fV[:, :k]), k, True)
     return PipelineReport(int(rep.p), int(rep.n), int(rep.rho_r), int(rep.rho_c), trace, plan, xt, x,
-                          bool(rep.decoder_converged), int(rep.decoder_iterations), stages)
+                          bool(rep.decoder_converged), int(rep.decoder_iterations), stages,
+                          int(rep.detected_rank), factors, bool(rep.has_factors))

@@ -415,6 +415,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg_tol,
                         double prune_tol);
 
+void singular_values_device(Ctx* c, const double* A, i64 m, i64 n, double* sigma);
+template <typename T>
+void to_f64_device(Ctx* c, const T* a, i64 n, double* out);
+i64 detect_rank_host(const std::vector<double>& s, double thr);
+
 template <typename T>
 void approx_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const std::vector<i64>& om_r,
                           const std::vector<i64>& om_c, i64 p, i64 n, Csr* Lr, Csr* Lc,

@@ -51,7 +51,7 @@ __global__ void scatter_full_k(const T* __restrict__ Xt, i64 rho_r, i64 rho_c, c
 template <typename T>
 void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, const cpcag_pipeline_config& cfg,
                          T* Xt_out, T* X_out, i64* om_r_out, i64* om_c_out, double* objective,
-                         cpcag_pipeline_report* rep) {
+                         cpcag_pipeline_report* rep, const cpcag_pipeline_factors* factors) {
   std::memset(rep, 0, sizeof(*rep));
   rep->p = p;
   rep->n = n;
@@ -117,6 +117,23 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     fista_device<T>(c, Yt.p, rho_r, rho_c, Lr_s.get(), Lc_s.get(), cfg.frpcag, Xt_out, objective, &rep->trace);
   });
 
+  // pipeline.cpp:319-320: the detected rank of the compressed solution (its
+  // singular values only), outside the stage timers as in the reference.
+  {
+    const i64 q = std::min(rho_r, rho_c);
+    DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), sv(c, std::max<i64>(q, 1));
+    if (rho_r * rho_c) {
+      to_f64_device(c, Xt_out, rho_r * rho_c, A.p);
+      singular_values_device(c, A.p, rho_r, rho_c, sv.p);
+    }
+    std::vector<double> hs(static_cast<size_t>(q));
+    if (q) CUDA_OK(cudaMemcpyAsync(hs.data(), sv.p, sizeof(double) * q, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    rep->detected_rank = detect_rank_host(hs, cfg.approx.rank_threshold);
+  }
+  rep->has_factors = 0;
+  rep->factors_k = 0;
+
   rep->stage_ms[5] = tm.run("decode", [&] {
     if (full) {
       // pipeline.cpp:327-337: no compression, scatter back through the plan.
@@ -127,6 +144,19 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
       rep->decoder_iterations = 0;
       return;
     }
+    if (cfg.decoder_variant == CPCAG_DECODER_APPROX) {
+      i64 k = 0;
+      approx_decode_device<T>(c, Xt_out, rho_r, rho_c, om_r, om_c, p, n, Lr.get(), Lc.get(), cfg.approx, X_out,
+                              factors ? factors->U : nullptr, factors ? factors->sigma : nullptr,
+                              factors ? factors->V : nullptr, factors ? factors->k_cap : 0, &k);
+      rep->factors_k = k;
+      rep->has_factors = 1;
+      rep->decoder_converged = 1;
+      rep->decoder_iterations = 0;
+      return;
+    }
+    if (cfg.decoder_variant != CPCAG_DECODER_ALTERNATE)
+      invalid("run_pipeline: decoder variant not supported on the device path (alternate or approx)");
     int conv = 0;
     i64 it = 0;
     alternate_decode_device<T>(c, Xt_out, rho_r, rho_c, om_r.data(), om_c.data(), p, n, Lr.get(), Lc.get(),
@@ -145,7 +175,7 @@ using namespace cpcag_cuda;
 extern "C" int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void* Y, int64_t p, int64_t n,
                                        cpcag_csr W_r, cpcag_csr W_c, const cpcag_pipeline_config* cfg, void* Xt,
                                        void* X, int64_t* omega_r, int64_t* omega_c, double* objective,
-                                       cpcag_pipeline_report* report) {
+                                       cpcag_pipeline_report* report, const cpcag_pipeline_factors* factors) {
   auto run = [&](auto tag) {
     using T = decltype(tag);
     return guard([&] {
@@ -160,7 +190,7 @@ extern "C" int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void*
       OutView<T> xt(c, static_cast<T*>(Xt), static_cast<size_t>(std::max<i64>(rho_r, 1) * std::max<i64>(rho_c, 1)));
       OutView<T> x(c, static_cast<T*>(X), static_cast<size_t>(p * n));
       run_pipeline_device<T>(c, y.d, p, n, W_r ? as_csr(W_r) : nullptr, W_c ? as_csr(W_c) : nullptr, *cfg, xt.d, x.d,
-                             omega_r, omega_c, objective, report);
+                             omega_r, omega_c, objective, report, factors);
       xt.flush(c);
       x.flush(c);
       sync(c);

@@ -238,7 +238,7 @@ def test_pipeline_small_matches_oracle_stages(P, ctx):
     p, n = Y.shape
     cfg = P.PipelineConfig(knn=10, a=4, b=4, frpcag=P.FrpcagConfig(gamma_r=math.sqrt(max(p, n)),
                            gamma_c=math.sqrt(max(p, n)), tol=1e-300, max_iter=60),
-                           decoder=P.DecoderConfig(1.0, 1e-8, 100), lambda_k1_r=0.5, lambda_k1_c=0.5, seed=1602)
+                           decoder=P.DecoderConfig(1.0, 1e-8, 100, variant="alternate"), lambda_k1_r=0.5, lambda_k1_c=0.5, seed=1602)
     rep = P.run_pipeline(Y, cfg, ctx=ctx)
     # oracle stages
     gr = O.build_knn_graph(Y, True, 10)
@@ -255,6 +255,31 @@ def test_pipeline_small_matches_oracle_stages(P, ctx):
     assert rel(rep.X, dec.X) <= 1e-7
     assert abs(rep.decoder_iterations - dec.iterations) <= 1
     assert all(rep.stages[s] > 0 for s in ("graphs", "kron", "solve", "decode"))
+
+
+def test_pipeline_approx_decoder_matches_oracle(P, ctx):
+    """The reference default decoder (pipeline.cpp:361-367) and the detected
+    rank (pipeline.cpp:319-320) through run_pipeline."""
+    from paper_1602_02070_b200.workloads import config0
+
+    Y, truth = config0(seed=1602, small=True)
+    p, n = Y.shape
+    g = math.sqrt(max(p, n))
+    cfg = P.PipelineConfig(knn=10, a=4, b=4, frpcag=P.FrpcagConfig(gamma_r=g, gamma_c=g, tol=1e-300, max_iter=60),
+                           decoder=P.DecoderConfig(pcg_tol=1e-12, variant="approx", rank_threshold=0.1), seed=1602)
+    rep = P.run_pipeline(Y, cfg, ctx=ctx)
+    gr = O.build_knn_graph(Y, True, 10)
+    gc = O.build_knn_graph(Y, False, 10)
+    plan = O.draw_plan(p, n, -(-p // 4), -(-n // 4), seed=1602)
+    Yt = O.subsample(Y, plan)
+    Lr_t = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
+    Lc_t = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
+    Xt, _ = O.fista_solve(Yt, Lr_t, Lc_t, O.FrpcagConfig(g, g, "l1", 1e-300, 60))
+    assert rep.detected_rank == O.detect_rank(O.thin_svd(Xt)[1], 0.1)
+    dec = O.approx_decode(Xt, plan, gr.laplacian, gc.laplacian, rank_threshold=0.1, pcg_tol=1e-12)
+    assert rep.has_factors and rep.factors.k == dec.k
+    assert rel(rep.X, dec.X) <= 1e-6
+    assert rel(rep.factors.U, dec.U) <= 1e-6 and np.allclose(rep.factors.sigma, dec.sigma, rtol=1e-7)
 
 
 def test_pipeline_stage_error_is_tagged(P, ctx):
