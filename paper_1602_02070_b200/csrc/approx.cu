@@ -170,40 +170,6 @@ void thin_svd_device(Ctx* c, const double* A, i64 m, i64 n, double* U, double* s
   if (inf != 0) runtime("thin_svd: solver did not converge (info " + std::to_string(inf) + ")");
 }
 
-// Singular values only (descending) of the m x n fp64 matrix A.
-void singular_values_device(Ctx* c, const double* A, i64 m, i64 n, double* sigma) {
-  const i64 mn = m * n, q = std::min(m, n);
-  if (q == 0) return;
-  {
-    DevBuf<int> flag(c, 1);
-    flag.zero(c);
-    nonfinite_k<<<stride_blocks(c, mn), kBlock, 0, c->stream>>>(mn, A, flag.p);
-    launched(c);
-    if (read_back(c, flag.p)) invalid("thin_svd: non-finite input");
-  }
-  if (m > INT32_MAX || n > INT32_MAX) invalid("thin_svd: matrix too large");
-  cusolverDnHandle_t h = solver_handle(c);
-  gesvdjInfo_t params = nullptr;
-  solver_ok(cusolverDnCreateGesvdjInfo(&params), "gesvdj info");
-  std::unique_ptr<std::remove_pointer<gesvdjInfo_t>::type, void (*)(gesvdjInfo_t)> own(
-      params, [](gesvdjInfo_t p) { cusolverDnDestroyGesvdjInfo(p); });
-  solver_ok(cusolverDnXgesvdjSetSortEig(params, 1), "gesvdj sort");
-  DevBuf<double> W(c, mn), U(c, 1), V(c, 1);
-  CUDA_OK(cudaMemcpyAsync(W.p, A, sizeof(double) * mn, cudaMemcpyDeviceToDevice, c->stream));
-  const int mi = static_cast<int>(m), ni = static_cast<int>(n);
-  int lwork = 0;
-  solver_ok(cusolverDnDgesvdj_bufferSize(h, CUSOLVER_EIG_MODE_NOVECTOR, 1, mi, ni, W.p, mi, sigma, U.p, mi, V.p, ni,
-                                         &lwork, params),
-            "gesvdj buffer");
-  DevBuf<double> work(c, std::max(lwork, 1));
-  DevBuf<int> info(c, 1);
-  solver_ok(cusolverDnDgesvdj(h, CUSOLVER_EIG_MODE_NOVECTOR, 1, mi, ni, W.p, mi, sigma, U.p, mi, V.p, ni, work.p,
-                              lwork, info.p, params),
-            "gesvdj");
-  const int inf = read_back(c, info.p);
-  if (inf != 0) runtime("thin_svd: solver did not converge (info " + std::to_string(inf) + ")");
-}
-
 template <typename T>
 void to_f64_device(Ctx* c, const T* a, i64 n, double* out) {
   if (!n) return;

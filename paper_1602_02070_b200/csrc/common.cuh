@@ -415,7 +415,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg_tol,
                         double prune_tol);
 
-void singular_values_device(Ctx* c, const double* A, i64 m, i64 n, double* sigma);
+void thin_svd_device(Ctx* c, const double* A, i64 m, i64 n, double* U, double* sigma, double* V);
 template <typename T>
 void to_f64_device(Ctx* c, const T* a, i64 n, double* out);
 i64 detect_rank_host(const std::vector<double>& s, double thr);
