@@ -16,6 +16,7 @@
 // RHS blocks are sized to the free HBM so 50 000-column reductions run in
 // slices.
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <memory>
 #include <numeric>
@@ -360,7 +361,8 @@ constexpr int kCpb = 4;
 
 __device__ __forceinline__ i64 slab_at(i64 n, i64 i, i64 c) { return ((c / kCpb) * n + i) * kCpb + (c % kCpb); }
 
-__global__ void __launch_bounds__(1024, 1) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
                                                         const int* __restrict__ ci, const double* __restrict__ v,
                                                         const double* __restrict__ inv, const double* __restrict__ B,
                                                         double* __restrict__ X, double* __restrict__ R,
@@ -605,9 +607,19 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   DevBuf<ColState> st(c, nb);
   st.zero(c);
   {
+    // One CTA per kCpb columns: 1024 threads while the CTAs fit in one wave,
+    // else 512 threads at 2 CTAs per SM (cfg1 rows: 258 CTAs, one wave).
+    const i64 ctas = nbp / kCpb;
+    int nt = ctas > c->num_sms ? 512 : 1024;
+    if (const char* e = std::getenv("CPCAG_PCG_NT")) nt = std::atoi(e) == 512 ? 512 : 1024;
     KScope ks_(c, "pcg_persistent");
-    pcg_persistent_k<<<static_cast<unsigned>(nbp / kCpb), 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
-                                                                              R.p, P.p, AP.p, tol, max_iter, st.p);
+    if (nt == 512)
+      pcg_persistent_k<512><<<static_cast<unsigned>(ctas), 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
+                                                                                R.p, P.p, AP.p, tol, max_iter, st.p);
+    else
+      pcg_persistent_k<1024><<<static_cast<unsigned>(ctas), 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B,
+                                                                                  X, R.p, P.p, AP.p, tol, max_iter,
+                                                                                  st.p);
     launched(c);
   }
   CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));
