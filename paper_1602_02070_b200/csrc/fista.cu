@@ -12,6 +12,8 @@
 //   K3 momentum   Z_{j+1} = S_j + coef (S_j - S_{j-1}), ||Z_j||^2,
 //                 ||Z_{j+1} - Z_j||^2, stop test
 // Buffers rotate by parity of j (S_j in S[j&1], Z_j in Z[j&1]).
+#include <cstdlib>
+#include <string>
 #include <algorithm>
 
 #include "common.cuh"
@@ -427,6 +429,120 @@ __global__ void fista_splitk_objective_k(i64 rr, i64 rc, int S, double gamma_r, 
   }
 }
 
+// ---- linearity variant of the fp32 split-K path.  The
+// objective already computes L_r S_j and S_j L_c; by linearity
+//   L Z_{j+1} = L (S_j + coef (S_j - S_{j-1})) = LS_j + coef (LS_j - LS_{j-1}),
+// so the gradient of the next iteration needs no GEMM: one GEMM pair per
+// iteration instead of two.  LS is recomputed from S every iteration, so
+// rounding does not accumulate; the result stays within the fp32 tolerance
+// (the fp64 paths keep the reference's direct products).
+struct LinBufs {
+  float *LZr, *LZc;      // L_r Z_j, Z_j L_c
+  float *LSr[2], *LSc[2];  // L_r S_j, S_j L_c for j and j - 1 (index j & 1)
+};
+
+__global__ void fista_lin_init_k(i64 rr, i64 rc, int S, SplitWs ws, LinBufs lb) {
+  const i64 m = rr * rc;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < m; e += (i64)gridDim.x * blockDim.x) {
+    float x1, x2;
+    splitk_sum(ws, m, S, e, x1, x2);
+    lb.LZr[e] = x1;
+    lb.LZc[e] = x2;
+    lb.LSr[0][e] = x1;  // S_0 = Y = Z_1
+    lb.LSc[0][e] = x2;
+  }
+}
+
+__global__ void fista_lin_grad_prox_k(i64 rr, i64 rc, float s_r, float s_c, int use_r, int use_c, int loss,
+                                      float step, const float* __restrict__ Z, const float* __restrict__ Y,
+                                      float* __restrict__ Sout, LinBufs lb, const FistaState* st) {
+  if (st->done) return;
+  const i64 m = rr * rc;
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < m; e += (i64)gridDim.x * blockDim.x) {
+    float g = 0.f;
+    if (use_c) g = __fadd_rn(g, __fmul_rn(s_c, lb.LZc[e]));
+    if (use_r) g = __fadd_rn(g, __fmul_rn(s_r, lb.LZr[e]));
+    const float arg = __fsub_rn(Z[e], __fmul_rn(step, g));
+    Sout[e] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[e], step) : prox_l1_elem(arg, Y[e], step);
+  }
+}
+
+__global__ void fista_lin_objective_k(i64 rr, i64 rc, int S, double gamma_r, double gamma_c, int loss,
+                                      const float* __restrict__ Sv, const float* __restrict__ Y, SplitWs ws,
+                                      float* __restrict__ LSr, float* __restrict__ LSc, double* partials,
+                                      double* trace, FistaState* st) {
+  if (st->done) return;
+  const int use_r = gamma_r != 0.0, use_c = gamma_c != 0.0;
+  const i64 m = rr * rc;
+  double sm3[3] = {0.0, 0.0, 0.0};
+  for (i64 e = blockIdx.x * (i64)blockDim.x + threadIdx.x; e < m; e += (i64)gridDim.x * blockDim.x) {
+    float x1, x2;
+    splitk_sum(ws, m, S, e, x1, x2);
+    LSr[e] = x1;
+    LSc[e] = x2;
+    const double x = static_cast<double>(Sv[e]);
+    const double d = static_cast<double>(Y[e]) - x;
+    sm3[0] += loss == CPCAG_LOSS_L2 ? d * d : fabs(d);
+    sm3[1] += static_cast<double>(x2) * x;
+    sm3[2] += static_cast<double>(x1) * x;
+  }
+  double tot[3];
+  if (grid_sum_last<3>(sm3, partials, &st->cnt[0], tot) && threadIdx.x == 0) {
+    double val = tot[0];
+    if (use_c) val += gamma_c * tot[1];
+    if (use_r) val += gamma_r * tot[2];
+    const i64 j = st->j;
+    if (!isfinite(val)) {
+      st->err = 1;
+      st->err_j = j;
+      st->done = 1;
+      return;
+    }
+    trace[j - 1] = val;
+    st->iterations = j;
+    const double t = st->t;
+    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    st->t_next = tn;
+    st->coef = (t - 1.0) / tn;
+  }
+}
+
+__global__ void fista_lin_momentum_k(i64 N, const float* __restrict__ S, const float* __restrict__ Sp,
+                                     const float* __restrict__ Z, float* __restrict__ Zn,
+                                     const float* __restrict__ LSr, const float* __restrict__ LSrp,
+                                     const float* __restrict__ LSc, const float* __restrict__ LScp, LinBufs lb,
+                                     double tol, i64 max_iter, double* partials, FistaState* st) {
+  if (st->done) return;
+  const float coef = static_cast<float>(st->coef);
+  double s[2] = {0.0, 0.0};
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const float sv = S[q];
+    const float zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[q])));
+    const float z = Z[q];
+    Zn[q] = zn;
+    const float a = LSr[q], b = LSc[q];
+    lb.LZr[q] = add_rn(a, mul_rn(coef, sub_rn(a, LSrp[q])));
+    lb.LZc[q] = add_rn(b, mul_rn(coef, sub_rn(b, LScp[q])));
+    const double zd = static_cast<double>(z);
+    const double dd = static_cast<double>(sub_rn(zn, z));
+    s[0] += zd * zd;
+    s[1] += dd * dd;
+  }
+  double tot[2];
+  if (grid_sum_last<2>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double denom = tot[0], change = tot[1];
+    st->frc = denom > 0.0 ? change / denom : change;
+    if (change < tol * denom) {
+      st->converged = 1;
+      st->done = 1;
+      return;
+    }
+    st->t = st->t_next;
+    st->j += 1;
+    if (st->j > max_iter) st->done = 1;
+  }
+}
+
 template <typename T>
 struct SplitLauncher {
   static void grad(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, T, T, int, int, int, T, const T*, const T*, T*,
@@ -453,6 +569,56 @@ struct SplitLauncher<float> {
     fista_splitk_objective_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), gr, gc, loss, S, Y, ws,
                                                         partials, trace, st);
     launched(c);
+  }
+};
+
+template <typename T>
+struct LinLauncher {  // fp32 only; other precisions never take the linearity path
+  static void init(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, int, int, const T*, const SplitWs&,
+                   const LinBufs&, FistaState*) {}
+  static void step(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, T, T, int, int, const cpcag_frpcag_config&, T,
+                   const T*, const T*, T*, const T*, T*, const SplitWs&, const LinBufs&, i64, double*, double*,
+                   FistaState*) {}
+};
+template <>
+struct LinLauncher<float> {
+  static void init(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, int use_r, int use_c,
+                   const float* Y, const SplitWs& ws, const LinBufs& lb, FistaState* st) {
+    fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, use_r, use_c, Y, ws, st);
+    launched(c);
+    fista_lin_init_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), ws, lb);
+    launched(c);
+  }
+  // One FISTA iteration: prox from L Z (no GEMM), one GEMM pair on S_j for
+  // the objective, momentum carrying L Z_{j+1} forward.
+  static void step(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r, float s_c,
+                   int use_r, int use_c, const cpcag_frpcag_config& cfg, float stepT, const float* Z, const float* Y,
+                   float* S, const float* Sp, float* Zn, const SplitWs& ws, const LinBufs& lb, i64 j, double* partials,
+                   double* trace, FistaState* st) {
+    const i64 m = rr * rc;
+    {
+      KScope ks_(c, "fista_grad_prox");
+      fista_lin_grad_prox_k<<<eb, 256, 0, c->stream>>>(rr, rc, s_r, s_c, use_r, use_c, cfg.loss, stepT, Z, Y, S, lb,
+                                                       st);
+      launched(c);
+    }
+    {
+      KScope ks_(c, "fista_objective");
+      fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, S, ws,
+                                                       st);
+      launched(c);
+      fista_lin_objective_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), cfg.gamma_r, cfg.gamma_c,
+                                                       cfg.loss, S, Y, ws, lb.LSr[j & 1], lb.LSc[j & 1], partials,
+                                                       trace, st);
+      launched(c);
+    }
+    {
+      KScope ks_(c, "fista_momentum");
+      fista_lin_momentum_k<<<eb, 256, 0, c->stream>>>(m, S, Sp, Z, Zn, lb.LSr[j & 1], lb.LSr[(j - 1) & 1],
+                                                      lb.LSc[j & 1], lb.LSc[(j - 1) & 1], lb, cfg.tol, cfg.max_iter,
+                                                      partials, st);
+      launched(c);
+    }
   }
 };
 
@@ -552,6 +718,17 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     ssum.alloc(c, 3 * static_cast<size_t>(tiles));
     ws = SplitWs{sp1.p, sp2.p, scnt.p, scnt.p + tiles, ssum.p};
   }
+  // Linearity variant (fp32 split-K): one GEMM pair per iteration.
+  bool lin = splitk;
+  if (const char* e = std::getenv("CPCAG_FISTA_LIN")) lin = lin && std::string(e) != "0";
+  DevBuf<T> lbuf;
+  LinBufs lb{};
+  if (lin) {
+    lbuf.alloc(c, 6 * static_cast<size_t>(N));
+    float* b = reinterpret_cast<float*>(lbuf.p);
+    lb = LinBufs{b, b + N, {b + 2 * N, b + 3 * N}, {b + 4 * N, b + 5 * N}};
+    LinLauncher<T>::init(c, gk, nb1, rows, cols, Dr.p, Dc.p, use_r, use_c, Y, ws, lb, st.p);
+  }
 
   i64 j = 1;
   FistaState host{};
@@ -563,6 +740,11 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       T* Sj = Sb[j & 1].p;
       const T* Sprev = Sb[(j - 1) & 1].p;
       T* Znext = Zb[(j + 1) & 1].p;
+      if (lin) {
+        LinLauncher<T>::step(c, gk, nb1, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg, stepT, Zj, Y, Sj, Sprev,
+                             Znext, ws, lb, j, part.p, tr.p, st.p);
+        continue;
+      }
       if (splitk) {
         {
           KScope ks_(c, "fista_grad_prox");
