@@ -170,6 +170,92 @@ void thin_svd_device(Ctx* c, const double* A, i64 m, i64 n, double* U, double* s
   if (inf != 0) runtime("thin_svd: solver did not converge (info " + std::to_string(inf) + ")");
 }
 
+// ---------------------------------------------------------------- Gram SVD
+// The decoder only needs the leading singular triplets of the small sampled
+// matrix (k at sigma_k / sigma_1 >= rank_threshold), so it goes through the
+// Gram matrix of the short side: G = A^T A (n <= m) or A A^T, eigenpairs by
+// cuSOLVER syevd, sigma = sqrt(lambda), and the long-side vectors as
+// A v / sigma for the k requested columns.  The error of a used vector is
+// ~eps (sigma_1 / sigma_k)^2 <= 1e-14 at the default threshold 0.1.
+__global__ void gram_k(i64 m, i64 n, bool tall, const double* __restrict__ A, double* __restrict__ G) {
+  // tall: G (n x n) = A^T A, else G (m x m) = A A^T; fixed sequential order.
+  const i64 q = tall ? n : m;
+  const i64 a = blockIdx.x * (i64)blockDim.x + threadIdx.x, b = blockIdx.y;
+  if (a >= q || b > a) return;
+  double s = 0.0;
+  if (tall)
+    for (i64 i = 0; i < m; ++i) s += A[i + a * m] * A[i + b * m];
+  else
+    for (i64 j = 0; j < n; ++j) s += A[a + j * m] * A[b + j * m];
+  G[a + b * q] = s;
+  G[b + a * q] = s;
+}
+
+// Reverse eigenpairs to descending order; sigma = sqrt(max(lambda, 0)).
+__global__ void eig_to_svd_k(i64 q, i64 kvec, const double* __restrict__ lam, const double* __restrict__ E,
+                             double* __restrict__ sigma, double* __restrict__ W) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < q) sigma[i] = sqrt(fmax(lam[q - 1 - i], 0.0));
+  for (i64 j = blockIdx.y; j < kvec; j += gridDim.y)
+    if (i < q) W[i + j * q] = E[i + (q - 1 - j) * q];
+}
+
+// Out (len x k) = op(A) W diag(1 / sigma): tall -> A (m x n) W (n x k);
+// wide -> A^T (n x m) W (m x k).
+__global__ void project_k(i64 m, i64 n, bool tall, i64 k, const double* __restrict__ A, const double* __restrict__ W,
+                          const double* __restrict__ sigma, double* __restrict__ Out) {
+  const i64 len = tall ? m : n, q = tall ? n : m;
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= len) return;
+  for (i64 j = blockIdx.y; j < k; j += gridDim.y) {
+    double s = 0.0;
+    for (i64 t = 0; t < q; ++t) s += (tall ? A[i + t * m] : A[t + i * m]) * W[t + j * q];
+    Out[i + j * len] = s / sigma[j];
+  }
+}
+
+// sigma (q = min(m, n), descending); U (m x kvec) and V (n x kvec) when
+// kvec > 0 (every used sigma must be > 0).
+void gram_svd_device(Ctx* c, const double* A, i64 m, i64 n, i64 kvec, double* sigma, double* U, double* V) {
+  const i64 q = std::min(m, n);
+  if (q == 0) return;
+  {
+    DevBuf<int> flag(c, 1);
+    flag.zero(c);
+    nonfinite_k<<<stride_blocks(c, m * n), kBlock, 0, c->stream>>>(m * n, A, flag.p);
+    launched(c);
+    if (read_back(c, flag.p)) invalid("thin_svd: non-finite input");
+  }
+  if (q > INT32_MAX) invalid("thin_svd: matrix too large");
+  const bool tall = m >= n;
+  DevBuf<double> G(c, q * q), lam(c, q);
+  gram_k<<<dim3(blocks_for(q), static_cast<unsigned>(std::min<i64>(q, 65535))), kBlock, 0, c->stream>>>(m, n, tall, A,
+                                                                                                        G.p);
+  launched(c);
+  cusolverDnHandle_t h = solver_handle(c);
+  const cusolverEigMode_t mode = kvec > 0 ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
+  const int qi = static_cast<int>(q);
+  int lwork = 0;
+  solver_ok(cusolverDnDsyevd_bufferSize(h, mode, CUBLAS_FILL_MODE_LOWER, qi, G.p, qi, lam.p, &lwork), "syevd buffer");
+  DevBuf<double> work(c, std::max(lwork, 1));
+  DevBuf<int> info(c, 1);
+  solver_ok(cusolverDnDsyevd(h, mode, CUBLAS_FILL_MODE_LOWER, qi, G.p, qi, lam.p, work.p, lwork, info.p), "syevd");
+  if (read_back(c, info.p) != 0) runtime("thin_svd: eigensolver did not converge");
+  DevBuf<double> Wv(c, std::max<i64>(q * kvec, 1));
+  eig_to_svd_k<<<dim3(blocks_for(q), static_cast<unsigned>(std::max<i64>(1, std::min<i64>(kvec, 65535)))), kBlock, 0,
+                 c->stream>>>(q, kvec, lam.p, G.p, sigma, Wv.p);
+  launched(c);
+  if (kvec == 0) return;
+  // short-side vectors are the eigenvectors; the long side is projected
+  double* shortv = tall ? V : U;
+  double* longv = tall ? U : V;
+  CUDA_OK(cudaMemcpyAsync(shortv, Wv.p, sizeof(double) * q * kvec, cudaMemcpyDeviceToDevice, c->stream));
+  const i64 len = tall ? m : n;
+  project_k<<<dim3(blocks_for(len), static_cast<unsigned>(std::min<i64>(kvec, 65535))), kBlock, 0, c->stream>>>(
+      m, n, tall, kvec, A, Wv.p, sigma, longv);
+  launched(c);
+}
+
 template <typename T>
 void to_f64_device(Ctx* c, const T* a, i64 n, double* out) {
   if (!n) return;
@@ -202,12 +288,13 @@ void approx_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const std::
     to_f64_k<T><<<stride_blocks(c, rho_r * rho_c), kBlock, 0, c->stream>>>(rho_r * rho_c, Xt, A.p);
     launched(c);
   }
-  thin_svd_device(c, A.p, rho_r, rho_c, Ut.p, st.p, Vt.p);
+  gram_svd_device(c, A.p, rho_r, rho_c, 0, st.p, nullptr, nullptr);
   std::vector<double> s(static_cast<size_t>(q));
   if (q) CUDA_OK(cudaMemcpyAsync(s.data(), st.p, sizeof(double) * q, cudaMemcpyDeviceToHost, c->stream));
   sync(c);
   const i64 k = detect_rank_host(s, cfg.rank_threshold);
   if (k == 0) runtime("approximate decoder: no singular value above the rank threshold");
+  gram_svd_device(c, A.p, rho_r, rho_c, k, st.p, Ut.p, Vt.p);
 
   DevBuf<double> U(c, p * k), V(c, n * k);
   graph_upsample_device(c, Lr, om_r, Ut.p, k, cfg.pcg_tol, cfg.pcg_max_iter, U.p);

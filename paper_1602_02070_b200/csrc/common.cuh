@@ -416,6 +416,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
                         double prune_tol);
 
 void thin_svd_device(Ctx* c, const double* A, i64 m, i64 n, double* U, double* sigma, double* V);
+void gram_svd_device(Ctx* c, const double* A, i64 m, i64 n, i64 kvec, double* sigma, double* U, double* V);
 template <typename T>
 void to_f64_device(Ctx* c, const T* a, i64 n, double* out);
 i64 detect_rank_host(const std::vector<double>& s, double thr);

@@ -121,11 +121,10 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
   // singular values only), outside the stage timers as in the reference.
   {
     const i64 q = std::min(rho_r, rho_c);
-    DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), sv(c, std::max<i64>(q, 1)),
-        U(c, std::max<i64>(rho_r * q, 1)), V(c, std::max<i64>(rho_c * q, 1));
+    DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), sv(c, std::max<i64>(q, 1));
     if (rho_r * rho_c) {
       to_f64_device(c, Xt_out, rho_r * rho_c, A.p);
-      thin_svd_device(c, A.p, rho_r, rho_c, U.p, sv.p, V.p);
+      gram_svd_device(c, A.p, rho_r, rho_c, 0, sv.p, nullptr, nullptr);
     }
     std::vector<double> hs(static_cast<size_t>(q));
     if (q) CUDA_OK(cudaMemcpyAsync(hs.data(), sv.p, sizeof(double) * q, cudaMemcpyDeviceToHost, c->stream));
