@@ -846,6 +846,7 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
   const double per_col = 6.0 * 8.0 * static_cast<double>(ni) + 64.0;
   i64 slice = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
+  if (const char* e = std::getenv("CPCAG_KRON_SLICE")) slice = std::max<i64>(1, std::atoll(e));
   slice = std::max<i64>(1, std::min<i64>(slice, static_cast<i64>(active.size())));
   const i64 max_iter = 20 * ni + 100;
 

@@ -1,2 +1,1 @@
-timeout -s KILL 400 python -m pytest tests/test_gpu_approx.py tests/test_gpu_graph.py -m gpu -q -x -p no:cacheprovider > gpurun_out/t39.log 2>&1; tail -3 gpurun_out/t39.log
-timeout -s KILL 400 python bench.py --steps 5 --warmup 3 > gpurun_out/bench39.log 2>&1; tail -1 gpurun_out/bench39.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['stage_ms'])"
+timeout -s KILL 300 python tools/bench_stages.py > gpurun_out/stages40.log 2>&1; cat gpurun_out/stages40.log | cut -c1-200 | tail -8
