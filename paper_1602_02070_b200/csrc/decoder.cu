@@ -585,6 +585,101 @@ __global__ void __launch_bounds__(256) cg_apply_fast_k(int p, int c_lo, int c_hi
   }
 }
 
+// fast2: two rows per thread (i and i + 256) so each staged L_c entry and
+// its address arithmetic serve two gathers (the fast apply is issue- and
+// latency-bound, ~6 instructions per 4-byte gather).
+template <typename T>
+__global__ void __launch_bounds__(256, 4) cg_apply_fast2_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                           int cols_per_cta, const T* __restrict__ P,
+                                                           T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int RB = 512;
+  const int i0 = blockIdx.x * RB;
+  const int i1 = min(p, i0 + RB);
+  const int cb = blockIdx.y * cols_per_cta;
+  const int ce = min(n, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0];
+  const int er = static_cast<int>(Lr.rp[i1] - kr_base);
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0;
+  const int ec = cb < ce ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  OffEnt<T>* Er = reinterpret_cast<OffEnt<T>*>(smraw);
+  OffEnt<T>* Ec = Er + er;
+  int* crp = reinterpret_cast<int*>(Ec + ec);
+  for (int k = threadIdx.x; k < er; k += blockDim.x) {
+    OffEnt<T> e;
+    e.v = Lr.v[kr_base + k];
+    e.off = Lr.ci[kr_base + k];
+    Er[k] = e;
+  }
+  for (int k = threadIdx.x; k < ec; k += blockDim.x) {
+    OffEnt<T> e;
+    e.v = Lc.v[kc_base + k];
+    e.off = Lc.ci[kc_base + k] * p;
+    Ec[k] = e;
+  }
+  for (int q = threadIdx.x; q <= ce - cb; q += blockDim.x) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  __syncthreads();
+  double s[1] = {0.0};
+  const int ia = i0 + threadIdx.x, ib = ia + 256;
+  const bool va = ia < p, vb = ib < p;
+  if (va) {
+    const int a0 = static_cast<int>(Lr.rp[ia] - kr_base), a1 = static_cast<int>(Lr.rp[ia + 1] - kr_base);
+    const int b0 = vb ? static_cast<int>(Lr.rp[ib] - kr_base) : 0, b1 = vb ? static_cast<int>(Lr.rp[ib + 1] - kr_base) : 0;
+    const bool sa = pl.rsel[ia] >= 0, sb = vb && pl.rsel[ib] >= 0;
+    const T* Pa = P + ia;
+    for (int c = cb; c < ce; ++c) {
+      const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
+      T xa = T(0), xb = T(0);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const OffEnt<T> e = Ec[k];
+        xa = madd_entry(xa, e.v, Pa[e.off]);
+        if (vb) xb = madd_entry(xb, e.v, Pa[e.off + 256]);
+      }
+      const T* pc = P + static_cast<i64>(c) * p;
+      T ya = T(0), yb = T(0);
+#pragma unroll 4
+      for (int k = a0; k < a1; ++k) {
+        const OffEnt<T> e = Er[k];
+        ya = madd_entry(ya, e.v, pc[e.off]);
+      }
+#pragma unroll 4
+      for (int k = b0; k < b1; ++k) {
+        const OffEnt<T> e = Er[k];
+        yb = madd_entry(yb, e.v, pc[e.off]);
+      }
+      const bool cs = pl.csel[c] >= 0;
+      {
+        T out = add_rn(mul_rn(gc, xa), mul_rn(gr, ya));
+        const T pv = pc[ia];
+        if (sa && cs) out = add_rn(out, pv);
+        AP[ia + static_cast<i64>(c) * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+      if (vb) {
+        T out = add_rn(mul_rn(gc, xb), mul_rn(gr, yb));
+        const T pv = pc[ib];
+        if (sb && cs) out = add_rn(out, pv);
+        AP[ib + static_cast<i64>(c) * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 template <typename T>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
@@ -1358,6 +1453,28 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     }
   }
   if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
+  // fast2 geometry: 512-row blocks, ~16 CTAs per SM.
+  const unsigned gx2 = static_cast<unsigned>((p + 511) / 512);
+  const i64 y2cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx2);
+  const i64 cpc2 = std::max<i64>({i64{1}, std::min<i64>((n + std::min<i64>(n, y2cap) - 1) / std::max<i64>(1, std::min<i64>(n, y2cap)), 128),
+                                  (n + 65534) / 65535});
+  const dim3 gs2(gx2, static_cast<unsigned>(std::min<i64>((n + cpc2 - 1) / cpc2, 65535)));
+  size_t fast2_smem = 0;
+  if (variant == "fast2") {
+    i64 mer = 0, mec = 0;
+    for (unsigned b = 0; b < gx2; ++b) {
+      const i64 a = static_cast<i64>(b) * 512, e = std::min<i64>(p, a + 512);
+      mer = std::max(mer, rpr[e] - rpr[a]);
+    }
+    for (unsigned b = 0; b < gs2.y; ++b) {
+      const i64 a = static_cast<i64>(b) * cpc2, e = std::min<i64>(n, a + cpc2);
+      mec = std::max(mec, rpc[e] - rpc[a]);
+    }
+    fast2_smem = static_cast<size_t>(mer + mec) * sizeof(OffEnt<T>) + sizeof(int) * (cpc2 + 2) + 16;
+    if (!(p * n < (i64{1} << 31) && fast2_smem <= 96 * 1024)) variant = "staged";
+    else ensure_smem(cg_apply_fast2_k<T>, fast2_smem);
+    if (part.n < static_cast<size_t>(gs2.x) * gs2.y) part.alloc(c, static_cast<size_t>(gs2.x) * gs2.y);
+  }
   if (variant == "panel") {
     ensure_smem(cg_apply_panel_k<T>, panel_smem);
     if (part.n < panel_blocks) part.alloc(c, panel_blocks);
@@ -1399,6 +1516,10 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
                                                                   st.p);
         } else if (variant == "band") {
           band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
+        } else if (variant == "fast2") {
+          cg_apply_fast2_k<T><<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr,
+                                                                     gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
+                                                                     st.p);
         } else if (variant == "fast") {
           cg_apply_fast_k<T><<<gs, kBlock, fast_smem, c->stream>>>(static_cast<int>(p), 0, static_cast<int>(n), pr, pc,
                                                                   gr, gc, pl, static_cast<int>(cols_per_cta), P.p, AP.p,

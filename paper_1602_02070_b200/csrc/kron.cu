@@ -16,6 +16,7 @@
 // RHS blocks are sized to the free HBM so 50 000-column reductions run in
 // slices.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
 #include <memory>
@@ -866,6 +867,16 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
     trace_mark(c, "kron: slice setup");
     PcgBatchOut res;
     pcg_slab(c, Laa, inv.p, B.p, X.p, ni, nb, pcg_tol, max_iter, &res);
+    if (std::getenv("CPCAG_TRACE")) {
+      i64 mx = 0, sum = 0;
+      for (const ColState& cs : res.cols) {
+        mx = std::max<i64>(mx, cs.it);
+        sum += cs.it;
+      }
+      std::fprintf(stderr, "[kron] interior %lld, %lld solves, PCG iterations mean %.1f max %lld\n",
+                   static_cast<long long>(ni), static_cast<long long>(nb),
+                   nb ? static_cast<double>(sum) / nb : 0.0, static_cast<long long>(mx));
+    }
     for (i64 q = 0; q < nb; ++q) {
       const ColState& cs = res.cols[q];
       const i64 j = cols[q];

@@ -177,7 +177,10 @@ def _decoder_case(p=150, n=120, rr=40, rc=30, seed=21):
     return Lr, Lc, plan, Xt
 
 
-def test_alternate_decode_fp64_matches_oracle(P, ctx):
+@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "staged", "plain", "band"])
+def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
+    if variant != "default":
+        monkeypatch.setenv("CPCAG_APPLY", variant)
     Lr, Lc, plan_o, Xt = _decoder_case()
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
     res = P.alternate_decode(Xt, plan, to_device(ctx, Lr), to_device(ctx, Lc), P.SpectralGap(lambda_k1=0.3),
