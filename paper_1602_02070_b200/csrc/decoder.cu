@@ -1406,7 +1406,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 
   // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
   // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
-  std::string variant = p * n < (i64{1} << 31) ? "fast" : "staged";
+  std::string variant = p * n < (i64{1} << 31) ? "fast2" : "staged";
   if (BandApply<T>::preferred(p, n)) variant = "band";
   if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
   if (variant == "band" && !BandApply<T>::feasible(p)) variant = "staged";
