@@ -16,6 +16,7 @@
 // RHS blocks are sized to the free HBM so 50 000-column reductions run in
 // slices.
 #include <algorithm>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -362,8 +363,25 @@ constexpr int kCpb = 4;
 
 __device__ __forceinline__ i64 slab_at(i64 n, i64 i, i64 c) { return ((c / kCpb) * n + i) * kCpb + (c % kCpb); }
 
-template <int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
+// One slab row (kCpb = 4 columns, 32 bytes, 32-byte aligned) per access:
+// two 16-byte loads/stores instead of four 8-byte ones (the kernel is
+// L1/LSU-throughput bound on the scalar form).
+static_assert(kCpb == 4, "slab records are 4 doubles");
+__device__ __forceinline__ void ld4(const double* __restrict__ p, double (&o)[4]) {
+  const double2 x = *reinterpret_cast<const double2*>(p);
+  const double2 y = *reinterpret_cast<const double2*>(p + 2);
+  o[0] = x.x;
+  o[1] = x.y;
+  o[2] = y.x;
+  o[3] = y.y;
+}
+__device__ __forceinline__ void st4(double* __restrict__ p, const double (&v)[4]) {
+  *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  *reinterpret_cast<double2*>(p + 2) = make_double2(v[2], v[3]);
+}
+
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) pcg_persistent_k(i64 n, i64 nb, const i64* __restrict__ rp,
                                                         const int* __restrict__ ci, const double* __restrict__ v,
                                                         const double* __restrict__ inv, const double* __restrict__ B,
                                                         double* __restrict__ X, double* __restrict__ R,
@@ -384,23 +402,28 @@ __global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb,
     for (int q = 0; q < kCpb; ++q) ax[q] = 0.0;
     for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
       const double a = v[k];
-      const double* xr = X + base + static_cast<i64>(ci[k]) * kCpb;
+      double xr[4];
+      ld4(X + base + static_cast<i64>(ci[k]) * kCpb, xr);
 #pragma unroll
       for (int q = 0; q < kCpb; ++q) ax[q] = __dadd_rn(ax[q], __dmul_rn(a, xr[q]));
     }
     const double iv = inv[i];
+    const i64 at = base + i * kCpb;
+    double bv[4], rv[4], zv[4];
+    ld4(B + at, bv);
 #pragma unroll
     for (int q = 0; q < kCpb; ++q) {
-      const i64 at = base + i * kCpb + q;
-      const double b = B[at];
+      const double b = bv[q];
       const double r = __dsub_rn(b, ax[q]);
       const double z = __dmul_rn(iv, r);
-      R[at] = r;
-      P[at] = z;
+      rv[q] = r;
+      zv[q] = z;
       s3[q] += b * b;
       s3[kCpb + q] += r * z;
       s3[2 * kCpb + q] += r * r;
     }
+    st4(R + at, rv);
+    st4(P + at, zv);
   }
   block_sum<3 * kCpb>(s3);
   if (threadIdx.x == 0) {
@@ -442,16 +465,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb,
       for (int q = 0; q < kCpb; ++q) ap[q] = 0.0;
       for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
         const double a = v[k];
-        const double* pr = P + base + static_cast<i64>(ci[k]) * kCpb;
+        double pr[4];
+        ld4(P + base + static_cast<i64>(ci[k]) * kCpb, pr);
 #pragma unroll
         for (int q = 0; q < kCpb; ++q) ap[q] = __dadd_rn(ap[q], __dmul_rn(a, pr[q]));
       }
+      const i64 at = base + i * kCpb;
+      double pv[4];
+      ld4(P + at, pv);
+      st4(AP + at, ap);
 #pragma unroll
-      for (int q = 0; q < kCpb; ++q) {
-        const i64 at = base + i * kCpb + q;
-        AP[at] = ap[q];
-        cv[q] += P[at] * ap[q];
-      }
+      for (int q = 0; q < kCpb; ++q) cv[q] += pv[q] * ap[q];
     }
     block_sum<kCpb>(cv);
     // alpha, breakdown
@@ -478,17 +502,24 @@ __global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb,
     for (int q = 0; q < 2 * kCpb; ++q) s2[q] = 0.0;
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
       const double iv = inv[i];
+      const i64 at = base + i * kCpb;
+      double xv[4], pv[4], rv[4], av[4];
+      ld4(X + at, xv);
+      ld4(P + at, pv);
+      ld4(R + at, rv);
+      ld4(AP + at, av);
 #pragma unroll
       for (int q = 0; q < kCpb; ++q) {
         if (!live[q]) continue;
-        const i64 at = base + i * kCpb + q;
-        X[at] = __dadd_rn(X[at], __dmul_rn(alpha[q], P[at]));
-        const double r = __dsub_rn(R[at], __dmul_rn(alpha[q], AP[at]));
-        R[at] = r;
+        xv[q] = __dadd_rn(xv[q], __dmul_rn(alpha[q], pv[q]));
+        const double r = __dsub_rn(rv[q], __dmul_rn(alpha[q], av[q]));
+        rv[q] = r;
         const double z = __dmul_rn(iv, r);
         s2[q] += r * z;
         s2[kCpb + q] += r * r;
       }
+      st4(X + at, xv);
+      st4(R + at, rv);
     }
     block_sum<2 * kCpb>(s2);
     // p = z + beta p
@@ -497,12 +528,14 @@ __global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb,
     for (int q = 0; q < kCpb; ++q) beta[q] = s2[q] / rho_s[q];
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
       const double iv = inv[i];
+      const i64 at = base + i * kCpb;
+      double pv[4], rv[4];
+      ld4(P + at, pv);
+      ld4(R + at, rv);
 #pragma unroll
-      for (int q = 0; q < kCpb; ++q) {
-        if (!live[q]) continue;
-        const i64 at = base + i * kCpb + q;
-        P[at] = __dadd_rn(__dmul_rn(iv, R[at]), __dmul_rn(beta[q], P[at]));
-      }
+      for (int q = 0; q < kCpb; ++q)
+        if (live[q]) pv[q] = __dadd_rn(__dmul_rn(iv, rv[q]), __dmul_rn(beta[q], pv[q]));
+      st4(P + at, pv);
     }
     __syncthreads();
     if (threadIdx.x == 0)
@@ -524,13 +557,16 @@ __global__ void __launch_bounds__(NT, 1024 / NT) pcg_persistent_k(i64 n, i64 nb,
     for (int q = 0; q < kCpb; ++q) ax[q] = 0.0;
     for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
       const double a = v[k];
-      const double* xr = X + base + static_cast<i64>(ci[k]) * kCpb;
+      double xr[4];
+      ld4(X + base + static_cast<i64>(ci[k]) * kCpb, xr);
 #pragma unroll
       for (int q = 0; q < kCpb; ++q) ax[q] = __dadd_rn(ax[q], __dmul_rn(a, xr[q]));
     }
+    double bv[4];
+    ld4(B + base + i * kCpb, bv);
 #pragma unroll
     for (int q = 0; q < kCpb; ++q) {
-      const double e = __dsub_rn(B[base + i * kCpb + q], ax[q]);
+      const double e = __dsub_rn(bv[q], ax[q]);
       sr[q] += e * e;
     }
   }
@@ -611,16 +647,19 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
     // One CTA per kCpb columns: 1024 threads while the CTAs fit in one wave,
     // else 512 threads at 2 CTAs per SM (cfg1 rows: 258 CTAs, one wave).
     const i64 ctas = nbp / kCpb;
-    int nt = ctas > c->num_sms ? 512 : 1024;
-    if (const char* e = std::getenv("CPCAG_PCG_NT")) nt = std::atoi(e) == 512 ? 512 : 1024;
+    std::string cfg = ctas > c->num_sms ? "512x1" : "1024x1";
+    if (const char* e = std::getenv("CPCAG_PCG_NT")) cfg = e;
     KScope ks_(c, "pcg_persistent");
-    if (nt == 512)
-      pcg_persistent_k<512><<<static_cast<unsigned>(ctas), 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X,
-                                                                                R.p, P.p, AP.p, tol, max_iter, st.p);
+    const unsigned g = static_cast<unsigned>(ctas);
+    if (cfg == "512x2")
+      pcg_persistent_k<512, 2><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                        max_iter, st.p);
+    else if (cfg == "512x1")
+      pcg_persistent_k<512, 1><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                        max_iter, st.p);
     else
-      pcg_persistent_k<1024><<<static_cast<unsigned>(ctas), 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B,
-                                                                                  X, R.p, P.p, AP.p, tol, max_iter,
-                                                                                  st.p);
+      pcg_persistent_k<1024, 1><<<g, 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                          max_iter, st.p);
     launched(c);
   }
   CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));

@@ -1,1 +1,2 @@
-timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"pcg_persistent|cg_apply_fast2" -c 2 -o gpurun_out/kron_r1 -f python tools/profile_step.py > gpurun_out/ncu42.log 2>&1; tail -2 gpurun_out/ncu42.log
+timeout -s KILL 400 python -m pytest tests/test_gpu_graph.py tests/test_gpu_approx.py -m gpu -q -x -p no:cacheprovider > gpurun_out/t43.log 2>&1; tail -2 gpurun_out/t43.log
+timeout -s KILL 300 python tools/bench_stages.py > gpurun_out/stages43.log 2>&1; grep -E "kron" gpurun_out/stages43.log | cut -c1-200
