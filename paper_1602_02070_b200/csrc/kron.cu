@@ -647,7 +647,7 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
     // One CTA per kCpb columns: 1024 threads while the CTAs fit in one wave,
     // else 512 threads at 2 CTAs per SM (cfg1 rows: 258 CTAs, one wave).
     const i64 ctas = nbp / kCpb;
-    std::string cfg = ctas > c->num_sms ? "512x1" : "1024x1";
+    std::string cfg = ctas > c->num_sms ? "512x2" : "1024x1";
     if (const char* e = std::getenv("CPCAG_PCG_NT")) cfg = e;
     KScope ks_(c, "pcg_persistent");
     const unsigned g = static_cast<unsigned>(ctas);
