@@ -10,7 +10,8 @@ import sys
 
 TAGS = {
     "cg_apply": "cg_apply", "cg_residual": "cg_residual", "cg_update": "cg_update",
-    "fista_splitk_partial": "fista_grad_prox", "pcg_persistent": "pcg_persistent",
+    "fista_splitk_partial": "fista_objective", "pcg_persistent": "pcg_persistent",
+    "cg_apply_band": "cg_apply_band", "cg_apply_col": "cg_apply_col",
     "knn_tile": "knn_tile", "knn_tc_filter": "knn_tc_filter", "power_iter": "power_iter",
 }
 
@@ -31,7 +32,7 @@ WANT = [
 
 def to_mb(val, unit):
     v = float(val)
-    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1e-6)
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}.get(unit, 1e-6)
     return v * scale
 
 
@@ -52,7 +53,8 @@ def main(rep, json_out=None):
                 vals.append("-")
                 continue
             if key == "gpu__time_duration.sum":
-                f = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(u[key], 1.0)
+                f = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                     "second": 1e6, "s": 1e6}.get(u[key], 1.0)
                 vals.append(f"{float(d[key]) * f:.1f}")
             elif scale is None:
                 vals.append(f"{to_mb(d[key], u[key]):.1f}")
@@ -71,11 +73,12 @@ def main(rep, json_out=None):
         tot = sum(stalls.values()) or 1.0
         top = ", ".join(f"{k} {v / tot * 100:.0f}%" for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:3])
         print(f"| {name} | {' | '.join(vals)} | {top} |")
-        for frag, tag in TAGS.items():
+        for frag, tag in sorted(TAGS.items(), key=lambda kv: -len(kv[0])):  # most specific first
             if frag in name and "dram__bytes_read.sum" in d:
                 b = (to_mb(d["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) +
                      to_mb(d["dram__bytes_write.sum"], u["dram__bytes_write.sum"])) * 1e6
                 traffic.setdefault(tag, int(b))
+                break
     if json_out:
         json.dump(traffic, open(json_out, "w"), indent=1)
 
