@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __re
 // w (double-buffered by iteration parity) and its partial ||w||^2, then every
 // CTA sums the partials in the same fixed order and renormalises the whole of
 // v into its own shared copy.
-__global__ void __launch_bounds__(256) power_iter_coop_k(i64 n, const i64* __restrict__ rp,
+__global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
                                                          const double* __restrict__ v0, double* wbuf,
@@ -563,8 +563,13 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
     }
     return read_back(c, st.p).est;
   }
-  // One CTA per SM; slice CSR and v in shared memory when they fit.
-  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(c->num_sms, (n + 3) / 4)));
+  // As few CTAs as keep each CSR slice (~150 KB) in shared memory: every
+  // iteration ends in a grid barrier and a re-read of w, whose cost grows
+  // with the CTA count (the product itself is tiny).
+  const i64 nnz = A->nnz;
+  i64 want = std::max<i64>((nnz * 12 + 150 * 1024 - 1) / (150 * 1024), (n + 1023) / 1024);
+  if (const char* e = std::getenv("CPCAG_POWER_NB")) want = std::max<i64>(1, std::atoll(e));
+  const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>({static_cast<i64>(c->num_sms), want, n})));
   std::vector<i64> rph(static_cast<size_t>(n) + 1);
   CUDA_OK(cudaMemcpyAsync(rph.data(), A->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
@@ -580,7 +585,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   if (slice_in_smem) smem += static_cast<size_t>(max_slice) * 12 + 16;
   ensure_smem(power_iter_coop_k, smem);
   int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 256, smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 512, smem));
   if (per_sm < 1) invalid("power iteration: kernel does not fit on an SM");
   DevBuf<double> part(c, 2 * nb), wb(c, 2 * n);
   const i64* rp = A->rp;
@@ -594,7 +599,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
                   (void*)&tol, (void*)&max_iter, (void*)&slice_in_smem, (void*)&v_in_smem, (void*)&sp};
   {
     KScope ks_(c, "power_iter");
-    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(256), args, smem, c->stream));
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(512), args, smem, c->stream));
     launched(c);
   }
   return read_back(c, st.p).est;
