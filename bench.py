@@ -257,6 +257,8 @@ def run_ours(args, rank, local_rank, world):
     ctx.enable_kernel_timing(False)
     live = ctx.kernel_times()
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    print(f"[bench] step ms {[round(x, 2) for x in step_ms]} wall/step {(wall1 - wall0) / args.steps * 1e3:.2f} "
+          f"stages {[round(sum(r.stages.values()), 2) for r in reports]}", file=sys.stderr, flush=True)
     ms = sum(step_ms) / len(step_ms)
     if dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
