@@ -85,6 +85,8 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # diagnostics only: the driver's runs always sample
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -259,6 +261,8 @@ def run_ours(args, rank, local_rank, world):
     step_ms = [a.elapsed_time(b) for a, b in ev]
     print(f"[bench] step ms {[round(x, 2) for x in step_ms]} wall/step {(wall1 - wall0) / args.steps * 1e3:.2f} "
           f"stages {[round(sum(r.stages.values()), 2) for r in reports]}", file=sys.stderr, flush=True)
+    for r in reports:
+        print("[bench]   " + " ".join(f"{k}={v:.1f}" for k, v in r.stages.items()), file=sys.stderr, flush=True)
     ms = sum(step_ms) / len(step_ms)
     if dist:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)

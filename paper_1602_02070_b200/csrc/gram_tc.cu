@@ -17,6 +17,9 @@
 // before the shared-memory stage is refilled.
 #include <math_constants.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 
 #include "common.cuh"
@@ -316,6 +319,247 @@ __global__ void __launch_bounds__(128) knn_tc_filter_k(const float* __restrict__
 }
 
 size_t knn_tc_smem() { return 4 * static_cast<size_t>(tc::kTileBytes) + kCand * tc::kM * (sizeof(float) + sizeof(int)); }
+
+// ------------------------------------------------------------------ pipelined filter (TMA + warp roles)
+// Same arithmetic and selection as knn_tc_filter_k, restructured the
+// Blackwell way:
+//   warp 0    TMA producer: 2D tensor loads (SWIZZLE_128B, one 32-float k
+//             chunk = one 128-byte row per point) of A-hi, A-lo, B-hi, B-lo
+//             into a 3-stage ring, full/empty mbarriers;
+//   warp 1    MMA issuer: 3 tcgen05.mma kind::tf32 per k8 step into one of
+//             two TMEM accumulators (2 x 128 columns), commit -> empty[stage]
+//             and, after the last k chunk, -> tmem_full[acc];
+//   warps 2-5 epilogue (TMEM lane quarter w % 4 = 32 query rows each):
+//             distances + top-kCand insertion for tile t while the MMAs of
+//             tile t+1 run; arrive tmem_empty[acc].
+namespace tc2 {
+constexpr int kStages = 3;
+constexpr int kTile = 128 * 32 * 4;        // 16 KiB: 128 rows x 128 B
+constexpr int kStageBytes = 4 * kTile;     // Ah, Al, Bh, Bl
+constexpr int kThreads = 192;
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc::smem_u32(mbar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(tc::smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* mbar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(mbar))
+      : "memory");
+}
+// K-major SWIZZLE_128B operand: rows of 128 B, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;    // SBO
+  d |= static_cast<uint64_t>(1) << 46;            // sm100 descriptor version
+  d |= static_cast<uint64_t>(2) << 61;            // SWIZZLE_128B
+  return d;
+}
+}  // namespace tc2
+
+__global__ void __launch_bounds__(tc2::kThreads, 1)
+    knn_tc_filter2_k(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapL,
+                     const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split, float* __restrict__ cand_d,
+                     int* __restrict__ cand_j) {
+  using namespace tc;
+  using namespace tc2;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* lst_d = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [kCand][128]
+  int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);                // [kCand][128]
+  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kM;
+  const i64 n_tiles = (n + kN - 1) / kN;
+  const i64 jt0 = static_cast<i64>(blockIdx.y) * tiles_per_split;
+  const i64 jt1 = min(n_tiles, jt0 + tiles_per_split);
+  const int nkc = static_cast<int>(dp / kKc);
+  if (warp == 1) tmem_alloc(&tmem_base, 2 * kN);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp >= 2) {
+    const int r = (warp & 3) * 32 + lane;
+    for (int q = 0; q < kCand; ++q) {
+      lst_d[q * kM + r] = CUDART_INF_F;
+      lst_j[q * kM + r] = INT32_MAX;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = tmem_base;
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (i64 jt = jt0; jt < jt1; ++jt) {
+        const int j0 = static_cast<int>(jt * kN);
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          unsigned char* st = smem + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          tma_load_2d(st, &mapH, &full[stage], kc * kKc, static_cast<int>(i0));
+          tma_load_2d(st + kTile, &mapL, &full[stage], kc * kKc, static_cast<int>(i0));
+          tma_load_2d(st + 2 * kTile, &mapH, &full[stage], kc * kKc, j0);
+          tma_load_2d(st + 3 * kTile, &mapL, &full[stage], kc * kKc, j0);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(kM, kN);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      for (i64 jt = jt0; jt < jt1; ++jt) {
+        mbar_wait(&tempty[acc], aphase ^ 1u);
+        fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(acc * kN);
+        for (int kc = 0; kc < nkc; ++kc) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t ah = smem_u32(smem + stage * kStageBytes);
+          const uint32_t al = ah + kTile, bh = ah + 2 * kTile, bl = ah + 3 * kTile;
+#pragma unroll
+          for (int kk = 0; kk < kKc / 8; ++kk) {
+            const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
+            const uint32_t accum = (kc > 0 || kk > 0) ? 1u : 0u;
+            mma_tf32(d, desc_sw128(ah + off), desc_sw128(bh + off), idesc, accum);
+            mma_tf32(d, desc_sw128(ah + off), desc_sw128(bl + off), idesc, 1u);
+            mma_tf32(d, desc_sw128(al + off), desc_sw128(bh + off), idesc, 1u);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1u;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1u;
+      }
+    }
+  } else {  // ---- epilogue warps 2..5: TMEM lanes [32 (w % 4), +32)
+    const int eq = warp & 3;
+    const int r = eq * 32 + lane;
+    const i64 gi = i0 + r;
+    const double sqi = gi < n ? sq[gi] : 0.0;
+    float thr = CUDART_INF_F;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (i64 jt = jt0; jt < jt1; ++jt) {
+      const i64 j0 = jt * kN;
+      mbar_wait(&tfull[acc], aphase);
+      fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < kN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN + c0), v);
+        if (gi < n) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const i64 gj = j0 + c0 + q;
+            if (gj >= n || gj == gi) continue;
+            const double dd = (sqi + __ldg(sq + gj)) - 2.0 * static_cast<double>(v[q]);
+            const float df = static_cast<float>(dd);
+            if (!(df < thr)) continue;
+            int pos = kCand - 1;
+            while (pos > 0) {
+              const float pd = lst_d[(pos - 1) * kM + r];
+              if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
+              lst_d[pos * kM + r] = pd;
+              lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
+              --pos;
+            }
+            lst_d[pos * kM + r] = df;
+            lst_j[pos * kM + r] = static_cast<int>(gj);
+            thr = lst_d[(kCand - 1) * kM + r];
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1u;
+    }
+    if (gi < n) {
+      float* od = cand_d + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
+      int* oj = cand_j + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
+      for (int q = 0; q < kCand; ++q) {
+        od[q] = lst_d[q * kM + r];
+        oj[q] = lst_j[q * kM + r];
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 2 * kN);
+}
+
+size_t knn_tc2_smem() {
+  return static_cast<size_t>(tc2::kStages) * tc2::kStageBytes + kCand * tc::kM * (sizeof(float) + sizeof(int)) + 1024;
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) fail(CPCAG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// n x dp fp32 point-major matrix, boxes of 128 points x 32 floats (128 B),
+// 128-byte swizzle; rows past n read as zero.
+CUtensorMap point_map(const float* base, i64 n, i64 dp) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(dp), static_cast<cuuint64_t>(n)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(dp) * sizeof(float)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(CPCAG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+}  // namespace
+
+void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
+                    i64 tps, float* cd, int* cj) {
+  if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
+  const CUtensorMap mh = point_map(H, n, dp), ml = point_map(L, n, dp);
+  const size_t smem = knn_tc2_smem();
+  ensure_smem(knn_tc_filter2_k, smem);
+  knn_tc_filter2_k<<<dim3(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits)), tc2::kThreads, smem,
+                     c->stream>>>(mh, ml, sq, n, dp, static_cast<int>(tps), cd, cj);
+  launched(c);
+}
 
 // hi = tf32(x) (round to nearest), lo = tf32(x - hi); rows padded to dp.
 __global__ void split_tf32_k(const double* __restrict__ Pm, i64 n, i64 d, i64 dp, float* __restrict__ H,
