@@ -352,6 +352,28 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(mbar))
       : "memory");
 }
+// mbarrier wait with a watchdog: a pipeline that never completes (a bad
+// descriptor, a lost transaction) traps after ~10 s instead of hanging.
+__device__ __forceinline__ void mbar_wait_guarded(uint64_t* mbar, uint32_t phase) {
+  uint32_t done = 0;
+  unsigned long long t0 = 0;
+  for (uint32_t spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(done)
+        : "r"(tc::smem_u32(mbar)), "r"(phase)
+        : "memory");
+    if (done) return;
+    if ((spin & 1023u) == 0u) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      else if (t - t0 > 10000000000ull) asm volatile("trap;");
+    }
+  }
+}
 // K-major SWIZZLE_128B operand: rows of 128 B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
@@ -412,7 +434,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       for (i64 jt = jt0; jt < jt1; ++jt) {
         const int j0 = static_cast<int>(jt * kN);
         for (int kc = 0; kc < nkc; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1u);
+          mbar_wait_guarded(&empty[stage], phase ^ 1u);
           unsigned char* st = smem + stage * kStageBytes;
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
           tma_load_2d(st, &mapH, &full[stage], kc * kKc, static_cast<int>(i0));
@@ -432,11 +454,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
       for (i64 jt = jt0; jt < jt1; ++jt) {
-        mbar_wait(&tempty[acc], aphase ^ 1u);
+        mbar_wait_guarded(&tempty[acc], aphase ^ 1u);
         fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * kN);
         for (int kc = 0; kc < nkc; ++kc) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_guarded(&full[stage], phase);
           fence_after();
           const uint32_t ah = smem_u32(smem + stage * kStageBytes);
           const uint32_t al = ah + kTile, bh = ah + 2 * kTile, bl = ah + 3 * kTile;
@@ -469,7 +491,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     uint32_t aphase = 0;
     for (i64 jt = jt0; jt < jt1; ++jt) {
       const i64 j0 = jt * kN;
-      mbar_wait(&tfull[acc], aphase);
+      mbar_wait_guarded(&tfull[acc], aphase);
       fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < kN; c0 += 32) {

@@ -1,4 +1,9 @@
-timeout -s KILL 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b48a.log 2>&1; grep "\[bench\]" gpurun_out/b48a.log
-timeout -s KILL 600 python -m pytest tests/test_gpu_graph.py -m gpu -q -x -p no:cacheprovider -k "knn or tc or gram" > gpurun_out/t48.log 2>&1; tail -3 gpurun_out/t48.log
-timeout -s KILL 600 python bench.py --config cfg2 --steps 2 --warmup 1 > gpurun_out/b48c.log 2>&1; tail -1 gpurun_out/b48c.log | cut -c 500-900
-CPCAG_KNN_FILTER=v1 timeout -s KILL 600 python bench.py --config cfg2 --steps 2 --warmup 1 > gpurun_out/b48d.log 2>&1; tail -1 gpurun_out/b48d.log | cut -c 500-900
+CPCAG_TRACE=1 timeout -s KILL 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b49.log 2>&1; grep "\[bench\]" gpurun_out/b49.log | head -3
+python - <<'PY'
+import re
+lines=open('gpurun_out/b49.log').read().splitlines()
+# print kron trace blocks whose 'solves+schur' or others exceed 30 ms
+for i,l in enumerate(lines):
+    m=re.match(r'\[cpcag trace\] (.+?)\s+([0-9.]+) ms', l)
+    if m and float(m.group(2))>15: print(i, l)
+PY
