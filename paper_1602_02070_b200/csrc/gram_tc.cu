@@ -374,6 +374,28 @@ __device__ __forceinline__ void mbar_wait_guarded(uint64_t* mbar, uint32_t phase
     }
   }
 }
+// TMA 2D load with an L2 cache policy (createpolicy): the query block A is
+// re-read once per candidate tile and must survive in L2 (evict_last); the
+// candidate stream B is consumed by the concurrently running CTAs within a
+// short window (evict_first), so it must not push A out.
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, uint64_t* mbar, int c0, int c1,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;\n" ::"r"(tc::smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(tc::smem_u32(mbar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
 // K-major SWIZZLE_128B operand: rows of 128 B, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   uint64_t d = 0;
@@ -431,16 +453,17 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     if (lane == 0) {  // ---- TMA producer
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
       for (i64 jt = jt0; jt < jt1; ++jt) {
         const int j0 = static_cast<int>(jt * kN);
         for (int kc = 0; kc < nkc; ++kc) {
           mbar_wait_guarded(&empty[stage], phase ^ 1u);
           unsigned char* st = smem + stage * kStageBytes;
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
-          tma_load_2d(st, &mapH, &full[stage], kc * kKc, static_cast<int>(i0));
-          tma_load_2d(st + kTile, &mapL, &full[stage], kc * kKc, static_cast<int>(i0));
-          tma_load_2d(st + 2 * kTile, &mapH, &full[stage], kc * kKc, j0);
-          tma_load_2d(st + 3 * kTile, &mapL, &full[stage], kc * kKc, j0);
+          tma_load_2d_hint(st, &mapH, &full[stage], kc * kKc, static_cast<int>(i0), keep);
+          tma_load_2d_hint(st + kTile, &mapL, &full[stage], kc * kKc, static_cast<int>(i0), keep);
+          tma_load_2d_hint(st + 2 * kTile, &mapH, &full[stage], kc * kKc, j0, stream);
+          tma_load_2d_hint(st + 3 * kTile, &mapL, &full[stage], kc * kKc, j0, stream);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
