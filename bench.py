@@ -462,6 +462,7 @@ def timed_steps(fn, steps, warmup, stream):
         fn()
     torch.cuda.synchronize()
     evs = []
+    torch.cuda.profiler.start()  # ncu --profile-from-start off captures the timed steps only
     for _ in range(steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
@@ -469,6 +470,7 @@ def timed_steps(fn, steps, warmup, stream):
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     return sum(a.elapsed_time(b) for a, b in evs) / len(evs)
 
 
