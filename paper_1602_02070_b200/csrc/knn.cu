@@ -19,6 +19,7 @@
 // (row << 32 | col) -> duplicates dropped (union symmetrisation) ->
 // Gaussian weights (w == 0 dropped) -> CSR W -> degrees -> CSR L.
 #include <algorithm>
+#include <cstdio>
 #include <cub/cub.cuh>
 #include <math_constants.h>
 
@@ -237,10 +238,25 @@ __global__ void knn_merge_k(i64 n, int K, int splits, const double* __restrict__
 }
 
 // sigma2 = sum_i (mean_i / K) / n, summed in point order (graph.cpp:104-107).
-__global__ void sigma2_k(i64 n, int K, const double* __restrict__ mean_d2, double override_, double* out) {
+// sigma^2 = (sum_i mean_d2[i] / K) / n with the reference's left-to-right
+// sum (graph.cpp:104,107).  The divisions are independent (q_i, parallel);
+// only the additions form the sequential chain.
+__global__ void sigma2_div_k(i64 n, int K, const double* __restrict__ mean_d2, double* __restrict__ q) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < n) q[i] = __ddiv_rn(mean_d2[i], static_cast<double>(K));
+}
+__global__ void sigma2_k(i64 n, const double* __restrict__ q, double override_, double* out) {
   if (blockIdx.x || threadIdx.x) return;
   double s = 0.0;
-  for (i64 i = 0; i < n; ++i) s = __dadd_rn(s, __ddiv_rn(mean_d2[i], static_cast<double>(K)));
+  i64 i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = q[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[u]);
+  }
+  for (; i < n; ++i) s = __dadd_rn(s, q[i]);
   *out = override_ > 0.0 ? override_ : __ddiv_rn(s, static_cast<double>(n));
 }
 
@@ -554,6 +570,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   out->d = d;
   out->Pm.alloc(c, std::max<i64>(n * d, 1));
   DevBuf<double> sq(c, n);
+  trace_mark(c, "knn: enter");
   if (n * d) {
     gather_points_k<T><<<blocks_for(n * d), kBlock, 0, c->stream>>>(X, x_rows, n, d, axis_rows ? 1 : 0, out->Pm.p);
     launched(c);
@@ -610,6 +627,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
                                                                  out->mean.p, ovf.p, dup.p);
       launched(c);
     }
+    trace_mark(c, "knn: tc filter+merge+rerank");
     std::vector<int> of(static_cast<size_t>(n));
     CUDA_OK(cudaMemcpyAsync(of.data(), ovf.p, sizeof(int) * n, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
@@ -617,6 +635,9 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
     for (i64 i = 0; i < n; ++i)
       if (of[i]) rows.push_back(static_cast<int>(i));
     out->tc_rows = n - static_cast<i64>(rows.size());
+    if (std::getenv("CPCAG_TRACE"))
+      std::fprintf(stderr, "[knn] %lld points, %lld certified by the tensor-core filter, %zu exact fallback rows\n",
+                   static_cast<long long>(n), static_cast<long long>(out->tc_rows), rows.size());
     if (!rows.empty()) {
       DevBuf<int> qd(c, rows.size());
       CUDA_OK(cudaMemcpyAsync(qd.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice, c->stream));
@@ -624,6 +645,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
                      out->d2.p, out->mean.p);
       sync(c);
     }
+    trace_mark(c, "knn: exact fallback rows");
   } else {
     knn_exact_rows(c, out->Pm.p, sq.p, n, d, K, nullptr, n, dup.p, out->nbr.p, out->d2.p, out->mean.p);
   }
@@ -633,6 +655,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   launched(c);
   const unsigned long long nd = read_back(c, ndup.p);
   const i64 distinct = n - static_cast<i64>(nd);
+  trace_mark(c, "knn: lists done");
   if (distinct < K)
     invalid("knn graph: fewer distinct points (" + std::to_string(distinct) + ") than K (" + std::to_string(K) + ")");
 }
@@ -643,8 +666,10 @@ void knn_graph_device(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows
   KnnLists kl;
   knn_lists<T>(c, X, x_rows, x_cols, axis_rows, K, &kl);
   const i64 n = kl.n;
-  DevBuf<double> s2(c, 1);
-  sigma2_k<<<1, 1, 0, c->stream>>>(n, static_cast<int>(K), kl.mean.p, sigma2_override, s2.p);
+  DevBuf<double> s2(c, 1), q(c, std::max<i64>(n, 1));
+  sigma2_div_k<<<blocks_for(std::max<i64>(n, 1)), kBlock, 0, c->stream>>>(n, static_cast<int>(K), kl.mean.p, q.p);
+  launched(c);
+  sigma2_k<<<1, 1, 0, c->stream>>>(n, q.p, sigma2_override, s2.p);
   launched(c);
 
   const i64 m = 2 * n * K;
@@ -691,6 +716,7 @@ void knn_graph_device(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows
   Csr* L = build_laplacian(c, W, degrees_dev, kind);
   L->sym = 1;
   *sigma2 = read_back(c, s2.p);
+  trace_mark(c, "knn: union, W, L");
   *Wout = ownW.release();
   *Lout = L;
 }

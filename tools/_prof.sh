@@ -1,3 +1,2 @@
-timeout -s KILL 300 python -m pytest tests/test_gpu_graph.py -m gpu -q -x -p no:cacheprovider -k "knn or tc or gram" > gpurun_out/t54.log 2>&1; tail -2 gpurun_out/t54.log
-timeout -s KILL 600 python bench.py --config cfg2 --steps 2 --warmup 1 > gpurun_out/b54.log 2>&1; tail -1 gpurun_out/b54.log | cut -c 1-120; tail -1 gpurun_out/b54.log | cut -c 500-900
-timeout -s KILL 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active -k regex:knn_tc_filter2 -c 1 python bench.py --config cfg2 --steps 1 --warmup 1 2>&1 | grep -E "dram__|gpu__time|tensor" | head
+CPCAG_TRACE=1 timeout -s KILL 300 python bench.py --config cfg2 --steps 1 --warmup 1 > gpurun_out/b56.log 2>&1; grep -E "trace|\[knn\]" gpurun_out/b56.log | tail -14; tail -1 gpurun_out/b56.log | cut -c1-150
+timeout -s KILL 300 python -m pytest tests/test_gpu_graph.py -m gpu -q -x -p no:cacheprovider > gpurun_out/t56.log 2>&1; tail -2 gpurun_out/t56.log
