@@ -21,6 +21,8 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -333,9 +335,7 @@ size_t knn_tc_smem() { return 4 * static_cast<size_t>(tc::kTileBytes) + kCand * 
 //             distances + top-kCand insertion for tile t while the MMAs of
 //             tile t+1 run; arrive tmem_empty[acc].
 namespace tc2 {
-constexpr int kStages = 3;
-constexpr int kTile = 128 * 32 * 4;        // 16 KiB: 128 rows x 128 B
-constexpr int kStageBytes = 4 * kTile;     // Ah, Al, Bh, Bl
+constexpr int kTile = 128 * 32 * 4;        // 16 KiB: 128 rows x 128 B (an A plane chunk)
 constexpr int kThreads = 192;
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
@@ -408,12 +408,29 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 }
 }  // namespace tc2
 
+// NT = candidate rows per tile (UMMA N): 128 (3-stage ring of 64 KiB) or
+// 256 (2-stage ring of 96 KiB; each A chunk then serves twice the
+// candidates, 65 instead of 48 flops per staged byte).
+template <int NT>
 __global__ void __launch_bounds__(tc2::kThreads, 1)
     knn_tc_filter2_k(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapL,
+                     const __grid_constant__ CUtensorMap mapHb, const __grid_constant__ CUtensorMap mapLb,
                      const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split, float* __restrict__ cand_d,
                      int* __restrict__ cand_j) {
   using namespace tc;
-  using namespace tc2;
+  using tc2::kTile;
+  using tc2::kThreads;
+  using tc2::mbar_wait_guarded;
+  using tc2::mbar_arrive_expect_tx;
+  using tc2::mbar_arrive;
+  using tc2::tma_load_2d_hint;
+  using tc2::policy_evict_last;
+  using tc2::policy_evict_first;
+  using tc2::desc_sw128;
+  constexpr int kN = NT;
+  constexpr int kBTile = NT * 128;                   // NT rows x 128 B
+  constexpr int kStageBytes = 2 * kTile + 2 * kBTile;
+  constexpr int kStages = NT == 128 ? 3 : 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* lst_d = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [kCand][128]
@@ -462,8 +479,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
           tma_load_2d_hint(st, &mapH, &full[stage], kc * kKc, static_cast<int>(i0), keep);
           tma_load_2d_hint(st + kTile, &mapL, &full[stage], kc * kKc, static_cast<int>(i0), keep);
-          tma_load_2d_hint(st + 2 * kTile, &mapH, &full[stage], kc * kKc, j0, stream);
-          tma_load_2d_hint(st + 3 * kTile, &mapL, &full[stage], kc * kKc, j0, stream);
+          tma_load_2d_hint(st + 2 * kTile, &mapHb, &full[stage], kc * kKc, j0, stream);
+          tma_load_2d_hint(st + 2 * kTile + kBTile, &mapLb, &full[stage], kc * kKc, j0, stream);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1u;
@@ -484,7 +501,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
           mbar_wait_guarded(&full[stage], phase);
           fence_after();
           const uint32_t ah = smem_u32(smem + stage * kStageBytes);
-          const uint32_t al = ah + kTile, bh = ah + 2 * kTile, bl = ah + 3 * kTile;
+          const uint32_t al = ah + kTile, bh = ah + 2 * kTile, bl = ah + 2 * kTile + kBTile;
 #pragma unroll
           for (int kk = 0; kk < kKc / 8; ++kk) {
             const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
@@ -562,8 +579,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 2 * kN);
 }
 
-size_t knn_tc2_smem() {
-  return static_cast<size_t>(tc2::kStages) * tc2::kStageBytes + kCand * tc::kM * (sizeof(float) + sizeof(int)) + 1024;
+size_t knn_tc2_smem(int nt) {
+  const size_t stage = 2 * static_cast<size_t>(tc2::kTile) + 2 * static_cast<size_t>(nt) * 128;
+  const size_t stages = nt == 128 ? 3 : 2;
+  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + 1024;
 }
 
 namespace {
@@ -581,11 +600,11 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // n x dp fp32 point-major matrix, boxes of 128 points x 32 floats (128 B),
 // 128-byte swizzle; rows past n read as zero.
-CUtensorMap point_map(const float* base, i64 n, i64 dp) {
+CUtensorMap point_map(const float* base, i64 n, i64 dp, int box_rows = 128) {
   CUtensorMap m;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(dp), static_cast<cuuint64_t>(n)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(dp) * sizeof(float)};
-  cuuint32_t box[2] = {32, 128};
+  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t es[2] = {1, 1};
   const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
                                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -596,13 +615,25 @@ CUtensorMap point_map(const float* base, i64 n, i64 dp) {
 }  // namespace
 
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
-                    i64 tps, float* cd, int* cj) {
+                    i64 /*tps128*/, float* cd, int* cj) {
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
+  int nt = 256;
+  if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 128 ? 128 : 256;
+  const i64 nt_tiles = (n + nt - 1) / nt;
+  const i64 tps = (nt_tiles + splits - 1) / splits;  // splits keep the caller's output layout
   const CUtensorMap mh = point_map(H, n, dp), ml = point_map(L, n, dp);
-  const size_t smem = knn_tc2_smem();
-  ensure_smem(knn_tc_filter2_k, smem);
-  knn_tc_filter2_k<<<dim3(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits)), tc2::kThreads, smem,
-                     c->stream>>>(mh, ml, sq, n, dp, static_cast<int>(tps), cd, cj);
+  const CUtensorMap mhb = point_map(H, n, dp, nt), mlb = point_map(L, n, dp, nt);
+  const size_t smem = knn_tc2_smem(nt);
+  const dim3 grid(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits));
+  if (nt == 256) {
+    ensure_smem(knn_tc_filter2_k<256>, smem);
+    knn_tc_filter2_k<256><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
+                                                                     cd, cj);
+  } else {
+    ensure_smem(knn_tc_filter2_k<128>, smem);
+    knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
+                                                                     cd, cj);
+  }
   launched(c);
 }
 
