@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     knn_tc_filter2_k(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapL,
                      const __grid_constant__ CUtensorMap mapHb, const __grid_constant__ CUtensorMap mapLb,
                      const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split, float* __restrict__ cand_d,
-                     int* __restrict__ cand_j) {
+                     int* __restrict__ cand_j, int stagger) {
   using namespace tc;
   using tc2::kTile;
   using tc2::kThreads;
@@ -473,7 +473,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
       for (i64 jt = jt0; jt < jt1; ++jt) {
         const int j0 = static_cast<int>(jt * kN);
-        for (int kc = 0; kc < nkc; ++kc) {
+        for (int kq = 0; kq < nkc; ++kq) {
+          const int kc = stagger ? (kq + static_cast<int>(blockIdx.x)) % nkc : kq;
           mbar_wait_guarded(&empty[stage], phase ^ 1u);
           unsigned char* st = smem + stage * kStageBytes;
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
@@ -497,7 +498,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
         mbar_wait_guarded(&tempty[acc], aphase ^ 1u);
         fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(acc * kN);
-        for (int kc = 0; kc < nkc; ++kc) {
+        for (int kc = 0; kc < nkc; ++kc) {  // order of the chunks is the producer's; accumulate from the 2nd
           mbar_wait_guarded(&full[stage], phase);
           fence_after();
           const uint32_t ah = smem_u32(smem + stage * kStageBytes);
@@ -619,6 +620,8 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
   int nt = 256;
   if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 128 ? 128 : 256;
+  int stagger = 1;
+  if (const char* e = std::getenv("CPCAG_KNN_STAGGER")) stagger = std::atoi(e) != 0;
   const i64 nt_tiles = (n + nt - 1) / nt;
   const i64 tps = (nt_tiles + splits - 1) / splits;  // splits keep the caller's output layout
   const CUtensorMap mh = point_map(H, n, dp), ml = point_map(L, n, dp);
@@ -628,11 +631,11 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
   if (nt == 256) {
     ensure_smem(knn_tc_filter2_k<256>, smem);
     knn_tc_filter2_k<256><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj);
+                                                                     cd, cj, stagger);
   } else {
     ensure_smem(knn_tc_filter2_k<128>, smem);
     knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj);
+                                                                     cd, cj, stagger);
   }
   launched(c);
 }
