@@ -416,7 +416,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     knn_tc_filter2_k(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapL,
                      const __grid_constant__ CUtensorMap mapHb, const __grid_constant__ CUtensorMap mapLb,
                      const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split, float* __restrict__ cand_d,
-                     int* __restrict__ cand_j, int stagger) {
+                     int* __restrict__ cand_j, const unsigned long long* __restrict__ max_norm_bits, int stagger,
+                     int dbg) {
   using namespace tc;
   using tc2::kTile;
   using tc2::kThreads;
@@ -432,9 +433,13 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   constexpr int kStageBytes = 2 * kTile + 2 * kBTile;
   constexpr int kStages = NT == 128 ? 3 : 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment for SWIZZLE_128B by pointer arithmetic on the shared
+  // array (an integer round trip would lose the address space: generic LD/ST).
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* lst_d = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [kCand][128]
   int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);                // [kCand][128]
+  double* sqd = reinterpret_cast<double*>(lst_j + kCand * kM);            // [NT] candidate sq (fp64)
+  float* sqf = reinterpret_cast<float*>(sqd + NT);                        // [NT] candidate sq (fp32)
   __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -504,7 +509,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
           const uint32_t ah = smem_u32(smem + stage * kStageBytes);
           const uint32_t al = ah + kTile, bh = ah + 2 * kTile, bl = ah + 2 * kTile + kBTile;
 #pragma unroll
-          for (int kk = 0; kk < kKc / 8; ++kk) {
+          for (int kk = 0; kk < (dbg == 2 ? 0 : kKc / 8); ++kk) {
             const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
             const uint32_t accum = (kc > 0 || kk > 0) ? 1u : 0u;
             mma_tf32(d, desc_sw128(ah + off), desc_sw128(bh + off), idesc, accum);
@@ -525,38 +530,68 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   } else {  // ---- epilogue warps 2..5: TMEM lanes [32 (w % 4), +32)
     const int eq = warp & 3;
     const int r = eq * 32 + lane;
+    const int et = threadIdx.x - 64;  // 0..127 across the epilogue warps
     const i64 gi = i0 + r;
     const double sqi = gi < n ? sq[gi] : 0.0;
+    const float sqi_f = static_cast<float>(sqi);
+    // Quick reject in fp32.  The exact test below is df < thr with
+    // df = fp32((sq_i + sq_j) - 2 g) evaluated in fp64.  The fp32 estimate
+    // e = fma(-2, g, fp32(sq_i) + fp32(sq_j)) differs from it by at most
+    // 4 * 2^-24 (sq_i + sq_j + 2|g|) plus df's own rounding, and
+    // |g| <= (sq_i + sq_j) / 2 (1 + the filter's relative error), so
+    // |e - df| < 2^-20 (sq_i + max sq): a candidate skipped here has df >=
+    // thr and the exact test would skip it too.
+    const double mxn = __longlong_as_double(static_cast<long long>(*max_norm_bits));
+    const float margin = static_cast<float>(0x1.0p-20 * (sqi + mxn * mxn)) * 1.0001f;
     float thr = CUDART_INF_F;
     int acc = 0;
     uint32_t aphase = 0;
     for (i64 jt = jt0; jt < jt1; ++jt) {
       const i64 j0 = jt * kN;
+      // stage the candidate tile's squared norms (padding columns: +inf)
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      for (int q = et; q < kN; q += 128) {
+        const i64 gj = j0 + q;
+        const double vq = gj < n ? sq[gj] : CUDART_INF;
+        sqd[q] = vq;
+        sqf[q] = static_cast<float>(vq);
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
       mbar_wait_guarded(&tfull[acc], aphase);
       fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < kN; c0 += 32) {
         float v[32];
         tmem_ld32(tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN + c0), v);
-        if (gi < n) {
+        if (gi < n && dbg != 1) {
+          float e[32];
+          float mn = CUDART_INF_F;
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const i64 gj = j0 + c0 + q;
-            if (gj >= n || gj == gi) continue;
-            const double dd = (sqi + __ldg(sq + gj)) - 2.0 * static_cast<double>(v[q]);
-            const float df = static_cast<float>(dd);
-            if (!(df < thr)) continue;
-            int pos = kCand - 1;
-            while (pos > 0) {
-              const float pd = lst_d[(pos - 1) * kM + r];
-              if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
-              lst_d[pos * kM + r] = pd;
-              lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
-              --pos;
+            e[q] = fmaf(-2.0f, v[q], sqi_f + sqf[c0 + q]);
+            mn = fminf(mn, e[q]);
+          }
+          if (mn <= thr + margin) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              if (!(e[q] <= thr + margin)) continue;
+              const i64 gj = j0 + c0 + q;
+              if (gj >= n || gj == gi) continue;
+              const double dd = (sqi + sqd[c0 + q]) - 2.0 * static_cast<double>(v[q]);
+              const float df = static_cast<float>(dd);
+              if (!(df < thr)) continue;
+              int pos = kCand - 1;
+              while (pos > 0) {
+                const float pd = lst_d[(pos - 1) * kM + r];
+                if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
+                lst_d[pos * kM + r] = pd;
+                lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
+                --pos;
+              }
+              lst_d[pos * kM + r] = df;
+              lst_j[pos * kM + r] = static_cast<int>(gj);
+              thr = lst_d[(kCand - 1) * kM + r];
             }
-            lst_d[pos * kM + r] = df;
-            lst_j[pos * kM + r] = static_cast<int>(gj);
-            thr = lst_d[(kCand - 1) * kM + r];
           }
         }
       }
@@ -583,7 +618,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
 size_t knn_tc2_smem(int nt) {
   const size_t stage = 2 * static_cast<size_t>(tc2::kTile) + 2 * static_cast<size_t>(nt) * 128;
   const size_t stages = nt == 128 ? 3 : 2;
-  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + 1024;
+  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + static_cast<size_t>(nt) * 12 + 1024;
 }
 
 namespace {
@@ -616,11 +651,12 @@ CUtensorMap point_map(const float* base, i64 n, i64 dp, int box_rows = 128) {
 }  // namespace
 
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
-                    i64 /*tps128*/, float* cd, int* cj) {
+                    i64 /*tps128*/, float* cd, int* cj, const unsigned long long* max_norm_bits) {
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
   int nt = 256;
   if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 128 ? 128 : 256;
-  int stagger = 1;
+  int stagger = 1, dbg = 0;
+  if (const char* e = std::getenv("CPCAG_KNN_DBG")) dbg = std::atoi(e);
   if (const char* e = std::getenv("CPCAG_KNN_STAGGER")) stagger = std::atoi(e) != 0;
   const i64 nt_tiles = (n + nt - 1) / nt;
   const i64 tps = (nt_tiles + splits - 1) / splits;  // splits keep the caller's output layout
@@ -631,11 +667,11 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
   if (nt == 256) {
     ensure_smem(knn_tc_filter2_k<256>, smem);
     knn_tc_filter2_k<256><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj, stagger);
+                                                                     cd, cj, max_norm_bits, stagger, dbg);
   } else {
     ensure_smem(knn_tc_filter2_k<128>, smem);
     knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj, stagger);
+                                                                     cd, cj, max_norm_bits, stagger, dbg);
   }
   launched(c);
 }

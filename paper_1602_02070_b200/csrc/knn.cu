@@ -416,7 +416,7 @@ constexpr int kCandTc = 32;  // == kCand in gram_tc.cu
 void split_points(Ctx* c, const double* Pm, i64 n, i64 d, i64 dp, float* H, float* L);  // gram_tc.cu
 size_t knn_tc_smem();
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
-                    i64 tps, float* cd, int* cj);
+                    i64 tps, float* cd, int* cj, const unsigned long long* max_norm_bits);
 __global__ void knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
                                 const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split,
                                 float* __restrict__ cand_d, int* __restrict__ cand_j);
@@ -598,6 +598,10 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
     DevBuf<float> cd(c, splits * n * kCandTc), md(c, n * kCandTc);
     DevBuf<int> cj(c, splits * n * kCandTc), mj(c, n * kCandTc), ovf(c, n);
     ovf.zero(c);
+    DevBuf<unsigned long long> mxn(c, 1);
+    mxn.zero(c);
+    max_norm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(sq.p, n, mxn.p);
+    launched(c);
     const char* fv = std::getenv("CPCAG_KNN_FILTER");
     if (fv && std::string(fv) == "v1") {
       const size_t smem = knn_tc_smem();
@@ -608,13 +612,9 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
       launched(c);
     } else {
       KScope ks_(c, "knn_tc_filter");
-      knn_tc_filter2(c, H.p, L.p, sq.p, n, dp, q_tiles, splits, tps, cd.p, cj.p);
+      knn_tc_filter2(c, H.p, L.p, sq.p, n, dp, q_tiles, splits, tps, cd.p, cj.p, mxn.p);
     }
     tc_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(splits), cd.p, cj.p, md.p, mj.p);
-    launched(c);
-    DevBuf<unsigned long long> mxn(c, 1);
-    mxn.zero(c);
-    max_norm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(sq.p, n, mxn.p);
     launched(c);
     // Rigorous bound on |G~ - G| / (|x_i| |x_j|): split error 3 * 2^-22 plus
     // fp32 accumulation of 3 d exact tf32 products, 2^-23 per addition
