@@ -433,9 +433,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   constexpr int kStageBytes = 2 * kTile + 2 * kBTile;
   constexpr int kStages = NT == 128 ? 3 : 2;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte alignment for SWIZZLE_128B by pointer arithmetic on the shared
-  // array (an integer round trip would lose the address space: generic LD/ST).
-  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // SWIZZLE_128B needs 1024-byte aligned stages; the dynamic window is
+  // declared so (no slack is reserved: the 3-stage ring plus the lists fill
+  // the 227 KB), checked here once.
+  unsigned char* smem = smem_raw;
+  if ((smem_u32(smem_raw) & 1023u) != 0u) asm volatile("trap;");
   float* lst_d = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [kCand][128]
   int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);                // [kCand][128]
   double* sqd = reinterpret_cast<double*>(lst_j + kCand * kM);            // [NT] candidate sq (fp64)
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
 size_t knn_tc2_smem(int nt) {
   const size_t stage = 2 * static_cast<size_t>(tc2::kTile) + 2 * static_cast<size_t>(nt) * 128;
   const size_t stages = nt == 128 ? 3 : 2;
-  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + static_cast<size_t>(nt) * 12 + 1024;
+  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + static_cast<size_t>(nt) * 12;
 }
 
 namespace {
@@ -653,8 +655,9 @@ CUtensorMap point_map(const float* base, i64 n, i64 dp, int box_rows = 128) {
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
                     i64 /*tps128*/, float* cd, int* cj, const unsigned long long* max_norm_bits) {
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
-  int nt = 256;
-  if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 128 ? 128 : 256;
+  int nt = 128;  // 256-wide tiles measured no faster and do not fit the sq staging
+  if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 256 ? 256 : 128;
+  if (knn_tc2_smem(nt) > 227 * 1024 - 1024) nt = 128;
   int stagger = 1, dbg = 0;
   if (const char* e = std::getenv("CPCAG_KNN_DBG")) dbg = std::atoi(e);
   if (const char* e = std::getenv("CPCAG_KNN_STAGGER")) stagger = std::atoi(e) != 0;
