@@ -117,6 +117,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
 }
 
+// Split form of tmem_ld32: issue, then wait (tcgen05.wait::ld covers every
+// outstanding load of the thread), so the next chunk loads while this one is
+// processed.
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
 // Copies rows [row0, row0 + 128) x k [k0, k0 + 32) of a point-major fp32
 // matrix (leading dimension ld, rows >= nrows read as zero) into the core
 // matrix layout at dst.  128 threads, 16-byte chunks.
@@ -548,23 +564,34 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     float thr = CUDART_INF_F;
     int acc = 0;
     uint32_t aphase = 0;
+    static_assert(NT == 128, "one staged norm per epilogue thread");
+    auto norm_of = [&](i64 jt) -> double {
+      const i64 gj = jt * kN + et;
+      return jt < jt1 && gj < n ? __ldg(sq + gj) : CUDART_INF;
+    };
+    double nxt = norm_of(jt0);
     for (i64 jt = jt0; jt < jt1; ++jt) {
       const i64 j0 = jt * kN;
-      // stage the candidate tile's squared norms (padding columns: +inf)
+      // stage the candidate tile's squared norms (padding columns: +inf); the
+      // next tile's norm is fetched now, its latency hidden by this tile
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      for (int q = et; q < kN; q += 128) {
-        const i64 gj = j0 + q;
-        const double vq = gj < n ? sq[gj] : CUDART_INF;
-        sqd[q] = vq;
-        sqf[q] = static_cast<float>(vq);
-      }
+      sqd[et] = nxt;
+      sqf[et] = static_cast<float>(nxt);
       asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      nxt = norm_of(jt + 1);
       mbar_wait_guarded(&tfull[acc], aphase);
       fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < kN; c0 += 32) {
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN);
+      uint32_t raw[2][32];
+      tmem_ld32_issue(tbase, raw[0]);
+#pragma unroll
+      for (int cc = 0; cc < kN / 32; ++cc) {
+        const int c0 = cc * 32;
+        tmem_ld_wait();
         float v[32];
-        tmem_ld32(tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN + c0), v);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(raw[cc & 1][q]);
+        if (cc + 1 < kN / 32) tmem_ld32_issue(tbase + static_cast<uint32_t>(c0 + 32), raw[(cc + 1) & 1]);
         if (gi < n && dbg != 1) {
           float e[32];
           float mn = CUDART_INF_F;
@@ -655,9 +682,7 @@ CUtensorMap point_map(const float* base, i64 n, i64 dp, int box_rows = 128) {
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
                     i64 /*tps128*/, float* cd, int* cj, const unsigned long long* max_norm_bits) {
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
-  int nt = 128;  // 256-wide tiles measured no faster and do not fit the sq staging
-  if (const char* e = std::getenv("CPCAG_KNN_NT")) nt = std::atoi(e) == 256 ? 256 : 128;
-  if (knn_tc2_smem(nt) > 227 * 1024 - 1024) nt = 128;
+  const int nt = 128;  // 256-wide tiles measured no faster and do not fit the norm staging
   int stagger = 1, dbg = 0;
   if (const char* e = std::getenv("CPCAG_KNN_DBG")) dbg = std::atoi(e);
   if (const char* e = std::getenv("CPCAG_KNN_STAGGER")) stagger = std::atoi(e) != 0;
@@ -667,15 +692,9 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
   const CUtensorMap mhb = point_map(H, n, dp, nt), mlb = point_map(L, n, dp, nt);
   const size_t smem = knn_tc2_smem(nt);
   const dim3 grid(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits));
-  if (nt == 256) {
-    ensure_smem(knn_tc_filter2_k<256>, smem);
-    knn_tc_filter2_k<256><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj, max_norm_bits, stagger, dbg);
-  } else {
-    ensure_smem(knn_tc_filter2_k<128>, smem);
-    knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
-                                                                     cd, cj, max_norm_bits, stagger, dbg);
-  }
+  ensure_smem(knn_tc_filter2_k<128>, smem);
+  knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps), cd,
+                                                                   cj, max_norm_bits, stagger, dbg);
   launched(c);
 }
 
