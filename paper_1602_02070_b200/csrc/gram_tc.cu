@@ -582,16 +582,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       mbar_wait_guarded(&tfull[acc], aphase);
       fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN);
-      uint32_t raw[2][32];
-      tmem_ld32_issue(tbase, raw[0]);
-#pragma unroll
-      for (int cc = 0; cc < kN / 32; ++cc) {
-        const int c0 = cc * 32;
-        tmem_ld_wait();
+#pragma unroll 1
+      for (int c0 = 0; c0 < kN; c0 += 32) {
         float v[32];
-#pragma unroll
-        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(raw[cc & 1][q]);
-        if (cc + 1 < kN / 32) tmem_ld32_issue(tbase + static_cast<uint32_t>(c0 + 32), raw[(cc + 1) & 1]);
+        tmem_ld32(tbase + static_cast<uint32_t>(c0), v);
         if (gi < n && dbg != 1) {
           float e[32];
           float mn = CUDART_INF_F;
