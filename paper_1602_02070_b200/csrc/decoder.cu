@@ -1455,7 +1455,9 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
   // fast2 geometry: 512-row blocks, ~16 CTAs per SM.
   const unsigned gx2 = static_cast<unsigned>((p + 511) / 512);
-  const i64 y2cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx2);
+  i64 f2_per_sm = 16;  // CTAs per SM the column chunking aims at (staging amortisation vs waves)
+  if (const char* e = std::getenv("CPCAG_FAST2_CTAS")) f2_per_sm = std::max<i64>(1, std::atoll(e));
+  const i64 y2cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * f2_per_sm) / gx2);
   const i64 cpc2 = std::max<i64>({i64{1}, std::min<i64>((n + std::min<i64>(n, y2cap) - 1) / std::max<i64>(1, std::min<i64>(n, y2cap)), 128),
                                   (n + 65534) / 65535});
   const dim3 gs2(gx2, static_cast<unsigned>(std::min<i64>((n + cpc2 - 1) / cpc2, 65535)));

@@ -1,2 +1,1 @@
-timeout -s KILL 300 python -m pytest tests/test_gpu_graph.py -m gpu -q -x -p no:cacheprovider -k "knn or tc or gram" > gpurun_out/t62.log 2>&1; tail -2 gpurun_out/t62.log
-timeout -s KILL 300 python bench.py --config cfg2 --steps 2 --warmup 1 > gpurun_out/b62.log 2>&1; tail -1 gpurun_out/b62.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['kernel_ms'], d['roofline']['frac'])"
+for k in 16 8 6 4; do CPCAG_FAST2_CTAS=$k timeout -s KILL 300 python tools/bench_stages.py 2>&1 | grep "decode" | cut -c1-140 | sed "s/^/ctas=$k /"; done
