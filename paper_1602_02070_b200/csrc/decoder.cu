@@ -1455,7 +1455,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "fast") ensure_smem(cg_apply_fast_k<T>, fast_smem);
   // fast2 geometry: 512-row blocks, ~16 CTAs per SM.
   const unsigned gx2 = static_cast<unsigned>((p + 511) / 512);
-  i64 f2_per_sm = 16;  // CTAs per SM the column chunking aims at (staging amortisation vs waves)
+  i64 f2_per_sm = 8;  // CTAs per SM the column chunking aims at (measured: 8 best of 16/8/6/4)
   if (const char* e = std::getenv("CPCAG_FAST2_CTAS")) f2_per_sm = std::max<i64>(1, std::atoll(e));
   const i64 y2cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * f2_per_sm) / gx2);
   const i64 cpc2 = std::max<i64>({i64{1}, std::min<i64>((n + std::min<i64>(n, y2cap) - 1) / std::max<i64>(1, std::min<i64>(n, y2cap)), 128),
