@@ -2,15 +2,17 @@
 # and one ncu --set full capture per top kernel (each after its command ran
 # clean without ncu).
 O=gpurun_out/r01
-mkdir -p $O
-timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --json-out $O/bench_cfg1.json > $O/bench_cfg1.log 2>&1; echo "cfg1 rc=$?"; tail -1 $O/bench_cfg1.log | cut -c1-300
-timeout -s KILL 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.log 2>&1; echo "ref rc=$?"; tail -1 $O/bench_ref.log | cut -c1-300
+rm -rf $O; mkdir -p $O
+timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --json-out $O/bench_cfg1.json > $O/bench_cfg1.log 2>&1; echo "cfg1 rc=$?"; grep "\[bench\]" $O/bench_cfg1.log | head -2
+timeout -s KILL 600 python bench.py --impl reference --steps 2 --warmup 1 --json-out $O/bench_ref.json > $O/bench_ref.log 2>&1; echo "ref rc=$?"
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg1.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "launch list rc=$?"
-for k in cg_apply_fast2 pcg_persistent fista_splitk_partial power_iter_coop cg_update cg_residual; do
+for k in cg_apply_fast2 pcg_persistent fista_splitk_partial power_iter_coop cg_update cg_residual fista_lin_objective; do
   timeout -s KILL 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:$k -c 1 -o $O/full_cfg1_$k -f python tools/profile_step.py > $O/ncu_full_cfg1_$k.log 2>&1; echo "ncu $k rc=$?"
 done
-timeout -s KILL 600 python bench.py --config cfg3 --steps 2 --warmup 1 > $O/bench_cfg3.log 2>&1; echo "cfg3 rc=$?"
+timeout -s KILL 600 python bench.py --config cfg3 --steps 2 --warmup 1 --json-out $O/bench_cfg3.json > $O/bench_cfg3.log 2>&1; echo "cfg3 rc=$?"
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg3.csv python bench.py --config cfg3 --steps 1 --warmup 1 > $O/ncu_launch3.log 2>&1; echo "launch list cfg3 rc=$?"
 SWEEP_ITERS=3 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"cg_apply_(band|col)_k" -s 2 -c 2 -o $O/full_cfg3_band -f python tools/band_sweep.py 1,1024,32,1 > $O/ncu_full_cfg3.log 2>&1; echo "ncu cfg3 rc=$?"
-timeout -s KILL 600 python bench.py --config cfg2 --steps 2 --warmup 1 > $O/bench_cfg2.log 2>&1; echo "cfg2 rc=$?"
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:knn_tc_filter -c 1 -o $O/full_cfg2_tc -f python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_full_cfg2.log 2>&1; echo "ncu cfg2 rc=$?"
-ls -la $O | head -40
+timeout -s KILL 600 python bench.py --config cfg2 --steps 2 --warmup 1 --json-out $O/bench_cfg2.json > $O/bench_cfg2.log 2>&1; echo "cfg2 rc=$?"
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_launch2.log 2>&1; echo "launch list cfg2 rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:knn_tc_filter2 -c 1 -o $O/full_cfg2_tc -f python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_full_cfg2.log 2>&1; echo "ncu cfg2 rc=$?"
+ls $O | wc -l
