@@ -212,6 +212,19 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
                                 const cpcag_decoder_config* cfg, void* X, int* converged,
                                 int64_t* iterations);
 
+/* sym_eig (eigs.hpp:22, eigs.cpp:34-51): the k smallest eigenpairs of the
+ * symmetric part 0.5 (A + A^T) of a CSR matrix, by a dense eigensolver on the
+ * device (like the reference's; n <= 46340).  eigenvalues (k, ascending);
+ * eigenvectors (n x k col-major, may be NULL) with each column's first entry
+ * above 1e-12 of its peak made positive. */
+int cpcag_cuda_sym_eig(cpcag_ctx ctx, cpcag_csr A, int64_t k, double* eigenvalues, double* eigenvectors);
+
+/* SpectralGap (graph.hpp:53-58). */
+typedef struct cpcag_spectral_gap {
+  int64_t k;
+  double lambda_k, lambda_k1, ratio;
+} cpcag_spectral_gap;
+
 /* DecoderConfig fields the approximate decoder reads (decoders.hpp:13-22). */
 typedef struct cpcag_approx_config {
   double delta_for_scaling; /* default 0; sigma scale sqrt(np / (rho_r rho_c (1 - delta))) */
@@ -285,7 +298,8 @@ typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36
   double kron_pcg_tol;       /* default 1e-11 */
   cpcag_frpcag_config frpcag;
   cpcag_decoder_config decoder;
-  double lambda_k1_r, lambda_k1_c; /* SpectralGap::lambda_k1 supplied by the caller */
+  double lambda_k1_r, lambda_k1_c; /* SpectralGap::lambda_k1; <= 0: computed as the reference does
+                                      (sym_eig of the full Laplacian, k = max(1, detected rank)) */
   uint64_t seed;
   int decoder_variant;       /* DecoderVariant (decoders.hpp:11): CPCAG_DECODER_ALTERNATE or _APPROX */
   cpcag_approx_config approx; /* the approximate decoder's DecoderConfig fields */
@@ -310,6 +324,7 @@ typedef struct cpcag_pipeline_report { /* PipelineReport subset, pipeline.hpp:73
   int64_t detected_rank;  /* detect_rank(thin_svd(Xt).sigma, rank_threshold), pipeline.cpp:319-320 */
   int64_t factors_k;      /* approximate decoder: rank of the factors (0 otherwise) */
   int has_factors;
+  double lambda_k1_r, lambda_k1_c; /* gaps the alternate decoder used (supplied or computed) */
   /* Stage timings in ms (device events), in the reference's stage order:
    * graphs, plan, subsample, kron, solve, decode (pipeline.cpp:273-350). */
   double stage_ms[6];

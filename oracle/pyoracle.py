@@ -553,3 +553,37 @@ def approx_decode(Xt, plan: SamplingPlan, Lr: Csr, Lc: Csr, delta_for_scaling=0.
     sigma = math.sqrt(norm_const / (1.0 - delta_for_scaling)) * s[:k]
     X = np.asfortranarray((U * sigma) @ V.T)
     return ApproxDecodeResult(X, U, sigma, V, k)
+
+
+def sym_eig(L: Csr, k: int):
+    """eigs.cpp:34-51: dense symmetrised eigendecomposition (numpy LAPACK
+    stands in for Eigen's SelfAdjointEigenSolver), first k pairs, column
+    signs fixed so the first entry above 1e-12 of the column peak is
+    positive."""
+    rp, ci, v = L.arrays()
+    n = L.rows
+    D = np.zeros((n, n))
+    for r in range(n):
+        D[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
+    D = 0.5 * (D + D.T)
+    w, E = np.linalg.eigh(D)
+    E = E[:, :k].copy()
+    for j in range(k):
+        peak = np.abs(E[:, j]).max()
+        if peak == 0.0:
+            continue
+        idx = np.nonzero(np.abs(E[:, j]) > 1e-12 * peak)[0][0]
+        if E[idx, j] < 0:
+            E[:, j] = -E[:, j]
+    return w[:k].copy(), E
+
+
+def spectral_gap(eigenvalues, k):
+    """graph.cpp:237-249."""
+    if k < 1 or len(eigenvalues) < k + 1:
+        raise ValueError("spectral gap: need at least k+1 eigenvalues")
+    lk = max(0.0, float(eigenvalues[k - 1]))
+    lk1 = max(0.0, float(eigenvalues[k]))
+    if lk1 <= 1e-14:
+        raise RuntimeError("gap undefined: graph has > k components")
+    return lk, lk1, lk / lk1

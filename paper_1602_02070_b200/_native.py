@@ -63,7 +63,8 @@ class PipelineFactorsC(C.Structure):
 class PipelineReportC(C.Structure):
     _fields_ = [("p", i64), ("n", i64), ("rho_r", i64), ("rho_c", i64), ("trace", SolveTraceC),
                 ("decoder_converged", C.c_int), ("decoder_iterations", i64), ("detected_rank", i64),
-                ("factors_k", i64), ("has_factors", C.c_int), ("stage_ms", dbl * 6)]
+                ("factors_k", i64), ("has_factors", C.c_int), ("lambda_k1_r", dbl), ("lambda_k1_c", dbl),
+                ("stage_ms", dbl * 6)]
 
 
 # (name, restype, argtypes) of every exported symbol.
@@ -110,6 +111,7 @@ SIGNATURES = {
                                               dbl, dbl, C.POINTER(DecoderConfigC), vp,
                                               C.POINTER(C.c_int), ip]),
     "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
+    "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_graph_upsample": (C.c_int, [vp, vp, vp, i64, vp, i64, dbl, i64, vp]),
     "cpcag_cuda_approx_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                            C.POINTER(ApproxConfigC), vp, vp, vp, vp, i64, ip]),

@@ -28,7 +28,7 @@ __all__ = [
     "kron_reduce", "draw_plan", "subsample", "objective", "prox_l1", "prox_l2", "grad_g",
     "fista_solve", "alternate_decode", "power_iteration_norm", "pcg_solve", "run_pipeline",
     "default_context", "SvdResult", "thin_svd", "detect_rank", "graph_upsample", "LowRankFactors",
-    "ApproxDecodeResult", "approx_decode",
+    "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "spectral_gap",
 ]
 
 
@@ -636,6 +636,42 @@ def alternate_decode(Xt, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix,
     return AlternateDecodeResult(out, bool(cv.value), int(it.value))
 
 
+# ------------------------------------------------------------------ eigen / spectral gap
+@dataclass
+class EigenPairs:  # eigs.hpp:11-19
+    eigenvalues: np.ndarray
+    eigenvectors: Optional[np.ndarray]
+
+    def order(self) -> int:
+        return len(self.eigenvalues)
+
+    def leading(self, k: int):
+        if k > self.order():
+            raise ValueError("EigenPairs: fewer pairs than requested")
+        return self.eigenvectors[:, :k]
+
+
+def sym_eig(A: SparseMatrix, k: int, vectors: bool = True, ctx=None) -> EigenPairs:
+    """eigs.cpp:34-51 on the device (dense symmetric eigensolver)."""
+    n = A.rows()
+    ev = np.empty(max(int(k), 1), np.float64)
+    vec = np.empty((n, max(int(k), 1)), np.float64, order="F") if vectors else None
+    N.check(N.lib().cpcag_cuda_sym_eig(_ctx(ctx), A.handle, int(k), ev.ctypes.data,
+                                       vec.ctypes.data if vectors else None))
+    return EigenPairs(ev[:k].copy(), np.asfortranarray(vec[:, :k]) if vectors else None)
+
+
+def spectral_gap(basis: EigenPairs, k: int) -> "SpectralGap":
+    """graph.cpp:237-249 (host logic on the eigenvalues)."""
+    if k < 1 or basis.order() < k + 1:
+        raise ValueError("spectral gap: need at least k+1 eigenvalues")
+    lk = max(0.0, float(basis.eigenvalues[k - 1]))
+    lk1 = max(0.0, float(basis.eigenvalues[k]))
+    if lk1 <= 1e-14:
+        raise RuntimeError("gap undefined: graph has > k components")
+    return SpectralGap(k, lk, lk1, lk / lk1)
+
+
 # ------------------------------------------------------------------ approximate decoder
 @dataclass
 class SvdResult:  # eigs.hpp (thin_svd)
@@ -748,8 +784,8 @@ class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
     kron_pcg_tol: float = 1e-11
     frpcag: FrpcagConfig = field(default_factory=FrpcagConfig)
     decoder: DecoderConfig = field(default_factory=DecoderConfig)
-    lambda_k1_r: float = 1.0
-    lambda_k1_c: float = 1.0
+    lambda_k1_r: float = 0.0  # <= 0: computed on the device as the reference does (pipeline.cpp:343-349)
+    lambda_k1_c: float = 0.0
     seed: int = 0
 
     def c(self) -> N.PipelineConfigC:
@@ -786,6 +822,7 @@ class PipelineReport:  # pipeline.hpp:73-94 (subset)
     detected_rank: int = 0
     factors: Optional[LowRankFactors] = None  # approximate decoder only
     has_factors: bool = False
+    lambda_k1: tuple = (0.0, 0.0)  # gaps the alternate decoder used (rows, columns)
 
     def stage_ms(self, name: str) -> float:
         return self.stages.get(name, 0.0)
@@ -829,4 +866,5 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
         factors = LowRankFactors(np.asfortranarray(fU[:, :k]), fs[:k].copy(), np.asfortranarray(fV[:, :k]), k, True)
     return PipelineReport(int(rep.p), int(rep.n), int(rep.rho_r), int(rep.rho_c), trace, plan, xt, x,
                           bool(rep.decoder_converged), int(rep.decoder_iterations), stages,
-                          int(rep.detected_rank), factors, bool(rep.has_factors))
+                          int(rep.detected_rank), factors, bool(rep.has_factors),
+                          (float(rep.lambda_k1_r), float(rep.lambda_k1_c)))

@@ -265,6 +265,94 @@ void to_f64_device(Ctx* c, const T* a, i64 n, double* out) {
 template void to_f64_device<float>(Ctx*, const float*, i64, double*);
 template void to_f64_device<double>(Ctx*, const double*, i64, double*);
 
+// ---------------------------------------------------------------- sym_eig
+// eigs.cpp:34-51: densify, symmetrise 0.5 (D + D^T), dense symmetric
+// eigensolver (cuSOLVER syevd, eigenvalues ascending), the first k pairs, and
+// each eigenvector column's sign fixed so its first entry above 1e-12 times
+// the column peak is positive.  Dense by design (the reference's own
+// desk-scale solver): n is limited by memory (n^2 doubles).
+__global__ void densify_sym_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                              const double* __restrict__ v, double* __restrict__ D) {
+  const i64 r = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (i64 k = rp[r]; k < rp[r + 1]; ++k) D[r + static_cast<i64>(ci[k]) * n] = v[k];
+}
+__global__ void symmetrize_k(i64 n, const double* __restrict__ D, double* __restrict__ S) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (i64 j = blockIdx.y; j < n; j += gridDim.y) S[i + j * n] = 0.5 * (D[i + j * n] + D[j + i * n]);
+}
+// One CTA per column: peak = max |x|, then the first index with |x| > 1e-12 peak.
+__global__ void fix_signs_k(i64 n, double* __restrict__ E) {
+  __shared__ double red[1024];
+  __shared__ i64 first;
+  const i64 j = blockIdx.x;
+  double* x = E + j * n;
+  double m = 0.0;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(x[i]));
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double peak = red[0];
+  if (threadIdx.x == 0) first = n;
+  __syncthreads();
+  if (peak == 0.0) return;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x)
+    if (fabs(x[i]) > 1e-12 * peak) atomicMin(reinterpret_cast<unsigned long long*>(&first), static_cast<unsigned long long>(i));
+  __syncthreads();
+  const bool flip = first < n && x[first] < 0.0;
+  __syncthreads();
+  if (flip)
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) x[i] = -x[i];
+}
+
+void sym_eig_device(Ctx* c, Csr* A, i64 k, double* evals, double* evecs) {
+  if (A->rows != A->cols) invalid("sym_eig: square matrix required");
+  const i64 n = A->rows;
+  if (k < 1 || k > n)
+    invalid("sym_eig: order k out of range (k = " + std::to_string(k) + ", dim = " + std::to_string(n) + ")");
+  if (n > 46340) invalid("sym_eig: dense eigensolver limited to n <= 46340 on the device");
+  DevBuf<double> D(c, n * n), S(c, n * n), lam(c, n);
+  D.zero(c);
+  densify_sym_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, A->rp, A->ci, A->v, D.p);
+  launched(c);
+  symmetrize_k<<<dim3(blocks_for(n), static_cast<unsigned>(std::min<i64>(n, 65535))), kBlock, 0, c->stream>>>(n, D.p,
+                                                                                                          S.p);
+  launched(c);
+  D.release();
+  cusolverDnHandle_t h = solver_handle(c);
+  const cusolverEigMode_t mode = evecs ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
+  const int ni = static_cast<int>(n);
+  int lwork = 0;
+  solver_ok(cusolverDnDsyevd_bufferSize(h, mode, CUBLAS_FILL_MODE_LOWER, ni, S.p, ni, lam.p, &lwork), "syevd buffer");
+  DevBuf<double> work(c, std::max(lwork, 1));
+  DevBuf<int> info(c, 1);
+  solver_ok(cusolverDnDsyevd(h, mode, CUBLAS_FILL_MODE_LOWER, ni, S.p, ni, lam.p, work.p, lwork, info.p), "syevd");
+  if (read_back(c, info.p) != 0) runtime("sym_eig: eigensolver failed");
+  CUDA_OK(cudaMemcpyAsync(evals, lam.p, sizeof(double) * k, cudaMemcpyDefault, c->stream));
+  if (evecs) {
+    fix_signs_k<<<static_cast<unsigned>(k), 1024, 0, c->stream>>>(n, S.p);
+    launched(c);
+    CUDA_OK(cudaMemcpyAsync(evecs, S.p, sizeof(double) * n * k, cudaMemcpyDefault, c->stream));
+  }
+  sync(c);
+}
+
+// graph.cpp:237-249.
+cpcag_spectral_gap spectral_gap_host(const double* evals, i64 order, i64 k) {
+  if (k < 1 || order < k + 1) invalid("spectral gap: need at least k+1 eigenvalues");
+  cpcag_spectral_gap g;
+  g.k = k;
+  g.lambda_k = std::max(0.0, evals[k - 1]);
+  g.lambda_k1 = std::max(0.0, evals[k]);
+  if (g.lambda_k1 <= 1e-14) runtime("gap undefined: graph has > k components");
+  g.ratio = g.lambda_k / g.lambda_k1;
+  return g;
+}
+
 // eigs.cpp:59-64.
 i64 detect_rank_host(const std::vector<double>& s, double thr) {
   if (s.empty() || !(s[0] > 0.0)) return 0;
@@ -416,4 +504,18 @@ extern "C" int cpcag_cuda_approx_decode(cpcag_ctx ctx, int precision, const void
   if (precision == CPCAG_F32) return run(float{});
   set_last_error("unknown precision flag");
   return CPCAG_ERR_INVALID_ARGUMENT;
+}
+
+extern "C" int cpcag_cuda_sym_eig(cpcag_ctx ctx, cpcag_csr A, int64_t k, double* eigenvalues, double* eigenvectors) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    Csr* a = as_csr(A);
+    if (!eigenvalues) invalid("null argument");
+    OutView<double> ev(c, eigenvalues, static_cast<size_t>(std::max<int64_t>(k, 0)));
+    OutView<double> ex(c, eigenvectors, eigenvectors ? static_cast<size_t>(a->rows * std::max<int64_t>(k, 0)) : 0);
+    sym_eig_device(c, a, k, ev.d, eigenvectors ? ex.d : nullptr);
+    ev.flush(c);
+    if (eigenvectors) ex.flush(c);
+    sync(c);
+  });
 }

@@ -420,6 +420,8 @@ void gram_svd_device(Ctx* c, const double* A, i64 m, i64 n, i64 kvec, double* si
 template <typename T>
 void to_f64_device(Ctx* c, const T* a, i64 n, double* out);
 i64 detect_rank_host(const std::vector<double>& s, double thr);
+void sym_eig_device(Ctx* c, Csr* A, i64 k, double* evals, double* evecs);
+cpcag_spectral_gap spectral_gap_host(const double* evals, i64 order, i64 k);
 
 template <typename T>
 void approx_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const std::vector<i64>& om_r,

@@ -157,10 +157,31 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     }
     if (cfg.decoder_variant != CPCAG_DECODER_ALTERNATE)
       invalid("run_pipeline: decoder variant not supported on the device path (alternate or approx)");
+    // pipeline.cpp:343-349: gaps from the k+1 smallest eigenvalues of the full
+    // Laplacians, k = max(1, detected rank), unless the caller supplies them.
+    double lk1_r = cfg.lambda_k1_r, lk1_c = cfg.lambda_k1_c;
+    if (!(lk1_r > 0.0) || !(lk1_c > 0.0)) {
+      const i64 k = std::max<i64>(1, rep->detected_rank);
+      std::vector<double> ev(static_cast<size_t>(k + 1));
+      if (!(lk1_r > 0.0)) {
+        DevBuf<double> e(c, k + 1);
+        sym_eig_device(c, Lr.get(), k + 1, e.p, nullptr);
+        CUDA_OK(cudaMemcpy(ev.data(), e.p, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+        lk1_r = spectral_gap_host(ev.data(), k + 1, k).lambda_k1;
+      }
+      if (!(lk1_c > 0.0)) {
+        DevBuf<double> e(c, k + 1);
+        sym_eig_device(c, Lc.get(), k + 1, e.p, nullptr);
+        CUDA_OK(cudaMemcpy(ev.data(), e.p, sizeof(double) * (k + 1), cudaMemcpyDeviceToHost));
+        lk1_c = spectral_gap_host(ev.data(), k + 1, k).lambda_k1;
+      }
+    }
+    rep->lambda_k1_r = lk1_r;
+    rep->lambda_k1_c = lk1_c;
     int conv = 0;
     i64 it = 0;
-    alternate_decode_device<T>(c, Xt_out, rho_r, rho_c, om_r.data(), om_c.data(), p, n, Lr.get(), Lc.get(),
-                               cfg.lambda_k1_r, cfg.lambda_k1_c, cfg.decoder, X_out, &conv, &it);
+    alternate_decode_device<T>(c, Xt_out, rho_r, rho_c, om_r.data(), om_c.data(), p, n, Lr.get(), Lc.get(), lk1_r,
+                               lk1_c, cfg.decoder, X_out, &conv, &it);
     rep->decoder_converged = conv;
     rep->decoder_iterations = it;
   });

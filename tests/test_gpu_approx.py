@@ -144,3 +144,47 @@ def test_approx_decode_errors(P, ctx):
         P.approx_decode(np.zeros_like(Xt), plan, dLr, dLc, ctx=ctx)
     with pytest.raises(ValueError, match="delta_for_scaling must be in"):
         P.approx_decode(Xt, plan, dLr, dLc, P.DecoderConfig(delta_for_scaling=1.5), ctx=ctx)
+
+
+# ------------------------------------------------------------------ sym_eig / spectral gap (eigs.cpp:34-51)
+@pytest.mark.parametrize("n,k", [(60, 5), (257, 11)])
+def test_sym_eig_matches_lapack(P, ctx, n, k):
+    L = knn_laplacian(n, 3, 10, n)
+    ep = P.sym_eig(to_device(ctx, L), k, ctx=ctx)
+    w, E = O.sym_eig(L, k)
+    assert np.allclose(ep.eigenvalues, w, rtol=1e-10, atol=1e-12)
+    # same sign rule; vectors of simple eigenvalues agree
+    assert np.abs(ep.eigenvectors - E).max() <= 1e-8
+
+
+def test_spectral_gap_and_errors(P, ctx):
+    L = knn_laplacian(80, 3, 10, 9)
+    ep = P.sym_eig(to_device(ctx, L), 4, vectors=False, ctx=ctx)
+    g = P.spectral_gap(ep, 3)
+    lk, lk1, ratio = O.spectral_gap(O.sym_eig(L, 4)[0], 3)
+    assert g.k == 3 and abs(g.lambda_k1 - lk1) <= 1e-10 * lk1 and abs(g.ratio - ratio) <= 1e-9
+    with pytest.raises(ValueError, match="order k out of range"):
+        P.sym_eig(to_device(ctx, L), 81, ctx=ctx)
+    two = blocks_laplacian([10, 12], 3)
+    with pytest.raises(RuntimeError, match="gap undefined: graph has > k components"):
+        P.spectral_gap(P.sym_eig(to_device(ctx, two), 2, vectors=False, ctx=ctx), 1)
+
+
+def test_pipeline_computes_gaps_like_the_reference(P, ctx):
+    """lambda_k1 <= 0: run_pipeline computes the gaps (pipeline.cpp:343-349)."""
+    import math
+
+    from paper_1602_02070_b200.workloads import config0
+
+    Y, _ = config0(seed=1602, small=True)
+    p, n = Y.shape
+    g = math.sqrt(max(p, n))
+    cfg = P.PipelineConfig(knn=10, a=4, b=4, frpcag=P.FrpcagConfig(gamma_r=g, gamma_c=g, tol=1e-300, max_iter=40),
+                           decoder=P.DecoderConfig(1.0, 1e-8, 100, variant="alternate"), seed=1602)
+    rep = P.run_pipeline(Y, cfg, ctx=ctx)
+    k = max(1, rep.detected_rank)
+    gr = O.build_knn_graph(Y, True, 10)
+    gc = O.build_knn_graph(Y, False, 10)
+    lr = O.spectral_gap(O.sym_eig(gr.laplacian, k + 1)[0], k)[1]
+    lc = O.spectral_gap(O.sym_eig(gc.laplacian, k + 1)[0], k)[1]
+    assert abs(rep.lambda_k1[0] - lr) <= 1e-10 * lr and abs(rep.lambda_k1[1] - lc) <= 1e-10 * lc
