@@ -515,6 +515,30 @@ void knn_select(const Points& P, i64 K, i64* nbr, double* nbr_d2, Vec& mean_d2) 
   }
 }
 
+// knn_select for a subset of query points (full-size spot checks): the same
+// per-point selection over all n candidates.
+void knn_select_rows(const Points& P, i64 K, const i64* rows, i64 nq, i64* nbr, double* nbr_d2) {
+  const i64 n = P.n;
+#pragma omp parallel
+  {
+    std::vector<std::pair<double, i64>> order;
+    order.reserve(static_cast<size_t>(n));
+#pragma omp for schedule(dynamic, 1)
+    for (i64 q = 0; q < nq; ++q) {
+      const i64 i = rows[q];
+      order.clear();
+      for (i64 j = 0; j < n; ++j)
+        if (j != i) order.emplace_back(pair_d2(P, i, j), j);
+      std::nth_element(order.begin(), order.begin() + (K - 1), order.end());
+      std::sort(order.begin(), order.begin() + K);
+      for (i64 k = 0; k < K; ++k) {
+        nbr[q * K + k] = order[static_cast<size_t>(k)].second;
+        nbr_d2[q * K + k] = order[static_cast<size_t>(k)].first;
+      }
+    }
+  }
+}
+
 struct Graph {
   Csr W, L;
   Vec deg;
@@ -1108,6 +1132,17 @@ int ora_knn_neighbors(const double* X, int64_t rows, int64_t cols, int axis_rows
       throw std::invalid_argument("knn graph: need at least K+1 points, got " + std::to_string(P.n));
     Vec mean;
     knn_select(P, K, nbr, nbr_d2, mean);
+  });
+}
+
+int ora_knn_rows(const double* X, int64_t rows, int64_t cols, int axis_rows, int64_t K, const int64_t* query,
+                 int64_t nq, int64_t* nbr, double* nbr_d2) {
+  return guard([&] {
+    const Points P = gather_points(X, rows, cols, axis_rows != 0);
+    if (K < 1 || P.n < K + 1) throw std::invalid_argument("knn rows: bad K");
+    for (int64_t q = 0; q < nq; ++q)
+      if (query[q] < 0 || query[q] >= P.n) throw std::invalid_argument("knn rows: query out of range");
+    knn_select_rows(P, K, query, nq, nbr, nbr_d2);
   });
 }
 

@@ -80,6 +80,9 @@ int ora_graph_from_adjacency(const ora_csr* W, int normalized, ora_csr** laplaci
  * rows R (n_known x r). */
 int ora_graph_upsample(const ora_csr* L, const int64_t* known, int64_t n_known, const double* R, int64_t r,
                        double pcg_tol, int64_t pcg_max_iter, double* S);
+/* Exact kNN lists of the query points only (full-size spot checks). */
+int ora_knn_rows(const double* X, int64_t rows, int64_t cols, int axis_rows, int64_t K, const int64_t* query,
+                 int64_t nq, int64_t* nbr, double* nbr_d2);
 int ora_kron_reduce(const ora_csr* L, const int64_t* keep, int64_t nkeep, double pcg_tol,
                     double prune_tol, ora_csr** out);
 

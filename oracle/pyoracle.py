@@ -305,6 +305,17 @@ def knn_neighbors(X, axis_rows: bool, K: int):
     return nbr, d2
 
 
+def knn_rows(X, axis_rows: bool, K: int, rows):
+    """Exact kNN lists (graph.cpp:86-105) of the query points `rows` only."""
+    X = _f64(X)
+    rows = _idx(rows)
+    nbr = np.empty((len(rows), K), np.int64)
+    d2 = np.empty((len(rows), K))
+    _check(lib().ora_knn_rows(_d(X), i64(X.shape[0]), i64(X.shape[1]), C.c_int(int(axis_rows)), i64(K),
+                              _i(rows), i64(len(rows)), _i(nbr), _d(d2)))
+    return nbr, d2
+
+
 def graph_from_adjacency(W: Csr, normalized=False) -> GraphModel:
     L = vp()
     deg = np.empty(W.rows)

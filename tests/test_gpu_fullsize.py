@@ -1,0 +1,149 @@
+"""Parity at the BASELINE configurations' full sizes, through checks whose
+cost does not grow with the whole problem (the oracle cannot run the full
+problems in test time):
+
+  cfg2  kNN graph of 100 000 x 512 points: the device neighbour lists of a
+        random sample of points are bit-exact against the oracle's exact
+        per-point selection (graph.cpp:86-105) over all 100 000 candidates;
+        every list is sorted by (d2, j) and excludes the point; W is
+        symmetric and the Laplacian rows sum to zero.
+  cfg3  decoder operator 4096 x 200 000 (band apply, the path the size
+        selects): one fp64 apply is bit-exact on sampled columns against
+        the reference's per-entry arithmetic (decoders.cpp:160-170),
+        emulated in Python floats (IEEE binary64, same operation order).
+  cfg1  the whole pipeline at 10 304 x 1 000 with reduced iteration counts
+        (FISTA 20, decoder 20) against the oracle's stage-by-stage fp64
+        composite: fp32 X within the north_star 1e-4.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import rel
+from oracle import pyoracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1602_02070_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    return P.Context(0)
+
+
+def test_cfg2_knn_full_size_sampled_rows_bit_exact(P, ctx):
+    import torch
+
+    from paper_1602_02070_b200 import workloads
+
+    X = workloads.config2_points()  # d x n fp32
+    d, n = X.shape
+    Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda").t()
+    nbr, d2 = P.knn(Xd, "cols", 10, ctx=ctx)
+    rows = np.random.default_rng(7).choice(n, 48, replace=False)
+    onbr, od2 = O.knn_rows(X.astype(np.float64), False, 10, rows)
+    assert np.array_equal(nbr[rows], onbr)
+    assert np.array_equal(d2[rows], od2)
+    # size-independent properties over every point
+    assert np.all((d2[:, 1:] > d2[:, :-1]) | ((d2[:, 1:] == d2[:, :-1]) & (nbr[:, 1:] > nbr[:, :-1])))
+    assert not np.any(nbr == np.arange(n)[:, None])
+    g = P.build_knn_graph(Xd, "cols", 10, ctx=ctx)
+    W = g.adjacency.to_scipy()
+    assert abs(W - W.T).max() == 0.0
+    Ls = g.laplacian.to_scipy()
+    assert np.abs(np.asarray(Ls.sum(axis=1)).ravel()).max() <= 1e-12 * max(1.0, np.abs(g.degrees).max())
+
+
+def _apply_entry(rp_r, ci_r, v_r, rp_c, ci_c, v_c, Pm, rsel, csel, gr, gc, i, c):
+    """decoders.cpp:160-170 for one entry, binary64 in the reference order."""
+    x1 = 0.0
+    for k in range(rp_c[c], rp_c[c + 1]):
+        x1 = x1 + v_c[k] * Pm[i, ci_c[k]]
+    x2 = 0.0
+    for k in range(rp_r[i], rp_r[i + 1]):
+        x2 = x2 + v_r[k] * Pm[ci_r[k], c]
+    out = gc * x1 + gr * x2
+    if rsel[i] and csel[c]:
+        out = out + Pm[i, c]
+    return out
+
+
+def test_cfg3_band_apply_full_size_sampled_columns_bit_exact(P, ctx):
+    import torch
+
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200 import workloads
+    from paper_1602_02070_b200.sharded import CudaBlockBackend
+
+    Pr, Pc = workloads.config3_points()
+    p, n = Pr.shape[1], Pc.shape[1]
+    gr_ = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    gc_ = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
+    gr, gc = 1.0 / 0.37, 1.0 / 0.53
+    be = CudaBlockBackend(ctx, N.F64, plan, gr_.laplacian, gc_.laplacian, gr, gc, 0, n)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    Pflat = torch.randn(p * n, dtype=torch.float64, device="cuda", generator=gen)
+    AP = torch.empty_like(Pflat)
+    be.apply(Pflat, AP)
+    torch.cuda.synchronize()
+    cols = np.random.default_rng(3).choice(n, 6, replace=False)
+    # neighbour columns the sampled outputs read
+    rp_c, ci_c, v_c = gc_.laplacian.arrays()
+    rp_r, ci_r, v_r = gr_.laplacian.arrays()
+    need = sorted(set(int(j) for c in cols for j in ci_c[rp_c[c]:rp_c[c + 1]]) | set(int(c) for c in cols))
+    Pm = np.zeros((p, n))
+    Pv = Pflat.view(n, p)
+    for j in need:
+        Pm[:, j] = Pv[j].cpu().numpy()
+    rsel = np.zeros(p, bool)
+    rsel[np.asarray(plan.omega_r)] = True
+    csel = np.zeros(n, bool)
+    csel[np.asarray(plan.omega_c)] = True
+    APv = AP.view(n, p)
+    rows = np.random.default_rng(4).choice(p, 64, replace=False)
+    for c in cols:
+        got = APv[int(c)].cpu().numpy()
+        for i in rows:
+            want = _apply_entry(rp_r, ci_r, v_r, rp_c, ci_c, v_c, Pm, rsel, csel, gr, gc, int(i), int(c))
+            assert got[i] == want, (i, c)
+    be.close()
+
+
+def test_cfg1_pipeline_full_size_reduced_iterations(P, ctx):
+    import torch
+
+    from paper_1602_02070_b200 import workloads
+
+    wl = workloads.config1()
+    p, n = wl.Y.shape
+    its = 20
+    cfg = P.PipelineConfig(knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
+                           frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
+                                                 max_iter=its),
+                           decoder=P.DecoderConfig(1.0, 1e-30, its, variant="alternate"),
+                           lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1603)
+    Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=torch.float32, device="cuda").t()
+    Wr = P.SparseMatrix.from_scipy(wl.W_r, ctx=ctx)
+    rep = P.run_pipeline(Yd, cfg, W_r=Wr, ctx=ctx)
+    # oracle composite, stage by stage (pipeline.cpp:273-350), fp64
+    Y = wl.Y.astype(np.float32).astype(np.float64)
+    gr = O.graph_from_adjacency(O.Csr.from_scipy(wl.W_r))
+    gc = O.build_knn_graph(Y, False, 10)
+    plan = O.draw_plan(p, n, -(-p // wl.b), -(-n // wl.a), seed=1603)
+    assert np.array_equal(rep.plan.omega_r, plan.omega_r) and np.array_equal(rep.plan.omega_c, plan.omega_c)
+    Yt = O.subsample(Y, plan)
+    Lr_t = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
+    Lc_t = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
+    Xt, _ = O.fista_solve(Yt, Lr_t, Lc_t, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, its))
+    assert rel(rep.Xt.cpu().numpy(), Xt) <= 1e-4
+    dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, its)
+    assert rel(rep.X.cpu().numpy(), dec.X) <= 1e-4
+    assert math.isfinite(rep.trace.objective[-1])
