@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "frpcag.cuh"
+#include "fista_tc.cuh"
 
 namespace cpcag_cuda {
 
@@ -578,7 +579,7 @@ struct LinLauncher {  // fp32 only; other precisions never take the linearity pa
                    const LinBufs&, FistaState*) {}
   static void step(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, T, T, int, int, const cpcag_frpcag_config&, T,
                    const T*, const T*, T*, const T*, T*, const SplitWs&, const LinBufs&, i64, double*, double*,
-                   FistaState*) {}
+                   FistaState*, const FistaTcPlan*, float*, float*) {}
 };
 template <>
 struct LinLauncher<float> {
@@ -594,7 +595,7 @@ struct LinLauncher<float> {
   static void step(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r, float s_c,
                    int use_r, int use_c, const cpcag_frpcag_config& cfg, float stepT, const float* Z, const float* Y,
                    float* S, const float* Sp, float* Zn, const SplitWs& ws, const LinBufs& lb, i64 j, double* partials,
-                   double* trace, FistaState* st) {
+                   double* trace, FistaState* st, const FistaTcPlan* tcp, float* Zh, float* Zl) {
     const i64 m = rr * rc;
     {
       KScope ks_(c, "fista_grad_prox");
@@ -604,9 +605,12 @@ struct LinLauncher<float> {
     }
     {
       KScope ks_(c, "fista_objective");
-      fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, S, ws,
-                                                       st);
+      // L~_r S on the tensor cores when planned (the CUDA-core split-K kernel
+      // then only forms S L~_c and zeroes part1, which the TC kernel fills).
+      fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, tcp ? 0 : cfg.gamma_r != 0.0,
+                                                       cfg.gamma_c != 0.0, S, ws, st);
       launched(c);
+      if (tcp) fista_tc_part1(c, *tcp, S, Zh, Zl, ws.part1, &st->done);
       fista_lin_objective_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), cfg.gamma_r, cfg.gamma_c,
                                                        cfg.loss, S, Y, ws, lb.LSr[j & 1], lb.LSc[j & 1], partials,
                                                        trace, st);
@@ -729,6 +733,21 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     lb = LinBufs{b, b + N, {b + 2 * N, b + 3 * N}, {b + 4 * N, b + 5 * N}};
     LinLauncher<T>::init(c, gk, nb1, rows, cols, Dr.p, Dc.p, use_r, use_c, Y, ws, lb, st.p);
   }
+  // Tensor-core L~_r S (fp32 linearity path): 3xTF32 tcgen05.
+  bool use_tc = lin && use_r && sizeof(T) == 4 && fista_tc_supported(rows, cols, static_cast<int>(gk.z));
+  if (const char* e = std::getenv("CPCAG_FISTA_TC")) use_tc = use_tc && std::string(e) != "0";
+  FistaTcPlan tcp;
+  DevBuf<float> tcb;
+  float *Zh = nullptr, *Zl = nullptr;
+  if (use_tc) {
+    const i64 ld = (rows + 3) / 4 * 4;
+    tcb.alloc(c, static_cast<size_t>(ld) * (2 * rows + 2 * cols));
+    float* Ah = tcb.p;
+    float* Al = Ah + ld * rows;
+    Zh = Al + ld * rows;
+    Zl = Zh + ld * cols;
+    fista_tc_setup(c, rows, cols, static_cast<int>(gk.z), reinterpret_cast<const float*>(Dr.p), Ah, Al, Zh, Zl, &tcp);
+  }
 
   i64 j = 1;
   FistaState host{};
@@ -742,7 +761,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       T* Znext = Zb[(j + 1) & 1].p;
       if (lin) {
         LinLauncher<T>::step(c, gk, nb1, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg, stepT, Zj, Y, Sj, Sprev,
-                             Znext, ws, lb, j, part.p, tr.p, st.p);
+                             Znext, ws, lb, j, part.p, tr.p, st.p, use_tc ? &tcp : nullptr, Zh, Zl);
         continue;
       }
       if (splitk) {

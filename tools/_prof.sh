@@ -1,1 +1,3 @@
-for k in 16 8 6 4; do CPCAG_FAST2_CTAS=$k timeout -s KILL 300 python tools/bench_stages.py 2>&1 | grep "decode" | cut -c1-140 | sed "s/^/ctas=$k /"; done
+CPCAG_TRACE=1 JIT_N=60 timeout -s KILL 300 python tools/jitter.py > gpurun_out/jit66.log 2>&1
+grep "kron ms" gpurun_out/jit66.log | head -1
+grep "cpcag trace" gpurun_out/jit66.log | awk '{print $(NF-1), $0}' | sort -rn | head -12
