@@ -751,6 +751,8 @@ extern "C" int cpcag_cuda_gram_tf32x3(cpcag_ctx ctx, const double* P, int64_t n,
   });
 }
 
+namespace cpcag_cuda {
+
 // ------------------------------------------------------------------ FISTA L_r Z on the tensor cores
 // part1[s] (rr x rc, col-major) = rows of L~_r times Z over the s-th slice of
 // k, 3xTF32 (hi.hi + hi.lo + lo.hi) into TMEM -- the dominant product of the
@@ -925,3 +927,5 @@ void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, fl
   else go(fista_tc_part1_k<256>);
   launched(c);
 }
+
+}  // namespace cpcag_cuda
