@@ -119,6 +119,7 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
 
   // pipeline.cpp:319-320: the detected rank of the compressed solution (its
   // singular values only), outside the stage timers as in the reference.
+  trace_mark(c, "pipeline: stages to solve");
   {
     const i64 q = std::min(rho_r, rho_c);
     DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), sv(c, std::max<i64>(q, 1));
@@ -131,6 +132,7 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     sync(c);
     rep->detected_rank = detect_rank_host(hs, cfg.approx.rank_threshold);
   }
+  trace_mark(c, "pipeline: detected rank");
   rep->has_factors = 0;
   rep->factors_k = 0;
 
