@@ -223,6 +223,8 @@ T read_back(Ctx* c, const T* dptr) {
 // fp32 copy is made on first fp32 use.  `sym` records exact symmetry (A ==
 // A^T bit for bit), which lets X*A run as a pull over CSR rows in exactly the
 // reference's accumulation order (sparse.cpp:100-111).
+void* csr_malloc(Ctx* c, size_t bytes);  // stream-ordered pool (see core.cu)
+
 struct Csr {
   i64 rows = 0, cols = 0, nnz = 0;
   i64* rp = nullptr;

@@ -125,15 +125,26 @@ static void harvest(Ctx* c) {
 }
 
 // ------------------------------------------------------------------ CSR
+// CSR arrays live in the stream-ordered pool (cudaMallocAsync on the context
+// stream): plain cudaMalloc/cudaFree map and unmap device memory on every
+// graph built and dropped, which measured as 20-500 ms stalls inside the
+// pipeline.  The destructor cannot know which stream last used the arrays,
+// so it synchronises the device (what cudaFree would do) and returns them to
+// the pool, where the next allocation reuses them without a remap.
+void* csr_malloc(Ctx* c, size_t bytes) {
+  void* p = nullptr;
+  if (bytes) CUDA_OK(cudaMallocAsync(&p, bytes, c->stream));
+  return p;
+}
+
 Csr::~Csr() {
-  cudaFree(rp);
-  cudaFree(ci);
-  cudaFree(v);
-  cudaFree(v32);
-  cudaFree(t_rp);
-  cudaFree(t_ci);
-  cudaFree(t_v);
-  cudaFree(t_v32);
+  void* arrays[] = {rp, ci, v, v32, t_rp, t_ci, t_v, t_v32};
+  bool any = false;
+  for (void* p : arrays) any |= p != nullptr;
+  if (!any) return;
+  if (cudaDeviceSynchronize() != cudaSuccess) return;  // context gone (process exit)
+  for (void* p : arrays)
+    if (p) cudaFreeAsync(p, 0);
 }
 
 Csr* csr_alloc(Ctx* c, i64 rows, i64 cols, i64 nnz) {
@@ -143,11 +154,11 @@ Csr* csr_alloc(Ctx* c, i64 rows, i64 cols, i64 nnz) {
   a->nnz = nnz;
   a->device = c->device;
   try {
-    CUDA_OK(cudaMalloc(&a->rp, sizeof(i64) * (rows + 1)));
+    a->rp = static_cast<i64*>(csr_malloc(c, sizeof(i64) * (rows + 1)));
     CUDA_OK(cudaMemsetAsync(a->rp, 0, sizeof(i64) * (rows + 1), c->stream));
     if (nnz) {
-      CUDA_OK(cudaMalloc(&a->ci, sizeof(int) * nnz));
-      CUDA_OK(cudaMalloc(&a->v, sizeof(double) * nnz));
+      a->ci = static_cast<int*>(csr_malloc(c, sizeof(int) * nnz));
+      a->v = static_cast<double*>(csr_malloc(c, sizeof(double) * nnz));
     }
   } catch (...) {
     delete a;
@@ -168,7 +179,7 @@ const double* csr_values<double>(Ctx*, Csr* a) {
 template <>
 const float* csr_values<float>(Ctx* c, Csr* a) {
   if (!a->v32 && a->nnz) {
-    CUDA_OK(cudaMalloc(&a->v32, sizeof(float) * a->nnz));
+    a->v32 = static_cast<float*>(csr_malloc(c, sizeof(float) * a->nnz));
     to_f32_k<<<stride_blocks(c, a->nnz), kBlock, 0, c->stream>>>(a->v, a->v32, a->nnz);
     launched(c);
   }
@@ -252,13 +263,13 @@ __global__ void iota_k(i64 n, int* out) {
 void csr_build_transpose(Ctx* c, Csr* a) {
   if (a->t_rp) return;
   const i64 nnz = a->nnz;
-  CUDA_OK(cudaMalloc(&a->t_rp, sizeof(i64) * (a->cols + 1)));
+  a->t_rp = static_cast<i64*>(csr_malloc(c, sizeof(i64) * (a->cols + 1)));
   if (nnz == 0) {
     CUDA_OK(cudaMemsetAsync(a->t_rp, 0, sizeof(i64) * (a->cols + 1), c->stream));
     return;
   }
-  CUDA_OK(cudaMalloc(&a->t_ci, sizeof(int) * nnz));
-  CUDA_OK(cudaMalloc(&a->t_v, sizeof(double) * nnz));
+  a->t_ci = static_cast<int*>(csr_malloc(c, sizeof(int) * nnz));
+  a->t_v = static_cast<double*>(csr_malloc(c, sizeof(double) * nnz));
   DevBuf<int> keys_out(c, nnz), idx(c, nnz), idx_out(c, nnz), row_of(c, nnz);
   iota_k<<<blocks_for(nnz), kBlock, 0, c->stream>>>(nnz, idx.p);
   launched(c);
@@ -287,7 +298,7 @@ template <>
 const float* csr_t_values<float>(Ctx* c, Csr* a) {
   csr_build_transpose(c, a);
   if (!a->t_v32 && a->nnz) {
-    CUDA_OK(cudaMalloc(&a->t_v32, sizeof(float) * a->nnz));
+    a->t_v32 = static_cast<float*>(csr_malloc(c, sizeof(float) * a->nnz));
     to_f32_k<<<stride_blocks(c, a->nnz), kBlock, 0, c->stream>>>(a->t_v, a->t_v32, a->nnz);
     launched(c);
   }

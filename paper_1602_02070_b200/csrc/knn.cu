@@ -392,8 +392,8 @@ Csr* build_laplacian(Ctx* c, Csr* W, const double* deg, int kind) {
   }
   L->nnz = scan_counts(c, cnt.p, n, L->rp);
   if (L->nnz) {
-    CUDA_OK(cudaMalloc(&L->ci, sizeof(int) * L->nnz));
-    CUDA_OK(cudaMalloc(&L->v, sizeof(double) * L->nnz));
+    L->ci = static_cast<int*>(csr_malloc(c, sizeof(int) * L->nnz));
+    L->v = static_cast<double*>(csr_malloc(c, sizeof(double) * L->nnz));
     lap_fill_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, kind, W->rp, W->ci, W->v, deg, dis.p, L->rp, L->ci, L->v);
     launched(c);
   }

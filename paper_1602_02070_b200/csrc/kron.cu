@@ -762,8 +762,8 @@ Csr* dense_to_csr(Ctx* c, const double* S, i64 m, double prune, bool symmetrize)
   const i64 nnz = scan_counts(c, cnt.p, m, out->rp);
   out->nnz = nnz;
   if (nnz) {
-    CUDA_OK(cudaMalloc(&out->ci, sizeof(int) * nnz));
-    CUDA_OK(cudaMalloc(&out->v, sizeof(double) * nnz));
+    out->ci = static_cast<int*>(csr_malloc(c, sizeof(int) * nnz));
+    out->v = static_cast<double*>(csr_malloc(c, sizeof(double) * nnz));
     sym_fill_k<<<blocks_for(m, 128), 128, 0, c->stream>>>(m, S, prune, symmetrize, out->rp, out->ci, out->v);
     launched(c);
   }
@@ -781,8 +781,8 @@ Csr* gather_sub(Ctx* c, Csr* L, const i64* rsrc_dev, i64 nr, const int* cmap_dev
   const i64 nnz = scan_counts(c, cnt.p, nr, out->rp);
   out->nnz = nnz;
   if (nnz) {
-    CUDA_OK(cudaMalloc(&out->ci, sizeof(int) * nnz));
-    CUDA_OK(cudaMalloc(&out->v, sizeof(double) * nnz));
+    out->ci = static_cast<int*>(csr_malloc(c, sizeof(int) * nnz));
+    out->v = static_cast<double*>(csr_malloc(c, sizeof(double) * nnz));
     sub_fill_k<<<blocks_for(nr), kBlock, 0, c->stream>>>(nr, rsrc_dev, L->rp, L->ci, L->v, cmap_dev, out->rp,
                                                          out->ci, out->v);
     launched(c);
