@@ -1,5 +1,6 @@
 """Per-call wall time of repeated kron_reduce / alternate_decode calls on the
 config-1 operators (diagnoses run-to-run jitter)."""
+import gc
 import os
 import sys
 import time
@@ -11,6 +12,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1602_02070_b200 as P  # noqa: E402
 from bench import make_workload, pipeline_config  # noqa: E402
 
+if os.environ.get("JIT_NOGC"):
+    gc.disable()
 wl = make_workload()
 ctx = P.Context(0)
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -29,7 +32,7 @@ for _ in range(int(os.environ.get("JIT_N", "30"))):
 print("kron ms", [round(t, 1) for t in ts], flush=True)
 
 flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-for use_flush in (False, True):
+for use_flush in ((False,) if os.environ.get("JIT_ONE") else (False, True)):
     ts, st = [], []
     for _ in range(int(os.environ.get("JIT_N", "20"))):
         if use_flush:
