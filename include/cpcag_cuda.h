@@ -65,6 +65,10 @@ const char* cpcag_cuda_version(void);
  * stream, a workspace cache and pinned staging buffers. */
 int cpcag_ctx_create(int device, cpcag_ctx* out);
 int cpcag_ctx_destroy(cpcag_ctx ctx);
+/* Grows the context's stream-ordered memory pool to at least `bytes` now
+ * (the pool keeps freed memory), so the first runs of a workload do not pay
+ * for mapping device memory while the pool grows to its peak. */
+int cpcag_ctx_reserve(cpcag_ctx ctx, int64_t bytes);
 /* Use an external stream (e.g. torch.cuda.current_stream()); NULL restores
  * the context's own stream. */
 int cpcag_ctx_set_stream(cpcag_ctx ctx, void* cuda_stream);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "cpcag_cuda_alternate_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                               dbl, dbl, C.POINTER(DecoderConfigC), vp,
                                               C.POINTER(C.c_int), ip]),
+    "cpcag_ctx_reserve": (C.c_int, [vp, i64]),
     "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_graph_upsample": (C.c_int, [vp, vp, vp, i64, vp, i64, dbl, i64, vp]),

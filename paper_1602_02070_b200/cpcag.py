@@ -140,6 +140,10 @@ class Context:
     def reset_launch_count(self):
         N.lib().cpcag_ctx_reset_launch_count(self._h)
 
+    def reserve(self, nbytes: int):
+        """Grow the stream-ordered memory pool to `nbytes` up front."""
+        N.check(N.lib().cpcag_ctx_reserve(self._h, int(nbytes)))
+
     def enable_kernel_timing(self, on: bool = True):
         """CUDA-event timing of every hot-kernel launch (for roofline figures)."""
         N.check(N.lib().cpcag_ctx_enable_kernel_timing(self._h, int(bool(on))))

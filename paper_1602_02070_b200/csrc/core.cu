@@ -785,6 +785,17 @@ int cpcag_ctx_create(int device, cpcag_ctx* out) {
   });
 }
 
+int cpcag_ctx_reserve(cpcag_ctx ctx, int64_t bytes) {
+  return guard([&] {
+    Ctx* c = as_ctx(ctx);
+    if (bytes <= 0) return;
+    void* p = nullptr;
+    CUDA_OK(cudaMallocAsync(&p, static_cast<size_t>(bytes), c->stream));
+    CUDA_OK(cudaFreeAsync(p, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+  });
+}
+
 int cpcag_ctx_destroy(cpcag_ctx ctx) {
   return guard([&] {
     Ctx* c = as_ctx(ctx);

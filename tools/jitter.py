@@ -16,6 +16,8 @@ if os.environ.get("JIT_NOGC"):
     gc.disable()
 wl = make_workload()
 ctx = P.Context(0)
+if os.environ.get("JIT_RESERVE"):
+    ctx.reserve(int(float(os.environ["JIT_RESERVE"]) * 2**30))
 ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=torch.float32, device="cuda").t()
 Wr = P.SparseMatrix.from_scipy(wl.W_r, ctx=ctx)
