@@ -785,6 +785,7 @@ int cpcag_ctx_create(int device, cpcag_ctx* out) {
   });
 }
 
+namespace cpcag_cuda {
 // The stream-ordered pool grows chunk by chunk while a workload's allocation
 // pattern settles, and each growth maps device memory inside the run (20-700
 // ms stalls observed over the first tens of pipeline runs).  After a major
@@ -803,6 +804,7 @@ void pool_settle(Ctx* c) {
   if (cudaMallocAsync(&p, static_cast<size_t>(want), c->stream) == cudaSuccess) cudaFreeAsync(p, c->stream);
   cudaGetLastError();
 }
+}  // namespace cpcag_cuda
 
 int cpcag_ctx_reserve(cpcag_ctx ctx, int64_t bytes) {
   return guard([&] {
