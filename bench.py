@@ -198,6 +198,10 @@ def run_ours(args, rank, local_rank, world):
     ctx = P.Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
+    # Allocator warm-up (untimed): grow the library's stream-ordered memory
+    # pool once, so the pool does not grow chunk by chunk (each growth maps
+    # device memory, measured as 100-700 ms stalls) during the first runs.
+    ctx.reserve(8 << 30)
     Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=tdt, device="cuda").t()  # col-major p x n
     Wr_sp = wl.W_r
     Wr_dev = P.SparseMatrix.from_scipy(Wr_sp, ctx=ctx)

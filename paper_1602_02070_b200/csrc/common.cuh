@@ -224,7 +224,6 @@ T read_back(Ctx* c, const T* dptr) {
 // A^T bit for bit), which lets X*A run as a pull over CSR rows in exactly the
 // reference's accumulation order (sparse.cpp:100-111).
 void* csr_malloc(Ctx* c, size_t bytes);  // stream-ordered pool (see core.cu)
-void pool_settle(Ctx* c);                  // grow the pool once to 2x the high-water mark
 
 struct Csr {
   i64 rows = 0, cols = 0, nnz = 0;

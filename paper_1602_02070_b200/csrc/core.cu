@@ -753,26 +753,6 @@ std::vector<i64> host_list(Ctx* c, const int64_t* p, int64_t n) {
 }
 }  // namespace
 
-namespace cpcag_cuda {
-// The stream-ordered pool grows chunk by chunk while a workload's allocation
-// pattern settles, and each growth maps device memory inside the run (20-700
-// ms stalls observed over the first tens of pipeline runs).  After a major
-// call the pool is grown once, in one chunk, to twice the call's high-water
-// mark whenever its reserve is below that; once settled this is two
-// attribute queries.
-void pool_settle(Ctx* c) {
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, c->device) != cudaSuccess) return;
-  unsigned long long high = 0, reserved = 0;
-  if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high) != cudaSuccess) return;
-  if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) != cudaSuccess) return;
-  const unsigned long long want = 2 * high;
-  if (reserved >= want + high) return;
-  void* p = nullptr;
-  if (cudaMallocAsync(&p, static_cast<size_t>(want), c->stream) == cudaSuccess) cudaFreeAsync(p, c->stream);
-  cudaGetLastError();
-}
-}  // namespace cpcag_cuda
 
 extern "C" {
 

@@ -1894,7 +1894,6 @@ extern "C" int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const v
                                  lambda_k1_r, lambda_k1_c, *cfg, x.d, converged, iterations);
       x.flush(c);
       sync(c);
-      pool_settle(c);
     });
   };
   if (precision == CPCAG_F64) return run(double{});

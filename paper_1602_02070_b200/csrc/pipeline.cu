@@ -217,7 +217,6 @@ extern "C" int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void*
       xt.flush(c);
       x.flush(c);
       sync(c);
-      pool_settle(c);
     });
   };
   if (precision == CPCAG_F64) return run(double{});
