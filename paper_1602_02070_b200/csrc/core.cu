@@ -565,7 +565,9 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   DevBuf<PowerState> st(c, 1);
   st.zero(c);
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
-  if (small_smem <= 200 * 1024 && A->nnz <= 4096) {
+  i64 small_nnz = 4096;  // single-CTA kernel (no grid barrier) up to this many entries
+  if (const char* e = std::getenv("CPCAG_POWER_SMALL_NNZ")) small_nnz = std::atoll(e);
+  if (small_smem <= 200 * 1024 && A->nnz <= small_nnz) {
     ensure_smem(power_iter_small_k, small_smem);
     {
       KScope ks_(c, "power_iter");

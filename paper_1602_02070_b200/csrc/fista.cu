@@ -714,6 +714,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     const unsigned tiles = gk.x * gk.y;
     unsigned S = static_cast<unsigned>(std::max<i64>(1, (4 * static_cast<i64>(c->num_sms)) / tiles));
     S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / (4 * kSK) + 1, 32}));
+    if (const char* e = std::getenv("CPCAG_FISTA_SPLITS")) S = static_cast<unsigned>(std::max(1, std::atoi(e)));
     gk.z = S;
     sp1.alloc(c, static_cast<size_t>(S) * N);
     sp2.alloc(c, static_cast<size_t>(S) * N);

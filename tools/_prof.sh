@@ -1,2 +1,2 @@
-timeout -s KILL 600 python bench.py --steps 5 --warmup 3 > gpurun_out/b73.log 2>&1; grep "\[bench\] step" gpurun_out/b73.log; tail -1 gpurun_out/b73.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['stage_ms'], d['roofline']['frac'])"
-timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/b73b.log 2>&1; grep "\[bench\] step" gpurun_out/b73b.log; tail -1 gpurun_out/b73b.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'])"
+for v in 4096 16384 65536; do CPCAG_POWER_SMALL_NNZ=$v timeout -s KILL 300 python tools/bench_stages.py 2>&1 | grep fista | cut -c1-150 | sed "s/^/small_nnz=$v /"; done
+for sp in 2 4 8 17; do CPCAG_FISTA_SPLITS=$sp timeout -s KILL 300 python tools/bench_stages.py 2>&1 | grep fista | cut -c1-150 | sed "s/^/splits=$sp /"; done

@@ -43,7 +43,7 @@ def main():
     plan = rep.plan
     dcfg = P.DecoderConfig(1.0, 1e-30, 200)
     ref = None
-    for variant in ["fast2"]:
+    for variant in []:
         os.environ["CPCAG_APPLY"] = variant
         res, wall, kt = timed(ctx, lambda: P.alternate_decode(rep.Xt, plan, gr.laplacian, gc.laplacian,
                                                                P.SpectralGap(lambda_k1=wl.lambda_k1_r),
@@ -61,7 +61,7 @@ def main():
     fcfg = P.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, 300)
     _, wall, kt = timed(ctx, lambda: P.fista_solve(Yt, Lrt, Lct, fcfg, ctx=ctx))
     print(f"fista wall {wall:8.2f} ms  " + "  ".join(f"{k}={v[1]:.2f}ms/{v[0]}" for k, v in kt.items()), flush=True)
-    for nt, sl in [("512x2", "0")]:
+    for nt, sl in []:
         os.environ["CPCAG_PCG_NT"] = nt
         if sl != "0":
             os.environ["CPCAG_KRON_SLICE"] = sl
