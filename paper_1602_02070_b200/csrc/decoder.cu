@@ -1341,6 +1341,202 @@ struct BandApply {
   }
 };
 
+// ------------------------------------------------------------------ tile apply (banded column graph)
+// When the column graph has a small bandwidth after reverse Cuthill-McKee
+// ordering (config 1: max 69, median 12 over 1 000 columns), the iterates are
+// stored with columns in RCM order and each CTA (64 rows x 64 columns)
+// stages the window P[rows, c0 - h : c0 + 64 + h] in shared memory once; the
+// ~19 L_c gathers of every output then read shared memory instead of L2.
+// L_r (the pixel grid at config 1) gathers along the same column from L1.
+// Each L_c row keeps its CSR entry order (only the column labels are mapped),
+// so the per-entry arithmetic -- and fp64 bit-exactness -- is unchanged.
+__global__ void unpermute_cols_k(i64 p, i64 n, const int* __restrict__ pos, const float* __restrict__ src32,
+                                 float* __restrict__ dst32, const double* __restrict__ src64,
+                                 double* __restrict__ dst64) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= p) return;
+  for (i64 c = blockIdx.y; c < n; c += gridDim.y) {
+    const i64 s = pos[c];
+    if (src32) dst32[i + c * p] = src32[i + s * p];
+    else dst64[i + c * p] = src64[i + s * p];
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) cg_apply_tile_k(int p, int n, Pull<T> Lr, const i64* __restrict__ crp,
+                                                       const OffEnt<T>* __restrict__ cent, const int* __restrict__ wlo,
+                                                       const int* __restrict__ whi, T gr, T gc, Plan pl,
+                                                       const T* __restrict__ P, T* __restrict__ AP,
+                                                       double* partials, CgState* st, int force) {
+  if (!force && st->done) return;
+  constexpr int kR = 64;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* Pw = reinterpret_cast<T*>(smraw);  // [window][kR]
+  const int r = threadIdx.x & (kR - 1), cgp = threadIdx.x / kR, ngp = blockDim.x / kR;
+  const int i0 = blockIdx.x * kR, i = i0 + r;
+  const int c0 = blockIdx.y * 64, c1 = min(n, c0 + 64);
+  const int w0 = wlo[blockIdx.y], w1 = whi[blockIdx.y];
+  const int rows = min(kR, p - i0);
+  for (int idx = threadIdx.x; idx < (w1 - w0) * kR; idx += blockDim.x) {
+    const int j = idx / kR, rr = idx % kR;
+    Pw[idx] = rr < rows ? P[static_cast<i64>(i0 + rr) + static_cast<i64>(w0 + j) * p] : T(0);
+  }
+  __syncthreads();
+  double s = 0.0;
+  if (i < p) {
+    const i64 a0 = Lr.rp[i], a1 = Lr.rp[i + 1];
+    const bool rs = pl.rsel[i] >= 0;
+    for (int c = c0 + cgp; c < c1; c += ngp) {
+      T x1 = T(0);
+      for (i64 k = crp[c]; k < crp[c + 1]; ++k) {
+        const OffEnt<T> e = cent[k];
+        x1 = madd_entry(x1, e.v, Pw[(e.off - w0) * kR + r]);
+      }
+      const T* pc = P + static_cast<i64>(c) * p;
+      T x2 = T(0);
+      for (i64 k = a0; k < a1; ++k) x2 = madd_entry(x2, Lr.v[k], pc[Lr.ci[k]]);
+      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
+      const T pv = Pw[(c - w0) * kR + r];
+      if (rs && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[i + static_cast<i64>(c) * p] = out;
+      s += static_cast<double>(pv) * static_cast<double>(out);
+    }
+  }
+  if (force) return;
+  double sv[1] = {s}, tot[1];
+  if (grid_sum_last<1>(sv, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
+template <typename T>
+struct TileApply {
+  static constexpr int kR = 64, kC = 64;
+  i64 p = 0, n = 0;
+  int bandwidth = 0, wmax = 0;
+  size_t smem = 0;
+  DevBuf<int> pos, wlo, whi;
+  DevBuf<i64> crp;
+  DevBuf<OffEnt<T>> cent;
+
+  // Reverse Cuthill-McKee of the symmetric pattern (per component: start at
+  // a minimum-degree node, BFS visiting neighbours by ascending degree).
+  static std::vector<int> rcm(i64 n, const std::vector<i64>& rp, const std::vector<int>& ci) {
+    std::vector<int> order, deg(static_cast<size_t>(n));
+    order.reserve(static_cast<size_t>(n));
+    for (i64 u = 0; u < n; ++u) deg[u] = static_cast<int>(rp[u + 1] - rp[u]);
+    std::vector<char> seen(static_cast<size_t>(n), 0);
+    std::vector<int> byd(static_cast<size_t>(n));
+    for (i64 u = 0; u < n; ++u) byd[u] = static_cast<int>(u);
+    std::stable_sort(byd.begin(), byd.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+    std::vector<int> nb;
+    for (int start : byd) {
+      if (seen[start]) continue;
+      size_t head = order.size();
+      order.push_back(start);
+      seen[start] = 1;
+      while (head < order.size()) {
+        const int u = order[head++];
+        nb.clear();
+        for (i64 k = rp[u]; k < rp[u + 1]; ++k)
+          if (!seen[ci[k]]) {
+            seen[ci[k]] = 1;
+            nb.push_back(ci[k]);
+          }
+        std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+        order.insert(order.end(), nb.begin(), nb.end());
+      }
+    }
+    std::reverse(order.begin(), order.end());
+    return order;  // stored position -> original column
+  }
+
+  // Returns false (and builds nothing) when the column graph is not banded
+  // enough for the shared-memory window.
+  bool build(Ctx* c, Csr* Lc, const std::vector<i64>& rpc, i64 p_, int cap) {
+    p = p_;
+    n = Lc->rows;
+    if (n > INT32_MAX || p > INT32_MAX) return false;
+    const Pull<T> pc = make_pull<T>(c, Lc, true);
+    const i64 nnz = rpc[n];
+    std::vector<int> hci(static_cast<size_t>(nnz));
+    std::vector<T> hv(static_cast<size_t>(nnz));
+    if (nnz) {
+      CUDA_OK(cudaMemcpyAsync(hci.data(), pc.ci, sizeof(int) * nnz, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OK(cudaMemcpyAsync(hv.data(), pc.v, sizeof(T) * nnz, cudaMemcpyDeviceToHost, c->stream));
+    }
+    sync(c);
+    const std::vector<int> ord = rcm(n, rpc, hci);
+    std::vector<int> hpos(static_cast<size_t>(n));
+    for (i64 k = 0; k < n; ++k) hpos[ord[k]] = static_cast<int>(k);
+    bandwidth = 0;
+    for (i64 u = 0; u < n; ++u)
+      for (i64 k = rpc[u]; k < rpc[u + 1]; ++k) bandwidth = std::max(bandwidth, std::abs(hpos[u] - hpos[hci[k]]));
+    if (bandwidth > cap) return false;
+    // permuted rows (stored column order), entry order kept, labels mapped
+    std::vector<i64> hrp(static_cast<size_t>(n) + 1, 0);
+    std::vector<OffEnt<T>> hent(static_cast<size_t>(std::max<i64>(nnz, 1)));
+    for (i64 st_ = 0; st_ < n; ++st_) {
+      const i64 u = ord[st_];
+      i64 o = hrp[st_];
+      for (i64 k = rpc[u]; k < rpc[u + 1]; ++k, ++o) {
+        hent[o].v = hv[k];
+        hent[o].off = hpos[hci[k]];
+      }
+      hrp[st_ + 1] = o;
+    }
+    const i64 chunks = (n + kC - 1) / kC;
+    std::vector<int> lo(static_cast<size_t>(chunks)), hi(static_cast<size_t>(chunks));
+    wmax = 0;
+    for (i64 b = 0; b < chunks; ++b) {
+      const i64 a = b * kC, e = std::min<i64>(n, a + kC);
+      int l = static_cast<int>(a), h = static_cast<int>(e);
+      for (i64 st_ = a; st_ < e; ++st_)
+        for (i64 k = hrp[st_]; k < hrp[st_ + 1]; ++k) {
+          l = std::min(l, hent[k].off);
+          h = std::max(h, hent[k].off + 1);
+        }
+      lo[b] = l;
+      hi[b] = h;
+      wmax = std::max(wmax, h - l);
+    }
+    smem = static_cast<size_t>(wmax) * kR * sizeof(T);
+    if (smem > 96 * 1024) return false;
+    pos.alloc(c, n);
+    wlo.alloc(c, chunks);
+    whi.alloc(c, chunks);
+    crp.alloc(c, n + 1);
+    cent.alloc(c, hent.size());
+    CUDA_OK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(wlo.p, lo.data(), sizeof(int) * chunks, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(whi.p, hi.data(), sizeof(int) * chunks, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(crp.p, hrp.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(cent.p, hent.data(), sizeof(OffEnt<T>) * hent.size(), cudaMemcpyHostToDevice, c->stream));
+    ensure_smem(cg_apply_tile_k<T>, smem);
+    sync(c);
+    return true;
+  }
+
+  dim3 grid() const {
+    return dim3(static_cast<unsigned>((p + kR - 1) / kR), static_cast<unsigned>((n + kC - 1) / kC));
+  }
+
+  void apply(Ctx* c, const Pull<T>& pr, const T* P, T* AP, const Plan& pl, T gr, T gc, double* part, CgState* st,
+             int force) const {
+    cg_apply_tile_k<T><<<grid(), 256, smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, crp.p, cent.p,
+                                                        wlo.p, whi.p, gr, gc, pl, P, AP, part, st, force);
+    launched(c);
+  }
+};
+
 template <typename T>
 void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i64* om_r_host,
                              const i64* om_c_host, i64 p, i64 n, Csr* Lr, Csr* Lc, double lk1_r,
@@ -1406,7 +1602,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 
   // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
   // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
-  std::string variant = p * n < (i64{1} << 31) ? "fast2" : "staged";
+  std::string variant = p * n < (i64{1} << 31) ? "fast3" : "staged";
   if (BandApply<T>::preferred(p, n)) variant = "band";
   if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
   if (variant == "band" && !BandApply<T>::feasible(p)) variant = "staged";
@@ -1438,6 +1634,21 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "panel" && !(panel_smem <= 220 * 1024)) variant = "staged";
   const size_t fast_smem = static_cast<size_t>(max_er + max_ec) * sizeof(OffEnt<T>) + sizeof(int) * (cols_per_cta + 2) + 16;
   if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
+  TileApply<T> tile;
+  DevBuf<int> csel_perm;
+  if (variant == "fast3") {
+    // banded column graph: RCM column order and shared-memory windows
+    if (tile.build(c, Lc, rpc, p, 128)) {
+      if (part.n < static_cast<size_t>(tile.grid().x) * tile.grid().y)
+        part.alloc(c, static_cast<size_t>(tile.grid().x) * tile.grid().y);
+      csel_perm.alloc(c, n);
+      permute_sel_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, tile.pos.p, csel.p, csel_perm.p);
+      launched(c);
+      pl.csel = csel_perm.p;
+    } else {
+      variant = "fast2";
+    }
+  }
   BandApply<T> band;
   DevBuf<int> rsel_perm;
   if (variant == "band") {
@@ -1518,6 +1729,8 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
                                                                   st.p);
         } else if (variant == "band") {
           band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
+        } else if (variant == "fast3") {
+          tile.apply(c, pr, P.p, AP.p, pl, gr, gc, part.p, st.p, 0);
         } else if (variant == "fast2") {
           cg_apply_fast2_k<T><<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr,
                                                                      gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
@@ -1544,7 +1757,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
         } else {
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         }
-        if (variant != "band") launched(c);
+        if (variant != "band" && variant != "fast3") launched(c);
       }
       {
         KScope ks_(c, "cg_residual");
@@ -1567,7 +1780,20 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     *iterations = 0;
     return;
   }
-  if (variant == "band") {
+  if (variant == "fast3") {
+    tile.apply(c, pr, X, AP.p, pl, gr, gc, part.p, st.p, 1);
+    cg_true_res_ap_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, AP.p, part.p, st.p);
+    launched(c);
+    // back to the caller's column order
+    CUDA_OK(cudaMemcpyAsync(AP.p, X, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
+    if constexpr (sizeof(T) == 4)
+      unpermute_cols_k<<<g2, kBlock, 0, c->stream>>>(p, n, tile.pos.p, reinterpret_cast<const float*>(AP.p),
+                                                     reinterpret_cast<float*>(X), nullptr, nullptr);
+    else
+      unpermute_cols_k<<<g2, kBlock, 0, c->stream>>>(p, n, tile.pos.p, nullptr, nullptr,
+                                                     reinterpret_cast<const double*>(AP.p),
+                                                     reinterpret_cast<double*>(X));
+  } else if (variant == "band") {
     band.apply(c, X, AP.p, 0, n, pl, gr, gc, part.p, st.p, 1);
     cg_true_res_ap_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, AP.p, part.p, st.p);
     if (band.permuted) {  // back to the caller's row order

@@ -43,7 +43,7 @@ def main():
     plan = rep.plan
     dcfg = P.DecoderConfig(1.0, 1e-30, 200)
     ref = None
-    for variant in []:
+    for variant in ["fast2", "fast3"]:
         os.environ["CPCAG_APPLY"] = variant
         res, wall, kt = timed(ctx, lambda: P.alternate_decode(rep.Xt, plan, gr.laplacian, gc.laplacian,
                                                                P.SpectralGap(lambda_k1=wl.lambda_k1_r),
