@@ -1371,30 +1371,57 @@ __global__ void __launch_bounds__(256) cg_apply_tile_k(int p, int n, Pull<T> Lr,
   if (!force && st->done) return;
   constexpr int kR = 64;
   extern __shared__ __align__(16) unsigned char smraw[];
-  T* Pw = reinterpret_cast<T*>(smraw);  // [window][kR]
-  const int r = threadIdx.x & (kR - 1), cgp = threadIdx.x / kR, ngp = blockDim.x / kR;
-  const int i0 = blockIdx.x * kR, i = i0 + r;
+  const int i0 = blockIdx.x * kR;
   const int c0 = blockIdx.y * 64, c1 = min(n, c0 + 64);
   const int w0 = wlo[blockIdx.y], w1 = whi[blockIdx.y];
   const int rows = min(kR, p - i0);
+  // shared: window P[rows][w0:w1) | L_c entries (offset pre-scaled) | L_r entries | chunk row ptrs
+  T* Pw = reinterpret_cast<T*>(smraw);
+  const i64 kc_base = crp[c0];
+  const int ec = static_cast<int>(crp[c1] - kc_base);
+  const i64 kr_base = Lr.rp[i0];
+  const int er = static_cast<int>(Lr.rp[i0 + rows] - kr_base);
+  OffEnt<T>* Ec = reinterpret_cast<OffEnt<T>*>(smraw + static_cast<size_t>(w1 - w0) * kR * sizeof(T));
+  OffEnt<T>* Er = Ec + ec;
+  int* cr = reinterpret_cast<int*>(Er + er);  // 65 entries
   for (int idx = threadIdx.x; idx < (w1 - w0) * kR; idx += blockDim.x) {
     const int j = idx / kR, rr = idx % kR;
     Pw[idx] = rr < rows ? P[static_cast<i64>(i0 + rr) + static_cast<i64>(w0 + j) * p] : T(0);
   }
+  for (int k = threadIdx.x; k < ec; k += blockDim.x) {
+    OffEnt<T> e = cent[kc_base + k];
+    e.off = (e.off - w0) * kR;
+    Ec[k] = e;
+  }
+  for (int k = threadIdx.x; k < er; k += blockDim.x) {
+    OffEnt<T> e;
+    e.v = Lr.v[kr_base + k];
+    e.off = Lr.ci[kr_base + k];
+    Er[k] = e;
+  }
+  for (int q = threadIdx.x; q <= c1 - c0; q += blockDim.x) cr[q] = static_cast<int>(crp[c0 + q] - kc_base);
   __syncthreads();
+  const int r = threadIdx.x & (kR - 1), cgp = threadIdx.x / kR, ngp = blockDim.x / kR;
+  const int i = i0 + r;
   double s = 0.0;
-  if (i < p) {
-    const i64 a0 = Lr.rp[i], a1 = Lr.rp[i + 1];
+  if (r < rows) {
+    const int a0 = static_cast<int>(Lr.rp[i] - kr_base), a1 = static_cast<int>(Lr.rp[i + 1] - kr_base);
     const bool rs = pl.rsel[i] >= 0;
     for (int c = c0 + cgp; c < c1; c += ngp) {
       T x1 = T(0);
-      for (i64 k = crp[c]; k < crp[c + 1]; ++k) {
-        const OffEnt<T> e = cent[k];
-        x1 = madd_entry(x1, e.v, Pw[(e.off - w0) * kR + r]);
+      const int b0 = cr[c - c0], b1 = cr[c - c0 + 1];
+#pragma unroll 4
+      for (int k = b0; k < b1; ++k) {
+        const OffEnt<T> e = Ec[k];
+        x1 = madd_entry(x1, e.v, Pw[e.off + r]);
       }
       const T* pc = P + static_cast<i64>(c) * p;
       T x2 = T(0);
-      for (i64 k = a0; k < a1; ++k) x2 = madd_entry(x2, Lr.v[k], pc[Lr.ci[k]]);
+#pragma unroll 4
+      for (int k = a0; k < a1; ++k) {
+        const OffEnt<T> e = Er[k];
+        x2 = madd_entry(x2, e.v, pc[e.off]);
+      }
       T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
       const T pv = Pw[(c - w0) * kR + r];
       if (rs && pl.csel[c] >= 0) out = add_rn(out, pv);
@@ -1461,7 +1488,7 @@ struct TileApply {
 
   // Returns false (and builds nothing) when the column graph is not banded
   // enough for the shared-memory window.
-  bool build(Ctx* c, Csr* Lc, const std::vector<i64>& rpc, i64 p_, int cap) {
+  bool build(Ctx* c, Csr* Lc, const std::vector<i64>& rpc, const std::vector<i64>& rpr_, i64 p_, int cap) {
     p = p_;
     n = Lc->rows;
     if (n > INT32_MAX || p > INT32_MAX) return false;
@@ -1508,7 +1535,11 @@ struct TileApply {
       hi[b] = h;
       wmax = std::max(wmax, h - l);
     }
-    smem = static_cast<size_t>(wmax) * kR * sizeof(T);
+    i64 mec = 0, mer = 0;
+    for (i64 b = 0; b < chunks; ++b) mec = std::max(mec, hrp[std::min<i64>(n, b * kC + kC)] - hrp[b * kC]);
+    for (i64 a = 0; a < p; a += kR) mer = std::max(mer, rpr_[std::min<i64>(p, a + kR)] - rpr_[a]);
+    smem = static_cast<size_t>(wmax) * kR * sizeof(T) + static_cast<size_t>(mec + mer) * sizeof(OffEnt<T>) +
+           sizeof(int) * (kC + 1) + 16;
     if (smem > 96 * 1024) return false;
     pos.alloc(c, n);
     wlo.alloc(c, chunks);
@@ -1638,7 +1669,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   DevBuf<int> csel_perm;
   if (variant == "fast3") {
     // banded column graph: RCM column order and shared-memory windows
-    if (tile.build(c, Lc, rpc, p, 128)) {
+    if (tile.build(c, Lc, rpc, rpr, p, 128)) {
       if (part.n < static_cast<size_t>(tile.grid().x) * tile.grid().y)
         part.alloc(c, static_cast<size_t>(tile.grid().x) * tile.grid().y);
       csel_perm.alloc(c, n);
