@@ -1633,7 +1633,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
 
   // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
   // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
-  std::string variant = p * n < (i64{1} << 31) ? "fast3" : "staged";
+  // fast2 by default for L2-sized iterates; fast3 (RCM column windows in
+  // shared memory, CPCAG_APPLY=fast3) measured slower at config 1 (39.9 vs
+  // 29.1 ms per 224 applies): the window staging and its occupancy cost
+  // more than the L2 gathers it saves at this size.
+  std::string variant = p * n < (i64{1} << 31) ? "fast2" : "staged";
   if (BandApply<T>::preferred(p, n)) variant = "band";
   if (const char* e = std::getenv("CPCAG_APPLY")) variant = e;
   if (variant == "band" && !BandApply<T>::feasible(p)) variant = "staged";
