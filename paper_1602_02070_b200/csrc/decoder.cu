@@ -120,112 +120,6 @@ __global__ void cg_apply_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Pla
   }
 }
 
-template <typename T>
-struct alignas(sizeof(T) == 8 ? 16 : 8) LcEnt {
-  T v;
-  int ci;
-};
-
-// Two-kernel apply (HBM-friendly; used when the panels fit in shared memory):
-//  cg_apply_lr_k  Yr = L_r P      CTA = kLrCols columns x all p rows; the
-//                                 columns are staged in shared memory, so the
-//                                 L_r gathers are shared-memory loads and each
-//                                 CSR entry is read once for kLrCols columns.
-//  cg_apply_lc_k  AP = gc (P L_c) + gr Yr (+ P on the sampled grid), <P, AP>
-//                 CTA = a 32-row panel x all n columns staged in shared memory
-//                 (row-major, padded), lane = row, warp = column; the L_c
-//                 row of each column is read with one coalesced load per 32
-//                 entries and broadcast from shared memory.
-// Per-entry operation order is the reference's (bit-identical to cg_apply_k).
-constexpr int kLrCols = 4;
-constexpr int kPanel = 32;
-
-template <typename T>
-__global__ void __launch_bounds__(512) cg_apply_lr_k(i64 p, i64 n, Pull<T> Lr, const T* __restrict__ P,
-                                                     T* __restrict__ Yr, const CgState* st) {
-  if (st->done) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  T* Ps = reinterpret_cast<T*>(smraw);  // kLrCols x p
-  const i64 c0 = static_cast<i64>(blockIdx.x) * kLrCols;
-  const int nc = static_cast<int>(min(static_cast<i64>(kLrCols), n - c0));
-  for (int q = 0; q < nc; ++q)
-    for (i64 i = threadIdx.x; i < p; i += blockDim.x) Ps[q * p + i] = P[i + (c0 + q) * p];
-  __syncthreads();
-  for (i64 i = threadIdx.x; i < p; i += blockDim.x) {
-    T acc[kLrCols];
-#pragma unroll
-    for (int q = 0; q < kLrCols; ++q) acc[q] = T(0);
-    for (i64 k = Lr.rp[i]; k < Lr.rp[i + 1]; ++k) {
-      const T v = Lr.v[k];
-      const int j = Lr.ci[k];
-#pragma unroll
-      for (int q = 0; q < kLrCols; ++q)
-        if (q < nc) acc[q] = add_rn(acc[q], mul_rn(v, Ps[q * p + j]));
-    }
-#pragma unroll
-    for (int q = 0; q < kLrCols; ++q)
-      if (q < nc) Yr[i + (c0 + q) * p] = acc[q];
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) cg_apply_lc_k(i64 p, i64 n, Pull<T> Lc, T gr, T gc, Plan pl,
-                                                     const T* __restrict__ P, const T* __restrict__ Yr,
-                                                     T* __restrict__ AP, double* partials, CgState* st) {
-  if (st->done) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  LcEnt<T>* ents = reinterpret_cast<LcEnt<T>*>(smraw);     // nw x 32 staging of L_c rows
-  T* Ps = reinterpret_cast<T*>(ents + nw * 32);             // n x (kPanel + 1)
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kPanel;
-  const i64 i = i0 + lane;
-  const bool in = i < p;
-  for (i64 c = wid; c < n; c += nw) Ps[c * (kPanel + 1) + lane] = in ? P[i + c * p] : T(0);
-  __syncthreads();
-  const bool row_sampled = in && pl.rsel[i] >= 0;
-  double s[1] = {0.0};
-  LcEnt<T>* mine = ents + wid * 32;
-  for (i64 c = wid; c < n; c += nw) {
-    const i64 k0 = Lc.rp[c], k1 = Lc.rp[c + 1];
-    T x1 = T(0);
-    for (i64 kb = k0; kb < k1; kb += 32) {
-      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - kb));
-      if (lane < cnt) {
-        LcEnt<T> e;
-        e.v = Lc.v[kb + lane];
-        e.ci = Lc.ci[kb + lane];
-        mine[lane] = e;
-      }
-      __syncwarp();
-      for (int k = 0; k < cnt; ++k) {
-        const LcEnt<T> e = mine[k];
-        x1 = add_rn(x1, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanel + 1) + lane]));
-      }
-      __syncwarp();
-    }
-    if (in) {
-      const i64 at = i + c * p;
-      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, Yr[at]));
-      const T pv = Ps[c * (kPanel + 1) + lane];
-      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
-      AP[at] = out;
-      s[0] += static_cast<double>(pv) * static_cast<double>(out);
-    }
-  }
-  double tot[1];
-  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
-    const double curv = tot[0];
-    st->curv = curv;
-    if (!isfinite(curv) || curv <= 0.0) {
-      st->err = 1;
-      st->err_it = st->it;
-      st->done = 1;
-      return;
-    }
-    st->alpha = st->rho / curv;
-  }
-}
-
 // Staged variant of cg_apply_k: a CTA owns rows [i0, i0 + 256) and a
 // contiguous chunk of columns [cb, ce).  The CSR rows of L_r for its rows and
 // of L_c for its columns are copied into shared memory once, so the inner
@@ -293,205 +187,6 @@ __global__ void __launch_bounds__(256) cg_apply_staged_k(i64 p, i64 c_lo, i64 c_
 }
 
 
-
-template <typename T, int kRmax>
-__global__ void __launch_bounds__(256, 2) cg_apply_reg_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
-                                                      i64 cols_per_cta, const T* __restrict__ P,
-                                                      T* __restrict__ AP, double* partials, CgState* st) {
-  if (st->done) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  LcEnt<T>* ent = reinterpret_cast<LcEnt<T>*>(smraw);
-  const i64 i0 = static_cast<i64>(blockIdx.x) * blockDim.x;
-  const i64 cb = static_cast<i64>(blockIdx.y) * cols_per_cta;
-  const i64 ce = min(n, cb + cols_per_cta);
-  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0, ec = cb < ce ? Lc.rp[ce] - kc_base : 0;
-  for (i64 k = threadIdx.x; k < ec; k += blockDim.x) {
-    LcEnt<T> e;
-    e.v = Lc.v[kc_base + k];
-    e.ci = Lc.ci[kc_base + k];
-    ent[k] = e;
-  }
-  const i64 i = i0 + threadIdx.x;
-  T rv[kRmax];
-  int rc[kRmax];
-  int rlen = 0;
-  i64 ra = 0;
-  bool row_sampled = false;
-  if (i < p) {
-    ra = Lr.rp[i];
-    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
-#pragma unroll
-    for (int k = 0; k < kRmax; ++k) {
-      rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
-      rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
-    }
-    row_sampled = pl.rsel[i] >= 0;
-  }
-  __syncthreads();
-  double s[1] = {0.0};
-  if (i < p) {
-    for (i64 c = cb; c < ce; ++c) {
-      const i64 b0 = Lc.rp[c] - kc_base, b1 = Lc.rp[c + 1] - kc_base;
-      T x1 = T(0);
-      for (i64 k = b0; k < b1; ++k) {
-        const LcEnt<T> e = ent[k];
-        x1 = add_rn(x1, mul_rn(e.v, P[i + static_cast<i64>(e.ci) * p]));
-      }
-      const T* pc = P + c * p;
-      T x2 = T(0);
-      if (rlen <= kRmax) {
-#pragma unroll
-        for (int k = 0; k < kRmax; ++k)
-          if (k < rlen) x2 = add_rn(x2, mul_rn(rv[k], pc[rc[k]]));
-      } else {
-        for (i64 k = ra; k < ra + rlen; ++k) x2 = add_rn(x2, mul_rn(Lr.v[k], pc[Lr.ci[k]]));
-      }
-      T out = add_rn(mul_rn(gc, x1), mul_rn(gr, x2));
-      const T pv = pc[i];
-      if (row_sampled && pl.csel[c] >= 0) out = add_rn(out, pv);
-      AP[i + c * p] = out;
-      s[0] += static_cast<double>(pv) * static_cast<double>(out);
-    }
-  }
-  double tot[1];
-  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
-    const double curv = tot[0];
-    st->curv = curv;
-    if (!isfinite(curv) || curv <= 0.0) {
-      st->err = 1;
-      st->err_it = st->it;
-      st->done = 1;
-      return;
-    }
-    st->alpha = st->rho / curv;
-  }
-}
-
-// Fused row-panel apply ("panel"): a CTA owns 32 consecutive rows and every
-// column.  P(i0:i0+32, :) is staged in shared memory (row-major per column,
-// padded), lane = row, warp = column; each warp handles two columns at a
-// time for ILP.  X L_c reads its neighbour columns from the panel (one
-// conflict-free shared load per entry); L_r P reads the lane's L_r row from
-// registers (loaded once) and gathers P(j, c) from global memory (coalesced
-// along the lane's consecutive rows for stencil-like graphs).
-constexpr int kPanelRows = 32;
-constexpr int kPanelRmax = 16;
-
-template <typename T>
-__global__ void __launch_bounds__(512, 1) cg_apply_panel_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
-                                                            Plan pl, const T* __restrict__ P, T* __restrict__ AP,
-                                                            double* partials, CgState* st) {
-  if (st->done) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  LcEnt<T>* ents = reinterpret_cast<LcEnt<T>*>(smraw);  // nw x 2 x 32
-  T* Ps = reinterpret_cast<T*>(ents + nw * 64);          // n x (32 + 1)
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kPanelRows;
-  const i64 i = i0 + lane;
-  const bool in = i < p;
-  for (i64 c = wid; c < n; c += nw) Ps[c * (kPanelRows + 1) + lane] = in ? P[i + c * p] : T(0);
-  T rv[kPanelRmax];
-  int rc[kPanelRmax];
-  int rlen = 0;
-  i64 ra = 0;
-  if (in) {
-    ra = Lr.rp[i];
-    rlen = static_cast<int>(Lr.rp[i + 1] - ra);
-  }
-#pragma unroll
-  for (int k = 0; k < kPanelRmax; ++k) {
-    rv[k] = k < rlen ? Lr.v[ra + k] : T(0);
-    rc[k] = k < rlen ? Lr.ci[ra + k] : 0;
-  }
-  __syncthreads();
-  const bool row_sampled = in && pl.rsel[i] >= 0;
-  LcEnt<T>* mine = ents + wid * 64;
-  double s[1] = {0.0};
-  for (i64 cA = wid; cA < n; cA += 2 * nw) {
-    const i64 cB = cA + nw;
-    const bool hasB = cB < n;
-    const i64 a0 = Lc.rp[cA], a1 = Lc.rp[cA + 1];
-    const i64 b0 = hasB ? Lc.rp[cB] : 0, b1 = hasB ? Lc.rp[cB + 1] : 0;
-    T xA = T(0), xB = T(0);
-    i64 ka = a0, kb = b0;
-    while (ka < a1 || kb < b1) {
-      const int cntA = static_cast<int>(min(static_cast<i64>(32), a1 - ka));
-      const int cntB = static_cast<int>(min(static_cast<i64>(32), b1 - kb));
-      if (lane < cntA) {
-        LcEnt<T> e;
-        e.v = Lc.v[ka + lane];
-        e.ci = Lc.ci[ka + lane];
-        mine[lane] = e;
-      }
-      if (lane < cntB) {
-        LcEnt<T> e;
-        e.v = Lc.v[kb + lane];
-        e.ci = Lc.ci[kb + lane];
-        mine[32 + lane] = e;
-      }
-      __syncwarp();
-      const int cmax = cntA > cntB ? cntA : cntB;
-      for (int k = 0; k < cmax; ++k) {
-        if (k < cntA) {
-          const LcEnt<T> e = mine[k];
-          xA = add_rn(xA, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanelRows + 1) + lane]));
-        }
-        if (k < cntB) {
-          const LcEnt<T> e = mine[32 + k];
-          xB = add_rn(xB, mul_rn(e.v, Ps[static_cast<i64>(e.ci) * (kPanelRows + 1) + lane]));
-        }
-      }
-      __syncwarp();
-      ka += cntA > 0 ? cntA : 0;
-      kb += cntB > 0 ? cntB : 0;
-    }
-    if (in) {
-      // L_r P for both columns, CSR order per row
-      const T* pA = P + cA * p;
-      const T* pB = P + (hasB ? cB : cA) * p;
-      T yA = T(0), yB = T(0);
-      if (rlen <= kPanelRmax) {
-#pragma unroll
-        for (int k = 0; k < kPanelRmax; ++k)
-          if (k < rlen) {
-            yA = add_rn(yA, mul_rn(rv[k], pA[rc[k]]));
-            yB = add_rn(yB, mul_rn(rv[k], pB[rc[k]]));
-          }
-      } else {
-        for (i64 k = ra; k < ra + rlen; ++k) {
-          yA = add_rn(yA, mul_rn(Lr.v[k], pA[Lr.ci[k]]));
-          yB = add_rn(yB, mul_rn(Lr.v[k], pB[Lr.ci[k]]));
-        }
-      }
-      {
-        T out = add_rn(mul_rn(gc, xA), mul_rn(gr, yA));
-        const T pv = Ps[cA * (kPanelRows + 1) + lane];
-        if (row_sampled && pl.csel[cA] >= 0) out = add_rn(out, pv);
-        AP[i + cA * p] = out;
-        s[0] += static_cast<double>(pv) * static_cast<double>(out);
-      }
-      if (hasB) {
-        T out = add_rn(mul_rn(gc, xB), mul_rn(gr, yB));
-        const T pv = Ps[cB * (kPanelRows + 1) + lane];
-        if (row_sampled && pl.csel[cB] >= 0) out = add_rn(out, pv);
-        AP[i + cB * p] = out;
-        s[0] += static_cast<double>(pv) * static_cast<double>(out);
-      }
-    }
-  }
-  double tot[1];
-  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
-    const double curv = tot[0];
-    st->curv = curv;
-    if (!isfinite(curv) || curv <= 0.0) {
-      st->err = 1;
-      st->err_it = st->it;
-      st->done = 1;
-      return;
-    }
-    st->alpha = st->rho / curv;
-  }
-}
 
 // Lean variant of the staged apply (default when p * n < 2^31): the staged
 // entries carry 32-bit element offsets (L_c: ci * p, L_r: ci), so a gather
@@ -802,14 +497,9 @@ __device__ __forceinline__ void store_stream(T* p, T v) {
   __stcs(p, v);
 }
 
-// Warp per column, lane = row.  Two variants (CPCAG_BAND_V):
-//  1  entries read per step (warp-uniform loads), 4 steps unrolled;
-//     32 registers, full occupancy;
-//  2/3 the column's entries loaded with one coalesced load (lane t holds
-//     entry t) and broadcast by shuffle, the next column's entries
-//     prefetched while this column gathers; 8 steps in flight
-//     (2: 64 registers, 3: 40 registers).
-// U is stored evict-first so it does not push the band out of L2.
+// Warp per column, lane = row; the column's entries are read per step
+// (warp-uniform loads, 4 steps in flight).  Shuffle-broadcast and
+// next-column-prefetch variants measured slower (lower occupancy).
 template <typename T, int RPL>
 __device__ __forceinline__ void band_column_simple(const OffEnt<T>* __restrict__ ent, i64 k0, i64 k1,
                                                    const T* __restrict__ P, i64 p, i64 r0, const bool (&ok)[RPL],
@@ -824,8 +514,9 @@ __device__ __forceinline__ void band_column_simple(const OffEnt<T>* __restrict__
   }
 }
 
-template <typename T, int RPL, int V>
-__global__ void __launch_bounds__(256, (V == 1 || V == 4) ? 8 : (V == 2 ? 4 : (V == 3 ? 6 : 1)))
+// U is stored evict-first so it does not push the band out of L2.
+template <typename T, int RPL>
+__global__ void __launch_bounds__(256, 8)
     cg_apply_band_k(i64 p, i64 c_lo, i64 c_hi, const i64* __restrict__ rp, const OffEnt<T>* __restrict__ ent, T gc,
                     i64 cols_per_cta, const T* __restrict__ P, T* __restrict__ U, const CgState* st, int force) {
   if (!force && st->done) return;
@@ -836,29 +527,9 @@ __global__ void __launch_bounds__(256, (V == 1 || V == 4) ? 8 : (V == 2 ? 4 : (V
   bool ok[RPL];
 #pragma unroll
   for (int t = 0; t < RPL; ++t) ok[t] = r0 + 32 * t < p;
-  if constexpr (V == 5) {  // plain: per-column row pointers, plain stores
-    for (i64 c = cb + warp; c < ce; c += nw) {
-      T acc[RPL];
-#pragma unroll
-      for (int t = 0; t < RPL; ++t) acc[t] = T(0);
-      band_column_simple<T, RPL>(ent, rp[c], rp[c + 1], P, p, r0, ok, acc);
-      T* out = U + c * p + r0;
-#pragma unroll
-      for (int t = 0; t < RPL; ++t)
-        if (ok[t]) out[32 * t] = mul_rn(gc, acc[t]);
-    }
-    return;
-  }
   // Row pointers of this warp's columns (lane m holds column cb + warp + m*nw).
   const i64 cm = cb + warp + static_cast<i64>(lane) * nw;
   const i64 my_k0 = cm < ce ? rp[cm] : 0, my_k1 = cm < ce ? rp[cm + 1] : 0;
-  OffEnt<T> nxt;
-  nxt.v = T(0);
-  nxt.off = 0;
-  if (V != 1) {
-    const i64 k0 = __shfl_sync(0xffffffffu, my_k0, 0), k1 = __shfl_sync(0xffffffffu, my_k1, 0);
-    if (k0 + lane < k1) nxt = ent[k0 + lane];
-  }
   for (int m = 0;; ++m) {
     const i64 c = cb + warp + static_cast<i64>(m) * nw;
     if (c >= ce) break;
@@ -866,39 +537,11 @@ __global__ void __launch_bounds__(256, (V == 1 || V == 4) ? 8 : (V == 2 ? 4 : (V
     T acc[RPL];
 #pragma unroll
     for (int t = 0; t < RPL; ++t) acc[t] = T(0);
-    if constexpr (V == 1 || V == 4) {
-      band_column_simple<T, RPL>(ent, k0, k1, P, p, r0, ok, acc);
-    } else {
-      const OffEnt<T> mine = nxt;
-      {  // prefetch the next column's first 32 entries
-        const i64 n0 = __shfl_sync(0xffffffffu, my_k0, (m + 1) & 31);
-        const i64 n1 = __shfl_sync(0xffffffffu, my_k1, (m + 1) & 31);
-        nxt.v = T(0);
-        nxt.off = 0;
-        if (c + nw < ce && n0 + lane < n1) nxt = ent[n0 + lane];
-      }
-      const int cnt = static_cast<int>(min(static_cast<i64>(32), k1 - k0));
-#pragma unroll 8
-      for (int q = 0; q < cnt; ++q) {
-        const int j = __shfl_sync(0xffffffffu, mine.off, q);
-        const T v = __shfl_sync(0xffffffffu, mine.v, q);
-        const T* col = P + static_cast<i64>(j) * p + r0;
-#pragma unroll
-        for (int t = 0; t < RPL; ++t)
-          if (ok[t]) acc[t] = madd_entry(acc[t], v, col[32 * t]);
-      }
-      if (k1 - k0 > 32) band_column_simple<T, RPL>(ent, k0 + 32, k1, P, p, r0, ok, acc);
-    }
+    band_column_simple<T, RPL>(ent, k0, k1, P, p, r0, ok, acc);
     T* out = U + c * p + r0;
 #pragma unroll
-    for (int t = 0; t < RPL; ++t) {
-      if (ok[t]) {
-        if constexpr (V == 4)
-          out[32 * t] = mul_rn(gc, acc[t]);
-        else
-          __stcs(out + 32 * t, mul_rn(gc, acc[t]));
-      }
-    }
+    for (int t = 0; t < RPL; ++t)
+      if (ok[t]) __stcs(out + 32 * t, mul_rn(gc, acc[t]));
   }
 }
 
@@ -1107,7 +750,7 @@ struct BandApply {
   static constexpr i64 kBandBytes = i64{128} << 20;  // band budget (measured: taller bands win even past L2)
   static constexpr int kColsPerCta = 64;
   i64 p = 0, n = 0;
-  int rpl = 1, rb = 32, band_v = 1, col_nt = 1024;
+  int rpl = 1, rb = 32, col_nt = 1024;
   size_t col_smem = 0;
 
   template <typename F>
@@ -1117,19 +760,10 @@ struct BandApply {
     else if (col_nt == 1024) f(cg_apply_col_k<T, 16, 1024>);
     else f(cg_apply_col_k<T, 16, 512>);
   }
-  template <int RPL, int V>
-  void launch_band(Ctx* c, dim3 gb, const T* P, T* AP, i64 c_lo, i64 c_hi, T gc, const CgState* st, int force) const {
-    cg_apply_band_k<T, RPL, V><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st,
-                                                          force);
-  }
   template <int RPL>
   void launch_band_v(Ctx* c, dim3 gb, const T* P, T* AP, i64 c_lo, i64 c_hi, T gc, const CgState* st,
                      int force) const {
-    if (band_v == 2) launch_band<RPL, 2>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
-    else if (band_v == 3) launch_band<RPL, 3>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
-    else if (band_v == 4) launch_band<RPL, 4>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
-    else if (band_v == 5) launch_band<RPL, 5>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
-    else launch_band<RPL, 1>(c, gb, P, AP, c_lo, c_hi, gc, st, force);
+    cg_apply_band_k<T, RPL><<<gb, 256, 0, c->stream>>>(p, c_lo, c_hi, rpc, ent.p, gc, kColsPerCta, P, AP, st, force);
   }
   DevBuf<OffEnt<T>> ent, ell;
   DevBuf<int> base, order, pos, vrow, vdeg, vslot, split_row, split_first, split_n;
@@ -1303,7 +937,6 @@ struct BandApply {
     col_smem = static_cast<size_t>(p) * rb + static_cast<size_t>(nslots) * rb +
                sizeof(double) * static_cast<size_t>(groups + ns);
     if (col_smem > 220 * 1024) invalid("band apply: column group and split partials exceed shared memory");
-    if (const char* e = std::getenv("CPCAG_BAND_V")) band_v = std::max(1, std::min(5, std::atoi(e)));
     if (const char* e = std::getenv("CPCAG_BAND_NT")) col_nt = std::atoi(e) == 512 ? 512 : 1024;
     with_col_kernel([&](auto kern) { ensure_smem(kern, col_smem); });
     sync(c);  // hb must outlive the copy
@@ -1631,8 +1264,8 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned nb1 = stride_blocks(c, N);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
-  // Apply variant: "staged" (default), "reg" (L_r row in registers), "split"
-  // (two kernels, shared-memory panels) or "plain"; CPCAG_APPLY overrides.
+  // Apply variant (CPCAG_APPLY overrides): fast2 | fast | fast3 | staged |
+  // plain for L2-sized iterates, band for iterates larger than L2.
   // fast2 by default for L2-sized iterates; fast3 (RCM column windows in
   // shared memory, CPCAG_APPLY=fast3) measured slower at config 1 (39.9 vs
   // 29.1 ms per 224 applies): the window staging and its occupancy cost
@@ -1650,23 +1283,16 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const i64 cols_per_cta = std::max<i64>({i64{1}, std::min<i64>((n + g2.y - 1) / g2.y, 128), (n + 65534) / 65535});
   const dim3 gs(gx, static_cast<unsigned>(std::min<i64>((n + cols_per_cta - 1) / cols_per_cta, 65535)));
   if (part.n < static_cast<size_t>(gs.x) * gs.y) part.alloc(c, static_cast<size_t>(gs.x) * gs.y);
-  i64 max_er = 0, max_ec = 0, max_row = 0;
+  i64 max_er = 0, max_ec = 0;
   for (unsigned b = 0; b < gx; ++b) {
     const i64 a = static_cast<i64>(b) * kBlock, e = std::min<i64>(p, a + kBlock);
     max_er = std::max(max_er, rpr[e] - rpr[a]);
   }
-  for (i64 r = 0; r < p; ++r) max_row = std::max(max_row, rpr[r + 1] - rpr[r]);
   for (unsigned b = 0; b < gs.y; ++b) {
     const i64 a = static_cast<i64>(b) * cols_per_cta, e = std::min<i64>(n, a + cols_per_cta);
     max_ec = std::max(max_ec, rpc[e] - rpc[a]);
   }
   const size_t staged_smem = static_cast<size_t>(max_er + max_ec) * (sizeof(T) + sizeof(int)) + 16;
-  const size_t reg_smem = static_cast<size_t>(max_ec) * sizeof(LcEnt<T>) + 16;
-  const size_t lr_smem = static_cast<size_t>(kLrCols) * p * sizeof(T);
-  const size_t lc_smem = 8 * 32 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanel + 1) * sizeof(T);
-  const size_t panel_smem = 16 * 64 * sizeof(LcEnt<T>) + static_cast<size_t>(n) * (kPanelRows + 1) * sizeof(T);
-  const unsigned panel_blocks = static_cast<unsigned>((p + kPanelRows - 1) / kPanelRows);
-  if (variant == "panel" && !(panel_smem <= 220 * 1024)) variant = "staged";
   const size_t fast_smem = static_cast<size_t>(max_er + max_ec) * sizeof(OffEnt<T>) + sizeof(int) * (cols_per_cta + 2) + 16;
   if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
   TileApply<T> tile;
@@ -1723,31 +1349,8 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     else ensure_smem(cg_apply_fast2_k<T>, fast2_smem);
     if (part.n < static_cast<size_t>(gs2.x) * gs2.y) part.alloc(c, static_cast<size_t>(gs2.x) * gs2.y);
   }
-  if (variant == "panel") {
-    ensure_smem(cg_apply_panel_k<T>, panel_smem);
-    if (part.n < panel_blocks) part.alloc(c, panel_blocks);
-  }
-  if (variant == "split" && !(lr_smem <= 200 * 1024 && lc_smem <= 200 * 1024)) variant = "staged";
-  if (variant == "reg" && !(max_row <= 32 && reg_smem <= 96 * 1024)) variant = "staged";
   if (variant == "staged" && !(staged_smem <= 96 * 1024)) variant = "plain";
-  const bool split = variant == "split";
-  DevBuf<T> Yr;
-  const unsigned lr_blocks = static_cast<unsigned>((n + kLrCols - 1) / kLrCols);
-  const unsigned lc_blocks = static_cast<unsigned>((p + kPanel - 1) / kPanel);
-  if (split) {
-    Yr.alloc(c, N);
-    ensure_smem(cg_apply_lr_k<T>, lr_smem);
-    ensure_smem(cg_apply_lc_k<T>, lc_smem);
-    if (part.n < lc_blocks) part.alloc(c, lc_blocks);
-  } else if (variant == "staged") {
-    ensure_smem(cg_apply_staged_k<T>, staged_smem);
-  }
-  auto launch_reg = [&](auto rmax_tag) {
-    constexpr int R = decltype(rmax_tag)::value;
-    ensure_smem(cg_apply_reg_k<T, R>, reg_smem);
-    cg_apply_reg_k<T, R><<<gs, kBlock, reg_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, cols_per_cta, P.p, AP.p,
-                                                              part.p, st.p);
-  };
+  if (variant == "staged") ensure_smem(cg_apply_staged_k<T>, staged_smem);
 
   cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
   launched(c);
@@ -1757,12 +1360,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
     for (i64 k = 0; k < chunk; ++k) {
       {
         KScope ks_(c, "cg_apply");
-        if (split) {
-          cg_apply_lr_k<T><<<lr_blocks, 512, lr_smem, c->stream>>>(p, n, pr, P.p, Yr.p, st.p);
-          launched(c);
-          cg_apply_lc_k<T><<<lc_blocks, 256, lc_smem, c->stream>>>(p, n, pc, gr, gc, pl, P.p, Yr.p, AP.p, part.p,
-                                                                  st.p);
-        } else if (variant == "band") {
+        if (variant == "band") {
           band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
         } else if (variant == "fast3") {
           tile.apply(c, pr, P.p, AP.p, pl, gr, gc, part.p, st.p, 0);
@@ -1774,21 +1372,9 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           cg_apply_fast_k<T><<<gs, kBlock, fast_smem, c->stream>>>(static_cast<int>(p), 0, static_cast<int>(n), pr, pc,
                                                                   gr, gc, pl, static_cast<int>(cols_per_cta), P.p, AP.p,
                                                                   part.p, st.p);
-        } else if (variant == "panel") {
-          cg_apply_panel_k<T><<<panel_blocks, 512, panel_smem, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p,
-                                                                            part.p, st.p);
         } else if (variant == "staged") {
           cg_apply_staged_k<T><<<gs, kBlock, staged_smem, c->stream>>>(p, 0, n, pr, pc, gr, gc, pl, cols_per_cta, P.p,
                                                                       AP.p, part.p, st.p);
-        } else if (variant == "reg") {
-          if (max_row <= 8)
-            launch_reg(std::integral_constant<int, 8>{});
-          else if (max_row <= 12)
-            launch_reg(std::integral_constant<int, 12>{});
-          else if (max_row <= 20)
-            launch_reg(std::integral_constant<int, 20>{});
-          else
-            launch_reg(std::integral_constant<int, 32>{});
         } else {
           cg_apply_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, P.p, AP.p, part.p, st.p);
         }
