@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="compute in fp64 (config 1 is fp32)")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--sharded", action="store_true",
+                    help="cfg3 through the column-sharded decoder over NCCL (one column block per rank)")
     ap.add_argument("--config", choices=["cfg1", "cfg2", "cfg3"], default="cfg1",
                     help="cfg1 (default, the headline): full CPCA; cfg2: kNN graph alone; cfg3: decoder at scale")
     return ap.parse_args()
@@ -585,13 +587,86 @@ def run_cfg3(args):
     print(json.dumps(out), flush=True)
 
 
+def run_cfg3_sharded(args, rank, local_rank, world):
+    """cfg3 through alternate_decode_sharded: rank g owns columns
+    [g w, (g + 1) w) of the 4096 x 200 000 iterate, the search direction is
+    all-gathered and the CG dots all-reduced over NCCL every iteration
+    (SURVEY §8e).  Strong scaling: the problem is fixed, value = seconds per
+    decode (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1602_02070_b200 as P
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200 import workloads
+    from paper_1602_02070_b200.sharded import (CudaBlockBackend, TorchCollectives, alternate_decode_sharded,
+                                               column_blocks)
+
+    torch.cuda.set_device(local_rank)
+    if "MASTER_ADDR" not in os.environ:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+    Pr, Pc = workloads.config3_points()
+    p, n = Pr.shape[1], Pc.shape[1]
+    ctx = P.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.reserve(16 << 30)
+    gr = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    gc = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
+    rs = np.random.default_rng(1606)
+    Xt = torch.tensor(rs.standard_normal((len(plan.omega_r), len(plan.omega_c))), device="cuda")
+    Xt = Xt.float().t().contiguous().t()
+    _, blocks = column_blocks(n, world)
+    c0, c1 = blocks[rank]
+    be = CudaBlockBackend(ctx, N.F32, plan, gr.laplacian, gc.laplacian, 1.0, 1.0, c0, c1)
+    coll = TorchCollectives()
+    zeros = lambda k: torch.zeros(k, dtype=torch.float32, device="cuda")
+    its = 100
+    res = {}
+
+    def step():
+        res["r"] = alternate_decode_sharded(Xt, plan, be, coll, zeros, tol=1e-30, max_iter=its)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    dist.barrier()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        step()
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    it = res["r"].iterations
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic: seeded config-3 generator",
+               "config": {"workload": f"cfg3 sharded: column-block CG over NCCL, p={p}, n={n}, "
+                                      f"1/8 x 1/8 sampling, {it} iterations", "parallelism": f"colblock{world}",
+                          "block_cols": c1 - c0},
+               "iters_per_s": round(it / (ms / 1e3), 1)}
+        print(json.dumps(out), flush=True)
+    be.close()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
     if args.config == "cfg2" and args.impl == "ours":
         return run_cfg2(args)
     if args.config == "cfg3" and args.impl == "ours":
-        return run_cfg3(args)
+        return run_cfg3_sharded(args, rank, local_rank, world) if args.sharded else run_cfg3(args)
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

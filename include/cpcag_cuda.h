@@ -70,7 +70,10 @@ int cpcag_ctx_destroy(cpcag_ctx ctx);
  * for mapping device memory while the pool grows to its peak. */
 int cpcag_ctx_reserve(cpcag_ctx ctx, int64_t bytes);
 /* Use an external stream (e.g. torch.cuda.current_stream()); NULL restores
- * the context's own stream. */
+ * the context's own stream (a blocking stream, implicitly ordered with the
+ * legacy default stream).  To run on the legacy default
+ * stream -- torch's default stream, whose handle is 0 -- pass
+ * cudaStreamLegacy ((void*)0x1), not NULL. */
 int cpcag_ctx_set_stream(cpcag_ctx ctx, void* cuda_stream);
 void* cpcag_ctx_stream(cpcag_ctx ctx);
 int cpcag_ctx_synchronize(cpcag_ctx ctx);

@@ -51,6 +51,8 @@ def _np_dtype(precision: int):
     return np.float64 if precision == N.F64 else np.float32
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (driver_types.h)
+
 class _In:
     """Pointer to a caller array in the requested precision, column-major."""
 
@@ -128,6 +130,12 @@ class Context:
         return self._h
 
     def set_stream(self, stream_ptr: Optional[int]):
+        """Launch on `stream_ptr` (e.g. torch.cuda.current_stream().cuda_stream).
+        None restores the context's own stream.  Handle 0 is torch's default
+        stream, the legacy default stream, passed as cudaStreamLegacy: the
+        C-ABI reads NULL as "own stream", which is not ordered with torch."""
+        if stream_ptr is not None and int(stream_ptr) == 0:
+            stream_ptr = CUDA_STREAM_LEGACY
         N.check(N.lib().cpcag_ctx_set_stream(self._h, stream_ptr))
 
     def synchronize(self):

@@ -777,7 +777,10 @@ int cpcag_ctx_create(int device, cpcag_ctx* out) {
     Ctx* c = new Ctx();
     c->device = dev;
     c->num_sms = prop.multiProcessorCount;
-    CUDA_OK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+    // A blocking stream: it is implicitly ordered with the legacy default
+    // stream, so inputs a caller produced there (torch's default stream)
+    // are complete before the context's kernels read them, and vice versa.
+    CUDA_OK(cudaStreamCreateWithFlags(&c->own, cudaStreamDefault));
     c->stream = c->own;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {

@@ -1643,8 +1643,8 @@ extern "C" int cpcag_cuda_decoder_block_rhs(cpcag_decoder_block bh, const void* 
     if (!Xt || !B || !sq_norm) invalid("null argument");
     const Plan pl{b->rsel.p, b->csel.p, b->rho_r};
     b->st.zero(c);
-    const i64 ncol = b->c1 - b->c0;
-    dim3 g(blocks_for(std::max<i64>(b->p, 1)), static_cast<unsigned>(std::max<i64>(1, std::min<i64>(ncol, 65535))));
+    // b->grid (columns strided over grid.y): b->part holds one partial per CTA of it
+    const dim3 g = b->grid;
     if (b->prec == CPCAG_F64)
       block_rhs_k<double><<<g, kBlock, 0, c->stream>>>(b->p, b->c0, b->c1, pl, static_cast<const double*>(Xt),
                                                        static_cast<double*>(B), b->part.p, b->st.p);

@@ -114,6 +114,14 @@ def test_cfg3_band_apply_full_size_sampled_columns_bit_exact(P, ctx):
         for i in rows:
             want = _apply_entry(rp_r, ci_r, v_r, rp_c, ci_c, v_c, Pm, rsel, csel, gr, gc, int(i), int(c))
             assert got[i] == want, (i, c)
+    # Repeat calls with a fresh torch-zeroed output: the zeroing (torch's
+    # stream) must be ordered before the apply (regression: a context on an
+    # unordered stream raced the memset from the second call on).
+    for _ in range(2):
+        AP2 = torch.zeros_like(Pflat)
+        be.apply(Pflat, AP2)
+        torch.cuda.synchronize()
+        assert torch.equal(AP2, AP)
     be.close()
 
 
@@ -147,3 +155,36 @@ def test_cfg1_pipeline_full_size_reduced_iterations(P, ctx):
     dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, its)
     assert rel(rep.X.cpu().numpy(), dec.X) <= 1e-4
     assert math.isfinite(rep.trace.objective[-1])
+
+
+def test_cfg3_sharded_block_driver_matches_single_gpu(P, ctx):
+    """The column-block primitives at the full cfg3 size (one block = all
+    200 000 columns, fp32): a few CG iterations of the sharded driver equal
+    the single-GPU decoder's (same operator, dots reduced in another order)."""
+    import torch
+
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200 import workloads
+    from paper_1602_02070_b200.sharded import CudaBlockBackend, alternate_decode_sharded
+    from shard_double import ThreadCollectives
+
+    Pr, Pc = workloads.config3_points()
+    p, n = Pr.shape[1], Pc.shape[1]
+    gr_ = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    gc_ = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
+    plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    Xt = torch.randn(len(plan.omega_c), len(plan.omega_r), device="cuda", generator=gen).t()
+    its = 4
+    be = CudaBlockBackend(ctx, N.F32, plan, gr_.laplacian, gc_.laplacian, 1.0, 1.0, 0, n)
+    coll = ThreadCollectives(ThreadCollectives.Shared(1), 0)
+    res = alternate_decode_sharded(Xt, plan, be, coll, lambda k: torch.zeros(k, device="cuda"), tol=1e-30,
+                                   max_iter=its)
+    Xs = res.X_block.view(n, p).t().cpu().numpy().astype(np.float64)
+    be.close()
+    del res
+    g1 = P.SpectralGap(lambda_k1=1.0)
+    one = P.alternate_decode(Xt, plan, gr_.laplacian, gc_.laplacian, g1, g1, P.DecoderConfig(1.0, 1e-30, its),
+                             ctx=ctx)
+    assert one.iterations == its
+    assert rel(Xs, one.X.cpu().numpy().astype(np.float64)) <= 1e-4

@@ -250,3 +250,21 @@ def test_fista_dense_operator_path(P, ctx, prec):
     Xo, tro = O.fista_solve(Y.astype(dt).astype(np.float64), Lr, Lc, O.FrpcagConfig(8.0, 8.0, "l1", 1e-300, 150))
     assert rel(X, Xo) <= (1e-9 if prec == "f64" else 1e-4)
     assert np.allclose(tr.objective, tro.objective, rtol=1e-9 if prec == "f64" else 1e-4)
+
+
+def test_context_stream_follows_torch_default_stream(P):
+    """torch's default stream (handle 0) maps to cudaStreamLegacy, not to the
+    C-ABI's NULL = "own stream"."""
+    import torch
+
+    from paper_1602_02070_b200 import _native as N
+
+    c = P.Context(0)
+    c.set_stream(torch.cuda.current_stream().cuda_stream)
+    assert N.lib().cpcag_ctx_stream(c.handle) == P.cpcag.CUDA_STREAM_LEGACY
+    s = torch.cuda.Stream()
+    c.set_stream(s.cuda_stream)
+    assert N.lib().cpcag_ctx_stream(c.handle) == s.cuda_stream
+    c.set_stream(None)
+    own = N.lib().cpcag_ctx_stream(c.handle)
+    assert own not in (None, 0, P.cpcag.CUDA_STREAM_LEGACY)

@@ -132,3 +132,53 @@ def test_sharded_decoder_cuda_three_ranks_one_gpu(prec):
     # from the one-GPU solver), which CG amplifies on this ill-conditioned
     # case; the fp64 bar is therefore 1e-6 (the small gloo case holds 1e-9).
     assert rel(X, ro.X) <= (1e-6 if prec == "f64" else 1e-4)
+
+
+def _nccl_worker(port, out):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1602_02070_b200 as P
+    from helpers import to_device
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200.sharded import (CudaBlockBackend, TorchCollectives, alternate_decode_sharded,
+                                               column_blocks)
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    ctx = P.Context(0)
+    _, blocks = column_blocks(plan.n, 1)
+    c0, c1 = blocks[0]
+    be = CudaBlockBackend(ctx, N.F64, plan, to_device(ctx, Lr), to_device(ctx, Lc), 1.0 / 0.3, 1.0 / 0.4, c0, c1)
+    coll = TorchCollectives()
+    assert dist.get_backend() == "nccl"
+    Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), device="cuda").t()
+    res = alternate_decode_sharded(Xt_d, plan, be, coll, lambda k: torch.zeros(k, dtype=torch.float64, device="cuda"),
+                                   tol=1e-10, max_iter=300)
+    torch.cuda.synchronize()
+    out["r"] = (res.X_block.cpu().numpy().copy(), res.iterations)
+    be.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_decoder_nccl_world1_matches_oracle():
+    """The column-sharded driver over a real NCCL communicator (world 1: the
+    all-gather and the all-reduced dots go through NCCL on the device)."""
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    pr = mp.get_context("spawn").Process(target=_nccl_worker, args=(port, out))
+    pr.start()
+    pr.join(300)
+    assert pr.exitcode == 0
+    Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
+    blk, it = out["r"]
+    X = blk.reshape((plan_o.p, plan_o.n), order="F")
+    assert abs(it - ro.iterations) <= 1
+    assert rel(X, ro.X) <= 1e-6
