@@ -280,6 +280,169 @@ __global__ void __launch_bounds__(256) cg_apply_fast_k(int p, int c_lo, int c_hi
   }
 }
 
+// slab: a CTA (1024 threads, one per SM) owns a 32-row slab of P across
+// ALL n columns in shared memory (n * 128 B, n <= 1600 in fp32), so the
+// ~19 L_c gathers of every entry are conflict-free shared-memory reads
+// (lane = row) and only the L_r gathers go to L2.  Warp w takes columns
+// c_lo + w, c_lo + w + 32, ... of the unit; units = slabs x column parts are
+// dealt to the persistent CTAs in a fixed order (deterministic <P, AP>).
+// Per-entry arithmetic and order are fast2's: results are identical.
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) cg_apply_slab_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                           int col_parts, int units, const T* __restrict__ P,
+                                                           T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* S = reinterpret_cast<T*>(smraw);  // S[c * 32 + r] = P[i0 + r, c]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double s[1] = {0.0};
+  int staged = -1;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    const int slab = u / col_parts, part = u - slab * col_parts;
+    const int i0 = slab * 32, rows = min(32, p - i0);
+    const int cw = (n + col_parts - 1) / col_parts;
+    const int c_lo = part * cw, c_hi = min(n, c_lo + cw);
+    if (slab != staged) {
+      __syncthreads();
+      for (int c = warp; c < n; c += 32) S[c * 32 + lane] = lane < rows ? P[i0 + lane + static_cast<i64>(c) * p] : T(0);
+      __syncthreads();
+      staged = slab;
+    }
+    const int i = i0 + lane;
+    const bool valid = lane < rows;
+    const int a0 = valid ? static_cast<int>(Lr.rp[i]) : 0, a1 = valid ? static_cast<int>(Lr.rp[i + 1]) : 0;
+    const bool rs = valid && pl.rsel[i] >= 0;
+    for (int c = c_lo + warp; c < c_hi; c += 32) {
+      const int k0 = static_cast<int>(Lc.rp[c]), k1 = static_cast<int>(Lc.rp[c + 1]);
+      T x = T(0);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) x = madd_entry(x, __ldg(Lc.v + k), S[__ldg(Lc.ci + k) * 32 + lane]);
+      if (valid) {
+        const T* pc = P + static_cast<i64>(c) * p;
+        T y = T(0);
+#pragma unroll 4
+        for (int k = a0; k < a1; ++k) y = madd_entry(y, __ldg(Lr.v + k), pc[__ldg(Lr.ci + k)]);
+        T o = add_rn(mul_rn(gc, x), mul_rn(gr, y));
+        const T pv = S[c * 32 + lane];
+        if (rs && pl.csel[c] >= 0) o = add_rn(o, pv);
+        AP[i + static_cast<i64>(c) * p] = o;
+        s[0] += static_cast<double>(pv) * static_cast<double>(o);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
+// fast4: R rows per thread, strided by the CTA width (i, i + NT, ...), so
+// each staged L_c entry serves R independent 4/8-byte gathers (R loads in
+// flight per thread per entry, 128 B per warp request) and the L_r gathers
+// stay unit-stride across lanes.  The config-1 gather is latency-bound
+// (bytes in flight per SM); fast2 is the R = 2, NT = 256 case.  Per-entry
+// arithmetic and order are fast2's: results are identical.
+template <typename T, int R, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_fast4_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc,
+                                                                  Plan pl, int cols_per_cta, const T* __restrict__ P,
+                                                                  T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int RB = NT * R;
+  const int i0 = blockIdx.x * RB;
+  const int i1 = min(p, i0 + RB);
+  const int cb = blockIdx.y * cols_per_cta;
+  const int ce = min(n, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0];
+  const int er = static_cast<int>(Lr.rp[i1] - kr_base);
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0;
+  const int ec = cb < ce ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  OffEnt<T>* Er = reinterpret_cast<OffEnt<T>*>(smraw);
+  OffEnt<T>* Ec = Er + er;
+  int* crp = reinterpret_cast<int*>(Ec + ec);
+  int* rrp = crp + (ce - cb + 1);  // L_r row starts of this CTA's rows (RB + 1)
+  for (int k = threadIdx.x; k < er; k += NT) {
+    OffEnt<T> e;
+    e.v = Lr.v[kr_base + k];
+    e.off = Lr.ci[kr_base + k];
+    Er[k] = e;
+  }
+  for (int k = threadIdx.x; k < ec; k += NT) {
+    OffEnt<T> e;
+    e.v = Lc.v[kc_base + k];
+    e.off = Lc.ci[kc_base + k] * p;
+    Ec[k] = e;
+  }
+  for (int q = threadIdx.x; q <= ce - cb; q += NT) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  for (int q = threadIdx.x; q <= i1 - i0; q += NT) rrp[q] = static_cast<int>(Lr.rp[i0 + q] - kr_base);
+  __syncthreads();
+  double s[1] = {0.0};
+  const int ia = i0 + threadIdx.x;
+  int nr = 0;  // valid rows of this thread: ia + NT * r < p for r < nr
+#pragma unroll
+  for (int r = 0; r < R; ++r) nr += ia + NT * r < p ? 1 : 0;
+  unsigned sr = 0;  // sampled-row bits
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (r < nr && pl.rsel[ia + NT * r] >= 0) sr |= 1u << r;
+  const T* Pa = P + ia;
+  if (nr > 0) {
+    for (int c = cb; c < ce; ++c) {
+      const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
+      T x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[r] = T(0);
+#pragma unroll 2
+      for (int k = k0; k < k1; ++k) {
+        const OffEnt<T> e = Ec[k];
+        T g[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) g[r] = r < nr ? Pa[e.off + NT * r] : T(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = madd_entry(x[r], e.v, g[r]);
+      }
+      const T* pc = P + static_cast<i64>(c) * p;
+      const bool cs = pl.csel[c] >= 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r < nr) {
+          const int lr = threadIdx.x + NT * r;
+          T y = T(0);
+          for (int q = rrp[lr]; q < rrp[lr + 1]; ++q) {
+            const OffEnt<T> e = Er[q];
+            y = madd_entry(y, e.v, pc[e.off]);
+          }
+          T o = add_rn(mul_rn(gc, x[r]), mul_rn(gr, y));
+          const T pv = pc[ia + NT * r];
+          if (((sr >> r) & 1u) && cs) o = add_rn(o, pv);
+          AP[ia + NT * r + static_cast<i64>(c) * p] = o;
+          s[0] += static_cast<double>(pv) * static_cast<double>(o);
+        }
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 // fast2: two rows per thread (i and i + 256) so each staged L_c entry and
 // its address arithmetic serve two gathers (the fast apply is issue- and
 // latency-bound, ~6 instructions per 4-byte gather).
@@ -1121,7 +1284,13 @@ struct TileApply {
 
   // Returns false (and builds nothing) when the column graph is not banded
   // enough for the shared-memory window.
-  bool build(Ctx* c, Csr* Lc, const std::vector<i64>& rpc, const std::vector<i64>& rpr_, i64 p_, int cap) {
+  // windows = false (rcm2): only the RCM order and the permuted L_c as a
+  // CSR pull (pci / pv), for the fast2 kernel on column-permuted iterates.
+  DevBuf<int> pci;
+  DevBuf<T> pv;
+  std::vector<i64> hrp_host;
+  bool build(Ctx* c, Csr* Lc, const std::vector<i64>& rpc, const std::vector<i64>& rpr_, i64 p_, int cap,
+             bool windows = true) {
     p = p_;
     n = Lc->rows;
     if (n > INT32_MAX || p > INT32_MAX) return false;
@@ -1152,6 +1321,25 @@ struct TileApply {
         hent[o].off = hpos[hci[k]];
       }
       hrp[st_ + 1] = o;
+    }
+    if (!windows) {
+      std::vector<int> ci2(hent.size());
+      std::vector<T> v2(hent.size());
+      for (size_t k = 0; k < hent.size(); ++k) {
+        ci2[k] = hent[k].off;
+        v2[k] = hent[k].v;
+      }
+      pos.alloc(c, n);
+      crp.alloc(c, n + 1);
+      pci.alloc(c, ci2.size());
+      pv.alloc(c, v2.size());
+      CUDA_OK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(crp.p, hrp.data(), sizeof(i64) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(pci.p, ci2.data(), sizeof(int) * ci2.size(), cudaMemcpyHostToDevice, c->stream));
+      CUDA_OK(cudaMemcpyAsync(pv.p, v2.data(), sizeof(T) * v2.size(), cudaMemcpyHostToDevice, c->stream));
+      hrp_host = hrp;
+      sync(c);
+      return true;
     }
     const i64 chunks = (n + kC - 1) / kC;
     std::vector<int> lo(static_cast<size_t>(chunks)), hi(static_cast<size_t>(chunks));
@@ -1264,7 +1452,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const unsigned nb1 = stride_blocks(c, N);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
-  // Apply variant (CPCAG_APPLY overrides): fast2 | fast | fast3 | staged |
+  // Apply variant (CPCAG_APPLY overrides): fast2 | fast | fast3 | fast4 | slab | rcm2 | staged |
   // plain for L2-sized iterates, band for iterates larger than L2.
   // fast2 by default for L2-sized iterates; fast3 (RCM column windows in
   // shared memory, CPCAG_APPLY=fast3) measured slower at config 1 (39.9 vs
@@ -1297,6 +1485,24 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   if (variant == "fast" && !(p * n < (i64{1} << 31) && fast_smem <= 96 * 1024)) variant = "staged";
   TileApply<T> tile;
   DevBuf<int> csel_perm;
+  const Plan pl0 = pl;  // caller's column order (the true residual of rcm2)
+  Pull<T> pc2 = pc;     // L_c pull of the fast2 kernel (permuted for rcm2)
+  if (variant == "rcm2") {
+    // fast2 on iterates stored in RCM column order (CPCAG_APPLY=rcm2):
+    // consecutive columns share most of their L_c neighbours, so a CTA's
+    // gathers hit L1.  Measured equal to fast2 (0.128 vs 0.127 ms): L2
+    // locality is not what bounds the gather.
+    if (p * n < (i64{1} << 31) && tile.build(c, Lc, rpc, rpr, p, INT32_MAX, false)) {
+      csel_perm.alloc(c, n);
+      permute_sel_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, tile.pos.p, csel.p, csel_perm.p);
+      launched(c);
+      pl.csel = csel_perm.p;
+      pc2 = Pull<T>{tile.crp.p, tile.pci.p, tile.pv.p};
+      rpc = tile.hrp_host;  // fast2 geometry below sizes its L_c staging from these
+    } else {
+      variant = "fast2";
+    }
+  }
   if (variant == "fast3") {
     // banded column graph: RCM column order and shared-memory windows
     if (tile.build(c, Lc, rpc, rpr, p, 128)) {
@@ -1334,7 +1540,68 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
                                   (n + 65534) / 65535});
   const dim3 gs2(gx2, static_cast<unsigned>(std::min<i64>((n + cpc2 - 1) / cpc2, 65535)));
   size_t fast2_smem = 0;
-  if (variant == "fast2") {
+  // slab (32-row slabs of P in shared memory, CPCAG_APPLY=slab): measured
+  // slower than fast2 at config 1 (0.19 vs 0.127 ms per apply): one
+  // 1024-thread CTA per SM stalls on slab staging and on the L_r gathers.
+  int slab_parts = 0, slab_units = 0;
+  unsigned slab_grid = 0;
+  size_t slab_smem = 0;
+  if (variant == "slab") {
+    if (n * 32 * sizeof(T) > 200 * 1024) invalid("alternate decoder: slab apply needs n * 32 * sizeof(T) <= 200 KB");
+    const i64 slabs = (p + 31) / 32, sms = c->num_sms;
+    // parts per slab: minimise rounds x (staging + compute / parts), staging ~0.1 of a slab's compute
+    double best = 1e300;
+    for (int q = 1; q <= 4; ++q) {
+      const double rounds = static_cast<double>((slabs * q + sms - 1) / sms);
+      const double t = rounds * (0.1 + 1.0 / q);
+      if (t < best - 1e-9) {
+        best = t;
+        slab_parts = q;
+      }
+    }
+    if (const char* e = std::getenv("CPCAG_SLAB_PARTS")) slab_parts = std::max(1, std::atoi(e));
+    slab_units = static_cast<int>(slabs * slab_parts);
+    slab_grid = static_cast<unsigned>(std::min<i64>(slab_units, sms));
+    slab_smem = static_cast<size_t>(n) * 32 * sizeof(T);
+    ensure_smem(cg_apply_slab_k<T>, slab_smem);
+    if (part.n < slab_grid) part.alloc(c, slab_grid);
+  }
+  // fast4 (R rows per thread, 128-thread CTAs; CPCAG_APPLY=fast4): measured
+  // slower than fast2 (0.18 ms at R = 2, worse at R = 4, 8): the gather wants
+  // resident warps, not more loads per thread.
+  int f4_rows = 4;
+  if (const char* e = std::getenv("CPCAG_FAST4_ROWS")) f4_rows = std::atoi(e) == 8 ? 8 : (std::atoi(e) == 2 ? 2 : 4);
+  const i64 kF4Rows = 128 * f4_rows;  // rows per CTA
+  const unsigned gx4 = static_cast<unsigned>((p + kF4Rows - 1) / kF4Rows);
+  i64 f4_per_sm = 8;  // CTAs per SM the column chunking aims at
+  if (const char* e = std::getenv("CPCAG_FAST4_CTAS")) f4_per_sm = std::max<i64>(1, std::atoll(e));
+  const i64 y4cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * f4_per_sm) / gx4);
+  const i64 cpc4 = std::max<i64>({i64{1}, std::min<i64>((n + std::min<i64>(n, y4cap) - 1) / std::max<i64>(1, std::min<i64>(n, y4cap)), 128),
+                                  (n + 65534) / 65535});
+  const dim3 gs4(gx4, static_cast<unsigned>(std::min<i64>((n + cpc4 - 1) / cpc4, 65535)));
+  size_t fast4_smem = 0;
+  auto f4_kernel = [&]() {
+    return f4_rows == 8 ? cg_apply_fast4_k<T, 8, 128> : (f4_rows == 2 ? cg_apply_fast4_k<T, 2, 128> : cg_apply_fast4_k<T, 4, 128>);
+  };
+  if (variant == "fast4") {
+    i64 mer = 0, mec = 0;
+    for (unsigned b = 0; b < gx4; ++b) {
+      const i64 a = static_cast<i64>(b) * kF4Rows, e = std::min<i64>(p, a + kF4Rows);
+      mer = std::max(mer, rpr[e] - rpr[a]);
+    }
+    for (unsigned b = 0; b < gs4.y; ++b) {
+      const i64 a = static_cast<i64>(b) * cpc4, e = std::min<i64>(n, a + cpc4);
+      mec = std::max(mec, rpc[e] - rpc[a]);
+    }
+    fast4_smem = static_cast<size_t>(mer + mec) * sizeof(OffEnt<T>) + sizeof(int) * (cpc4 + 2 + kF4Rows + 1) + 16;
+    if (!(p * n < (i64{1} << 31) && fast4_smem <= 96 * 1024)) {
+      variant = "fast2";
+    } else {
+      ensure_smem(f4_kernel(), fast4_smem);
+      if (part.n < static_cast<size_t>(gs4.x) * gs4.y) part.alloc(c, static_cast<size_t>(gs4.x) * gs4.y);
+    }
+  }
+  if (variant == "fast2" || variant == "rcm2") {
     i64 mer = 0, mec = 0;
     for (unsigned b = 0; b < gx2; ++b) {
       const i64 a = static_cast<i64>(b) * 512, e = std::min<i64>(p, a + 512);
@@ -1345,7 +1612,10 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       mec = std::max(mec, rpc[e] - rpc[a]);
     }
     fast2_smem = static_cast<size_t>(mer + mec) * sizeof(OffEnt<T>) + sizeof(int) * (cpc2 + 2) + 16;
-    if (!(p * n < (i64{1} << 31) && fast2_smem <= 96 * 1024)) variant = "staged";
+    if (!(p * n < (i64{1} << 31) && fast2_smem <= 96 * 1024)) {
+      if (variant == "rcm2") invalid("alternate decoder: rcm2 apply slice exceeds shared memory");
+      variant = "staged";
+    }
     else ensure_smem(cg_apply_fast2_k<T>, fast2_smem);
     if (part.n < static_cast<size_t>(gs2.x) * gs2.y) part.alloc(c, static_cast<size_t>(gs2.x) * gs2.y);
   }
@@ -1364,8 +1634,15 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
         } else if (variant == "fast3") {
           tile.apply(c, pr, P.p, AP.p, pl, gr, gc, part.p, st.p, 0);
-        } else if (variant == "fast2") {
-          cg_apply_fast2_k<T><<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr,
+        } else if (variant == "slab") {
+          cg_apply_slab_k<T><<<slab_grid, 1024, slab_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc,
+                                                                        gr, gc, pl, slab_parts, slab_units, P.p, AP.p,
+                                                                        part.p, st.p);
+        } else if (variant == "fast4") {
+          f4_kernel()<<<gs4, 128, fast4_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl,
+                                                       static_cast<int>(cpc4), P.p, AP.p, part.p, st.p);
+        } else if (variant == "fast2" || variant == "rcm2") {
+          cg_apply_fast2_k<T><<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc2, gr,
                                                                      gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
                                                                      st.p);
         } else if (variant == "fast") {
@@ -1423,7 +1700,18 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       unpermute_rows_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, band.pos.p, AP.p, X);
     }
   } else {
-    cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl, Xt, X, part.p, st.p);
+    if (variant == "rcm2") {  // back to the caller's column order
+      CUDA_OK(cudaMemcpyAsync(AP.p, X, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
+      if constexpr (sizeof(T) == 4)
+        unpermute_cols_k<<<g2, kBlock, 0, c->stream>>>(p, n, tile.pos.p, reinterpret_cast<const float*>(AP.p),
+                                                       reinterpret_cast<float*>(X), nullptr, nullptr);
+      else
+        unpermute_cols_k<<<g2, kBlock, 0, c->stream>>>(p, n, tile.pos.p, nullptr, nullptr,
+                                                       reinterpret_cast<const double*>(AP.p),
+                                                       reinterpret_cast<double*>(X));
+      launched(c);
+    }
+    cg_true_residual_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pr, pc, gr, gc, pl0, Xt, X, part.p, st.p);
   }
   launched(c);
   host = read_back(c, st.p);

@@ -177,7 +177,7 @@ def _decoder_case(p=150, n=120, rr=40, rc=30, seed=21):
     return Lr, Lc, plan, Xt
 
 
-@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast3", "staged", "plain", "band"])
+@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast4", "slab", "rcm2", "fast3", "staged", "plain", "band"])
 def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
@@ -191,7 +191,10 @@ def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     assert rel(res.X, ro.X) <= 1e-9
 
 
-def test_alternate_decode_fixed_iterations_fp32(P, ctx):
+@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "slab", "rcm2"])
+def test_alternate_decode_fixed_iterations_fp32(P, ctx, monkeypatch, variant):
+    if variant != "default":
+        monkeypatch.setenv("CPCAG_APPLY", variant)
     Lr, Lc, plan_o, Xt = _decoder_case(400, 300, 100, 75, 23)
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
     res = P.alternate_decode(Xt.astype(np.float32), plan, to_device(ctx, Lr), to_device(ctx, Lc),
