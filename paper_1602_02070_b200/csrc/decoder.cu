@@ -280,6 +280,129 @@ __global__ void __launch_bounds__(256) cg_apply_fast_k(int p, int c_lo, int c_hi
   }
 }
 
+// fast5 (fp32, p % 4 == 0): each warp owns 128 rows.  The L_c gathers load
+// 4 contiguous rows per lane as one 16-byte LDG (512 B per warp request, a
+// quarter of fast2's LDG count for that part; the gather is bound by LSU
+// issue, ~1.8 cycles per LDG per SM); the L_c sums go through a warp-private
+// shared-memory transpose so the L_r gathers, the own value and the store
+// stay unit-stride across lanes (rows r0 + lane + 32 k).  Per-entry
+// arithmetic and order are fast2's: results are identical.
+template <int U>
+__global__ void __launch_bounds__(128, 8) cg_apply_fast5_k(int p, int n, Pull<float> Lr, Pull<float> Lc, float gr,
+                                                           float gc, Plan pl, int cols_per_cta,
+                                                           const float* __restrict__ P, float* __restrict__ AP,
+                                                           double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int RB = 512;  // 4 warps x 128 rows
+  __shared__ __align__(16) float xs[4][128];
+  const int i0 = blockIdx.x * RB;
+  const int i1 = min(p, i0 + RB);
+  const int cb = blockIdx.y * cols_per_cta;
+  const int ce = min(n, cb + cols_per_cta);
+  const i64 kr_base = Lr.rp[i0];
+  const int er = static_cast<int>(Lr.rp[i1] - kr_base);
+  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0;
+  const int ec = cb < ce ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  OffEnt<float>* Er = reinterpret_cast<OffEnt<float>*>(smraw);
+  OffEnt<float>* Ec = Er + er;
+  int* crp = reinterpret_cast<int*>(Ec + ec);
+  int* rrp = crp + (ce - cb + 1);
+  for (int k = threadIdx.x; k < er; k += 128) {
+    OffEnt<float> e;
+    e.v = Lr.v[kr_base + k];
+    e.off = Lr.ci[kr_base + k];
+    Er[k] = e;
+  }
+  for (int k = threadIdx.x; k < ec; k += 128) {
+    OffEnt<float> e;
+    e.v = Lc.v[kc_base + k];
+    e.off = Lc.ci[kc_base + k] * p;
+    Ec[k] = e;
+  }
+  for (int q = threadIdx.x; q <= ce - cb; q += 128) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  for (int q = threadIdx.x; q <= i1 - i0; q += 128) rrp[q] = static_cast<int>(Lr.rp[i0 + q] - kr_base);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = i0 + warp * 128;
+  const bool vrow = r0 + 4 * lane < p;  // p % 4 == 0: the whole float4 is valid
+  float* xw = xs[warp];
+  unsigned sr = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = r0 + lane + 32 * k;
+    if (i < p && pl.rsel[i] >= 0) sr |= 1u << k;
+  }
+  double s[1] = {0.0};
+  const float* Pv = P + r0 + 4 * lane;
+  for (int c = cb; c < ce; ++c) {
+    const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (vrow) {
+      int k = k0;
+      for (; k + U <= k1; k += U) {
+        float4 g[U];
+        float w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const OffEnt<float> e = Ec[k + u];
+          w[u] = e.v;
+          g[u] = *reinterpret_cast<const float4*>(Pv + e.off);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          x.x = madd_entry(x.x, w[u], g[u].x);
+          x.y = madd_entry(x.y, w[u], g[u].y);
+          x.z = madd_entry(x.z, w[u], g[u].z);
+          x.w = madd_entry(x.w, w[u], g[u].w);
+        }
+      }
+      for (; k < k1; ++k) {
+        const OffEnt<float> e = Ec[k];
+        const float4 g = *reinterpret_cast<const float4*>(Pv + e.off);
+        x.x = madd_entry(x.x, e.v, g.x);
+        x.y = madd_entry(x.y, e.v, g.y);
+        x.z = madd_entry(x.z, e.v, g.z);
+        x.w = madd_entry(x.w, e.v, g.w);
+      }
+    }
+    __syncwarp();
+    *reinterpret_cast<float4*>(xw + 4 * lane) = x;
+    __syncwarp();
+    const float* pc = P + static_cast<i64>(c) * p;
+    const bool cs = pl.csel[c] >= 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = r0 + lane + 32 * k;
+      if (i < p) {
+        const int lr = i - i0;
+        float y = 0.f;
+        for (int q = rrp[lr]; q < rrp[lr + 1]; ++q) {
+          const OffEnt<float> e = Er[q];
+          y = madd_entry(y, e.v, pc[e.off]);
+        }
+        float o = add_rn(mul_rn(gc, xw[lane + 32 * k]), mul_rn(gr, y));
+        const float pv = pc[i];
+        if (((sr >> k) & 1u) && cs) o = add_rn(o, pv);
+        AP[i + static_cast<i64>(c) * p] = o;
+        s[0] += static_cast<double>(pv) * static_cast<double>(o);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 // slab: a CTA (1024 threads, one per SM) owns a 32-row slab of P across
 // ALL n columns in shared memory (n * 128 B, n <= 1600 in fp32), so the
 // ~19 L_c gathers of every entry are conflict-free shared-memory reads
@@ -446,8 +569,8 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_fast4_k(int p, int n, 
 // fast2: two rows per thread (i and i + 256) so each staged L_c entry and
 // its address arithmetic serve two gathers (the fast apply is issue- and
 // latency-bound, ~6 instructions per 4-byte gather).
-template <typename T>
-__global__ void __launch_bounds__(256, 4) cg_apply_fast2_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+template <typename T, int MINB = 4>
+__global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
                                                            int cols_per_cta, const T* __restrict__ P,
                                                            T* __restrict__ AP, double* partials, CgState* st) {
   if (st->done) return;
@@ -1540,6 +1663,40 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
                                   (n + 65534) / 65535});
   const dim3 gs2(gx2, static_cast<unsigned>(std::min<i64>((n + cpc2 - 1) / cpc2, 65535)));
   size_t fast2_smem = 0;
+  int f2_minb = 4;  // resident CTAs per SM the register budget targets
+  if (const char* e = std::getenv("CPCAG_FAST2_MINB")) f2_minb = std::min(6, std::max(4, std::atoi(e)));
+  auto f2_kernel = [&]() {
+    return f2_minb == 6 ? cg_apply_fast2_k<T, 6> : (f2_minb == 5 ? cg_apply_fast2_k<T, 5> : cg_apply_fast2_k<T, 4>);
+  };
+  // fast5 (fp32, p % 4 == 0; CPCAG_APPLY=fast5): 16-byte L_c gathers.
+  unsigned gx5 = static_cast<unsigned>((p + 511) / 512);
+  i64 f5_per_sm = 16;  // 128-thread CTAs per SM the column chunking aims at
+  if (const char* e = std::getenv("CPCAG_FAST5_CTAS")) f5_per_sm = std::max<i64>(1, std::atoll(e));
+  int f5_unroll = 4;
+  if (const char* e = std::getenv("CPCAG_FAST5_UNROLL")) f5_unroll = std::atoi(e) == 8 ? 8 : (std::atoi(e) == 2 ? 2 : 4);
+  const i64 y5cap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * f5_per_sm) / gx5);
+  const i64 cpc5 = std::max<i64>({i64{1}, std::min<i64>((n + std::min<i64>(n, y5cap) - 1) / std::max<i64>(1, std::min<i64>(n, y5cap)), 128),
+                                  (n + 65534) / 65535});
+  const dim3 gs5(gx5, static_cast<unsigned>(std::min<i64>((n + cpc5 - 1) / cpc5, 65535)));
+  size_t fast5_smem = 0;
+  if (variant == "fast5") {
+    if (sizeof(T) != 4 || p % 4 != 0) invalid("alternate decoder: fast5 apply needs fp32 and p % 4 == 0");
+    i64 mer = 0, mec = 0;
+    for (unsigned b = 0; b < gx5; ++b) {
+      const i64 a = static_cast<i64>(b) * 512, e = std::min<i64>(p, a + 512);
+      mer = std::max(mer, rpr[e] - rpr[a]);
+    }
+    for (unsigned b = 0; b < gs5.y; ++b) {
+      const i64 a = static_cast<i64>(b) * cpc5, e = std::min<i64>(n, a + cpc5);
+      mec = std::max(mec, rpc[e] - rpc[a]);
+    }
+    fast5_smem = static_cast<size_t>(mer + mec) * sizeof(OffEnt<T>) + sizeof(int) * (cpc5 + 2 + 512 + 1) + 16;
+    if (!(p * n < (i64{1} << 31) && fast5_smem <= 96 * 1024)) invalid("alternate decoder: fast5 slice exceeds shared memory");
+    ensure_smem(cg_apply_fast5_k<2>, fast5_smem);
+    ensure_smem(cg_apply_fast5_k<4>, fast5_smem);
+    ensure_smem(cg_apply_fast5_k<8>, fast5_smem);
+    if (part.n < static_cast<size_t>(gs5.x) * gs5.y) part.alloc(c, static_cast<size_t>(gs5.x) * gs5.y);
+  }
   // slab (32-row slabs of P in shared memory, CPCAG_APPLY=slab): measured
   // slower than fast2 at config 1 (0.19 vs 0.127 ms per apply): one
   // 1024-thread CTA per SM stalls on slab staging and on the L_r gathers.
@@ -1616,7 +1773,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       if (variant == "rcm2") invalid("alternate decoder: rcm2 apply slice exceeds shared memory");
       variant = "staged";
     }
-    else ensure_smem(cg_apply_fast2_k<T>, fast2_smem);
+    else {
+      ensure_smem(cg_apply_fast2_k<T, 4>, fast2_smem);
+      ensure_smem(cg_apply_fast2_k<T, 5>, fast2_smem);
+      ensure_smem(cg_apply_fast2_k<T, 6>, fast2_smem);
+    }
     if (part.n < static_cast<size_t>(gs2.x) * gs2.y) part.alloc(c, static_cast<size_t>(gs2.x) * gs2.y);
   }
   if (variant == "staged" && !(staged_smem <= 96 * 1024)) variant = "plain";
@@ -1634,6 +1795,12 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           band.apply(c, P.p, AP.p, 0, n, pl, gr, gc, part.p, st.p, 0);
         } else if (variant == "fast3") {
           tile.apply(c, pr, P.p, AP.p, pl, gr, gc, part.p, st.p, 0);
+        } else if (variant == "fast5") {
+          if constexpr (sizeof(T) == 4) {
+            auto k5 = f5_unroll == 8 ? cg_apply_fast5_k<8> : (f5_unroll == 2 ? cg_apply_fast5_k<2> : cg_apply_fast5_k<4>);
+            k5<<<gs5, 128, fast5_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl,
+                                                    static_cast<int>(cpc5), P.p, AP.p, part.p, st.p);
+          }
         } else if (variant == "slab") {
           cg_apply_slab_k<T><<<slab_grid, 1024, slab_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc,
                                                                         gr, gc, pl, slab_parts, slab_units, P.p, AP.p,
@@ -1642,7 +1809,7 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
           f4_kernel()<<<gs4, 128, fast4_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl,
                                                        static_cast<int>(cpc4), P.p, AP.p, part.p, st.p);
         } else if (variant == "fast2" || variant == "rcm2") {
-          cg_apply_fast2_k<T><<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc2, gr,
+          f2_kernel()<<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc2, gr,
                                                                      gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
                                                                      st.p);
         } else if (variant == "fast") {

@@ -191,7 +191,7 @@ def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     assert rel(res.X, ro.X) <= 1e-9
 
 
-@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "slab", "rcm2"])
+@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "fast5", "slab", "rcm2"])
 def test_alternate_decode_fixed_iterations_fp32(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
