@@ -104,6 +104,23 @@ def _out(like_cuda, device, shape, precision: int, kind="float"):
     return a, (a.ctypes.data if a.size else None)
 
 
+def _given_out(a, shape, precision: int, name: str):
+    """A caller-provided column-major output (numpy F-order array, e.g. a view
+    of pinned memory, or a column-major CUDA tensor) -> (array, pointer)."""
+    want = _np_dtype(precision)
+    if hasattr(a, "data_ptr"):  # torch tensor
+        torch = _torch()
+        tdt = torch.float64 if precision == N.F64 else torch.float32
+        ok = tuple(a.shape) == tuple(shape) and a.dtype == tdt and (a.numel() == 0 or a.t().is_contiguous())
+        if not ok:
+            raise ValueError(f"{name}: expected a column-major {tuple(shape)} {tdt} tensor")
+        return a, a.data_ptr()
+    a = np.asarray(a)
+    if a.shape != tuple(shape) or a.dtype != want or not (a.size == 0 or a.flags.f_contiguous):
+        raise ValueError(f"{name}: expected a Fortran-ordered {tuple(shape)} {np.dtype(want).name} array")
+    return a, (a.ctypes.data if a.size else None)
+
+
 def _precision(x, precision):
     if precision is not None:
         return N.F32 if precision in (N.F32, "f32", "float32", np.float32) else N.F64
@@ -841,8 +858,12 @@ class PipelineReport:  # pipeline.hpp:73-94 (subset)
 
 
 def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
-                 W_c: Optional[SparseMatrix] = None, precision=None, ctx=None) -> PipelineReport:
-    """pipeline.hpp:100 / pipeline.cpp:228-350 on a resident data matrix Y (p x n)."""
+                 W_c: Optional[SparseMatrix] = None, precision=None, ctx=None, out=None) -> PipelineReport:
+    """pipeline.hpp:100 / pipeline.cpp:228-350 on a resident data matrix Y (p x n).
+
+    out: optional (Xt, X) column-major buffers to write the results into (for
+    host inputs, e.g. views of pinned memory reused across calls, so the
+    device->host copies are direct DMA); by default they are allocated."""
     prec = _precision(Y, precision)
     y = _In(Y, prec)
     p, n = y.shape
@@ -850,8 +871,12 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
     rho_c = cfg.rho_c_override if cfg.rho_c_override > 0 else -(-n // max(cfg.a, 1))
     rho_r, rho_c = min(rho_r, p), min(rho_c, n)
     cuda = _is_cuda(Y)
-    xt, xtp = _out(cuda, _torch_device(Y), (rho_r, rho_c), prec)
-    x, xp = _out(cuda, _torch_device(Y), (p, n), prec)
+    if out is not None:
+        xt, xtp = _given_out(out[0], (rho_r, rho_c), prec, "out[0] (Xt)")
+        x, xp = _given_out(out[1], (p, n), prec, "out[1] (X)")
+    else:
+        xt, xtp = _out(cuda, _torch_device(Y), (rho_r, rho_c), prec)
+        x, xp = _out(cuda, _torch_device(Y), (p, n), prec)
     om_r = np.empty(max(rho_r, 1), np.int64)
     om_c = np.empty(max(rho_c, 1), np.int64)
     obj = np.zeros(max(int(cfg.frpcag.max_iter), 1))

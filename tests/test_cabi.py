@@ -79,3 +79,20 @@ def test_fails_loudly_without_device():
     rc = L.cpcag_ctx_create(0, ctypes.byref(h))
     assert rc == _native.ERR_CUDA
     assert L.cpcag_cuda_last_error()
+
+
+def test_pipeline_out_buffer_validation():
+    """run_pipeline(out=...) accepts Fortran-ordered arrays of the result
+    shape and dtype, and rejects anything else before calling the library."""
+    import numpy as np
+
+    from paper_1602_02070_b200 import _native as N
+    from paper_1602_02070_b200.cpcag import _given_out
+
+    a = np.empty((5, 3), np.float32, order="F")
+    arr, ptr = _given_out(a, (5, 3), N.F32, "X")
+    assert arr is a and ptr == a.ctypes.data
+    for bad in (np.empty((5, 3), np.float32), np.empty((5, 3), np.float64, order="F"),
+                np.empty((3, 5), np.float32, order="F")):
+        with pytest.raises(ValueError, match="X: expected a Fortran-ordered"):
+            _given_out(bad, (5, 3), N.F32, "X")

@@ -254,6 +254,16 @@ def test_pipeline_small_matches_oracle_stages(P, ctx):
     dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, 0.5, 0.5, 1.0, 1e-8, 100)
     assert rel(rep.X, dec.X) <= 1e-7
     assert abs(rep.decoder_iterations - dec.iterations) <= 1
+    # caller-provided (pinned) result buffers: same results, written in place
+    import torch
+
+    Xh = torch.empty((n, p), dtype=torch.float64, pin_memory=True).numpy().T
+    Xth = torch.empty((rep.rho_c, rep.rho_r), dtype=torch.float64, pin_memory=True).numpy().T
+    rep2 = P.run_pipeline(Y, cfg, ctx=ctx, out=(Xth, Xh))
+    assert rep2.X is Xh and rep2.Xt is Xth
+    assert np.array_equal(rep2.X, rep.X) and np.array_equal(rep2.Xt, rep.Xt)
+    with pytest.raises(ValueError, match="out\\[1\\] \\(X\\): expected"):
+        P.run_pipeline(Y, cfg, ctx=ctx, out=(Xth, np.empty((p, n))))
     assert all(rep.stages[s] > 0 for s in ("graphs", "kron", "solve", "decode"))
 
 
