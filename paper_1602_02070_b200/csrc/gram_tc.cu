@@ -428,13 +428,19 @@ __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
 // NT = candidate rows per tile (UMMA N): 128 (3-stage ring of 64 KiB) or
 // 256 (2-stage ring of 96 KiB; each A chunk then serves twice the
 // candidates, 65 instead of 48 flops per staged byte).
-template <int NT>
+//
+// KC = candidates kept per query (32: first pass over every point, 3-stage
+// ring; 64: second pass over the queries the first pass could not certify,
+// 2-stage ring so the longer lists fit).  qidx (null = identity) maps the
+// nq query rows of mapH / mapL to point indices; outputs are indexed by
+// query row: cand[(split * nq + q) * KC + rank].
+template <int NT, int KC = 32>
 __global__ void __launch_bounds__(tc2::kThreads, 1)
     knn_tc_filter2_k(const __grid_constant__ CUtensorMap mapH, const __grid_constant__ CUtensorMap mapL,
                      const __grid_constant__ CUtensorMap mapHb, const __grid_constant__ CUtensorMap mapLb,
                      const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split, float* __restrict__ cand_d,
                      int* __restrict__ cand_j, const unsigned long long* __restrict__ max_norm_bits, int stagger,
-                     int dbg) {
+                     int dbg, const int* __restrict__ qidx, i64 nq) {
   using namespace tc;
   using tc2::kTile;
   using tc2::kThreads;
@@ -448,7 +454,8 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   constexpr int kN = NT;
   constexpr int kBTile = NT * 128;                   // NT rows x 128 B
   constexpr int kStageBytes = 2 * kTile + 2 * kBTile;
-  constexpr int kStages = NT == 128 ? 3 : 2;
+  constexpr int kStages = (NT == 128 && KC == 32) ? 3 : 2;
+  constexpr int kCand = KC;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // SWIZZLE_128B needs 1024-byte aligned stages; the dynamic window is
   // declared so (no slack is reserved: the 3-stage ring plus the lists fill
@@ -550,8 +557,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     const int eq = warp & 3;
     const int r = eq * 32 + lane;
     const int et = threadIdx.x - 64;  // 0..127 across the epilogue warps
-    const i64 gi = i0 + r;
-    const double sqi = gi < n ? sq[gi] : 0.0;
+    const i64 qr = i0 + r;            // query row
+    const bool qv = qr < nq;
+    const i64 gi = qv ? (qidx ? static_cast<i64>(qidx[qr]) : qr) : n;  // its point (n = none)
+    const double sqi = qv ? sq[gi] : 0.0;
     const float sqi_f = static_cast<float>(sqi);
     // Quick reject in fp32.  The exact test below is df < thr with
     // df = fp32((sq_i + sq_j) - 2 g) evaluated in fp64.  The fp32 estimate
@@ -587,7 +596,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       for (int c0 = 0; c0 < kN; c0 += 32) {
         float v[32];
         tmem_ld32(tbase + static_cast<uint32_t>(c0), v);
-        if (gi < n && dbg != 1) {
+        if (qv && dbg != 1) {
           float e[32];
           float mn = CUDART_INF_F;
 #pragma unroll
@@ -625,9 +634,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       acc ^= 1;
       if (acc == 0) aphase ^= 1u;
     }
-    if (gi < n) {
-      float* od = cand_d + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
-      int* oj = cand_j + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
+    if (qv) {
+      float* od = cand_d + (static_cast<i64>(blockIdx.y) * nq + qr) * kCand;
+      int* oj = cand_j + (static_cast<i64>(blockIdx.y) * nq + qr) * kCand;
       for (int q = 0; q < kCand; ++q) {
         od[q] = lst_d[q * kM + r];
         oj[q] = lst_j[q * kM + r];
@@ -639,10 +648,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   if (warp == 1) tmem_dealloc(tmem, 2 * kN);
 }
 
-size_t knn_tc2_smem(int nt) {
+size_t knn_tc2_smem(int nt, int kc = 32) {
   const size_t stage = 2 * static_cast<size_t>(tc2::kTile) + 2 * static_cast<size_t>(nt) * 128;
-  const size_t stages = nt == 128 ? 3 : 2;
-  return stages * stage + kCand * tc::kM * (sizeof(float) + sizeof(int)) + static_cast<size_t>(nt) * 12;
+  const size_t stages = (nt == 128 && kc == 32) ? 3 : 2;
+  return stages * stage + static_cast<size_t>(kc) * tc::kM * (sizeof(float) + sizeof(int)) +
+         static_cast<size_t>(nt) * 12;
 }
 
 namespace {
@@ -687,9 +697,45 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
   const CUtensorMap mhb = point_map(H, n, dp, nt), mlb = point_map(L, n, dp, nt);
   const size_t smem = knn_tc2_smem(nt);
   const dim3 grid(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits));
-  ensure_smem(knn_tc_filter2_k<128>, smem);
-  knn_tc_filter2_k<128><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps), cd,
-                                                                   cj, max_norm_bits, stagger, dbg);
+  ensure_smem(knn_tc_filter2_k<128, 32>, smem);
+  knn_tc_filter2_k<128, 32><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
+                                                                       cd, cj, max_norm_bits, stagger, dbg, nullptr, n);
+  launched(c);
+}
+
+// Second pass: the nq queries Hq / Lq (rows qidx of H / L, gathered) against
+// every point with 64-candidate lists.
+void knn_tc_filter2_rows(Ctx* c, const float* Hq, const float* Lq, const int* qidx, i64 nq, const float* H,
+                         const float* L, const double* sq, i64 n, i64 dp, i64 splits, float* cd, int* cj,
+                         const unsigned long long* max_norm_bits) {
+  if (n > INT32_MAX || dp > INT32_MAX || nq > INT32_MAX) invalid("knn: tensor-core filter size out of range");
+  const int nt = 128;
+  const i64 nt_tiles = (n + nt - 1) / nt;
+  const i64 tps = (nt_tiles + splits - 1) / splits;
+  const CUtensorMap mh = point_map(Hq, nq, dp), ml = point_map(Lq, nq, dp);
+  const CUtensorMap mhb = point_map(H, n, dp, nt), mlb = point_map(L, n, dp, nt);
+  const size_t smem = knn_tc2_smem(nt, 64);
+  const dim3 grid(static_cast<unsigned>((nq + 127) / 128), static_cast<unsigned>(splits));
+  ensure_smem(knn_tc_filter2_k<128, 64>, smem);
+  knn_tc_filter2_k<128, 64><<<grid, tc2::kThreads, smem, c->stream>>>(mh, ml, mhb, mlb, sq, n, dp, static_cast<int>(tps),
+                                                                       cd, cj, max_norm_bits, 1, 0, qidx, nq);
+  launched(c);
+}
+
+// Hq[q] = H[qidx[q]], Lq[q] = L[qidx[q]] (dp floats per row).
+__global__ void gather_rows_k(const float* __restrict__ H, const float* __restrict__ L, const int* __restrict__ qidx,
+                              i64 nq, i64 dp, float* __restrict__ Hq, float* __restrict__ Lq) {
+  const i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (t >= nq * dp) return;
+  const i64 q = t / dp, k = t - q * dp;
+  const i64 src = static_cast<i64>(qidx[q]) * dp + k;
+  Hq[t] = H[src];
+  Lq[t] = L[src];
+}
+
+void gather_point_rows(Ctx* c, const float* H, const float* L, const int* qidx, i64 nq, i64 dp, float* Hq, float* Lq) {
+  if (nq == 0) return;
+  gather_rows_k<<<blocks_for(nq * dp), kBlock, 0, c->stream>>>(H, L, qidx, nq, dp, Hq, Lq);
   launched(c);
 }
 

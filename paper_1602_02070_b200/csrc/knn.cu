@@ -417,6 +417,10 @@ void split_points(Ctx* c, const double* Pm, i64 n, i64 d, i64 dp, float* H, floa
 size_t knn_tc_smem();
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
                     i64 tps, float* cd, int* cj, const unsigned long long* max_norm_bits);
+void knn_tc_filter2_rows(Ctx* c, const float* Hq, const float* Lq, const int* qidx, i64 nq, const float* H,
+                         const float* L, const double* sq, i64 n, i64 dp, i64 splits, float* cd, int* cj,
+                         const unsigned long long* max_norm_bits);
+void gather_point_rows(Ctx* c, const float* H, const float* L, const int* qidx, i64 nq, i64 dp, float* Hq, float* Lq);
 __global__ void knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
                                 const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split,
                                 float* __restrict__ cand_d, int* __restrict__ cand_j);
@@ -426,20 +430,21 @@ __global__ void max_norm_k(const double* __restrict__ sq, i64 n, unsigned long l
   if (i < n) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(sqrt(sq[i]))));
 }
 
-// Merge the per-split sorted approximate lists of each point (first kCandTc).
-__global__ void tc_merge_k(i64 n, int splits, const float* __restrict__ cd, const int* __restrict__ cj,
+// Merge the per-split sorted approximate lists of each query (first KC).
+template <int KC>
+__global__ void tc_merge_k(i64 nq, int splits, const float* __restrict__ cd, const int* __restrict__ cj,
                            float* __restrict__ md, int* __restrict__ mj) {
   const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  if (i >= n) return;
+  if (i >= nq) return;
   int pos[64];
   for (int s = 0; s < splits; ++s) pos[s] = 0;
-  for (int q = 0; q < kCandTc; ++q) {
+  for (int q = 0; q < KC; ++q) {
     int bs = -1;
     float bd = CUDART_INF_F;
     int bj = INT32_MAX;
     for (int s = 0; s < splits; ++s) {
-      if (pos[s] >= kCandTc) continue;
-      const i64 at = (static_cast<i64>(s) * n + i) * kCandTc + pos[s];
+      if (pos[s] >= KC) continue;
+      const i64 at = (static_cast<i64>(s) * nq + i) * KC + pos[s];
       const float dv = cd[at];
       const int jv = cj[at];
       if (bs < 0 || dv < bd || (dv == bd && jv < bj)) {
@@ -449,59 +454,81 @@ __global__ void tc_merge_k(i64 n, int splits, const float* __restrict__ cd, cons
       }
     }
     pos[bs]++;
-    md[i * kCandTc + q] = bd;
-    mj[i * kCandTc + q] = bj;
+    md[i * KC + q] = bd;
+    mj[i * KC + q] = bj;
   }
 }
 
-// One warp per point, lane q = q-th approximate candidate.  The window
-// [.., D_K + 2E] with E a rigorous bound of the 3xTF32 distance error
-// contains every true top-K neighbour; if the whole list lies inside the
-// window some candidate may be missing and the point is deferred to the
-// exact path (overflow[i] = 1).  Otherwise the candidates inside the window
-// get the canonical fp64 distance (sequential k, no FMA) and the K smallest
-// (d2, j) are selected exactly.
-__global__ void tc_rerank_k(const double* __restrict__ Pm, const double* __restrict__ sq, i64 n, i64 d, int K,
-                            double cg, const unsigned long long* __restrict__ maxnorm_bits,
-                            const float* __restrict__ md, const int* __restrict__ mj, int64_t* __restrict__ nbr,
-                            double* __restrict__ nbr_d2, double* __restrict__ mean_d2, int* __restrict__ overflow,
-                            int* __restrict__ dup) {
-  const i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+// One warp per query, lane l holds candidates l, l + 32, ... (KC / 32 per
+// lane).  The window [.., D_K + 2E] with E a rigorous bound of the 3xTF32
+// distance error contains every true top-K neighbour; if the whole list lies
+// inside the window some candidate may be missing and the point is deferred
+// (overflow[q] = 1: a second pass with longer lists, then the exact path).
+// Otherwise the candidates inside the window get the canonical fp64 distance
+// (sequential k, no FMA) and the K smallest (d2, j) are selected exactly.
+// qidx (null = identity) maps query q to its point; rows of nbr / nbr_d2 /
+// mean_d2 / dup are indexed by point.
+template <int KC>
+__global__ void tc_rerank_k(const double* __restrict__ Pm, const double* __restrict__ sq, i64 nq,
+                            const int* __restrict__ qidx, i64 d, int K, double cg,
+                            const unsigned long long* __restrict__ maxnorm_bits, const float* __restrict__ md,
+                            const int* __restrict__ mj, int64_t* __restrict__ nbr, double* __restrict__ nbr_d2,
+                            double* __restrict__ mean_d2, int* __restrict__ overflow, int* __restrict__ dup) {
+  constexpr int QPL = KC / 32;
+  const i64 q = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (i >= n) return;
+  if (q >= nq) return;
+  const i64 i = qidx ? static_cast<i64>(qidx[q]) : q;
   const double maxnorm = __longlong_as_double(static_cast<long long>(*maxnorm_bits));
-  const float dq = md[i * kCandTc + lane];
-  const int jq = mj[i * kCandTc + lane];
-  const double DK = static_cast<double>(__shfl_sync(0xffffffffu, dq, K - 1));
-  const double last = static_cast<double>(__shfl_sync(0xffffffffu, dq, kCandTc - 1));
+  float dq[QPL];
+  int jq[QPL];
+#pragma unroll
+  for (int t = 0; t < QPL; ++t) {
+    dq[t] = md[q * KC + t * 32 + lane];
+    jq[t] = mj[q * KC + t * 32 + lane];
+  }
+  const double DK = static_cast<double>(__shfl_sync(0xffffffffu, dq[0], K - 1));  // K <= 32
+  const double last = static_cast<double>(__shfl_sync(0xffffffffu, dq[QPL - 1], 31));
   const double E = 2.0 * cg * sqrt(sq[i]) * maxnorm;
   const double W = DK + fabs(DK) * 0x1.0p-22 + 2.0 * E;  // + float rounding of the stored d~
   const bool ovf = last - fabs(last) * 0x1.0p-22 <= W;
   if (ovf) {
-    if (lane == 0) overflow[i] = 1;
+    if (lane == 0) overflow[q] = 1;
     return;
   }
-  const double dql = static_cast<double>(dq) - fabs(static_cast<double>(dq)) * 0x1.0p-22;
-  double ex = CUDART_INF;
-  if (jq != INT32_MAX && dql <= W) {
-    const double* a = Pm + i * d;
-    const double* b = Pm + static_cast<i64>(jq) * d;
-    double g = 0.0;
-    for (i64 k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(a[k], b[k]));
-    const double t = __dsub_rn(__dadd_rn(sq[i], sq[jq]), __dmul_rn(2.0, g));
-    ex = t > 0.0 ? t : 0.0;
-    if (ex == 0.0 && jq < i) {
-      bool same = true;
-      for (i64 k = 0; k < d && same; ++k) same = a[k] == b[k];
-      if (same) dup[i] = 1;
+  double ex[QPL];
+  int jc[QPL];
+#pragma unroll
+  for (int t = 0; t < QPL; ++t) {
+    const double dql = static_cast<double>(dq[t]) - fabs(static_cast<double>(dq[t])) * 0x1.0p-22;
+    ex[t] = CUDART_INF;
+    jc[t] = INT32_MAX;
+    if (jq[t] != INT32_MAX && dql <= W) {
+      const double* a = Pm + i * d;
+      const double* b = Pm + static_cast<i64>(jq[t]) * d;
+      double g = 0.0;
+      for (i64 k = 0; k < d; ++k) g = __dadd_rn(g, __dmul_rn(a[k], b[k]));
+      const double tt = __dsub_rn(__dadd_rn(sq[i], sq[jq[t]]), __dmul_rn(2.0, g));
+      ex[t] = tt > 0.0 ? tt : 0.0;
+      jc[t] = jq[t];
+      if (ex[t] == 0.0 && jq[t] < i) {
+        bool same = true;
+        for (i64 k = 0; k < d && same; ++k) same = a[k] == b[k];
+        if (same) dup[i] = 1;
+      }
     }
   }
   // K rounds of a lexicographic warp argmin.
   double m = 0.0;
-  int jcur = ex < CUDART_INF ? jq : INT32_MAX;
-  for (int q = 0; q < K; ++q) {
-    double bv = ex;
-    int bj = jcur;
+  for (int r = 0; r < K; ++r) {
+    double bv = CUDART_INF;
+    int bj = INT32_MAX;
+#pragma unroll
+    for (int t = 0; t < QPL; ++t)
+      if (ex[t] < bv || (ex[t] == bv && jc[t] < bj)) {
+        bv = ex[t];
+        bj = jc[t];
+      }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -512,14 +539,16 @@ __global__ void tc_rerank_k(const double* __restrict__ Pm, const double* __restr
       }
     }
     if (lane == 0) {
-      nbr[i * K + q] = bj;
-      nbr_d2[i * K + q] = bv;
+      nbr[i * K + r] = bj;
+      nbr_d2[i * K + r] = bv;
     }
     m = __dadd_rn(m, bv);
-    if (jcur == bj) {
-      ex = CUDART_INF;
-      jcur = INT32_MAX;
-    }
+#pragma unroll
+    for (int t = 0; t < QPL; ++t)
+      if (jc[t] == bj) {
+        ex[t] = CUDART_INF;
+        jc[t] = INT32_MAX;
+      }
   }
   if (lane == 0) mean_d2[i] = m;
 }
@@ -614,7 +643,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
       KScope ks_(c, "knn_tc_filter");
       knn_tc_filter2(c, H.p, L.p, sq.p, n, dp, q_tiles, splits, tps, cd.p, cj.p, mxn.p);
     }
-    tc_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(splits), cd.p, cj.p, md.p, mj.p);
+    tc_merge_k<kCandTc><<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(splits), cd.p, cj.p, md.p, mj.p);
     launched(c);
     // Rigorous bound on |G~ - G| / (|x_i| |x_j|): split error 3 * 2^-22 plus
     // fp32 accumulation of 3 d exact tf32 products, 2^-23 per addition
@@ -622,9 +651,10 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
     const double cg = 2.0 * (3.0 + 3.0 * static_cast<double>(d)) * 0x1.0p-23;
     {
       KScope ks_(c, "knn_tc_rerank");
-      tc_rerank_k<<<blocks_for(n * 32, 256), 256, 0, c->stream>>>(out->Pm.p, sq.p, n, d, static_cast<int>(K), cg,
-                                                                 mxn.p, md.p, mj.p, out->nbr.p, out->d2.p,
-                                                                 out->mean.p, ovf.p, dup.p);
+      tc_rerank_k<kCandTc><<<blocks_for(n * 32, 256), 256, 0, c->stream>>>(out->Pm.p, sq.p, n, nullptr, d,
+                                                                          static_cast<int>(K), cg, mxn.p, md.p, mj.p,
+                                                                          out->nbr.p, out->d2.p, out->mean.p, ovf.p,
+                                                                          dup.p);
       launched(c);
     }
     trace_mark(c, "knn: tc filter+merge+rerank");
@@ -634,10 +664,53 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
     std::vector<int> rows;
     for (i64 i = 0; i < n; ++i)
       if (of[i]) rows.push_back(static_cast<int>(i));
+    const size_t pass1_rows = rows.size();
+    const char* p2 = std::getenv("CPCAG_KNN_PASS2");
+    if (!rows.empty() && !(p2 && std::string(p2) == "0") && K <= 32) {
+      // Second pass for the uncertified points: their rows again on the
+      // tensor cores with 64-candidate lists, then the same certified re-rank.
+      trace_mark(c, "knn: pass-1 readback");
+      const i64 nq = static_cast<i64>(rows.size());
+      DevBuf<int> qd(c, nq), ovf2(c, nq);
+      CUDA_OK(cudaMemcpyAsync(qd.p, rows.data(), sizeof(int) * nq, cudaMemcpyHostToDevice, c->stream));
+      ovf2.zero(c);
+      DevBuf<float> Hq(c, nq * dp), Lq(c, nq * dp);
+      gather_point_rows(c, H.p, L.p, qd.p, nq, dp, Hq.p, Lq.p);
+      const i64 q2 = (nq + 127) / 128;
+      i64 s2 = std::max<i64>(1, static_cast<i64>(c->num_sms) / q2);
+      s2 = std::min<i64>({s2, n_tiles, 64});
+      const i64 tps2 = (n_tiles + s2 - 1) / s2;
+      s2 = (n_tiles + tps2 - 1) / tps2;
+      DevBuf<float> cd2(c, s2 * nq * 64), md2(c, nq * 64);
+      DevBuf<int> cj2(c, s2 * nq * 64), mj2(c, nq * 64);
+      {
+        KScope ks_(c, "knn_tc_filter_pass2");
+        knn_tc_filter2_rows(c, Hq.p, Lq.p, qd.p, nq, H.p, L.p, sq.p, n, dp, s2, cd2.p, cj2.p, mxn.p);
+      }
+      tc_merge_k<64><<<blocks_for(nq, 128), 128, 0, c->stream>>>(nq, static_cast<int>(s2), cd2.p, cj2.p, md2.p, mj2.p);
+      launched(c);
+      {
+        KScope ks_(c, "knn_tc_rerank");
+        tc_rerank_k<64><<<blocks_for(nq * 32, 256), 256, 0, c->stream>>>(out->Pm.p, sq.p, nq, qd.p, d,
+                                                                        static_cast<int>(K), cg, mxn.p, md2.p, mj2.p,
+                                                                        out->nbr.p, out->d2.p, out->mean.p, ovf2.p,
+                                                                        dup.p);
+        launched(c);
+      }
+      std::vector<int> of2(static_cast<size_t>(nq));
+      CUDA_OK(cudaMemcpyAsync(of2.data(), ovf2.p, sizeof(int) * nq, cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      std::vector<int> rest;
+      for (i64 q = 0; q < nq; ++q)
+        if (of2[q]) rest.push_back(rows[q]);
+      rows.swap(rest);
+      trace_mark(c, "knn: tc pass 2");
+    }
     out->tc_rows = n - static_cast<i64>(rows.size());
     if (std::getenv("CPCAG_TRACE"))
-      std::fprintf(stderr, "[knn] %lld points, %lld certified by the tensor-core filter, %zu exact fallback rows\n",
-                   static_cast<long long>(n), static_cast<long long>(out->tc_rows), rows.size());
+      std::fprintf(stderr, "[knn] %lld points, %lld certified by the tensor-core filter (%zu left by pass 1), "
+                   "%zu exact fallback rows\n", static_cast<long long>(n), static_cast<long long>(out->tc_rows),
+                   pass1_rows, rows.size());
     if (!rows.empty()) {
       DevBuf<int> qd(c, rows.size());
       CUDA_OK(cudaMemcpyAsync(qd.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice, c->stream));

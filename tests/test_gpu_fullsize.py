@@ -188,3 +188,33 @@ def test_cfg3_sharded_block_driver_matches_single_gpu(P, ctx):
                              ctx=ctx)
     assert one.iterations == its
     assert rel(Xs, one.X.cpu().numpy().astype(np.float64)) <= 1e-4
+
+
+def test_knn_second_tensor_core_pass_equals_exact_path(P, ctx, monkeypatch, capfd):
+    """Points the 32-candidate filter cannot certify go through a second
+    tensor-core pass with 64-candidate lists (knn.cu); its lists must equal
+    the exact fp64 path's (CPCAG_KNN_PASS2=0 sends them all there)."""
+    import re
+
+    import torch
+
+    from paper_1602_02070_b200 import workloads
+
+    X = workloads.config2_points()  # 100 000 x 512: ~2.3 % of the points need the second pass
+    d, n = X.shape
+    Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda").t()
+    monkeypatch.setenv("CPCAG_TRACE", "1")
+    capfd.readouterr()
+    nbr, d2 = P.knn(Xd, "cols", 10, ctx=ctx)
+    err = capfd.readouterr().err
+    m = re.search(r"\[knn\] (\d+) points, (\d+) certified by the tensor-core filter \((\d+) left by pass 1\), "
+                  r"(\d+) exact fallback rows", err)
+    assert m, err[-2000:]
+    left1, rest = int(m.group(3)), int(m.group(4))
+    assert left1 > 0 and rest < left1  # pass 2 certified some points
+    monkeypatch.setenv("CPCAG_KNN_PASS2", "0")
+    nbr0, d20 = P.knn(Xd, "cols", 10, ctx=ctx)
+    assert np.array_equal(nbr, nbr0) and np.array_equal(d2, d20)
+    rows = np.random.default_rng(11).choice(n, 24, replace=False)
+    onbr, od2 = O.knn_rows(X.astype(np.float64), False, 10, rows)
+    assert np.array_equal(nbr[rows], onbr) and np.array_equal(d2[rows], od2)
