@@ -118,6 +118,14 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
 }
 
+// One column: lane l gets TMEM lane (base lane + l) at column taddr (waits).
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  return __uint_as_float(r);
+}
+
 // Split form of tmem_ld32: issue, then wait (tcgen05.wait::ld covers every
 // outstanding load of the thread), so the next chunk loads while this one is
 // processed.
@@ -464,8 +472,6 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   if ((smem_u32(smem_raw) & 1023u) != 0u) asm volatile("trap;");
   float* lst_d = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // [kCand][128]
   int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);                // [kCand][128]
-  double* sqd = reinterpret_cast<double*>(lst_j + kCand * kM);            // [NT] candidate sq (fp64)
-  float* sqf = reinterpret_cast<float*>(sqd + NT);                        // [NT] candidate sq (fp32)
   __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -556,7 +562,6 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
   } else {  // ---- epilogue warps 2..5: TMEM lanes [32 (w % 4), +32)
     const int eq = warp & 3;
     const int r = eq * 32 + lane;
-    const int et = threadIdx.x - 64;  // 0..127 across the epilogue warps
     const i64 qr = i0 + r;            // query row
     const bool qv = qr < nq;
     const i64 gi = qv ? (qidx ? static_cast<i64>(qidx[qr]) : qr) : n;  // its point (n = none)
@@ -571,59 +576,80 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
     // thr and the exact test would skip it too.
     const double mxn = __longlong_as_double(static_cast<long long>(*max_norm_bits));
     const float margin = static_cast<float>(0x1.0p-20 * (sqi + mxn * mxn)) * 1.0001f;
-    float thr = CUDART_INF_F;
+    float thr = CUDART_INF_F;  // largest d in the (unsorted) list
+    int maxpos = 0;            // its slot
     int acc = 0;
     uint32_t aphase = 0;
-    static_assert(NT == 128, "one staged norm per epilogue thread");
-    auto norm_of = [&](i64 jt) -> double {
-      const i64 gj = jt * kN + et;
+    static_assert(NT == 128, "four candidate norms per lane");
+    // Candidate norms live in registers: lane l holds columns l + 32 k of the
+    // tile (fetched one tile ahead) and the warp reads them by shuffle, so the
+    // four epilogue warps never wait on one another.
+    auto norm_of = [&](i64 jt, int k) -> double {
+      const i64 gj = jt * kN + lane + 32 * k;
       return jt < jt1 && gj < n ? __ldg(sq + gj) : CUDART_INF;
     };
-    double nxt = norm_of(jt0);
+    double nd[4], nx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) nx[k] = norm_of(jt0, k);
     for (i64 jt = jt0; jt < jt1; ++jt) {
       const i64 j0 = jt * kN;
-      // stage the candidate tile's squared norms (padding columns: +inf); the
-      // next tile's norm is fetched now, its latency hidden by this tile
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      sqd[et] = nxt;
-      sqf[et] = static_cast<float>(nxt);
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      nxt = norm_of(jt + 1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        nd[k] = nx[k];
+        nx[k] = norm_of(jt + 1, k);
+      }
       mbar_wait_guarded(&tfull[acc], aphase);
       fence_after();
       const uint32_t tbase = tmem + (static_cast<uint32_t>(32 * eq) << 16) + static_cast<uint32_t>(acc * kN);
-#pragma unroll 1
-      for (int c0 = 0; c0 < kN; c0 += 32) {
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c0 = 32 * cc;
         float v[32];
         tmem_ld32(tbase + static_cast<uint32_t>(c0), v);
-        if (qv && dbg != 1) {
-          float e[32];
-          float mn = CUDART_INF_F;
+        // fast path: one bit per column whose fp32 estimate passes the
+        // quick reject (a superset of what the exact test below accepts)
+        const float nf = static_cast<float>(nd[cc]);
+        const float lim = thr + margin;
+        unsigned m = 0;
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
-            e[q] = fmaf(-2.0f, v[q], sqi_f + sqf[c0 + q]);
-            mn = fminf(mn, e[q]);
-          }
-          if (mn <= thr + margin) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              if (!(e[q] <= thr + margin)) continue;
-              const i64 gj = j0 + c0 + q;
-              if (gj >= n || gj == gi) continue;
-              const double dd = (sqi + sqd[c0 + q]) - 2.0 * static_cast<double>(v[q]);
-              const float df = static_cast<float>(dd);
-              if (!(df < thr)) continue;
-              int pos = kCand - 1;
-              while (pos > 0) {
-                const float pd = lst_d[(pos - 1) * kM + r];
-                if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
-                lst_d[pos * kM + r] = pd;
-                lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
-                --pos;
+        for (int q = 0; q < 32; ++q) {
+          const float e = fmaf(-2.0f, v[q], sqi_f + __shfl_sync(0xffffffffu, nf, q));
+          m |= (e <= lim ? 1u : 0u) << q;
+        }
+        if (!qv || dbg == 1) m = 0;
+        // slow path, warp-uniform and not unrolled: columns any lane kept, in
+        // ascending order (the order the lists are built in)
+        unsigned wm = __reduce_or_sync(0xffffffffu, m);
+        while (wm) {
+          const int q = __ffs(wm) - 1;
+          wm &= wm - 1u;
+          const float vq = tmem_ld1(tbase + static_cast<uint32_t>(c0 + q));
+          const double sqj = __shfl_sync(0xffffffffu, nd[cc], q);
+          const i64 gj = j0 + c0 + q;
+          if (((m >> q) & 1u) && gj < n && gj != gi) {
+            const double dd = (sqi + sqj) - 2.0 * static_cast<double>(vq);
+            const float df = static_cast<float>(dd);
+            if (df < thr) {
+              // the list is unsorted: the candidate replaces the
+              // lexicographic (d, j) maximum, then the maximum is found again
+              // (independent loads, no shifting chain).  Candidates arrive in
+              // increasing j, so this keeps exactly the (d, j)-smallest kCand.
+              lst_d[maxpos * kM + r] = df;
+              lst_j[maxpos * kM + r] = static_cast<int>(gj);
+              float bd = lst_d[r];
+              int bj = lst_j[r], bp = 0;
+#pragma unroll 8
+              for (int t = 1; t < kCand; ++t) {
+                const float td = lst_d[t * kM + r];
+                const int tj = lst_j[t * kM + r];
+                if (td > bd || (td == bd && tj > bj)) {
+                  bd = td;
+                  bj = tj;
+                  bp = t;
+                }
               }
-              lst_d[pos * kM + r] = df;
-              lst_j[pos * kM + r] = static_cast<int>(gj);
-              thr = lst_d[(kCand - 1) * kM + r];
+              thr = bd;
+              maxpos = bp;
             }
           }
         }
@@ -635,6 +661,22 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
       if (acc == 0) aphase ^= 1u;
     }
     if (qv) {
+      // sort the row's list by (d, j) once (insertion sort in place)
+      for (int t = 1; t < kCand; ++t) {
+        const float dv = lst_d[t * kM + r];
+        const int jv = lst_j[t * kM + r];
+        int pos = t;
+        while (pos > 0) {
+          const float pd = lst_d[(pos - 1) * kM + r];
+          const int pj = lst_j[(pos - 1) * kM + r];
+          if (pd < dv || (pd == dv && pj < jv)) break;
+          lst_d[pos * kM + r] = pd;
+          lst_j[pos * kM + r] = pj;
+          --pos;
+        }
+        lst_d[pos * kM + r] = dv;
+        lst_j[pos * kM + r] = jv;
+      }
       float* od = cand_d + (static_cast<i64>(blockIdx.y) * nq + qr) * kCand;
       int* oj = cand_j + (static_cast<i64>(blockIdx.y) * nq + qr) * kCand;
       for (int q = 0; q < kCand; ++q) {
@@ -651,8 +693,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1)
 size_t knn_tc2_smem(int nt, int kc = 32) {
   const size_t stage = 2 * static_cast<size_t>(tc2::kTile) + 2 * static_cast<size_t>(nt) * 128;
   const size_t stages = (nt == 128 && kc == 32) ? 3 : 2;
-  return stages * stage + static_cast<size_t>(kc) * tc::kM * (sizeof(float) + sizeof(int)) +
-         static_cast<size_t>(nt) * 12;
+  return stages * stage + static_cast<size_t>(kc) * tc::kM * (sizeof(float) + sizeof(int));
 }
 
 namespace {
