@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "frpcag.cuh"
 #include "fista_tc.cuh"
+#include "fista_persist.cuh"
 
 namespace cpcag_cuda {
 
@@ -703,6 +704,26 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   }
   dim3 gd(static_cast<unsigned>((rows + kDT - 1) / kDT), static_cast<unsigned>((cols + kDT - 1) / kDT));
   if (dense) part.alloc(c, 3 * static_cast<size_t>(std::max<unsigned>(gd.x * gd.y, nb1)));
+  // fp32 dense: the whole solve as one cooperative kernel (fista_persist.cu)
+  // when the tiling fits; otherwise the per-kernel paths below.
+  if constexpr (sizeof(T) == 4) {
+    FistaPersistOut pres{};
+    if (dense && fista_persist_enabled() &&
+        fista_persist_run(c, Y, rows, cols, Dr.p, Dc.p, cfg, step, X, tr.p, &pres)) {
+      if (pres.err)
+        runtime("fista: diverged (non-finite objective at iteration " + std::to_string(pres.iterations) +
+                "); step too large");
+      const i64 J = pres.iterations;
+      if (objective_host && J > 0)
+        CUDA_OK(cudaMemcpyAsync(objective_host, tr.p, sizeof(double) * J, cudaMemcpyDefault, c->stream));
+      sync(c);
+      trace->iterations = J;
+      trace->converged = pres.converged;
+      trace->final_rel_change = pres.frc;
+      trace->step = step;
+      return;
+    }
+  }
   // fp32: split the k-space so the grid covers ~6 CTAs per SM.
   const bool splitk = dense && sizeof(T) == 4;
   DevBuf<float> sp1, sp2;

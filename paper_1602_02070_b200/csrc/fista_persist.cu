@@ -1,0 +1,494 @@
+// fista_persist.cu -- the whole FISTA solve (frpcag.cpp:62-112, Algorithm 1
+// of the paper) as ONE cooperative kernel, for the fp32
+// path with dense Kron-reduced Laplacians (config 1: 1031 x 100, L~_r 56 %
+// full, L~_c 100 % full).
+//
+// Why: at config-1 size one iteration is ~230 MFLOP and ~400 KB of state, so
+// the per-kernel path (4 launches per iteration, split-K partial sums through
+// HBM) is launch- and latency-bound at ~47 us per iteration.  Here the grid
+// is one CTA per SM, each CTA owns an output tile (TM rows x TN columns) of
+// every m-sized array for the whole solve, and an iteration costs one grid
+// barrier:
+//
+//   phase A (tile-local)  S_j = prox(Z_j - step * 2 H(Z_j), Y, step)
+//                         -> tile of S_j to global (column- and row-major)
+//   grid barrier          (S_j complete; partial sums of iteration j-1 visible)
+//   reduce j-1            objective, finite check, trace, stop test of j-1
+//   phase B (tile GEMM)   H(S_j) = g_r L~_r S_j + g_c S_j L~_c for the tile:
+//                         g_r L~_r rows resident in shared memory, S_j column
+//                         panel streamed in k-chunks with cp.async (L2 -> smem)
+//   phase B (tile-local)  objective partials, t_{j+1}, Z_{j+1} = S + coef
+//                         (S - S_prev), H(Z_{j+1}) by linearity,
+//                         ||Z_j||^2, ||Z_{j+1} - Z_j||^2 partials
+//
+// H = g_c S L~_c + g_r L~_r S is the only combination the solve reads: the
+// gradient is 2 H(Z) (frpcag.cpp:53-60 with s = 2 g) and the two objective
+// penalties are sum H(S) o S (frpcag.cpp:27-33; L~_c is exactly symmetric,
+// so (L~_c S^T) o S^T sums like (S L~_c) o S).  The operators are pre-scaled
+// by their weights once.  All reductions are fixed-order (per-CTA block
+// sums, partials summed in block order by every CTA), so the run is
+// deterministic and every CTA takes the same stop decision.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "fista_persist.cuh"
+#include "frpcag.cuh"
+
+namespace cpcag_cuda {
+
+namespace {
+
+constexpr int kPT = 256;      // threads per CTA
+constexpr int kPartRegs = 5;  // partial-sum loads per lane: grid <= 160 CTAs
+
+struct PersistArgs {
+  int rr, rc, ldS, ldT;
+  int TM, TN, C, KS, KC;
+  int use_r, use_c, loss;
+  int dbg;  // diagnostics (CPCAG_FISTA_PERSIST_DBG): 1 = no B chunk loads, 2 = no chunk FMAs
+  float step;
+  double tol;
+  i64 max_iter;
+  double gamma_r, gamma_c;
+  const float* Dr;  // rr x rr dense, exactly symmetric
+  const float* Dc;  // rc x rc dense, exactly symmetric
+  const float* Y;   // rr x rc column-major
+  float* Sg[2];     // S_j column-major, ldS rows (padding rows stay 0)
+  float* SgT[2];    // S_j row-major, ldT columns (padding stays 0)
+  double* part;     // [2][grid][4] per-CTA partial sums by iteration parity
+  double* trace;    // objective per iteration
+  float* X;         // output, rr x rc column-major
+  FistaPersistOut* out;
+  unsigned* bar;    // grid barrier count, generation
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void fma44(float (&acc)[4][4], const float4 a, const float4 b) {
+  const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(av[x], bv[y], acc[x][y]);
+}
+
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// acc += sum over cnt k-steps of a(k) b(k)^T, a/b float4 strips at strides
+// sa/sb, k ascending.  (Prefetching the operands four k-steps ahead measured
+// slower: the loop is bound by shared-memory wavefronts, ncu: 4.4 per LDS.128.)
+__device__ __forceinline__ void strip_gemm(float (&acc)[4][4], const float* ap, int sa, const float* bp, int sb,
+                                           int cnt) {
+#pragma unroll 4
+  for (int q = 0; q < cnt; ++q) fma44(acc, lds4(ap + q * sa), lds4(bp + q * sb));
+}
+
+__global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
+  extern __shared__ __align__(16) float sm[];
+  __shared__ double tot_sh[4];
+  const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int TM = a.TM, TN = a.TN, TE = TM * TN, rr = a.rr, rc = a.rc, KC = a.KC, KS = a.KS;
+  const int rb = blockIdx.x / a.C, cb = blockIdx.x % a.C;
+  const int r0 = rb * TM, c0 = cb * TN;
+  const int rn = min(TM, rr - r0), cn = min(TN, rc - c0);
+  float* As = sm;                                     // [rr][TM]  g_r L~_r(r0 + i, k)
+  float* Bc = As + static_cast<size_t>(rr) * TM;      // [rc][TN]  g_c L~_c(k, c0 + j)
+  float* A2 = Bc + static_cast<size_t>(rc) * TN;      // [rc][TM]  S(r0 + i, k)
+  float* Bb = A2 + static_cast<size_t>(rc) * TM;      // [2][KC][TN]  S(k, c0 + j)
+  float* red = Bb + 2 * static_cast<size_t>(KC) * TN;  // [KS][TE]  split-k partials
+  float* Yt = red + static_cast<size_t>(KS) * TE;     // tile state, e = i + TM j
+  float* Zt = Yt + TE;                                // Z_j
+  float* HZ = Zt + TE;                                // H(Z_j)
+  float* Sp = HZ + TE;                                // S_{j-1}
+  float* Hp = Sp + TE;                                // H(S_{j-1})
+  float* Sc = Hp + TE;                                // S_j
+
+  // ---- one-time staging of the pre-scaled operators and the tile of Y
+  if (a.use_r)
+    for (int t = tid; t < rr * TM; t += kPT) {
+      const int k = t / TM, i = t - k * TM;
+      // L~_r(r0 + i, k) from the column-major dense copy (contiguous in i)
+      As[t] = i < rn ? static_cast<float>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
+                     : 0.f;
+    }
+  if (a.use_c)
+    for (int t = tid; t < rc * TN; t += kPT) {
+      const int k = t / TN, j = t - k * TN;
+      Bc[t] = j < cn ? static_cast<float>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
+                     : 0.f;
+    }
+  for (int e = tid; e < TE; e += kPT) {
+    const int j = e / TM, i = e - j * TM;
+    const bool ok = i < rn && j < cn;
+    const float y = ok ? a.Y[(r0 + i) + static_cast<i64>(c0 + j) * rr] : 0.f;
+    Yt[e] = y;
+    Zt[e] = y;  // Z_1 = Y
+    Sp[e] = y;  // S_0 = Y
+    Sc[e] = y;
+    if (ok) {
+      a.Sg[0][(r0 + i) + static_cast<i64>(c0 + j) * a.ldS] = y;
+      a.SgT[0][(c0 + j) + static_cast<i64>(r0 + i) * a.ldT] = y;
+    }
+  }
+
+  // ---- tile GEMM: red[s] = partial H of the tile over the k-slice of split s
+  const int nmi = TM / 4, NMT = nmi * (TN / 4);
+  const bool gthr = tid < NMT * KS;
+  const int mt = tid % NMT, s = tid / NMT, mi = mt % nmi, ni = mt / nmi;
+  auto tile_gemm = [&](const float* Sbuf, const float* SbufT) {
+    float acc[4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+    const int q4m = TM / 4, q4n = TN / 4;
+    if (a.use_c)  // S(r0.., k) for every k: TM contiguous floats per column k
+      for (int t = tid; t < rc * q4m; t += kPT) {
+        const int k = t / q4m, q = t - k * q4m;
+        cp_async16(A2 + k * TM + 4 * q, Sbuf + (r0 + 4 * q) + static_cast<i64>(k) * a.ldS);
+      }
+    const int nch = a.use_r ? (rr + KC - 1) / KC : 0;
+    auto issue_chunk = [&](int ch) {
+      const int k0 = ch * KC, kl = min(KC, rr - k0);
+      float* dst = Bb + (ch & 1) * KC * TN;
+      for (int t = tid; t < kl * q4n; t += kPT) {
+        const int k = t / q4n, q = t - k * q4n;
+        cp_async16(dst + k * TN + 4 * q, SbufT + (c0 + 4 * q) + static_cast<i64>(k0 + k) * a.ldT);
+      }
+    };
+    if (nch > 0 && !(a.dbg & 1)) issue_chunk(0);
+    cp_async_commit();
+    for (int ch = 0; ch < nch; ++ch) {
+      if (ch + 1 < nch) {
+        if (!(a.dbg & 1)) issue_chunk(ch + 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      if (gthr && !(a.dbg & 2)) {
+        const int k0 = ch * KC, kl = min(KC, rr - k0);
+        const int cnt = s < kl ? (kl - 1 - s) / KS + 1 : 0;
+        strip_gemm(acc, As + static_cast<size_t>(k0 + s) * TM + 4 * mi, KS * TM,
+                   Bb + (ch & 1) * KC * TN + s * TN + 4 * ni, KS * TN, cnt);
+      }
+      __syncthreads();
+    }
+    if (nch == 0) {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    if (a.use_c && gthr) {
+      const int cnt = s < rc ? (rc - 1 - s) / KS + 1 : 0;
+      strip_gemm(acc, A2 + s * TM + 4 * mi, KS * TM, Bc + s * TN + 4 * ni, KS * TN, cnt);
+    }
+    if (gthr) {
+      float* o = red + static_cast<size_t>(s) * TE;
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) o[(4 * mi + x) + TM * (4 * ni + y)] = acc[x][y];
+    }
+    __syncthreads();
+  };
+  auto tile_h = [&](int e) {
+    float h = 0.f;
+    for (int q = 0; q < KS; ++q) h += red[q * TE + e];
+    return h;
+  };
+
+  // ---- H(Y): Z_1 = S_0 = Y, so H(Z_1) = H(S_0)
+  grid_barrier(&a.bar[0], &a.bar[1]);
+  tile_gemm(a.Sg[0], a.SgT[0]);
+  for (int e = tid; e < TE; e += kPT) {
+    const float h = tile_h(e);
+    HZ[e] = h;
+    Hp[e] = h;
+  }
+  __syncthreads();
+
+  const float step = a.step;
+  // phase timers (CTA 0, thread 0; read by tools/fista_diag.py)
+  unsigned long long pt[5] = {0, 0, 0, 0, 0}, tq = gtimer_ns();
+  auto mark = [&](int ph) {
+    if (tid == 0) {
+      const unsigned long long now = gtimer_ns();
+      pt[ph] += now - tq;
+      tq = now;
+    }
+  };
+  double t = 1.0;
+  i64 J = 0;
+  int conv = 0, err = 0;
+  double frc = 0.0;
+  for (i64 j = 1;; ++j) {
+    const int b = static_cast<int>(j & 1);
+    if (j <= a.max_iter) {
+      // ---- phase A: gradient step + prox (frpcag.cpp:82-88)
+      float* Sgb = a.Sg[b];
+      float* SgTb = a.SgT[b];
+      for (int e = tid; e < TE; e += kPT) {
+        const int jj = e / TM, i = e - jj * TM;
+        if (i < rn && jj < cn) {
+          const float g = 2.f * HZ[e];
+          const float arg = __fsub_rn(Zt[e], __fmul_rn(step, g));
+          const float y = Yt[e];
+          const float sv = a.loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, y, step) : prox_l1_elem(arg, y, step);
+          Sc[e] = sv;
+          Sgb[(r0 + i) + static_cast<i64>(c0 + jj) * a.ldS] = sv;
+          SgTb[(c0 + jj) + static_cast<i64>(r0 + i) * a.ldT] = sv;
+        }
+      }
+    }
+    mark(0);
+    grid_barrier(&a.bar[0], &a.bar[1]);
+    mark(1);
+    // partial sums of iteration j-1: loads issued now, consumed after the
+    // tile GEMM (their L2 latency hides behind it)
+    double pv[kPartRegs][4];
+    const double* pp = a.part + static_cast<size_t>((j - 1) & 1) * G * 4;
+    if (j >= 2 && warp == 0)
+#pragma unroll
+      for (int r = 0; r < kPartRegs; ++r) {
+        const int q = lane + 32 * r;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pv[r][u] = q < G ? __ldcg(pp + q * 4 + u) : 0.0;
+      }
+    // ---- phase B GEMM: H(S_j) (frpcag.cpp:89-90 penalties, linearity for Z)
+    if (j <= a.max_iter) tile_gemm(a.Sg[b], a.SgT[b]);
+    mark(3);
+    if (j >= 2) {
+      // ---- iteration j-1: objective, divergence, trace, stop test
+      //      (frpcag.cpp:89-106)
+      if (warp == 0) {
+        double v[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < kPartRegs; ++r)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] += pv[r][u];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = warp_sum(v[u]);
+        if (lane == 0)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tot_sh[u] = v[u];
+      }
+      __syncthreads();
+      const double obj = tot_sh[0] + tot_sh[1];
+      const double denom = tot_sh[2], change = tot_sh[3];
+      __syncthreads();
+      J = j - 1;
+      if (!isfinite(obj)) {
+        err = 1;
+        break;
+      }
+      if (blockIdx.x == 0 && tid == 0) a.trace[j - 2] = obj;
+      frc = denom > 0.0 ? change / denom : change;
+      if (change < a.tol * denom) {
+        conv = 1;
+        break;
+      }
+    }
+    if (j > a.max_iter) break;
+    mark(2);
+
+    // ---- phase B element-wise: objective partials, momentum (frpcag.cpp:89-110)
+    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    const float coef = static_cast<float>((t - 1.0) / tn);
+    t = tn;
+    double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int e = tid; e < TE; e += kPT) {
+      const int jj = e / TM, i = e - jj * TM;
+      if (i < rn && jj < cn) {
+        const float h = tile_h(e);
+        const float sv = Sc[e];
+        const double d = static_cast<double>(Yt[e]) - static_cast<double>(sv);
+        acc4[0] += a.loss == CPCAG_LOSS_L2 ? d * d : fabs(d);
+        acc4[1] += static_cast<double>(h) * static_cast<double>(sv);
+        const float zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[e])));
+        const float hz = add_rn(h, mul_rn(coef, sub_rn(h, Hp[e])));
+        const float z = Zt[e];
+        const double zd = static_cast<double>(z), dd = static_cast<double>(sub_rn(zn, z));
+        acc4[2] += zd * zd;
+        acc4[3] += dd * dd;
+        Sp[e] = sv;
+        Hp[e] = h;
+        Zt[e] = zn;
+        HZ[e] = hz;
+      }
+    }
+    block_sum<4>(acc4);
+    if (tid == 0) {
+      double* pp = a.part + static_cast<size_t>(j & 1) * G * 4 + static_cast<size_t>(blockIdx.x) * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pp[u] = acc4[u];
+    }
+    mark(4);
+  }
+  // ---- output: the last prox result S_J (frpcag.cpp:111), own tile
+  if (J >= 1 && !err) {
+    const float* Sgb = a.Sg[J & 1];
+    for (int e = tid; e < TE; e += kPT) {
+      const int jj = e / TM, i = e - jj * TM;
+      if (i < rn && jj < cn)
+        a.X[(r0 + i) + static_cast<i64>(c0 + jj) * rr] = Sgb[(r0 + i) + static_cast<i64>(c0 + jj) * a.ldS];
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    a.out->iterations = J;
+    a.out->converged = conv;
+    a.out->err = err;
+    a.out->frc = frc;
+#pragma unroll
+    for (int u = 0; u < 5; ++u) a.out->prof_ns[u] = pt[u];
+  }
+}
+
+struct Geom {
+  int TM, TN, R, C, KS, KC;
+  size_t smem;
+};
+
+size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int KS, int KC) {
+  const size_t TE = static_cast<size_t>(TM) * TN;
+  return 4 * (static_cast<size_t>(rr) * TM + static_cast<size_t>(rc) * TN + static_cast<size_t>(rc) * TM +
+              2 * static_cast<size_t>(KC) * TN + static_cast<size_t>(KS) * TE + 6 * TE);
+}
+
+// Picks the tile shape: R x C CTAs (at most one per SM), TM/TN multiples of
+// 4, every CTA holding its g_r L~_r rows; minimises the per-CTA multiply-add
+// count TM TN (rr + rc) within the shared-memory budget.
+bool plan_geom(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
+  bool found = false;
+  double best = 0.0;
+  const i64 sms = c->num_sms;
+  for (i64 TN = 4; TN <= ((rc + 3) / 4) * 4; TN += 4) {
+    const i64 C = (rc + TN - 1) / TN;
+    if (C > sms) continue;
+    if ((rc + C - 1) / C + 3 < TN) continue;  // same C with a smaller TN exists
+    const i64 Rmax = sms / C;
+    i64 TM = ((rr + Rmax - 1) / Rmax + 3) / 4 * 4;
+    for (; TM <= ((rr + 3) / 4) * 4; TM += 4) {
+      const i64 NMT = (TM / 4) * (TN / 4);
+      if (NMT > kPT) break;
+      const int KS = static_cast<int>(std::min<i64>(8, kPT / NMT));
+      int KC = 128;
+      size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), KS, KC);
+      if (sm > budget) {
+        KC = 32;
+        sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), KS, KC);
+      }
+      if (sm > budget) break;  // a taller tile only needs more
+      const i64 R = (rr + TM - 1) / TM;
+      // multiply-adds per GEMM thread (the critical path of a CTA)
+      const double cost = static_cast<double>(TM * TN) * static_cast<double>(rr + rc) /
+                          static_cast<double>(NMT * KS) + 64.0 * static_cast<double>(rr) / KC;
+      if (!found || cost < best) {
+        found = true;
+        best = cost;
+        *out = Geom{static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), KS, KC, sm};
+      }
+      break;  // the smallest feasible TM for this TN is the cheapest
+    }
+  }
+  return found;
+}
+
+}  // namespace
+
+bool fista_persist_enabled() {
+  const char* e = std::getenv("CPCAG_FISTA_PERSIST");
+  return !(e && std::string(e) == "0");
+}
+
+bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, const float* Dc,
+                       const cpcag_frpcag_config& cfg, double step, float* X, double* trace_dev,
+                       FistaPersistOut* res) {
+  if (rr < 1 || rc < 1 || rr > (1 << 20) || rc > (1 << 20)) return false;
+  int optin = 0;
+  CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+  const size_t budget = static_cast<size_t>(optin) > 4096 ? static_cast<size_t>(optin) - 4096 : 0;
+  Geom g;
+  if (!plan_geom(c, rr, rc, budget, &g)) return false;
+  ensure_smem(fista_persist_k, g.smem);
+  int per_sm = 0;
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_persist_k, kPT, g.smem));
+  const i64 grid = static_cast<i64>(g.R) * g.C;
+  if (per_sm < 1 || grid > static_cast<i64>(per_sm) * c->num_sms || grid > 32 * kPartRegs) return false;
+
+  const i64 ldS = static_cast<i64>(g.R) * g.TM, ldT = static_cast<i64>(g.C) * g.TN;
+  const size_t sz = static_cast<size_t>(ldS * ldT);
+  DevBuf<float> sbuf(c, 4 * sz);
+  sbuf.zero(c);
+  DevBuf<double> part(c, 2 * 4 * static_cast<size_t>(grid));
+  DevBuf<unsigned> bar(c, 2);
+  bar.zero(c);
+  DevBuf<FistaPersistOut> out(c, 1);
+  out.zero(c);
+  PersistArgs a{};
+  a.rr = static_cast<int>(rr);
+  a.rc = static_cast<int>(rc);
+  a.ldS = static_cast<int>(ldS);
+  a.ldT = static_cast<int>(ldT);
+  a.TM = g.TM;
+  a.TN = g.TN;
+  a.C = g.C;
+  a.KS = g.KS;
+  a.KC = g.KC;
+  a.use_r = cfg.gamma_r != 0.0;
+  a.use_c = cfg.gamma_c != 0.0;
+  a.loss = cfg.loss;
+  if (const char* e = std::getenv("CPCAG_FISTA_PERSIST_DBG")) a.dbg = std::atoi(e);
+  a.step = static_cast<float>(step);
+  a.tol = cfg.tol;
+  a.max_iter = cfg.max_iter;
+  a.gamma_r = cfg.gamma_r;
+  a.gamma_c = cfg.gamma_c;
+  a.Dr = Dr;
+  a.Dc = Dc;
+  a.Y = Y;
+  a.Sg[0] = sbuf.p;
+  a.Sg[1] = sbuf.p + sz;
+  a.SgT[0] = sbuf.p + 2 * sz;
+  a.SgT[1] = sbuf.p + 3 * sz;
+  a.part = part.p;
+  a.trace = trace_dev;
+  a.X = X;
+  a.out = out.p;
+  a.bar = bar.p;
+  void* args[] = {(void*)&a};
+  {
+    KScope ks_(c, "fista_persist");
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)fista_persist_k, dim3(static_cast<unsigned>(grid)), dim3(kPT), args,
+                                        g.smem, c->stream));
+    launched(c);
+  }
+  *res = read_back(c, out.p);
+  if (std::getenv("CPCAG_FISTA_PERSIST_PROF"))
+    std::fprintf(stderr,
+                 "[fista_persist] grid %lld (%d x %d tiles of %d x %d, KS %d, KC %d, smem %zu) its %lld: "
+                 "phaseA %.1f barrier %.1f reduce %.1f gemm %.1f elem %.1f us\n",
+                 static_cast<long long>(grid), g.R, g.C, g.TM, g.TN, g.KS, g.KC, g.smem,
+                 static_cast<long long>(res->iterations), res->prof_ns[0] * 1e-3, res->prof_ns[1] * 1e-3,
+                 res->prof_ns[2] * 1e-3, res->prof_ns[3] * 1e-3, res->prof_ns[4] * 1e-3);
+  return true;
+}
+
+}  // namespace cpcag_cuda

@@ -1,0 +1,26 @@
+// fista_persist.cuh -- single-kernel FISTA for the fp32 dense path
+// (fista_persist.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace cpcag_cuda {
+
+struct FistaPersistOut {
+  i64 iterations;
+  int converged, err;
+  double frc;
+  unsigned long long prof_ns[5];  // CTA 0: phase A, barrier wait, reduce, tile GEMM, element-wise
+};
+
+// CPCAG_FISTA_PERSIST=0 disables the path (the per-kernel path then runs).
+bool fista_persist_enabled();
+
+// Runs the whole solve; false when the shape does not fit the tiling (the
+// caller then takes the per-kernel path).  Dr/Dc are the dense, exactly
+// symmetric operators; trace_dev receives one objective value per iteration.
+bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, const float* Dc,
+                       const cpcag_frpcag_config& cfg, double step, float* X, double* trace_dev,
+                       FistaPersistOut* res);
+
+}  // namespace cpcag_cuda
