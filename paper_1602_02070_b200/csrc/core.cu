@@ -463,9 +463,9 @@ __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __re
 // contiguous slice of rows whose CSR entries stay resident in its shared
 // memory for the whole iteration (when they fit), a private shared-memory copy
 // of v, and ONE grid barrier per iteration: every CTA publishes its slice of
-// w (double-buffered by iteration parity) and its partial ||w||^2, then every
-// CTA sums the partials in the same fixed order and renormalises the whole of
-// v into its own shared copy.
+// w (double-buffered by iteration parity), then every CTA reads all of w,
+// forms ||w||^2 in the same fixed order and renormalises the whole of v into
+// its own shared copy (`partials` is unused).
 __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
@@ -494,7 +494,6 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   i64 it = 0;
   for (; it < max_iter; ++it) {
     double* w = wbuf + (it & 1) * n;
-    double part = 0.0;
     for (i64 r = r0 + wid; r < r1; r += nw) {
       double acc = 0.0;
       if (slice_in_smem) {
@@ -503,21 +502,19 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
         for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) acc += val[k] * vsrc[ci[k]];
       }
       acc = warp_sum(acc);
-      if (lane == 0) {
-        w[r] = acc;
-        part += acc * acc;
-      }
-    }
-    if (lane == 0) warp_part[wid] = part;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double b = 0.0;
-      for (int q = 0; q < nw; ++q) b += warp_part[q];
-      partials[(it & 1) * nb + blockIdx.x] = b;
+      if (lane == 0) w[r] = acc;
     }
     grid_barrier(&st->bar_count, &st->bar_gen);
+    // ||w||^2 straight from w, which every CTA reads anyway: one L2 round
+    // trip per iteration instead of two (partials, then w).  Same data and
+    // the same fixed-order block reduction in every CTA, so every CTA gets
+    // the same norm and takes the same stop decision.
     double t[1] = {0.0};
-    for (unsigned i = threadIdx.x; i < nb; i += blockDim.x) t[0] += __ldcg(partials + (it & 1) * nb + i);
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+      const double x = __ldcg(w + i);
+      if (v_in_smem) vs[i] = x;
+      t[0] += x * x;
+    }
     block_sum<1>(t);
     const double nrm = sqrt(t[0]);
     if (nrm == 0.0) {
@@ -527,13 +524,13 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
     const double prev = est;
     est = nrm;
     if (v_in_smem) {
-      for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(__ldcg(w + i), nrm);
+      for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(vs[i], nrm);
       __syncthreads();
     } else {
       // v lives in global memory: the grid renormalises its own rows and
       // needs a second barrier before the next product reads them.
       double* vg = const_cast<double*>(v0);
-      for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(w[i], nrm);
+      for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(__ldcg(w + i), nrm);
     }
     if (it > 0 && fabs(est - prev) <= tol * est) {
       ++it;

@@ -566,13 +566,195 @@ __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_fast4_k(int p, int n, 
   }
 }
 
+// Two-pass apply, pass 1 (CPCAG_APPLY=slab2, opt-in; needs a 32-row slab of
+// P over all n columns to fit in shared memory): U = P L_c without the
+// weight, i.e. exactly fast2's x (same entries, same CSR order, same
+// madd_entry), so pass 2 (fast2<kU>: the L_r pull, the mask, the weights and
+// <P, AP>) produces bit-identical AP.  The slab makes every L_c gather a
+// conflict-free shared-memory read (lane = row); a column's entries are read
+// staged in shared memory per unit and read as warp broadcasts.  CTAs take contiguous
+// runs of (slab, column part) units and restage only when the slab changes.
+// Measured at config 1 (decode stage, 200 iterations): slab2 59.6 ms vs
+// fast2 45.0 ms -- the slab pass is issue-bound (89 us, ncu) and pass 2
+// re-reads P and U from DRAM at low occupancy (latency-bound, 137 us).
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) cg_lc_slab_k(int p, int n, Pull<T> Lc, int parts, int units,
+                                                        const T* __restrict__ P, T* __restrict__ U,
+                                                        const CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* S = reinterpret_cast<T*>(smraw);  // S[c * 32 + r] = P[i0 + r, c]
+  // the unit's L_c entries (value, slab offset), read as warp broadcasts
+  OffEnt<T>* E = reinterpret_cast<OffEnt<T>*>(smraw + static_cast<size_t>(n) * 32 * sizeof(T));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u0 = static_cast<int>((static_cast<i64>(units) * blockIdx.x) / gridDim.x);
+  const int u1 = static_cast<int>((static_cast<i64>(units) * (blockIdx.x + 1)) / gridDim.x);
+  const int cw = (n + parts - 1) / parts;
+  int staged = -1, staged_part = -1;
+  for (int u = u0; u < u1; ++u) {
+    const int slab = u / parts, part = u - slab * parts;
+    const int i0 = slab * 32, rows = min(32, p - i0);
+    const int c_lo = part * cw, c_hi = min(n, c_lo + cw);
+    const i64 e0 = Lc.rp[c_lo];
+    if (slab != staged || part != staged_part) {
+      __syncthreads();
+      if (slab != staged)
+        for (int c = warp; c < n; c += 32) S[c * 32 + lane] = lane < rows ? P[i0 + lane + static_cast<i64>(c) * p] : T(0);
+      if (part != staged_part) {
+        const int ne = static_cast<int>(Lc.rp[c_hi] - e0);
+        for (int k = threadIdx.x; k < ne; k += blockDim.x) {
+          OffEnt<T> e;
+          e.v = Lc.v[e0 + k];
+          e.off = Lc.ci[e0 + k] * 32;
+          E[k] = e;
+        }
+      }
+      __syncthreads();
+      staged = slab;
+      staged_part = part;
+    }
+    for (int c = c_lo + warp; c < c_hi; c += 32) {
+      const int k0 = static_cast<int>(Lc.rp[c] - e0), k1 = static_cast<int>(Lc.rp[c + 1] - e0);
+      T x = T(0);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const OffEnt<T> e = E[k];
+        x = madd_entry(x, e.v, S[e.off + lane]);
+      }
+      if (lane < rows) U[i0 + lane + static_cast<i64>(c) * p] = x;
+    }
+  }
+}
+
+// regr: fast2 with each thread's L_r rows held in REGISTERS (row degree <=
+// MAXD; the pixel-grid row graph of config 1 has degree 9).  L_r is the same
+// for every column, so fast2's per-column re-read of the row's (value,
+// offset) entries from shared memory -- two dependent loads in front of
+// every gather -- goes away: the MAXD gathers of a row are independent loads
+// issued together.  kU: x = P L_c comes from the slab pass (cg_lc_slab_k)
+// instead of the L2 gathers.  Per-entry arithmetic and order are fast2's
+// (CSR order, madd_entry, the same combination), so AP is bit-identical.
+// Opt-in (CPCAG_APPLY=regr): measured slower than fast2 at config 1 (decode
+// 68.2 vs 45.0 ms): 128 registers halve the occupancy and the L1-miss
+// latency of the gathers is no longer hidden.
+template <typename T, int MAXD, bool kU>
+__global__ void __launch_bounds__(256, 2) cg_apply_regr_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                          int cols_per_cta, const T* __restrict__ P,
+                                                          T* __restrict__ AP, double* partials, CgState* st,
+                                                          const T* __restrict__ U) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  constexpr int RB = 512;
+  const int i0 = blockIdx.x * RB;
+  const int cb = blockIdx.y * cols_per_cta;
+  const int ce = min(n, cb + cols_per_cta);
+  const i64 kc_base = (!kU && cb < ce) ? Lc.rp[cb] : 0;
+  const int ec = (!kU && cb < ce) ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  OffEnt<T>* Ec = reinterpret_cast<OffEnt<T>*>(smraw);
+  int* crp = reinterpret_cast<int*>(Ec + ec);
+  if (!kU) {
+    for (int k = threadIdx.x; k < ec; k += blockDim.x) {
+      OffEnt<T> e;
+      e.v = Lc.v[kc_base + k];
+      e.off = Lc.ci[kc_base + k] * p;
+      Ec[k] = e;
+    }
+    for (int q = threadIdx.x; q <= ce - cb; q += blockDim.x) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  }
+  const int ia = i0 + threadIdx.x, ib = ia + 256;
+  const bool va = ia < p, vb = ib < p;
+  T ra[MAXD], rb[MAXD];
+  int oa[MAXD], ob[MAXD];
+  int da = 0, db = 0;
+  if (va) {
+    const i64 a0 = Lr.rp[ia];
+    da = static_cast<int>(Lr.rp[ia + 1] - a0);
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      ra[k] = k < da ? Lr.v[a0 + k] : T(0);
+      oa[k] = k < da ? Lr.ci[a0 + k] : 0;
+    }
+  }
+  if (vb) {
+    const i64 b0 = Lr.rp[ib];
+    db = static_cast<int>(Lr.rp[ib + 1] - b0);
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) {
+      rb[k] = k < db ? Lr.v[b0 + k] : T(0);
+      ob[k] = k < db ? Lr.ci[b0 + k] : 0;
+    }
+  }
+  __syncthreads();
+  double s[1] = {0.0};
+  if (va) {
+    const bool sa = pl.rsel[ia] >= 0, sb = vb && pl.rsel[ib] >= 0;
+    const T* Pa = P + ia;
+    for (int c = cb; c < ce; ++c) {
+      T xa = T(0), xb = T(0);
+      if constexpr (kU) {
+        xa = U[ia + static_cast<i64>(c) * p];
+        if (vb) xb = U[ib + static_cast<i64>(c) * p];
+      } else {
+        const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
+#pragma unroll 4
+        for (int k = k0; k < k1; ++k) {
+          const OffEnt<T> e = Ec[k];
+          xa = madd_entry(xa, e.v, Pa[e.off]);
+          if (vb) xb = madd_entry(xb, e.v, Pa[e.off + 256]);
+        }
+      }
+      const T* pc = P + static_cast<i64>(c) * p;
+      T ga[MAXD], gb[MAXD];
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k) {
+        ga[k] = k < da ? pc[oa[k]] : T(0);
+        gb[k] = k < db ? pc[ob[k]] : T(0);
+      }
+      T ya = T(0), yb = T(0);
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k) {
+        if (k < da) ya = madd_entry(ya, ra[k], ga[k]);
+        if (k < db) yb = madd_entry(yb, rb[k], gb[k]);
+      }
+      const bool cs = pl.csel[c] >= 0;
+      {
+        T out = add_rn(mul_rn(gc, xa), mul_rn(gr, ya));
+        const T pv = pc[ia];
+        if (sa && cs) out = add_rn(out, pv);
+        AP[ia + static_cast<i64>(c) * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+      if (vb) {
+        T out = add_rn(mul_rn(gc, xb), mul_rn(gr, yb));
+        const T pv = pc[ib];
+        if (sb && cs) out = add_rn(out, pv);
+        AP[ib + static_cast<i64>(c) * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 // fast2: two rows per thread (i and i + 256) so each staged L_c entry and
 // its address arithmetic serve two gathers (the fast apply is issue- and
 // latency-bound, ~6 instructions per 4-byte gather).
-template <typename T, int MINB = 4>
+template <typename T, int MINB = 4, bool kU = false>
 __global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
                                                            int cols_per_cta, const T* __restrict__ P,
-                                                           T* __restrict__ AP, double* partials, CgState* st) {
+                                                           T* __restrict__ AP, double* partials, CgState* st,
+                                                           const T* __restrict__ U = nullptr) {
   if (st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int RB = 512;
@@ -582,8 +764,8 @@ __global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull
   const int ce = min(n, cb + cols_per_cta);
   const i64 kr_base = Lr.rp[i0];
   const int er = static_cast<int>(Lr.rp[i1] - kr_base);
-  const i64 kc_base = cb < ce ? Lc.rp[cb] : 0;
-  const int ec = cb < ce ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
+  const i64 kc_base = (!kU && cb < ce) ? Lc.rp[cb] : 0;
+  const int ec = (!kU && cb < ce) ? static_cast<int>(Lc.rp[ce] - kc_base) : 0;
   OffEnt<T>* Er = reinterpret_cast<OffEnt<T>*>(smraw);
   OffEnt<T>* Ec = Er + er;
   int* crp = reinterpret_cast<int*>(Ec + ec);
@@ -599,7 +781,8 @@ __global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull
     e.off = Lc.ci[kc_base + k] * p;
     Ec[k] = e;
   }
-  for (int q = threadIdx.x; q <= ce - cb; q += blockDim.x) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
+  if (!kU)
+    for (int q = threadIdx.x; q <= ce - cb; q += blockDim.x) crp[q] = static_cast<int>(Lc.rp[cb + q] - kc_base);
   __syncthreads();
   double s[1] = {0.0};
   const int ia = i0 + threadIdx.x, ib = ia + 256;
@@ -610,13 +793,19 @@ __global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull
     const bool sa = pl.rsel[ia] >= 0, sb = vb && pl.rsel[ib] >= 0;
     const T* Pa = P + ia;
     for (int c = cb; c < ce; ++c) {
-      const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
       T xa = T(0), xb = T(0);
+      if constexpr (kU) {
+        // two-pass apply: P L_c of this entry from cg_lc_slab_k
+        xa = U[ia + static_cast<i64>(c) * p];
+        if (vb) xb = U[ib + static_cast<i64>(c) * p];
+      } else {
+        const int k0 = crp[c - cb], k1 = crp[c - cb + 1];
 #pragma unroll 4
-      for (int k = k0; k < k1; ++k) {
-        const OffEnt<T> e = Ec[k];
-        xa = madd_entry(xa, e.v, Pa[e.off]);
-        if (vb) xb = madd_entry(xb, e.v, Pa[e.off + 256]);
+        for (int k = k0; k < k1; ++k) {
+          const OffEnt<T> e = Ec[k];
+          xa = madd_entry(xa, e.v, Pa[e.off]);
+          if (vb) xb = madd_entry(xb, e.v, Pa[e.off + 256]);
+        }
       }
       const T* pc = P + static_cast<i64>(c) * p;
       T ya = T(0), yb = T(0);
@@ -661,13 +850,55 @@ __global__ void __launch_bounds__(256, MINB) cg_apply_fast2_k(int p, int n, Pull
   }
 }
 
+// 16-byte vectors of the iterate (4 fp32 / 2 fp64 entries).
 template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  using V = float4;
+  static constexpr int W = 4;
+};
+template <>
+struct Vec16<double> {
+  using V = double2;
+  static constexpr int W = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ T& vlane(typename Vec16<T>::V& v, int k) {
+  return reinterpret_cast<T*>(&v)[k];
+}
+
+// R -= alpha AP, ||R||^2.  kVec: 16-byte loads/stores over the first
+// N - N % W entries (all pointers 16-byte aligned), the tail scalar; the
+// per-entry arithmetic is the same either way.
+template <typename T, bool kVec = false>
 __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP, double* partials,
                               CgState* st) {
   if (st->done) return;
   const T alpha = static_cast<T>(st->alpha);
   double s[1] = {0.0};
-  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+  const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, ts = (i64)gridDim.x * blockDim.x;
+  i64 done = 0;
+  if constexpr (kVec) {
+    using V = typename Vec16<T>::V;
+    constexpr int W = Vec16<T>::W;
+    const i64 nv = N / W;
+    V* Rv = reinterpret_cast<V*>(R);
+    const V* Av = reinterpret_cast<const V*>(AP);
+    for (i64 q = t0; q < nv; q += ts) {
+      V r = Rv[q];
+      V a = Av[q];
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        vlane<T>(r, k) = sub_rn(vlane<T>(r, k), mul_rn(alpha, vlane<T>(a, k)));
+        s[0] += static_cast<double>(vlane<T>(r, k)) * static_cast<double>(vlane<T>(r, k));
+      }
+      Rv[q] = r;
+    }
+    done = nv * W;
+  }
+  for (i64 q = done + t0; q < N; q += ts) {
     const T r = sub_rn(R[q], mul_rn(alpha, AP[q]));
     R[q] = r;
     s[0] += static_cast<double>(r) * static_cast<double>(r);
@@ -679,12 +910,35 @@ __global__ void cg_residual_k(i64 N, T* __restrict__ R, const T* __restrict__ AP
   }
 }
 
-template <typename T>
+template <typename T, bool kVec = false>
 __global__ void cg_update_k(i64 N, T* __restrict__ X, T* __restrict__ P, const T* __restrict__ R,
                             i64 max_iter, CgState* st) {
   if (st->done) return;
   const T alpha = static_cast<T>(st->alpha), beta = static_cast<T>(st->beta);
-  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+  const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, ts = (i64)gridDim.x * blockDim.x;
+  i64 done = 0;
+  if constexpr (kVec) {
+    using V = typename Vec16<T>::V;
+    constexpr int W = Vec16<T>::W;
+    const i64 nv = N / W;
+    V* Xv = reinterpret_cast<V*>(X);
+    V* Pv = reinterpret_cast<V*>(P);
+    const V* Rv = reinterpret_cast<const V*>(R);
+    for (i64 q = t0; q < nv; q += ts) {
+      V x = Xv[q], pv = Pv[q];
+      const V r = Rv[q];
+      V pn;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        vlane<T>(x, k) = add_rn(vlane<T>(x, k), mul_rn(alpha, vlane<T>(pv, k)));
+        vlane<T>(pn, k) = add_rn(reinterpret_cast<const T*>(&r)[k], mul_rn(beta, vlane<T>(pv, k)));
+      }
+      Xv[q] = x;
+      Pv[q] = pn;
+    }
+    done = nv * W;
+  }
+  for (i64 q = done + t0; q < N; q += ts) {
     const T pv = P[q];
     X[q] = add_rn(X[q], mul_rn(alpha, pv));
     P[q] = add_rn(R[q], mul_rn(beta, pv));
@@ -1573,6 +1827,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx);
   dim3 g2(gx, static_cast<unsigned>(std::max<i64>(1, std::min<i64>({n, ycap, 65535}))));
   const unsigned nb1 = stride_blocks(c, N);
+  // 16-byte vector residual/update when every iterate is 16-byte aligned
+  // (X is the caller's buffer); CPCAG_CG_VEC=0 forces the scalar kernels.
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && !(std::getenv("CPCAG_CG_VEC") &&
+                                                                        std::string(std::getenv("CPCAG_CG_VEC")) == "0");
+  const unsigned nb1v = stride_blocks(c, (N + Vec16<T>::W - 1) / Vec16<T>::W);
   DevBuf<double> part(c, std::max<size_t>(g2.x * g2.y, nb1));
 
   // Apply variant (CPCAG_APPLY overrides): fast2 | fast | fast3 | fast4 | slab | rcm2 | staged |
@@ -1758,7 +2017,42 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       if (part.n < static_cast<size_t>(gs4.x) * gs4.y) part.alloc(c, static_cast<size_t>(gs4.x) * gs4.y);
     }
   }
-  if (variant == "fast2" || variant == "rcm2") {
+  // slab2 (two-pass apply: cg_lc_slab_k then fast2<kU>), when a 32-row slab
+  // over all n columns fits in shared memory.
+  int s2_parts = 4, s2_units = 0;
+  unsigned s2_grid = 0;
+  size_t s2_smem = 0;
+  DevBuf<T> Ubuf;
+  if (variant == "slab2") {
+    if (!(p * n < (i64{1} << 31) && n * 32 * static_cast<i64>(sizeof(T)) <= 200 * 1024)) {
+      variant = "fast2";
+    } else {
+      const i64 slabs = (p + 31) / 32;
+      if (const char* e = std::getenv("CPCAG_SLAB2_PARTS")) s2_parts = std::max(1, std::atoi(e));
+      s2_units = static_cast<int>(slabs * s2_parts);
+      s2_grid = static_cast<unsigned>(std::min<i64>(s2_units, c->num_sms));
+      const i64 cw2 = (n + s2_parts - 1) / s2_parts;
+      i64 ecap = 0;
+      for (i64 q = 0; q < s2_parts; ++q) {
+        const i64 a = std::min(n, q * cw2), e = std::min(n, a + cw2);
+        ecap = std::max(ecap, rpc[e] - rpc[a]);
+      }
+      s2_smem = static_cast<size_t>(n) * 32 * sizeof(T) + static_cast<size_t>(ecap) * sizeof(OffEnt<T>);
+      if (s2_smem > 220 * 1024) {
+        variant = "fast2";
+        s2_grid = 0;
+      } else {
+        ensure_smem(cg_lc_slab_k<T>, s2_smem);
+      }
+      if (s2_grid) Ubuf.alloc(c, static_cast<size_t>(N));
+    }
+  }
+  // regr (register-resident L_r rows) needs row degree <= 16.
+  i64 maxdeg_r = 0;
+  for (i64 i = 0; i < p; ++i) maxdeg_r = std::max(maxdeg_r, rpr[i + 1] - rpr[i]);
+  const bool regr_ok = maxdeg_r <= 16;
+  if (variant == "regr" && !regr_ok) variant = "fast2";
+  if (variant == "fast2" || variant == "rcm2" || variant == "slab2" || variant == "regr") {
     i64 mer = 0, mec = 0;
     for (unsigned b = 0; b < gx2; ++b) {
       const i64 a = static_cast<i64>(b) * 512, e = std::min<i64>(p, a + 512);
@@ -1777,7 +2071,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       ensure_smem(cg_apply_fast2_k<T, 4>, fast2_smem);
       ensure_smem(cg_apply_fast2_k<T, 5>, fast2_smem);
       ensure_smem(cg_apply_fast2_k<T, 6>, fast2_smem);
+      ensure_smem(cg_apply_fast2_k<T, 4, true>, fast2_smem);
+      ensure_smem(cg_apply_regr_k<T, 16, false>, fast2_smem);
+      ensure_smem(cg_apply_regr_k<T, 16, true>, fast2_smem);
     }
+    if (variant == "staged" && s2_grid) Ubuf.release();
     if (part.n < static_cast<size_t>(gs2.x) * gs2.y) part.alloc(c, static_cast<size_t>(gs2.x) * gs2.y);
   }
   if (variant == "staged" && !(staged_smem <= 96 * 1024)) variant = "plain";
@@ -1808,10 +2106,26 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
         } else if (variant == "fast4") {
           f4_kernel()<<<gs4, 128, fast4_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl,
                                                        static_cast<int>(cpc4), P.p, AP.p, part.p, st.p);
+        } else if (variant == "slab2") {
+          cg_lc_slab_k<T><<<s2_grid, 1024, s2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pc,
+                                                                 s2_parts, s2_units, P.p, Ubuf.p, st.p);
+          launched(c);
+          if (regr_ok)
+            cg_apply_regr_k<T, 16, true><<<gs2, kBlock, fast2_smem, c->stream>>>(
+                static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl, static_cast<int>(cpc2), P.p, AP.p,
+                part.p, st.p, Ubuf.p);
+          else
+            cg_apply_fast2_k<T, 4, true><<<gs2, kBlock, fast2_smem, c->stream>>>(
+                static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl, static_cast<int>(cpc2), P.p, AP.p,
+                part.p, st.p, Ubuf.p);
+        } else if (variant == "regr") {
+          cg_apply_regr_k<T, 16, false><<<gs2, kBlock, fast2_smem, c->stream>>>(
+              static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
+              st.p, nullptr);
         } else if (variant == "fast2" || variant == "rcm2") {
           f2_kernel()<<<gs2, kBlock, fast2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc2, gr,
                                                                      gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,
-                                                                     st.p);
+                                                                     st.p, nullptr);
         } else if (variant == "fast") {
           cg_apply_fast_k<T><<<gs, kBlock, fast_smem, c->stream>>>(static_cast<int>(p), 0, static_cast<int>(n), pr, pc,
                                                                   gr, gc, pl, static_cast<int>(cols_per_cta), P.p, AP.p,
@@ -1826,12 +2140,18 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       }
       {
         KScope ks_(c, "cg_residual");
-        cg_residual_k<T><<<nb1, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+        if (vec_ok)
+          cg_residual_k<T, true><<<nb1v, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+        else
+          cg_residual_k<T><<<nb1, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
         launched(c);
       }
       {
         KScope ks_(c, "cg_update");
-        cg_update_k<T><<<nb1, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
+        if (vec_ok)
+          cg_update_k<T, true><<<nb1v, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
+        else
+          cg_update_k<T><<<nb1, kBlock, 0, c->stream>>>(N, X, P.p, R.p, cfg.pcg_max_iter, st.p);
         launched(c);
       }
     }

@@ -177,7 +177,7 @@ def _decoder_case(p=150, n=120, rr=40, rc=30, seed=21):
     return Lr, Lc, plan, Xt
 
 
-@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast4", "slab", "rcm2", "fast3", "staged", "plain", "band"])
+@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast4", "slab", "slab2", "regr", "rcm2", "fast3", "staged", "plain", "band"])
 def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
@@ -191,7 +191,7 @@ def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     assert rel(res.X, ro.X) <= 1e-9
 
 
-@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "fast5", "slab", "rcm2"])
+@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "fast5", "slab", "slab2", "regr", "rcm2"])
 def test_alternate_decode_fixed_iterations_fp32(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
@@ -203,6 +203,23 @@ def test_alternate_decode_fixed_iterations_fp32(P, ctx, monkeypatch, variant):
     ro = O.alternate_decode(Xt.astype(np.float32).astype(np.float64), plan_o, Lr, Lc, 1.0, 1.0, 1.0, 1e-8, 100)
     assert res.iterations == ro.iterations
     assert rel(res.X, ro.X) <= 1e-4
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_slab2_regr_applies_bit_identical_to_fast2(P, ctx, monkeypatch, dt):
+    """The two-pass apply (L_c slab pass + fast2 without the L_c gathers)
+    keeps fast2's per-entry arithmetic and order: every iterate is equal."""
+    Lr, Lc, plan_o, Xt = _decoder_case(700, 300, 170, 75, 29)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    out = {}
+    for v in ("fast2", "slab2", "regr"):
+        monkeypatch.setenv("CPCAG_APPLY", v)
+        out[v] = P.alternate_decode(Xt.astype(dt), plan, to_device(ctx, Lr), to_device(ctx, Lc),
+                                    P.SpectralGap(lambda_k1=0.7), P.SpectralGap(lambda_k1=0.9),
+                                    P.DecoderConfig(1.0, 1e-30, 60), ctx=ctx)
+    assert out["fast2"].iterations == out["slab2"].iterations == out["regr"].iterations == 60
+    assert np.array_equal(out["fast2"].X, out["slab2"].X)
+    assert np.array_equal(out["fast2"].X, out["regr"].X)
 
 
 def test_alternate_decode_zero_rhs_and_validation(P, ctx):
