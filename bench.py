@@ -520,6 +520,9 @@ def run_cfg2(args):
                            "peak": 1100.0, "unit": "TFLOP/s", "frac": round(3 * flops / (t_tc / 1e3) / 1e12 / 1100.0, 4),
                            "peak_source": "nominal dense TF32 (B200_PROFILING.md), 3 MMAs per product counted"}
     print(json.dumps(out), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            json.dump(out, f)
 
 
 def run_cfg3(args):
@@ -591,6 +594,9 @@ def run_cfg3(args):
            "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()},
            "kernel_algorithmic_GBps": kgbps}
     print(json.dumps(out), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            json.dump(out, f)
 
 
 def run_cfg3_sharded(args, rank, local_rank, world):
@@ -662,6 +668,9 @@ def run_cfg3_sharded(args, rank, local_rank, world):
                           "block_cols": c1 - c0},
                "iters_per_s": round(it / (ms / 1e3), 1)}
         print(json.dumps(out), flush=True)
+        if args.json_out:
+            with open(args.json_out, "w") as f:
+                json.dump(out, f)
     be.close()
     dist.destroy_process_group()
 

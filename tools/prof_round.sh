@@ -1,0 +1,20 @@
+# Round evidence for profiles/: bench lines (cfg1 default + reference arm,
+# cfg2, cfg3), timed-region launch lists, and one ncu --set full capture per
+# top kernel (each after its command ran clean without ncu).
+# usage: bash tools/prof_round.sh [outdir]
+O=${1:-gpurun_out/prof}
+rm -rf $O; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt 2>&1
+timeout -s KILL 600 python bench.py --steps 5 --warmup 3 --json-out $O/bench_cfg1.json > $O/bench_cfg1.log 2>&1; echo "cfg1 rc=$?"; grep "\[bench\] step" $O/bench_cfg1.log
+timeout -s KILL 600 python bench.py --impl reference --steps 2 --warmup 1 --json-out $O/bench_ref.json > $O/bench_ref.log 2>&1; echo "ref rc=$?"
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg1.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_launch.log 2>&1; echo "launch list rc=$?"
+for k in cg_apply_fast2 pcg_persistent fista_persist power_iter_coop cg_update cg_residual; do
+  timeout -s KILL 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:$k -c 1 -o $O/full_cfg1_$k -f python tools/profile_step.py > $O/ncu_full_cfg1_$k.log 2>&1; echo "ncu $k rc=$?"
+done
+timeout -s KILL 900 python bench.py --config cfg3 --steps 3 --warmup 3 --json-out $O/bench_cfg3.json > $O/bench_cfg3.log 2>&1; echo "cfg3 rc=$?"
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg3.csv python bench.py --config cfg3 --steps 1 --warmup 1 > $O/ncu_launch3.log 2>&1; echo "launch list cfg3 rc=$?"
+SWEEP_ITERS=3 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:"cg_apply_(band|col)_k|cg_update|cg_residual" -s 4 -c 4 -o $O/full_cfg3 -f python tools/band_sweep.py 1,1024,32,1 > $O/ncu_full_cfg3.log 2>&1; echo "ncu cfg3 rc=$?"
+timeout -s KILL 600 python bench.py --config cfg2 --steps 3 --warmup 3 --json-out $O/bench_cfg2.json > $O/bench_cfg2.log 2>&1; echo "cfg2 rc=$?"
+timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_launch2.log 2>&1; echo "launch list cfg2 rc=$?"
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:knn_tc_filter2 -c 1 -o $O/full_cfg2_tc -f python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_full_cfg2.log 2>&1; echo "ncu cfg2 rc=$?"
+ls $O | wc -l
