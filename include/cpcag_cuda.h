@@ -226,6 +226,17 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
  * above 1e-12 of its peak made positive. */
 int cpcag_cuda_sym_eig(cpcag_ctx ctx, cpcag_csr A, int64_t k, double* eigenvalues, double* eigenvectors);
 
+/* The k smallest eigenvalues of a large sparse symmetric matrix (eigenvalues
+ * only; replaces the dense sym_eig of eigs.cpp:34-51 where it is infeasible,
+ * i.e. the spectral gaps of pipeline.cpp:343-349 on 1e5-1e6-node graphs):
+ * Lanczos with full reorthogonalisation on sigma I - A (sigma = Gershgorin
+ * bound), stopping when the k extreme Ritz residuals are <= tol * sigma.
+ * eigenvalues: k, ascending.  iterations (may be NULL): Lanczos steps.
+ * Errors: invalid_argument for a non-square A or k out of range;
+ * runtime_error "lanczos: not converged after N steps". */
+int cpcag_cuda_sym_eigvals_lanczos(cpcag_ctx ctx, cpcag_csr A, int64_t k, double tol, int64_t max_iter,
+                                   uint64_t seed, double* eigenvalues, int64_t* iterations);
+
 /* SpectralGap (graph.hpp:53-58). */
 typedef struct cpcag_spectral_gap {
   int64_t k;

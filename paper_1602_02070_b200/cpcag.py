@@ -28,7 +28,7 @@ __all__ = [
     "kron_reduce", "draw_plan", "subsample", "objective", "prox_l1", "prox_l2", "grad_g",
     "fista_solve", "alternate_decode", "power_iteration_norm", "pcg_solve", "run_pipeline",
     "default_context", "SvdResult", "thin_svd", "detect_rank", "graph_upsample", "LowRankFactors",
-    "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "spectral_gap",
+    "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "sym_eigvals_lanczos", "spectral_gap",
 ]
 
 
@@ -688,6 +688,19 @@ def sym_eig(A: SparseMatrix, k: int, vectors: bool = True, ctx=None) -> EigenPai
     N.check(N.lib().cpcag_cuda_sym_eig(_ctx(ctx), A.handle, int(k), ev.ctypes.data,
                                        vec.ctypes.data if vectors else None))
     return EigenPairs(ev[:k].copy(), np.asfortranarray(vec[:, :k]) if vectors else None)
+
+
+def sym_eigvals_lanczos(A: SparseMatrix, k: int, tol: float = 1e-10, max_iter: int = 5000, seed: int = 0,
+                        ctx=None):
+    """The k smallest eigenvalues (ascending) of a large sparse symmetric
+    matrix by Lanczos with full reorthogonalisation on the device: the
+    spectral gaps of pipeline.cpp:343-349 where the dense eigs.cpp:34-51 is
+    infeasible.  Returns (eigenvalues, lanczos_steps)."""
+    ev = np.empty(max(int(k), 1), np.float64)
+    it = N.i64()
+    N.check(N.lib().cpcag_cuda_sym_eigvals_lanczos(_ctx(ctx), A.handle, int(k), float(tol), int(max_iter), int(seed),
+                                                   ev.ctypes.data, C.byref(it)))
+    return ev[:k].copy(), int(it.value)
 
 
 def spectral_gap(basis: EigenPairs, k: int) -> "SpectralGap":

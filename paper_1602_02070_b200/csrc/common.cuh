@@ -404,6 +404,9 @@ struct HostRng {
 
 // Internal entry points shared between translation units.
 double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter);
+// k smallest eigenvalues (ascending, host array) by Lanczos (lanczos.cu).
+void sym_eigvals_lanczos(Ctx* c, Csr* A, i64 k, double tol, i64 max_iter, uint64_t seed, double* evals,
+                         i64* iterations);
 
 template <typename T>
 void spmm_left(Ctx* c, Csr* A, const T* X, i64 m, T* Y);

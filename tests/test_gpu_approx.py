@@ -188,3 +188,50 @@ def test_pipeline_computes_gaps_like_the_reference(P, ctx):
     lr = O.spectral_gap(O.sym_eig(gr.laplacian, k + 1)[0], k)[1]
     lc = O.spectral_gap(O.sym_eig(gc.laplacian, k + 1)[0], k)[1]
     assert abs(rep.lambda_k1[0] - lr) <= 1e-10 * lr and abs(rep.lambda_k1[1] - lc) <= 1e-10 * lc
+
+
+# ------------------------------------------------------------------ Lanczos spectral gap (large graphs)
+@pytest.mark.parametrize("n,dim,k", [(400, 3, 6), (3000, 8, 21)])
+def test_lanczos_smallest_eigenvalues_match_lapack(P, ctx, n, dim, k):
+    """sym_eigvals_lanczos vs the dense oracle (numpy LAPACK) on kNN
+    Laplacians small enough for the dense solver."""
+    L = knn_laplacian(n, dim, 10, 7 + n)
+    ev, steps = P.sym_eigvals_lanczos(to_device(ctx, L), k, tol=1e-10, ctx=ctx)
+    w = np.linalg.eigvalsh(0.5 * (L.to_dense() + L.to_dense().T))[:k]
+    assert steps >= k
+    assert np.allclose(ev, w, rtol=1e-8, atol=1e-9 * np.abs(w).max())
+    # deterministic for a seed
+    ev2, steps2 = P.sym_eigvals_lanczos(to_device(ctx, L), k, tol=1e-10, ctx=ctx)
+    assert steps2 == steps and np.array_equal(ev, ev2)
+
+
+def test_lanczos_errors_and_components(P, ctx):
+    L = knn_laplacian(50, 3, 10, 3)
+    with pytest.raises(ValueError, match="order k out of range"):
+        P.sym_eigvals_lanczos(to_device(ctx, L), 51, ctx=ctx)
+    two = blocks_laplacian([30, 40], 3)
+    ev, _ = P.sym_eigvals_lanczos(to_device(ctx, two), 3, ctx=ctx)
+    # two components: a double zero eigenvalue, then the smaller Fiedler value
+    assert abs(ev[0]) <= 1e-9 and abs(ev[1]) <= 1e-9 and ev[2] > 1e-6
+    with pytest.raises(RuntimeError, match="not converged after"):
+        P.sym_eigvals_lanczos(to_device(ctx, knn_laplacian(3000, 8, 10, 5)), 21, tol=1e-14, max_iter=40, ctx=ctx)
+
+
+def test_pipeline_gaps_by_lanczos_match_dense(P, ctx, monkeypatch):
+    """CPCAG_GAP_LANCZOS=1 forces the Lanczos gap inside run_pipeline; it
+    agrees with the dense path (which the previous test pins to the oracle)."""
+    import math
+
+    from paper_1602_02070_b200.workloads import config0
+
+    Y, _ = config0(seed=1602, small=True)
+    p, n = Y.shape
+    g = math.sqrt(max(p, n))
+    cfg = P.PipelineConfig(knn=10, a=4, b=4, frpcag=P.FrpcagConfig(gamma_r=g, gamma_c=g, tol=1e-300, max_iter=40),
+                           decoder=P.DecoderConfig(1.0, 1e-8, 100, variant="alternate"), seed=1602)
+    dense = P.run_pipeline(Y, cfg, ctx=ctx)
+    monkeypatch.setenv("CPCAG_GAP_LANCZOS", "1")
+    lz = P.run_pipeline(Y, cfg, ctx=ctx)
+    for a, b in zip(lz.lambda_k1, dense.lambda_k1):
+        assert abs(a - b) <= 1e-8 * b
+    assert rel(lz.X, dense.X) <= 1e-8
