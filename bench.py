@@ -134,6 +134,65 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class NvmlClockSampler:
+    """Clocks and throttle reasons through NVML, sampled from the bench's own
+    thread BETWEEN timed steps (tick()), each sample taken while the GPU runs
+    the L2 flush that precedes the next step.  A background `nvidia-smi
+    -lms 200` (ClockSampler, BENCH_CLOCKS=smi) measurably perturbs this
+    host-synchronising pipeline: 25-75 ms stalls in 2 of 5 steps vs none
+    without it (tools/micro/run_diag.sh, round 1)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, device: int):
+        self.device = device
+        self.h = None
+        self.sm, self.smax, self.reasons = [], [], set()
+
+    def start(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.device)
+        except Exception:
+            self.h = None
+        self.tick()
+
+    def tick(self):
+        if self.h is None:
+            return
+        N = self.N
+        try:
+            self.sm.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+            self.smax.append(float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)))
+            mask = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for name, attr in self.REASONS:
+                if mask & getattr(N, attr):
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def stop(self):
+        self.tick()
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        hi = max(self.sm)
+        loaded = [x for x in self.sm if x >= 0.5 * hi] or self.sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(self.smax), "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml, sampled between timed steps"}
+
+
+def clock_sampler(device: int):
+    if os.environ.get("BENCH_CLOCKS") == "smi":
+        return ClockSampler(device)
+    return NvmlClockSampler(device)
+
+
 # ------------------------------------------------------------------ workload
 def make_workload():
     from paper_1602_02070_b200 import workloads
@@ -240,7 +299,7 @@ def run_ours(args, rank, local_rank, world):
         ctx.enable_kernel_timing(True)
 
     # ---------------- timed region (device events, L2 flushed between steps)
-    clocks = ClockSampler(local_rank)
+    clocks = clock_sampler(local_rank)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -252,6 +311,8 @@ def run_ours(args, rank, local_rank, world):
     torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
     for k in range(args.steps):
         flush.zero_()
+        if hasattr(clocks, "tick"):
+            clocks.tick()
         ev[k][0].record(stream)
         reports.append(P.run_pipeline(Yd, cfg, W_r=Wr_dev, ctx=ctx))
         ev[k][1].record(stream)
@@ -467,15 +528,21 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ cfg2 / cfg3
-def timed_steps(fn, steps, warmup, stream):
+def timed_steps(fn, steps, warmup, stream, clocks_out=None):
+    """Mean device ms of `steps` calls after `warmup`; clocks sampled between
+    steps (NVML, see NvmlClockSampler) into clocks_out when given."""
     import torch
 
     for _ in range(warmup):
         fn()
     torch.cuda.synchronize()
+    clocks = clock_sampler(torch.cuda.current_device())
+    clocks.start()
     evs = []
     torch.cuda.profiler.start()  # ncu --profile-from-start off captures the timed steps only
     for _ in range(steps):
+        if hasattr(clocks, "tick"):
+            clocks.tick()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         fn()
@@ -483,7 +550,12 @@ def timed_steps(fn, steps, warmup, stream):
         evs.append((a, b))
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
-    return sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+    clk = clocks.stop()
+    if clocks_out is not None:
+        clocks_out.update(clk)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    print(f"[bench] step ms {[round(x, 2) for x in step_ms]}", file=sys.stderr, flush=True)
+    return sum(step_ms) / len(step_ms)
 
 
 def run_cfg2(args):
@@ -502,7 +574,8 @@ def run_cfg2(args):
     Xd = torch.tensor(np.ascontiguousarray(X.T), device="cuda").t()
     ctx.reset_kernel_timing()
     ctx.enable_kernel_timing(True)
-    ms = timed_steps(lambda: P.build_knn_graph(Xd, "cols", 10, ctx=ctx), args.steps, args.warmup, stream)
+    clk = {}
+    ms = timed_steps(lambda: P.build_knn_graph(Xd, "cols", 10, ctx=ctx), args.steps, args.warmup, stream, clk)
     ctx.enable_kernel_timing(False)
     kt = ctx.kernel_times()
     flops = 2.0 * n * n * d
@@ -511,7 +584,9 @@ def run_cfg2(args):
            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f32 in, 3xTF32 filter + fp64 exact re-rank",
            "data": "synthetic: seeded config-2 generator (50/50 N(0,I) + 20 clusters)",
-           "config": {"workload": "cfg2: kNN graph, n=100000, d=512, K=10, CSR combinatorial Laplacian"},
+           "config": {"workload": "cfg2: kNN graph, n=100000, d=512, K=10, CSR combinatorial Laplacian",
+                      "l2": "input (205 MB fp32 points) larger than L2; no flush"},
+           "clocks": clk,
            "kernel_ms": {k: round(v[1] / max(v[0], 1) * v[0] / (args.steps + args.warmup), 3) for k, v in kt.items()},
            "gram_useful_tflops": round(flops / (ms / 1e3) / 1e12, 2)}
     if tc:
@@ -566,7 +641,8 @@ def run_cfg3(args):
     def step():
         res["r"] = P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, ctx=ctx)
 
-    ms = timed_steps(step, args.steps, max(args.warmup, 1), stream)
+    clk = {}
+    ms = timed_steps(step, args.steps, max(args.warmup, 1), stream, clk)
     ctx.enable_kernel_timing(False)
     kt = ctx.kernel_times()
     N = p * n
@@ -587,8 +663,15 @@ def run_cfg3(args):
            "vs_baseline": None, "dtype": "f32",
            "data": "synthetic: seeded config-3 generator (N(0,I_64) points, rank-20 low-pass basis)",
            "config": {"workload": f"cfg3: alternate CG decoder, p={p}, n={n}, 1/8 x 1/8 sampling, {it} iterations",
-                      "graphs_s_untimed": round(t_graphs, 3)},
+                      "graphs_s_untimed": round(t_graphs, 3),
+                      "l2": "iterates (3.3 GB each) larger than L2; no flush"},
+           "clocks": clk,
            "iters_per_s": round(it / (ms / 1e3), 1),
+           "cg_iteration_survey": {"bytes_B_iter": 6 * N * 4 + (nnz_r + nnz_c) * 8,
+                                   "model": "SURVEY 8(d): 6 N w + (nnz_r + nnz_c)(w + 4)",
+                                   "achieved_GBps": round((6 * N * 4 + (nnz_r + nnz_c) * 8) * it / (ms / 1e3) / 1e9, 1),
+                                   "frac_of_hbm": round((6 * N * 4 + (nnz_r + nnz_c) * 8) * it / (ms / 1e3) / 1e9 / peak,
+                                                        4)},
            "cg_iteration": {"bytes_B_iter": b_iter, "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
                             "frac_of_hbm": round(b_iter * it / (ms / 1e3) / 1e9 / peak, 4), "peak_source": src},
            "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()},

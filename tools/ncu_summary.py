@@ -13,6 +13,7 @@ TAGS = {
     "fista_splitk_partial": "fista_objective", "pcg_persistent": "pcg_persistent",
     "cg_apply_band": "cg_apply_band", "cg_apply_col": "cg_apply_col",
     "knn_tile": "knn_tile", "knn_tc_filter": "knn_tc_filter", "power_iter": "power_iter",
+    "fista_persist": "fista_persist",
 }
 
 WANT = [
