@@ -325,6 +325,34 @@ typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36
 
 enum { CPCAG_DECODER_IDEAL = 0, CPCAG_DECODER_ALTERNATE = 1, CPCAG_DECODER_APPROX = 2 };
 
+/* ------------------------------------------------------------------ GLR1 I/O
+ * The reference's binary container (io.hpp:14-30, io.cpp:16-230): magic
+ * "GLR1", u64 block kind (1 dense, 2 CSR, 3 factors), u64 dimensions, raw
+ * little-endian arrays.  Dense blocks stream through pinned double buffers
+ * straight into/out of device memory (fp64 on disk; fp32 buffers are
+ * narrowed/widened on the device).  Buffers may be host or device memory.
+ * Errors are std::runtime_error with the reference's texts: "<path>: cannot
+ * open for reading", "<path>: not a GLR1 container (bad magic)", "<path>: not
+ * a dense-matrix block", "<path>: truncated data section", ... */
+/* kind and dims of a GLR1 file (dims: 2 dense rows/cols, 3 CSR rows/cols/nnz,
+ * 4 factors p/n/k/scale flag). */
+int cpcag_glr1_info(const char* path, int64_t* kind, int64_t* dims);
+/* load_matrix / save_matrix, format glr1 (io.cpp:88-118). */
+int cpcag_cuda_load_matrix_glr1(cpcag_ctx ctx, const char* path, int precision, void* out, int64_t rows,
+                                int64_t cols);
+int cpcag_cuda_save_matrix_glr1(cpcag_ctx ctx, const char* path, int precision, const void* M, int64_t rows,
+                                int64_t cols);
+/* load_sparse / save_sparse (io.cpp:151-188); a non-canonical file is
+ * rebuilt like SparseMatrix::from_triplets (sorted, duplicates summed, exact
+ * zeros dropped). */
+int cpcag_cuda_load_sparse_glr1(cpcag_ctx ctx, const char* path, cpcag_csr* out);
+int cpcag_cuda_save_sparse_glr1(cpcag_ctx ctx, cpcag_csr A, const char* path);
+/* save_factors / load_factors (io.cpp:200-230): U p x k, sigma k, V n x k. */
+int cpcag_cuda_save_factors_glr1(cpcag_ctx ctx, const char* path, int64_t p, int64_t n, int64_t k,
+                                 int scale_applied, const double* U, const double* sigma, const double* V);
+int cpcag_cuda_load_factors_glr1(cpcag_ctx ctx, const char* path, int64_t p, int64_t n, int64_t k,
+                                 int* scale_applied, double* U, double* sigma, double* V);
+
 /* Optional factor output of the approximate decoder (PipelineReport::factors,
  * pipeline.hpp:91): fp64 U (p x k), sigma (k), V (n x k) when k <= k_cap. */
 typedef struct cpcag_pipeline_factors {

@@ -114,6 +114,13 @@ SIGNATURES = {
     "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_sym_eigvals_lanczos": (C.c_int, [vp, vp, i64, C.c_double, i64, C.c_uint64, vp, vp]),
+    "cpcag_glr1_info": (C.c_int, [C.c_char_p, vp, vp]),
+    "cpcag_cuda_load_matrix_glr1": (C.c_int, [vp, C.c_char_p, C.c_int, vp, i64, i64]),
+    "cpcag_cuda_save_matrix_glr1": (C.c_int, [vp, C.c_char_p, C.c_int, vp, i64, i64]),
+    "cpcag_cuda_load_sparse_glr1": (C.c_int, [vp, C.c_char_p, vp]),
+    "cpcag_cuda_save_sparse_glr1": (C.c_int, [vp, vp, C.c_char_p]),
+    "cpcag_cuda_save_factors_glr1": (C.c_int, [vp, C.c_char_p, i64, i64, i64, C.c_int, vp, vp, vp]),
+    "cpcag_cuda_load_factors_glr1": (C.c_int, [vp, C.c_char_p, i64, i64, i64, vp, vp, vp, vp]),
     "cpcag_cuda_graph_upsample": (C.c_int, [vp, vp, vp, i64, vp, i64, dbl, i64, vp]),
     "cpcag_cuda_approx_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                            C.POINTER(ApproxConfigC), vp, vp, vp, vp, i64, ip]),

@@ -13,6 +13,7 @@ HBM never round-trips through the host.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import Optional
@@ -29,6 +30,8 @@ __all__ = [
     "fista_solve", "alternate_decode", "power_iteration_norm", "pcg_solve", "run_pipeline",
     "default_context", "SvdResult", "thin_svd", "detect_rank", "graph_upsample", "LowRankFactors",
     "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "sym_eigvals_lanczos", "spectral_gap",
+    "glr1_info", "load_matrix", "save_matrix", "load_sparse", "save_sparse", "save_factors",
+    "load_factors", "plan_to_json", "plan_from_json", "save_plan", "load_plan",
 ]
 
 
@@ -918,3 +921,172 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
                           bool(rep.decoder_converged), int(rep.decoder_iterations), stages,
                           int(rep.detected_rank), factors, bool(rep.has_factors),
                           (float(rep.lambda_k1_r), float(rep.lambda_k1_c)))
+
+
+# ------------------------------------------------------------------ I/O (io.hpp:14-44)
+def glr1_info(path: str):
+    """(kind, dims) of a GLR1 file: kind 1 dense (rows, cols), 2 CSR (rows,
+    cols, nnz), 3 factors (p, n, k, scale flag)."""
+    kind = N.i64()
+    dims = (N.i64 * 4)()
+    N.check(N.lib().cpcag_glr1_info(os.fsencode(path), C.byref(kind), dims))
+    nd = {1: 2, 2: 3, 3: 4}[int(kind.value)]
+    return int(kind.value), tuple(int(dims[i]) for i in range(nd))
+
+
+def load_matrix(path: str, format: str = "glr1", precision=None, device=None, ctx=None):
+    """io.cpp:88-149.  glr1: streamed through pinned buffers into a
+    column-major CUDA tensor (device given, default "cuda") or a numpy array
+    (device="cpu"); fp32 destinations are narrowed on the device.  csv:
+    "rows,cols" header then one line per row (host text, as the reference)."""
+    prec = N.F64 if precision in (None, "f64", N.F64, np.float64) else N.F32
+    if format == "csv":
+        return _load_csv(path, prec)
+    if format != "glr1":
+        raise ValueError("load_matrix: format must be 'glr1' or 'csv'")
+    kind, dims = glr1_info(path)
+    if kind != 1:
+        raise RuntimeError(f"{path}: not a dense-matrix block")
+    rows, cols = dims
+    dev = "cuda" if device is None else device
+    out, op = _out(str(dev) != "cpu", dev if str(dev) != "cpu" else None, (rows, cols), prec)
+    N.check(N.lib().cpcag_cuda_load_matrix_glr1(_ctx(ctx), os.fsencode(path), prec, op, rows, cols))
+    return out
+
+
+def save_matrix(M, path: str, format: str = "glr1", precision=None, ctx=None):
+    """io.cpp:88-117 (fp64 on disk; fp32 device data is widened on the device)."""
+    if format == "csv":
+        a = M.detach().cpu().numpy() if _is_torch(M) else np.asarray(M)
+        _save_csv(np.asarray(a, np.float64), path)
+        return
+    if format != "glr1":
+        raise ValueError("save_matrix: format must be 'glr1' or 'csv'")
+    prec = _precision(M, precision)
+    m = _In(M, prec)
+    if len(m.shape) != 2:
+        raise ValueError("save_matrix: M must be a matrix")
+    N.check(N.lib().cpcag_cuda_save_matrix_glr1(_ctx(ctx), os.fsencode(path), prec, m.ptr, m.shape[0], m.shape[1]))
+
+
+def load_sparse(path: str, ctx=None) -> "SparseMatrix":
+    """io.cpp:164-188: CSR block -> device SparseMatrix."""
+    h = N.vp()
+    N.check(N.lib().cpcag_cuda_load_sparse_glr1(_ctx(ctx), os.fsencode(path), C.byref(h)))
+    return SparseMatrix(h, ctx)
+
+
+def save_sparse(A: "SparseMatrix", path: str, ctx=None):
+    """io.cpp:151-162."""
+    N.check(N.lib().cpcag_cuda_save_sparse_glr1(_ctx(ctx), A.handle, os.fsencode(path)))
+
+
+def save_factors(f: LowRankFactors, path: str, ctx=None):
+    """io.cpp:200-211."""
+    U = np.asfortranarray(f.U, np.float64)
+    V = np.asfortranarray(f.V, np.float64)
+    s = np.ascontiguousarray(f.sigma, np.float64)
+    N.check(N.lib().cpcag_cuda_save_factors_glr1(_ctx(ctx), os.fsencode(path), U.shape[0], V.shape[0], int(f.k),
+                                                 int(bool(f.scale_applied)), U.ctypes.data, s.ctypes.data,
+                                                 V.ctypes.data))
+
+
+def load_factors(path: str, ctx=None) -> LowRankFactors:
+    """io.cpp:213-230."""
+    kind, dims = glr1_info(path)
+    if kind != 3:
+        raise RuntimeError(f"{path}: not a factors block")
+    p, n, k, _ = dims
+    U = np.empty((p, k), np.float64, order="F")
+    V = np.empty((n, k), np.float64, order="F")
+    s = np.empty(k, np.float64)
+    sc = C.c_int()
+    N.check(N.lib().cpcag_cuda_load_factors_glr1(_ctx(ctx), os.fsencode(path), p, n, k, C.byref(sc),
+                                                 U.ctypes.data, s.ctypes.data, V.ctypes.data))
+    return LowRankFactors(U, s, V, k, bool(sc.value))
+
+
+def _save_csv(a: np.ndarray, path: str):
+    with open(path, "w") as f:
+        f.write(f"{a.shape[0]},{a.shape[1]}\n")
+        for row in a:
+            f.write(",".join(_g17(x) for x in row) + "\n")
+
+
+def _g17(x: float) -> str:
+    return "%.17g" % x
+
+
+def _load_csv(path: str, prec: int):
+    """io.cpp:119-149 with its error texts."""
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"{path}: cannot open for reading")
+    with f:
+        lines = f.read().split("\n")
+    if not lines or lines[0] == "":
+        raise RuntimeError(f"{path}: empty file")
+    head = lines[0].split(",")
+    if len(head) < 2:
+        raise RuntimeError(f"{path}: malformed dimension header at line 1")
+    rows, cols = int(_num(head[0], path, 1)), int(_num(head[1], path, 1))
+    if rows < 0 or cols < 0:
+        raise RuntimeError(f"{path}: negative dimensions in header")
+    a = np.empty((rows, cols), np.float64, order="F")
+    for i in range(rows):
+        if i + 1 >= len(lines):
+            raise RuntimeError(f"{path}: missing row {i + 1}")
+        tok = lines[i + 1].split(",") if lines[i + 1] != "" else []
+        if len(tok) < cols:
+            raise RuntimeError(f"{path}: row {i + 1} has fewer than {cols} columns")
+        if len(tok) > cols:
+            raise RuntimeError(f"{path}: row {i + 1} has more than {cols} columns (dimension header mismatch)")
+        for j in range(cols):
+            a[i, j] = _num(tok[j], path, i + 2)
+    return a if prec == N.F64 else a.astype(np.float32, order="F")
+
+
+def _num(tok: str, path: str, line: int) -> float:
+    try:
+        if tok.strip() != tok or tok == "":
+            raise ValueError
+        return float(tok)
+    except ValueError:
+        raise RuntimeError(f"{path}: malformed number '{tok}' at line {line}")
+
+
+def plan_to_json(plan: SamplingPlan) -> str:
+    """io.cpp:232-243: nlohmann::json dump(2) of {seed, p, n, omega_r,
+    omega_c, delta, epsilon} (object keys in sorted order, as nlohmann's
+    std::map-backed objects print them)."""
+    import json
+
+    d = {"seed": int(plan.seed), "p": int(plan.p), "n": int(plan.n),
+         "omega_r": [int(x) for x in plan.omega_r], "omega_c": [int(x) for x in plan.omega_c],
+         "delta": float(plan.delta), "epsilon": float(plan.epsilon)}
+    return json.dumps(d, indent=2, sort_keys=True)
+
+
+def plan_from_json(text: str) -> SamplingPlan:
+    """io.cpp:245-263 (index ranges validated)."""
+    import json
+
+    j = json.loads(text)
+    plan = SamplingPlan(np.asarray(j["omega_r"], np.int64), np.asarray(j["omega_c"], np.int64), int(j["p"]),
+                        int(j["n"]), float(j["delta"]), float(j["epsilon"]), int(j["seed"]))
+    if np.any(plan.omega_r < 0) or np.any(plan.omega_r >= plan.p):
+        raise RuntimeError("plan: omega_r index out of range")
+    if np.any(plan.omega_c < 0) or np.any(plan.omega_c >= plan.n):
+        raise RuntimeError("plan: omega_c index out of range")
+    return plan
+
+
+def save_plan(plan: SamplingPlan, path: str):
+    with open(path, "w") as f:
+        f.write(plan_to_json(plan) + "\n")
+
+
+def load_plan(path: str) -> SamplingPlan:
+    with open(path) as f:
+        return plan_from_json(f.read())
