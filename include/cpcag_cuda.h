@@ -353,6 +353,27 @@ int cpcag_cuda_save_factors_glr1(cpcag_ctx ctx, const char* path, int64_t p, int
 int cpcag_cuda_load_factors_glr1(cpcag_ctx ctx, const char* path, int64_t p, int64_t n, int64_t k,
                                  int* scale_applied, double* U, double* sigma, double* V);
 
+/* ------------------------------------------------------------------ clustering
+ * kmeans (clustering.hpp:26-29, clustering.cpp:40-137) on the COLUMNS of X
+ * (rows x n, col-major, fp64 or fp32 widened to fp64): k-means++ seeding,
+ * Lloyd iterations, best of `restarts` by within-cluster sum of squares
+ * (written to wcss, may be NULL), emptied clusters re-seeded from the
+ * farthest point; deterministic for a seed (reference counter RNG streams
+ * derive(seed, restart)).  assignments: n ints in [0, k).
+ * Errors: "kmeans: k must be >= 1", "kmeans: more clusters than points",
+ * "kmeans: restarts must be >= 1" (invalid_argument). */
+int cpcag_cuda_kmeans(cpcag_ctx ctx, int precision, const void* X, int64_t rows, int64_t n, int64_t k,
+                      int64_t restarts, uint64_t seed, int64_t max_iter, int* assignments, double* wcss);
+/* decode_labels (clustering.hpp:31-35, clustering.cpp:139-160): upsample the
+ * indicator of the sampled-column labels (rho_c, values in [0, k)) over L_c
+ * with known set omega_c, then row-wise max pooling (ties: lowest column).
+ * labels: n ints. */
+int cpcag_cuda_decode_labels(cpcag_ctx ctx, const int* sampled, int64_t rho_c, int64_t k, const int64_t* omega_c,
+                             int64_t n, cpcag_csr Lc, double pcg_tol, int64_t pcg_max_iter, int* labels);
+/* clustering_error (clustering.hpp:37-39, clustering.cpp:220-238): host. */
+int cpcag_clustering_error(const int* pred, const int* truth, int64_t n, int64_t k_pred, int64_t k_truth,
+                           double* out);
+
 /* Optional factor output of the approximate decoder (PipelineReport::factors,
  * pipeline.hpp:91): fp64 U (p x k), sigma (k), V (n x k) when k <= k_cap. */
 typedef struct cpcag_pipeline_factors {

@@ -972,6 +972,158 @@ std::vector<i64> to_list(const int64_t* p, int64_t n) { return std::vector<i64>(
 
 }  // namespace
 
+// ---------------------------------------------------------------- clustering
+// clustering.cpp:40-137: Lloyd iterations with k-means++ seeding on the
+// columns of X (rows x n, column-major); squared norms are sequential sums
+// over the rows (Eigen's squaredNorm order is unspecified: the device
+// kernels use this same order, so they are compared bit for bit).
+namespace {
+
+double col_d2(const double* X, i64 rows, i64 j, const double* c) {
+  double s = 0.0;
+  const double* x = X + j * rows;
+  for (i64 i = 0; i < rows; ++i) {
+    const double d = x[i] - c[i];
+    s += d * d;
+  }
+  return s;
+}
+
+struct LloydRun {
+  std::vector<int> a;
+  double wcss = std::numeric_limits<double>::infinity();
+};
+
+LloydRun lloyd_once(const double* X, i64 rows, i64 n, i64 k, i64 max_iter, Rng rng) {
+  std::vector<double> cent(static_cast<size_t>(rows * k));
+  auto col = [&](i64 c) { return cent.data() + c * rows; };
+  auto set_col = [&](i64 c, i64 j) { std::copy(X + j * rows, X + (j + 1) * rows, col(c)); };
+  set_col(0, static_cast<i64>(rng.below(static_cast<uint64_t>(n))));  // :44
+  std::vector<double> min_d2(static_cast<size_t>(n), std::numeric_limits<double>::infinity());
+  for (i64 c = 1; c < k; ++c) {  // :46-66
+    for (i64 j = 0; j < n; ++j) min_d2[j] = std::min(min_d2[j], col_d2(X, rows, j, col(c - 1)));
+    double total = 0.0;
+    for (i64 j = 0; j < n; ++j) total += min_d2[j];
+    i64 pick = 0;
+    if (total > 0.0) {
+      double target = rng.uniform() * total;
+      for (i64 j = 0; j < n; ++j) {
+        target -= min_d2[j];
+        if (target <= 0.0) {
+          pick = j;
+          break;
+        }
+        pick = j;
+      }
+    } else {
+      pick = static_cast<i64>(rng.below(static_cast<uint64_t>(n)));
+    }
+    set_col(c, pick);
+  }
+  LloydRun run;
+  run.a.assign(static_cast<size_t>(n), 0);
+  std::vector<i64> counts(static_cast<size_t>(k));
+  std::vector<double> sums(static_cast<size_t>(rows * k));
+  for (i64 it = 0; it < max_iter; ++it) {  // :71-107
+    bool changed = false;
+    for (i64 j = 0; j < n; ++j) {
+      i64 best = 0;
+      double bd = std::numeric_limits<double>::infinity();
+      for (i64 c = 0; c < k; ++c) {
+        const double d = col_d2(X, rows, j, col(c));
+        if (d < bd) {
+          bd = d;
+          best = c;
+        }
+      }
+      if (static_cast<int>(best) != run.a[j]) {
+        run.a[j] = static_cast<int>(best);
+        changed = true;
+      }
+    }
+    if (!changed && it > 0) break;
+    std::fill(sums.begin(), sums.end(), 0.0);
+    std::fill(counts.begin(), counts.end(), i64{0});
+    for (i64 j = 0; j < n; ++j) {
+      double* sc = sums.data() + static_cast<i64>(run.a[j]) * rows;
+      const double* x = X + j * rows;
+      for (i64 i = 0; i < rows; ++i) sc[i] += x[i];
+      ++counts[run.a[j]];
+    }
+    for (i64 c = 0; c < k; ++c) {
+      if (counts[c] > 0) {
+        const double cn = static_cast<double>(counts[c]);
+        for (i64 i = 0; i < rows; ++i) col(c)[i] = sums[c * rows + i] / cn;
+      } else {
+        i64 far = 0;
+        double fd = -1.0;
+        for (i64 j = 0; j < n; ++j) {
+          const double d = col_d2(X, rows, j, col(run.a[j]));
+          if (d > fd) {
+            fd = d;
+            far = j;
+          }
+        }
+        set_col(c, far);
+        run.a[far] = static_cast<int>(c);
+      }
+    }
+  }
+  run.wcss = 0.0;
+  for (i64 j = 0; j < n; ++j) run.wcss += col_d2(X, rows, j, col(run.a[j]));
+  return run;
+}
+
+// clustering.cpp:165-218 (Hungarian method on cost = -score).
+std::vector<i64> max_assignment(const std::vector<double>& score, i64 n) {
+  std::vector<double> u(static_cast<size_t>(n) + 1, 0.0), v(static_cast<size_t>(n) + 1, 0.0);
+  std::vector<i64> match(static_cast<size_t>(n) + 1, 0), way(static_cast<size_t>(n) + 1, 0);
+  const double inf = std::numeric_limits<double>::infinity();
+  for (i64 i = 1; i <= n; ++i) {
+    match[0] = i;
+    i64 j0 = 0;
+    std::vector<double> minv(static_cast<size_t>(n) + 1, inf);
+    std::vector<char> used(static_cast<size_t>(n) + 1, 0);
+    do {
+      used[j0] = 1;
+      const i64 i0 = match[j0];
+      double delta = inf;
+      i64 j1 = 0;
+      for (i64 j = 1; j <= n; ++j) {
+        if (used[j]) continue;
+        const double cur = -score[(i0 - 1) + (j - 1) * n] - u[i0] - v[j];
+        if (cur < minv[j]) {
+          minv[j] = cur;
+          way[j] = j0;
+        }
+        if (minv[j] < delta) {
+          delta = minv[j];
+          j1 = j;
+        }
+      }
+      for (i64 j = 0; j <= n; ++j) {
+        if (used[j]) {
+          u[match[j]] += delta;
+          v[j] -= delta;
+        } else {
+          minv[j] -= delta;
+        }
+      }
+      j0 = j1;
+    } while (match[j0] != 0);
+    do {
+      const i64 j1 = way[j0];
+      match[j0] = match[j1];
+      j0 = j1;
+    } while (j0 != 0);
+  }
+  std::vector<i64> r2c(static_cast<size_t>(n), 0);
+  for (i64 j = 1; j <= n; ++j) r2c[match[j] - 1] = j - 1;
+  return r2c;
+}
+
+}  // namespace
+
 struct ora_csr : Csr {
   explicit ora_csr(Csr&& m) : Csr(std::move(m)) {}
 };
@@ -1243,6 +1395,34 @@ int ora_decoder_apply(const double* X, int64_t p, int64_t n, const int64_t* omeg
     const auto omc = to_list(omega_c, rho_c);
     DecoderOp op{*Lr, *Lc, to_csc(*Lc), omr, omc, gbar_r, gbar_c, p, n};
     op.apply(X, out);
+  });
+}
+
+int ora_kmeans(const double* X, int64_t rows, int64_t n, int64_t k, int64_t restarts, uint64_t seed,
+               int64_t max_iter, int* assignments, double* wcss) {
+  return guard([&] {
+    if (k < 1) throw std::invalid_argument("kmeans: k must be >= 1");
+    if (k > n) throw std::invalid_argument("kmeans: more clusters than points");
+    if (restarts < 1) throw std::invalid_argument("kmeans: restarts must be >= 1");
+    LloydRun best;
+    for (int64_t r = 0; r < restarts; ++r) {  // clustering.cpp:131-134
+      LloydRun run = lloyd_once(X, rows, n, k, max_iter, Rng::derive(seed, static_cast<uint64_t>(r)));
+      if (run.wcss < best.wcss) best = std::move(run);
+    }
+    std::copy(best.a.begin(), best.a.end(), assignments);
+    if (wcss) *wcss = best.wcss;
+  });
+}
+
+int ora_clustering_error(const int* pred, const int* truth, int64_t n, int64_t k, double* out) {
+  return guard([&] {
+    if (n == 0) throw std::invalid_argument("clustering error: empty labels");
+    std::vector<double> cont(static_cast<size_t>(k * k), 0.0);
+    for (int64_t i = 0; i < n; ++i) cont[pred[i] + static_cast<int64_t>(truth[i]) * k] += 1.0;
+    const std::vector<i64> perm = max_assignment(cont, k);
+    double agree = 0.0;
+    for (int64_t c = 0; c < k; ++c) agree += cont[c + perm[c] * k];
+    *out = 1.0 - agree / static_cast<double>(n);
   });
 }
 

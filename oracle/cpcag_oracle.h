@@ -125,6 +125,12 @@ int ora_decoder_apply(const double* X, int64_t p, int64_t n, const int64_t* omeg
                       int64_t rho_r, const int64_t* omega_c, int64_t rho_c, const ora_csr* Lr,
                       const ora_csr* Lc, double gbar_r, double gbar_c, double* out);
 
+/* kmeans (clustering.cpp:40-137): assignments n; wcss of the kept restart. */
+int ora_kmeans(const double* X, int64_t rows, int64_t n, int64_t k, int64_t restarts, uint64_t seed,
+               int64_t max_iter, int* assignments, double* wcss);
+/* clustering_error (clustering.cpp:222-238). */
+int ora_clustering_error(const int* pred, const int* truth, int64_t n, int64_t k, double* out);
+
 #ifdef __cplusplus
 }
 #endif

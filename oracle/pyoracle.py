@@ -64,6 +64,8 @@ def lib():
         L.ora_rng_gaussian.argtypes = [C.c_uint64, i64, dp]
         L.ora_power_iteration_norm.argtypes = [vp, C.c_double, C.c_uint64, i64, dp]
         L.ora_draw_plan.argtypes = [i64, i64, i64, i64, C.c_uint64, ip, ip]
+        L.ora_kmeans.argtypes = [dp, i64, i64, i64, i64, C.c_uint64, i64, C.POINTER(C.c_int), dp]
+        L.ora_clustering_error.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_int), i64, i64, dp]
         _lib = L
     return _lib
 
@@ -598,3 +600,44 @@ def spectral_gap(eigenvalues, k):
     if lk1 <= 1e-14:
         raise RuntimeError("gap undefined: graph has > k components")
     return lk, lk1, lk / lk1
+
+
+# ------------------------------------------------------------------ clustering (clustering.cpp)
+def kmeans(X, k, restarts=10, seed=0, max_iter=100):
+    """clustering.cpp:40-137 on the columns of X.  Returns (assignments, wcss)."""
+    X = _f64(np.asarray(X).reshape(-1, 1) if np.ndim(X) == 1 else X)
+    rows, n = X.shape
+    a = np.empty(n, np.int32)
+    w = C.c_double()
+    _check(lib().ora_kmeans(_d(X), i64(rows), i64(n), i64(k), i64(restarts), C.c_uint64(int(seed) & (2**64 - 1)),
+                            i64(max_iter), a.ctypes.data_as(C.POINTER(C.c_int)), C.byref(w)))
+    return a, w.value
+
+
+def decode_labels(sampled, k, plan, Lc: Csr, pcg_tol=1e-10, pcg_max_iter=5000):
+    """clustering.cpp:139-160: upsample the sampled-column indicator over the
+    column graph, then row-wise max pooling (ties keep the lowest column)."""
+    sampled = np.asarray(sampled, np.int64)
+    if len(sampled) != len(plan.omega_c):
+        raise ValueError("decode_labels: sampled labels do not match plan")
+    if Lc.rows != plan.n:
+        raise ValueError("decode_labels: column Laplacian does not match plan")
+    if k < 1 or np.any(sampled < 0) or np.any(sampled >= k):
+        raise ValueError("labels: assignment out of range")
+    Ct = np.zeros((len(sampled), k))
+    Ct[np.arange(len(sampled)), sampled] = 1.0
+    Cm = graph_upsample(Lc, plan.omega_c, Ct, pcg_tol, pcg_max_iter)
+    return np.argmax(Cm, axis=1).astype(np.int32), Cm  # argmax: first maximum = strict '>' scan
+
+
+def clustering_error(pred, truth, k):
+    """clustering.cpp:222-238 (Hungarian max assignment on the k x k
+    contingency matrix)."""
+    pred = np.ascontiguousarray(pred, np.int32)
+    truth = np.ascontiguousarray(truth, np.int32)
+    if len(pred) != len(truth):
+        raise ValueError("clustering error: label vectors differ in length")
+    out = C.c_double()
+    _check(lib().ora_clustering_error(pred.ctypes.data_as(C.POINTER(C.c_int)), truth.ctypes.data_as(C.POINTER(C.c_int)),
+                                      i64(len(pred)), i64(k), C.byref(out)))
+    return out.value

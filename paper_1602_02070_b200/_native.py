@@ -115,6 +115,9 @@ SIGNATURES = {
     "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_sym_eigvals_lanczos": (C.c_int, [vp, vp, i64, C.c_double, i64, C.c_uint64, vp, vp]),
     "cpcag_glr1_info": (C.c_int, [C.c_char_p, vp, vp]),
+    "cpcag_cuda_kmeans": (C.c_int, [vp, C.c_int, vp, i64, i64, i64, i64, C.c_uint64, i64, vp, vp]),
+    "cpcag_cuda_decode_labels": (C.c_int, [vp, vp, i64, i64, vp, i64, vp, C.c_double, i64, vp]),
+    "cpcag_clustering_error": (C.c_int, [vp, vp, i64, i64, i64, vp]),
     "cpcag_cuda_load_matrix_glr1": (C.c_int, [vp, C.c_char_p, C.c_int, vp, i64, i64]),
     "cpcag_cuda_save_matrix_glr1": (C.c_int, [vp, C.c_char_p, C.c_int, vp, i64, i64]),
     "cpcag_cuda_load_sparse_glr1": (C.c_int, [vp, C.c_char_p, vp]),

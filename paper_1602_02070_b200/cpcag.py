@@ -32,6 +32,7 @@ __all__ = [
     "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "sym_eigvals_lanczos", "spectral_gap",
     "glr1_info", "load_matrix", "save_matrix", "load_sparse", "save_sparse", "save_factors",
     "load_factors", "plan_to_json", "plan_from_json", "save_plan", "load_plan",
+    "ClusterLabels", "kmeans", "decode_labels", "clustering_error",
 ]
 
 
@@ -1090,3 +1091,70 @@ def save_plan(plan: SamplingPlan, path: str):
 def load_plan(path: str) -> SamplingPlan:
     with open(path) as f:
         return plan_from_json(f.read())
+
+
+# ------------------------------------------------------------------ clustering (clustering.hpp)
+@dataclass
+class ClusterLabels:  # clustering.hpp:13-21
+    assignments: np.ndarray
+    k: int = 0
+
+    def size(self) -> int:
+        return len(self.assignments)
+
+    def indicator(self) -> np.ndarray:
+        C = np.zeros((self.size(), self.k))
+        C[np.arange(self.size()), self.assignments] = 1.0
+        return C
+
+    @staticmethod
+    def from_assignments(assignments, k: int) -> "ClusterLabels":
+        a = np.asarray(assignments, np.int32)
+        if k < 1:
+            raise ValueError("labels: k must be >= 1")
+        if np.any(a < 0) or np.any(a >= k):
+            raise ValueError("labels: assignment out of range")
+        return ClusterLabels(a, int(k))
+
+
+def kmeans(X, k: int, restarts: int = 10, seed: int = 0, max_iter: int = 100, precision=None,
+           ctx=None) -> ClusterLabels:
+    """clustering.hpp:26-29: k-means++ / Lloyd on the columns of X, on the device."""
+    prec = _precision(X, precision)
+    x = _In(X, prec)
+    if len(x.shape) != 2:
+        raise ValueError("kmeans: X must be a matrix")
+    rows, n = x.shape
+    a = np.empty(max(n, 1), np.int32)
+    w = N.dbl()
+    N.check(N.lib().cpcag_cuda_kmeans(_ctx(ctx), prec, x.ptr, rows, n, int(k), int(restarts), int(seed) & (2**64 - 1),
+                                      int(max_iter), a.ctypes.data, C.byref(w)))
+    return ClusterLabels(a[:n].copy(), int(k))
+
+
+def decode_labels(sampled: ClusterLabels, plan: SamplingPlan, Lc: "SparseMatrix", pcg_tol: float = 1e-10,
+                  pcg_max_iter: int = 5000, ctx=None) -> ClusterLabels:
+    """clustering.hpp:31-35 / clustering.cpp:139-160 on the device."""
+    if sampled.size() != plan.rho_c():
+        raise ValueError("decode_labels: sampled labels do not match plan")
+    if Lc.rows() != plan.n:
+        raise ValueError("decode_labels: column Laplacian does not match plan")
+    lab = np.ascontiguousarray(sampled.assignments, np.int32)
+    om = np.ascontiguousarray(plan.omega_c, np.int64)
+    out = np.empty(max(plan.n, 1), np.int32)
+    N.check(N.lib().cpcag_cuda_decode_labels(_ctx(ctx), lab.ctypes.data, len(lab), int(sampled.k), om.ctypes.data,
+                                             int(plan.n), Lc.handle, float(pcg_tol), int(pcg_max_iter),
+                                             out.ctypes.data))
+    return ClusterLabels(out[:plan.n].copy(), int(sampled.k))
+
+
+def clustering_error(pred: ClusterLabels, truth: ClusterLabels) -> float:
+    """clustering.hpp:37-39 / clustering.cpp:220-238."""
+    if pred.size() != truth.size():
+        raise ValueError("clustering error: label vectors differ in length")
+    p = np.ascontiguousarray(pred.assignments, np.int32)
+    t = np.ascontiguousarray(truth.assignments, np.int32)
+    out = N.dbl()
+    N.check(N.lib().cpcag_clustering_error(p.ctypes.data, t.ctypes.data, len(p), int(pred.k), int(truth.k),
+                                           C.byref(out)))
+    return float(out.value)
