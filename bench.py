@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="cfg3 through the column-sharded decoder over NCCL (one column block per rank)")
-    ap.add_argument("--config", choices=["cfg1", "cfg2", "cfg3"], default="cfg1",
+    ap.add_argument("--config", choices=["cfg0", "cfg1", "cfg2", "cfg3"], default="cfg1",
                     help="cfg1 (default, the headline): full CPCA; cfg2: kNN graph alone; cfg3: decoder at scale")
     return ap.parse_args()
 
@@ -466,15 +466,21 @@ def cpu_sample_times(wl, fista_iters=4, cg_iters=3):
     Lrt = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
     Lct = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
     t["kron"] = time.perf_counter() - t0
+    # the step's two power iterations (frpcag.cpp:70-75) run once per solve:
+    # timed in full, then the sampled FISTA iterations reuse the step
     t0 = time.perf_counter()
-    Xt, tr = O.fista_solve(Yt, Lrt, Lct, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, fista_iters))
+    beta = (2.0 * wl.gamma * O.power_iteration_norm(Lct, 1e-7, 42, 50000) +
+            2.0 * wl.gamma * O.power_iteration_norm(Lrt, 1e-7, 42, 50000))
+    t["power"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Xt, tr = O.fista_solve(Yt, Lrt, Lct, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, fista_iters,
+                                                         step=1.0 / beta))
     t["solve_sample"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, cg_iters)
     t["decode_sample"] = time.perf_counter() - t0
-    # the power iterations for the FISTA step are included once in solve_sample
-    full = (t["graphs"] + t["plan"] + t["subsample"] + t["kron"] + t["solve_sample"] / fista_iters * wl.fista_iters
-            + t["decode_sample"] / cg_iters * wl.cg_iters)
+    full = (t["graphs"] + t["plan"] + t["subsample"] + t["kron"] + t["power"] +
+            t["solve_sample"] / fista_iters * wl.fista_iters + t["decode_sample"] / cg_iters * wl.cg_iters)
     return full, t
 
 
@@ -484,8 +490,8 @@ def cpu_baseline(wl):
     cores = O.get_threads()
     full, t = cpu_sample_times(wl)
     return {"value": round(full, 3), "unit": "s", "cores": cores, "kind": "port",
-            "sample": "oracle port on config 1: graphs, plan, subsample and Kron in full; FRPCAG 4 of 300 and "
-                      "decoder 3 of 200 iterations timed and extrapolated linearly "
+            "sample": "oracle port on config 1: graphs, plan, subsample, Kron and the step's power iterations in "
+                      "full; FRPCAG 4 of 300 and decoder 3 of 200 iterations timed and extrapolated linearly "
                       f"(stage seconds {json.dumps({k: round(v, 3) for k, v in t.items()})})"}
 
 
@@ -509,8 +515,8 @@ def run_reference(args, rank, world):
     t_all1 = time.perf_counter()
     v = sum(vals) / len(vals)
     sample = ("oracle port (CPU restatement of the reference; the reference needs Eigen3, absent) on config 1: "
-              "graphs, plan, subsample, Kron in full; FRPCAG 4/300 and decoder 3/200 iterations per step, "
-              "extrapolated linearly to the full run")
+              "graphs, plan, subsample, Kron and the step's power iterations in full; FRPCAG 4/300 and decoder "
+              "3/200 iterations per step, extrapolated linearly to the full run")
     out = {"metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded config-1 generator",
@@ -528,7 +534,7 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ cfg2 / cfg3
-def timed_steps(fn, steps, warmup, stream, clocks_out=None):
+def timed_steps(fn, steps, warmup, stream, clocks_out=None, pre=None):
     """Mean device ms of `steps` calls after `warmup`; clocks sampled between
     steps (NVML, see NvmlClockSampler) into clocks_out when given."""
     import torch
@@ -541,6 +547,8 @@ def timed_steps(fn, steps, warmup, stream, clocks_out=None):
     evs = []
     torch.cuda.profiler.start()  # ncu --profile-from-start off captures the timed steps only
     for _ in range(steps):
+        if pre is not None:
+            pre()  # e.g. the L2 flush, outside the events
         if hasattr(clocks, "tick"):
             clocks.tick()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -556,6 +564,69 @@ def timed_steps(fn, steps, warmup, stream, clocks_out=None):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     print(f"[bench] step ms {[round(x, 2) for x in step_ms]}", file=sys.stderr, flush=True)
     return sum(step_ms) / len(step_ms)
+
+
+def run_cfg0(args):
+    """Small full CPCA in fp64 (BASELINE config 0): latency-bound, reported as
+    end-to-end seconds and FRPCAG + decoder iterations/s; the
+    oracle port runs the same pipeline in full as the CPU baseline."""
+    import torch
+
+    import paper_1602_02070_b200 as P
+    from oracle import pyoracle as O
+    from paper_1602_02070_b200 import workloads
+
+    wl = workloads.config0_workload()
+    p, n = wl.Y.shape
+    ctx = P.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.reserve(1 << 30)
+    Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=torch.float64, device="cuda").t()
+    cfg = P.PipelineConfig(knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
+                           frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
+                                                 max_iter=wl.fista_iters),
+                           decoder=P.DecoderConfig(gamma=1.0, pcg_tol=wl.cg_tol, pcg_max_iter=wl.cg_iters,
+                                                   variant="alternate"),
+                           lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1602)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+    res = {}
+
+    def step():
+        res["r"] = P.run_pipeline(Yd, cfg, ctx=ctx)
+
+    clk = {}
+    ms = timed_steps(step, args.steps, max(args.warmup, 3), stream, clk, pre=flush.zero_)
+    rep = res["r"]
+    it_f, it_c = rep.trace.iterations, rep.decoder_iterations
+    st = rep.stages
+    out = {"metric": METRIC, "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic: seeded config-0 generator (circle manifolds, rank 10 on the kNN graphs, 5% outliers)",
+           "config": {"workload": f"cfg0: CPCA {p}x{n} fp64, kNN(K=10) row and column graphs, a=b={wl.a}, "
+                                  f"FRPCAG {wl.fista_iters} it, alternate CG decoder max {wl.cg_iters} it tol 1e-8",
+                      "l2": "flushed between steps (512 MiB write outside the events)"},
+           "clocks": clk, "stage_ms": {k: round(v, 3) for k, v in st.items()},
+           "iters": {"fista_iters": it_f, "decoder_iters": it_c,
+                     "frpcag_plus_decoder_iters_per_s": round((it_f + it_c) / ((st["solve"] + st["decode"]) / 1e3), 1)},
+           "roofline": None, "roofline_note": "latency-bound at this size (SURVEY 8(d)): no roofline fraction"}
+    if not args.no_cpu_baseline:
+        t0 = time.perf_counter()
+        Y = np.asfortranarray(wl.Y)
+        gr, gc = O.build_knn_graph(Y, True, 10), O.build_knn_graph(Y, False, 10)
+        plan = O.draw_plan(p, n, -(-p // wl.b), -(-n // wl.a), seed=1602)
+        Xt, _ = O.fista_solve(O.subsample(Y, plan), O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11),
+                              O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11),
+                              O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, wl.fista_iters))
+        O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, wl.cg_tol,
+                           wl.cg_iters)
+        out["cpu_baseline"] = {"value": round(time.perf_counter() - t0, 4), "unit": "s", "cores": O.get_threads(),
+                               "kind": "port", "sample": "oracle port, the whole config-0 pipeline once"}
+    print(json.dumps(out), flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            json.dump(out, f)
 
 
 def run_cfg2(args):
@@ -761,6 +832,8 @@ def run_cfg3_sharded(args, rank, local_rank, world):
 def main():
     args = parse()
     rank, local_rank, world = dist_env()
+    if args.config == "cfg0" and args.impl == "ours":
+        return run_cfg0(args)
     if args.config == "cfg2" and args.impl == "ours":
         return run_cfg2(args)
     if args.config == "cfg3" and args.impl == "ours":
