@@ -626,6 +626,111 @@ __global__ void __launch_bounds__(1024, 1) cg_lc_slab_k(int p, int n, Pull<T> Lc
   }
 }
 
+// slabr: one-pass apply for iterates with few columns (config 1: n = 1000)
+// and a low-degree row graph (the pixel grid, degree <= MAXD).  A CTA owns
+// (32-row slab, column part) units: the slab of P over ALL n columns sits in
+// shared memory, so every L_c gather is a conflict-free shared read (lane =
+// row; fast2 instead re-reads ~19 P columns per output from L2, ~800 MB per
+// config-1 apply); the unit's L_c entries are staged in shared memory and
+// read as warp broadcasts; each lane holds its row's L_r entries in
+// registers, so the stencil gathers P(k, c) (rows within the grid's halo of
+// the slab) are independent global loads issued together.  Per-entry
+// arithmetic and order are fast2's (CSR order, madd_entry, the same
+// combination): AP is bit-identical to fast2.  <P, AP> is summed in a fixed
+// order per CTA (deterministic; its order differs from fast2's).
+template <typename T, int MAXD>
+__global__ void __launch_bounds__(1024, 1) cg_apply_slabr_k(int p, int n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                            int parts, int units, const T* __restrict__ P,
+                                                            T* __restrict__ AP, double* partials, CgState* st) {
+  if (st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* S = reinterpret_cast<T*>(smraw);  // S[c * 32 + r] = P[i0 + r, c]
+  OffEnt<T>* E = reinterpret_cast<OffEnt<T>*>(smraw + static_cast<size_t>(n) * 32 * sizeof(T));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int u0 = static_cast<int>((static_cast<i64>(units) * blockIdx.x) / gridDim.x);
+  const int u1 = static_cast<int>((static_cast<i64>(units) * (blockIdx.x + 1)) / gridDim.x);
+  const int cw = (n + parts - 1) / parts;
+  int staged = -1, staged_part = -1;
+  T ra[MAXD];
+  int oa[MAXD];
+  int da = 0;
+  bool valid = false, rs = false;
+  double s[1] = {0.0};
+  for (int u = u0; u < u1; ++u) {
+    const int slab = u / parts, part = u - slab * parts;
+    const int i0 = slab * 32, rows = min(32, p - i0);
+    const int c_lo = part * cw, c_hi = min(n, c_lo + cw);
+    const i64 e0 = Lc.rp[c_lo];
+    if (slab != staged || part != staged_part) {
+      __syncthreads();
+      if (slab != staged) {
+        for (int c = warp; c < n; c += 32) S[c * 32 + lane] = lane < rows ? P[i0 + lane + static_cast<i64>(c) * p] : T(0);
+        const int i = i0 + lane;
+        valid = lane < rows;
+        da = 0;
+        rs = valid && pl.rsel[i] >= 0;
+        if (valid) {
+          const i64 a0 = Lr.rp[i];
+          da = static_cast<int>(Lr.rp[i + 1] - a0);
+#pragma unroll
+          for (int k = 0; k < MAXD; ++k) {
+            ra[k] = k < da ? Lr.v[a0 + k] : T(0);
+            oa[k] = k < da ? Lr.ci[a0 + k] : 0;
+          }
+        }
+      }
+      if (part != staged_part) {
+        const int ne = static_cast<int>(Lc.rp[c_hi] - e0);
+        for (int k = threadIdx.x; k < ne; k += blockDim.x) {
+          OffEnt<T> e;
+          e.v = Lc.v[e0 + k];
+          e.off = Lc.ci[e0 + k] * 32;
+          E[k] = e;
+        }
+      }
+      __syncthreads();
+      staged = slab;
+      staged_part = part;
+    }
+    for (int c = c_lo + warp; c < c_hi; c += 32) {
+      const T* pc = P + static_cast<i64>(c) * p;
+      T g[MAXD];
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k) g[k] = k < da ? pc[oa[k]] : T(0);
+      const int k0 = static_cast<int>(Lc.rp[c] - e0), k1 = static_cast<int>(Lc.rp[c + 1] - e0);
+      T x = T(0);
+#pragma unroll 4
+      for (int k = k0; k < k1; ++k) {
+        const OffEnt<T> e = E[k];
+        x = madd_entry(x, e.v, S[e.off + lane]);
+      }
+      T y = T(0);
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k)
+        if (k < da) y = madd_entry(y, ra[k], g[k]);
+      if (valid) {
+        T out = add_rn(mul_rn(gc, x), mul_rn(gr, y));
+        const T pv = S[c * 32 + lane];
+        if (rs && pl.csel[c] >= 0) out = add_rn(out, pv);
+        AP[i0 + lane + static_cast<i64>(c) * p] = out;
+        s[0] += static_cast<double>(pv) * static_cast<double>(out);
+      }
+    }
+  }
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[1], tot) && threadIdx.x == 0) {
+    const double curv = tot[0];
+    st->curv = curv;
+    if (!isfinite(curv) || curv <= 0.0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+      return;
+    }
+    st->alpha = st->rho / curv;
+  }
+}
+
 // regr: fast2 with each thread's L_r rows held in REGISTERS (row degree <=
 // MAXD; the pixel-grid row graph of config 1 has degree 9).  L_r is the same
 // for every column, so fast2's per-column re-read of the row's (value,
@@ -2017,13 +2122,16 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
       if (part.n < static_cast<size_t>(gs4.x) * gs4.y) part.alloc(c, static_cast<size_t>(gs4.x) * gs4.y);
     }
   }
+  i64 maxdeg_r_pre = 0;
+  for (i64 i = 0; i < p; ++i) maxdeg_r_pre = std::max(maxdeg_r_pre, rpr[i + 1] - rpr[i]);
   // slab2 (two-pass apply: cg_lc_slab_k then fast2<kU>), when a 32-row slab
   // over all n columns fits in shared memory.
   int s2_parts = 4, s2_units = 0;
   unsigned s2_grid = 0;
   size_t s2_smem = 0;
   DevBuf<T> Ubuf;
-  if (variant == "slab2") {
+  if (variant == "slabr" && !(maxdeg_r_pre <= 16)) variant = "fast2";
+  if (variant == "slab2" || variant == "slabr") {
     if (!(p * n < (i64{1} << 31) && n * 32 * static_cast<i64>(sizeof(T)) <= 200 * 1024)) {
       variant = "fast2";
     } else {
@@ -2043,8 +2151,11 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
         s2_grid = 0;
       } else {
         ensure_smem(cg_lc_slab_k<T>, s2_smem);
+        ensure_smem(cg_apply_slabr_k<T, 10>, s2_smem);
+        ensure_smem(cg_apply_slabr_k<T, 16>, s2_smem);
       }
-      if (s2_grid) Ubuf.alloc(c, static_cast<size_t>(N));
+      if (s2_grid && variant == "slab2") Ubuf.alloc(c, static_cast<size_t>(N));
+      if (s2_grid && part.n < s2_grid) part.alloc(c, s2_grid);
     }
   }
   // regr (register-resident L_r rows) needs row degree <= 16.
@@ -2118,6 +2229,10 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
             cg_apply_fast2_k<T, 4, true><<<gs2, kBlock, fast2_smem, c->stream>>>(
                 static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl, static_cast<int>(cpc2), P.p, AP.p,
                 part.p, st.p, Ubuf.p);
+        } else if (variant == "slabr") {
+          auto kr = maxdeg_r_pre <= 10 ? cg_apply_slabr_k<T, 10> : cg_apply_slabr_k<T, 16>;
+          kr<<<s2_grid, 1024, s2_smem, c->stream>>>(static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl,
+                                                    s2_parts, s2_units, P.p, AP.p, part.p, st.p);
         } else if (variant == "regr") {
           cg_apply_regr_k<T, 16, false><<<gs2, kBlock, fast2_smem, c->stream>>>(
               static_cast<int>(p), static_cast<int>(n), pr, pc, gr, gc, pl, static_cast<int>(cpc2), P.p, AP.p, part.p,

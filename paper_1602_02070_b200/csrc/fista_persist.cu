@@ -42,11 +42,13 @@ namespace cpcag_cuda {
 namespace {
 
 constexpr int kPT = 256;      // threads per CTA
-constexpr int kPartRegs = 5;  // partial-sum loads per lane: grid <= 160 CTAs
+constexpr int kMaxGrid = 160;      // CTAs (one per SM)
+constexpr int kPsm = 4 * kMaxGrid;  // doubles of the partial-sum staging area
 
 struct PersistArgs {
   int rr, rc, ldS, ldT;
   int TM, TN, C, KS, KC;
+  int ldA, ldB;  // shared-memory row strides of the k-major A (TM) and B (TN) panels
   int use_r, use_c, loss;
   int dbg;  // diagnostics (CPCAG_FISTA_PERSIST_DBG): 1 = no B chunk loads, 2 = no chunk FMAs
   float step;
@@ -100,19 +102,59 @@ __device__ __forceinline__ void strip_gemm(float (&acc)[4][4], const float* ap, 
   for (int q = 0; q < cnt; ++q) fma44(acc, lds4(ap + q * sa), lds4(bp + q * sb));
 }
 
-__global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
-  extern __shared__ __align__(16) float sm[];
+// acc[x 8 + y] += a[x] b[y] for one k (8-float strips of A and B).
+__device__ __forceinline__ void fma88(float (&acc)[64], const float* ap, const float* bp) {
+  const float4 a0 = lds4(ap), a1 = lds4(ap + 4), b0 = lds4(bp), b1 = lds4(bp + 4);
+  const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+  for (int x = 0; x < 8; ++x)
+#pragma unroll
+    for (int y = 0; y < 8; ++y) acc[x * 8 + y] = fmaf(av[x], bv[y], acc[x * 8 + y]);
+}
+
+// Sum of the 64 partial entries over the 32 lanes, scattered: after five
+// halving rounds (partner lane ^ 16, 8, 4, 2, 1; the lane with the bit set
+// keeps the upper half) lane l holds entries 2 l and 2 l + 1 in acc[0..1].
+// The summation tree is fixed, so the result is deterministic.
+__device__ __forceinline__ void reduce_scatter64(float (&acc)[64], int lane) {
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int o = 16 >> r, half = 32 >> r;
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? acc[i] : acc[i + half];
+      const float keep = up ? acc[i + half] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
+// MODE 0: 4 x 4 micro-tiles, the k range split across thread groups (KS),
+//         partial tiles summed through shared memory.
+// MODE 1: 8 x 8 micro-tiles, one warp per micro-tile with the k range split
+//         across its lanes, lanes reduced by a fixed shuffle reduce-scatter
+//         (twice the multiply-adds per shared-memory wavefront of MODE 0).
+template <int MODE>
+__global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(const PersistArgs a) {
+  const int kPT = blockDim.x;
+  constexpr int NST = MODE == 0 ? 2 : 4;  // stages of the S-panel ring
+  extern __shared__ __align__(16) double smd[];
+  double* psm = smd;  // [kPsm] partial sums of the previous iteration (4 per CTA)
+  float* sm = reinterpret_cast<float*>(smd + kPsm);
   __shared__ double tot_sh[4];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int TM = a.TM, TN = a.TN, TE = TM * TN, rr = a.rr, rc = a.rc, KC = a.KC, KS = a.KS;
   const int rb = blockIdx.x / a.C, cb = blockIdx.x % a.C;
   const int r0 = rb * TM, c0 = cb * TN;
   const int rn = min(TM, rr - r0), cn = min(TN, rc - c0);
-  float* As = sm;                                     // [rr][TM]  g_r L~_r(r0 + i, k)
-  float* Bc = As + static_cast<size_t>(rr) * TM;      // [rc][TN]  g_c L~_c(k, c0 + j)
-  float* A2 = Bc + static_cast<size_t>(rc) * TN;      // [rc][TM]  S(r0 + i, k)
-  float* Bb = A2 + static_cast<size_t>(rc) * TM;      // [2][KC][TN]  S(k, c0 + j)
-  float* red = Bb + 2 * static_cast<size_t>(KC) * TN;  // [KS][TE]  split-k partials
+  const int ldA = a.ldA, ldB = a.ldB;
+  float* As = sm;                                      // [rr][ldA]  g_r L~_r(r0 + i, k)
+  float* Bc = As + static_cast<size_t>(rr) * ldA;      // [rc][ldB]  g_c L~_c(k, c0 + j)
+  float* A2 = Bc + static_cast<size_t>(rc) * ldB;      // [rc][ldA]  S(r0 + i, k)
+  float* Bb = A2 + static_cast<size_t>(rc) * ldA;      // [2][KC][ldB]  S(k, c0 + j)
+  float* red = Bb + NST * static_cast<size_t>(KC) * ldB;  // [KS][TE]  split-k partials (MODE 1: KS = 1)
   float* Yt = red + static_cast<size_t>(KS) * TE;     // tile state, e = i + TM j
   float* Zt = Yt + TE;                                // Z_j
   float* HZ = Zt + TE;                                // H(Z_j)
@@ -125,13 +167,13 @@ __global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
     for (int t = tid; t < rr * TM; t += kPT) {
       const int k = t / TM, i = t - k * TM;
       // L~_r(r0 + i, k) from the column-major dense copy (contiguous in i)
-      As[t] = i < rn ? static_cast<float>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
+      As[k * ldA + i] = i < rn ? static_cast<float>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
                      : 0.f;
     }
   if (a.use_c)
     for (int t = tid; t < rc * TN; t += kPT) {
       const int k = t / TN, j = t - k * TN;
-      Bc[t] = j < cn ? static_cast<float>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
+      Bc[k * ldB + j] = j < cn ? static_cast<float>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
                      : 0.f;
     }
   for (int e = tid; e < TE; e += kPT) {
@@ -152,43 +194,60 @@ __global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
   const int nmi = TM / 4, NMT = nmi * (TN / 4);
   const bool gthr = tid < NMT * KS;
   const int mt = tid % NMT, s = tid / NMT, mi = mt % nmi, ni = mt / nmi;
+  const int mi8 = warp % max(TM / 8, 1), ni8 = warp / max(TM / 8, 1);
+  const bool w8 = MODE == 1 && warp < (TM / 8) * (TN / 8);
   auto tile_gemm = [&](const float* Sbuf, const float* SbufT) {
     float acc[4][4];
+    float acc8[MODE == 1 ? 64 : 1];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+#pragma unroll
+    for (int q = 0; q < (MODE == 1 ? 64 : 1); ++q) acc8[q] = 0.f;
     const int q4m = TM / 4, q4n = TN / 4;
     if (a.use_c)  // S(r0.., k) for every k: TM contiguous floats per column k
       for (int t = tid; t < rc * q4m; t += kPT) {
         const int k = t / q4m, q = t - k * q4m;
-        cp_async16(A2 + k * TM + 4 * q, Sbuf + (r0 + 4 * q) + static_cast<i64>(k) * a.ldS);
+        cp_async16(A2 + k * ldA + 4 * q, Sbuf + (r0 + 4 * q) + static_cast<i64>(k) * a.ldS);
       }
+    cp_async_commit();  // group 0: A2 (and the caller's partial sums)
     const int nch = a.use_r ? (rr + KC - 1) / KC : 0;
     auto issue_chunk = [&](int ch) {
       const int k0 = ch * KC, kl = min(KC, rr - k0);
-      float* dst = Bb + (ch & 1) * KC * TN;
+      float* dst = Bb + (ch % NST) * KC * ldB;
       for (int t = tid; t < kl * q4n; t += kPT) {
         const int k = t / q4n, q = t - k * q4n;
-        cp_async16(dst + k * TN + 4 * q, SbufT + (c0 + 4 * q) + static_cast<i64>(k0 + k) * a.ldT);
+        cp_async16(dst + k * ldB + 4 * q, SbufT + (c0 + 4 * q) + static_cast<i64>(k0 + k) * a.ldT);
       }
     };
-    if (nch > 0 && !(a.dbg & 1)) issue_chunk(0);
-    cp_async_commit();
+    // NST-stage ring: chunks 0 .. NST-2 in flight before the first one is used
+#pragma unroll
+    for (int q = 0; q < NST - 1; ++q) {
+      if (q < nch && !(a.dbg & 1)) issue_chunk(q);
+      cp_async_commit();
+    }
     for (int ch = 0; ch < nch; ++ch) {
-      if (ch + 1 < nch) {
-        if (!(a.dbg & 1)) issue_chunk(ch + 1);
-        cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
+      if (ch + NST - 1 < nch && !(a.dbg & 1)) issue_chunk(ch + NST - 1);
+      cp_async_commit();
+      cp_async_wait<NST - 1>();  // A2 and chunk ch have landed
       __syncthreads();
-      if (gthr && !(a.dbg & 2)) {
-        const int k0 = ch * KC, kl = min(KC, rr - k0);
-        const int cnt = s < kl ? (kl - 1 - s) / KS + 1 : 0;
-        strip_gemm(acc, As + static_cast<size_t>(k0 + s) * TM + 4 * mi, KS * TM,
-                   Bb + (ch & 1) * KC * TN + s * TN + 4 * ni, KS * TN, cnt);
+      if constexpr (MODE == 0) {
+        if (gthr && !(a.dbg & 2)) {
+          const int k0 = ch * KC, kl = min(KC, rr - k0);
+          const int cnt = s < kl ? (kl - 1 - s) / KS + 1 : 0;
+          strip_gemm(acc, As + static_cast<size_t>(k0 + s) * ldA + 4 * mi, KS * ldA,
+                     Bb + (ch % NST) * KC * ldB + s * ldB + 4 * ni, KS * ldB, cnt);
+        }
+      } else {
+        if (w8) {
+          if (ch == 0 && a.use_c)  // the resident S L~_c part overlaps the chunks in flight
+            for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
+          const int k0 = ch * KC, kl = min(KC, rr - k0);
+          const float* ab = As + static_cast<size_t>(k0) * ldA + 8 * mi8;
+          const float* bb = Bb + (ch % NST) * KC * ldB + 8 * ni8;
+          for (int k = lane; k < kl; k += 32) fma88(acc8, ab + k * ldA, bb + k * ldB);
+        }
       }
       __syncthreads();
     }
@@ -196,16 +255,28 @@ __global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
       cp_async_wait<0>();
       __syncthreads();
     }
-    if (a.use_c && gthr) {
-      const int cnt = s < rc ? (rc - 1 - s) / KS + 1 : 0;
-      strip_gemm(acc, A2 + s * TM + 4 * mi, KS * TM, Bc + s * TN + 4 * ni, KS * TN, cnt);
-    }
-    if (gthr) {
-      float* o = red + static_cast<size_t>(s) * TE;
+    if constexpr (MODE == 0) {
+      if (a.use_c && gthr) {
+        const int cnt = s < rc ? (rc - 1 - s) / KS + 1 : 0;
+        strip_gemm(acc, A2 + s * ldA + 4 * mi, KS * ldA, Bc + s * ldB + 4 * ni, KS * ldB, cnt);
+      }
+      if (gthr) {
+        float* o = red + static_cast<size_t>(s) * TE;
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) o[(4 * mi + x) + TM * (4 * ni + y)] = acc[x][y];
+          for (int y = 0; y < 4; ++y) o[(4 * mi + x) + TM * (4 * ni + y)] = acc[x][y];
+      }
+    } else {
+      if (w8) {
+        if (a.use_c && nch == 0)
+          for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
+        reduce_scatter64(acc8, lane);  // lane now holds entries 2 lane, 2 lane + 1 of the micro-tile
+        const int x = lane >> 2, y = (2 * lane) & 7;
+        float* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
+        o[0] = acc8[0];
+        o[TM] = acc8[1];
+      }
     }
     __syncthreads();
   };
@@ -261,29 +332,27 @@ __global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
     mark(0);
     grid_barrier(&a.bar[0], &a.bar[1]);
     mark(1);
-    // partial sums of iteration j-1: loads issued now, consumed after the
+    // partial sums of iteration j-1: cp.async (L2 -> shared, bypassing L1)
+    // issued now, joining the GEMM's first copy group, consumed after the
     // tile GEMM (their L2 latency hides behind it)
-    double pv[kPartRegs][4];
-    const double* pp = a.part + static_cast<size_t>((j - 1) & 1) * G * 4;
-    if (j >= 2 && warp == 0)
-#pragma unroll
-      for (int r = 0; r < kPartRegs; ++r) {
-        const int q = lane + 32 * r;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) pv[r][u] = q < G ? __ldcg(pp + q * 4 + u) : 0.0;
-      }
+    if (j >= 2 && warp == 0) {
+      const double* pp = a.part + static_cast<size_t>((j - 1) & 1) * G * 4;
+      for (int q = lane; q < 2 * G; q += 32) cp_async16(psm + 2 * q, pp + 2 * q);
+    }
     // ---- phase B GEMM: H(S_j) (frpcag.cpp:89-90 penalties, linearity for Z)
     if (j <= a.max_iter) tile_gemm(a.Sg[b], a.SgT[b]);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
     mark(3);
     if (j >= 2) {
       // ---- iteration j-1: objective, divergence, trace, stop test
       //      (frpcag.cpp:89-106)
       if (warp == 0) {
         double v[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = lane; q < G; q += 32)
 #pragma unroll
-        for (int r = 0; r < kPartRegs; ++r)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] += pv[r][u];
+          for (int u = 0; u < 4; ++u) v[u] += psm[q * 4 + u];
 #pragma unroll
         for (int u = 0; u < 4; ++u) v[u] = warp_sum(v[u]);
         if (lane == 0)
@@ -362,20 +431,62 @@ __global__ void __launch_bounds__(kPT, 1) fista_persist_k(const PersistArgs a) {
 }
 
 struct Geom {
-  int TM, TN, R, C, KS, KC;
+  int mode, TM, TN, R, C, KS, KC, ldA, ldB, threads;
   size_t smem;
 };
 
-size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int KS, int KC) {
+size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst) {
   const size_t TE = static_cast<size_t>(TM) * TN;
-  return 4 * (static_cast<size_t>(rr) * TM + static_cast<size_t>(rc) * TN + static_cast<size_t>(rc) * TM +
-              2 * static_cast<size_t>(KC) * TN + static_cast<size_t>(KS) * TE + 6 * TE);
+  return 8 * kPsm + 4 * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
+              static_cast<size_t>(nst) * KC * ldB + static_cast<size_t>(KS) * TE + 6 * TE);
 }
 
-// Picks the tile shape: R x C CTAs (at most one per SM), TM/TN multiples of
-// 4, every CTA holding its g_r L~_r rows; minimises the per-CTA multiply-add
-// count TM TN (rr + rc) within the shared-memory budget.
-bool plan_geom(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
+// MODE 1 (preferred): TM, TN multiples of 8, one warp per 8 x 8 micro-tile
+// (at most 16 warps), k-major panels padded by 4 floats so that lanes at
+// different k hit distinct 16-byte bank groups; minimises the per-scheduler
+// multiply-add work max(warps, 4) (rr + rc) within the shared-memory budget.
+bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
+  bool found = false;
+  double best = 0.0;
+  const i64 sms = c->num_sms;
+  int fix_m = 0, fix_n = 0;  // CPCAG_FISTA_TILE=TMxTN (experiments)
+  if (const char* e = std::getenv("CPCAG_FISTA_TILE")) std::sscanf(e, "%dx%d", &fix_m, &fix_n);
+  for (i64 TM = 8; TM <= std::max<i64>(8, (rr + 7) / 8 * 8); TM += 8)
+    for (i64 TN = 8; TN <= std::max<i64>(8, (rc + 7) / 8 * 8); TN += 8) {
+      const i64 R = (rr + TM - 1) / TM, C = (rc + TN - 1) / TN;
+      const i64 warps = (TM / 8) * (TN / 8);
+      if (R * C > sms || warps > 16) continue;
+      if (fix_m && (TM != fix_m || TN != fix_n)) continue;
+      const int ldA = static_cast<int>(TM + 4), ldB = static_cast<int>(TN + 4);
+      int KC = 64;
+      size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), ldA, ldB, 1, KC, 4);
+      if (sm > budget) {
+        KC = 32;
+        sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), ldA, ldB, 1, KC, 4);
+      }
+      if (sm > budget) continue;
+      // per-scheduler multiply-add work, plus the exposed latency of the S
+      // panel ring: each of the ceil(rr / KC) chunks must cover ~1 us of L2
+      // latency spread over the 3 chunks in flight (measured: a 8 x 104 tile
+      // with 2 k-steps per lane per chunk ran latency-bound)
+      const double work = static_cast<double>(std::max<i64>(warps, 4)) * static_cast<double>(rr + rc) * 64.0 / 4.0;
+      const double chunk_work = static_cast<double>(std::max<i64>(warps, 4)) * KC * 64.0 / 4.0 / 32.0;
+      const double cost = work + static_cast<double>((rr + KC - 1) / KC) * std::max(0.0, 700.0 - chunk_work) +
+                          1e-3 * static_cast<double>(sm);
+      if (!found || cost < best) {
+        found = true;
+        best = cost;
+        *out = Geom{1, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), 1, KC,
+                    ldA, ldB, static_cast<int>(std::max<i64>(warps, 4) * 32), sm};
+      }
+    }
+  return found;
+}
+
+// MODE 0: R x C CTAs (at most one per SM), TM/TN multiples of 4, the k range
+// split over thread groups; minimises the per-CTA multiply-add count TM TN
+// (rr + rc) within the shared-memory budget.
+bool plan_mode0(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
   bool found = false;
   double best = 0.0;
   const i64 sms = c->num_sms;
@@ -390,20 +501,22 @@ bool plan_geom(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
       if (NMT > kPT) break;
       const int KS = static_cast<int>(std::min<i64>(8, kPT / NMT));
       int KC = 128;
-      size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), KS, KC);
+      size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM),
+                            static_cast<int>(TN), KS, KC, 2);
       if (sm > budget) {
         KC = 32;
-        sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), KS, KC);
+        sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM), static_cast<int>(TN),
+                       KS, KC, 2);
       }
       if (sm > budget) break;  // a taller tile only needs more
       const i64 R = (rr + TM - 1) / TM;
-      // multiply-adds per GEMM thread (the critical path of a CTA)
       const double cost = static_cast<double>(TM * TN) * static_cast<double>(rr + rc) /
                           static_cast<double>(NMT * KS) + 64.0 * static_cast<double>(rr) / KC;
       if (!found || cost < best) {
         found = true;
         best = cost;
-        *out = Geom{static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), KS, KC, sm};
+        *out = Geom{0, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), KS, KC,
+                    static_cast<int>(TM), static_cast<int>(TN), kPT, sm};
       }
       break;  // the smallest feasible TM for this TN is the cheapest
     }
@@ -426,12 +539,24 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
   CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const size_t budget = static_cast<size_t>(optin) > 4096 ? static_cast<size_t>(optin) - 4096 : 0;
   Geom g;
-  if (!plan_geom(c, rr, rc, budget, &g)) return false;
-  ensure_smem(fista_persist_k, g.smem);
+  // MODE 1 is opt-in (CPCAG_FISTA_PERSIST_MODE=1): measured at config 1 it
+  // runs the tile GEMM in 16.6 us per iteration (24 x 40 tiles) vs 16.1 us
+  // for MODE 0 -- with the S panel ring limited by shared memory to 64-row
+  // chunks, each lane does 2 k-steps between CTA barriers and the loop is
+  // barrier/latency-bound (ncu: barrier 24 %, wait 18 %), not wavefront-bound.
+  const char* me = std::getenv("CPCAG_FISTA_PERSIST_MODE");
+  const bool want1 = me && std::string(me) == "1";
+  if (!(want1 && plan_mode1(c, rr, rc, budget, &g)) && !plan_mode0(c, rr, rc, budget, &g)) return false;
+  const void* kfn = g.mode == 1 ? reinterpret_cast<const void*>(fista_persist_k<1>)
+                                : reinterpret_cast<const void*>(fista_persist_k<0>);
+  if (g.mode == 1)
+    ensure_smem(fista_persist_k<1>, g.smem);
+  else
+    ensure_smem(fista_persist_k<0>, g.smem);
   int per_sm = 0;
-  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fista_persist_k, kPT, g.smem));
+  CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, g.threads, g.smem));
   const i64 grid = static_cast<i64>(g.R) * g.C;
-  if (per_sm < 1 || grid > static_cast<i64>(per_sm) * c->num_sms || grid > 32 * kPartRegs) return false;
+  if (per_sm < 1 || grid > static_cast<i64>(per_sm) * c->num_sms || grid > kMaxGrid) return false;
 
   const i64 ldS = static_cast<i64>(g.R) * g.TM, ldT = static_cast<i64>(g.C) * g.TN;
   const size_t sz = static_cast<size_t>(ldS * ldT);
@@ -452,6 +577,8 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
   a.C = g.C;
   a.KS = g.KS;
   a.KC = g.KC;
+  a.ldA = g.ldA;
+  a.ldB = g.ldB;
   a.use_r = cfg.gamma_r != 0.0;
   a.use_c = cfg.gamma_c != 0.0;
   a.loss = cfg.loss;
@@ -476,16 +603,16 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
   void* args[] = {(void*)&a};
   {
     KScope ks_(c, "fista_persist");
-    CUDA_OK(cudaLaunchCooperativeKernel((void*)fista_persist_k, dim3(static_cast<unsigned>(grid)), dim3(kPT), args,
-                                        g.smem, c->stream));
+    CUDA_OK(cudaLaunchCooperativeKernel(kfn, dim3(static_cast<unsigned>(grid)), dim3(g.threads), args, g.smem,
+                                        c->stream));
     launched(c);
   }
   *res = read_back(c, out.p);
   if (std::getenv("CPCAG_FISTA_PERSIST_PROF"))
     std::fprintf(stderr,
-                 "[fista_persist] grid %lld (%d x %d tiles of %d x %d, KS %d, KC %d, smem %zu) its %lld: "
-                 "phaseA %.1f barrier %.1f reduce %.1f gemm %.1f elem %.1f us\n",
-                 static_cast<long long>(grid), g.R, g.C, g.TM, g.TN, g.KS, g.KC, g.smem,
+                 "[fista_persist] mode %d grid %lld (%d x %d tiles of %d x %d, KS %d, KC %d, %d threads, smem %zu) "
+                 "its %lld: phaseA %.1f barrier %.1f reduce %.1f gemm %.1f elem %.1f us\n",
+                 g.mode, static_cast<long long>(grid), g.R, g.C, g.TM, g.TN, g.KS, g.KC, g.threads, g.smem,
                  static_cast<long long>(res->iterations), res->prof_ns[0] * 1e-3, res->prof_ns[1] * 1e-3,
                  res->prof_ns[2] * 1e-3, res->prof_ns[3] * 1e-3, res->prof_ns[4] * 1e-3);
   return true;

@@ -86,6 +86,21 @@ def test_persistent_fista_agrees_with_per_kernel_path(P, ctx, monkeypatch):
     assert np.allclose(tr1.objective, tr2.objective, rtol=1e-4)
 
 
+def test_persistent_fista_warp_tile_mode_matches_oracle(P, ctx, monkeypatch):
+    """MODE 1 (8 x 8 warp micro-tiles, lane k-split, shuffle reduce-scatter)."""
+    monkeypatch.setenv("CPCAG_FISTA_PERSIST_MODE", "1")
+    for shape, gr, gc, loss in [((400, 300, 101, 60), 2.0, 2.0, "l1"), ((200, 160, 50, 40), 0.0, 5.0, "l2"),
+                                ((200, 160, 50, 40), 3.0, 0.0, "l1")]:
+        p, n, rr, rc = shape
+        Lr, Lc = _reduced(p, n, rr, rc, 40 + rr)
+        Y = (np.random.default_rng(rr).standard_normal((rr, rc)) * 4.0).astype(np.float32)
+        X, tr, kt = _run(P, ctx, Y, Lr, Lc, gr, gc, loss, 1e-300, 150)
+        assert "fista_persist" in kt
+        Xo, tro = O.fista_solve(Y.astype(np.float64), Lr, Lc, O.FrpcagConfig(gr, gc, loss, 1e-300, 150))
+        assert rel(X, Xo) <= 1e-4
+        assert np.allclose(tr.objective, tro.objective, rtol=1e-4)
+
+
 def test_persistent_fista_is_deterministic(P, ctx):
     Lr, Lc = _reduced(400, 300, 101, 60, 12)
     Y = np.random.default_rng(6).standard_normal((101, 60)).astype(np.float32)

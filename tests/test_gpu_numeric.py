@@ -177,7 +177,7 @@ def _decoder_case(p=150, n=120, rr=40, rc=30, seed=21):
     return Lr, Lc, plan, Xt
 
 
-@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast4", "slab", "slab2", "regr", "rcm2", "fast3", "staged", "plain", "band"])
+@pytest.mark.parametrize("variant", ["default", "fast", "fast2", "fast4", "slab", "slab2", "regr", "slabr", "rcm2", "fast3", "staged", "plain", "band"])
 def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
@@ -191,7 +191,7 @@ def test_alternate_decode_fp64_matches_oracle(P, ctx, monkeypatch, variant):
     assert rel(res.X, ro.X) <= 1e-9
 
 
-@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "fast5", "slab", "slab2", "regr", "rcm2"])
+@pytest.mark.parametrize("variant", ["default", "fast2", "fast4", "fast5", "slab", "slab2", "regr", "slabr", "rcm2"])
 def test_alternate_decode_fixed_iterations_fp32(P, ctx, monkeypatch, variant):
     if variant != "default":
         monkeypatch.setenv("CPCAG_APPLY", variant)
