@@ -34,6 +34,12 @@ struct CgState {
   unsigned cnt[4];
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 struct Plan {
   const int* rsel;   // p: index into omega_r or -1
   const int* csel;   // n: index into omega_c or -1
@@ -1066,6 +1072,183 @@ __global__ void cg_update_k(i64 N, T* __restrict__ X, T* __restrict__ P, const T
 }
 
 // ||b - A(x)||^2 for the exit test (solvers.hpp:69-72).
+// The whole CG loop of a SMALL decoder problem (p n <= 2^20, e.g. config 0)
+// as one cooperative kernel (opt-in, CPCAG_CG_PERSIST=1; see the host code
+// for the measurement): each CTA owns a contiguous range of entries;
+// per iteration apply + <P, AP> | grid barrier | R -= alpha AP, ||R||^2 |
+// grid barrier | X += alpha P, P = R + beta P | grid barrier.  At these sizes
+// the per-kernel loop is launch/latency-bound (config 0: 46 us per
+// iteration for three tiny kernels).  Per-entry arithmetic is the per-kernel
+// path's (pulls in CSR order, madd_entry; the same residual/update
+// formulas); the reductions are fixed-order, summed identically by every CTA,
+// so every CTA takes the same alpha/beta/stop decisions.  P changes between
+// barriers inside the launch: it is read with plain (weak) loads ordered
+// after the barrier's gpu-scope acquire (never through the non-coherent
+// read-only path: P is not declared const __restrict__).
+template <typename T>
+__global__ void __launch_bounds__(512) cg_persist_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
+                                                    T* __restrict__ X, T* __restrict__ R, T* P, T* __restrict__ AP,
+                                                    double* partials, i64 max_iter, CgState* st, unsigned* bar,
+                                                    int prof) {
+  __shared__ double tot_sh;
+  const int G = gridDim.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const i64 N = p * n;
+  const i64 e0 = (N * blockIdx.x) / G, e1 = (N * (blockIdx.x + 1)) / G;
+  if (st->done) return;
+  // stage the operators once: L_r (all rows) and the L_c rows of this CTA's
+  // columns, as (value, index) records; per iteration only the P gathers go
+  // to L2 (the barrier's acquire leaves L1 cold each iteration)
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int nr = static_cast<int>(Lr.rp[p]);
+  OffEnt<T>* Er = reinterpret_cast<OffEnt<T>*>(smraw);
+  const i64 ca = e0 / p, cb = e1 > e0 ? (e1 - 1) / p : ca;  // columns touched
+  const i64 kc0 = Lc.rp[ca];
+  const int nc = static_cast<int>(Lc.rp[cb + 1] - kc0);
+  OffEnt<T>* Ec = Er + nr;
+  int* rpr_s = reinterpret_cast<int*>(Ec + nc);
+  int* rpc_s = rpr_s + (p + 1);
+  for (int k = threadIdx.x; k < nr; k += blockDim.x) {
+    OffEnt<T> en;
+    en.v = Lr.v[k];
+    en.off = Lr.ci[k];
+    Er[k] = en;
+  }
+  for (int k = threadIdx.x; k < nc; k += blockDim.x) {
+    OffEnt<T> en;
+    en.v = Lc.v[kc0 + k];
+    en.off = Lc.ci[kc0 + k];
+    Ec[k] = en;
+  }
+  for (i64 q = threadIdx.x; q <= p; q += blockDim.x) rpr_s[q] = static_cast<int>(Lr.rp[q]);
+  for (i64 q = threadIdx.x; q <= cb - ca + 1; q += blockDim.x) rpc_s[q] = static_cast<int>(Lc.rp[ca + q] - kc0);
+  __syncthreads();
+  double rho = st->rho;
+  const double target = st->target;
+  i64 it = st->it;
+  double alpha = 0.0, beta = 0.0, curv = 0.0;
+  bool err = false;
+  unsigned long long pt[6] = {0, 0, 0, 0, 0, 0}, tq = gtimer();  // CTA 0 phase timers (CPCAG_CG_PERSIST_PROF)
+  auto mark = [&](int ph) {
+    if (threadIdx.x == 0) {
+      const unsigned long long now = gtimer();
+      pt[ph] += now - tq;
+      tq = now;
+    }
+  };
+  // fixed-order sum of the G block partials (the same in every CTA)
+  auto grid_total = [&](const double* part) {
+    if (warp == 0) {
+      double v = 0.0;
+      for (int q = lane; q < G; q += 32) v += __ldcg(part + q);
+      v = warp_sum(v);
+      if (lane == 0) tot_sh = v;
+    }
+    __syncthreads();
+    const double t = tot_sh;
+    __syncthreads();
+    return t;
+  };
+  while (true) {
+    double d[1] = {0.0};
+    for (i64 e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const i64 c = e / p, i = e - c * p;
+      // entries from shared memory, gathers issued 8 at a time, accumulated
+      // in CSR order
+      T a1 = T(0), a2 = T(0);
+      {
+        const int k0 = rpc_s[c - ca], k1 = rpc_s[c - ca + 1];
+        for (int kb = k0; kb < k1; kb += 8) {
+          T vv[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (kb + u < k1) {
+              const OffEnt<T> en = Ec[kb + u];
+              vv[u] = en.v;
+              xv[u] = P[i + static_cast<i64>(en.off) * p];
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (kb + u < k1) a1 = madd_entry(a1, vv[u], xv[u]);
+        }
+      }
+      {
+        const int k0 = rpr_s[i], k1 = rpr_s[i + 1];
+        for (int kb = k0; kb < k1; kb += 8) {
+          T vv[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (kb + u < k1) {
+              const OffEnt<T> en = Er[kb + u];
+              vv[u] = en.v;
+              xv[u] = P[en.off + c * p];
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (kb + u < k1) a2 = madd_entry(a2, vv[u], xv[u]);
+        }
+      }
+      T out = add_rn(mul_rn(gc, a1), mul_rn(gr, a2));
+      const T pv = P[e];
+      if (pl.rsel[i] >= 0 && pl.csel[c] >= 0) out = add_rn(out, pv);
+      AP[e] = out;
+      d[0] += static_cast<double>(pv) * static_cast<double>(out);
+    }
+    block_sum<1>(d);
+    if (threadIdx.x == 0) partials[blockIdx.x] = d[0];
+    mark(0);
+    grid_barrier(&bar[0], &bar[1]);
+    mark(1);
+    curv = grid_total(partials);
+    if (!isfinite(curv) || curv <= 0.0) {
+      err = true;
+      break;
+    }
+    alpha = rho / curv;
+    const T aT = static_cast<T>(alpha);
+    double r2[1] = {0.0};
+    for (i64 e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const T r = sub_rn(R[e], mul_rn(aT, AP[e]));
+      R[e] = r;
+      r2[0] += static_cast<double>(r) * static_cast<double>(r);
+    }
+    block_sum<1>(r2);
+    if (threadIdx.x == 0) partials[G + blockIdx.x] = r2[0];
+    mark(2);
+    grid_barrier(&bar[0], &bar[1]);
+    mark(3);
+    const double rho_next = grid_total(partials + G);
+    beta = rho_next / rho;
+    const T bT = static_cast<T>(beta);
+    for (i64 e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      const T pv = P[e];
+      X[e] = add_rn(X[e], mul_rn(aT, pv));
+      P[e] = add_rn(R[e], mul_rn(bT, pv));
+    }
+    rho = rho_next;
+    it += 1;
+    mark(4);
+    if (sqrt(rho) <= target || it >= max_iter) break;
+    grid_barrier(&bar[0], &bar[1]);
+    mark(5);
+  }
+  if (prof && blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[cg_persist] G %d its %lld: apply %.1f bar %.1f resid %.1f bar %.1f update %.1f bar %.1f us\n", G,
+           static_cast<long long>(it), pt[0] * 1e-3, pt[1] * 1e-3, pt[2] * 1e-3, pt[3] * 1e-3, pt[4] * 1e-3,
+           pt[5] * 1e-3);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->curv = curv;
+    st->alpha = alpha;
+    st->beta = beta;
+    st->rho = rho;
+    st->it = it;
+    st->done = 1;
+    if (err) {
+      st->err = 1;
+      st->err_it = it;
+    }
+  }
+}
+
 template <typename T>
 __global__ void cg_true_residual_k(i64 p, i64 n, Pull<T> Lr, Pull<T> Lc, T gr, T gc, Plan pl,
                                    const T* __restrict__ Xt, const T* __restrict__ X,
@@ -1217,11 +1400,6 @@ struct ColMeta {
   unsigned long long* prof;  // diagnostics (CPCAG_BAND_PROF): per-CTA phase times, else null
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 template <typename T, int RB, int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) cg_apply_col_k(int p, i64 c_lo, i64 c_hi, ColMeta cm,
@@ -2195,6 +2373,57 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   cg_init_k<T><<<g2, kBlock, 0, c->stream>>>(p, n, pl, Xt, X, R.p, P.p, cfg.pcg_tol, part.p, st.p);
   launched(c);
   CgState host = read_back(c, st.p);
+  // small problems: the whole loop as one cooperative kernel (cg_persist_k)
+  // (default path only: an explicit CPCAG_APPLY variant keeps its own loop,
+  // and the permuted layouts of rcm2 / fast3 / band never take it)
+  // Opt-in (CPCAG_CG_PERSIST=1): measured at config 0 (fp64, 200 x 300) the
+  // apply phase costs 14-30 us per iteration across CTAs (one entry per
+  // thread, L1-cold gathers after each barrier), so the loop runs at 48 vs
+  // 46 us per iteration for the per-kernel path.
+  const char* pe = std::getenv("CPCAG_CG_PERSIST");
+  const bool persist = pe && std::string(pe) == "1" && N <= (i64{1} << 20) && N > 0 && variant != "band" &&
+                       variant != "fast3" && variant != "rcm2";
+  if (persist && !host.done) {
+    // shared memory: L_r entries, this CTA's L_c rows, both row-pointer arrays
+    i64 Gp = std::min<i64>((N + 511) / 512, static_cast<i64>(c->num_sms));
+    if (const char* e = std::getenv("CPCAG_CG_PERSIST_G")) Gp = std::max<i64>(1, std::min<i64>(Gp, std::atoll(e)));
+    i64 max_ec = 0, max_cols = 0;
+    for (i64 b = 0; b < Gp; ++b) {
+      const i64 e0 = (N * b) / Gp, e1 = (N * (b + 1)) / Gp;
+      const i64 ca = e0 / p, cb = e1 > e0 ? (e1 - 1) / p : ca;
+      max_ec = std::max(max_ec, rpc[cb + 1] - rpc[ca]);
+      max_cols = std::max(max_cols, cb - ca + 1);
+    }
+    const size_t psmem = static_cast<size_t>(rpr[p] + max_ec) * sizeof(OffEnt<T>) +
+                         sizeof(int) * static_cast<size_t>(p + 1 + max_cols + 1);
+    int per_sm = 0;
+    if (psmem <= 200 * 1024) {
+      ensure_smem(cg_persist_k<T>, psmem);
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_persist_k<T>, 512, psmem));
+    }
+    if (per_sm >= 1) {
+      DevBuf<double> pp(c, 2 * static_cast<size_t>(Gp));
+      DevBuf<unsigned> bar(c, 2);
+      bar.zero(c);
+      T* Xp = X;
+      T *Rp = R.p, *Pp = P.p, *APp = AP.p;
+      double* ppp = pp.p;
+      i64 mi = cfg.pcg_max_iter;
+      CgState* sp = st.p;
+      unsigned* bp = bar.p;
+      int prof = std::getenv("CPCAG_CG_PERSIST_PROF") ? 1 : 0;
+      void* args[] = {(void*)&p, (void*)&n, (void*)&pr, (void*)&pc, (void*)&gr, (void*)&gc, (void*)&pl,
+                      (void*)&Xp, (void*)&Rp, (void*)&Pp, (void*)&APp, (void*)&ppp, (void*)&mi, (void*)&sp,
+                      (void*)&bp, (void*)&prof};
+      {
+        KScope ks_(c, "cg_persist");
+        CUDA_OK(cudaLaunchCooperativeKernel((void*)cg_persist_k<T>, dim3(static_cast<unsigned>(Gp)), dim3(512), args,
+                                            psmem, c->stream));
+        launched(c);
+      }
+      host = read_back(c, st.p);
+    }
+  }
   const i64 chunk = 32;
   while (!host.done) {
     for (i64 k = 0; k < chunk; ++k) {

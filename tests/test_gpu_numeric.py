@@ -222,6 +222,22 @@ def test_slab2_regr_applies_bit_identical_to_fast2(P, ctx, monkeypatch, dt):
     assert np.array_equal(out["fast2"].X, out["regr"].X)
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_persistent_cg_loop_matches_oracle(P, ctx, monkeypatch, dt):
+    """CPCAG_CG_PERSIST=1: the whole CG loop as one cooperative kernel."""
+    monkeypatch.setenv("CPCAG_CG_PERSIST", "1")
+    Lr, Lc, plan_o, Xt = _decoder_case()
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    res = P.alternate_decode(Xt.astype(dt), plan, to_device(ctx, Lr), to_device(ctx, Lc), P.SpectralGap(lambda_k1=0.3),
+                             P.SpectralGap(lambda_k1=0.4), P.DecoderConfig(1.0, 1e-10, 400), ctx=ctx)
+    ro = O.alternate_decode(Xt.astype(dt).astype(np.float64), plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 400)
+    if dt == np.float64:
+        assert res.converged == ro.converged and abs(res.iterations - ro.iterations) <= 1
+        assert rel(res.X, ro.X) <= 1e-9
+    else:
+        assert rel(res.X, ro.X) <= 1e-4
+
+
 def test_alternate_decode_zero_rhs_and_validation(P, ctx):
     Lr, Lc, plan_o, Xt = _decoder_case(20, 15, 5, 4, 3)
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
