@@ -487,7 +487,6 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
     }
   if (v_in_smem)
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
-  __shared__ double warp_part[32];
   __syncthreads();
   const double* vsrc = v_in_smem ? vs : v0;
   double est = 0.0;

@@ -704,9 +704,9 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   }
   dim3 gd(static_cast<unsigned>((rows + kDT - 1) / kDT), static_cast<unsigned>((cols + kDT - 1) / kDT));
   if (dense) part.alloc(c, 3 * static_cast<size_t>(std::max<unsigned>(gd.x * gd.y, nb1)));
-  // fp32 dense: the whole solve as one cooperative kernel (fista_persist.cu)
-  // when the tiling fits; otherwise the per-kernel paths below.
-  if constexpr (sizeof(T) == 4) {
+  // dense: the whole solve as one cooperative kernel (fista_persist.cu) when
+  // the tiling fits; otherwise the per-kernel paths below.
+  {
     FistaPersistOut pres{};
     if (dense && fista_persist_enabled() &&
         fista_persist_run(c, Y, rows, cols, Dr.p, Dc.p, cfg, step, X, tr.p, &pres)) {

@@ -45,24 +45,25 @@ constexpr int kPT = 256;      // threads per CTA
 constexpr int kMaxGrid = 160;      // CTAs (one per SM)
 constexpr int kPsm = 4 * kMaxGrid;  // doubles of the partial-sum staging area
 
+template <typename T>
 struct PersistArgs {
   int rr, rc, ldS, ldT;
   int TM, TN, C, KS, KC;
   int ldA, ldB;  // shared-memory row strides of the k-major A (TM) and B (TN) panels
   int use_r, use_c, loss;
   int dbg;  // diagnostics (CPCAG_FISTA_PERSIST_DBG): 1 = no B chunk loads, 2 = no chunk FMAs
-  float step;
+  T step;
   double tol;
   i64 max_iter;
   double gamma_r, gamma_c;
-  const float* Dr;  // rr x rr dense, exactly symmetric
-  const float* Dc;  // rc x rc dense, exactly symmetric
-  const float* Y;   // rr x rc column-major
-  float* Sg[2];     // S_j column-major, ldS rows (padding rows stay 0)
-  float* SgT[2];    // S_j row-major, ldT columns (padding stays 0)
+  const T* Dr;  // rr x rr dense, exactly symmetric
+  const T* Dc;  // rc x rc dense, exactly symmetric
+  const T* Y;   // rr x rc column-major
+  T* Sg[2];     // S_j column-major, ldS rows (padding rows stay 0)
+  T* SgT[2];    // S_j row-major, ldT columns (padding stays 0)
   double* part;     // [2][grid][4] per-CTA partial sums by iteration parity
   double* trace;    // objective per iteration
-  float* X;         // output, rr x rc column-major
+  T* X;         // output, rr x rc column-major
   FistaPersistOut* out;
   unsigned* bar;    // grid barrier count, generation
 };
@@ -83,23 +84,42 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   return t;
 }
 
-__device__ __forceinline__ void fma44(float (&acc)[4][4], const float4 a, const float4 b) {
-  const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(av[x], bv[y], acc[x][y]);
-}
-
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
-// acc += sum over cnt k-steps of a(k) b(k)^T, a/b float4 strips at strides
+// four consecutive values (16-byte aligned) of either precision
+__device__ __forceinline__ void ld4v(const float* p, float (&v)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(p);
+  v[0] = x.x;
+  v[1] = x.y;
+  v[2] = x.z;
+  v[3] = x.w;
+}
+__device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
+  const double2 x = *reinterpret_cast<const double2*>(p);
+  const double2 y = *reinterpret_cast<const double2*>(p + 2);
+  v[0] = x.x;
+  v[1] = x.y;
+  v[2] = y.x;
+  v[3] = y.y;
+}
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
+
+// acc += sum over cnt k-steps of a(k) b(k)^T, a/b 4-value strips at strides
 // sa/sb, k ascending.  (Prefetching the operands four k-steps ahead measured
 // slower: the loop is bound by shared-memory wavefronts, ncu: 4.4 per LDS.128.)
-__device__ __forceinline__ void strip_gemm(float (&acc)[4][4], const float* ap, int sa, const float* bp, int sb,
-                                           int cnt) {
+template <typename T>
+__device__ __forceinline__ void strip_gemm(T (&acc)[4][4], const T* ap, int sa, const T* bp, int sb, int cnt) {
 #pragma unroll 4
-  for (int q = 0; q < cnt; ++q) fma44(acc, lds4(ap + q * sa), lds4(bp + q * sb));
+  for (int q = 0; q < cnt; ++q) {
+    T av[4], bv[4];
+    ld4v(ap + q * sa, av);
+    ld4v(bp + q * sb, bv);
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma_t(av[x], bv[y], acc[x][y]);
+  }
 }
 
 // acc[x 8 + y] += a[x] b[y] for one k (8-float strips of A and B).
@@ -136,13 +156,15 @@ __device__ __forceinline__ void reduce_scatter64(float (&acc)[64], int lane) {
 // MODE 1: 8 x 8 micro-tiles, one warp per micro-tile with the k range split
 //         across its lanes, lanes reduced by a fixed shuffle reduce-scatter
 //         (twice the multiply-adds per shared-memory wavefront of MODE 0).
-template <int MODE>
-__global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(const PersistArgs a) {
+template <typename T, int MODE>
+__global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(const PersistArgs<T> a) {
+  static_assert(MODE == 0 || sizeof(T) == 4, "MODE 1 is fp32 only");
+  constexpr int EPC = 16 / static_cast<int>(sizeof(T));  // values per 16-byte cp.async
   const int kPT = blockDim.x;
   constexpr int NST = MODE == 0 ? 2 : 4;  // stages of the S-panel ring
   extern __shared__ __align__(16) double smd[];
   double* psm = smd;  // [kPsm] partial sums of the previous iteration (4 per CTA)
-  float* sm = reinterpret_cast<float*>(smd + kPsm);
+  T* sm = reinterpret_cast<T*>(smd + kPsm);
   __shared__ double tot_sh[4];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int TM = a.TM, TN = a.TN, TE = TM * TN, rr = a.rr, rc = a.rc, KC = a.KC, KS = a.KS;
@@ -150,36 +172,36 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   const int r0 = rb * TM, c0 = cb * TN;
   const int rn = min(TM, rr - r0), cn = min(TN, rc - c0);
   const int ldA = a.ldA, ldB = a.ldB;
-  float* As = sm;                                      // [rr][ldA]  g_r L~_r(r0 + i, k)
-  float* Bc = As + static_cast<size_t>(rr) * ldA;      // [rc][ldB]  g_c L~_c(k, c0 + j)
-  float* A2 = Bc + static_cast<size_t>(rc) * ldB;      // [rc][ldA]  S(r0 + i, k)
-  float* Bb = A2 + static_cast<size_t>(rc) * ldA;      // [2][KC][ldB]  S(k, c0 + j)
-  float* red = Bb + NST * static_cast<size_t>(KC) * ldB;  // [KS][TE]  split-k partials (MODE 1: KS = 1)
-  float* Yt = red + static_cast<size_t>(KS) * TE;     // tile state, e = i + TM j
-  float* Zt = Yt + TE;                                // Z_j
-  float* HZ = Zt + TE;                                // H(Z_j)
-  float* Sp = HZ + TE;                                // S_{j-1}
-  float* Hp = Sp + TE;                                // H(S_{j-1})
-  float* Sc = Hp + TE;                                // S_j
+  T* As = sm;                                      // [rr][ldA]  g_r L~_r(r0 + i, k)
+  T* Bc = As + static_cast<size_t>(rr) * ldA;      // [rc][ldB]  g_c L~_c(k, c0 + j)
+  T* A2 = Bc + static_cast<size_t>(rc) * ldB;      // [rc][ldA]  S(r0 + i, k)
+  T* Bb = A2 + static_cast<size_t>(rc) * ldA;      // [2][KC][ldB]  S(k, c0 + j)
+  T* red = Bb + NST * static_cast<size_t>(KC) * ldB;  // [KS][TE]  split-k partials (MODE 1: KS = 1)
+  T* Yt = red + static_cast<size_t>(KS) * TE;     // tile state, e = i + TM j
+  T* Zt = Yt + TE;                                // Z_j
+  T* HZ = Zt + TE;                                // H(Z_j)
+  T* Sp = HZ + TE;                                // S_{j-1}
+  T* Hp = Sp + TE;                                // H(S_{j-1})
+  T* Sc = Hp + TE;                                // S_j
 
   // ---- one-time staging of the pre-scaled operators and the tile of Y
   if (a.use_r)
     for (int t = tid; t < rr * TM; t += kPT) {
       const int k = t / TM, i = t - k * TM;
       // L~_r(r0 + i, k) from the column-major dense copy (contiguous in i)
-      As[k * ldA + i] = i < rn ? static_cast<float>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
-                     : 0.f;
+      As[k * ldA + i] = i < rn ? static_cast<T>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
+                     : T(0);
     }
   if (a.use_c)
     for (int t = tid; t < rc * TN; t += kPT) {
       const int k = t / TN, j = t - k * TN;
-      Bc[k * ldB + j] = j < cn ? static_cast<float>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
-                     : 0.f;
+      Bc[k * ldB + j] = j < cn ? static_cast<T>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
+                     : T(0);
     }
   for (int e = tid; e < TE; e += kPT) {
     const int j = e / TM, i = e - j * TM;
     const bool ok = i < rn && j < cn;
-    const float y = ok ? a.Y[(r0 + i) + static_cast<i64>(c0 + j) * rr] : 0.f;
+    const T y = ok ? a.Y[(r0 + i) + static_cast<i64>(c0 + j) * rr] : T(0);
     Yt[e] = y;
     Zt[e] = y;  // Z_1 = Y
     Sp[e] = y;  // S_0 = Y
@@ -196,29 +218,29 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   const int mt = tid % NMT, s = tid / NMT, mi = mt % nmi, ni = mt / nmi;
   const int mi8 = warp % max(TM / 8, 1), ni8 = warp / max(TM / 8, 1);
   const bool w8 = MODE == 1 && warp < (TM / 8) * (TN / 8);
-  auto tile_gemm = [&](const float* Sbuf, const float* SbufT) {
-    float acc[4][4];
+  auto tile_gemm = [&](const T* Sbuf, const T* SbufT) {
+    T acc[4][4];
     float acc8[MODE == 1 ? 64 : 1];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+      for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
 #pragma unroll
     for (int q = 0; q < (MODE == 1 ? 64 : 1); ++q) acc8[q] = 0.f;
-    const int q4m = TM / 4, q4n = TN / 4;
+    const int q4m = TM / EPC, q4n = TN / EPC;
     if (a.use_c)  // S(r0.., k) for every k: TM contiguous floats per column k
       for (int t = tid; t < rc * q4m; t += kPT) {
         const int k = t / q4m, q = t - k * q4m;
-        cp_async16(A2 + k * ldA + 4 * q, Sbuf + (r0 + 4 * q) + static_cast<i64>(k) * a.ldS);
+        cp_async16(A2 + k * ldA + EPC * q, Sbuf + (r0 + EPC * q) + static_cast<i64>(k) * a.ldS);
       }
     cp_async_commit();  // group 0: A2 (and the caller's partial sums)
     const int nch = a.use_r ? (rr + KC - 1) / KC : 0;
     auto issue_chunk = [&](int ch) {
       const int k0 = ch * KC, kl = min(KC, rr - k0);
-      float* dst = Bb + (ch % NST) * KC * ldB;
+      T* dst = Bb + (ch % NST) * KC * ldB;
       for (int t = tid; t < kl * q4n; t += kPT) {
         const int k = t / q4n, q = t - k * q4n;
-        cp_async16(dst + k * ldB + 4 * q, SbufT + (c0 + 4 * q) + static_cast<i64>(k0 + k) * a.ldT);
+        cp_async16(dst + k * ldB + EPC * q, SbufT + (c0 + EPC * q) + static_cast<i64>(k0 + k) * a.ldT);
       }
     };
     // NST-stage ring: chunks 0 .. NST-2 in flight before the first one is used
@@ -261,7 +283,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
         strip_gemm(acc, A2 + s * ldA + 4 * mi, KS * ldA, Bc + s * ldB + 4 * ni, KS * ldB, cnt);
       }
       if (gthr) {
-        float* o = red + static_cast<size_t>(s) * TE;
+        T* o = red + static_cast<size_t>(s) * TE;
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -273,7 +295,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
           for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
         reduce_scatter64(acc8, lane);  // lane now holds entries 2 lane, 2 lane + 1 of the micro-tile
         const int x = lane >> 2, y = (2 * lane) & 7;
-        float* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
+        T* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
         o[0] = acc8[0];
         o[TM] = acc8[1];
       }
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
     __syncthreads();
   };
   auto tile_h = [&](int e) {
-    float h = 0.f;
+    T h = T(0);
     for (int q = 0; q < KS; ++q) h += red[q * TE + e];
     return h;
   };
@@ -296,7 +318,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   }
   __syncthreads();
 
-  const float step = a.step;
+  const T step = a.step;
   // phase timers (CTA 0, thread 0; read by tools/fista_diag.py)
   unsigned long long pt[5] = {0, 0, 0, 0, 0}, tq = gtimer_ns();
   auto mark = [&](int ph) {
@@ -314,15 +336,15 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
     const int b = static_cast<int>(j & 1);
     if (j <= a.max_iter) {
       // ---- phase A: gradient step + prox (frpcag.cpp:82-88)
-      float* Sgb = a.Sg[b];
-      float* SgTb = a.SgT[b];
+      T* Sgb = a.Sg[b];
+      T* SgTb = a.SgT[b];
       for (int e = tid; e < TE; e += kPT) {
         const int jj = e / TM, i = e - jj * TM;
         if (i < rn && jj < cn) {
-          const float g = 2.f * HZ[e];
-          const float arg = __fsub_rn(Zt[e], __fmul_rn(step, g));
-          const float y = Yt[e];
-          const float sv = a.loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, y, step) : prox_l1_elem(arg, y, step);
+          const T g = T(2) * HZ[e];
+          const T arg = sub_rn(Zt[e], mul_rn(step, g));
+          const T y = Yt[e];
+          const T sv = a.loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, y, step) : prox_l1_elem(arg, y, step);
           Sc[e] = sv;
           Sgb[(r0 + i) + static_cast<i64>(c0 + jj) * a.ldS] = sv;
           SgTb[(c0 + jj) + static_cast<i64>(r0 + i) * a.ldT] = sv;
@@ -380,20 +402,20 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
 
     // ---- phase B element-wise: objective partials, momentum (frpcag.cpp:89-110)
     const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
-    const float coef = static_cast<float>((t - 1.0) / tn);
+    const T coef = static_cast<T>((t - 1.0) / tn);
     t = tn;
     double acc4[4] = {0.0, 0.0, 0.0, 0.0};
     for (int e = tid; e < TE; e += kPT) {
       const int jj = e / TM, i = e - jj * TM;
       if (i < rn && jj < cn) {
-        const float h = tile_h(e);
-        const float sv = Sc[e];
+        const T h = tile_h(e);
+        const T sv = Sc[e];
         const double d = static_cast<double>(Yt[e]) - static_cast<double>(sv);
         acc4[0] += a.loss == CPCAG_LOSS_L2 ? d * d : fabs(d);
         acc4[1] += static_cast<double>(h) * static_cast<double>(sv);
-        const float zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[e])));
-        const float hz = add_rn(h, mul_rn(coef, sub_rn(h, Hp[e])));
-        const float z = Zt[e];
+        const T zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[e])));
+        const T hz = add_rn(h, mul_rn(coef, sub_rn(h, Hp[e])));
+        const T z = Zt[e];
         const double zd = static_cast<double>(z), dd = static_cast<double>(sub_rn(zn, z));
         acc4[2] += zd * zd;
         acc4[3] += dd * dd;
@@ -413,7 +435,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   }
   // ---- output: the last prox result S_J (frpcag.cpp:111), own tile
   if (J >= 1 && !err) {
-    const float* Sgb = a.Sg[J & 1];
+    const T* Sgb = a.Sg[J & 1];
     for (int e = tid; e < TE; e += kPT) {
       const int jj = e / TM, i = e - jj * TM;
       if (i < rn && jj < cn)
@@ -435,9 +457,9 @@ struct Geom {
   size_t smem;
 };
 
-size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst) {
+size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst, size_t w = 4) {
   const size_t TE = static_cast<size_t>(TM) * TN;
-  return 8 * kPsm + 4 * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
+  return 8 * kPsm + w * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
               static_cast<size_t>(nst) * KC * ldB + static_cast<size_t>(KS) * TE + 6 * TE);
 }
 
@@ -486,7 +508,7 @@ bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
 // MODE 0: R x C CTAs (at most one per SM), TM/TN multiples of 4, the k range
 // split over thread groups; minimises the per-CTA multiply-add count TM TN
 // (rr + rc) within the shared-memory budget.
-bool plan_mode0(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
+bool plan_mode0(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out, size_t w = 4) {
   bool found = false;
   double best = 0.0;
   const i64 sms = c->num_sms;
@@ -502,11 +524,11 @@ bool plan_mode0(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
       const int KS = static_cast<int>(std::min<i64>(8, kPT / NMT));
       int KC = 128;
       size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM),
-                            static_cast<int>(TN), KS, KC, 2);
+                            static_cast<int>(TN), KS, KC, 2, w);
       if (sm > budget) {
         KC = 32;
         sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM), static_cast<int>(TN),
-                       KS, KC, 2);
+                       KS, KC, 2, w);
       }
       if (sm > budget) break;  // a taller tile only needs more
       const i64 R = (rr + TM - 1) / TM;
@@ -531,9 +553,9 @@ bool fista_persist_enabled() {
   return !(e && std::string(e) == "0");
 }
 
-bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, const float* Dc,
-                       const cpcag_frpcag_config& cfg, double step, float* X, double* trace_dev,
-                       FistaPersistOut* res) {
+template <typename T>
+bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T* Dc, const cpcag_frpcag_config& cfg,
+                       double step, T* X, double* trace_dev, FistaPersistOut* res) {
   if (rr < 1 || rc < 1 || rr > (1 << 20) || rc > (1 << 20)) return false;
   int optin = 0;
   CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
@@ -545,14 +567,20 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
   // chunks, each lane does 2 k-steps between CTA barriers and the loop is
   // barrier/latency-bound (ncu: barrier 24 %, wait 18 %), not wavefront-bound.
   const char* me = std::getenv("CPCAG_FISTA_PERSIST_MODE");
-  const bool want1 = me && std::string(me) == "1";
-  if (!(want1 && plan_mode1(c, rr, rc, budget, &g)) && !plan_mode0(c, rr, rc, budget, &g)) return false;
-  const void* kfn = g.mode == 1 ? reinterpret_cast<const void*>(fista_persist_k<1>)
-                                : reinterpret_cast<const void*>(fista_persist_k<0>);
-  if (g.mode == 1)
-    ensure_smem(fista_persist_k<1>, g.smem);
-  else
-    ensure_smem(fista_persist_k<0>, g.smem);
+  const bool want1 = sizeof(T) == 4 && me && std::string(me) == "1";
+  if (!(want1 && plan_mode1(c, rr, rc, budget, &g)) && !plan_mode0(c, rr, rc, budget, &g, sizeof(T))) return false;
+  const void* kfn;
+  if constexpr (sizeof(T) == 4) {
+    kfn = g.mode == 1 ? reinterpret_cast<const void*>(fista_persist_k<T, 1>)
+                      : reinterpret_cast<const void*>(fista_persist_k<T, 0>);
+    if (g.mode == 1)
+      ensure_smem(fista_persist_k<T, 1>, g.smem);
+    else
+      ensure_smem(fista_persist_k<T, 0>, g.smem);
+  } else {
+    kfn = reinterpret_cast<const void*>(fista_persist_k<T, 0>);
+    ensure_smem(fista_persist_k<T, 0>, g.smem);
+  }
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, g.threads, g.smem));
   const i64 grid = static_cast<i64>(g.R) * g.C;
@@ -560,14 +588,14 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
 
   const i64 ldS = static_cast<i64>(g.R) * g.TM, ldT = static_cast<i64>(g.C) * g.TN;
   const size_t sz = static_cast<size_t>(ldS * ldT);
-  DevBuf<float> sbuf(c, 4 * sz);
+  DevBuf<T> sbuf(c, 4 * sz);
   sbuf.zero(c);
   DevBuf<double> part(c, 2 * 4 * static_cast<size_t>(grid));
   DevBuf<unsigned> bar(c, 2);
   bar.zero(c);
   DevBuf<FistaPersistOut> out(c, 1);
   out.zero(c);
-  PersistArgs a{};
+  PersistArgs<T> a{};
   a.rr = static_cast<int>(rr);
   a.rc = static_cast<int>(rc);
   a.ldS = static_cast<int>(ldS);
@@ -583,7 +611,7 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
   a.use_c = cfg.gamma_c != 0.0;
   a.loss = cfg.loss;
   if (const char* e = std::getenv("CPCAG_FISTA_PERSIST_DBG")) a.dbg = std::atoi(e);
-  a.step = static_cast<float>(step);
+  a.step = static_cast<T>(step);
   a.tol = cfg.tol;
   a.max_iter = cfg.max_iter;
   a.gamma_r = cfg.gamma_r;
@@ -617,5 +645,10 @@ bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, 
                  res->prof_ns[2] * 1e-3, res->prof_ns[3] * 1e-3, res->prof_ns[4] * 1e-3);
   return true;
 }
+
+template bool fista_persist_run<float>(Ctx*, const float*, i64, i64, const float*, const float*,
+                                       const cpcag_frpcag_config&, double, float*, double*, FistaPersistOut*);
+template bool fista_persist_run<double>(Ctx*, const double*, i64, i64, const double*, const double*,
+                                        const cpcag_frpcag_config&, double, double*, double*, FistaPersistOut*);
 
 }  // namespace cpcag_cuda

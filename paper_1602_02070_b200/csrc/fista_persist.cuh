@@ -16,11 +16,11 @@ struct FistaPersistOut {
 // CPCAG_FISTA_PERSIST=0 disables the path (the per-kernel path then runs).
 bool fista_persist_enabled();
 
-// Runs the whole solve; false when the shape does not fit the tiling (the
+// Runs the whole solve (fp32 or fp64); false when the shape does not fit the tiling (the
 // caller then takes the per-kernel path).  Dr/Dc are the dense, exactly
 // symmetric operators; trace_dev receives one objective value per iteration.
-bool fista_persist_run(Ctx* c, const float* Y, i64 rr, i64 rc, const float* Dr, const float* Dc,
-                       const cpcag_frpcag_config& cfg, double step, float* X, double* trace_dev,
-                       FistaPersistOut* res);
+template <typename T>
+bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T* Dc, const cpcag_frpcag_config& cfg,
+                       double step, T* X, double* trace_dev, FistaPersistOut* res);
 
 }  // namespace cpcag_cuda
