@@ -386,9 +386,10 @@ __global__ void __launch_bounds__(NT, MINB) pcg_persistent_k(i64 n, i64 nb, cons
                                                         const double* __restrict__ inv, const double* __restrict__ B,
                                                         double* __restrict__ X, double* __restrict__ R,
                                                         double* __restrict__ P, double* __restrict__ AP, double tol,
-                                                        i64 max_iter, ColState* st) {
-  const i64 c0 = static_cast<i64>(blockIdx.x) * kCpb;
-  const i64 base = static_cast<i64>(blockIdx.x) * n * kCpb;
+                                                        i64 max_iter, ColState* st, i64 gbase) {
+  const i64 grp = gbase + blockIdx.x;  // column group of this CTA
+  const i64 c0 = grp * kCpb;
+  const i64 base = grp * n * kCpb;
   __shared__ int done_s[kCpb];
   __shared__ double rho_s[kCpb], target_s[kCpb];
   __shared__ i64 it_s[kCpb];
@@ -650,17 +651,24 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
     std::string cfg = ctas > c->num_sms ? "512x2" : "1024x1";
     if (const char* e = std::getenv("CPCAG_PCG_NT")) cfg = e;
     KScope ks_(c, "pcg_persistent");
-    const unsigned g = static_cast<unsigned>(ctas);
-    if (cfg == "512x2")
-      pcg_persistent_k<512, 2><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
-                                                        max_iter, st.p);
-    else if (cfg == "512x1")
-      pcg_persistent_k<512, 1><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
-                                                        max_iter, st.p);
-    else
-      pcg_persistent_k<1024, 1><<<g, 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
-                                                          max_iter, st.p);
-    launched(c);
+    // batches > 1: column groups in sequential launches, so one batch's
+    // slabs stay L2-resident across its iterations (CPCAG_KRON_BATCHES)
+    i64 batches = 1;
+    if (const char* e = std::getenv("CPCAG_KRON_BATCHES")) batches = std::max<i64>(1, std::atoll(e));
+    const i64 per = (ctas + batches - 1) / batches;
+    for (i64 g0 = 0; g0 < ctas; g0 += per) {
+      const unsigned g = static_cast<unsigned>(std::min(per, ctas - g0));
+      if (cfg == "512x2")
+        pcg_persistent_k<512, 2><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                          max_iter, st.p, g0);
+      else if (cfg == "512x1")
+        pcg_persistent_k<512, 1><<<g, 512, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                          max_iter, st.p, g0);
+      else
+        pcg_persistent_k<1024, 1><<<g, 1024, 0, c->stream>>>(n, nb, A->rp, A->ci, A->v, inv, B, X, R.p, P.p, AP.p, tol,
+                                                            max_iter, st.p, g0);
+      launched(c);
+    }
   }
   CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));
   sync(c);
