@@ -755,9 +755,9 @@ def run_cfg3(args):
 
 def run_cfg3_sharded(args, rank, local_rank, world):
     """cfg3 through alternate_decode_sharded: rank g owns columns
-    [g w, (g + 1) w) of the 4096 x 200 000 iterate, the search direction is
-    all-gathered and the CG dots all-reduced over NCCL every iteration
-    (SURVEY §8e).  Strong scaling: the problem is fixed, value = seconds per
+    [g w, (g + 1) w) of the 4096 x 200 000 iterate, the search direction's
+    halo columns are exchanged (NCCL all-to-all) and the CG dots all-reduced
+    over NCCL every iteration.  Strong scaling: the problem is fixed, value = seconds per
     decode (max over ranks)."""
     import torch
     import torch.distributed as dist
@@ -765,7 +765,7 @@ def run_cfg3_sharded(args, rank, local_rank, world):
     import paper_1602_02070_b200 as P
     from paper_1602_02070_b200 import _native as N
     from paper_1602_02070_b200 import workloads
-    from paper_1602_02070_b200.sharded import (CudaBlockBackend, TorchCollectives, alternate_decode_sharded,
+    from paper_1602_02070_b200.sharded import (CudaBlockBackend, HaloPlan, TorchCollectives, alternate_decode_sharded,
                                                column_blocks)
 
     torch.cuda.set_device(local_rank)
@@ -791,9 +791,14 @@ def run_cfg3_sharded(args, rank, local_rank, world):
     zeros = lambda k: torch.zeros(k, dtype=torch.float32, device="cuda")
     its = 100
     res = {}
+    # halo exchange (only the X L_c columns each block needs move; BENCH_ALLGATHER=1: all-gather)
+    halo = None
+    if not os.environ.get("BENCH_ALLGATHER"):
+        rpc, cic, _ = gc.laplacian.arrays()
+        halo = HaloPlan(rpc, cic, n, world, rank)
 
     def step():
-        res["r"] = alternate_decode_sharded(Xt, plan, be, coll, zeros, tol=1e-30, max_iter=its)
+        res["r"] = alternate_decode_sharded(Xt, plan, be, coll, zeros, tol=1e-30, max_iter=its, halo=halo)
 
     for _ in range(max(args.warmup, 1)):
         step()
@@ -819,7 +824,11 @@ def run_cfg3_sharded(args, rank, local_rank, world):
                "vs_baseline": None, "dtype": "f32", "data": "synthetic: seeded config-3 generator",
                "config": {"workload": f"cfg3 sharded: column-block CG over NCCL, p={p}, n={n}, "
                                       f"1/8 x 1/8 sampling, {it} iterations", "parallelism": f"colblock{world}",
-                          "block_cols": c1 - c0},
+                          "block_cols": c1 - c0,
+                          "exchange": ("halo all-to-all: rank 0 receives %d of its %d remote columns (%.1f %%)"
+                                       % (halo.halo_cols, halo.remote_cols,
+                                          100.0 * halo.halo_cols / max(halo.remote_cols, 1))) if halo
+                          else "all-gather of the column blocks"},
                "iters_per_s": round(it / (ms / 1e3), 1)}
         print(json.dumps(out), flush=True)
         if args.json_out:

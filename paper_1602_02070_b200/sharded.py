@@ -4,10 +4,13 @@ X (p x n) is split into contiguous column blocks, one per rank.  Per CG
 iteration (the reference recurrence of detail::pcg_core, solvers.hpp:33-74,
 identity preconditioner):
 
-  1. all-gather the search-direction blocks P_g into the full P (NCCL over
-     NVLink): the X·L_c term of a block needs P's halo columns, and for kNN
-     graphs over high-dimensional points the halo is nearly every column
-     (SURVEY §0.5), so a full all-gather is the exchange;
+  1. exchange the halo: the X·L_c term of block g needs the columns of P
+     that L_c's rows in the block reference outside it.  With a `HaloPlan`
+     every rank sends exactly the columns each other rank needs (one NCCL
+     all-to-all with uneven splits over NVLink) and receives only its own
+     halo; without one, the blocks are all-gathered (for kNN graphs over
+     high-dimensional points the halo is 82-100 % of the remote columns,
+     SURVEY §8(e), so the two move similar bytes there);
   2. AP_g = (γ̄_c P L_c + γ̄_r L_r P + M∘P)(:, block g) on the local GPU;
      L_r·P is block-local;
   3. all-reduce ⟨P_g, AP_g⟩ -> α;  R_g -= α AP_g;  all-reduce ‖R_g‖² -> β;
@@ -39,8 +42,47 @@ def column_blocks(n: int, world: int):
     return w, [(min(n, g * w), min(n, (g + 1) * w)) for g in range(world)]
 
 
+class HaloPlan:
+    """Which columns of P each rank sends to / receives from every other rank
+    for the X·L_c term (the pull over L_c's rows c of the block: L_c is a
+    symmetric Laplacian).  Built identically on every rank from L_c's CSR
+    structure (host arrays), O(nnz)."""
+
+    def __init__(self, rp, ci, n, world, rank):
+        rp = np.asarray(rp, np.int64)
+        ci = np.asarray(ci, np.int64)
+        w, blocks = column_blocks(n, world)
+        self.w, self.world, self.rank = w, world, rank
+        need = []
+        for r in range(world):
+            c0, c1 = blocks[r]
+            cols = ci[rp[c0]:rp[c1]]
+            need.append(np.unique(cols[(cols < c0) | (cols >= c1)]))
+        c0 = blocks[rank][0]
+        # send[d]: local indices (in this rank's block) of the columns rank d needs
+        self.send = [need[d][need[d] // w == rank] - c0 if d != rank else np.zeros(0, np.int64)
+                     for d in range(world)]
+        # recv[s]: global indices of the columns this rank receives from rank s
+        self.recv = [need[rank][need[rank] // w == s] if s != rank else np.zeros(0, np.int64) for s in range(world)]
+        self.halo_cols = int(sum(len(x) for x in self.recv))
+        self.remote_cols = int(n - (blocks[rank][1] - blocks[rank][0]))
+        self._dev = {}
+
+    def device_index(self, device):
+        import torch
+
+        key = str(device)
+        if key not in self._dev:
+            self._dev[key] = (torch.as_tensor(np.concatenate(self.send) if self.send else np.zeros(0, np.int64),
+                                              dtype=torch.int64, device=device),
+                              torch.as_tensor(np.concatenate(self.recv) if self.recv else np.zeros(0, np.int64),
+                                              dtype=torch.int64, device=device))
+        return self._dev[key]
+
+
 class TorchCollectives:
-    """all-gather / all-reduce on torch.distributed (NCCL for CUDA tensors)."""
+    """all-gather / all-to-all / all-reduce on torch.distributed (NCCL for
+    CUDA tensors)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -57,6 +99,22 @@ class TorchCollectives:
         else:
             parts = list(full_padded.chunk(self.world))
             self.dist.all_gather(parts, block_padded, group=self.group)
+
+    def exchange_halo(self, full_padded, block_padded, halo: HaloPlan, p: int, c0: int, nloc: int):
+        """full_padded[:, c0:c0+nloc] = this block; full_padded[:, halo] =
+        the columns other ranks own, received with one all-to-all (uneven
+        splits); columns nobody needs are left stale (never read)."""
+        send_idx, recv_idx = halo.device_index(block_padded.device)
+        Pv = block_padded[: p * nloc].view(nloc, p)  # column-major p x nloc
+        Pf = full_padded.view(-1, p)
+        Pf[c0:c0 + nloc] = Pv
+        sendbuf = Pv.index_select(0, send_idx).reshape(-1)
+        in_split = [len(x) * p for x in halo.send]
+        out_split = [len(x) * p for x in halo.recv]
+        recvbuf = full_padded.new_empty(sum(out_split))
+        self.dist.all_to_all_single(recvbuf, sendbuf, out_split, in_split, group=self.group)
+        if recv_idx.numel():
+            Pf.index_copy_(0, recv_idx, recvbuf.view(-1, p))
 
     def allreduce_sum(self, value: float, like) -> float:
         import torch
@@ -129,11 +187,13 @@ class ShardedResult:
     iterations: int
 
 
-def alternate_decode_sharded(Xt, plan, backend, coll, zeros, tol=1e-10, max_iter=5000) -> ShardedResult:
+def alternate_decode_sharded(Xt, plan, backend, coll, zeros, tol=1e-10, max_iter=5000,
+                             halo: Optional[HaloPlan] = None) -> ShardedResult:
     """The CG of decoders.cpp:145-186 over column blocks.
 
     backend: local primitives (rhs/apply/residual/update) of this rank's block.
-    coll:    rank/world + all_gather_blocks + allreduce_sum.
+    coll:    rank/world + all_gather_blocks + allreduce_sum (+ exchange_halo
+             when a HaloPlan is given: only the halo columns move).
     zeros:   allocator zeros(count) -> 1-D array/tensor on the backend's device.
     Blocks are p x w with w = ceil(n / world) columns (zero-padded).
     """
@@ -160,7 +220,10 @@ def alternate_decode_sharded(Xt, plan, backend, coll, zeros, tol=1e-10, max_iter
     while it < max_iter:
         if math.sqrt(rho) <= target:
             break
-        coll.all_gather_blocks(Pfull, P)
+        if halo is not None:
+            coll.exchange_halo(Pfull, P, halo, p, c0, nloc)
+        else:
+            coll.all_gather_blocks(Pfull, P)
         curv = coll.allreduce_sum(backend.apply(Pfull, view(AP)), AP)
         if not math.isfinite(curv) or curv <= 0.0:
             raise RuntimeError(f"pcg: breakdown (nonpositive curvature) at iteration {it}")

@@ -28,11 +28,11 @@ def _free_port():
     return port
 
 
-def _gloo_worker(rank, world, port, out):
+def _gloo_worker(rank, world, port, out, use_halo=False):
     import torch
     import torch.distributed as dist
 
-    from paper_1602_02070_b200.sharded import TorchCollectives, alternate_decode_sharded, column_blocks
+    from paper_1602_02070_b200.sharded import HaloPlan, TorchCollectives, alternate_decode_sharded, column_blocks
     from shard_double import NumpyBlockBackend
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -41,20 +41,28 @@ def _gloo_worker(rank, world, port, out):
     c0, c1 = blocks[rank]
     be = NumpyBlockBackend(plan, Lr, Lc, 1.0 / 0.3, 1.0 / 0.4, c0, c1)
     coll = TorchCollectives()
+    halo = None
+    if use_halo:
+        rp, ci, _ = Lc.arrays()
+        halo = HaloPlan(rp, ci, plan.n, world, rank)
     res = alternate_decode_sharded(Xt, plan, be, coll, lambda k: torch.zeros(k, dtype=torch.float64),
-                                   tol=1e-10, max_iter=400)
-    out[rank] = (c0, c1, res.X_block.numpy().copy(), res.iterations, res.converged)
+                                   tol=1e-10, max_iter=400, halo=halo)
+    out[rank] = (c0, c1, res.X_block.numpy().copy(), res.iterations, res.converged,
+                 halo.halo_cols if halo else -1)
     dist.destroy_process_group()
 
 
-def test_sharded_decoder_gloo_world2_matches_oracle():
+@pytest.mark.parametrize("world,use_halo", [(2, False), (2, True), (3, True)])
+def test_sharded_decoder_gloo_matches_oracle(world, use_halo):
+    """gloo ranks; with a HaloPlan only the halo columns move (all-to-all
+    with uneven splits), without one the blocks are all-gathered."""
     import torch.multiprocessing as mp
 
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
     ctx = mp.get_context("spawn")
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, out)) for r in range(2)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, out, use_halo)) for r in range(world)]
     for pr in procs:
         pr.start()
     for pr in procs:
@@ -63,11 +71,32 @@ def test_sharded_decoder_gloo_world2_matches_oracle():
     Lr, Lc, plan, Xt = _case()
     ro = O.alternate_decode(Xt, plan, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 400)
     X = np.zeros((plan.p, plan.n))
-    for r in range(2):
-        c0, c1, blk, it, conv = out[r]
+    for r in range(world):
+        c0, c1, blk, it, conv, hc = out[r]
         X[:, c0:c1] = blk.reshape((plan.p, c1 - c0), order="F")
         assert abs(it - ro.iterations) <= 1 and conv == ro.converged
+        if use_halo:
+            assert 0 < hc <= plan.n - (c1 - c0)  # at most the remote columns move
     assert rel(X, ro.X) <= 1e-9
+
+
+def test_halo_plan_covers_exactly_the_needed_columns():
+    from paper_1602_02070_b200.sharded import HaloPlan, column_blocks
+
+    Lc = knn_laplacian(101, 3, 6, 4)
+    rp, ci, _ = Lc.arrays()
+    world = 4
+    w, blocks = column_blocks(101, world)
+    plans = [HaloPlan(rp, ci, 101, world, r) for r in range(world)]
+    for r in range(world):
+        c0, c1 = blocks[r]
+        cols = set(ci[rp[c0]:rp[c1]].tolist())
+        need = sorted(c for c in cols if not c0 <= c < c1)
+        got = sorted(int(x) for s in range(world) for x in plans[r].recv[s])
+        assert got == need
+        for s in range(world):  # what s sends to r is what r receives from s
+            sent = (plans[s].send[r] + blocks[s][0]).tolist()
+            assert sent == plans[r].recv[s].tolist()
 
 
 def test_column_blocks_cover_and_pad():
@@ -134,14 +163,14 @@ def test_sharded_decoder_cuda_three_ranks_one_gpu(prec):
     assert rel(X, ro.X) <= (1e-6 if prec == "f64" else 1e-4)
 
 
-def _nccl_worker(port, out):
+def _nccl_worker(port, out, use_halo=False):
     import torch
     import torch.distributed as dist
 
     import paper_1602_02070_b200 as P
     from helpers import to_device
     from paper_1602_02070_b200 import _native as N
-    from paper_1602_02070_b200.sharded import (CudaBlockBackend, TorchCollectives, alternate_decode_sharded,
+    from paper_1602_02070_b200.sharded import (CudaBlockBackend, HaloPlan, TorchCollectives, alternate_decode_sharded,
                                                column_blocks)
 
     torch.cuda.set_device(0)
@@ -155,8 +184,12 @@ def _nccl_worker(port, out):
     coll = TorchCollectives()
     assert dist.get_backend() == "nccl"
     Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), device="cuda").t()
+    halo = None
+    if use_halo:
+        rp, ci, _ = Lc.arrays()
+        halo = HaloPlan(rp, ci, plan.n, 1, 0)
     res = alternate_decode_sharded(Xt_d, plan, be, coll, lambda k: torch.zeros(k, dtype=torch.float64, device="cuda"),
-                                   tol=1e-10, max_iter=300)
+                                   tol=1e-10, max_iter=300, halo=halo)
     torch.cuda.synchronize()
     out["r"] = (res.X_block.cpu().numpy().copy(), res.iterations)
     be.close()
@@ -164,7 +197,8 @@ def _nccl_worker(port, out):
 
 
 @pytest.mark.gpu
-def test_sharded_decoder_nccl_world1_matches_oracle():
+@pytest.mark.parametrize("use_halo", [False, True])
+def test_sharded_decoder_nccl_world1_matches_oracle(use_halo):
     """The column-sharded driver over a real NCCL communicator (world 1: the
     all-gather and the all-reduced dots go through NCCL on the device)."""
     import torch.multiprocessing as mp
@@ -172,7 +206,7 @@ def test_sharded_decoder_nccl_world1_matches_oracle():
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    pr = mp.get_context("spawn").Process(target=_nccl_worker, args=(port, out))
+    pr = mp.get_context("spawn").Process(target=_nccl_worker, args=(port, out, use_halo))
     pr.start()
     pr.join(300)
     assert pr.exitcode == 0
