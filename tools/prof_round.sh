@@ -20,4 +20,9 @@ SWEEP_ITERS=3 timeout -s KILL 900 ncu --set full --clock-control none --import-s
 timeout -s KILL 600 python bench.py --config cfg2 --steps 3 --warmup 3 --json-out $O/bench_cfg2.json > $O/bench_cfg2.log 2>&1; echo "cfg2 rc=$?"
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file $O/launches_cfg2.csv python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_launch2.log 2>&1; echo "launch list cfg2 rc=$?"
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:knn_tc_filter2 -c 1 -o $O/full_cfg2_tc -f python bench.py --config cfg2 --steps 1 --warmup 1 > $O/ncu_full_cfg2.log 2>&1; echo "ncu cfg2 rc=$?"
-ls $O | wc -l
+# summarise the full captures here and drop the reports (gpurun copies back <= 64 MiB)
+for r in $O/*.ncu-rep; do python tools/ncu_summary.py $r > ${r%.ncu-rep}.md 2>/dev/null; done
+python tools/ncu_hot.py $O/full_cfg1_cg_apply_fast2.ncu-rep cg_apply_fast2 20 > $O/hot_cfg1_apply.txt 2>/dev/null
+python tools/ncu_hot.py $O/full_cfg1_fista_persist.ncu-rep fista_persist 20 > $O/hot_cfg1_fista.txt 2>/dev/null
+rm -f $O/*.ncu-rep
+ls $O | wc -l; du -sh $O
