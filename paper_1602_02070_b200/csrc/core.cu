@@ -402,6 +402,7 @@ struct PowerState {
   double est;
   i64 iterations;
   unsigned bar_count, bar_gen;
+  int prof;  // CPCAG_POWER_PROF: CTA 0 prints its phase times
 };
 
 __device__ __forceinline__ double warp_row_dot(i64 k0, i64 k1, const int* __restrict__ ci,
@@ -491,6 +492,16 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   const double* vsrc = v_in_smem ? vs : v0;
   double est = 0.0;
   i64 it = 0;
+  unsigned long long pt[4] = {0, 0, 0, 0}, tq = 0;  // CTA 0 phase timers (CPCAG_POWER_PROF)
+  auto mark = [&](int ph) {
+    if (st->prof && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long now;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+      if (ph >= 0) pt[ph] += now - tq;
+      tq = now;
+    }
+  };
+  mark(-1);
   for (; it < max_iter; ++it) {
     double* w = wbuf + (it & 1) * n;
     for (i64 r = r0 + wid; r < r1; r += nw) {
@@ -503,7 +514,9 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       acc = warp_sum(acc);
       if (lane == 0) w[r] = acc;
     }
+    mark(0);
     grid_barrier(&st->bar_count, &st->bar_gen);
+    mark(1);
     // ||w||^2 straight from w, which every CTA reads anyway: one L2 round
     // trip per iteration instead of two (partials, then w).  Same data and
     // the same fixed-order block reduction in every CTA, so every CTA gets
@@ -515,6 +528,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       t[0] += x * x;
     }
     block_sum<1>(t);
+    mark(2);
     const double nrm = sqrt(t[0]);
     if (nrm == 0.0) {
       est = 0.0;
@@ -531,12 +545,17 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       double* vg = const_cast<double*>(v0);
       for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(__ldcg(w + i), nrm);
     }
+    mark(3);
     if (it > 0 && fabs(est - prev) <= tol * est) {
       ++it;
       break;
     }
     if (!v_in_smem) grid_barrier(&st->bar_count, &st->bar_gen);
   }
+  if (st->prof && blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[power_iter] grid %d n %lld its %lld: spmv %.1f barrier %.1f read+norm %.1f scale %.1f us\n", gridDim.x,
+           static_cast<long long>(n), static_cast<long long>(it), pt[0] * 1e-3, pt[1] * 1e-3, pt[2] * 1e-3,
+           pt[3] * 1e-3);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->est = est;
     st->iterations = it;
@@ -560,6 +579,11 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   CUDA_OK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   DevBuf<PowerState> st(c, 1);
   st.zero(c);
+  if (std::getenv("CPCAG_POWER_PROF")) {
+    PowerState ps{};
+    ps.prof = 1;
+    CUDA_OK(cudaMemcpyAsync(st.p, &ps, sizeof(ps), cudaMemcpyHostToDevice, c->stream));
+  }
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
   i64 small_nnz = 4096;  // single-CTA kernel (no grid barrier) up to this many entries
   if (const char* e = std::getenv("CPCAG_POWER_SMALL_NNZ")) small_nnz = std::atoll(e);
