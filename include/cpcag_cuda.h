@@ -321,7 +321,12 @@ typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36
   uint64_t seed;
   int decoder_variant;       /* DecoderVariant (decoders.hpp:11): CPCAG_DECODER_ALTERNATE or _APPROX */
   cpcag_approx_config approx; /* the approximate decoder's DecoderConfig fields */
+  int task;                  /* Task (pipeline.hpp:18): CPCAG_TASK_LOWRANK (default), _CLUSTER or _BOTH */
+  int64_t n_clusters;        /* clustering: k (0 = max(1, detected rank)), pipeline.cpp:374 */
+  int64_t kmeans_restarts;   /* default 10 */
 } cpcag_pipeline_config;
+
+enum { CPCAG_TASK_LOWRANK = 0, CPCAG_TASK_CLUSTER = 1, CPCAG_TASK_BOTH = 2 };
 
 enum { CPCAG_DECODER_IDEAL = 0, CPCAG_DECODER_ALTERNATE = 1, CPCAG_DECODER_APPROX = 2 };
 
@@ -374,13 +379,16 @@ int cpcag_cuda_decode_labels(cpcag_ctx ctx, const int* sampled, int64_t rho_c, i
 int cpcag_clustering_error(const int* pred, const int* truth, int64_t n, int64_t k_pred, int64_t k_truth,
                            double* out);
 
-/* Optional factor output of the approximate decoder (PipelineReport::factors,
- * pipeline.hpp:91): fp64 U (p x k), sigma (k), V (n x k) when k <= k_cap. */
+/* Optional outputs of run_pipeline: the approximate decoder's factors
+ * (PipelineReport::factors, pipeline.hpp:91): fp64 U (p x k), sigma (k),
+ * V (n x k) when k <= k_cap; and the decoded cluster labels
+ * (PipelineReport::labels, pipeline.hpp:89; n ints, cluster/both tasks). */
 typedef struct cpcag_pipeline_factors {
   double* U;
   double* sigma;
   double* V;
   int64_t k_cap;
+  int* labels;
 } cpcag_pipeline_factors;
 
 typedef struct cpcag_pipeline_report { /* PipelineReport subset, pipeline.hpp:73-94 */
@@ -395,12 +403,16 @@ typedef struct cpcag_pipeline_report { /* PipelineReport subset, pipeline.hpp:73
   /* Stage timings in ms (device events), in the reference's stage order:
    * graphs, plan, subsample, kron, solve, decode (pipeline.cpp:273-350). */
   double stage_ms[6];
+  double cluster_ms;      /* the "cluster" stage (cluster/both tasks) */
+  int64_t n_clusters;     /* k the clustering stage used */
 } cpcag_pipeline_report;
 
-/* run_pipeline, low-rank task (pipeline.cpp:228-350): graphs (row graph
- * from W_r when given, else kNN over rows; column graph from W_c when given,
- * else kNN over columns) -> plan -> subsample -> Kron -> FISTA -> detected
- * rank -> decode with the alternate or the approximate decoder.  Y is p x n.
+/* run_pipeline (pipeline.cpp:228-391): graphs (row graph from W_r when
+ * given, else kNN over rows; column graph from W_c when given, else kNN over
+ * columns) -> plan -> subsample -> Kron -> FISTA -> detected rank -> decode
+ * with the alternate or the approximate decoder (lowrank/both tasks) ->
+ * k-means on Xt + decode_labels (cluster/both tasks, labels into
+ * factors->labels).  Y is p x n; X may be NULL for the cluster task.
  * Xt (rho_r x rho_c) and X (p x n) receive the compressed and decoded
  * solutions; omega_r/omega_c (may be NULL) receive the plan; objective (may
  * be NULL) the FISTA trace; factors (may be NULL) the approximate decoder's

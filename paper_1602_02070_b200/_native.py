@@ -53,18 +53,19 @@ class PipelineConfigC(C.Structure):
     _fields_ = [("knn", i64), ("laplacian", C.c_int), ("sigma2", dbl), ("a", i64), ("b", i64),
                 ("rho_r_override", i64), ("rho_c_override", i64), ("kron_pcg_tol", dbl),
                 ("frpcag", FrpcagConfigC), ("decoder", DecoderConfigC), ("lambda_k1_r", dbl),
-                ("lambda_k1_c", dbl), ("seed", u64), ("decoder_variant", C.c_int), ("approx", ApproxConfigC)]
+                ("lambda_k1_c", dbl), ("seed", u64), ("decoder_variant", C.c_int), ("approx", ApproxConfigC),
+                ("task", C.c_int), ("n_clusters", i64), ("kmeans_restarts", i64)]
 
 
 class PipelineFactorsC(C.Structure):
-    _fields_ = [("U", vp), ("sigma", vp), ("V", vp), ("k_cap", i64)]
+    _fields_ = [("U", vp), ("sigma", vp), ("V", vp), ("k_cap", i64), ("labels", vp)]
 
 
 class PipelineReportC(C.Structure):
     _fields_ = [("p", i64), ("n", i64), ("rho_r", i64), ("rho_c", i64), ("trace", SolveTraceC),
                 ("decoder_converged", C.c_int), ("decoder_iterations", i64), ("detected_rank", i64),
                 ("factors_k", i64), ("has_factors", C.c_int), ("lambda_k1_r", dbl), ("lambda_k1_c", dbl),
-                ("stage_ms", dbl * 6)]
+                ("stage_ms", dbl * 6), ("cluster_ms", dbl), ("n_clusters", i64)]
 
 
 # (name, restype, argtypes) of every exported symbol.

@@ -819,7 +819,7 @@ STAGES = ("graphs", "plan", "subsample", "kron", "solve", "decode")
 
 
 @dataclass
-class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
+class PipelineConfig:  # pipeline.hpp:36-63
     knn: int = 10
     laplacian: str = "combinatorial"
     sigma2: float = 0.0
@@ -833,6 +833,9 @@ class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
     lambda_k1_r: float = 0.0  # <= 0: computed on the device as the reference does (pipeline.cpp:343-349)
     lambda_k1_c: float = 0.0
     seed: int = 0
+    task: str = "lowrank"     # Task (pipeline.hpp:18): "lowrank" | "cluster" | "both"
+    n_clusters: int = 0       # 0: max(1, detected rank) (pipeline.cpp:374)
+    kmeans_restarts: int = 10
 
     def c(self) -> N.PipelineConfigC:
         return N.PipelineConfigC(int(self.knn), _kind(self.laplacian), float(self.sigma2), int(self.a),
@@ -840,7 +843,15 @@ class PipelineConfig:  # pipeline.hpp:36-63 (low-rank task, alternate decoder)
                                  float(self.kron_pcg_tol), self.frpcag.c(), self.decoder.c(),
                                  float(self.lambda_k1_r), float(self.lambda_k1_c),
                                  int(self.seed) & (2**64 - 1), _variant(self.decoder.variant),
-                                 self.decoder.approx_c())
+                                 self.decoder.approx_c(), _task(self.task), int(self.n_clusters),
+                                 int(self.kmeans_restarts))
+
+
+def _task(t) -> int:
+    table = {"lowrank": 0, "cluster": 1, "both": 2}
+    if t not in table:
+        raise ValueError(f"unknown task {t!r}")
+    return table[t]
 
 
 def _variant(v) -> int:
@@ -869,6 +880,7 @@ class PipelineReport:  # pipeline.hpp:73-94 (subset)
     factors: Optional[LowRankFactors] = None  # approximate decoder only
     has_factors: bool = False
     lambda_k1: tuple = (0.0, 0.0)  # gaps the alternate decoder used (rows, columns)
+    labels: Optional[np.ndarray] = None  # decoded cluster labels (cluster/both tasks, pipeline.hpp:89)
 
     def stage_ms(self, name: str) -> float:
         return self.stages.get(name, 0.0)
@@ -893,7 +905,7 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
         x, xp = _given_out(out[1], (p, n), prec, "out[1] (X)")
     else:
         xt, xtp = _out(cuda, _torch_device(Y), (rho_r, rho_c), prec)
-        x, xp = _out(cuda, _torch_device(Y), (p, n), prec)
+        x, xp = _out(cuda, _torch_device(Y), (p, n), prec) if cfg.task != "cluster" else (None, None)
     om_r = np.empty(max(rho_r, 1), np.int64)
     om_c = np.empty(max(rho_c, 1), np.int64)
     obj = np.zeros(max(int(cfg.frpcag.max_iter), 1))
@@ -903,8 +915,10 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
     fU = np.empty((p, kcap), np.float64, order="F")
     fV = np.empty((n, kcap), np.float64, order="F")
     fs = np.empty(max(kcap, 1), np.float64)
+    labels = np.empty(n, np.int32) if cfg.task in ("cluster", "both") else None
     fac = N.PipelineFactorsC(fU.ctypes.data if kcap else None, fs.ctypes.data if kcap else None,
-                             fV.ctypes.data if kcap else None, kcap)
+                             fV.ctypes.data if kcap else None, kcap,
+                             labels.ctypes.data if labels is not None else None)
     N.check(N.lib().cpcag_cuda_run_pipeline(_ctx(ctx), prec, y.ptr, p, n, W_r.handle if W_r else None,
                                             W_c.handle if W_c else None, C.byref(c), xtp, xp,
                                             om_r.ctypes.data, om_c.ctypes.data, obj.ctypes.data,
@@ -914,6 +928,8 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
                        float(rep.trace.step))
     plan = SamplingPlan(om_r[:rep.rho_r].copy(), om_c[:rep.rho_c].copy(), p, n, seed=cfg.seed)
     stages = {name: float(rep.stage_ms[k]) for k, name in enumerate(STAGES)}
+    if labels is not None:
+        stages["cluster"] = float(rep.cluster_ms)
     factors = None
     if rep.has_factors:
         k = int(rep.factors_k)
@@ -921,7 +937,7 @@ def run_pipeline(Y, cfg: PipelineConfig, W_r: Optional[SparseMatrix] = None,
     return PipelineReport(int(rep.p), int(rep.n), int(rep.rho_r), int(rep.rho_c), trace, plan, xt, x,
                           bool(rep.decoder_converged), int(rep.decoder_iterations), stages,
                           int(rep.detected_rank), factors, bool(rep.has_factors),
-                          (float(rep.lambda_k1_r), float(rep.lambda_k1_c)))
+                          (float(rep.lambda_k1_r), float(rep.lambda_k1_c)), labels)
 
 
 # ------------------------------------------------------------------ I/O (io.hpp:14-44)

@@ -343,6 +343,20 @@ void kmeans_device(Ctx* c, const double* X, i64 rows, i64 n, i64 k, i64 restarts
   sync(c);
 }
 
+// decode_labels (clustering.cpp:139-160) on device data: sampled labels
+// (rho_c ints, device, values in [0, k)) -> labels (n ints, device).
+void decode_labels_device(Ctx* c, Csr* Lc, const std::vector<i64>& om_c, const int* sampled_dev, i64 k,
+                          double pcg_tol, i64 pcg_max_iter, i64 n, int* labels_dev) {
+  const i64 rho_c = static_cast<i64>(om_c.size());
+  if (Lc->rows != n) invalid("decode_labels: column Laplacian does not match plan");
+  DevBuf<double> Ct(c, static_cast<size_t>(std::max<i64>(rho_c * k, 1))), C(c, static_cast<size_t>(std::max<i64>(n * k, 1)));
+  indicator_k<<<blocks_for(rho_c), kBlock, 0, c->stream>>>(rho_c, k, sampled_dev, Ct.p);  // ClusterLabels::indicator
+  launched(c);
+  graph_upsample_device(c, Lc, om_c, Ct.p, k, pcg_tol, pcg_max_iter, C.p);
+  max_pool_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, k, C.p, labels_dev);
+  launched(c);
+}
+
 }  // namespace cpcag_cuda
 
 using namespace cpcag_cuda;
@@ -441,14 +455,9 @@ extern "C" int cpcag_cuda_decode_labels(cpcag_ctx ctx, const int* sampled, int64
     std::vector<i64> om(static_cast<size_t>(rho_c));
     CUDA_OK(cudaMemcpy(om.data(), omega_c, sizeof(i64) * rho_c, cudaMemcpyDefault));
     DevBuf<int> ld(c, static_cast<size_t>(std::max<i64>(rho_c, 1)));
-    DevBuf<double> Ct(c, static_cast<size_t>(std::max<i64>(rho_c * k, 1))), C(c, static_cast<size_t>(std::max<i64>(n * k, 1)));
     CUDA_OK(cudaMemcpyAsync(ld.p, lab.data(), sizeof(int) * rho_c, cudaMemcpyHostToDevice, c->stream));
-    indicator_k<<<blocks_for(rho_c), kBlock, 0, c->stream>>>(rho_c, k, ld.p, Ct.p);  // ClusterLabels::indicator
-    launched(c);
-    graph_upsample_device(c, L, om, Ct.p, k, pcg_tol, pcg_max_iter, C.p);
     DevBuf<int> out(c, static_cast<size_t>(std::max<i64>(n, 1)));
-    max_pool_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, k, C.p, out.p);
-    launched(c);
+    decode_labels_device(c, L, om, ld.p, k, pcg_tol, pcg_max_iter, n, out.p);
     CUDA_OK(cudaMemcpyAsync(labels, out.p, sizeof(int) * n, cudaMemcpyDefault, c->stream));
     sync(c);
   });

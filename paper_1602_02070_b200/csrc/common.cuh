@@ -404,6 +404,11 @@ struct HostRng {
 
 // Internal entry points shared between translation units.
 double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter);
+// kmeans / decode_labels on the device (cluster.cu).
+void kmeans_device(Ctx* c, const double* X, i64 rows, i64 n, i64 k, i64 restarts, uint64_t seed, i64 max_iter,
+                   int* assignments_dev, double* wcss_out);
+void decode_labels_device(Ctx* c, Csr* Lc, const std::vector<i64>& om_c, const int* sampled_dev, i64 k,
+                          double pcg_tol, i64 pcg_max_iter, i64 n, int* labels_dev);
 // k smallest eigenvalues (ascending, host array) by Lanczos (lanczos.cu).
 void sym_eigvals_lanczos(Ctx* c, Csr* A, i64 k, double tol, i64 max_iter, uint64_t seed, double* evals,
                          i64* iterations);

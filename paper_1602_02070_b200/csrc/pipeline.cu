@@ -139,7 +139,8 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
   rep->has_factors = 0;
   rep->factors_k = 0;
 
-  rep->stage_ms[5] = tm.run("decode", [&] {
+  const bool want_x = cfg.task != CPCAG_TASK_CLUSTER;
+  if (want_x) rep->stage_ms[5] = tm.run("decode", [&] {
     if (full) {
       // pipeline.cpp:327-337: no compression, scatter back through the plan.
       dim3 g(blocks_for(rho_r), static_cast<unsigned>(std::min<i64>(rho_c, 65535)));
@@ -199,6 +200,22 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     rep->decoder_converged = conv;
     rep->decoder_iterations = it;
   });
+  // pipeline.cpp:371-388: k-means on the compressed solution's columns
+  // (seed mix(seed ^ "kmean")), then decode_labels over the column graph
+  if (cfg.task == CPCAG_TASK_CLUSTER || cfg.task == CPCAG_TASK_BOTH) {
+    rep->cluster_ms = tm.run("cluster", [&] {
+      const i64 k = cfg.n_clusters > 0 ? cfg.n_clusters : std::max<i64>(1, rep->detected_rank);
+      DevBuf<double> Xd(c, static_cast<size_t>(std::max<i64>(rho_r * rho_c, 1)));
+      to_f64_device(c, Xt_out, rho_r * rho_c, Xd.p);
+      DevBuf<int> sl(c, static_cast<size_t>(std::max<i64>(rho_c, 1))), lab(c, static_cast<size_t>(n));
+      kmeans_device(c, Xd.p, rho_r, rho_c, k, cfg.kmeans_restarts > 0 ? cfg.kmeans_restarts : 10,
+                    HostRng::mix(cfg.seed ^ 0x6b6d65616eULL), 100, sl.p, nullptr);
+      decode_labels_device(c, Lc.get(), om_c, sl.p, k, cfg.decoder.pcg_tol, cfg.decoder.pcg_max_iter, n, lab.p);
+      if (factors && factors->labels)
+        CUDA_OK(cudaMemcpyAsync(factors->labels, lab.p, sizeof(int) * n, cudaMemcpyDefault, c->stream));
+      rep->n_clusters = k;
+    });
+  }
   if (om_r_out) std::copy(om_r.begin(), om_r.end(), om_r_out);
   if (om_c_out) std::copy(om_c.begin(), om_c.end(), om_c_out);
 }
@@ -215,7 +232,7 @@ extern "C" int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void*
     using T = decltype(tag);
     return guard([&] {
       Ctx* c = as_ctx(ctx);
-      if (!cfg || !report || !Xt || !X) invalid("null argument");
+      if (!cfg || !report || !Xt || (!X && cfg->task != CPCAG_TASK_CLUSTER)) invalid("null argument");
       if (p < 1 || n < 1) invalid("run_pipeline: empty data matrix");
       i64 rho_r = cfg->rho_r_override > 0 ? cfg->rho_r_override : (cfg->b >= 1 ? (p + cfg->b - 1) / cfg->b : p);
       i64 rho_c = cfg->rho_c_override > 0 ? cfg->rho_c_override : (cfg->a >= 1 ? (n + cfg->a - 1) / cfg->a : n);
@@ -223,7 +240,7 @@ extern "C" int cpcag_cuda_run_pipeline(cpcag_ctx ctx, int precision, const void*
       rho_c = std::min<i64>(rho_c, n);
       InView<T> y(c, static_cast<const T*>(Y), static_cast<size_t>(p * n));
       OutView<T> xt(c, static_cast<T*>(Xt), static_cast<size_t>(std::max<i64>(rho_r, 1) * std::max<i64>(rho_c, 1)));
-      OutView<T> x(c, static_cast<T*>(X), static_cast<size_t>(p * n));
+      OutView<T> x(c, static_cast<T*>(X), X ? static_cast<size_t>(p * n) : 0);
       run_pipeline_device<T>(c, y.d, p, n, W_r ? as_csr(W_r) : nullptr, W_c ? as_csr(W_c) : nullptr, *cfg, xt.d, x.d,
                              omega_r, omega_c, objective, report, factors);
       xt.flush(c);

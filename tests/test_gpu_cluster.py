@@ -97,3 +97,32 @@ def test_decode_labels_component_example_and_clustering_error(P, ctx):
         assert P.clustering_error(P.ClusterLabels(p, 5), P.ClusterLabels(q, 5)) == O.clustering_error(p, q, 5)
     with pytest.raises(ValueError, match="cluster counts differ"):
         P.clustering_error(P.ClusterLabels(np.zeros(4, np.int32), 2), P.ClusterLabels(np.zeros(4, np.int32), 3))
+
+
+@pytest.mark.parametrize("task", ["cluster", "both"])
+def test_pipeline_cluster_task_matches_oracle(P, ctx, task):
+    """run_pipeline with the clustering task (pipeline.cpp:371-388): k-means on
+    Xt (seed mix(seed ^ "kmean")) then decode_labels over the column graph."""
+    rs = np.random.default_rng(31)
+    p, n, k = 40, 90, 3
+    centres = rs.standard_normal((p, k)) * 4.0
+    truth = np.repeat(np.arange(k), n // k)
+    Y = np.asfortranarray(centres[:, truth] + 0.3 * rs.standard_normal((p, n)))
+    g = float(np.sqrt(max(p, n)))
+    cfg = P.PipelineConfig(knn=10, a=3, b=2, kron_pcg_tol=1e-11,
+                           frpcag=P.FrpcagConfig(gamma_r=g, gamma_c=g, loss="l1", tol=1e-300, max_iter=50),
+                           decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-10, pcg_max_iter=500, variant="alternate"),
+                           lambda_k1_r=0.1, lambda_k1_c=0.1, seed=77, task=task, n_clusters=k, kmeans_restarts=4)
+    rep = P.run_pipeline(Y, cfg, ctx=ctx)
+    assert rep.labels is not None and rep.labels.shape == (n,)
+    assert (rep.X is None) == (task == "cluster")
+    # oracle composite
+    gr, gc = O.build_knn_graph(Y, True, 10), O.build_knn_graph(Y, False, 10)
+    plan = O.draw_plan(p, n, -(-p // 2), -(-n // 3), seed=77)
+    assert np.array_equal(rep.plan.omega_c, plan.omega_c)
+    Xt, _ = O.fista_solve(O.subsample(Y, plan), O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11),
+                          O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11), O.FrpcagConfig(g, g, "l1", 1e-300, 50))
+    a, _ = O.kmeans(Xt, k, 4, O.rng_mix(77 ^ 0x6B6D65616E))
+    lab, _ = O.decode_labels(a, k, plan, gc.laplacian, 1e-10, 500)
+    assert np.array_equal(rep.labels, lab)
+    assert O.clustering_error(rep.labels, truth, k) <= 0.05
