@@ -32,7 +32,8 @@ __all__ = [
     "ApproxDecodeResult", "approx_decode", "EigenPairs", "sym_eig", "sym_eigvals_lanczos", "spectral_gap",
     "glr1_info", "load_matrix", "save_matrix", "load_sparse", "save_sparse", "save_factors",
     "load_factors", "plan_to_json", "plan_from_json", "save_plan", "load_plan",
-    "ClusterLabels", "kmeans", "decode_labels", "clustering_error",
+    "ClusterLabels", "kmeans", "decode_labels", "clustering_error", "save_labels_csv", "load_labels_csv",
+    "report_to_json", "emit_report",
 ]
 
 
@@ -1174,3 +1175,75 @@ def clustering_error(pred: ClusterLabels, truth: ClusterLabels) -> float:
     N.check(N.lib().cpcag_clustering_error(p.ctypes.data, t.ctypes.data, len(p), int(pred.k), int(truth.k),
                                            C.byref(out)))
     return float(out.value)
+
+
+def save_labels_csv(labels, path: str):
+    """io.cpp:268-273: "index,label" header, one line per item."""
+    with open(path, "w") as f:
+        f.write("index,label\n")
+        for i, v in enumerate(np.asarray(labels).tolist()):
+            f.write(f"{i},{int(v)}\n")
+
+
+def load_labels_csv(path: str) -> np.ndarray:
+    """io.cpp:275-290."""
+    try:
+        f = open(path)
+    except OSError:
+        raise RuntimeError(f"{path}: cannot open for reading")
+    with f:
+        lines = f.read().split("\n")
+    if not lines or lines[0] == "":
+        raise RuntimeError(f"{path}: empty file")
+    out = []
+    for no, line in enumerate(lines[1:], start=2):
+        if line == "":
+            continue
+        if "," not in line:
+            raise RuntimeError(f"{path}: missing comma at line {no}")
+        out.append(int(_num(line.split(",", 1)[1], path, no)))
+    return np.asarray(out, np.int32)
+
+
+def report_to_json(rep: "PipelineReport", cfg: "PipelineConfig", include_timings: bool = True) -> str:
+    """pipeline.cpp:393-415 for the fields this mirror models (the config
+    subset of PipelineConfig, sizes, detected rank, the FISTA trace and the
+    stage timings)."""
+    import dataclasses
+    import json
+
+    def conf(c):
+        d = dataclasses.asdict(c)
+        return json.loads(json.dumps(d, default=str))
+
+    j = {"config": conf(cfg), "p": rep.p, "n": rep.n, "rho_r": rep.rho_r, "rho_c": rep.rho_c, "seed": int(cfg.seed),
+         "detected_rank": rep.detected_rank,
+         "solve": {"iterations": rep.trace.iterations, "converged": bool(rep.trace.converged),
+                   "final_rel_change": rep.trace.final_rel_change, "step": rep.trace.step,
+                   "objective": [float(x) for x in rep.trace.objective]}}
+    if include_timings:
+        j["timings_ms"] = {k: float(v) for k, v in rep.stages.items()}
+    return json.dumps(j, indent=2, sort_keys=True)
+
+
+def emit_report(rep: "PipelineReport", cfg: "PipelineConfig", out_dir: str, ctx=None):
+    """pipeline.cpp:417-439: report.json, plan.json, solution_compressed.glr1,
+    decoded.glr1 + decoded.csv (when decoded), factors.glr1 (approximate
+    decoder), labels.csv (clustering tasks), objective.csv.  Device results
+    are written straight from HBM (GLR1 through pinned buffers)."""
+    os.makedirs(out_dir, exist_ok=True)
+    with open(os.path.join(out_dir, "report.json"), "w") as f:
+        f.write(report_to_json(rep, cfg, True) + "\n")
+    save_plan(rep.plan, os.path.join(out_dir, "plan.json"))
+    save_matrix(rep.Xt, os.path.join(out_dir, "solution_compressed.glr1"), ctx=ctx)
+    if rep.X is not None:
+        save_matrix(rep.X, os.path.join(out_dir, "decoded.glr1"), ctx=ctx)
+        save_matrix(rep.X, os.path.join(out_dir, "decoded.csv"), format="csv")
+    if rep.has_factors and rep.factors is not None:
+        save_factors(rep.factors, os.path.join(out_dir, "factors.glr1"), ctx=ctx)
+    if rep.labels is not None:
+        save_labels_csv(rep.labels, os.path.join(out_dir, "labels.csv"))
+    with open(os.path.join(out_dir, "objective.csv"), "w") as f:
+        f.write("iteration,objective\n")
+        for i, v in enumerate(rep.trace.objective):
+            f.write(f"{i + 1},{_g17(float(v))}\n")

@@ -114,3 +114,28 @@ def test_factors_round_trip(P, ctx, tmp_path):
     g = str(tmp_path / "f.glr1")
     P.save_factors(f, g, ctx=ctx)
     assert open(g, "rb").read() == open(_g("factors_4x3_k2.glr1"), "rb").read()
+
+
+def test_emit_report_artifacts(P, ctx, tmp_path):
+    """pipeline.cpp:417-439: the artifact set of a run, written from HBM."""
+    import json
+
+    from paper_1602_02070_b200.workloads import config0
+
+    Y, _ = config0(seed=1602, small=True)
+    cfg = P.PipelineConfig(knn=10, a=4, b=4, frpcag=P.FrpcagConfig(gamma_r=9.0, gamma_c=9.0, tol=1e-300, max_iter=20),
+                           decoder=P.DecoderConfig(1.0, 1e-8, 100, variant="alternate"), lambda_k1_r=0.05,
+                           lambda_k1_c=0.07, seed=1602, task="both", n_clusters=2, kmeans_restarts=2)
+    rep = P.run_pipeline(Y, cfg, ctx=ctx)
+    out = str(tmp_path / "run")
+    P.emit_report(rep, cfg, out, ctx=ctx)
+    names = sorted(os.listdir(out))
+    assert names == ["decoded.csv", "decoded.glr1", "labels.csv", "objective.csv", "plan.json", "report.json",
+                     "solution_compressed.glr1"]
+    j = json.load(open(os.path.join(out, "report.json")))
+    assert j["solve"]["iterations"] == 20 and len(j["solve"]["objective"]) == 20 and "timings_ms" in j
+    _, X = glr1.read(open(os.path.join(out, "decoded.glr1"), "rb").read())
+    assert np.array_equal(X, rep.X)
+    assert np.array_equal(P.load_labels_csv(os.path.join(out, "labels.csv")), rep.labels)
+    assert list(P.load_plan(os.path.join(out, "plan.json")).omega_c) == list(rep.plan.omega_c)
+    assert open(os.path.join(out, "objective.csv")).readline() == "iteration,objective\n"
