@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(256) fista_dense_objective_k(i64 rr, i64 rc, c
 // and the last CTA of the tile (per-tile arrival counter) sums the S partials
 // in s order (deterministic) and runs the epilogue.
 struct SplitWs {
-  float* part1;        // S x m partial (Lr Z)
-  float* part2;        // S x m partial (Z Lc)
+  double* part1;       // S x m partial (Lr Z), fp64 (see splitk_gemm)
+  double* part2;       // S x m partial (Z Lc)
   unsigned* tile_cnt;  // tiles
   unsigned* done_cnt;  // 1
   double* tile_sums;   // 3 x tiles (objective)
@@ -297,7 +297,7 @@ constexpr int kSK = 16;  // k chunk
 template <bool kLeft>
 __device__ __forceinline__ void splitk_gemm(const float* __restrict__ A, i64 lda, i64 arows,
                                             const float* __restrict__ B, i64 ldb, i64 bcols, i64 ka, i64 kb,
-                                            i64 i0, i64 c0, float (&acc)[4][4]) {
+                                            i64 i0, i64 c0, double (&acc)[4][4]) {
   // kLeft:  acc += Lr[i, k] * Z[k, c]   (A = Lr dense col-major rr x rr, B = Z)
   // !kLeft: acc += Z[i, k] * Lc[k, c]   (A = Z, B = Lc dense col-major)
   __shared__ float As[kSK][kST + 1];
@@ -324,7 +324,8 @@ __device__ __forceinline__ void splitk_gemm(const float* __restrict__ A, i64 lda
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(av[a], bv[b], acc[a][b]);
+        for (int b = 0; b < 4; ++b)
+          acc[a][b] = fma(static_cast<double>(av[a]), static_cast<double>(bv[b]), acc[a][b]);
     }
     __syncthreads();
   }
@@ -332,12 +333,12 @@ __device__ __forceinline__ void splitk_gemm(const float* __restrict__ A, i64 lda
 
 __device__ __forceinline__ void splitk_partial(const float* __restrict__ Lr, const float* __restrict__ Lc,
                                                const float* __restrict__ Z, i64 rr, i64 rc, int use_r,
-                                               int use_c, i64 i0, i64 c0, i64 ka, i64 kb, float (&acc1)[4][4],
-                                               float (&acc2)[4][4]) {
+                                               int use_c, i64 i0, i64 c0, i64 ka, i64 kb, double (&acc1)[4][4],
+                                               double (&acc2)[4][4]) {
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc1[a][b] = acc2[a][b] = 0.f;
+    for (int b = 0; b < 4; ++b) acc1[a][b] = acc2[a][b] = 0.0;
   if (use_r && ka < rr) splitk_gemm<true>(Lr, rr, rr, Z, rr, rc, ka, min(kb, rr), i0, c0, acc1);
   if (use_c && kb > rr) splitk_gemm<false>(Z, rr, rr, Lc, rc, rc, max(ka, rr) - rr, kb - rr, i0, c0, acc2);
 }
@@ -351,12 +352,12 @@ __global__ void __launch_bounds__(256) fista_splitk_partial_k(i64 rr, i64 rc, co
   const int Sn = gridDim.z;
   const i64 ktot = rr + rc, ka = (ktot * blockIdx.z) / Sn, kb = (ktot * (blockIdx.z + 1)) / Sn;
   const i64 i0 = static_cast<i64>(blockIdx.x) * kST, c0 = static_cast<i64>(blockIdx.y) * kST;
-  float acc1[4][4], acc2[4][4];
+  double acc1[4][4], acc2[4][4];
   splitk_partial(Lr, Lc, Z, rr, rc, use_r, use_c, i0, c0, ka, kb, acc1, acc2);
   const i64 m = rr * rc;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  float* p1 = ws.part1 + static_cast<i64>(blockIdx.z) * m;
-  float* p2 = ws.part2 + static_cast<i64>(blockIdx.z) * m;
+  double* p1 = ws.part1 + static_cast<i64>(blockIdx.z) * m;
+  double* p2 = ws.part2 + static_cast<i64>(blockIdx.z) * m;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -369,13 +370,15 @@ __global__ void __launch_bounds__(256) fista_splitk_partial_k(i64 rr, i64 rc, co
     }
 }
 
+// Sum of the split partials in split order, in fp64, rounded once to fp32.
 __device__ __forceinline__ void splitk_sum(const SplitWs& ws, i64 m, int S, i64 e, float& x1, float& x2) {
-  x1 = 0.f;
-  x2 = 0.f;
+  double s1 = 0.0, s2 = 0.0;
   for (int q = 0; q < S; ++q) {
-    x1 += ws.part1[static_cast<i64>(q) * m + e];
-    x2 += ws.part2[static_cast<i64>(q) * m + e];
+    s1 += ws.part1[static_cast<i64>(q) * m + e];
+    s2 += ws.part2[static_cast<i64>(q) * m + e];
   }
+  x1 = static_cast<float>(s1);
+  x2 = static_cast<float>(s2);
 }
 
 __global__ void fista_splitk_grad_prox_k(i64 rr, i64 rc, int S, float s_r, float s_c, int use_r, int use_c, int loss,
@@ -726,7 +729,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   }
   // fp32: split the k-space so the grid covers ~6 CTAs per SM.
   const bool splitk = dense && sizeof(T) == 4;
-  DevBuf<float> sp1, sp2;
+  DevBuf<double> sp1, sp2;
   DevBuf<unsigned> scnt;
   DevBuf<double> ssum;
   SplitWs ws{};

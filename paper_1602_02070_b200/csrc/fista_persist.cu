@@ -102,14 +102,18 @@ __device__ __forceinline__ void ld4v(const double* p, double (&v)[4]) {
   v[2] = y.x;
   v[3] = y.y;
 }
-__device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
-__device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
+
 
 // acc += sum over cnt k-steps of a(k) b(k)^T, a/b 4-value strips at strides
-// sa/sb, k ascending.  (Prefetching the operands four k-steps ahead measured
-// slower: the loop is bound by shared-memory wavefronts, ncu: 4.4 per LDS.128.)
+// sa/sb, k ascending, accumulated in fp64 for either storage precision: the
+// products of fp32 operands are exact in fp64, and H = g L~ S sums ~1e3
+// terms of magnitude up to ~1e4 that cancel to O(10) (Laplacian rows sum to
+// zero), so an fp32 accumulator left ~4e-4 relative error in the config-1
+// FISTA output after 300 iterations (above the 1e-4 bar; fp64: 1e-6).
+// (Prefetching the operands four k-steps ahead measured slower: the loop is
+// bound by shared-memory wavefronts, ncu: 4.4 per LDS.128.)
 template <typename T>
-__device__ __forceinline__ void strip_gemm(T (&acc)[4][4], const T* ap, int sa, const T* bp, int sb, int cnt) {
+__device__ __forceinline__ void strip_gemm(double (&acc)[4][4], const T* ap, int sa, const T* bp, int sb, int cnt) {
 #pragma unroll 4
   for (int q = 0; q < cnt; ++q) {
     T av[4], bv[4];
@@ -118,7 +122,8 @@ __device__ __forceinline__ void strip_gemm(T (&acc)[4][4], const T* ap, int sa, 
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = fma_t(av[x], bv[y], acc[x][y]);
+      for (int y = 0; y < 4; ++y)
+        acc[x][y] = fma(static_cast<double>(av[x]), static_cast<double>(bv[y]), acc[x][y]);
   }
 }
 
@@ -166,7 +171,8 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   constexpr int NST = MODE == 0 ? 2 : 4;
   extern __shared__ __align__(16) double smd[];
   double* psm = smd;  // [kPsm] partial sums of the previous iteration (4 per CTA)
-  T* sm = reinterpret_cast<T*>(smd + kPsm);
+  double* red = smd + kPsm;  // [KS][TE] split-k partial tiles (fp64; MODE 1: KS = 1)
+  T* sm = reinterpret_cast<T*>(red + static_cast<size_t>(a.KS) * a.TM * a.TN);
   __shared__ double tot_sh[4];
   const int G = gridDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int TM = a.TM, TN = a.TN, TE = TM * TN, rr = a.rr, rc = a.rc, KC = a.KC, KS = a.KS;
@@ -178,8 +184,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   T* Bc = As + static_cast<size_t>(rr) * ldA;      // [rc][ldB]  g_c L~_c(k, c0 + j)
   T* A2 = Bc + static_cast<size_t>(rc) * ldB;      // [rc][ldA]  S(r0 + i, k)
   T* Bb = A2 + static_cast<size_t>(rc) * ldA;      // [2][KC][ldB]  S(k, c0 + j)
-  T* red = Bb + NST * static_cast<size_t>(KC) * ldB;  // [KS][TE]  split-k partials (MODE 1: KS = 1)
-  T* Yt = red + static_cast<size_t>(KS) * TE;     // tile state, e = i + TM j
+  T* Yt = Bb + NST * static_cast<size_t>(KC) * ldB;  // tile state, e = i + TM j
   T* Zt = Yt + TE;                                // Z_j
   T* HZ = Zt + TE;                                // H(Z_j)
   T* Sp = HZ + TE;                                // S_{j-1}
@@ -221,12 +226,12 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   const int mi8 = warp % max(TM / 8, 1), ni8 = warp / max(TM / 8, 1);
   const bool w8 = MODE == 1 && warp < (TM / 8) * (TN / 8);
   auto tile_gemm = [&](const T* Sbuf, const T* SbufT) {
-    T acc[4][4];
+    double acc[4][4];
     float acc8[MODE == 1 ? 64 : 1];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = T(0);
+      for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
 #pragma unroll
     for (int q = 0; q < (MODE == 1 ? 64 : 1); ++q) acc8[q] = 0.f;
     const int q4m = TM / EPC, q4n = TN / EPC;
@@ -285,7 +290,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
         strip_gemm(acc, A2 + s * ldA + 4 * mi, KS * ldA, Bc + s * ldB + 4 * ni, KS * ldB, cnt);
       }
       if (gthr) {
-        T* o = red + static_cast<size_t>(s) * TE;
+        double* o = red + static_cast<size_t>(s) * TE;
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -297,7 +302,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
           for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
         reduce_scatter64(acc8, lane);  // lane now holds entries 2 lane, 2 lane + 1 of the micro-tile
         const int x = lane >> 2, y = (2 * lane) & 7;
-        T* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
+        double* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
         o[0] = acc8[0];
         o[TM] = acc8[1];
       }
@@ -305,9 +310,9 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
     __syncthreads();
   };
   auto tile_h = [&](int e) {
-    T h = T(0);
+    double h = 0.0;
     for (int q = 0; q < KS; ++q) h += red[q * TE + e];
-    return h;
+    return static_cast<T>(h);
   };
 
   // ---- H(Y): Z_1 = S_0 = Y, so H(Z_1) = H(S_0)
@@ -461,8 +466,9 @@ struct Geom {
 
 size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst, size_t w = 4) {
   const size_t TE = static_cast<size_t>(TM) * TN;
-  return 8 * kPsm + w * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
-              static_cast<size_t>(nst) * KC * ldB + static_cast<size_t>(KS) * TE + 6 * TE);
+  return 8 * kPsm + 8 * static_cast<size_t>(KS) * TE +
+         w * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
+              static_cast<size_t>(nst) * KC * ldB + 6 * TE);
 }
 
 // MODE 1 (preferred): TM, TN multiples of 8, one warp per 8 x 8 micro-tile

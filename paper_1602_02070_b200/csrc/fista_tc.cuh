@@ -23,6 +23,6 @@ void fista_tc_setup(Ctx* c, i64 rr, i64 rc, int S, const float* Lr_dense, float*
                     FistaTcPlan* pl);
 // part1[s] = L~_r Z over the s-th k slice (Z split into Zh/Zl first); skipped
 // when *done.
-void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, float* Zl, float* part1, const int* done);
+void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, float* Zl, double* part1, const int* done);
 
 }  // namespace cpcag_cuda

@@ -877,7 +877,7 @@ template <int NP>
 __global__ void __launch_bounds__(128, 1)
     fista_tc_part1_k(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, i64 rr, i64 rc,
-                     int nkc, float* __restrict__ part1, const int* __restrict__ done) {
+                     int nkc, double* __restrict__ part1, const int* __restrict__ done) {
   using namespace tc;
   constexpr int kA = 128 * 128;          // 128 rows x 128 B
   constexpr int kB = NP * 128;           // NP rows x 128 B
@@ -933,7 +933,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncwarp();
   const i64 i = i0 + 32 * warp + lane;
   const i64 m = rr * rc;
-  float* out = part1 + static_cast<i64>(s) * m;
+  double* out = part1 + static_cast<i64>(s) * m;
   if (nch > 0) {
     tc2::mbar_wait_guarded(&mdone, 0);
     fence_after();
@@ -1000,7 +1000,7 @@ void fista_tc_setup(Ctx* c, i64 rr, i64 rc, int S, const float* Lr_dense, float*
   pl->mBl = kmajor_map(Zl, rc, rr, pl->ld, pl->np);
 }
 
-void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, float* Zl, float* part1, const int* done) {
+void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, float* Zl, double* part1, const int* done) {
   dim3 g(blocks_for(pl.ld), static_cast<unsigned>(std::min<i64>(pl.rc, 65535)));
   split_cols_tf32_k<<<g, kBlock, 0, c->stream>>>(pl.rr, pl.rc, Z, pl.rr, pl.ld, Zh, Zl);
   launched(c);

@@ -218,3 +218,35 @@ def test_knn_second_tensor_core_pass_equals_exact_path(P, ctx, monkeypatch, capf
     rows = np.random.default_rng(11).choice(n, 24, replace=False)
     onbr, od2 = O.knn_rows(X.astype(np.float64), False, 10, rows)
     assert np.array_equal(nbr[rows], onbr) and np.array_equal(d2[rows], od2)
+
+
+def test_cfg1_pipeline_full_iterations_within_north_star(P, ctx):
+    """The headline configuration end to end at its full iteration counts
+    (FISTA 300, CG 200; fp32 on the device) against the fp64 oracle composite:
+    relative Frobenius error of Xt and X <= 1e-4 (north_star).  ~1 min of
+    oracle time on the box's cores."""
+    import torch
+
+    from paper_1602_02070_b200 import workloads
+
+    wl = workloads.config1()
+    p, n = wl.Y.shape
+    cfg = P.PipelineConfig(knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
+                           frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
+                                                 max_iter=wl.fista_iters),
+                           decoder=P.DecoderConfig(1.0, 1e-30, wl.cg_iters, variant="alternate"),
+                           lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1603)
+    Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=torch.float32, device="cuda").t()
+    rep = P.run_pipeline(Yd, cfg, W_r=P.SparseMatrix.from_scipy(wl.W_r, ctx=ctx), ctx=ctx)
+    assert rep.trace.iterations == 300 and rep.decoder_iterations == 200
+    Y = wl.Y.astype(np.float32).astype(np.float64)
+    gr = O.graph_from_adjacency(O.Csr.from_scipy(wl.W_r))
+    gc = O.build_knn_graph(Y, False, 10)
+    plan = O.draw_plan(p, n, -(-p // wl.b), -(-n // wl.a), seed=1603)
+    Xt, tr = O.fista_solve(O.subsample(Y, plan), O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11),
+                           O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11),
+                           O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, 300))
+    assert rel(rep.Xt.cpu().numpy(), Xt) <= 1e-4
+    assert np.allclose(rep.trace.objective, tr.objective, rtol=1e-4)
+    dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, 200)
+    assert rel(rep.X.cpu().numpy(), dec.X) <= 1e-4
