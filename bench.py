@@ -719,7 +719,7 @@ def run_cfg3(args):
     plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
     A = torch.tensor(rs.standard_normal((20, 20)), device="cuda")
     Xt = (Br[torch.tensor(plan.omega_r, device="cuda")] @ A @ Bc[torch.tensor(plan.omega_c, device="cuda")].T)
-    Xt = Xt.float().t().contiguous().t()
+    Xt = (Xt if args.fp64 else Xt.float()).t().contiguous().t()
     g1 = P.SpectralGap(lambda_k1=1.0)
     dcfg = P.DecoderConfig(1.0, 1e-30, 100)
     ctx.reset_kernel_timing()
@@ -739,26 +739,29 @@ def run_cfg3(args):
     # Algorithmic HBM bytes per CG iteration: apply reads P and writes AP
     # (2N), residual reads R, AP and writes R (3N), update reads X, P, R and
     # writes X, P (5N); plus one pass over both Laplacians.
-    b_iter = 10 * N * 4 + (nnz_r + nnz_c) * 8
+    wb = 8 if args.fp64 else 4
+    b_iter = 10 * N * wb + (nnz_r + nnz_c) * (wb + 4)
     peak, src = measured_peaks()
-    kbytes = {"cg_apply": 2 * N * 4 + (nnz_r + nnz_c) * 8,
-              "cg_apply_band": 2 * N * 4 + nnz_c * 8,      # P read once, U written
-              "cg_apply_col": 3 * N * 4 + nnz_r * 8,       # P, U read; AP written
-              "cg_residual": 3 * N * 4, "cg_update": 5 * N * 4}
+    kbytes = {"cg_apply": 2 * N * wb + (nnz_r + nnz_c) * (wb + 4),
+              "cg_apply_band": 2 * N * wb + nnz_c * (wb + 4),      # P read once, U written
+              "cg_apply_col": 3 * N * wb + nnz_r * (wb + 4),       # P, U read; AP written
+              "cg_residual": 3 * N * wb, "cg_update": 5 * N * wb}
     kgbps = {k: round(kbytes[k] / (v[1] / v[0] / 1e3) / 1e9, 1) for k, v in kt.items() if k in kbytes}
     out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f32",
+           "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",
            "data": "synthetic: seeded config-3 generator (N(0,I_64) points, rank-20 low-pass basis)",
            "config": {"workload": f"cfg3: alternate CG decoder, p={p}, n={n}, 1/8 x 1/8 sampling, {it} iterations",
                       "graphs_s_untimed": round(t_graphs, 3),
-                      "l2": "iterates (3.3 GB each) larger than L2; no flush"},
+                      "l2": "iterates (%.1f GB each) larger than L2; no flush" % (N * wb / 1e9)},
            "clocks": clk,
            "iters_per_s": round(it / (ms / 1e3), 1),
-           "cg_iteration_survey": {"bytes_B_iter": 6 * N * 4 + (nnz_r + nnz_c) * 8,
+           "cg_iteration_survey": {"bytes_B_iter": 6 * N * wb + (nnz_r + nnz_c) * (wb + 4),
                                    "model": "SURVEY 8(d): 6 N w + (nnz_r + nnz_c)(w + 4)",
-                                   "achieved_GBps": round((6 * N * 4 + (nnz_r + nnz_c) * 8) * it / (ms / 1e3) / 1e9, 1),
-                                   "frac_of_hbm": round((6 * N * 4 + (nnz_r + nnz_c) * 8) * it / (ms / 1e3) / 1e9 / peak,
+                                   "achieved_GBps": round((6 * N * wb + (nnz_r + nnz_c) * (wb + 4)) * it / (ms / 1e3) / 1e9,
+                                                          1),
+                                   "frac_of_hbm": round((6 * N * wb + (nnz_r + nnz_c) * (wb + 4)) * it / (ms / 1e3) / 1e9
+                                                        / peak,
                                                         4)},
            "cg_iteration": {"bytes_B_iter": b_iter, "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
                             "frac_of_hbm": round(b_iter * it / (ms / 1e3) / 1e9 / peak, 4), "peak_source": src},

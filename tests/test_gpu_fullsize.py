@@ -262,10 +262,11 @@ def test_cfg3_decoder_fp32_against_fp64(P, ctx):
     on this system (gamma-bar = 1, 1/64 of the entries in the mask) is far
     from converged after 100 iterations, and the fp32 recurrence (X, R, P
     rounded at 6e-8 per step) drifts from the fp64 one; accumulating the
-    applies in fp64 only moved it to 7.2e-4 (and cost 9 %), so the fix is
-    fp64 iterates (a mixed-precision CG), not a more accurate apply.  The
-    bound below records the measured state; the config-1 decoder (a
-    better-conditioned system) is within 3e-6 of the oracle."""
+    applies in fp64 only moved it to 7.2e-4, and fp64 iterates with fp32
+    applies (tools/mixed_cg_experiment.py) to 1.05e-3: CG amplifies the fp32
+    operator's perturbation.  The bound below records the measured state;
+    the fp64 decoder is the parity path at this size, and the config-1
+    decoder (a better-conditioned system) is within 3e-6 of the oracle."""
     import torch
 
     from paper_1602_02070_b200 import workloads
