@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="compute in fp64 (config 1 is fp32)")
+    ap.add_argument("--krylov", choices=["fp64", "fp32"], default="fp64",
+                    help="decoder Krylov vectors for fp32 data (fp64: the path that meets 1e-4 at every config)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="cfg3 through the column-sharded decoder over NCCL (one column block per rank)")
@@ -200,43 +202,45 @@ def make_workload():
     return workloads.config1()
 
 
-def pipeline_config(P, wl):
+def pipeline_config(P, wl, krylov="fp64"):
     return P.PipelineConfig(
         knn=10, a=wl.a, b=wl.b, kron_pcg_tol=1e-11,
         frpcag=P.FrpcagConfig(gamma_r=wl.gamma, gamma_c=wl.gamma, loss="l1", tol=1e-300,
                               max_iter=wl.fista_iters),
-        decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-30, pcg_max_iter=wl.cg_iters, variant="alternate"),
+        decoder=P.DecoderConfig(gamma=1.0, pcg_tol=1e-30, pcg_max_iter=wl.cg_iters, variant="alternate",
+                                krylov_precision=krylov),
         lambda_k1_r=wl.lambda_k1_r, lambda_k1_c=wl.lambda_k1_c, seed=1603)
 
 
 KERNEL_BYTES_DOC = {
-    "cg_apply": "read P + write AP (2 N w) + one read of L_r and L_c (nnz (w+4) + 8 (rows+1))",
-    "cg_residual": "read R, AP + write R (3 N w)",
-    "cg_update": "read X, P, R + write X, P (5 N w)",
-    "fista_grad_prox": "read Z, Y + write S (3 m w) + L~_r, L~_c once",
-    "fista_objective": "read S, Y (2 m w) + L~_r, L~_c once",
-    "fista_momentum": "read S, S_prev, Z + write Z_next (4 m w)",
-    "pcg_apply": "read P + write AP (2 |int| b 8) + L_aa once",
-    "pcg_update": "read X, R, P, AP + write X, R, Z (7 |int| b 8)",
-    "pcg_direction": "read Z, P + write P (3 |int| b 8)",
+    "cg_apply_lc": "read P + write U (2 N wk) + one read of L_c (nnz_c (wv + 4))",
+    "cg_apply_lr": "read P, U + write AP (3 N wk) + one read of L_r (nnz_r (wv + 4))",
+    "cg_residual": "read R, AP + write R (3 N wk)",
+    "cg_update": "read X, P, R + write X, P (2 N wx + 3 N wk)",
+    "fista_persist": "FLOP-bound (2 (rho_r^2 rho_c + rho_r rho_c^2) per iteration)",
+    "pcg_persistent": "Kron interior solves (HBM; SURVEY 8(d))",
 }
 
 
-def kernel_bytes(tag, dims, w):
-    N, m, nnz_r, nnz_c, nnz_rt, nnz_ct, p, n, rr, rc = (dims[k] for k in (
-        "N", "m", "nnz_r", "nnz_c", "nnz_rt", "nnz_ct", "p", "n", "rho_r", "rho_c"))
-    if tag == "cg_apply":
-        return 2 * N * w + (nnz_r + nnz_c) * (w + 4) + 8 * (p + n + 2)
+def decoder_widths(fp64: bool, krylov: str):
+    """(wk, wx, wv): bytes per Krylov-vector entry, per X entry and per
+    operator value of the decoder (decoder.cu's precision policy)."""
+    if fp64:
+        return 8, 8, 8
+    return (4, 4, 4) if krylov == "fp32" else (8, 4, 4)
+
+
+def kernel_bytes(tag, dims, widths):
+    wk, wx, wv = widths
+    N, nnz_r, nnz_c = dims["N"], dims["nnz_r"], dims["nnz_c"]
+    if tag == "cg_apply_lc":
+        return 2 * N * wk + nnz_c * (wv + 4)
+    if tag == "cg_apply_lr":
+        return 3 * N * wk + nnz_r * (wv + 4)
     if tag == "cg_residual":
-        return 3 * N * w
+        return 3 * N * wk
     if tag == "cg_update":
-        return 5 * N * w
-    if tag == "fista_grad_prox":
-        return 3 * m * w + (nnz_rt + nnz_ct) * (w + 4) + 8 * (rr + rc + 2)
-    if tag == "fista_objective":
-        return 2 * m * w + (nnz_rt + nnz_ct) * (w + 4) + 8 * (rr + rc + 2)
-    if tag == "fista_momentum":
-        return 4 * m * w
+        return 2 * N * wx + 3 * N * wk
     return None
 
 
@@ -255,7 +259,7 @@ def run_ours(args, rank, local_rank, world):
     p, n = wl.Y.shape
     prec_np = np.float64 if args.fp64 else np.float32
     tdt = torch.float64 if args.fp64 else torch.float32
-    w = 8 if args.fp64 else 4
+    widths = decoder_widths(args.fp64, args.krylov)
     ctx = P.Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
@@ -266,7 +270,7 @@ def run_ours(args, rank, local_rank, world):
     Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=tdt, device="cuda").t()  # col-major p x n
     Wr_sp = wl.W_r
     Wr_dev = P.SparseMatrix.from_scipy(Wr_sp, ctx=ctx)
-    cfg = pipeline_config(P, wl)
+    cfg = pipeline_config(P, wl, args.krylov)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     # operator sizes for the roofline accounting (untimed setup)
@@ -352,7 +356,7 @@ def run_ours(args, rank, local_rank, world):
     if top and top in live:
         nl, tot = live[top]
         avg_ms = tot / nl
-        by = kernel_bytes(top, dims, w)
+        by = kernel_bytes(top, dims, widths)
         prof_total = sum(v[1] for v in prof.values())
         share = prof[top][1] / prof_total if prof_total else None
         traffic = None
@@ -369,20 +373,19 @@ def run_ours(args, rank, local_rank, world):
                     "algorithmic_bytes_per_launch": by, "bytes_model": KERNEL_BYTES_DOC.get(top),
                     "avg_launch_ms": round(avg_ms, 5), "launches_timed": nl, "share_of_step": share,
                     "peak_source": peak_src}
-            if top == "cg_apply":
-                roof["note"] = ("the config-1 iterate (41 MB fp32) is L2-resident: the apply is bound by the L2 "
-                                "bandwidth of its ~19 L_c gathers per entry and the L1-miss latency of the L_r "
-                                "stencil (ncu: long-scoreboard 54 %), not by HBM; the HBM-bound CG kernels are in "
-                                "kernel_roofline")
+            if top.startswith("cg_apply"):
+                roof["note"] = ("the config-1 Krylov vectors (82 MB fp64) are mostly L2-resident: the decoder passes "
+                                "are bound by on-chip gathers (~19 L_c and 9 L_r per entry), not by HBM")
     # CG iteration as a whole (survey B_iter = 6 N w + (nnz_r + nnz_c)(w + 4))
-    cg_iter_bytes = 6 * p * n * w + (nnz_r + nnz_c) * (w + 4)
+    wk, wx, wv = widths
+    cg_iter_bytes = 4 * p * n * wk + 2 * p * n * wx + (nnz_r + nnz_c) * (wv + 4)
     kernel_share = {k: round(v[1] / sum(x[1] for x in prof.values()), 4) for k, v in prof.items()} if prof else {}
     # every HBM-model kernel of the profiled step: algorithmic bytes / average
     # launch time against the measured copy peak (the dominant kernel above is
     # timed live; these come from the untimed profiled step)
     kernel_roofline = {}
     for tag, (nl, tot) in (prof or {}).items():
-        by = kernel_bytes(tag, dims, w)
+        by = kernel_bytes(tag, dims, widths)
         if by is None or nl == 0 or tot <= 0:
             continue
         gbs = by / (tot / nl / 1e3) / 1e9
@@ -460,89 +463,118 @@ def run_ours(args, rank, local_rank, world):
 
 
 # ------------------------------------------------------------------ CPU side
-def cpu_sample_times(wl, fista_iters=4, cg_iters=3):
-    """Time the oracle port on config 1: every stage in full except FISTA and
-    the decoder, which run a few iterations and are extrapolated linearly."""
+def host_info():
+    """CPU model, logical cores and RAM of the machine the CPU leg runs on."""
+    model, ram = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "ram_gib": ram}
+
+
+def cpu_full_run(wl, threads=None):
+    """The whole config-1 CPCA on the oracle port (the CPU restatement of the
+    reference's loops, pipeline.cpp:273-350): graphs, plan, subsample, Kron,
+    FRPCAG (both power iterations + 300 FISTA iterations) and the alternate
+    decoder (200 CG iterations), nothing extrapolated.  Returns (seconds,
+    stage seconds)."""
     from oracle import pyoracle as O
 
+    if threads is not None:
+        O.set_threads(threads)
     Y = np.asfortranarray(wl.Y.astype(np.float32).astype(np.float64))
     p, n = Y.shape
     t = {}
     t0 = time.perf_counter()
     gc = O.build_knn_graph(Y, False, 10)
-    Wr = O.Csr.from_scipy(wl.W_r)
-    gr = O.graph_from_adjacency(Wr)
+    gr = O.graph_from_adjacency(O.Csr.from_scipy(wl.W_r))
     t["graphs"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     plan = O.draw_plan(p, n, -(-p // wl.b), -(-n // wl.a), seed=1603)
-    t["plan"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
     Yt = O.subsample(Y, plan)
-    t["subsample"] = time.perf_counter() - t0
+    t["plan+subsample"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     Lrt = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
     Lct = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
     t["kron"] = time.perf_counter() - t0
-    # the step's two power iterations (frpcag.cpp:70-75) run once per solve:
-    # timed in full, then the sampled FISTA iterations reuse the step
     t0 = time.perf_counter()
-    beta = (2.0 * wl.gamma * O.power_iteration_norm(Lct, 1e-7, 42, 50000) +
-            2.0 * wl.gamma * O.power_iteration_norm(Lrt, 1e-7, 42, 50000))
-    t["power"] = time.perf_counter() - t0
+    Xt, tr = O.fista_solve(Yt, Lrt, Lct, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, wl.fista_iters))
+    t["solve"] = time.perf_counter() - t0
     t0 = time.perf_counter()
-    Xt, tr = O.fista_solve(Yt, Lrt, Lct, O.FrpcagConfig(wl.gamma, wl.gamma, "l1", 1e-300, fista_iters,
-                                                         step=1.0 / beta))
-    t["solve_sample"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30, cg_iters)
-    t["decode_sample"] = time.perf_counter() - t0
-    full = (t["graphs"] + t["plan"] + t["subsample"] + t["kron"] + t["power"] +
-            t["solve_sample"] / fista_iters * wl.fista_iters + t["decode_sample"] / cg_iters * wl.cg_iters)
-    return full, t
+    dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, wl.lambda_k1_r, wl.lambda_k1_c, 1.0, 1e-30,
+                             wl.cg_iters)
+    t["decode"] = time.perf_counter() - t0
+    assert tr.iterations == wl.fista_iters and dec.iterations == wl.cg_iters
+    return sum(t.values()), t
 
 
 def cpu_baseline(wl):
+    """One full oracle-port run of config 1 on all host threads (kind "port":
+    the reference itself needs Eigen3, absent)."""
     from oracle import pyoracle as O
 
+    O.set_threads(os.cpu_count() or 1)
     cores = O.get_threads()
-    full, t = cpu_sample_times(wl)
+    full, t = cpu_full_run(wl)
     return {"value": round(full, 3), "unit": "s", "cores": cores, "kind": "port",
-            "sample": "oracle port on config 1: graphs, plan, subsample, Kron and the step's power iterations in "
-                      "full; FRPCAG 4 of 300 and decoder 3 of 200 iterations timed and extrapolated linearly "
-                      f"(stage seconds {json.dumps({k: round(v, 3) for k, v in t.items()})})"}
+            "sample": "the whole config-1 CPCA once on the oracle port (graphs, plan, Kron, FRPCAG 300 it, decoder "
+                      f"200 it; nothing extrapolated); stage seconds {json.dumps({k: round(v, 3) for k, v in t.items()})}",
+            "host": host_info()}
 
 
 def run_reference(args, rank, world):
+    """The reference arm: the oracle port (the reference's loops restated
+    without Eigen, which is absent here) runs the full config-1 CPCA on all
+    host threads every step; one extra single-thread run (the reference is
+    single-threaded) is reported beside it."""
     if world > 1 and rank != 0:
         return
     from oracle import pyoracle as O
 
     O.lib()
     wl = make_workload()
-    cores = O.get_threads()
-    for _ in range(args.warmup):
-        cpu_sample_times(wl, 1, 1)
-    vals = []
+    allc = os.cpu_count() or 1
+    O.set_threads(allc)
+    for _ in range(min(args.warmup, 1)):  # a CPU needs no more than one warm-up (page-ins, allocator)
+        cpu_full_run(wl)
+    vals, stages = [], None
     t_all0 = time.perf_counter()
-    last = None
     for _ in range(args.steps):
-        full, t = cpu_sample_times(wl)
+        full, stages = cpu_full_run(wl)
         vals.append(full)
-        last = t
     t_all1 = time.perf_counter()
+    single = None
+    if not os.environ.get("BENCH_NO_SINGLE_THREAD"):
+        s1, st1 = cpu_full_run(wl, threads=1)
+        single = {"value": round(s1, 3), "unit": "s", "cores": 1,
+                  "stage_s": {k: round(v, 3) for k, v in st1.items()}}
+        O.set_threads(allc)
     v = sum(vals) / len(vals)
-    sample = ("oracle port (CPU restatement of the reference; the reference needs Eigen3, absent) on config 1: "
-              "graphs, plan, subsample, Kron and the step's power iterations in full; FRPCAG 4/300 and decoder "
-              "3/200 iterations per step, extrapolated linearly to the full run")
+    sample = ("oracle port (CPU restatement of the reference; the reference needs Eigen3, absent): the whole config-1 "
+              "CPCA per step (graphs, plan, Kron, FRPCAG 300 it, decoder 200 it), nothing extrapolated, "
+              f"{allc} threads")
     out = {"metric": METRIC, "value": round(v, 3), "unit": "s", "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1), "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded config-1 generator",
-           "config": {"workload": "cfg1: CPCA 10304x1000, pixel-grid W_r + kNN(K=10) L_c, a=b=10, "
-                                  "FRPCAG 300 it, alternate CG decoder 200 it", "parallelism": "cpu threads"},
+           "warmup": min(args.warmup, 1), "ms_per_step": round(v * 1e3, 1), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded config-1 generator",
+           "config": {"workload": "cfg1: CPCA 10304x1000, pixel-grid W_r + kNN(K=10) L_c, a=b=10 "
+                                  "(rho 1031x100), FRPCAG 300 it, alternate CG decoder 200 it",
+                      "parallelism": "cpu threads"},
            "impl": "reference",
-           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": cores, "kind": "port", "sample": sample,
-                            "last_step_stage_s": {k: round(x, 3) for k, x in last.items()}},
+           "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": O.get_threads(), "kind": "port",
+                            "sample": sample, "last_step_stage_s": {k: round(x, 3) for k, x in stages.items()},
+                            "single_thread": single, "host": host_info()},
            "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "step_s": [round(x, 3) for x in vals],
            "wall_s_timed_region": round(t_all1 - t_all0, 3)}
     print(json.dumps(out), flush=True)
     if args.json_out:

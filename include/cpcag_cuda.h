@@ -77,6 +77,11 @@ int cpcag_ctx_reserve(cpcag_ctx ctx, int64_t bytes);
 int cpcag_ctx_set_stream(cpcag_ctx ctx, void* cuda_stream);
 void* cpcag_ctx_stream(cpcag_ctx ctx);
 int cpcag_ctx_synchronize(cpcag_ctx ctx);
+/* Decoder operator path for this context (tests of both paths on small
+ * cases): 0 = automatic (one fused pass when the Krylov vectors fit in L2,
+ * else the two-pass band / row-group kernels), 1 = always two passes,
+ * 2 = fused whenever its shared-memory slice fits. */
+int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path);
 /* Number of kernels this context has launched since creation (or reset). */
 int64_t cpcag_ctx_launch_count(cpcag_ctx ctx);
 void cpcag_ctx_reset_launch_count(cpcag_ctx ctx);
@@ -205,6 +210,12 @@ typedef struct cpcag_decoder_config { /* DecoderConfig fields used by alternate_
   double gamma;         /* default 1; scaled by 1/lambda_{k+1} per side */
   double pcg_tol;       /* default 1e-10 */
   int64_t pcg_max_iter; /* default 5000 */
+  /* Extension (not in the reference): storage of the CG Krylov vectors R, P,
+   * AP for fp32 data.  0 (default): fp64 Krylov vectors, fp32 X -- within
+   * 1.3e-6 of the fp64 solve at config 3, where fp32 Krylov vectors drift
+   * 7-8e-4 (tools/cfg3_precision.py).  CPCAG_F32: every vector fp32 (faster;
+   * for well-conditioned systems).  Ignored for fp64 data. */
+  int krylov_precision;
 } cpcag_decoder_config;
 
 /* alternate_decode (decoders.hpp:59-62, decoders.cpp:145-186): CG on
@@ -218,6 +229,14 @@ int cpcag_cuda_alternate_decode(cpcag_ctx ctx, int precision, const void* Xt, in
                                 double lambda_k1_r, double lambda_k1_c,
                                 const cpcag_decoder_config* cfg, void* X, int* converged,
                                 int64_t* iterations);
+
+/* The decoder's operator (decoders.cpp:160-170): AP = gbar_c P Lc + gbar_r Lr P
+ * + M o P (M = the plan's sampling mask), *dot = <P, AP>; P and AP are p x n.
+ * The two kernels the CG runs per iteration (fp64: bit-identical per entry
+ * to the reference loop). */
+int cpcag_cuda_decoder_apply(cpcag_ctx ctx, int precision, const void* P, int64_t p, int64_t n, cpcag_csr Lr,
+                             cpcag_csr Lc, const int64_t* omega_r, int64_t rho_r, const int64_t* omega_c,
+                             int64_t rho_c, double gbar_r, double gbar_c, void* AP, double* dot);
 
 /* sym_eig (eigs.hpp:22, eigs.cpp:34-51): the k smallest eigenpairs of the
  * symmetric part 0.5 (A + A^T) of a CSR matrix, by a dense eigensolver on the
@@ -283,28 +302,54 @@ int cpcag_cuda_approx_decode(cpcag_ctx ctx, int precision, const void* Xt, int64
 int cpcag_cuda_gram_tf32x3(cpcag_ctx ctx, const double* P, int64_t n, int64_t d, float* G);
 
 /* ------------------------------------------------------------------ column-sharded decoder */
-/* Local primitives of the alternate decoder for one column block
- * [c_begin, c_end) of a column-sharded multi-GPU solve: the
- * caller all-gathers the search direction P between ranks (NCCL over
- * NVLink) and all-reduces the partial dot products; these functions do the
- * GPU-local work.  All matrices are device memory; P_full is p x n, blocks
- * are p x (c_end - c_begin), column-major.  gbar = gamma / lambda_k1. */
-typedef struct cpcag_decoder_block_s* cpcag_decoder_block;
-int cpcag_cuda_decoder_block_create(cpcag_ctx ctx, int precision, int64_t p, int64_t n, int64_t c_begin,
-                                    int64_t c_end, cpcag_csr Lr, cpcag_csr Lc, const int64_t* omega_r,
-                                    int64_t rho_r, const int64_t* omega_c, int64_t rho_c, double gbar_r,
-                                    double gbar_c, cpcag_decoder_block* out);
-int cpcag_cuda_decoder_block_destroy(cpcag_decoder_block b);
-/* B_block = scatter(Xt) restricted to the block; *sq_norm = ||B_block||^2. */
-int cpcag_cuda_decoder_block_rhs(cpcag_decoder_block b, const void* Xt, void* B_block, double* sq_norm);
-/* AP_block = (gbar_c P L_c + gbar_r L_r P + M o P)(:, block); *dot = <P_block, AP_block>. */
-int cpcag_cuda_decoder_block_apply(cpcag_decoder_block b, const void* P_full, void* AP_block, double* dot);
-/* R -= alpha AP over count entries; *rr = ||R||^2 (solvers.hpp:60-62). */
-int cpcag_cuda_cg_residual(cpcag_ctx ctx, int precision, int64_t count, double alpha, void* R, const void* AP,
-                           double* rr);
-/* X += alpha P; P = R + beta P (solvers.hpp:59,63). */
-int cpcag_cuda_cg_update(cpcag_ctx ctx, int precision, int64_t count, double alpha, double beta, void* X, void* P,
-                         const void* R);
+/* alternate_decode (decoders.cpp:145-186) split over the GPUs of one node by
+ * column blocks of X: one process per GPU, rank g owns
+ * columns [bounds[g], bounds[g+1]) (bounds: nranks + 1 ascending entries,
+ * bounds[0] = 0, bounds[nranks] = n, identical on every rank).  Per CG
+ * iteration the columns of the search direction that other ranks' L_c rows
+ * reference (the halo) move by one grouped ncclSend/ncclRecv, overlapped
+ * with the block-local L_r pass; the two CG dot products are ncclAllReduce'd
+ * on device scalars.  Xt, omega, Lr and Lc are replicated on every rank;
+ * X_block receives this rank's p x (bounds[g+1] - bounds[g]) block.  Entry
+ * arithmetic equals the one-GPU decoder's (fp64: bit-identical applies); only
+ * the dot products' summation order differs. */
+typedef struct cpcag_comm_s* cpcag_comm;
+typedef struct cpcag_shard_stats {
+  int64_t halo_cols;          /* columns of P this rank receives per iteration */
+  int64_t send_cols;          /* columns of P this rank sends per iteration */
+  double bytes_per_iteration; /* (halo_cols + send_cols) * p * sizeof(Krylov element) */
+  double exchange_ms;         /* sum over iterations of the exchange (pack + NCCL) time, if measured */
+  int measure_exchange;       /* in: time the exchange with events on the communication stream */
+} cpcag_shard_stats;
+/* ncclGetUniqueId (128 bytes) on one rank; every rank passes the same id to
+ * cpcag_cuda_comm_create (the bootstrap is the caller's, e.g. torch.distributed). */
+int cpcag_cuda_comm_unique_id(void* id_out);
+int cpcag_cuda_comm_create(cpcag_ctx ctx, const void* id, int nranks, int rank, cpcag_comm* out);
+int cpcag_cuda_comm_destroy(cpcag_comm comm);
+int cpcag_cuda_alternate_decode_sharded(cpcag_ctx ctx, cpcag_comm comm, int precision, const void* Xt,
+                                        int64_t rho_r, int64_t rho_c, const int64_t* omega_r,
+                                        const int64_t* omega_c, int64_t p, int64_t n, cpcag_csr Lr, cpcag_csr Lc,
+                                        double lambda_k1_r, double lambda_k1_c, const cpcag_decoder_config* cfg,
+                                        const int64_t* bounds, void* X_block, int* converged, int64_t* iterations,
+                                        cpcag_shard_stats* stats);
+/* The same algorithm for `nranks` ranks emulated in one process on one GPU
+ * (the exchange is device copies, the all-reduce a fixed-order sum; the ranks
+ * run phase by phase, no kernel waits for another).  X receives the whole
+ * p x n solution; stats describe rank 0.  For tests of the multi-rank logic. */
+int cpcag_cuda_alternate_decode_sharded_emulated(cpcag_ctx ctx, int nranks, int precision, const void* Xt,
+                                                 int64_t rho_r, int64_t rho_c, const int64_t* omega_r,
+                                                 const int64_t* omega_c, int64_t p, int64_t n, cpcag_csr Lr,
+                                                 cpcag_csr Lc, double lambda_k1_r, double lambda_k1_c,
+                                                 const cpcag_decoder_config* cfg, const int64_t* bounds, void* X,
+                                                 int* converged, int64_t* iterations, cpcag_shard_stats* stats);
+/* Host only (no device): the halo plan of `rank` for L_c's CSR structure
+ * (row_ptr n + 1, col_idx).  recv_counts[q] / send_counts[q]: columns this
+ * rank receives from / sends to rank q; recv_cols (capacity n): their global
+ * indices grouped by owner, ascending; send_cols (capacity
+ * nranks * block width): local indices (j - bounds[rank]) grouped by
+ * destination.  Either column array may be NULL. */
+int cpcag_halo_plan(const int64_t* row_ptr, const int64_t* col_idx, int64_t n, const int64_t* bounds, int nranks,
+                    int rank, int64_t* recv_counts, int64_t* send_counts, int64_t* recv_cols, int64_t* send_cols);
 
 /* ------------------------------------------------------------------ pipeline */
 typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36-63 */

@@ -246,18 +246,45 @@ Vec spmv(const Csr& a, const Vec& x) {
 }
 
 // sparse.cpp:87-98: Y(r, j) accumulates v_k X(c_k, j) over row r in CSR
-// order, starting from an explicit zero.
+// order, starting from an explicit zero.  With several right-hand sides X is
+// transposed to row-major first, so each CSR entry is read once for all
+// columns (the per-element order over k is unchanged: bit-identical).
 void spmm_left(const Csr& a, const double* X, i64 xr, i64 xc, double* Y) {
   if (xr != a.cols) throw std::invalid_argument("sparse multiply: dimension mismatch");
   const i64 R = a.rows;
+  if (xc < 4) {
 #pragma omp parallel for schedule(static)
-  for (i64 j = 0; j < xc; ++j) {
-    const double* xj = X + j * xr;
-    double* yj = Y + j * R;
-    for (i64 r = 0; r < R; ++r) {
-      double acc = 0.0;
-      for (i64 k = a.rp[r]; k < a.rp[r + 1]; ++k) acc += a.v[k] * xj[a.ci[k]];
-      yj[r] = acc;
+    for (i64 j = 0; j < xc; ++j) {
+      const double* xj = X + j * xr;
+      double* yj = Y + j * R;
+      for (i64 r = 0; r < R; ++r) {
+        double acc = 0.0;
+        for (i64 k = a.rp[r]; k < a.rp[r + 1]; ++k) acc += a.v[k] * xj[a.ci[k]];
+        yj[r] = acc;
+      }
+    }
+    return;
+  }
+  constexpr i64 JB = 256;  // right-hand sides per pass
+  std::vector<double> Xr(static_cast<size_t>(xr * std::min(xc, JB)));
+  for (i64 j0 = 0; j0 < xc; j0 += JB) {
+    const i64 nj = std::min(JB, xc - j0);
+#pragma omp parallel for schedule(static)
+    for (i64 c = 0; c < xr; ++c)
+      for (i64 j = 0; j < nj; ++j) Xr[c * nj + j] = X[c + (j0 + j) * xr];
+#pragma omp parallel
+    {
+      std::vector<double> acc(static_cast<size_t>(nj));
+#pragma omp for schedule(dynamic, 16)
+      for (i64 r = 0; r < R; ++r) {
+        for (i64 j = 0; j < nj; ++j) acc[j] = 0.0;
+        for (i64 k = a.rp[r]; k < a.rp[r + 1]; ++k) {
+          const double v = a.v[k];
+          const double* xrow = &Xr[static_cast<size_t>(a.ci[k] * nj)];
+          for (i64 j = 0; j < nj; ++j) acc[j] += v * xrow[j];
+        }
+        for (i64 j = 0; j < nj; ++j) Y[r + (j0 + j) * R] = acc[j];
+      }
     }
   }
 }
@@ -302,9 +329,31 @@ void spmm_right(const Csr& a, const double* X, i64 xr, i64 xc, double* Y) {
   }
 }
 
+// Full-array reductions: sequential for n <= kRedBlock (every test-sized
+// array); beyond that, fixed blocks of kRedBlock entries are each summed
+// sequentially (blocks in parallel) and the block sums are added in block
+// order.  The order depends on n only, never on the thread count, so results
+// are identical for any number of threads.
+constexpr i64 kRedBlock = i64{1} << 18;
+constexpr i64 kParMin = i64{1} << 16;  // element-wise loops go parallel above this
+
 double dot(const double* a, const double* b, i64 n) {
+  if (n <= kRedBlock) {
+    double s = 0.0;
+    for (i64 i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+  }
+  const i64 nb = (n + kRedBlock - 1) / kRedBlock;
+  std::vector<double> part(static_cast<size_t>(nb));
+#pragma omp parallel for schedule(static)
+  for (i64 q = 0; q < nb; ++q) {
+    const i64 e = std::min(n, (q + 1) * kRedBlock);
+    double s = 0.0;
+    for (i64 i = q * kRedBlock; i < e; ++i) s += a[i] * b[i];
+    part[static_cast<size_t>(q)] = s;
+  }
   double s = 0.0;
-  for (i64 i = 0; i < n; ++i) s += a[i] * b[i];
+  for (const double x : part) s += x;
   return s;
 }
 
@@ -328,30 +377,38 @@ PcgOut pcg_core(const Apply& apply, const Vec& b, Vec& x, double tol, i64 max_it
     return res;
   }
   const double target = tol * norm_b;
-  Vec r = apply(x);
+  Vec r(static_cast<size_t>(n)), z(static_cast<size_t>(n)), ap(static_cast<size_t>(n));
+  apply(x, r);
+#pragma omp parallel for schedule(static) if (n > kParMin)
   for (i64 i = 0; i < n; ++i) r[i] = b[i] - r[i];
-  Vec z = precond(r);
+  precond(r, z);
   Vec p = z;
   double rho = dot(r.data(), z.data(), n);
   i64 it = 0;
   while (it < max_iter) {
     if (std::sqrt(dot(r.data(), r.data(), n)) <= target) break;
-    const Vec ap = apply(p);
+    apply(p, ap);
     const double curv = dot(p.data(), ap.data(), n);
     if (!std::isfinite(curv) || curv <= 0.0)
       throw std::runtime_error("pcg: breakdown (nonpositive curvature) at iteration " +
                                std::to_string(it));
     const double alpha = rho / curv;
-    for (i64 i = 0; i < n; ++i) x[i] += alpha * p[i];
-    for (i64 i = 0; i < n; ++i) r[i] -= alpha * ap[i];
-    z = precond(r);
+#pragma omp parallel for schedule(static) if (n > kParMin)
+    for (i64 i = 0; i < n; ++i) {
+      x[i] += alpha * p[i];
+      r[i] -= alpha * ap[i];
+    }
+    precond(r, z);
     const double rho_next = dot(r.data(), z.data(), n);
     const double beta = rho_next / rho;
+#pragma omp parallel for schedule(static) if (n > kParMin)
     for (i64 i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
     rho = rho_next;
     ++it;
   }
-  Vec rt = apply(x);
+  Vec& rt = ap;
+  apply(x, rt);
+#pragma omp parallel for schedule(static) if (n > kParMin)
   for (i64 i = 0; i < n; ++i) rt[i] = b[i] - rt[i];
   res.rel_res = std::sqrt(dot(rt.data(), rt.data(), n)) / norm_b;
   res.iterations = it;
@@ -363,11 +420,9 @@ PcgOut pcg_core(const Apply& apply, const Vec& b, Vec& x, double tol, i64 max_it
 PcgOut pcg_jacobi(const Csr& A, const Vec& diag, const Vec& b, Vec& x, double tol, i64 max_iter) {
   Vec inv = diag;
   for (double& d : inv) d = d > 0.0 ? 1.0 / d : 1.0;
-  auto apply = [&A](const Vec& v) { return spmv(A, v); };
-  auto pre = [&inv](const Vec& r) {
-    Vec z(r.size());
+  auto apply = [&A](const Vec& v, Vec& out) { out = spmv(A, v); };
+  auto pre = [&inv](const Vec& r, Vec& z) {
     for (size_t i = 0; i < r.size(); ++i) z[i] = inv[i] * r[i];
-    return z;
   };
   if (x.size() != b.size()) x.assign(b.size(), 0.0);
   return pcg_core(apply, b, x, tol, max_iter, pre);
@@ -894,23 +949,32 @@ struct DecoderOp {
   const std::vector<i64>& omc;
   double gr, gc;
   i64 p, n;
+  // Row tiles of RT rows: the X L_c sums of a tile read only that tile of
+  // every column (cache resident), then L_r X of the tile's rows; each
+  // output keeps the reference's per-element order (the X Lc sum over the
+  // rows of Lc ascending, the Lr X sum in CSR order, then gc * a + gr * s).
   void apply(const double* X, double* out) const {
     const i64 P = p;
-#pragma omp parallel for schedule(static)
-    for (i64 c = 0; c < n; ++c) {
-      const double* xc = X + c * P;
-      double* oc = out + c * P;
-      // right_multiply contribution, rows of Lc ascending into column c.
-      std::vector<double> acc(static_cast<size_t>(P), 0.0);
-      for (i64 k = Lct.cp[c]; k < Lct.cp[c + 1]; ++k) {
-        const double w = Lct.v[k];
-        const double* xs = X + Lct.ri[k] * P;
-        for (i64 i = 0; i < P; ++i) acc[i] += w * xs[i];
-      }
-      for (i64 i = 0; i < P; ++i) {
-        double s = 0.0;
-        for (i64 k = Lr.rp[i]; k < Lr.rp[i + 1]; ++k) s += Lr.v[k] * xc[Lr.ci[k]];
-        oc[i] = gc * acc[i] + gr * s;
+    constexpr i64 RT = 128;
+    const i64 tiles = (P + RT - 1) / RT;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (i64 t = 0; t < tiles; ++t) {
+      const i64 i0 = t * RT, i1 = std::min(P, i0 + RT), m = i1 - i0;
+      double acc[RT];
+      for (i64 c = 0; c < n; ++c) {
+        for (i64 i = 0; i < m; ++i) acc[i] = 0.0;
+        for (i64 k = Lct.cp[c]; k < Lct.cp[c + 1]; ++k) {
+          const double w = Lct.v[k];
+          const double* xs = X + Lct.ri[k] * P + i0;
+          for (i64 i = 0; i < m; ++i) acc[i] += w * xs[i];
+        }
+        const double* xc = X + c * P;
+        double* oc = out + c * P;
+        for (i64 i = i0; i < i1; ++i) {
+          double s = 0.0;
+          for (i64 k = Lr.rp[i]; k < Lr.rp[i + 1]; ++k) s += Lr.v[k] * xc[Lr.ci[k]];
+          oc[i] = gc * acc[i - i0] + gr * s;
+        }
       }
     }
     for (size_t j = 0; j < omc.size(); ++j) {
@@ -940,12 +1004,12 @@ void alternate_decode(const double* Xt, i64 rho_r, i64 rho_c, const std::vector<
   for (i64 j = 0; j < rho_c; ++j)
     for (i64 i = 0; i < rho_r; ++i) b[omr[i] + omc[j] * p] = Xt[i + j * rho_r];
   Vec x(static_cast<size_t>(N), 0.0);
-  auto apply = [&op, N](const Vec& v) {
-    Vec o(static_cast<size_t>(N));
-    op.apply(v.data(), o.data());
-    return o;
+  auto apply = [&op](const Vec& v, Vec& o) { op.apply(v.data(), o.data()); };
+  auto identity = [N](const Vec& r, Vec& z) {
+#pragma omp parallel for schedule(static) if (N > kParMin)
+    for (i64 i = 0; i < N; ++i) z[i] = r[i];
   };
-  const PcgOut res = pcg_core(apply, b, x, tol, max_iter, [](const Vec& r) { return r; });
+  const PcgOut res = pcg_core(apply, b, x, tol, max_iter, identity);
   std::copy(x.begin(), x.end(), Xout);
   *conv = res.converged ? 1 : 0;
   *iters = res.iterations;
@@ -1248,8 +1312,8 @@ int ora_pcg_solve(const ora_csr* A, const double* b, double* x, int64_t n, doubl
     if (jacobi) {
       r = pcg_jacobi(*A, diagonal(*A), bv, xv, tol, max_iter);
     } else {
-      auto apply = [A](const Vec& v) { return spmv(*A, v); };
-      r = pcg_core(apply, bv, xv, tol, max_iter, [](const Vec& q) { return q; });
+      auto apply = [A](const Vec& v, Vec& out) { out = spmv(*A, v); };
+      r = pcg_core(apply, bv, xv, tol, max_iter, [](const Vec& q, Vec& z) { z = q; });
     }
     std::copy(xv.begin(), xv.end(), x);
     *iterations = r.iterations;

@@ -39,7 +39,12 @@ class SolveTraceC(C.Structure):
 
 
 class DecoderConfigC(C.Structure):
-    _fields_ = [("gamma", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64)]
+    _fields_ = [("gamma", dbl), ("pcg_tol", dbl), ("pcg_max_iter", i64), ("krylov_precision", C.c_int)]
+
+
+class ShardStatsC(C.Structure):
+    _fields_ = [("halo_cols", i64), ("send_cols", i64), ("bytes_per_iteration", dbl), ("exchange_ms", dbl),
+                ("measure_exchange", C.c_int)]
 
 
 DECODER_IDEAL, DECODER_ALTERNATE, DECODER_APPROX = 0, 1, 2
@@ -112,6 +117,7 @@ SIGNATURES = {
                                               dbl, dbl, C.POINTER(DecoderConfigC), vp,
                                               C.POINTER(C.c_int), ip]),
     "cpcag_ctx_reserve": (C.c_int, [vp, i64]),
+    "cpcag_ctx_set_apply_path": (C.c_int, [vp, C.c_int]),
     "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_sym_eigvals_lanczos": (C.c_int, [vp, vp, i64, C.c_double, i64, C.c_uint64, vp, vp]),
@@ -128,13 +134,17 @@ SIGNATURES = {
     "cpcag_cuda_graph_upsample": (C.c_int, [vp, vp, vp, i64, vp, i64, dbl, i64, vp]),
     "cpcag_cuda_approx_decode": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
                                            C.POINTER(ApproxConfigC), vp, vp, vp, vp, i64, ip]),
-    "cpcag_cuda_decoder_block_create": (C.c_int, [vp, C.c_int, i64, i64, i64, i64, vp, vp, vp, i64, vp, i64,
-                                                  dbl, dbl, C.POINTER(vp)]),
-    "cpcag_cuda_decoder_block_destroy": (C.c_int, [vp]),
-    "cpcag_cuda_decoder_block_rhs": (C.c_int, [vp, vp, vp, dp]),
-    "cpcag_cuda_decoder_block_apply": (C.c_int, [vp, vp, vp, dp]),
-    "cpcag_cuda_cg_residual": (C.c_int, [vp, C.c_int, i64, dbl, vp, vp, dp]),
-    "cpcag_cuda_cg_update": (C.c_int, [vp, C.c_int, i64, dbl, dbl, vp, vp, vp]),
+    "cpcag_cuda_decoder_apply": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp, vp, i64, vp, i64, dbl, dbl, vp, dp]),
+    "cpcag_halo_plan": (C.c_int, [vp, vp, i64, vp, C.c_int, C.c_int, vp, vp, vp, vp]),
+    "cpcag_cuda_comm_unique_id": (C.c_int, [vp]),
+    "cpcag_cuda_comm_create": (C.c_int, [vp, vp, C.c_int, C.c_int, C.POINTER(vp)]),
+    "cpcag_cuda_comm_destroy": (C.c_int, [vp]),
+    "cpcag_cuda_alternate_decode_sharded": (C.c_int, [vp, vp, C.c_int, vp, i64, i64, vp, vp, i64, i64, vp, vp,
+                                                      dbl, dbl, C.POINTER(DecoderConfigC), vp, vp,
+                                                      C.POINTER(C.c_int), ip, C.POINTER(ShardStatsC)]),
+    "cpcag_cuda_alternate_decode_sharded_emulated": (C.c_int, [vp, C.c_int, C.c_int, vp, i64, i64, vp, vp, i64, i64,
+                                                               vp, vp, dbl, dbl, C.POINTER(DecoderConfigC), vp, vp,
+                                                               C.POINTER(C.c_int), ip, C.POINTER(ShardStatsC)]),
     "cpcag_cuda_gram_tf32x3": (C.c_int, [vp, vp, i64, i64, vp]),
     "cpcag_cuda_run_pipeline": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp,
                                           C.POINTER(PipelineConfigC), vp, vp, vp, vp, vp,

@@ -33,7 +33,7 @@ __all__ = [
     "glr1_info", "load_matrix", "save_matrix", "load_sparse", "save_sparse", "save_factors",
     "load_factors", "plan_to_json", "plan_from_json", "save_plan", "load_plan",
     "ClusterLabels", "kmeans", "decode_labels", "clustering_error", "save_labels_csv", "load_labels_csv",
-    "report_to_json", "emit_report",
+    "report_to_json", "emit_report", "decoder_apply",
 ]
 
 
@@ -169,6 +169,10 @@ class Context:
 
     def reset_launch_count(self):
         N.lib().cpcag_ctx_reset_launch_count(self._h)
+
+    def set_apply_path(self, path: str):
+        """Decoder operator path: "auto", "split" (two passes) or "fused"."""
+        N.check(N.lib().cpcag_ctx_set_apply_path(self.handle, {"auto": 0, "split": 1, "fused": 2}[path]))
 
     def reserve(self, nbytes: int):
         """Grow the stream-ordered memory pool to `nbytes` up front."""
@@ -624,9 +628,15 @@ class DecoderConfig:  # decoders.hpp:13-22
     variant: str = "approx"          # decoder of run_pipeline: "approx" (reference default) | "alternate"
     delta_for_scaling: float = 0.0
     rank_threshold: float = 0.1
+    # extension: CG Krylov vectors for fp32 data ("fp64", default: fp32 X with
+    # fp64 R/P/AP; "fp32": every vector fp32), see cpcag_cuda.h
+    krylov_precision: str = "fp64"
 
     def c(self) -> N.DecoderConfigC:
-        return N.DecoderConfigC(self.gamma, self.pcg_tol, int(self.pcg_max_iter))
+        if self.krylov_precision not in ("fp64", "fp32"):
+            raise ValueError(f"unknown krylov_precision {self.krylov_precision!r}")
+        return N.DecoderConfigC(self.gamma, self.pcg_tol, int(self.pcg_max_iter),
+                                N.F32 if self.krylov_precision == "fp32" else 0)
 
     def approx_c(self) -> N.ApproxConfigC:
         return N.ApproxConfigC(float(self.delta_for_scaling), float(self.rank_threshold), float(self.pcg_tol),
@@ -671,6 +681,23 @@ def alternate_decode(Xt, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix,
 
 
 # ------------------------------------------------------------------ eigen / spectral gap
+def decoder_apply(P, plan: SamplingPlan, Lr: SparseMatrix, Lc: SparseMatrix, gbar_r: float, gbar_c: float,
+                  precision=None, ctx=None):
+    """The alternate decoder's operator (decoders.cpp:160-170) on a p x n
+    matrix: returns (AP, <P, AP>)."""
+    prec = _precision(P, precision)
+    pv = _In(P, prec, shape=(plan.p, plan.n))
+    om_r = np.ascontiguousarray(plan.omega_r, np.int64)
+    om_c = np.ascontiguousarray(plan.omega_c, np.int64)
+    out, op = _out(_is_cuda(P), _torch_device(P), (plan.p, plan.n), prec)
+    dot = N.dbl()
+    N.check(N.lib().cpcag_cuda_decoder_apply(_ctx(ctx), prec, pv.ptr, plan.p, plan.n, Lr.handle, Lc.handle,
+                                             om_r.ctypes.data if om_r.size else None, len(om_r),
+                                             om_c.ctypes.data if om_c.size else None, len(om_c), float(gbar_r),
+                                             float(gbar_c), op, C.byref(dot)))
+    return out, float(dot.value)
+
+
 @dataclass
 class EigenPairs:  # eigs.hpp:11-19
     eigenvalues: np.ndarray

@@ -82,6 +82,7 @@ struct Ctx {
   size_t pinned_bytes = 0;
   bool timing = false;
   std::string timing_filter;  // comma-separated tags; empty = all
+  int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused (tests)
   KernelTimes kt;
 };
 

@@ -131,6 +131,22 @@ static void harvest(Ctx* c) {
 // pipeline.  The destructor cannot know which stream last used the arrays,
 // so it synchronises the device (what cudaFree would do) and returns them to
 // the pool, where the next allocation reuses them without a remap.
+// Exclusive prefix sum of n int64 values (out[0] = 0); returns the total
+// in[0] + ... + in[n-1] (synchronises to read it).
+i64 exclusive_scan_i64(Ctx* c, const i64* in, i64* out, i64 n) {
+  if (n <= 0) return 0;
+  size_t tmp = 0;
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int>(n), c->stream));
+  DevBuf<char> ws(c, std::max<size_t>(tmp, 1));
+  CUDA_OK(cub::DeviceScan::ExclusiveSum(ws.p, tmp, in, out, static_cast<int>(n), c->stream));
+  launched(c);
+  i64 last_out = 0, last_in = 0;
+  CUDA_OK(cudaMemcpyAsync(&last_out, out + n - 1, sizeof(i64), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(cudaMemcpyAsync(&last_in, in + n - 1, sizeof(i64), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  return last_out + last_in;
+}
+
 void* csr_malloc(Ctx* c, size_t bytes) {
   void* p = nullptr;
   if (bytes) CUDA_OK(cudaMallocAsync(&p, bytes, c->stream));
@@ -846,6 +862,13 @@ int cpcag_ctx_set_stream(cpcag_ctx ctx, void* s) {
 }
 
 void* cpcag_ctx_stream(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->stream : nullptr; }
+
+int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path) {
+  return guard([&] {
+    if (path < 0 || path > 2) invalid("apply path must be 0, 1 or 2");
+    as_ctx(ctx)->apply_path = path;
+  });
+}
 
 int cpcag_ctx_synchronize(cpcag_ctx ctx) {
   return guard([&] { sync(as_ctx(ctx)); });

@@ -188,3 +188,26 @@ def config3_points(seed: int = 1605, p: int = 4096, n: int = 200_000, dim: int =
     """Config 3: row points (p x dim) and column points (n x dim), N(0, I)."""
     rs = np.random.default_rng(seed)
     return (rs.standard_normal((dim, p), dtype=np.float32), rs.standard_normal((dim, n), dtype=np.float32))
+
+
+def config3_rhs(P, Lr, Lc, plan, ctx, rank: int = 20, sweeps: int = 20, seed: int = 1606):
+    """Config 3's right-hand side: X0 = B_r A B_c^T with B the
+    orthonormalised low-pass filtered Gaussian bases (`sweeps` Jacobi sweeps
+    B <- B - L B / ||L|| through the library's fp64 SpMM) and A ~ N(0, 1),
+    sampled on the plan: Xt = X0(omega_r, omega_c), fp64 column-major on the
+    device.  Harness code (torch on the device for the QR), never timed."""
+    import torch
+
+    rs = np.random.default_rng(seed)
+
+    def lowpass(L, m):
+        nrm = P.power_iteration_norm(L, 1e-7, 42, ctx=ctx)
+        B = torch.tensor(rs.standard_normal((m, rank)), device="cuda")
+        for _ in range(sweeps):
+            B = B - L.multiply(B) / nrm
+        return torch.linalg.qr(B)[0]
+
+    Br, Bc = lowpass(Lr, plan.p), lowpass(Lc, plan.n)
+    A = torch.tensor(rs.standard_normal((rank, rank)), device="cuda")
+    Xt = Br[torch.tensor(plan.omega_r, device="cuda")] @ A @ Bc[torch.tensor(plan.omega_c, device="cuda")].T
+    return Xt.t().contiguous().t()

@@ -75,12 +75,14 @@ def _apply_entry(rp_r, ci_r, v_r, rp_c, ci_c, v_c, Pm, rsel, csel, gr, gc, i, c)
     return out
 
 
-def test_cfg3_band_apply_full_size_sampled_columns_bit_exact(P, ctx):
+def test_cfg3_apply_full_size_sampled_columns_bit_exact(P, ctx):
+    """One fp64 application of the decoder operator at the full cfg3 size
+    (4096 x 200 000: the lc pass with the band resident in L2, the lr pass
+    over degree-sorted kNN rows) on sampled entries against the reference's
+    per-entry arithmetic (decoders.cpp:160-170) in Python binary64."""
     import torch
 
-    from paper_1602_02070_b200 import _native as N
     from paper_1602_02070_b200 import workloads
-    from paper_1602_02070_b200.sharded import CudaBlockBackend
 
     Pr, Pc = workloads.config3_points()
     p, n = Pr.shape[1], Pc.shape[1]
@@ -88,41 +90,33 @@ def test_cfg3_band_apply_full_size_sampled_columns_bit_exact(P, ctx):
     gc_ = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
     plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
     gr, gc = 1.0 / 0.37, 1.0 / 0.53
-    be = CudaBlockBackend(ctx, N.F64, plan, gr_.laplacian, gc_.laplacian, gr, gc, 0, n)
     gen = torch.Generator(device="cuda").manual_seed(5)
-    Pflat = torch.randn(p * n, dtype=torch.float64, device="cuda", generator=gen)
-    AP = torch.empty_like(Pflat)
-    be.apply(Pflat, AP)
+    Pt = torch.randn(n, p, dtype=torch.float64, device="cuda", generator=gen).t()
+    AP, dot = P.decoder_apply(Pt, plan, gr_.laplacian, gc_.laplacian, gr, gc, ctx=ctx)
     torch.cuda.synchronize()
     cols = np.random.default_rng(3).choice(n, 6, replace=False)
-    # neighbour columns the sampled outputs read
     rp_c, ci_c, v_c = gc_.laplacian.arrays()
     rp_r, ci_r, v_r = gr_.laplacian.arrays()
     need = sorted(set(int(j) for c in cols for j in ci_c[rp_c[c]:rp_c[c + 1]]) | set(int(c) for c in cols))
     Pm = np.zeros((p, n))
-    Pv = Pflat.view(n, p)
     for j in need:
-        Pm[:, j] = Pv[j].cpu().numpy()
+        Pm[:, j] = Pt[:, j].cpu().numpy()
     rsel = np.zeros(p, bool)
     rsel[np.asarray(plan.omega_r)] = True
     csel = np.zeros(n, bool)
     csel[np.asarray(plan.omega_c)] = True
-    APv = AP.view(n, p)
     rows = np.random.default_rng(4).choice(p, 64, replace=False)
     for c in cols:
-        got = APv[int(c)].cpu().numpy()
+        got = AP[:, int(c)].cpu().numpy()
         for i in rows:
             want = _apply_entry(rp_r, ci_r, v_r, rp_c, ci_c, v_c, Pm, rsel, csel, gr, gc, int(i), int(c))
             assert got[i] == want, (i, c)
-    # Repeat calls with a fresh torch-zeroed output: the zeroing (torch's
-    # stream) must be ordered before the apply (regression: a context on an
-    # unordered stream raced the memset from the second call on).
-    for _ in range(2):
-        AP2 = torch.zeros_like(Pflat)
-        be.apply(Pflat, AP2)
-        torch.cuda.synchronize()
-        assert torch.equal(AP2, AP)
-    be.close()
+    # size-independent: <P, AP> equals the sum of the stored products
+    assert abs(dot - float((Pt * AP).sum())) <= 1e-9 * abs(dot)
+    # repeat with a fresh output: the stream ordering holds across calls
+    AP2, _ = P.decoder_apply(Pt, plan, gr_.laplacian, gc_.laplacian, gr, gc, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(AP2, AP)
 
 
 def test_cfg1_pipeline_full_size_reduced_iterations(P, ctx):
@@ -157,16 +151,15 @@ def test_cfg1_pipeline_full_size_reduced_iterations(P, ctx):
     assert math.isfinite(rep.trace.objective[-1])
 
 
-def test_cfg3_sharded_block_driver_matches_single_gpu(P, ctx):
-    """The column-block primitives at the full cfg3 size (one block = all
-    200 000 columns, fp32): a few CG iterations of the sharded driver equal
-    the single-GPU decoder's (same operator, dots reduced in another order)."""
+def test_cfg3_sharded_emulated_matches_single_gpu(P, ctx):
+    """The device-resident sharded decoder at the full cfg3 size with four
+    ranks emulated on one GPU (halo exchange as device copies, all-reduced
+    dots), 4 CG iterations: equal to the one-GPU decoder's result up to the
+    dots' summation order."""
     import torch
 
-    from paper_1602_02070_b200 import _native as N
     from paper_1602_02070_b200 import workloads
-    from paper_1602_02070_b200.sharded import CudaBlockBackend, alternate_decode_sharded
-    from shard_double import ThreadCollectives
+    from paper_1602_02070_b200.sharded import alternate_decode_sharded_emulated
 
     Pr, Pc = workloads.config3_points()
     p, n = Pr.shape[1], Pc.shape[1]
@@ -176,18 +169,16 @@ def test_cfg3_sharded_block_driver_matches_single_gpu(P, ctx):
     gen = torch.Generator(device="cuda").manual_seed(9)
     Xt = torch.randn(len(plan.omega_c), len(plan.omega_r), device="cuda", generator=gen).t()
     its = 4
-    be = CudaBlockBackend(ctx, N.F32, plan, gr_.laplacian, gc_.laplacian, 1.0, 1.0, 0, n)
-    coll = ThreadCollectives(ThreadCollectives.Shared(1), 0)
-    res = alternate_decode_sharded(Xt, plan, be, coll, lambda k: torch.zeros(k, device="cuda"), tol=1e-30,
-                                   max_iter=its)
-    Xs = res.X_block.view(n, p).t().cpu().numpy().astype(np.float64)
-    be.close()
-    del res
     g1 = P.SpectralGap(lambda_k1=1.0)
-    one = P.alternate_decode(Xt, plan, gr_.laplacian, gc_.laplacian, g1, g1, P.DecoderConfig(1.0, 1e-30, its),
-                             ctx=ctx)
+    cfg = P.DecoderConfig(1.0, 1e-30, its)
+    sh, st = alternate_decode_sharded_emulated(Xt, plan, gr_.laplacian, gc_.laplacian, g1, g1, cfg, 4, ctx=ctx)
+    assert sh.iterations == its
+    assert 0 < st.halo_cols <= n - n // 4
+    Xs = sh.X.cpu().numpy().astype(np.float64)
+    del sh
+    one = P.alternate_decode(Xt, plan, gr_.laplacian, gc_.laplacian, g1, g1, cfg, ctx=ctx)
     assert one.iterations == its
-    assert rel(Xs, one.X.cpu().numpy().astype(np.float64)) <= 1e-4
+    assert rel(Xs, one.X.cpu().numpy().astype(np.float64)) <= 1e-6
 
 
 def test_knn_second_tensor_core_pass_equals_exact_path(P, ctx, monkeypatch, capfd):
@@ -252,51 +243,59 @@ def test_cfg1_pipeline_full_iterations_within_north_star(P, ctx):
     assert rel(rep.X.cpu().numpy(), dec.X) <= 1e-4
 
 
-def test_cfg3_decoder_fp32_against_fp64(P, ctx):
-    """Config 3 at full size (4096 x 200000, 100 CG iterations): the fp32
-    decoder (band apply) against the fp64 one on the device, which matches
-    the oracle to 1e-9 on every smaller case (a full fp64 oracle run here is
-    ~16 h single-threaded).
-
-    Measured: 1.04e-3 relative Frobenius -- ABOVE the north_star 1e-4.  CG
-    on this system (gamma-bar = 1, 1/64 of the entries in the mask) is far
-    from converged after 100 iterations, and the fp32 recurrence (X, R, P
-    rounded at 6e-8 per step) drifts from the fp64 one; accumulating the
-    applies in fp64 only moved it to 7.2e-4, and fp64 iterates with fp32
-    applies (tools/mixed_cg_experiment.py) to 1.05e-3: CG amplifies the fp32
-    operator's perturbation.  The bound below records the measured state;
-    the fp64 decoder is the parity path at this size, and the config-1
-    decoder (a better-conditioned system) is within 3e-6 of the oracle."""
+def _cfg3_problem(P, ctx, n=None):
+    """The bench's config-3 decoder problem: kNN graphs over
+    N(0, I_64) points, rank-20 low-pass right-hand side sampled 1/8 x 1/8.
+    n: a reduced column count (the same generator, fewer column points)."""
     import torch
 
     from paper_1602_02070_b200 import workloads
 
-    Pr, Pc = workloads.config3_points()
+    Pr, Pc = workloads.config3_points() if n is None else workloads.config3_points(n=n)
     p, n = Pr.shape[1], Pc.shape[1]
-    ctx.reserve(48 << 30)
     gr = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
     gc = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
     plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
-    # the bench's right-hand side: a rank-20 estimate on the graphs (low-pass
-    # filtered random bases, SURVEY 8(d)) sampled on the plan
-    rs = np.random.default_rng(1606)
+    Xt = workloads.config3_rhs(P, gr.laplacian, gc.laplacian, plan, ctx)
+    return gr, gc, plan, Xt
 
-    def lowpass(L, m, k=20, sweeps=20):
-        nrm = P.power_iteration_norm(L, 1e-7, 42, ctx=ctx)
-        B = torch.tensor(rs.standard_normal((m, k)), device="cuda")
-        for _ in range(sweeps):
-            B = B - L.multiply(B) / nrm
-        return torch.linalg.qr(B)[0]
 
-    Br, Bc = lowpass(gr.laplacian, p), lowpass(gc.laplacian, n)
-    A = torch.tensor(rs.standard_normal((20, 20)), device="cuda")
-    Xt = (Br[torch.tensor(plan.omega_r, device="cuda")] @ A @ Bc[torch.tensor(plan.omega_c, device="cuda")].T)
-    Xt = Xt.t().contiguous().t().cpu().numpy()
+def test_cfg3_decoder_fp32_within_north_star_of_fp64(P, ctx):
+    """Config 3 at full size (4096 x 200 000, 100 CG iterations): the fp32
+    decoder as the bench runs it (fp32 X, fp64 Krylov vectors) within the
+    north_star 1e-4 of the fp64 decoder, which matches the oracle to 1e-9
+    wherever the oracle runs (test below at n = 20 000).  Every-vector-fp32
+    CG drifts 7-8e-4 here (tools/cfg3_precision.py), which is why the fp32
+    path keeps R, P and AP in fp64."""
+    import torch
+
+    ctx.reserve(48 << 30)
+    gr, gc, plan, Xt = _cfg3_problem(P, ctx)
     g1 = P.SpectralGap(lambda_k1=1.0)
     dcfg = P.DecoderConfig(1.0, 1e-30, 100)
-    Xd = torch.tensor(np.ascontiguousarray(Xt.T), device="cuda").t()
-    X64 = P.alternate_decode(Xd, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, ctx=ctx).X
-    X32 = P.alternate_decode(Xd.float().t().contiguous().t(), plan, gr.laplacian, gc.laplacian, g1, g1, dcfg,
+    X64 = P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, ctx=ctx).X
+    X32 = P.alternate_decode(Xt.float().t().contiguous().t(), plan, gr.laplacian, gc.laplacian, g1, g1, dcfg,
                              ctx=ctx).X
+    assert X32.dtype == torch.float32
     d = torch.linalg.norm(X32.double() - X64) / torch.linalg.norm(X64)
-    assert float(d) <= 2e-3, float(d)
+    assert float(d) <= 1e-4, float(d)
+
+
+def test_cfg3_shaped_decoder_matches_oracle(P, ctx):
+    """A config-3-shaped case the oracle finishes in about a minute (p = 4096,
+    n = 20 000, gamma-bar = 1, 1/8 x 1/8 sampling, 100 iterations): the fp64
+    decoder within 1e-9 and the fp32 decoder (the bench's path) within the
+    north_star 1e-4 of the oracle (decoders.cpp:145-186)."""
+    gr, gc, plan, Xt = _cfg3_problem(P, ctx, n=20_000)
+    g1 = P.SpectralGap(lambda_k1=1.0)
+    dcfg = P.DecoderConfig(1.0, 1e-30, 100)
+    X64 = P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, ctx=ctx).X.cpu().numpy()
+    X32 = P.alternate_decode(Xt.float().t().contiguous().t(), plan, gr.laplacian, gc.laplacian, g1, g1, dcfg,
+                             ctx=ctx).X.cpu().numpy()
+    Lr = O.Csr.from_csr(*gr.laplacian.shape, *gr.laplacian.arrays())
+    Lc = O.Csr.from_csr(*gc.laplacian.shape, *gc.laplacian.arrays())
+    oplan = O.SamplingPlan(np.asarray(plan.omega_r), np.asarray(plan.omega_c), plan.p, plan.n)
+    ro = O.alternate_decode(Xt.cpu().numpy(), oplan, Lr, Lc, 1.0, 1.0, 1.0, 1e-30, 100)
+    assert rel(X64, ro.X) <= 1e-9
+    X32o = O.alternate_decode(Xt.float().double().cpu().numpy(), oplan, Lr, Lc, 1.0, 1.0, 1.0, 1e-30, 100)
+    assert rel(X32, X32o.X) <= 1e-4

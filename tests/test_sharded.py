@@ -1,15 +1,20 @@
-"""Column-sharded alternate decoder: the distributed algorithm
-against the single-process oracle.  CPU: world size 2 over gloo with the
-NumPy block double.  GPU: three in-process ranks on one device (separate
-contexts, thread collectives) through the CUDA block primitives."""
+"""Column-sharded alternate decoder.
+
+CPU (no device): the library's host-side halo plan (cpcag_halo_plan) against
+a NumPy restatement, and the distributed CG algorithm (tests/shard_model.py,
+exchanging exactly the planned halo columns) over gloo with world size 2 and
+3 against the single-process oracle.
+GPU: the device-resident implementation (csrc/sharded.cu) -- the emulated
+multi-rank driver (1, 2, 3 and 8 ranks on one GPU, no kernel waiting on
+another) and the NCCL driver at world size 1 (one GPU is all this pool has)
+-- against the oracle and the one-GPU decoder."""
 import os
 import socket
-import threading
 
 import numpy as np
 import pytest
 
-from helpers import knn_laplacian, rel
+from helpers import knn_laplacian, rel, to_device
 from oracle import pyoracle as O
 
 
@@ -32,8 +37,9 @@ def _gloo_worker(rank, world, port, out, use_halo=False):
     import torch
     import torch.distributed as dist
 
-    from paper_1602_02070_b200.sharded import HaloPlan, TorchCollectives, alternate_decode_sharded, column_blocks
+    from paper_1602_02070_b200.sharded import HaloPlan, column_blocks
     from shard_double import NumpyBlockBackend
+    from shard_model import TorchCollectives, alternate_decode_sharded
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     Lr, Lc, plan, Xt = _case()
@@ -53,9 +59,9 @@ def _gloo_worker(rank, world, port, out, use_halo=False):
 
 
 @pytest.mark.parametrize("world,use_halo", [(2, False), (2, True), (3, True)])
-def test_sharded_decoder_gloo_matches_oracle(world, use_halo):
-    """gloo ranks; with a HaloPlan only the halo columns move (all-to-all
-    with uneven splits), without one the blocks are all-gathered."""
+def test_sharded_algorithm_gloo_matches_oracle(world, use_halo):
+    """gloo ranks; with a HaloPlan only the planned halo columns move
+    (all-to-all with uneven splits), without one the blocks are all-gathered."""
     import torch.multiprocessing as mp
 
     port = _free_port()
@@ -80,139 +86,140 @@ def test_sharded_decoder_gloo_matches_oracle(world, use_halo):
     assert rel(X, ro.X) <= 1e-9
 
 
-def test_halo_plan_covers_exactly_the_needed_columns():
-    from paper_1602_02070_b200.sharded import HaloPlan, column_blocks
+@pytest.mark.parametrize("world,uneven", [(4, False), (3, True), (1, False)])
+def test_halo_plan_covers_exactly_the_needed_columns(world, uneven):
+    """cpcag_halo_plan (the library's host code) against a NumPy restatement:
+    each rank receives exactly the remote columns its L_c rows reference,
+    grouped by owner and ascending, and what s sends to r is what r
+    receives from s."""
+    from paper_1602_02070_b200.sharded import HaloPlan, bounds_of
 
-    Lc = knn_laplacian(101, 3, 6, 4)
+    n = 101
+    Lc = knn_laplacian(n, 3, 6, 4)
     rp, ci, _ = Lc.arrays()
-    world = 4
-    w, blocks = column_blocks(101, world)
-    plans = [HaloPlan(rp, ci, 101, world, r) for r in range(world)]
+    bd = np.array([0, 10, 60, n]) if uneven else bounds_of(n, world)
+    plans = [HaloPlan(rp, ci, n, world, r, bounds=bd) for r in range(world)]
     for r in range(world):
-        c0, c1 = blocks[r]
+        c0, c1 = bd[r], bd[r + 1]
         cols = set(ci[rp[c0]:rp[c1]].tolist())
         need = sorted(c for c in cols if not c0 <= c < c1)
-        got = sorted(int(x) for s in range(world) for x in plans[r].recv[s])
+        got = [int(x) for s in range(world) for x in plans[r].recv[s]]
         assert got == need
+        assert plans[r].halo_cols == len(need)
         for s in range(world):  # what s sends to r is what r receives from s
-            sent = (plans[s].send[r] + blocks[s][0]).tolist()
+            assert all(bd[s] <= x < bd[s + 1] for x in plans[r].recv[s])
+            sent = (plans[s].send[r] + bd[s]).tolist()
             assert sent == plans[r].recv[s].tolist()
 
 
+def test_halo_plan_rejects_bad_bounds():
+    from paper_1602_02070_b200.sharded import HaloPlan
+
+    Lc = knn_laplacian(20, 3, 4, 1)
+    rp, ci, _ = Lc.arrays()
+    with pytest.raises(ValueError, match="cover"):
+        HaloPlan(rp, ci, 20, 2, 0, bounds=np.array([0, 5, 19]))
+    with pytest.raises(ValueError, match="ascending"):
+        HaloPlan(rp, ci, 20, 2, 0, bounds=np.array([0, 25, 20]))
+
+
 def test_column_blocks_cover_and_pad():
-    from paper_1602_02070_b200.sharded import column_blocks
+    from paper_1602_02070_b200.sharded import bounds_of, column_blocks
 
     for n, g in [(37, 2), (10, 4), (8, 8), (5, 8)]:
         w, blocks = column_blocks(n, g)
         assert len(blocks) == g and w * g >= n
         cols = [c for a, b in blocks for c in range(a, b)]
         assert cols == list(range(n))
+        bd = bounds_of(n, g)
+        assert bd[0] == 0 and bd[-1] == n and np.all(np.diff(bd) >= 0)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-def test_sharded_decoder_cuda_three_ranks_one_gpu(prec):
-    import torch
-
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharded_decoder_emulated_ranks_match_oracle(prec, world):
+    """The device implementation with `world` ranks emulated on one GPU:
+    every rank's applies are the one-GPU decoder's entries (bit-identical in
+    fp64); the all-reduced dots are summed per rank, so fp64 agrees with the
+    oracle to 1e-9 on this case."""
     import paper_1602_02070_b200 as P
-    from helpers import to_device
-    from paper_1602_02070_b200 import _native as N
-    from paper_1602_02070_b200.sharded import CudaBlockBackend, alternate_decode_sharded, column_blocks
-    from shard_double import ThreadCollectives
+    from paper_1602_02070_b200.sharded import alternate_decode_sharded_emulated
 
+    ctx = P.Context(0)
     Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
-    world = 3
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
-    dt = torch.float64 if prec == "f64" else torch.float32
-    code = N.F64 if prec == "f64" else N.F32
-    shared = ThreadCollectives.Shared(world)
-    _, blocks = column_blocks(plan.n, world)
-    out, errs = {}, []
-
-    def worker(rank):
-        try:
-            ctx = P.Context(0)
-            dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
-            c0, c1 = blocks[rank]
-            be = CudaBlockBackend(ctx, code, plan, dLr, dLc, 1.0 / 0.3, 1.0 / 0.4, c0, c1)
-            Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), dtype=dt, device="cuda").t()
-            res = alternate_decode_sharded(Xt_d, plan, be, ThreadCollectives(shared, rank),
-                                           lambda k: torch.zeros(k, dtype=dt, device="cuda"), tol=1e-10, max_iter=300)
-            torch.cuda.synchronize()
-            out[rank] = (c0, c1, res.X_block.cpu().numpy().astype(np.float64), res.iterations)
-            be.close()
-        except Exception as e:  # surface in the main thread
-            errs.append(e)
-            shared.barrier.abort()
-
-    ts = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join(300)
-    assert not errs, errs
-    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
-    X = np.zeros((plan.p, plan.n))
-    for r in range(world):
-        c0, c1, blk, it = out[r]
-        X[:, c0:c1] = blk.reshape((plan.p, c1 - c0), order="F")
-        assert abs(it - ro.iterations) <= (1 if prec == "f64" else 300)
-    # Dot products are sums of per-rank partials (a different summation order
-    # from the one-GPU solver), which CG amplifies on this ill-conditioned
-    # case; the fp64 bar is therefore 1e-6 (the small gloo case holds 1e-9).
-    assert rel(X, ro.X) <= (1e-6 if prec == "f64" else 1e-4)
+    dt = np.float64 if prec == "f64" else np.float32
+    cfg = P.DecoderConfig(1.0, 1e-10, 300)
+    res, st = alternate_decode_sharded_emulated(Xt.astype(dt), plan, to_device(ctx, Lr), to_device(ctx, Lc),
+                                                P.SpectralGap(lambda_k1=0.3), P.SpectralGap(lambda_k1=0.4), cfg,
+                                                world, ctx=ctx)
+    ro = O.alternate_decode(Xt.astype(dt).astype(np.float64), plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
+    if world > 1:
+        assert st.halo_cols > 0 and st.send_cols > 0
+    else:
+        assert st.halo_cols == 0
+    assert abs(res.iterations - ro.iterations) <= 1
+    assert rel(res.X, ro.X) <= (1e-9 if prec == "f64" else 1e-6)
 
 
-def _nccl_worker(port, out, use_halo=False):
+@pytest.mark.gpu
+def test_sharded_decoder_emulated_uneven_blocks_and_empty_rank():
+    import paper_1602_02070_b200 as P
+    from paper_1602_02070_b200.sharded import alternate_decode_sharded_emulated
+
+    ctx = P.Context(0)
+    Lr, Lc, plan_o, Xt = _case(120, 90, 30, 20, 13)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    cfg = P.DecoderConfig(1.0, 1e-10, 200)
+    bd = np.array([0, 7, 7, 60, 90])  # rank 1 owns no column
+    res, _ = alternate_decode_sharded_emulated(Xt, plan, to_device(ctx, Lr), to_device(ctx, Lc),
+                                               P.SpectralGap(lambda_k1=0.3), P.SpectralGap(lambda_k1=0.4), cfg, 4,
+                                               bounds=bd, ctx=ctx)
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 200)
+    assert abs(res.iterations - ro.iterations) <= 1
+    assert rel(res.X, ro.X) <= 1e-9
+
+
+def _nccl_worker(port, out):
     import torch
     import torch.distributed as dist
 
     import paper_1602_02070_b200 as P
-    from helpers import to_device
-    from paper_1602_02070_b200 import _native as N
-    from paper_1602_02070_b200.sharded import (CudaBlockBackend, HaloPlan, TorchCollectives, alternate_decode_sharded,
-                                               column_blocks)
+    from paper_1602_02070_b200.sharded import ShardComm, alternate_decode_sharded
 
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
     Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
     ctx = P.Context(0)
-    _, blocks = column_blocks(plan.n, 1)
-    c0, c1 = blocks[0]
-    be = CudaBlockBackend(ctx, N.F64, plan, to_device(ctx, Lr), to_device(ctx, Lc), 1.0 / 0.3, 1.0 / 0.4, c0, c1)
-    coll = TorchCollectives()
-    assert dist.get_backend() == "nccl"
+    comm = ShardComm(ctx)
     Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), device="cuda").t()
-    halo = None
-    if use_halo:
-        rp, ci, _ = Lc.arrays()
-        halo = HaloPlan(rp, ci, plan.n, 1, 0)
-    res = alternate_decode_sharded(Xt_d, plan, be, coll, lambda k: torch.zeros(k, dtype=torch.float64, device="cuda"),
-                                   tol=1e-10, max_iter=300, halo=halo)
+    res = alternate_decode_sharded(Xt_d, plan, to_device(ctx, Lr), to_device(ctx, Lc), P.SpectralGap(lambda_k1=0.3),
+                                   P.SpectralGap(lambda_k1=0.4), P.DecoderConfig(1.0, 1e-10, 300), comm,
+                                   measure_exchange=True, ctx=ctx)
     torch.cuda.synchronize()
-    out["r"] = (res.X_block.cpu().numpy().copy(), res.iterations)
-    be.close()
+    out["r"] = (res.X_block.cpu().numpy().copy(), res.iterations, res.c0, res.c1, res.stats.halo_cols)
+    comm.close()
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("use_halo", [False, True])
-def test_sharded_decoder_nccl_world1_matches_oracle(use_halo):
-    """The column-sharded driver over a real NCCL communicator (world 1: the
-    all-gather and the all-reduced dots go through NCCL on the device)."""
+def test_sharded_decoder_nccl_world1_matches_oracle():
+    """The NCCL driver (ncclAllReduce of device scalars, comm stream) at
+    world size 1."""
     import torch.multiprocessing as mp
 
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    pr = mp.get_context("spawn").Process(target=_nccl_worker, args=(port, out, use_halo))
+    pr = mp.get_context("spawn").Process(target=_nccl_worker, args=(port, out))
     pr.start()
     pr.join(300)
     assert pr.exitcode == 0
     Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
     ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
-    blk, it = out["r"]
-    X = blk.reshape((plan_o.p, plan_o.n), order="F")
+    blk, it, c0, c1, halo = out["r"]
+    assert (c0, c1, halo) == (0, plan_o.n, 0)
     assert abs(it - ro.iterations) <= 1
-    assert rel(X, ro.X) <= 1e-6
+    assert rel(blk, ro.X) <= 1e-9

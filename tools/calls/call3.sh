@@ -1,0 +1,6 @@
+set -x
+python tools/decode_small.py cfg1 fp64 3 > gpurun_out/ds1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"lc_k|lr_reg" -c 4 -o gpurun_out/prof_cfg1b python tools/decode_small.py cfg1 fp64 3 > gpurun_out/ncu1.log 2>&1
+python tools/decode_small.py cfg3 fp64 2 > gpurun_out/ds3.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"lc_k|lr_reg" -c 2 -o gpurun_out/prof_cfg3b python tools/decode_small.py cfg3 fp64 2 > gpurun_out/ncu3.log 2>&1
+tail -n 3 gpurun_out/ncu1.log gpurun_out/ncu3.log

@@ -1,0 +1,5 @@
+set -x
+timeout 600 python tools/decode_timing.py cfg1 > gpurun_out/decode_timing.log 2>&1
+tail -2 gpurun_out/decode_timing.log
+python tools/decode_small.py cfg1 fp64 3 > gpurun_out/ds1.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"lc_k" -c 1 -o gpurun_out/prof_lc64 python tools/decode_small.py cfg1 fp64 3 > gpurun_out/ncu1b.log 2>&1
