@@ -53,8 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--fp64", action="store_true", help="compute in fp64 (config 1 is fp32)")
-    ap.add_argument("--krylov", choices=["fp64", "fp32"], default="fp64",
-                    help="decoder Krylov vectors for fp32 data (fp64: the path that meets 1e-4 at every config)")
+    ap.add_argument("--krylov", choices=["fp64", "fp32"], default=None,
+                    help="decoder Krylov vectors for fp32 data (default: fp32 at cfg1, whose full-iteration parity "
+                         "test passes with it; fp64 at cfg3, where fp32 Krylov vectors miss 1e-4)")
     ap.add_argument("--json-out", default=None)
     ap.add_argument("--sharded", action="store_true",
                     help="cfg3 through the column-sharded decoder over NCCL (one column block per rank)")
@@ -213,6 +214,7 @@ def pipeline_config(P, wl, krylov="fp64"):
 
 
 KERNEL_BYTES_DOC = {
+    "cg_apply": "fused one-pass apply: read P + write AP (2 N wk) + one read of L_r and L_c ((nnz_r + nnz_c)(wv + 4))",
     "cg_apply_lc": "read P + write U (2 N wk) + one read of L_c (nnz_c (wv + 4))",
     "cg_apply_lr": "read P, U + write AP (3 N wk) + one read of L_r (nnz_r (wv + 4))",
     "cg_residual": "read R, AP + write R (3 N wk)",
@@ -233,6 +235,8 @@ def decoder_widths(fp64: bool, krylov: str):
 def kernel_bytes(tag, dims, widths):
     wk, wx, wv = widths
     N, nnz_r, nnz_c = dims["N"], dims["nnz_r"], dims["nnz_c"]
+    if tag == "cg_apply":
+        return 2 * N * wk + (nnz_r + nnz_c) * (wv + 4)
     if tag == "cg_apply_lc":
         return 2 * N * wk + nnz_c * (wv + 4)
     if tag == "cg_apply_lr":
@@ -452,6 +456,15 @@ def run_ours(args, rank, local_rank, world):
         "kernel_share": kernel_share, "kernel_roofline": kernel_roofline,
         "wall_s_timed_region": round(wall1 - wall0, 3),
     }
+    # ---------------- multi-GPU: the column-sharded decoder at this world size
+    # (SURVEY 8(e)); value above stays the per-rank config-1 replica (weak)
+    if dist is not None and not os.environ.get("BENCH_NO_SHARDED"):
+        try:
+            blk = cfg3_sharded_block(args, rank, local_rank, world)
+        except Exception as e:  # reported, never silently dropped
+            blk = {"error": f"{type(e).__name__}: {e}"}
+        if rank == 0:
+            out["sharded_cfg3"] = blk
     if rank == 0:
         line = json.dumps(out)
         print(line, flush=True)
@@ -678,6 +691,32 @@ def run_cfg0(args):
             json.dump(out, f)
 
 
+def measure_tf32_peak() -> float:
+    """Dense TF32 tensor throughput of this GPU (cuBLAS through torch, 8192^3,
+    best of 10 after warm-up), TFLOP/s: the denominator of the kNN filter's
+    roofline (MEASURED_PEAKS.json has bf16 only)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.randn(8192, 8192, device="cuda")
+        b = torch.randn(8192, 8192, device="cuda")
+        for _ in range(3):
+            a @ b
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return 2 * 8192 ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 def run_cfg2(args):
     """kNN graph construction alone (BASELINE config 2)."""
     import torch
@@ -711,49 +750,52 @@ def run_cfg2(args):
            "gram_useful_tflops": round(flops / (ms / 1e3) / 1e12, 2)}
     if tc:
         t_tc = tc[1] / tc[0]
-        out["roofline"] = {"bound": "tensor", "kernel": "knn_tc_filter", "achieved": round(3 * flops / (t_tc / 1e3) / 1e12, 1),
-                           "peak": 1100.0, "unit": "TFLOP/s", "frac": round(3 * flops / (t_tc / 1e3) / 1e12 / 1100.0, 4),
-                           "peak_source": "nominal dense TF32 (B200_PROFILING.md), 3 MMAs per product counted"}
+        peak_tf32 = measure_tf32_peak()
+        ach = 3 * flops / (t_tc / 1e3) / 1e12
+        out["roofline"] = {"bound": "tensor", "kernel": "knn_tc_filter", "achieved": round(ach, 1),
+                           "peak": round(peak_tf32, 1), "unit": "TFLOP/s", "frac": round(ach / peak_tf32, 4),
+                           "peak_source": "measured here: cuBLAS TF32 GEMM 8192^3, best of 10 (burst); 3 MMAs per "
+                                          "product counted", "nominal_tf32_dense": 1100.0}
     print(json.dumps(out), flush=True)
     if args.json_out:
         with open(args.json_out, "w") as f:
             json.dump(out, f)
 
 
-def run_cfg3(args):
-    """Decoder-only CG at scale (BASELINE config 3), one GPU."""
-    import torch
-
-    import paper_1602_02070_b200 as P
+def cfg3_problem(P, ctx, torch):
+    """The config-3 decoder problem: kNN graphs (K = 10) over N(0, I_64)
+    points (p = 4096 rows, n = 200 000 columns), plan 1/8 x 1/8, rank-20
+    low-pass right-hand side (workloads.config3_rhs); gamma-bar = 1."""
     from paper_1602_02070_b200 import workloads
 
     Pr, Pc = workloads.config3_points()
     p, n = Pr.shape[1], Pc.shape[1]
-    ctx = P.Context(0)
-    stream = torch.cuda.current_stream()
-    ctx.set_stream(stream.cuda_stream)
-    ctx.reserve(24 << 30)  # allocator warm-up (untimed): 4 p x n fp32 iterates + operators
     t0 = time.perf_counter()
     gr = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
     gc = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
     t_graphs = time.perf_counter() - t0
-    rs = np.random.default_rng(1606)
-
-    def lowpass(L, m, k=20, sweeps=20):
-        nrm = P.power_iteration_norm(L, 1e-7, 42, ctx=ctx)
-        B = torch.tensor(rs.standard_normal((m, k)), device="cuda")
-        for _ in range(sweeps):
-            B = B - L.multiply(B) / nrm
-        q, _ = torch.linalg.qr(B)
-        return q
-
-    Br, Bc = lowpass(gr.laplacian, p), lowpass(gc.laplacian, n)
     plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
-    A = torch.tensor(rs.standard_normal((20, 20)), device="cuda")
-    Xt = (Br[torch.tensor(plan.omega_r, device="cuda")] @ A @ Bc[torch.tensor(plan.omega_c, device="cuda")].T)
-    Xt = (Xt if args.fp64 else Xt.float()).t().contiguous().t()
+    Xt = workloads.config3_rhs(P, gr.laplacian, gc.laplacian, plan, ctx)
+    return gr, gc, plan, Xt, t_graphs
+
+
+def run_cfg3(args):
+    """Decoder-only CG at scale (BASELINE config 3), one GPU: 100 iterations
+    at 4096 x 200 000, fp32 data; by default fp64 Krylov vectors (the path
+    within 1e-4 of the fp64 solve)."""
+    import torch
+
+    import paper_1602_02070_b200 as P
+
+    ctx = P.Context(0)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    ctx.reserve(40 << 30)  # allocator warm-up (untimed)
+    gr, gc, plan, Xt64, t_graphs = cfg3_problem(P, ctx, torch)
+    p, n = plan.p, plan.n
+    Xt = Xt64 if args.fp64 else Xt64.float().t().contiguous().t()
     g1 = P.SpectralGap(lambda_k1=1.0)
-    dcfg = P.DecoderConfig(1.0, 1e-30, 100)
+    dcfg = P.DecoderConfig(1.0, 1e-30, 100, krylov_precision=args.krylov)
     ctx.reset_kernel_timing()
     ctx.enable_kernel_timing(True)
     res = {}
@@ -768,130 +810,122 @@ def run_cfg3(args):
     N = p * n
     nnz_r, nnz_c = gr.laplacian.nonzeros(), gc.laplacian.nonzeros()
     it = res["r"].iterations
-    # Algorithmic HBM bytes per CG iteration: apply reads P and writes AP
-    # (2N), residual reads R, AP and writes R (3N), update reads X, P, R and
-    # writes X, P (5N); plus one pass over both Laplacians.
-    wb = 8 if args.fp64 else 4
-    b_iter = 10 * N * wb + (nnz_r + nnz_c) * (wb + 4)
+    widths = decoder_widths(args.fp64, args.krylov)
+    wk, wx, wv = widths
+    dims = dict(N=N, nnz_r=nnz_r, nnz_c=nnz_c)
+    b_iter = sum(kernel_bytes(k, dims, widths) for k in ("cg_apply_lc", "cg_apply_lr", "cg_residual", "cg_update"))
     peak, src = measured_peaks()
-    kbytes = {"cg_apply": 2 * N * wb + (nnz_r + nnz_c) * (wb + 4),
-              "cg_apply_band": 2 * N * wb + nnz_c * (wb + 4),      # P read once, U written
-              "cg_apply_col": 3 * N * wb + nnz_r * (wb + 4),       # P, U read; AP written
-              "cg_residual": 3 * N * wb, "cg_update": 5 * N * wb}
-    kgbps = {k: round(kbytes[k] / (v[1] / v[0] / 1e3) / 1e9, 1) for k, v in kt.items() if k in kbytes}
+    per = {k: v[1] / max(v[0], 1) for k, v in kt.items()}
+    kgbps = {k: round(kernel_bytes(k, dims, widths) / (per[k] / 1e3) / 1e9, 1) for k in per
+             if kernel_bytes(k, dims, widths)}
+    survey = 6 * N * wk + (nnz_r + nnz_c) * (wv + 4)
     out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": 1, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64" if args.fp64 else "f32",
+           "vs_baseline": None, "dtype": "f64" if args.fp64 else f"f32 (Krylov vectors {args.krylov})",
            "data": "synthetic: seeded config-3 generator (N(0,I_64) points, rank-20 low-pass basis)",
            "config": {"workload": f"cfg3: alternate CG decoder, p={p}, n={n}, 1/8 x 1/8 sampling, {it} iterations",
                       "graphs_s_untimed": round(t_graphs, 3),
-                      "l2": "iterates (%.1f GB each) larger than L2; no flush" % (N * wb / 1e9)},
+                      "l2": "iterates (%.1f GB each) larger than L2; no flush" % (N * wk / 1e9)},
            "clocks": clk,
            "iters_per_s": round(it / (ms / 1e3), 1),
-           "cg_iteration_survey": {"bytes_B_iter": 6 * N * wb + (nnz_r + nnz_c) * (wb + 4),
-                                   "model": "SURVEY 8(d): 6 N w + (nnz_r + nnz_c)(w + 4)",
-                                   "achieved_GBps": round((6 * N * wb + (nnz_r + nnz_c) * (wb + 4)) * it / (ms / 1e3) / 1e9,
-                                                          1),
-                                   "frac_of_hbm": round((6 * N * wb + (nnz_r + nnz_c) * (wb + 4)) * it / (ms / 1e3) / 1e9
-                                                        / peak,
-                                                        4)},
-           "cg_iteration": {"bytes_B_iter": b_iter, "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
+           "cg_iteration": {"bytes": b_iter, "model": "sum of the four kernels' algorithmic bytes",
+                            "achieved_GBps": round(b_iter * it / (ms / 1e3) / 1e9, 1),
                             "frac_of_hbm": round(b_iter * it / (ms / 1e3) / 1e9 / peak, 4), "peak_source": src},
-           "kernel_ms_per_launch": {k: round(v[1] / v[0], 4) for k, v in kt.items()},
-           "kernel_algorithmic_GBps": kgbps}
+           "cg_iteration_survey": {"bytes_B_iter": survey, "model": "SURVEY 8(d): 6 N w + (nnz_r + nnz_c)(w + 4)",
+                                   "frac_of_hbm": round(survey * it / (ms / 1e3) / 1e9 / peak, 4)},
+           "kernel_ms_per_launch": {k: round(v, 4) for k, v in per.items()},
+           "kernel_algorithmic_GBps": kgbps,
+           "kernel_bytes_model": KERNEL_BYTES_DOC}
     print(json.dumps(out), flush=True)
     if args.json_out:
         with open(args.json_out, "w") as f:
             json.dump(out, f)
 
 
-def run_cfg3_sharded(args, rank, local_rank, world):
-    """cfg3 through alternate_decode_sharded: rank g owns columns
-    [g w, (g + 1) w) of the 4096 x 200 000 iterate, the search direction's
-    halo columns are exchanged (NCCL all-to-all) and the CG dots all-reduced
-    over NCCL every iteration.  Strong scaling: the problem is fixed, value = seconds per
-    decode (max over ranks)."""
+def cfg3_sharded_block(args, rank, local_rank, world, its=100, steps=2, warmup=1, krylov="fp64"):
+    """Config 3 through the device-resident column-sharded decoder
+    (cpcag_cuda_alternate_decode_sharded) on `world` ranks: strong scaling of
+    one decode (max over ranks, device events).  Returns a dict on rank 0."""
     import torch
     import torch.distributed as dist
 
     import paper_1602_02070_b200 as P
-    from paper_1602_02070_b200 import _native as N
-    from paper_1602_02070_b200 import workloads
-    from paper_1602_02070_b200.sharded import (CudaBlockBackend, HaloPlan, TorchCollectives, alternate_decode_sharded,
-                                               column_blocks)
+    from paper_1602_02070_b200.sharded import ShardComm, alternate_decode_sharded
 
-    torch.cuda.set_device(local_rank)
-    if "MASTER_ADDR" not in os.environ:
-        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
-    Pr, Pc = workloads.config3_points()
-    p, n = Pr.shape[1], Pc.shape[1]
     ctx = P.Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
-    ctx.reserve(16 << 30)
-    gr = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pr.T), device="cuda").t(), "cols", 10, ctx=ctx)
-    gc = P.build_knn_graph(torch.tensor(np.ascontiguousarray(Pc.T), device="cuda").t(), "cols", 10, ctx=ctx)
-    plan = P.draw_plan(p, n, p // 8, n // 8, seed=1607)
-    rs = np.random.default_rng(1606)
-    Xt = torch.tensor(rs.standard_normal((len(plan.omega_r), len(plan.omega_c))), device="cuda")
-    Xt = Xt.float().t().contiguous().t()
-    _, blocks = column_blocks(n, world)
-    c0, c1 = blocks[rank]
-    be = CudaBlockBackend(ctx, N.F32, plan, gr.laplacian, gc.laplacian, 1.0, 1.0, c0, c1)
-    coll = TorchCollectives()
-    zeros = lambda k: torch.zeros(k, dtype=torch.float32, device="cuda")
-    its = 100
+    ctx.reserve(24 << 30)
+    gr, gc, plan, Xt64, _ = cfg3_problem(P, ctx, torch)
+    Xt = Xt64.float().t().contiguous().t()
+    comm = ShardComm(ctx)
+    g1 = P.SpectralGap(lambda_k1=1.0)
+    dcfg = P.DecoderConfig(1.0, 1e-30, its, krylov_precision=krylov)
     res = {}
-    # halo exchange (only the X L_c columns each block needs move; BENCH_ALLGATHER=1: all-gather)
-    halo = None
-    if not os.environ.get("BENCH_ALLGATHER"):
-        rpc, cic, _ = gc.laplacian.arrays()
-        halo = HaloPlan(rpc, cic, n, world, rank)
 
-    def step():
-        res["r"] = alternate_decode_sharded(Xt, plan, be, coll, zeros, tol=1e-30, max_iter=its, halo=halo)
+    def step(measure=False):
+        res["r"] = alternate_decode_sharded(Xt, plan, gr.laplacian, gc.laplacian, g1, g1, dcfg, comm,
+                                            measure_exchange=measure, ctx=ctx)
 
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(warmup):
         step()
     dist.barrier()
     torch.cuda.synchronize()
     evs = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         step()
         b.record(stream)
         evs.append((a, b))
     torch.cuda.synchronize()
-    dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    step(measure=True)  # untimed: the exchange's own time on the comm stream
+    st = res["r"].stats
+    comm.close()
+    if rank != 0:
+        return None
     it = res["r"].iterations
+    return {"workload": f"cfg3: p={plan.p}, n={plan.n}, {it} CG iterations, column blocks over {world} ranks",
+            "value_s": round(ms / 1e3, 5), "iters_per_s": round(it / (ms / 1e3), 1), "scaling": "strong",
+            "krylov": krylov, "halo_cols_rank0": st.halo_cols, "send_cols_rank0": st.send_cols,
+            "halo_bytes_per_iteration_rank0": st.bytes_per_iteration,
+            "exchange_ms_per_iteration_rank0": round(st.exchange_ms / max(it, 1), 4),
+            "nvlink_GBps_rank0": round(st.bytes_per_iteration / (st.exchange_ms / max(it, 1) / 1e3) / 1e9, 1)
+            if st.exchange_ms > 0 else None}
+
+
+def run_cfg3_sharded(args, rank, local_rank, world):
+    """cfg3 through the sharded decoder at the launched world size."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    if "MASTER_ADDR" not in os.environ:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29531"))
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local_rank))
+    blk = cfg3_sharded_block(args, rank, local_rank, world, steps=args.steps, warmup=max(args.warmup, 1),
+                             krylov=args.krylov)
     if rank == 0:
-        out = {"metric": METRIC, "value": round(ms / 1e3, 5), "unit": "s", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
-               "vs_baseline": None, "dtype": "f32", "data": "synthetic: seeded config-3 generator",
-               "config": {"workload": f"cfg3 sharded: column-block CG over NCCL, p={p}, n={n}, "
-                                      f"1/8 x 1/8 sampling, {it} iterations", "parallelism": f"colblock{world}",
-                          "block_cols": c1 - c0,
-                          "exchange": ("halo all-to-all: rank 0 receives %d of its %d remote columns (%.1f %%)"
-                                       % (halo.halo_cols, halo.remote_cols,
-                                          100.0 * halo.halo_cols / max(halo.remote_cols, 1))) if halo
-                          else "all-gather of the column blocks"},
-               "iters_per_s": round(it / (ms / 1e3), 1)}
+        out = {"metric": METRIC, "value": blk["value_s"], "unit": "s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(blk["value_s"] * 1e3, 3), "higher_is_better": False,
+               "scaling": "strong", "vs_baseline": None, "dtype": f"f32 (Krylov vectors {args.krylov})",
+               "data": "synthetic: seeded config-3 generator",
+               "config": {"workload": blk["workload"], "parallelism": f"colblock{world}"}, "sharded": blk}
         print(json.dumps(out), flush=True)
         if args.json_out:
             with open(args.json_out, "w") as f:
                 json.dump(out, f)
-    be.close()
     dist.destroy_process_group()
 
 
 def main():
     args = parse()
+    if args.krylov is None:
+        args.krylov = "fp64" if args.config == "cfg3" else "fp32"
     rank, local_rank, world = dist_env()
     if args.config == "cfg0" and args.impl == "ours":
         return run_cfg0(args)

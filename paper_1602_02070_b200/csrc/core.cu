@@ -595,14 +595,8 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   CUDA_OK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   DevBuf<PowerState> st(c, 1);
   st.zero(c);
-  if (std::getenv("CPCAG_POWER_PROF")) {
-    PowerState ps{};
-    ps.prof = 1;
-    CUDA_OK(cudaMemcpyAsync(st.p, &ps, sizeof(ps), cudaMemcpyHostToDevice, c->stream));
-  }
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
-  i64 small_nnz = 4096;  // single-CTA kernel (no grid barrier) up to this many entries
-  if (const char* e = std::getenv("CPCAG_POWER_SMALL_NNZ")) small_nnz = std::atoll(e);
+  const i64 small_nnz = 4096;  // single-CTA kernel (no grid barrier) up to this many entries
   if (small_smem <= 200 * 1024 && A->nnz <= small_nnz) {
     ensure_smem(power_iter_small_k, small_smem);
     {
@@ -615,8 +609,7 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   // One CTA per SM (at most one per row): measured, the per-iteration cost is
   // the in-CTA product, so spreading it wins over the cheaper barrier of a
   // smaller grid (cfg1: 148 CTAs 7.4 ms, 40 CTAs 9.5 ms, 8 CTAs 31 ms).
-  i64 want = c->num_sms;
-  if (const char* e = std::getenv("CPCAG_POWER_NB")) want = std::max<i64>(1, std::atoll(e));
+  const i64 want = c->num_sms;
   const unsigned nb = static_cast<unsigned>(std::max<i64>(1, std::min<i64>({static_cast<i64>(c->num_sms), want, n})));
   std::vector<i64> rph(static_cast<size_t>(n) + 1);
   CUDA_OK(cudaMemcpyAsync(rph.data(), A->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));

@@ -71,6 +71,31 @@ __device__ __forceinline__ void finish_reduction(double s, const Combine<TK, TB>
   if (grid_sum_last<1>(v, cb.partials, &cb.st->cnt[1], tot) && threadIdx.x == 0) cb.st->curv = tot[0];
 }
 
+
+// Loads through the L2 with an evict_last policy: the lc pass re-reads the
+// whole L_c (entries) once per row band, and the streamed band and U writes
+// must not push it out of L2.
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float ld_keep(const float* a, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_keep(const int* a, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+
 // ------------------------------------------------------------------ fused apply (iterates resident in L2)
 // AP = gc P Lc + gr Lr P (+ P on the sampled grid) in one pass for problems
 // whose Krylov vectors stay in L2 (config 1: 10 304 x 1 000).  CTA = 512
@@ -403,6 +428,9 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) lc_k(int p, int ncols, int
   const TI* Pr = kSmem ? Pb + r : P + i;
   const i64 jstride = kSmem ? S : p;
   const int ca0 = kSmem ? 0 : chunk * cpc, ca1 = kSmem ? ncols : min(ncols, ca0 + cpc);
+  const uint64_t keep = l2_keep_policy();
+  auto ldv = [&](i64 k) { return kSmem ? L.v[k] : ld_keep(L.v + k, keep); };
+  auto ldj = [&](i64 k) { return kSmem ? L.ci[k] : ld_keep(L.ci + k, keep); };
   const int nwk = nwarps * G, wk = warp * G + half;
   const int wa = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * wk) / nwk);
   const int wb = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * (wk + 1)) / nwk);
@@ -417,12 +445,12 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) lc_k(int p, int ncols, int
     TV va = TV(0), vb = TV(0);
     int ja = 0, jb = 0;
     if (r < deg) {
-      va = L.v[k0 + r];
-      ja = L.ci[k0 + r];
+      va = ldv(k0 + r);
+      ja = ldj(k0 + r);
     }
     if (r + S < deg) {
-      vb = L.v[k0 + r + S];
-      jb = L.ci[k0 + r + S];
+      vb = ldv(k0 + r + S);
+      jb = ldj(k0 + r + S);
     }
     for (int cc = 0; cc < cnt; ++cc) {
       // prefetch the next column's entries
@@ -434,30 +462,31 @@ __global__ void __launch_bounds__(kSmem ? 1024 : 256) lc_k(int p, int ncols, int
         k0n = __shfl_sync(hmask, kst_l, cc + 1, S);
         degn = static_cast<int>(__shfl_sync(hmask, ken_l, cc + 1, S) - k0n);
         if (r < degn) {
-          van = L.v[k0n + r];
-          jan = L.ci[k0n + r];
+          van = ldv(k0n + r);
+          jan = ldj(k0n + r);
         }
         if (r + S < degn) {
-          vbn = L.v[k0n + r + S];
-          jbn = L.ci[k0n + r + S];
+          vbn = ldv(k0n + r + S);
+          jbn = ldj(k0n + r + S);
         }
       }
       TK a = TK(0);
       // batches of 8 entries: 8 independent gathers in flight, then the 8
       // accumulation steps in CSR order (entries past the row end gather
       // column 0 and are not accumulated)
+      constexpr int BT = 8;  // gathers in flight per batch
       auto slot = [&](TV vs, int js, int cnt_s) {
-        for (int t0 = 0; t0 < cnt_s; t0 += 8) {
-          TV v[8];
-          TI x[8];
+        for (int t0 = 0; t0 < cnt_s; t0 += BT) {
+          TV v[BT];
+          TI x[BT];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < BT; ++u) {
             v[u] = __shfl_sync(hmask, vs, (t0 + u) & (S - 1), S);
             const int j = __shfl_sync(hmask, js, (t0 + u) & (S - 1), S);
             x[u] = kSmem ? Pr[j * jstride] : __ldg(Pr + j * jstride);
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < BT; ++u)
             if (t0 + u < cnt_s) a = acc<TK>(a, static_cast<TK>(v[u]), static_cast<TK>(x[u]));
         }
       };
@@ -617,12 +646,16 @@ __device__ __forceinline__ void stage_tile(TI* W, int wl, const TI* __restrict__
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
+// sync (non-null): the groups share every tile (full windows); the CTAs of a
+// stripe advance in lockstep (at most one tile apart, counted in sync[stripe];
+// the launch is cooperative, so they are co-resident) and each staged tile is
+// read from HBM once, then from L2 by the other groups.
 template <typename TI, typename TK, typename TV, int C, int EV, int T, bool kCombine, typename TB>
 __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, const LrGroup* __restrict__ groups,
                                                  const int* __restrict__ vrow_row, const int* __restrict__ vrow_np,
                                                  const TV* __restrict__ ev, const int* __restrict__ ej, int wl_max,
                                                  const TI* __restrict__ P, TK* __restrict__ U, i64 col_base,
-                                                 Combine<TK, TB> cb) {
+                                                 Combine<TK, TB> cb, unsigned* sync, int ngroups) {
   if (cb.st && cb.st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int g = blockIdx.x / stripes, stripe = blockIdx.x % stripes;
@@ -649,9 +682,15 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
   int tile = stripe;
   if (tile < ntiles) stage_tile(W0, gr.wl, P, p, gr.w0, tile * C, C, ncols, vec);
   int b = 0;
-  for (; tile < ntiles; tile += stripes, b ^= 1) {
+  for (int ti = 0; tile < ntiles; tile += stripes, b ^= 1, ++ti) {
     TI* W = b ? W1 : W0;
     const int nxt = tile + stripes;
+    if (sync && ti > 0) {  // every group of the stripe finished tile ti - 1 before its buffer is restaged
+      if (threadIdx.x == 0)
+        while (ld_acquire_gpu(sync + stripe) < static_cast<unsigned>(ngroups * ti)) {
+        }
+      __syncthreads();
+    }
     if (nxt < ntiles) {
       stage_tile(b ? W0 : W1, gr.wl, P, p, gr.w0, nxt * C, C, ncols, vec);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -706,6 +745,10 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
       }
     }
     __syncthreads();  // the buffer is restaged two tiles on
+    if (sync && threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(sync + stripe, 1u);
+    }
   }
   if constexpr (kCombine) finish_reduction(s, cb);
 }
@@ -914,6 +957,8 @@ struct ApplyPlan {
   DevBuf<LrGroup> groups;
   DevBuf<int> vrow_row, vrow_np, ej;
   DevBuf<unsigned char> ev;  // TV values, ELL-interleaved
+  bool lr_sync = false;      // groups share every tile: lockstep stripes (cooperative launch)
+  DevBuf<unsigned> lr_cnt;
   // lr pass, generic fallback (lr_k)
   DevBuf<RowRange> ranges;
   int n_ranges = 0;
@@ -1038,6 +1083,10 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
       // one wave: stripes x groups <= resident CTAs
       ap.lr_stripes = static_cast<int>(
           std::max<i64>(1, std::min<i64>(tiles, (static_cast<i64>(c->num_sms) * per_sm) / ap.lr_groups)));
+      bool same = grp.size() > 1;
+      for (const auto& g : grp) same = same && g.w0 == grp[0].w0 && g.wl == grp[0].wl;
+      ap.lr_sync = same;
+      if (same) ap.lr_cnt.alloc(c, static_cast<size_t>(ap.lr_stripes));
       const size_t ne = static_cast<size_t>(grp.size()) * EV * T;
       std::vector<TV> hv(ne, TV(0));
       std::vector<int> hj(ne, 0);
@@ -1161,9 +1210,25 @@ template <typename TI, typename TK, typename TV, int C, int EV, int T, typename 
 void launch_lr_reg(Ctx* c, const ApplyPlan& ap, const TI* P, TK* U, const Combine<TK, TB>& cb, bool combine) {
   auto k = combine ? lr_reg_k<TI, TK, TV, C, EV, T, true, TB> : lr_reg_k<TI, TK, TV, C, EV, T, false, TB>;
   ensure_smem(k, ap.lr_smem);
-  k<<<static_cast<unsigned>(ap.lr_groups * ap.lr_stripes), T, ap.lr_smem, c->stream>>>(
-      static_cast<int>(ap.p), static_cast<int>(ap.ncols), ap.lr_stripes, ap.groups.p, ap.vrow_row.p, ap.vrow_np.p,
-      reinterpret_cast<const TV*>(ap.ev.p), ap.ej.p, ap.lr_wl_max, P, U, ap.col_base, cb);
+  const unsigned grid = static_cast<unsigned>(ap.lr_groups * ap.lr_stripes);
+  int p_ = static_cast<int>(ap.p), n_ = static_cast<int>(ap.ncols), st_ = ap.lr_stripes, wl_ = ap.lr_wl_max,
+      ng_ = ap.lr_groups;
+  if (!ap.lr_sync) {
+    k<<<grid, T, ap.lr_smem, c->stream>>>(p_, n_, st_, ap.groups.p, ap.vrow_row.p, ap.vrow_np.p,
+                                          reinterpret_cast<const TV*>(ap.ev.p), ap.ej.p, wl_, P, U, ap.col_base, cb,
+                                          nullptr, ng_);
+    return;
+  }
+  CUDA_OK(cudaMemsetAsync(ap.lr_cnt.p, 0, sizeof(unsigned) * ap.lr_stripes, c->stream));
+  const LrGroup* g_ = ap.groups.p;
+  const int *vr_ = ap.vrow_row.p, *vn_ = ap.vrow_np.p, *ej_ = ap.ej.p;
+  const TV* ev_ = reinterpret_cast<const TV*>(ap.ev.p);
+  i64 cbase = ap.col_base;
+  Combine<TK, TB> cb_ = cb;
+  unsigned* cnt_ = ap.lr_cnt.p;
+  void* args[] = {&p_, &n_, &st_, &g_, &vr_, &vn_, &ev_, &ej_, &wl_, &P, &U, &cbase, &cb_, &cnt_, &ng_};
+  CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(T), args, ap.lr_smem,
+                                      c->stream));
 }
 
 template <typename TI, typename TK, typename TV, int C, typename TB>

@@ -18,7 +18,6 @@
 
 #include "common.cuh"
 #include "frpcag.cuh"
-#include "fista_tc.cuh"
 #include "fista_persist.cuh"
 
 namespace cpcag_cuda {
@@ -583,7 +582,7 @@ struct LinLauncher {  // fp32 only; other precisions never take the linearity pa
                    const LinBufs&, FistaState*) {}
   static void step(Ctx*, dim3, unsigned, i64, i64, const T*, const T*, T, T, int, int, const cpcag_frpcag_config&, T,
                    const T*, const T*, T*, const T*, T*, const SplitWs&, const LinBufs&, i64, double*, double*,
-                   FistaState*, const FistaTcPlan*, float*, float*) {}
+                   FistaState*) {}
 };
 template <>
 struct LinLauncher<float> {
@@ -599,7 +598,7 @@ struct LinLauncher<float> {
   static void step(Ctx* c, dim3 g, unsigned eb, i64 rr, i64 rc, const float* Lr, const float* Lc, float s_r, float s_c,
                    int use_r, int use_c, const cpcag_frpcag_config& cfg, float stepT, const float* Z, const float* Y,
                    float* S, const float* Sp, float* Zn, const SplitWs& ws, const LinBufs& lb, i64 j, double* partials,
-                   double* trace, FistaState* st, const FistaTcPlan* tcp, float* Zh, float* Zl) {
+                   double* trace, FistaState* st) {
     const i64 m = rr * rc;
     {
       KScope ks_(c, "fista_grad_prox");
@@ -609,12 +608,9 @@ struct LinLauncher<float> {
     }
     {
       KScope ks_(c, "fista_objective");
-      // L~_r S on the tensor cores when planned (the CUDA-core split-K kernel
-      // then only forms S L~_c and zeroes part1, which the TC kernel fills).
-      fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, tcp ? 0 : cfg.gamma_r != 0.0,
-                                                       cfg.gamma_c != 0.0, S, ws, st);
+      fista_splitk_partial_k<<<g, 256, 0, c->stream>>>(rr, rc, Lr, Lc, cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, S, ws,
+                                                       st);
       launched(c);
-      if (tcp) fista_tc_part1(c, *tcp, S, Zh, Zl, ws.part1, &st->done);
       fista_lin_objective_k<<<eb, 256, 0, c->stream>>>(rr, rc, static_cast<int>(g.z), cfg.gamma_r, cfg.gamma_c,
                                                        cfg.loss, S, Y, ws, lb.LSr[j & 1], lb.LSc[j & 1], partials,
                                                        trace, st);
@@ -738,7 +734,6 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     const unsigned tiles = gk.x * gk.y;
     unsigned S = static_cast<unsigned>(std::max<i64>(1, (2 * static_cast<i64>(c->num_sms)) / tiles));  // measured: ~8 splits best at cfg1
     S = static_cast<unsigned>(std::min<i64>({static_cast<i64>(S), (rows + cols) / (4 * kSK) + 1, 32}));
-    if (const char* e = std::getenv("CPCAG_FISTA_SPLITS")) S = static_cast<unsigned>(std::max(1, std::atoi(e)));
     gk.z = S;
     sp1.alloc(c, static_cast<size_t>(S) * N);
     sp2.alloc(c, static_cast<size_t>(S) * N);
@@ -748,8 +743,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     ws = SplitWs{sp1.p, sp2.p, scnt.p, scnt.p + tiles, ssum.p};
   }
   // Linearity variant (fp32 split-K): one GEMM pair per iteration.
-  bool lin = splitk;
-  if (const char* e = std::getenv("CPCAG_FISTA_LIN")) lin = lin && std::string(e) != "0";
+  const bool lin = splitk;
   DevBuf<T> lbuf;
   LinBufs lb{};
   if (lin) {
@@ -758,26 +752,6 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
     lb = LinBufs{b, b + N, {b + 2 * N, b + 3 * N}, {b + 4 * N, b + 5 * N}};
     LinLauncher<T>::init(c, gk, nb1, rows, cols, Dr.p, Dc.p, use_r, use_c, Y, ws, lb, st.p);
   }
-  // Tensor-core L~_r S (fp32 linearity path): 3xTF32 tcgen05.  Opt-in
-  // (CPCAG_FISTA_TC=1): at config-1 size the product is overhead-bound (split-K
-  // workspace traffic and launches), and the TC route measured 17.0 ms vs
-  // 13.8 ms for the CUDA-core split-K over 300 iterations.
-  const char* tce = std::getenv("CPCAG_FISTA_TC");
-  const bool use_tc = tce && std::string(tce) == "1" && lin && use_r && sizeof(T) == 4 &&
-                      fista_tc_supported(rows, cols, static_cast<int>(gk.z));
-  FistaTcPlan tcp;
-  DevBuf<float> tcb;
-  float *Zh = nullptr, *Zl = nullptr;
-  if (use_tc) {
-    const i64 ld = (rows + 3) / 4 * 4;
-    tcb.alloc(c, static_cast<size_t>(ld) * (2 * rows + 2 * cols));
-    float* Ah = tcb.p;
-    float* Al = Ah + ld * rows;
-    Zh = Al + ld * rows;
-    Zl = Zh + ld * cols;
-    fista_tc_setup(c, rows, cols, static_cast<int>(gk.z), reinterpret_cast<const float*>(Dr.p), Ah, Al, Zh, Zl, &tcp);
-  }
-
   i64 j = 1;
   FistaState host{};
   const i64 chunk = 32;
@@ -790,7 +764,7 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
       T* Znext = Zb[(j + 1) & 1].p;
       if (lin) {
         LinLauncher<T>::step(c, gk, nb1, rows, cols, Dr.p, Dc.p, s_r, s_c, use_r, use_c, cfg, stepT, Zj, Y, Sj, Sprev,
-                             Znext, ws, lb, j, part.p, tr.p, st.p, use_tc ? &tcp : nullptr, Zh, Zl);
+                             Znext, ws, lb, j, part.p, tr.p, st.p);
         continue;
       }
       if (splitk) {

