@@ -368,7 +368,7 @@ typedef struct cpcag_pipeline_config { /* PipelineConfig subset, pipeline.hpp:36
   cpcag_approx_config approx; /* the approximate decoder's DecoderConfig fields */
   int task;                  /* Task (pipeline.hpp:18): CPCAG_TASK_LOWRANK (default), _CLUSTER or _BOTH */
   int64_t n_clusters;        /* clustering: k (0 = max(1, detected rank)), pipeline.cpp:374 */
-  int64_t kmeans_restarts;   /* default 10 */
+  int64_t kmeans_restarts;   /* default 10; < 1 is rejected (clustering.cpp:129) */
 } cpcag_pipeline_config;
 
 enum { CPCAG_TASK_LOWRANK = 0, CPCAG_TASK_CLUSTER = 1, CPCAG_TASK_BOTH = 2 };

@@ -486,9 +486,11 @@ __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __re
 __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __restrict__ rp,
                                                          const int* __restrict__ ci,
                                                          const double* __restrict__ val,
-                                                         const double* __restrict__ v0, double* wbuf,
+                                                         double* v0, double* wbuf,
                                                          double* partials, double tol, i64 max_iter,
                                                          int slice_in_smem, int v_in_smem, PowerState* st) {
+  // v0 is rewritten in place between grid barriers when it does not fit in
+  // shared memory: plain (coherent) loads only, never the read-only path.
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const unsigned nb = gridDim.x;
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
     } else {
       // v lives in global memory: the grid renormalises its own rows and
       // needs a second barrier before the next product reads them.
-      double* vg = const_cast<double*>(v0);
+      double* vg = v0;
       for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(__ldcg(w + i), nrm);
     }
     mark(3);

@@ -208,7 +208,7 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
       DevBuf<double> Xd(c, static_cast<size_t>(std::max<i64>(rho_r * rho_c, 1)));
       to_f64_device(c, Xt_out, rho_r * rho_c, Xd.p);
       DevBuf<int> sl(c, static_cast<size_t>(std::max<i64>(rho_c, 1))), lab(c, static_cast<size_t>(n));
-      kmeans_device(c, Xd.p, rho_r, rho_c, k, cfg.kmeans_restarts > 0 ? cfg.kmeans_restarts : 10,
+      kmeans_device(c, Xd.p, rho_r, rho_c, k, cfg.kmeans_restarts,
                     HostRng::mix(cfg.seed ^ 0x6b6d65616eULL), 100, sl.p, nullptr);
       decode_labels_device(c, Lc.get(), om_c, sl.p, k, cfg.decoder.pcg_tol, cfg.decoder.pcg_max_iter, n, lab.p);
       if (factors && factors->labels)
