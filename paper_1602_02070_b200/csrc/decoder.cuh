@@ -646,16 +646,12 @@ __device__ __forceinline__ void stage_tile(TI* W, int wl, const TI* __restrict__
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// sync (non-null): the groups share every tile (full windows); the CTAs of a
-// stripe advance in lockstep (at most one tile apart, counted in sync[stripe];
-// the launch is cooperative, so they are co-resident) and each staged tile is
-// read from HBM once, then from L2 by the other groups.
 template <typename TI, typename TK, typename TV, int C, int EV, int T, bool kCombine, typename TB>
 __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, const LrGroup* __restrict__ groups,
                                                  const int* __restrict__ vrow_row, const int* __restrict__ vrow_np,
                                                  const TV* __restrict__ ev, const int* __restrict__ ej, int wl_max,
                                                  const TI* __restrict__ P, TK* __restrict__ U, i64 col_base,
-                                                 Combine<TK, TB> cb, unsigned* sync, int ngroups) {
+                                                 Combine<TK, TB> cb) {
   if (cb.st && cb.st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   const int g = blockIdx.x / stripes, stripe = blockIdx.x % stripes;
@@ -682,15 +678,9 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
   int tile = stripe;
   if (tile < ntiles) stage_tile(W0, gr.wl, P, p, gr.w0, tile * C, C, ncols, vec);
   int b = 0;
-  for (int ti = 0; tile < ntiles; tile += stripes, b ^= 1, ++ti) {
+  for (; tile < ntiles; tile += stripes, b ^= 1) {
     TI* W = b ? W1 : W0;
     const int nxt = tile + stripes;
-    if (sync && ti > 0) {  // every group of the stripe finished tile ti - 1 before its buffer is restaged
-      if (threadIdx.x == 0)
-        while (ld_acquire_gpu(sync + stripe) < static_cast<unsigned>(ngroups * ti)) {
-        }
-      __syncthreads();
-    }
     if (nxt < ntiles) {
       stage_tile(b ? W0 : W1, gr.wl, P, p, gr.w0, nxt * C, C, ncols, vec);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
@@ -745,10 +735,6 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
       }
     }
     __syncthreads();  // the buffer is restaged two tiles on
-    if (sync && threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(sync + stripe, 1u);
-    }
   }
   if constexpr (kCombine) finish_reduction(s, cb);
 }
@@ -957,8 +943,6 @@ struct ApplyPlan {
   DevBuf<LrGroup> groups;
   DevBuf<int> vrow_row, vrow_np, ej;
   DevBuf<unsigned char> ev;  // TV values, ELL-interleaved
-  bool lr_sync = false;      // groups share every tile: lockstep stripes (cooperative launch)
-  DevBuf<unsigned> lr_cnt;
   // lr pass, generic fallback (lr_k)
   DevBuf<RowRange> ranges;
   int n_ranges = 0;
@@ -1083,10 +1067,6 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
       // one wave: stripes x groups <= resident CTAs
       ap.lr_stripes = static_cast<int>(
           std::max<i64>(1, std::min<i64>(tiles, (static_cast<i64>(c->num_sms) * per_sm) / ap.lr_groups)));
-      bool same = grp.size() > 1;
-      for (const auto& g : grp) same = same && g.w0 == grp[0].w0 && g.wl == grp[0].wl;
-      ap.lr_sync = same;
-      if (same) ap.lr_cnt.alloc(c, static_cast<size_t>(ap.lr_stripes));
       const size_t ne = static_cast<size_t>(grp.size()) * EV * T;
       std::vector<TV> hv(ne, TV(0));
       std::vector<int> hj(ne, 0);
@@ -1210,25 +1190,9 @@ template <typename TI, typename TK, typename TV, int C, int EV, int T, typename 
 void launch_lr_reg(Ctx* c, const ApplyPlan& ap, const TI* P, TK* U, const Combine<TK, TB>& cb, bool combine) {
   auto k = combine ? lr_reg_k<TI, TK, TV, C, EV, T, true, TB> : lr_reg_k<TI, TK, TV, C, EV, T, false, TB>;
   ensure_smem(k, ap.lr_smem);
-  const unsigned grid = static_cast<unsigned>(ap.lr_groups * ap.lr_stripes);
-  int p_ = static_cast<int>(ap.p), n_ = static_cast<int>(ap.ncols), st_ = ap.lr_stripes, wl_ = ap.lr_wl_max,
-      ng_ = ap.lr_groups;
-  if (!ap.lr_sync) {
-    k<<<grid, T, ap.lr_smem, c->stream>>>(p_, n_, st_, ap.groups.p, ap.vrow_row.p, ap.vrow_np.p,
-                                          reinterpret_cast<const TV*>(ap.ev.p), ap.ej.p, wl_, P, U, ap.col_base, cb,
-                                          nullptr, ng_);
-    return;
-  }
-  CUDA_OK(cudaMemsetAsync(ap.lr_cnt.p, 0, sizeof(unsigned) * ap.lr_stripes, c->stream));
-  const LrGroup* g_ = ap.groups.p;
-  const int *vr_ = ap.vrow_row.p, *vn_ = ap.vrow_np.p, *ej_ = ap.ej.p;
-  const TV* ev_ = reinterpret_cast<const TV*>(ap.ev.p);
-  i64 cbase = ap.col_base;
-  Combine<TK, TB> cb_ = cb;
-  unsigned* cnt_ = ap.lr_cnt.p;
-  void* args[] = {&p_, &n_, &st_, &g_, &vr_, &vn_, &ev_, &ej_, &wl_, &P, &U, &cbase, &cb_, &cnt_, &ng_};
-  CUDA_OK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(T), args, ap.lr_smem,
-                                      c->stream));
+  k<<<static_cast<unsigned>(ap.lr_groups * ap.lr_stripes), T, ap.lr_smem, c->stream>>>(
+      static_cast<int>(ap.p), static_cast<int>(ap.ncols), ap.lr_stripes, ap.groups.p, ap.vrow_row.p, ap.vrow_np.p,
+      reinterpret_cast<const TV*>(ap.ev.p), ap.ej.p, ap.lr_wl_max, P, U, ap.col_base, cb);
 }
 
 template <typename TI, typename TK, typename TV, int C, typename TB>

@@ -143,8 +143,27 @@ def config0_workload(seed: int = 1602) -> Workload:
 
 
 def _lambda_k1_of_knn(Y, axis_rows, K, k):
-    pts = Y if axis_rows else Y.T
-    L = knn_laplacian_dense(np.ascontiguousarray(pts.T), K)
+    """lambda_{k+1} of the kNN Laplacian of Y's rows or columns (the decoder's
+    spectral gap, pipeline.cpp:343-349).  The graph comes from the library's
+    build_knn_graph when a GPU is present: its canonical fp64 distances are
+    the same on every machine, so near-tie neighbour choices (and with them
+    lambda) no longer depend on the host BLAS (round 1 saw 0.063-0.10 for
+    config 1 across boxes).  Without a GPU (CPU-only tests) the numpy Gram
+    form is used."""
+    try:
+        import torch
+
+        have_gpu = torch.cuda.is_available()
+    except ImportError:
+        have_gpu = False
+    if have_gpu:
+        from . import cpcag as P
+
+        g = P.build_knn_graph(np.asfortranarray(Y, dtype=np.float64), "rows" if axis_rows else "cols", K)
+        L = g.laplacian.to_dense()
+    else:
+        pts = Y if axis_rows else Y.T
+        L = knn_laplacian_dense(np.ascontiguousarray(pts.T), K)
     ev = np.linalg.eigvalsh(0.5 * (L + L.T))
     return float(max(ev[k], 1e-12))
 
