@@ -374,144 +374,107 @@ __global__ void __launch_bounds__(kLcSmemThreads) lc_smem_k(int p, int ncols, in
   if constexpr (kCombine) finish_reduction(s, cb);
 }
 
-// ------------------------------------------------------------------ lc pass
-// U = P Lc over row bands of S = 128 B / sizeof(TI) rows.  kSmem: one CTA
-// per band copies the band's segment of all n_local columns to shared memory
-// (n x 128 B) and gathers from there; otherwise (n too large) the grid is
-// band-major (blockIdx.x = band * chunks + chunk) so the CTAs in flight share
-// one band of S rows x all columns (n x 128 B), which stays resident in L2,
-// and the gathers are 128-byte global reads.  lane = row of the band (half
-// warps in fp64).  Each (half) warp owns a contiguous range of columns: the
-// row pointers of S columns at a time sit one per lane, and the L_c row of
-// the next column is loaded (one entry per lane, two slots) while the current
-// one is gathered; entries are broadcast by shuffle, in CSR order.
-template <typename TI, typename TK, typename TV, bool kSmem, bool kCombine, typename TB>
-__global__ void __launch_bounds__(kSmem ? 1024 : 256) lc_k(int p, int ncols, int nload, int chunks, int cpc,
-                                                           Pull<TV> L, const TI* __restrict__ P, TK* __restrict__ U,
-                                                           i64 col_base, Combine<TK, TB> cb) {
-  constexpr int S = 128 / sizeof(TI);
-  constexpr int G = 32 / S;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  TI* Pb = reinterpret_cast<TI*>(smraw);  // [nload][S]
+// ------------------------------------------------------------------ lc pass, band resident in L2
+// U = P Lc when the band of all columns does not fit in shared memory
+// (config 3/4): bands of 32 rows, the grid band-major (blockIdx.x = band *
+// chunks + chunk) so the CTAs in flight share one band of 32 rows x all
+// columns (<= 51 MB in fp64), which stays resident in L2; lane = row, one
+// warp per output column, each gather a 128/256-byte line group.  Each warp
+// owns a contiguous range of columns: the row pointers of 32 columns at a time
+// sit one per lane, and the L_c row of the next column is loaded (one entry
+// per lane, two slots, with an L2 evict_last policy so the whole L_c stays
+// cached across bands) while the current one is gathered in batches of 8
+// independent loads; entries are broadcast by shuffle, accumulated in CSR
+// order.
+template <typename TI, typename TK, typename TV, bool kCombine, typename TB>
+__global__ void __launch_bounds__(256) lc_k(int p, int ncols, int chunks, int cpc, Pull<TV> L,
+                                            const TI* __restrict__ P, TK* __restrict__ U, i64 col_base,
+                                            Combine<TK, TB> cb) {
   if (cb.st && cb.st->done) return;
-  const int band = kSmem ? blockIdx.x : blockIdx.x / chunks;
-  const int chunk = kSmem ? 0 : blockIdx.x % chunks;
-  const int i0 = band * S;
-  const int rows = min(S, p - i0);
-  if constexpr (kSmem) {
-    const bool vec = rows == S && (reinterpret_cast<uintptr_t>(P) % 16 == 0) &&
-                     ((static_cast<i64>(p) * sizeof(TI)) % 16 == 0);
-    if (vec) {
-      constexpr int CH = 128 / 16;
-      const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(Pb));
-      for (int q = threadIdx.x; q < nload * CH; q += blockDim.x) {
-        const int c = q / CH, k = q % CH;
-        const TI* src = P + static_cast<i64>(c) * p + i0 + k * (16 / sizeof(TI));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sbase + static_cast<unsigned>(q) * 16u),
-                     "l"(src)
-                     : "memory");
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-    } else {
-      for (int q = threadIdx.x; q < nload * S; q += blockDim.x) {
-        const int c = q / S, r = q % S;
-        Pb[q] = r < rows ? P[static_cast<i64>(c) * p + i0 + r] : TI(0);
-      }
-    }
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int half = lane / S, r = lane % S;
-  const unsigned hmask = S == 32 ? 0xffffffffu : (0xffffu << (16 * half));
+  const int band = blockIdx.x / chunks, chunk = blockIdx.x % chunks;
+  const int i0 = band * 32;
+  const int rows = min(32, p - i0);
+  const int r = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const bool vrow = r < rows;
   const i64 i = i0 + (vrow ? r : 0);
-  const TI* Pr = kSmem ? Pb + r : P + i;
-  const i64 jstride = kSmem ? S : p;
-  const int ca0 = kSmem ? 0 : chunk * cpc, ca1 = kSmem ? ncols : min(ncols, ca0 + cpc);
+  const TI* Pr = P + i;
+  const i64 jstride = p;
+  const int ca0 = chunk * cpc, ca1 = min(ncols, ca0 + cpc);
   const uint64_t keep = l2_keep_policy();
-  auto ldv = [&](i64 k) { return kSmem ? L.v[k] : ld_keep(L.v + k, keep); };
-  auto ldj = [&](i64 k) { return kSmem ? L.ci[k] : ld_keep(L.ci + k, keep); };
-  const int nwk = nwarps * G, wk = warp * G + half;
-  const int wa = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * wk) / nwk);
-  const int wb = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * (wk + 1)) / nwk);
+  auto ldv = [&](i64 k) { return ld_keep(L.v + k, keep); };
+  auto ldj = [&](i64 k) { return ld_keep(L.ci + k, keep); };
+  const int wa = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * warp) / nwarps);
+  const int wb = ca0 + static_cast<int>((static_cast<i64>(ca1 - ca0) * (warp + 1)) / nwarps);
   double s = 0.0;
-  for (int c0 = wa; c0 < wb; c0 += S) {
-    const int cnt = min(S, wb - c0);
+  for (int c0 = wa; c0 < wb; c0 += 32) {
+    const int cnt = min(32, wb - c0);
     const i64 kst_l = r < cnt ? L.rp[c0 + r] : 0;
     const i64 ken_l = r < cnt ? L.rp[c0 + r + 1] : 0;
-    // entries of column 0 of the chunk: two slots per lane (entries r, r + S)
-    i64 k0 = __shfl_sync(hmask, kst_l, 0, S);
-    int deg = static_cast<int>(__shfl_sync(hmask, ken_l, 0, S) - k0);
+    i64 k0 = __shfl_sync(0xffffffffu, kst_l, 0);
+    int deg = static_cast<int>(__shfl_sync(0xffffffffu, ken_l, 0) - k0);
     TV va = TV(0), vb = TV(0);
     int ja = 0, jb = 0;
     if (r < deg) {
       va = ldv(k0 + r);
       ja = ldj(k0 + r);
     }
-    if (r + S < deg) {
-      vb = ldv(k0 + r + S);
-      jb = ldj(k0 + r + S);
+    if (r + 32 < deg) {
+      vb = ldv(k0 + r + 32);
+      jb = ldj(k0 + r + 32);
     }
     for (int cc = 0; cc < cnt; ++cc) {
-      // prefetch the next column's entries
       i64 k0n = 0;
       int degn = 0;
       TV van = TV(0), vbn = TV(0);
       int jan = 0, jbn = 0;
       if (cc + 1 < cnt) {
-        k0n = __shfl_sync(hmask, kst_l, cc + 1, S);
-        degn = static_cast<int>(__shfl_sync(hmask, ken_l, cc + 1, S) - k0n);
+        k0n = __shfl_sync(0xffffffffu, kst_l, cc + 1);
+        degn = static_cast<int>(__shfl_sync(0xffffffffu, ken_l, cc + 1) - k0n);
         if (r < degn) {
           van = ldv(k0n + r);
           jan = ldj(k0n + r);
         }
-        if (r + S < degn) {
-          vbn = ldv(k0n + r + S);
-          jbn = ldj(k0n + r + S);
+        if (r + 32 < degn) {
+          vbn = ldv(k0n + r + 32);
+          jbn = ldj(k0n + r + 32);
         }
       }
       TK a = TK(0);
-      // batches of 8 entries: 8 independent gathers in flight, then the 8
-      // accumulation steps in CSR order (entries past the row end gather
-      // column 0 and are not accumulated)
-      constexpr int BT = 8;  // gathers in flight per batch
       auto slot = [&](TV vs, int js, int cnt_s) {
-        for (int t0 = 0; t0 < cnt_s; t0 += BT) {
-          TV v[BT];
-          TI x[BT];
+        for (int t0 = 0; t0 < cnt_s; t0 += 8) {
+          TV v[8];
+          TI x[8];
 #pragma unroll
-          for (int u = 0; u < BT; ++u) {
-            v[u] = __shfl_sync(hmask, vs, (t0 + u) & (S - 1), S);
-            const int j = __shfl_sync(hmask, js, (t0 + u) & (S - 1), S);
-            x[u] = kSmem ? Pr[j * jstride] : __ldg(Pr + j * jstride);
+          for (int u = 0; u < 8; ++u) {
+            v[u] = __shfl_sync(0xffffffffu, vs, (t0 + u) & 31);
+            const int j = __shfl_sync(0xffffffffu, js, (t0 + u) & 31);
+            x[u] = __ldg(Pr + j * jstride);
           }
 #pragma unroll
-          for (int u = 0; u < BT; ++u)
+          for (int u = 0; u < 8; ++u)
             if (t0 + u < cnt_s) a = acc<TK>(a, static_cast<TK>(v[u]), static_cast<TK>(x[u]));
         }
       };
-      slot(va, ja, min(deg, S));
-      if (deg > S) slot(vb, jb, min(deg, 2 * S) - S);
-      for (int t0 = 2 * S; t0 < deg; t0 += S) {  // hub columns: further slots on demand
+      slot(va, ja, min(deg, 32));
+      if (deg > 32) slot(vb, jb, min(deg, 64) - 32);
+      for (int t0 = 64; t0 < deg; t0 += 32) {  // hub columns: further slots on demand
         TV vc = TV(0);
         int jc = 0;
         if (t0 + r < deg) {
-          vc = L.v[k0 + t0 + r];
-          jc = L.ci[k0 + t0 + r];
+          vc = ldv(k0 + t0 + r);
+          jc = ldj(k0 + t0 + r);
         }
-        slot(vc, jc, min(S, deg - t0));
+        slot(vc, jc, min(32, deg - t0));
       }
       const int c = c0 + cc;
       if (vrow) {
         const i64 at = i + static_cast<i64>(c) * p;
         if constexpr (kCombine) {
           const bool sampled = cb.pl.rsel[i] >= 0 && cb.pl.csel[col_base + c] >= 0;
-          const TI pv = kSmem ? Pb[c * S + r] : P[at];
+          const TI pv = P[at];
           const TK out = combine_one<TK>(a, cb.other[at], cb.gr, cb.gc, sampled, pv);
           if (cb.AP) cb.AP[at] = out;
           s += static_cast<double>(pv) * static_cast<double>(out);
-        } else if constexpr (kSmem) {
-          U[at] = a;
         } else {
           __stcs(U + at, a);  // streamed: keep the L2 for the band
         }
@@ -989,7 +952,7 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
   const size_t band_bytes = static_cast<size_t>(n_local) * 128;
   ap.lc_smem = band_bytes + lc_smem_ent_bytes<TI, TV>() <= 220 * 1024;
   ap.lc_smem_bytes = std::max<size_t>(band_bytes, 16);
-  ap.lc_cpc = 8 * G * S;  // 8 warps x G workers x S columns (one row-pointer load per worker)
+  ap.lc_cpc = 8 * 32;  // L2 mode: 8 warps x 32 columns (one row-pointer load per warp)
   ap.lc_chunks = static_cast<int>(std::max<i64>(1, (ncols + ap.lc_cpc - 1) / ap.lc_cpc));
   // row order: degree-sorted when natural warps would pad the rows > 30 %
   std::vector<int> deg(static_cast<size_t>(p));
@@ -1156,8 +1119,8 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
 
 // Number of CTAs (reduction partials) of a pass.
 inline size_t lc_blocks(const ApplyPlan& ap, int S) {
-  const size_t bands = static_cast<size_t>((ap.p + S - 1) / S);
-  return ap.lc_smem ? bands : bands * ap.lc_chunks;
+  return ap.lc_smem ? static_cast<size_t>((ap.p + S - 1) / S)
+                    : static_cast<size_t>((ap.p + 31) / 32) * ap.lc_chunks;
 }
 inline size_t lr_blocks(const ApplyPlan& ap) {
   if (ap.fused) return static_cast<size_t>(ap.f_grid.x) * ap.f_grid.y;
@@ -1178,10 +1141,10 @@ void launch_lc(Ctx* c, const ApplyPlan& ap, Pull<TV> L, const TI* P, TK* U, cons
     k<<<bands, kLcSmemThreads, bytes, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols),
                                                    static_cast<int>(ap.n_local), L, P, U, ap.col_base, cb);
   } else {
-    auto k = combine ? lc_k<TI, TK, TV, false, true, TB> : lc_k<TI, TK, TV, false, false, TB>;
-    k<<<bands * ap.lc_chunks, 256, 0, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols),
-                                                   static_cast<int>(ap.n_local), ap.lc_chunks, ap.lc_cpc, L, P, U,
-                                                   ap.col_base, cb);
+    auto k = combine ? lc_k<TI, TK, TV, true, TB> : lc_k<TI, TK, TV, false, TB>;
+    const unsigned bands32 = static_cast<unsigned>((ap.p + 31) / 32);
+    k<<<bands32 * ap.lc_chunks, 256, 0, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols),
+                                                     ap.lc_chunks, ap.lc_cpc, L, P, U, ap.col_base, cb);
   }
   launched(c);
 }
