@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kLcSmemThreads) lc_smem_k(int p, int ncols, in
 // independent loads; entries are broadcast by shuffle, accumulated in CSR
 // order.
 template <typename TI, typename TK, typename TV, bool kCombine, typename TB>
-__global__ void __launch_bounds__(256) lc_k(int p, int ncols, int chunks, int cpc, Pull<TV> L,
+__global__ void __launch_bounds__(256, 4) lc_k(int p, int ncols, int chunks, int cpc, Pull<TV> L,
                                             const TI* __restrict__ P, TK* __restrict__ U, i64 col_base,
                                             Combine<TK, TB> cb) {
   if (cb.st && cb.st->done) return;
