@@ -583,28 +583,24 @@ struct LrGroup {
   int split;   // any row of the group spans several vrows
 };
 
-template <typename TI>
-__device__ __forceinline__ void stage_tile(TI* W, int wl, const TI* __restrict__ P, i64 p, int w0, int c0, int C,
-                                           int ncols, bool vec) {
-  if (vec) {
-    constexpr int E = 16 / sizeof(TI);
-    const int nch = wl / E;
-    const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(W));
-    for (int q = threadIdx.x; q < C * nch; q += blockDim.x) {
-      const int cc = q / nch, k = q % nch;
-      if (c0 + cc >= ncols) continue;
-      const TI* src = P + static_cast<i64>(c0 + cc) * p + w0 + k * E;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + static_cast<unsigned>((cc * wl + k * E) *
-                                                                                                 sizeof(TI))),
-                   "l"(src)
-                   : "memory");
-    }
-  } else {
-    for (int q = threadIdx.x; q < C * wl; q += blockDim.x) {
-      const int cc = q / wl, k = q % wl;
-      const int row = w0 + k;
-      W[q] = (c0 + cc < ncols && row < p) ? P[static_cast<i64>(c0 + cc) * p + row] : TI(0);
-    }
+// Stages rows [w0, w0 + wl) of the C columns [c0, c0 + C) as one C-wide
+// record per row (element-sized cp.async copies, so the copy stays
+// asynchronous while the layout turns row-major): a gather then reads all C
+// columns of a row with one 8/16-byte shared load, which halves the bank
+// conflicts of random 8-byte reads.
+template <typename TI, int C>
+__device__ __forceinline__ void stage_tile(Rec<TI, C>* W, int wl, const TI* __restrict__ P, i64 p, int w0, int c0,
+                                           int ncols) {
+  const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(W));
+  for (int q = threadIdx.x; q < C * wl; q += blockDim.x) {
+    const int cc = q / wl, k = q % wl;
+    const unsigned dst = sb + static_cast<unsigned>((k * C + cc) * sizeof(TI));
+    const int col = min(c0 + cc, ncols - 1);  // columns past the end: a valid duplicate, never combined
+    const TI* src = P + static_cast<i64>(col) * p + w0 + k;
+    if constexpr (sizeof(TI) == 8)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -619,9 +615,9 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
   extern __shared__ __align__(16) unsigned char smraw[];
   const int g = blockIdx.x / stripes, stripe = blockIdx.x % stripes;
   const LrGroup gr = groups[g];
-  TI* W0 = reinterpret_cast<TI*>(smraw);
-  TI* W1 = W0 + static_cast<size_t>(C) * wl_max;
-  TK* part = reinterpret_cast<TK*>(W1 + static_cast<size_t>(C) * wl_max);  // [T][C] when split
+  Rec<TI, C>* W0 = reinterpret_cast<Rec<TI, C>*>(smraw);
+  Rec<TI, C>* W1 = W0 + wl_max;
+  TK* part = reinterpret_cast<TK*>(W1 + wl_max);  // [T][C] when split
   const int t = threadIdx.x;
   const bool active = t < gr.nv;
   TV v[EV];
@@ -635,17 +631,16 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
   const int row = active ? vrow_row[gr.v0 + t] : 0;
   const int np = active ? vrow_np[gr.v0 + t] : 0;  // parts of a leader vrow, 0 for a follower
   const bool rs = active && np > 0 && cb.pl.rsel[row] >= 0;
-  const bool vec = (reinterpret_cast<uintptr_t>(P) % 16 == 0) && ((static_cast<i64>(p) * sizeof(TI)) % 16 == 0);
   const int ntiles = (ncols + C - 1) / C;
   double s = 0.0;
   int tile = stripe;
-  if (tile < ntiles) stage_tile(W0, gr.wl, P, p, gr.w0, tile * C, C, ncols, vec);
+  if (tile < ntiles) stage_tile<TI, C>(W0, gr.wl, P, p, gr.w0, tile * C, ncols);
   int b = 0;
   for (; tile < ntiles; tile += stripes, b ^= 1) {
-    TI* W = b ? W1 : W0;
+    const Rec<TI, C>* W = b ? W1 : W0;
     const int nxt = tile + stripes;
     if (nxt < ntiles) {
-      stage_tile(b ? W0 : W1, gr.wl, P, p, gr.w0, nxt * C, C, ncols, vec);
+      stage_tile<TI, C>(b ? W0 : W1, gr.wl, P, p, gr.w0, nxt * C, ncols);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -663,8 +658,9 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
     for (int cc = 0; cc < C; ++cc) a[cc] = TK(0);
 #pragma unroll
     for (int e = 0; e < EV; ++e) {
+      const Rec<TI, C> x = W[jj[e]];
 #pragma unroll
-      for (int cc = 0; cc < C; ++cc) a[cc] = acc<TK>(a[cc], static_cast<TK>(v[e]), static_cast<TK>(W[cc * gr.wl + jj[e]]));
+      for (int cc = 0; cc < C; ++cc) a[cc] = acc<TK>(a[cc], static_cast<TK>(v[e]), static_cast<TK>(x.v[cc]));
     }
     if (gr.split) {
 #pragma unroll
@@ -682,7 +678,7 @@ __global__ void __launch_bounds__(T, 1) lr_reg_k(int p, int ncols, int stripes, 
         if (c >= ncols) break;
         const i64 at = row + static_cast<i64>(c) * p;
         if constexpr (kCombine) {
-          const TI pv = W[cc * gr.wl + (row - gr.w0)];
+          const TI pv = W[row - gr.w0].v[cc];
           const bool sampled = rs && cb.pl.csel[col_base + c] >= 0;
           const TK out = combine_one<TK>(o[cc], a[cc], cb.gr, cb.gc, sampled, pv);
           if (cb.Xt) {
@@ -986,10 +982,11 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
       const int parts = std::max(1, (deg[i] + EV - 1) / EV);
       if (grp.empty() || grp.back().nv + parts > T) grp.push_back({static_cast<int>(vrow_row.size()), 0, 0, 0, 0});
       for (int q = 0; q < parts; ++q) {
+        const i64 k0 = rpr[i] + static_cast<i64>(q) * EV;
+        const int k1 = static_cast<int>(std::min<i64>(rpr[i + 1], k0 + EV));
         vrow_row.push_back(i);
         vrow_np.push_back(q == 0 ? parts : 0);
-        const i64 k0 = rpr[i] + static_cast<i64>(q) * EV;
-        vrow_k.push_back({static_cast<int>(k0), static_cast<int>(std::min<i64>(rpr[i + 1], k0 + EV))});
+        vrow_k.push_back({static_cast<int>(k0), k1});
       }
       grp.back().nv += parts;
       if (parts > 1) grp.back().split = 1;
