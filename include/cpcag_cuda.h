@@ -78,10 +78,15 @@ int cpcag_ctx_set_stream(cpcag_ctx ctx, void* cuda_stream);
 void* cpcag_ctx_stream(cpcag_ctx ctx);
 int cpcag_ctx_synchronize(cpcag_ctx ctx);
 /* Decoder operator path for this context (tests of both paths on small
- * cases): 0 = automatic (one fused pass when the Krylov vectors fit in L2,
- * else the two-pass band / row-group kernels), 1 = always two passes,
- * 2 = fused whenever its shared-memory slice fits. */
+ * cases): 0 = automatic (fp32 iterates whose 32-row slab of all columns fits
+ * in shared memory: the slab pass; other L2-resident Krylov vectors: one
+ * fused pass; else the two-pass band / row-group kernels), 1 = always two
+ * passes, 2 = fused whenever its shared-memory slice fits, 3 = slab whenever
+ * it applies. */
 int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path);
+/* The path (1, 2 or 3 as above) the most recently planned decoder operator
+ * took; 0 before any. */
+int cpcag_ctx_last_apply_path(cpcag_ctx ctx);
 /* Number of kernels this context has launched since creation (or reset). */
 int64_t cpcag_ctx_launch_count(cpcag_ctx ctx);
 void cpcag_ctx_reset_launch_count(cpcag_ctx ctx);

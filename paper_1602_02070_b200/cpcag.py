@@ -171,8 +171,12 @@ class Context:
         N.lib().cpcag_ctx_reset_launch_count(self._h)
 
     def set_apply_path(self, path: str):
-        """Decoder operator path: "auto", "split" (two passes) or "fused"."""
-        N.check(N.lib().cpcag_ctx_set_apply_path(self.handle, {"auto": 0, "split": 1, "fused": 2}[path]))
+        """Decoder operator path: "auto", "split" (two passes), "fused" or "slab"."""
+        N.check(N.lib().cpcag_ctx_set_apply_path(self.handle, {"auto": 0, "split": 1, "fused": 2, "slab": 3}[path]))
+
+    def last_apply_path(self) -> str:
+        """The path the most recently planned decoder operator took."""
+        return {0: "none", 1: "split", 2: "fused", 3: "slab"}[N.lib().cpcag_ctx_last_apply_path(self.handle)]
 
     def reserve(self, nbytes: int):
         """Grow the stream-ordered memory pool to `nbytes` up front."""

@@ -82,7 +82,8 @@ struct Ctx {
   size_t pinned_bytes = 0;
   bool timing = false;
   std::string timing_filter;  // comma-separated tags; empty = all
-  int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused (tests)
+  int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused, 3 slab (tests)
+  int last_apply_path = 0;    // the path the last planned operator took (1, 2 or 3; tests)
   KernelTimes kt;
 };
 

@@ -860,10 +860,12 @@ void* cpcag_ctx_stream(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)
 
 int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path) {
   return guard([&] {
-    if (path < 0 || path > 2) invalid("apply path must be 0, 1 or 2");
+    if (path < 0 || path > 3) invalid("apply path must be 0, 1, 2 or 3");
     as_ctx(ctx)->apply_path = path;
   });
 }
+
+int cpcag_ctx_last_apply_path(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->last_apply_path : -1; }
 
 int cpcag_ctx_synchronize(cpcag_ctx ctx) {
   return guard([&] { sync(as_ctx(ctx)); });

@@ -49,11 +49,10 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
   host_pull<TV>(c, pr, p, Lr->nnz, rpr, cir, &vr);
   ApplyPlan apK, apX;
   const bool exact = sizeof(TX) == 8;
-  std::vector<i64> rpc(static_cast<size_t>(n) + 1);
-  CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  plan_apply<TK, TK, TV>(c, apK, p, n, n, 0, rpr, cir, vr, exact, &rpc);
-  plan_apply<TX, TK, TV>(c, apX, p, n, n, 0, rpr, cir, vr, exact, &rpc);
+  HostPull<TV> lcp;
+  host_pull<TV>(c, pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
+  plan_apply<TK, TK, TV>(c, apK, p, n, n, 0, rpr, cir, vr, exact, &lcp);
+  plan_apply<TX, TK, TV>(c, apX, p, n, n, 0, rpr, cir, vr, exact, &lcp);
   DevBuf<TK> R(c, N), P(c, N), AP(c, N), U(c, N);
   DevBuf<CgState> st(c, 1);
   st.zero(c);
@@ -250,10 +249,9 @@ void decoder_apply_device(Ctx* c, const T* P, i64 p, i64 n, Csr* Lr, Csr* Lc, co
   std::vector<T> vr;
   host_pull<T>(c, pr, p, Lr->nnz, rpr, cir, &vr);
   ApplyPlan ap;
-  std::vector<i64> rpc(static_cast<size_t>(n) + 1);
-  CUDA_OK(cudaMemcpyAsync(rpc.data(), pc.rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
-  sync(c);
-  plan_apply<T, T, T>(c, ap, p, n, n, 0, rpr, cir, vr, sizeof(T) == 8, &rpc);
+  HostPull<T> lcp;
+  host_pull<T>(c, pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
+  plan_apply<T, T, T>(c, ap, p, n, n, 0, rpr, cir, vr, sizeof(T) == 8, &lcp);
   DevBuf<T> U(c, std::max<i64>(p * n, 1));
   DevBuf<CgState> st(c, 1);
   st.zero(c);

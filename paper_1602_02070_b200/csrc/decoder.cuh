@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstring>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -191,6 +192,241 @@ __global__ void __launch_bounds__(256, 4) fused_k(int p, int n, Pull<TV> Lr, Pul
   finish_reduction(s, cb);
 }
 
+// ------------------------------------------------------------------ slab apply (fp32 iterates, small n)
+// AP = gc P Lc + gr Lr P (+ P on the sampled grid) and <P, AP> in one pass
+// when a slab of 32 rows x all n columns fits in shared memory (config 1:
+// 10 304 x 1 000 fp32, 125 KB).  CTA = one slab (or one of `parts` column
+// ranges of it); the slab is copied once (cp.async, 16 bytes a thread).
+//  * L_c: a warp works on "quads" of 4 output columns of similar degree; lane
+//    (g, s) = (lane / 8, lane % 8) owns rows 4s .. 4s + 3 of column g, so one
+//    entry is one 16-byte shared load of the neighbour column's segment and
+//    four multiply-adds into independent sums.  A quad's entries are
+//    interleaved records (64 bytes: two (value, byte offset) entries of each
+//    of the 4 columns), zero padded to the longest column, streamed through
+//    a 4-chunk ring of 512 bytes (one 16-byte cp.async per lane per chunk)
+//    and read back by one 16-byte load per two entries (4 addresses a warp,
+//    broadcast).  Quads longer than the ring allows are split into steps.
+//  * The sums move to a per-warp scratch and come back lane = row for L_r,
+//    the combine and the coalesced store.
+//  * L_r: the rows a slab's L_r rows reference (for the pixel grid: the slab
+//    and the +-w stencil rows, <= 32 aligned 16-byte chunks of a column) are
+//    staged per quad into a per-warp window (one cp.async per lane per
+//    column), issued after the previous quad's L_r so the copy overlaps the
+//    next L_c loop; each lane keeps its row's entries in registers as
+//    (value, shared address in the window).
+// Per entry the reference's order (decoders.cpp:160-170).
+template <typename TV>
+struct alignas(sizeof(TV) == 8 ? 16 : 8) SEnt {
+  TV v;
+  int off;  // byte offset of the neighbour column's segment in the band / slab
+};
+
+struct SlabStep {  // 32 bytes, everything precomputed at plan time
+  int rec;       // byte offset of the step's records (multiple of 64)
+  int rows;      // 64-byte record rows (two entries of each column)
+  int flags;     // 1: first step of its quad, 2: last, 4: its records were issued this step; bit 8 + g: column g real
+  int issue_hi;  // ring chunks up to this index are issued at the start of the step
+  int col[4];    // output columns (missing ones repeat a real column)
+};
+static_assert(sizeof(SlabStep) == 32, "SlabStep is one 32-byte record");
+
+struct SlabPlan {
+  const unsigned char* rec;  // interleaved (value, byte offset) records
+  const SlabStep* steps;
+  const int* wsteps;  // [parts][kSlabWarps + 1] step ranges (indices into steps)
+  int max_steps;      // steps of the largest part (their shared-memory copy)
+  const int* win;     // [slabs][32]: first row (relative to the slab) of each window chunk, or kNoChunk
+  const float* lv;    // [EVR][p]: L_r row entries, zero padded
+  const int* lo;      // [EVR][p]: byte offset of the entry's row in a column's window
+};
+
+constexpr int kSlabWarps = 16;
+constexpr int kSlabThreads = kSlabWarps * 32;
+constexpr int kSlabRing = 4;  // 512-byte record chunks per warp
+constexpr int kNoChunk = 0x40000000;
+constexpr size_t kSlabWarpBytes = kSlabRing * 512 + 4 * 512 + 1024;  // ring, 4 windows, scratch
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ float lds_f32(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f128(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int4 lds_i128(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+
+template <typename TK, int EVR, bool kResid, typename TB>
+__global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int parts, SlabPlan sp,
+                                                           const float* __restrict__ P, Combine<TK, TB> cb) {
+  if (cb.st && cb.st->done) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int slab = blockIdx.x / parts, part = blockIdx.x % parts;
+  const int i0 = slab * 32, rows = min(32, p - i0);
+  float* Pb = reinterpret_cast<float*>(smraw);  // [n][32]
+  const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(Pb));
+  if (rows == 32) {
+    for (int q = threadIdx.x; q < n * 8; q += kSlabThreads)
+      cp_async16(sbase + static_cast<unsigned>(q) * 16u, P + static_cast<i64>(q >> 3) * p + i0 + (q & 7) * 4);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  } else {
+    for (int q = threadIdx.x; q < n * 32; q += kSlabThreads) {
+      const int c = q >> 5, r = q & 31;
+      Pb[q] = r < rows ? P[static_cast<i64>(c) * p + i0 + r] : 0.f;
+    }
+  }
+  // the part's step list next to the slab (copied with it)
+  const int pst0 = sp.wsteps[part * (kSlabWarps + 1)], pst1 = sp.wsteps[part * (kSlabWarps + 1) + kSlabWarps];
+  const unsigned stbase = sbase + static_cast<unsigned>(static_cast<size_t>(n) * 128);
+  {
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(sp.steps + pst0);
+    for (int q = threadIdx.x; q < (pst1 - pst0) * 2; q += kSlabThreads) cp_async16(stbase + q * 16u, src + q * 16);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const SlabStep* S = reinterpret_cast<const SlabStep*>(smraw + (stbase - sbase)) - pst0;  // indexed by step
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g4 = lane >> 3, s4 = lane & 7;  // quad layout: column g4, rows 4 s4 .. 4 s4 + 3
+  const bool vrow = lane < rows;
+  const int i = i0 + (vrow ? lane : 0);
+  const unsigned wbase = stbase + static_cast<unsigned>(sp.max_steps) * 32u +
+                         static_cast<unsigned>(warp) * static_cast<unsigned>(kSlabWarpBytes);
+  const unsigned rbase = wbase, hbase = wbase + kSlabRing * 512, xbase = hbase + 4 * 512;
+  float lv[EVR];
+  unsigned lo[EVR];  // shared address of the entry's row in window 0
+#pragma unroll
+  for (int e = 0; e < EVR; ++e) {
+    lv[e] = vrow ? sp.lv[static_cast<i64>(e) * p + i] : 0.f;
+    lo[e] = hbase + (vrow ? static_cast<unsigned>(sp.lo[static_cast<i64>(e) * p + i]) : 0u);
+  }
+  const int wrow = sp.win[slab * 32 + lane];  // this lane's window chunk (rows wrow .. wrow + 3)
+  const bool wcopy = wrow != kNoChunk;
+  const float* wsrc = P + i0 + (wcopy ? wrow : 0);
+  const bool rs = vrow && cb.pl.rsel[i] >= 0;
+  TK* const APi = kResid ? nullptr : cb.AP + i;
+  const int st0 = sp.wsteps[part * (kSlabWarps + 1) + warp], st1 = sp.wsteps[part * (kSlabWarps + 1) + warp + 1];
+  (void)st0;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  double s = 0.0;
+  if (st0 < st1) {
+    unsigned issued = static_cast<unsigned>(S[st0].rec) / 512u;
+    const unsigned char* gsrc = sp.rec + lane * 16;
+    auto window = [&](const SlabStep& q) {  // the quad's L_r windows (one commit group)
+      if (wcopy)
+#pragma unroll
+        for (int g = 0; g < 4; ++g) cp_async16(hbase + g * 512 + lane * 16, wsrc + static_cast<i64>(q.col[g]) * p);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    window(S[st0]);
+    float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    TK accd[4] = {TK(0), TK(0), TK(0), TK(0)};
+    for (int st = st0; st < st1; ++st) {
+      const SlabStep cur = S[st];
+      int csq[4];  // plan positions of the quad's columns, loaded ahead of the combine
+#pragma unroll
+      for (int g = 0; g < 4; ++g) csq[g] = cb.pl.csel[cur.col[g]];
+      __syncwarp();  // ring chunks of earlier steps are free
+      for (; static_cast<int>(issued) <= cur.issue_hi; ++issued)
+        cp_async16(rbase + (issued % kSlabRing) * 512u + lane * 16u, gsrc + static_cast<i64>(issued) * 512);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (cur.flags & 4)
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
+      __syncwarp();
+      // L_c: record rows of this step
+      const unsigned rb0 = rbase + g4 * 16;
+#pragma unroll 4
+      for (int k = 0; k < cur.rows; ++k) {
+        const unsigned rb = static_cast<unsigned>(cur.rec + k * 64);
+        const int4 e = lds_i128(rb0 + (rb % (kSlabRing * 512u)));
+        const float4 x0 = lds_f128(sbase + static_cast<unsigned>(e.y) + s4 * 16);
+        const float4 x1 = lds_f128(sbase + static_cast<unsigned>(e.w) + s4 * 16);
+        const float v0 = __int_as_float(e.x), v1 = __int_as_float(e.z);
+        if constexpr (sizeof(TK) == 4) {
+          acc4.x = fmaf(v0, x0.x, acc4.x);
+          acc4.y = fmaf(v0, x0.y, acc4.y);
+          acc4.z = fmaf(v0, x0.z, acc4.z);
+          acc4.w = fmaf(v0, x0.w, acc4.w);
+          acc4.x = fmaf(v1, x1.x, acc4.x);
+          acc4.y = fmaf(v1, x1.y, acc4.y);
+          acc4.z = fmaf(v1, x1.z, acc4.z);
+          acc4.w = fmaf(v1, x1.w, acc4.w);
+        } else {
+          accd[0] = acc<TK>(accd[0], v0, x0.x);
+          accd[1] = acc<TK>(accd[1], v0, x0.y);
+          accd[2] = acc<TK>(accd[2], v0, x0.z);
+          accd[3] = acc<TK>(accd[3], v0, x0.w);
+          accd[0] = acc<TK>(accd[0], v1, x1.x);
+          accd[1] = acc<TK>(accd[1], v1, x1.y);
+          accd[2] = acc<TK>(accd[2], v1, x1.z);
+          accd[3] = acc<TK>(accd[3], v1, x1.w);
+        }
+      }
+      if (cur.flags & 2) {
+        // sums to lane = row through the scratch
+        TK a[4];
+        if constexpr (sizeof(TK) == 4) {
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(xbase + g4 * 128 + s4 * 16), "f"(acc4.x),
+                       "f"(acc4.y), "f"(acc4.z), "f"(acc4.w)
+                       : "memory");
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 4; ++g) a[g] = lds_f32(xbase + g * 128 + lane * 4);
+        } else {
+          TK* X = reinterpret_cast<TK*>(smraw + (xbase - sbase));  // 4 x 32 sums
+#pragma unroll
+          for (int t = 0; t < 4; ++t) X[g4 * 32 + s4 * 4 + t] = accd[t];
+          __syncwarp();
+#pragma unroll
+          for (int g = 0; g < 4; ++g) a[g] = X[g * 32 + lane];
+        }
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // this quad's windows
+        __syncwarp();
+        TK y[4] = {TK(0), TK(0), TK(0), TK(0)};
+#pragma unroll
+        for (int e = 0; e < EVR; ++e)
+#pragma unroll
+          for (int g = 0; g < 4; ++g) y[g] = acc<TK>(y[g], static_cast<TK>(lv[e]), static_cast<TK>(lds_f32(lo[e] + g * 512)));
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const bool real = vrow && ((cur.flags >> (8 + g)) & 1);
+          const float pv = lds_f32(sbase + static_cast<unsigned>(cur.col[g] * 32 + lane) * 4u);
+          const TK out = combine_one<TK>(a[g], y[g], cb.gr, cb.gc, rs && csq[g] >= 0, pv);
+          if constexpr (kResid) {
+            const double d = real ? static_cast<double>(sub_rn(static_cast<TK>(rhs_at(cb.pl, cb.Xt, i, cur.col[g])), out))
+                                  : 0.0;
+            s += d * d;
+          } else {
+            if (real) APi[static_cast<i64>(cur.col[g]) * p] = out;
+            s += real ? static_cast<double>(pv) * static_cast<double>(out) : 0.0;
+          }
+        }
+        __syncwarp();  // windows and scratch are free
+        if (st + 1 < st1) window(S[st + 1]);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) accd[t] = TK(0);
+      } else {
+        asm volatile("cp.async.commit_group;" ::: "memory");  // keep two groups per step
+      }
+      issued = max(issued, static_cast<unsigned>(cur.issue_hi + 1));
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  finish_reduction(s, cb);
+}
+
 // ------------------------------------------------------------------ lc pass, band in shared memory
 // One CTA per band of S = 128 B / sizeof(TI) rows: the band's segment of all
 // n_local columns (n x 128 B) is copied to shared memory once.  A (half) warp
@@ -201,12 +437,6 @@ __global__ void __launch_bounds__(256, 4) fused_k(int p, int n, Pull<TV> Lr, Pul
 // an entry costs one gather, one add and one multiply-add.  Rows are padded
 // in the buffer to a multiple of 4 with zero entries pointing at column 0
 // (a zero product leaves the sum unchanged; CSR order is kept).
-template <typename TV>
-struct alignas(sizeof(TV) == 8 ? 16 : 8) SEnt {
-  TV v;
-  int off;  // byte offset of the neighbour column's segment in the band
-};
-
 template <typename TV>
 __device__ __forceinline__ void lds_ent4(const SEnt<TV>* e, TV (&v)[4], int (&o)[4]) {
   if constexpr (sizeof(TV) == 4) {
@@ -887,6 +1117,13 @@ static __global__ void scatter_sel_k(const i64* __restrict__ om, i64 rho, int* s
 // the sharded decoder) and produces columns [0, ncols).
 struct ApplyPlan {
   i64 p = 0, ncols = 0, n_local = 0, col_base = 0;
+  // slab apply (slab_k): fp32 iterates, a 32-row slab of all columns in shared memory
+  bool slab = false;
+  int s_parts = 1, s_evr = 9, s_max_steps = 0;
+  size_t s_smem = 0;
+  DevBuf<unsigned char> s_rec, s_steps;  // interleaved L_c records, SlabStep list
+  DevBuf<int> s_wsteps, s_win, s_lo;
+  DevBuf<float> s_lv;
   // fused one-pass apply (fused_k) for L2-resident iterates
   bool fused = false;
   dim3 f_grid;
@@ -916,16 +1153,207 @@ constexpr size_t kSmemMax = 200 * 1024;
 // exact: fp64 data -- rows may not be split (bit-identical sums).
 // rpc (L_c row pointers, host): when given and the Krylov vectors fit in L2,
 // the fused one-pass apply is planned instead of the two passes.
+inline int __float_as_int_host(float f) {
+  int i;
+  std::memcpy(&i, &f, sizeof(i));
+  return i;
+}
+
+// Host copy of the L_c pull (for the one-pass plans).
+template <typename TV>
+struct HostPull {
+  std::vector<i64> rp;
+  std::vector<int> ci;
+  std::vector<TV> v;
+};
+
+// Slab apply geometry (slab_k): fp32 iterates (p a multiple of 4), the slab
+// (n * 128 B) and the warps' rings and windows within one CTA's shared
+// memory, L_r rows of <= 16 entries whose referenced rows fit 32 aligned
+// 16-byte chunks per slab, L_c pull rows of <= (kSlabRing - 1) chunks.
+// Returns false when it does not apply.
+template <typename TI, typename TV>
+bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr, const std::vector<int>& cir,
+               const std::vector<TV>& vr, const HostPull<TV>& lc) {
+  if constexpr (sizeof(TI) != 4 || sizeof(TV) != 4) {
+    return false;
+  } else {
+    const size_t smem = ((static_cast<size_t>(n) * 128 + 15) / 16) * 16 + (kSlabThreads / 32) * kSlabWarpBytes;
+    if (p <= 0 || n <= 0 || p % 4 != 0 || smem > 227 * 1024) return false;
+    i64 mr = 0;
+    for (i64 i = 0; i < p; ++i) mr = std::max(mr, rpr[i + 1] - rpr[i]);
+    if (mr > 16) return false;
+    const int EVR = mr <= 9 ? 9 : 16;
+    // L_r windows
+    const i64 slabs = (p + 31) / 32;
+    std::vector<int> win(static_cast<size_t>(slabs) * 32, kNoChunk);
+    std::vector<float> lv(static_cast<size_t>(EVR) * p, 0.f);
+    std::vector<int> lo(static_cast<size_t>(EVR) * p, 0);
+    std::vector<int> ch;
+    for (i64 sl = 0; sl < slabs; ++sl) {
+      const i64 i0 = sl * 32, i1 = std::min(p, i0 + 32);
+      ch.clear();
+      for (i64 i = i0; i < i1; ++i) {
+        ch.push_back(static_cast<int>(i & ~i64{3}));
+        for (i64 k = rpr[i]; k < rpr[i + 1]; ++k) ch.push_back(cir[k] & ~3);
+      }
+      std::sort(ch.begin(), ch.end());
+      ch.erase(std::unique(ch.begin(), ch.end()), ch.end());
+      if (ch.size() > 32) return false;
+      for (size_t t = 0; t < ch.size(); ++t) win[sl * 32 + t] = ch[t] - static_cast<int>(i0);
+      auto where = [&](i64 j) {
+        const int t = static_cast<int>(std::lower_bound(ch.begin(), ch.end(), static_cast<int>(j & ~i64{3})) - ch.begin());
+        return (t * 4 + static_cast<int>(j & 3)) * 4;
+      };
+      for (i64 i = i0; i < i1; ++i) {
+        for (int e = 0; e < EVR; ++e) {
+          const i64 k = rpr[i] + e;
+          const bool in = k < rpr[i + 1];
+          lv[static_cast<size_t>(e) * p + i] = in ? static_cast<float>(vr[k]) : 0.f;
+          lo[static_cast<size_t>(e) * p + i] = where(in ? cir[k] : i);
+        }
+      }
+    }
+    // column ranges per slab: minimise waves x (slab copy + columns), the copy
+    // costing ~0.1 of a whole slab's compute
+    const i64 per_sm = smem <= 113 * 1024 ? 2 : 1;
+    int best = 1;
+    double best_t = 1e300;
+    for (int parts = 1; parts <= 4; ++parts) {
+      const i64 waves = (slabs * parts + c->num_sms * per_sm - 1) / (c->num_sms * per_sm);
+      const double t = static_cast<double>(waves) * (0.1 + 1.0 / parts);
+      if (t < best_t - 1e-9) best_t = t, best = parts;
+    }
+    // L_c quads: per part, columns sorted by degree, 4 at a time, dealt to the
+    // warps round-robin; each warp's steps (<= (kSlabRing - 1) chunks of
+    // records) laid out contiguously
+    constexpr int kMaxRows = (kSlabRing - 1) * 512 / 64;
+    std::vector<SlabStep> steps;
+    std::vector<int> wsteps;
+    std::vector<int4> rec;  // 16-byte groups
+    for (int part = 0; part < best; ++part) {
+      const i64 pa = n * part / best, pb = n * (part + 1) / best;
+      std::vector<int> cols(static_cast<size_t>(pb - pa));
+      std::iota(cols.begin(), cols.end(), static_cast<int>(pa));
+      auto deg = [&](int q) { return lc.rp[q + 1] - lc.rp[q]; };
+      std::stable_sort(cols.begin(), cols.end(), [&](int x, int y) { return deg(x) > deg(y); });
+      const i64 nq = (static_cast<i64>(cols.size()) + 3) / 4;
+      // quads to warps: longest first to the least loaded warp (record rows + a fixed per-quad cost)
+      std::vector<std::vector<i64>> wq(kSlabWarps);
+      {
+        std::vector<i64> load(kSlabWarps, 0);
+        for (i64 q = 0; q < nq; ++q) {
+          const int w = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+          wq[w].push_back(q);
+          load[w] += (deg(cols[q * 4]) + 1) / 2 + 6;
+        }
+      }
+      for (int w = 0; w < kSlabWarps; ++w) {
+        wsteps.push_back(static_cast<int>(steps.size()));
+        for (const i64 q : wq[w]) {
+          int cq[4];
+          i64 dmax = 0;
+          for (int g = 0; g < 4; ++g) {
+            const i64 at = q * 4 + g;
+            cq[g] = at < static_cast<i64>(cols.size()) ? cols[at] : -1;
+            if (cq[g] >= 0) dmax = std::max(dmax, deg(cq[g]));
+          }
+          const int rows_q = static_cast<int>((dmax + 1) / 2);
+          int mask = 0, any = -1;
+          for (int g = 0; g < 4; ++g)
+            if (cq[g] >= 0) mask |= 1 << g, any = any < 0 ? cq[g] : any;
+          int k = 0;
+          do {
+            const int r = std::min(kMaxRows, rows_q - k);
+            SlabStep st{};
+            st.rec = static_cast<int>(rec.size() * 16);
+            st.rows = r;
+            st.flags = (k == 0 ? 1 : 0) | (k + r == rows_q ? 2 : 0) | (mask << 8);
+            for (int g = 0; g < 4; ++g) st.col[g] = cq[g] >= 0 ? cq[g] : any;
+            for (int kr = k; kr < k + r; ++kr)
+              for (int g = 0; g < 4; ++g) {
+                int4 e{0, 0, 0, 0};
+                if (cq[g] >= 0) {
+                  const i64 b0 = lc.rp[cq[g]], d = deg(cq[g]);
+                  if (2 * kr < d) {
+                    e.x = __float_as_int_host(static_cast<float>(lc.v[b0 + 2 * kr]));
+                    e.y = lc.ci[b0 + 2 * kr] * 128;
+                  }
+                  if (2 * kr + 1 < d) {
+                    e.z = __float_as_int_host(static_cast<float>(lc.v[b0 + 2 * kr + 1]));
+                    e.w = lc.ci[b0 + 2 * kr + 1] * 128;
+                  }
+                }
+                rec.push_back(e);
+              }
+            steps.push_back(st);
+            k += r;
+          } while (k < rows_q);
+        }
+        // the warp's ring schedule: at each step issue the chunks up to
+        // min(last, first chunk of the step + kSlabRing - 1); a step whose last
+        // chunk is issued in that same step waits for it at once
+        const size_t w0 = static_cast<size_t>(wsteps.back());
+        if (w0 < steps.size()) {
+          const int clast = (steps.back().rec + steps.back().rows * 64 - 1) / 512;
+          int issued = steps[w0].rec / 512;
+          for (size_t t = w0; t < steps.size(); ++t) {
+            SlabStep& st = steps[t];
+            const int c0 = st.rec / 512, cl = (st.rec + st.rows * 64 - 1) / 512;
+            st.issue_hi = std::max(issued - 1, std::min(clast, c0 + kSlabRing - 1));
+            if (st.rows > 0 && cl >= issued) st.flags |= 4;
+            issued = std::max(issued, st.issue_hi + 1);
+          }
+        }
+      }
+      wsteps.push_back(static_cast<int>(steps.size()));
+    }
+    int max_steps = 0;
+    for (int part = 0; part < best; ++part)
+      max_steps = std::max(max_steps, wsteps[part * (kSlabWarps + 1) + kSlabWarps] - wsteps[part * (kSlabWarps + 1)]);
+    const size_t smem_all = smem + static_cast<size_t>(max_steps) * sizeof(SlabStep);
+    if (rec.size() * 16 >= (size_t{1} << 31) || smem_all > 227 * 1024) return false;
+    rec.resize(((rec.size() + 31) / 32 + 1) * 32, int4{0, 0, 0, 0});  // whole 512-byte chunks, one spare
+    ap.slab = true;
+    ap.s_parts = best;
+    ap.s_evr = EVR;
+    ap.s_smem = smem_all;
+    ap.s_max_steps = max_steps;
+    ap.s_rec.alloc(c, rec.size() * 16);
+    ap.s_steps.alloc(c, steps.size() * sizeof(SlabStep));
+    ap.s_wsteps.alloc(c, wsteps.size());
+    ap.s_win.alloc(c, win.size());
+    ap.s_lv.alloc(c, lv.size());
+    ap.s_lo.alloc(c, lo.size());
+    CUDA_OK(cudaMemcpyAsync(ap.s_rec.p, rec.data(), rec.size() * 16, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ap.s_steps.p, steps.data(), steps.size() * sizeof(SlabStep), cudaMemcpyHostToDevice,
+                            c->stream));
+    CUDA_OK(cudaMemcpyAsync(ap.s_wsteps.p, wsteps.data(), sizeof(int) * wsteps.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ap.s_win.p, win.data(), sizeof(int) * win.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ap.s_lv.p, lv.data(), sizeof(float) * lv.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ap.s_lo.p, lo.data(), sizeof(int) * lo.size(), cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    return true;
+  }
+}
+
 template <typename TI, typename TK, typename TV>
 void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_base, const std::vector<i64>& rpr,
                 const std::vector<int>& cir, const std::vector<TV>& vr, bool exact,
-                const std::vector<i64>* rpc = nullptr) {
+                const HostPull<TV>* lcp = nullptr) {
   ap.p = p;
   ap.ncols = ncols;
   ap.n_local = n_local;
   ap.col_base = col_base;
+  const std::vector<i64>* rpc = lcp ? &lcp->rp : nullptr;
   const bool l2_resident = p * ncols * static_cast<i64>(sizeof(TK)) <= (i64{96} << 20);
-  if (rpc && (c->apply_path == 2 || (c->apply_path == 0 && l2_resident)) && p * ncols < (i64{1} << 31) && p > 0 &&
+  if (lcp && ncols == n_local && (c->apply_path == 3 || (c->apply_path == 0 && l2_resident)) &&
+      plan_slab<TI, TV>(c, ap, p, ncols, rpr, cir, vr, *lcp)) {
+    c->last_apply_path = 3;
+    return;
+  }
+  c->last_apply_path = 1;
+  if (rpc && (c->apply_path >= 2 || (c->apply_path == 0 && l2_resident)) && p * ncols < (i64{1} << 31) && p > 0 &&
       ncols > 0) {
     const i64 gx = (p + 511) / 512;
     const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 8) / gx);
@@ -941,10 +1369,10 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
       ap.f_grid = dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy));
       ap.f_cpc = static_cast<int>(cpc);
       ap.f_smem = smem;
+      c->last_apply_path = 2;
       return;
     }
   }
-  constexpr int S = 128 / sizeof(TI), G = 32 / S;
   const size_t band_bytes = static_cast<size_t>(n_local) * 128;
   ap.lc_smem = band_bytes + lc_smem_ent_bytes<TI, TV>() <= 220 * 1024;
   ap.lc_smem_bytes = std::max<size_t>(band_bytes, 16);
@@ -1120,6 +1548,7 @@ inline size_t lc_blocks(const ApplyPlan& ap, int S) {
                     : static_cast<size_t>((ap.p + 31) / 32) * ap.lc_chunks;
 }
 inline size_t lr_blocks(const ApplyPlan& ap) {
+  if (ap.slab) return static_cast<size_t>((ap.p + 31) / 32) * ap.s_parts;
   if (ap.fused) return static_cast<size_t>(ap.f_grid.x) * ap.f_grid.y;
   return ap.lr_reg ? static_cast<size_t>(ap.lr_groups) * ap.lr_stripes
                    : static_cast<size_t>(ap.n_ranges) * ((ap.ncols + ap.gen_C - 1) / ap.gen_C);
@@ -1201,6 +1630,21 @@ void launch_lr(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, const TI* P, TK* U, con
 template <typename TI, typename TK, typename TV, typename TB>
 void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const TI* P, TK* U,
                   const Combine<TK, TB>& cb) {
+  if constexpr (sizeof(TI) == 4 && sizeof(TV) == 4) {
+    if (ap.slab) {
+      KScope ks_(c, "cg_apply");
+      auto k = cb.Xt ? (ap.s_evr == 9 ? slab_k<TK, 9, true, TB> : slab_k<TK, 16, true, TB>)
+                     : (ap.s_evr == 9 ? slab_k<TK, 9, false, TB> : slab_k<TK, 16, false, TB>);
+      ensure_smem(k, ap.s_smem);
+      const SlabPlan sp{ap.s_rec.p,  reinterpret_cast<const SlabStep*>(ap.s_steps.p), ap.s_wsteps.p, ap.s_max_steps,
+                        ap.s_win.p, ap.s_lv.p, ap.s_lo.p};
+      const unsigned grid = static_cast<unsigned>(((ap.p + 31) / 32) * ap.s_parts);
+      k<<<grid, kSlabThreads, ap.s_smem, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols), ap.s_parts,
+                                                     sp, P, cb);
+      launched(c);
+      return;
+    }
+  }
   if (ap.fused) {
     KScope ks_(c, "cg_apply");
     auto k = fused_k<TI, TK, TV, TB>;

@@ -205,9 +205,11 @@ def _case_by_name(name, seed=7):
     return Lr, Lc, plan, Xt
 
 
-@pytest.fixture(params=["fused", "split"])
+@pytest.fixture(params=["fused", "split", "slab"])
 def path(request, ctx):
-    """Both operator paths (fused one-pass / two-pass band + row groups)."""
+    """Every operator path (fused one-pass / two-pass band + row groups /
+    32-row slab for fp32 iterates; fp64 iterates fall back from "slab" to
+    the two passes)."""
     ctx.set_apply_path(request.param)
     yield request.param
     ctx.set_apply_path("auto")
@@ -224,6 +226,61 @@ def test_decoder_apply_fp64_bit_exact(P, ctx, case, path):
     want = O.decoder_apply(X, plan_o, Lr, Lc, 1 / 0.3, 1 / 0.4)
     assert np.array_equal(AP, want)
     assert abs(dot - float(np.sum(X * want))) <= 1e-12 * abs(dot)
+
+
+def _star_laplacian(n, hub_deg, seed):
+    """kNN graph plus one hub joined to `hub_deg` nodes: a pull row longer
+    than the slab pass's record ring holds at once."""
+    import scipy.sparse as sp
+
+    W = knn_laplacian(n, 3, 5, seed).to_scipy()
+    W = -(W - sp.diags(W.diagonal()))
+    hub = sp.coo_matrix((np.ones(hub_deg), (np.zeros(hub_deg, int), np.arange(1, hub_deg + 1))), shape=(n, n))
+    W = (W + hub + hub.T).tocsr()
+    return O.graph_from_adjacency(O.Csr.from_scipy(W)).laplacian
+
+
+SLAB_CASES = {  # (operators, p, n, |omega_r|, |omega_c>), the path the slab request takes
+    "knn_rows": (lambda: (knn_laplacian(96, 3, 7, 23), knn_laplacian(120, 3, 7, 24), 96, 120, 30, 30), "slab"),
+    "grid": (DECODER_CASES["grid"], "slab"),  # 9-entry pixel stencil, +-w rows in the staged window
+    "grid_ragged": (lambda: (_grid_laplacian(37, 28), knn_laplacian(300, 3, 10, 61), 37 * 28, 300, 110, 40), "slab"),
+    "col_hubs": (lambda: (_grid_laplacian(20, 16), knn_laplacian(700, 24, 10, 71), 320, 700, 40, 90), "slab"),
+    # a 231-entry pull row: its quad runs as several steps of the record ring
+    "long_pull_row": (lambda: (_grid_laplacian(16, 12), _star_laplacian(400, 230, 81), 192, 400, 30, 50), "slab"),
+    # fallbacks to the fused pass: p not a multiple of 4; row windows wider
+    # than 32 chunks (random rows over p = 600)
+    "p_odd": (DECODER_CASES["smem"], "fused"),
+    "wide_rows": (lambda: (knn_laplacian(600, 3, 7, 91), knn_laplacian(80, 3, 7, 92), 600, 80, 150, 20), "fused"),
+}
+
+
+@pytest.mark.parametrize("case", sorted(SLAB_CASES))
+def test_decoder_apply_fp32_slab_equals_fused(P, ctx, case):
+    """fp32 iterates: the slab pass (shared-memory slab of 32 rows x all
+    columns, L_c records streamed through warp rings) accumulates every
+    entry in the same CSR order as the fused pass -- bit-identical -- and
+    sits within fp32 rounding of the fp64 oracle (decoders.cpp:160-170)."""
+    make, want_path = SLAB_CASES[case]
+    Lr, Lc, p, n, rr, rc = make()
+    plan_o = O.draw_plan(p, n, rr, rc, seed=5)
+    plan = P.SamplingPlan(plan_o.omega_r, plan_o.omega_c, plan_o.p, plan_o.n)
+    X = np.asfortranarray(np.random.default_rng(4).standard_normal((p, n)).astype(np.float32))
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    out = {}
+    try:
+        for path in ("slab", "fused"):
+            ctx.set_apply_path(path)
+            out[path] = P.decoder_apply(X, plan, dLr, dLc, 1 / 0.3, 1 / 0.4, ctx=ctx)
+            assert ctx.last_apply_path() == (want_path if path == "slab" else "fused")
+    finally:
+        ctx.set_apply_path("auto")
+    (As, ds), (Af, df) = out["slab"], out["fused"]
+    assert As.dtype == np.float32
+    assert np.array_equal(As, Af)
+    assert abs(ds - df) <= 1e-12 * abs(df)  # fp64 partial sums over different CTA grids
+    want = O.decoder_apply(X.astype(np.float64), plan_o, Lr, Lc, 1 / 0.3, 1 / 0.4)
+    assert rel(As, want) <= 1e-6
+    assert abs(ds - float(np.sum(X.astype(np.float64) * want))) <= 1e-5 * abs(ds)
 
 
 @pytest.mark.parametrize("case", sorted(DECODER_CASES))

@@ -68,9 +68,14 @@ if "cfg1" in which:
     p, n = wl.Y.shape
     plan = P.draw_plan(p, n, -(-p // 10), -(-n // 10), seed=1603)
     Xt = P.subsample(Y, plan, ctx=ctx)
+    paths = os.environ.get("PATHS", "auto").split(",")
     for kp in ("fp64", "fp32"):
-        cfg = P.DecoderConfig(1.0, 1e-30, 200, krylov_precision=kp)
-        ms, kt, r = timed(lambda: P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian,
-                                                     P.SpectralGap(lambda_k1=wl.lambda_k1_r),
-                                                     P.SpectralGap(lambda_k1=wl.lambda_k1_c), cfg, ctx=ctx), reps=5)
-        print(f"cfg1 decode krylov {kp}: {ms:.2f} ms kernels {kt}", flush=True)
+        for path in paths:
+            ctx.set_apply_path(path)
+            cfg = P.DecoderConfig(1.0, 1e-30, 200, krylov_precision=kp)
+            ms, kt, r = timed(lambda: P.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian,
+                                                         P.SpectralGap(lambda_k1=wl.lambda_k1_r),
+                                                         P.SpectralGap(lambda_k1=wl.lambda_k1_c), cfg, ctx=ctx), reps=5)
+            print(f"cfg1 decode krylov {kp} path {path} ({ctx.last_apply_path()}): {ms:.2f} ms kernels {kt}",
+                  flush=True)
+    ctx.set_apply_path("auto")

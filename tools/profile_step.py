@@ -23,7 +23,7 @@ def main():
     tdt = torch.float64 if fp64 else torch.float32
     Yd = torch.tensor(np.ascontiguousarray(wl.Y.T), dtype=tdt, device="cuda").t()
     Wr = P.SparseMatrix.from_scipy(wl.W_r, ctx=ctx)
-    cfg = pipeline_config(P, wl)
+    cfg = pipeline_config(P, wl, "fp64" if fp64 else "fp32")  # the bench step's decoder precision
     P.run_pipeline(Yd, cfg, W_r=Wr, ctx=ctx)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
