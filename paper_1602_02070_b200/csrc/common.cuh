@@ -84,8 +84,21 @@ struct Ctx {
   std::string timing_filter;  // comma-separated tags; empty = all
   int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused, 3 slab (tests)
   int last_apply_path = 0;    // the path the last planned operator took (1, 2 or 3; tests)
+  cudaStream_t side = nullptr;  // second stream for independent work (lazily created)
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   KernelTimes kt;
 };
+
+// The context's side stream (non-blocking, created on first use) and its
+// fork / join events.
+inline cudaStream_t side_stream(Ctx* c) {
+  if (!c->side) {
+    CUDA_OK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&c->join_ev, cudaEventDisableTiming));
+  }
+  return c->side;
+}
 
 // RAII scope timing one kernel launch under `tag` when timing is enabled.
 struct KScope {
@@ -406,6 +419,8 @@ struct HostRng {
 
 // Internal entry points shared between translation units.
 double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter);
+void power_norm_pair(Ctx* c, Csr* A1, Csr* A2, double tol, uint64_t seed, i64 max_iter, double* out1,
+                     double* out2);
 // kmeans / decode_labels on the device (cluster.cu).
 void kmeans_device(Ctx* c, const double* X, i64 rows, i64 n, i64 k, i64 restarts, uint64_t seed, i64 max_iter,
                    int* assignments_dev, double* wcss_out);

@@ -428,15 +428,30 @@ __device__ __forceinline__ double warp_row_dot(i64 k0, i64 k1, const int* __rest
   return warp_sum(acc);
 }
 
-// Small operators: the whole iteration in one CTA, v and w in shared memory.
+// Small operators: the whole iteration in one CTA, v and w in shared memory
+// (and the CSR rows too when they fit: no grid barrier, no L2 round trip).
 __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __restrict__ rp,
                                                            const int* __restrict__ ci,
                                                            const double* __restrict__ val,
                                                            const double* __restrict__ v0, double tol,
-                                                           i64 max_iter, PowerState* st) {
+                                                           i64 max_iter, int mat_in_smem, PowerState* st) {
   extern __shared__ double sm[];
   double* vs = sm;
   double* ws = sm + n;
+  const i64 nnz = rp[n];
+  double* sval = ws + n;
+  i64* srp = reinterpret_cast<i64*>(sval + (mat_in_smem ? nnz : 0));
+  int* sci = reinterpret_cast<int*>(srp + (mat_in_smem ? n + 1 : 0));
+  if (mat_in_smem) {
+    for (i64 k = threadIdx.x; k < nnz; k += blockDim.x) {
+      sval[k] = val[k];
+      sci[k] = ci[k];
+    }
+    for (i64 i = threadIdx.x; i <= n; i += blockDim.x) srp[i] = rp[i];
+  }
+  const i64* RP = mat_in_smem ? srp : rp;
+  const int* CI = mat_in_smem ? sci : ci;
+  const double* VA = mat_in_smem ? sval : val;
   __shared__ double warp_part[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(512) power_iter_small_k(i64 n, const i64* __re
   for (; it < max_iter; ++it) {
     double part = 0.0;
     for (i64 r = wid; r < n; r += nw) {
-      const double acc = warp_row_dot(rp[r], rp[r + 1], ci, val, vs, lane);
+      const double acc = warp_row_dot(RP[r], RP[r + 1], CI, VA, vs, lane);
       if (lane == 0) {
         ws[r] = acc;
         part += acc * acc;
@@ -580,33 +595,57 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   }
 }
 
-double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
+// One power iteration, set up and launched on `s` (the host work -- start
+// vector, geometry -- happens now; the result lands in st->est).  Returns
+// false when there is nothing to launch (st->est is then set on the host:
+// n == 0, ||v0|| == 0 or max_iter <= 0 give 0).
+struct PowerJob {
+  DevBuf<double> v, w, part;
+  DevBuf<PowerState> st;
+  double host_est = 0.0;
+  bool launched = false;
+  bool small = false;
+};
+
+static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter, PowerJob& job, cudaStream_t s,
+                          bool timed) {
   if (A->rows != A->cols) invalid("power iteration: square matrix required");
   const i64 n = A->rows;
-  if (n == 0) return 0.0;
+  if (n == 0) return;
   HostRng rng(HostRng::mix(seed ^ 0x5ca1ab1eULL));
   std::vector<double> v0(static_cast<size_t>(n));
   for (i64 i = 0; i < n; ++i) v0[i] = rng.gaussian();
   double nv = 0.0;
   for (i64 i = 0; i < n; ++i) nv += v0[i] * v0[i];
   nv = std::sqrt(nv);
-  if (nv == 0.0) return 0.0;
+  if (nv == 0.0) return;
   for (double& x : v0) x /= nv;
-  if (max_iter <= 0) return 0.0;
-  DevBuf<double> v(c, n), w(c, n);
-  CUDA_OK(cudaMemcpyAsync(v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
-  DevBuf<PowerState> st(c, 1);
-  st.zero(c);
+  if (max_iter <= 0) return;
+  job.v.alloc(c, n);
+  job.st.alloc(c, 1);
+  job.st.zero(c);
+  CUDA_OK(cudaMemcpyAsync(job.v.p, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  // one CTA when v, w and the CSR rows fit its shared memory (no grid barrier)
   const size_t small_smem = 2 * sizeof(double) * static_cast<size_t>(n);
-  const i64 small_nnz = 4096;  // single-CTA kernel (no grid barrier) up to this many entries
-  if (small_smem <= 200 * 1024 && A->nnz <= small_nnz) {
-    ensure_smem(power_iter_small_k, small_smem);
-    {
-      KScope ks_(c, "power_iter");
-      power_iter_small_k<<<1, 512, small_smem, c->stream>>>(n, A->rp, A->ci, A->v, v.p, tol, max_iter, st.p);
-      launched(c);
+  const size_t mat_smem = static_cast<size_t>(A->nnz) * 12 + static_cast<size_t>(n + 1) * 8 + 16;
+  if (small_smem + mat_smem <= 200 * 1024 || (small_smem <= 200 * 1024 && A->nnz <= 4096)) {
+    const int in_smem = small_smem + mat_smem <= 200 * 1024 ? 1 : 0;
+    const size_t smem = small_smem + (in_smem ? mat_smem : 0);
+    ensure_smem(power_iter_small_k, smem);
+    job.small = true;
+    job.launched = true;
+    if (s != c->stream) {  // the side stream starts after this job's inputs
+      CUDA_OK(cudaEventRecord(c->fork_ev, c->stream));
+      CUDA_OK(cudaStreamWaitEvent(s, c->fork_ev, 0));
     }
-    return read_back(c, st.p).est;
+    if (timed) {
+      KScope ks_(c, "power_iter");
+      power_iter_small_k<<<1, 512, smem, s>>>(n, A->rp, A->ci, A->v, job.v.p, tol, max_iter, in_smem, job.st.p);
+    } else {
+      power_iter_small_k<<<1, 512, smem, s>>>(n, A->rp, A->ci, A->v, job.v.p, tol, max_iter, in_smem, job.st.p);
+    }
+    launched(c);
+    return;
   }
   // One CTA per SM (at most one per row): measured, the per-iteration cost is
   // the in-CTA product, so spreading it wins over the cheaper barrier of a
@@ -630,22 +669,54 @@ double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 512, smem));
   if (per_sm < 1) invalid("power iteration: kernel does not fit on an SM");
-  DevBuf<double> part(c, 2 * nb), wb(c, 2 * n);
+  job.part.alloc(c, 2 * nb);
+  job.w.alloc(c, 2 * n);
   const i64* rp = A->rp;
   const int* ci = A->ci;
   const double* val = A->v;
-  const double* vp = v.p;
-  double* wp = wb.p;
-  double* pp = part.p;
-  PowerState* sp = st.p;
-  void* args[] = {(void*)&n, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp, (void*)&pp,
+  const double* vp = job.v.p;
+  double* wp = job.w.p;
+  double* pp = job.part.p;
+  PowerState* sp = job.st.p;
+  i64 nn = n;
+  void* args[] = {(void*)&nn, (void*)&rp, (void*)&ci, (void*)&val, (void*)&vp, (void*)&wp, (void*)&pp,
                   (void*)&tol, (void*)&max_iter, (void*)&slice_in_smem, (void*)&v_in_smem, (void*)&sp};
-  {
+  job.launched = true;
+  if (timed) {
     KScope ks_(c, "power_iter");
-    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(512), args, smem, c->stream));
-    launched(c);
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(512), args, smem, s));
+  } else {
+    CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop_k, dim3(nb), dim3(512), args, smem, s));
   }
-  return read_back(c, st.p).est;
+  launched(c);
+}
+
+static double power_result(Ctx* c, PowerJob& job) {
+  return job.launched ? read_back(c, job.st.p).est : job.host_est;
+}
+
+double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter) {
+  PowerJob job;
+  power_prepare(c, A, tol, seed, max_iter, job, c->stream, true);
+  return power_result(c, job);
+}
+
+// Both FISTA norms (frpcag.cpp:72-73).  When one operator takes the
+// single-CTA kernel and the other the cooperative grid, the single CTA runs
+// on a side stream beside the grid (it fits next to a grid CTA on one SM).
+void power_norm_pair(Ctx* c, Csr* A1, Csr* A2, double tol, uint64_t seed, i64 max_iter, double* out1,
+                     double* out2) {
+  PowerJob j1, j2;
+  cudaStream_t side = side_stream(c);
+  const bool small1 = A1->rows == A1->cols &&
+                      2 * 8 * static_cast<size_t>(A1->rows) + static_cast<size_t>(A1->nnz) * 12 +
+                              static_cast<size_t>(A1->rows + 1) * 8 + 16 <= 200 * 1024;
+  power_prepare(c, A1, tol, seed, max_iter, j1, small1 ? side : c->stream, !small1);
+  power_prepare(c, A2, tol, seed, max_iter, j2, c->stream, true);
+  CUDA_OK(cudaEventRecord(c->join_ev, side));
+  CUDA_OK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+  *out1 = power_result(c, j1);
+  *out2 = power_result(c, j2);
 }
 
 // ------------------------------------------------------------------ gather / prox / grad / objective
@@ -844,6 +915,12 @@ int cpcag_ctx_destroy(cpcag_ctx ctx) {
     }
     for (auto e : c->kt.pool) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->side) {
+      cudaStreamSynchronize(c->side);
+      cudaStreamDestroy(c->side);
+      cudaEventDestroy(c->fork_ev);
+      cudaEventDestroy(c->join_ev);
+    }
     cudaStreamDestroy(c->own);
     delete c;
   });

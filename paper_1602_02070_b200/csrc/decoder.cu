@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "decoder.cuh"
@@ -51,19 +52,25 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
   const bool exact = sizeof(TX) == 8;
   HostPull<TV> lcp;
   host_pull<TV>(c, pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
+  trace_mark(c, "decode: operator copies");
   plan_apply<TK, TK, TV>(c, apK, p, n, n, 0, rpr, cir, vr, exact, &lcp);
-  plan_apply<TX, TK, TV>(c, apX, p, n, n, 0, rpr, cir, vr, exact, &lcp);
+  trace_mark(c, "decode: plan K");
+  constexpr bool same_plan = std::is_same<TX, TK>::value;  // the true residual reuses the CG's operator plan
+  if constexpr (!same_plan) plan_apply<TX, TK, TV>(c, apX, p, n, n, 0, rpr, cir, vr, exact, &lcp);
+  const ApplyPlan& apR = same_plan ? apK : apX;
+  trace_mark(c, "decode: plans");
   DevBuf<TK> R(c, N), P(c, N), AP(c, N), U(c, N);
   DevBuf<CgState> st(c, 1);
   st.zero(c);
   const unsigned nbv = stride_blocks(c, std::max<i64>(N, 1));
-  size_t nparts = std::max<size_t>({static_cast<size_t>(nbv), lr_blocks(apK), lr_blocks(apX)});
+  size_t nparts = std::max<size_t>({static_cast<size_t>(nbv), lr_blocks(apK), lr_blocks(apR)});
   DevBuf<double> part(c, std::max<size_t>(nparts, 1));
   cg_init_k<TK, TX, TX><<<nbv, kBlock, 0, c->stream>>>(p, n, 0, pl, Xt, X, R.p, P.p, part.p, st.p);
   launched(c);
   cg_start_k<<<1, 1, 0, c->stream>>>(st.p, cfg.pcg_tol, cfg.pcg_max_iter);
   launched(c);
   CgState host = read_back(c, st.p);
+  trace_mark(c, "decode: init");
   if (host.zero_rhs) {  // solvers.hpp:40-44: x = b = 0
     *converged = 1;
     *iterations = 0;
@@ -101,13 +108,14 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
     launched_it += todo;
     host = read_back(c, st.p);
   }
+  trace_mark(c, "decode: CG iterations");
   if (host.err) runtime("pcg: breakdown (nonpositive curvature) at iteration " + std::to_string(host.err_it));
   // true residual ||b - A x|| / ||b|| (solvers.hpp:69-72), x in its stored precision
   {
     KScope ks_(c, "cg_true_residual");
     CUDA_OK(cudaMemsetAsync(&st.p->done, 0, sizeof(int), c->stream));
     const Combine<TK, TX> cbR{U.p, nullptr, gr, gc, pl, Xt, part.p, st.p};
-    launch_apply<TX, TK, TV, TX>(c, apX, pr, pc, X, U.p, cbR);
+    launch_apply<TX, TK, TV, TX>(c, apR, pr, pc, X, U.p, cbR);
   }
   host = read_back(c, st.p);
   const double rel = host.norm_b > 0.0 ? std::sqrt(host.curv) / host.norm_b : 0.0;

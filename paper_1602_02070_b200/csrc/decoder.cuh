@@ -1184,27 +1184,47 @@ bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr,
     for (i64 i = 0; i < p; ++i) mr = std::max(mr, rpr[i + 1] - rpr[i]);
     if (mr > 16) return false;
     const int EVR = mr <= 9 ? 9 : 16;
+    trace_mark(c, "slab plan: enter");
     // L_r windows
     const i64 slabs = (p + 31) / 32;
     std::vector<int> win(static_cast<size_t>(slabs) * 32, kNoChunk);
     std::vector<float> lv(static_cast<size_t>(EVR) * p, 0.f);
     std::vector<int> lo(static_cast<size_t>(EVR) * p, 0);
     std::vector<int> ch;
+    std::vector<uint64_t> bits;
+    std::vector<int> rank;
     for (i64 sl = 0; sl < slabs; ++sl) {
       const i64 i0 = sl * 32, i1 = std::min(p, i0 + 32);
-      ch.clear();
+      // distinct 4-row chunks the slab's rows reference, in order (bitmap over their range)
+      int lo_c = INT32_MAX, hi_c = -1;
       for (i64 i = i0; i < i1; ++i) {
-        ch.push_back(static_cast<int>(i & ~i64{3}));
-        for (i64 k = rpr[i]; k < rpr[i + 1]; ++k) ch.push_back(cir[k] & ~3);
+        lo_c = std::min(lo_c, static_cast<int>(i >> 2));
+        hi_c = std::max(hi_c, static_cast<int>(i >> 2));
+        for (i64 k = rpr[i]; k < rpr[i + 1]; ++k) {
+          lo_c = std::min(lo_c, cir[k] >> 2);
+          hi_c = std::max(hi_c, cir[k] >> 2);
+        }
       }
-      std::sort(ch.begin(), ch.end());
-      ch.erase(std::unique(ch.begin(), ch.end()), ch.end());
+      if (hi_c - lo_c >= 65536) return false;  // rows scattered over more than 256 K rows
+      const size_t words = static_cast<size_t>(hi_c - lo_c) / 64 + 1;
+      bits.assign(words, 0);
+      auto mark = [&](int row) {
+        const int q = (row >> 2) - lo_c;
+        bits[q >> 6] |= uint64_t{1} << (q & 63);
+      };
+      for (i64 i = i0; i < i1; ++i) {
+        mark(static_cast<int>(i));
+        for (i64 k = rpr[i]; k < rpr[i + 1]; ++k) mark(cir[k]);
+      }
+      ch.clear();
+      for (size_t w = 0; w < words && ch.size() <= 32; ++w)
+        for (uint64_t b = bits[w]; b; b &= b - 1)
+          ch.push_back((lo_c + static_cast<int>(w * 64 + __builtin_ctzll(b))) * 4);
       if (ch.size() > 32) return false;
       for (size_t t = 0; t < ch.size(); ++t) win[sl * 32 + t] = ch[t] - static_cast<int>(i0);
-      auto where = [&](i64 j) {
-        const int t = static_cast<int>(std::lower_bound(ch.begin(), ch.end(), static_cast<int>(j & ~i64{3})) - ch.begin());
-        return (t * 4 + static_cast<int>(j & 3)) * 4;
-      };
+      rank.assign(static_cast<size_t>(hi_c - lo_c) + 1, 0);
+      for (size_t t = 0; t < ch.size(); ++t) rank[(ch[t] >> 2) - lo_c] = static_cast<int>(t);
+      auto where = [&](i64 j) { return (rank[(j >> 2) - lo_c] * 4 + static_cast<int>(j & 3)) * 4; };
       for (i64 i = i0; i < i1; ++i) {
         for (int e = 0; e < EVR; ++e) {
           const i64 k = rpr[i] + e;
@@ -1214,6 +1234,7 @@ bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr,
         }
       }
     }
+    trace_mark(c, "slab plan: windows");
     // column ranges per slab: minimise waves x (slab copy + columns), the copy
     // costing ~0.1 of a whole slab's compute
     const i64 per_sm = smem <= 113 * 1024 ? 2 : 1;
@@ -1308,6 +1329,7 @@ bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr,
       }
       wsteps.push_back(static_cast<int>(steps.size()));
     }
+    trace_mark(c, "slab plan: quads");
     int max_steps = 0;
     for (int part = 0; part < best; ++part)
       max_steps = std::max(max_steps, wsteps[part * (kSlabWarps + 1) + kSlabWarps] - wsteps[part * (kSlabWarps + 1)]);

@@ -663,8 +663,13 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
   double step = cfg.step;
   if (step <= 0.0) {
     // frpcag.cpp:70-75 (both norms with tol 1e-7, seed 42).
-    const double nc = cfg.gamma_c != 0.0 ? power_norm(c, Lc, 1e-7, 42, 50000) : 0.0;
-    const double nr = cfg.gamma_r != 0.0 ? power_norm(c, Lr, 1e-7, 42, 50000) : 0.0;
+    double nc = 0.0, nr = 0.0;
+    if (cfg.gamma_c != 0.0 && cfg.gamma_r != 0.0)
+      power_norm_pair(c, Lc, Lr, 1e-7, 42, 50000, &nc, &nr);
+    else if (cfg.gamma_c != 0.0)
+      nc = power_norm(c, Lc, 1e-7, 42, 50000);
+    else if (cfg.gamma_r != 0.0)
+      nr = power_norm(c, Lr, 1e-7, 42, 50000);
     const double beta = 2.0 * cfg.gamma_c * nc + 2.0 * cfg.gamma_r * nr;
     step = beta > 0.0 ? 1.0 / beta : 1.0;
   }

@@ -583,6 +583,214 @@ __global__ void __launch_bounds__(NT, MINB) pcg_persistent_k(i64 n, i64 nb, cons
     }
 }
 
+// ------------------------------------------------------------------ shared-memory resident PCG
+// One CTA per right-hand side, for interiors whose p, x and the Jacobi
+// inverse (3 n fp64) fit in one CTA's shared memory (config 1 rows: n = 9 273,
+// 222 KB).  Thread t owns rows t + r NT (r < RPT) and keeps their r and A p in
+// registers; the SpMV gathers p from shared memory; the matrix is read as ELL
+// (entry k of row i at k n + i, zero padded with the row's own column, CSR
+// order kept) from L2, shared by every CTA.  Per iteration three CTA barriers
+// (two reductions, the p update); every CTA runs its column to completion and
+// the hardware schedules the next column on the freed SM.  Same recurrence
+// and per-entry arithmetic as pcg_persistent_k (solvers.hpp:33-74).
+template <int NV, int NW>
+__device__ __forceinline__ void cta_sum(double (&v)[NV], double* red, int& par) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+  double* b = red + par * NV * NW;
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) b[q * NW + wid] = v[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += b[q * NW + w];
+    v[q] = t;
+  }
+  par ^= 1;
+}
+
+__global__ void csr_to_ell_k(i64 n, int E, const i64* __restrict__ rp, const int* __restrict__ ci,
+                             const double* __restrict__ v, double* __restrict__ ev, int* __restrict__ ec) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const i64 k0 = rp[i], d = rp[i + 1] - k0;
+  for (int k = 0; k < E; ++k) {
+    ev[k * n + i] = k < d ? v[k0 + k] : 0.0;
+    ec[k * n + i] = k < d ? ci[k0 + k] : static_cast<int>(i);
+  }
+}
+
+constexpr int kPcgSmemThreads = 512;
+
+template <int RPT, int E>
+__global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, const double* __restrict__ ev,
+                                                                 const int* __restrict__ ec,
+                                                                 const double* __restrict__ inv,
+                                                                 const double* __restrict__ B, double* __restrict__ X,
+                                                                 double tol, i64 max_iter, ColState* st) {
+  constexpr int NT = kPcgSmemThreads, NW = NT / 32;
+  extern __shared__ __align__(16) double smd[];
+  double* Ps = smd;
+  double* Xs = smd + n;
+  double* Is = smd + 2 * n;
+  __shared__ double red[2 * 3 * NW];
+  const i64 col = blockIdx.x;
+  const int t = threadIdx.x;
+  for (int i = t; i < n; i += NT) {
+    Is[i] = inv[i];
+    Xs[i] = X[slab_at(n, i, col)];
+  }
+  __syncthreads();
+  int par = 0;
+  auto spmv = [&](const double* src, int i) {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < E; ++k) a = __dadd_rn(a, __dmul_rn(ev[static_cast<i64>(k) * n + i], src[ec[static_cast<i64>(k) * n + i]]));
+    return a;
+  };
+  double R[RPT], AP[RPT];
+  // r = b - A x, z = inv o r, p = z
+  double s3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * NT;
+    R[r] = 0.0;
+    if (i < n) {
+      const double b = B[slab_at(n, i, col)];
+      const double rr = __dsub_rn(b, spmv(Xs, i));
+      const double z = __dmul_rn(Is[i], rr);
+      R[r] = rr;
+      Ps[i] = z;
+      s3[0] += b * b;
+      s3[1] += rr * z;
+      s3[2] += rr * rr;
+    }
+  }
+  cta_sum<3, NW>(s3, red, par);
+  const double norm_b = sqrt(s3[0]), target = tol * norm_b;
+  double rho = s3[1];
+  int done = norm_b == 0.0 ? 2 : ((sqrt(s3[2]) <= target || max_iter <= 0) ? 1 : 0);
+  int err = 0;
+  double curv = 0.0;
+  i64 it = 0;
+  __syncthreads();  // p complete
+  while (done == 0) {
+    double cv[1] = {0.0};
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * NT;
+      AP[r] = 0.0;
+      if (i < n) {
+        AP[r] = spmv(Ps, i);
+        cv[0] += Ps[i] * AP[r];
+      }
+    }
+    cta_sum<1, NW>(cv, red, par);
+    if (!isfinite(cv[0]) || cv[0] <= 0.0) {
+      err = 1;
+      curv = cv[0];
+      done = 1;
+      break;
+    }
+    const double alpha = rho / cv[0];
+    double s2[2] = {0.0, 0.0};
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * NT;
+      if (i < n) {
+        Xs[i] = __dadd_rn(Xs[i], __dmul_rn(alpha, Ps[i]));
+        const double rr = __dsub_rn(R[r], __dmul_rn(alpha, AP[r]));
+        R[r] = rr;
+        const double z = __dmul_rn(Is[i], rr);
+        s2[0] += rr * z;
+        s2[1] += rr * rr;
+      }
+    }
+    cta_sum<2, NW>(s2, red, par);
+    const double beta = s2[0] / rho;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+      const int i = t + r * NT;
+      if (i < n) Ps[i] = __dadd_rn(__dmul_rn(Is[i], R[r]), __dmul_rn(beta, Ps[i]));
+    }
+    rho = s2[0];
+    it += 1;
+    if (sqrt(s2[1]) <= target || it >= max_iter) done = 1;
+    __syncthreads();  // p and x complete
+  }
+  __syncthreads();
+  // true residual; x back to the slab layout
+  double sr[1] = {0.0};
+#pragma unroll
+  for (int r = 0; r < RPT; ++r) {
+    const int i = t + r * NT;
+    if (i < n) {
+      const double e = __dsub_rn(B[slab_at(n, i, col)], spmv(Xs, i));
+      sr[0] += e * e;
+      X[slab_at(n, i, col)] = Xs[i];
+    }
+  }
+  cta_sum<1, NW>(sr, red, par);
+  if (t == 0 && col < nb) {
+    ColState& S = st[col];
+    S.norm_b = norm_b;
+    S.target = target;
+    S.it = it;
+    S.err = err;
+    S.curv = curv;
+    S.done = done == 2 ? 2 : 1;
+    S.rel_res = sqrt(sr[0]) / norm_b;
+  }
+}
+
+// Runs pcg_smem_k when it applies (3 n fp64 within a CTA's shared memory,
+// rows of <= 16 entries, n <= 20 x 512); returns false otherwise.
+template <int RPT>
+bool pcg_smem_rpt(Ctx* c, int E, const double* ev, const int* ec, const double* inv, const double* B, double* X,
+                  i64 n, i64 nb, double tol, i64 max_iter, ColState* st) {
+  const size_t smem = static_cast<size_t>(3 * n) * sizeof(double);
+  auto launch = [&](auto k) {
+    ensure_smem(k, smem);
+    KScope ks_(c, "pcg_persistent");
+    k<<<static_cast<unsigned>(nb), kPcgSmemThreads, smem, c->stream>>>(static_cast<int>(n), nb, ev, ec, inv, B, X, tol,
+                                                                      max_iter, st);
+    launched(c);
+  };
+  if (E <= 9)
+    launch(pcg_smem_k<RPT, 9>);
+  else
+    launch(pcg_smem_k<RPT, 16>);
+  return true;
+}
+
+bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb, double tol,
+              i64 max_iter, ColState* st) {
+  const size_t smem = static_cast<size_t>(3 * n) * sizeof(double) + 2 * 3 * 16 * sizeof(double);
+  if (n <= 0 || n > 20 * kPcgSmemThreads || smem > 227 * 1024 || A->nnz == 0) return false;
+  // longest row (E): one small reduction on the host copy of the row pointers
+  std::vector<i64> rp(static_cast<size_t>(n) + 1);
+  CUDA_OK(cudaMemcpyAsync(rp.data(), A->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  i64 E = 0;
+  for (i64 i = 0; i < n; ++i) E = std::max(E, rp[i + 1] - rp[i]);
+  if (E > 16) return false;
+  const int Ep = E <= 9 ? 9 : 16;
+  DevBuf<double> ev(c, static_cast<size_t>(Ep) * n);
+  DevBuf<int> ec(c, static_cast<size_t>(Ep) * n);
+  csr_to_ell_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ev.p, ec.p);
+  launched(c);
+  const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
+  if (rpt <= 4) return pcg_smem_rpt<4>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+  if (rpt <= 8) return pcg_smem_rpt<8>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+  if (rpt <= 12) return pcg_smem_rpt<12>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+  if (rpt <= 16) return pcg_smem_rpt<16>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+  return pcg_smem_rpt<20>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+}
+
 struct PcgBatchOut {
   std::vector<ColState> cols;
 };
@@ -641,9 +849,14 @@ void pcg_slab(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   out->cols.assign(static_cast<size_t>(nb), ColState{});
   if (nb == 0) return;
   const i64 nbp = (nb + kCpb - 1) / kCpb * kCpb;
-  DevBuf<double> R(c, n * nbp), P(c, n * nbp), AP(c, n * nbp);
   DevBuf<ColState> st(c, nb);
   st.zero(c);
+  if (pcg_smem(c, A, inv, B, X, n, nb, tol, max_iter, st.p)) {
+    CUDA_OK(cudaMemcpyAsync(out->cols.data(), st.p, sizeof(ColState) * nb, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    return;
+  }
+  DevBuf<double> R(c, n * nbp), P(c, n * nbp), AP(c, n * nbp);
   {
     // One CTA per kCpb columns: 1024 threads while the CTAs fit in one wave,
     // else 512 threads at 2 CTAs per SM (cfg1 rows: 258 CTAs, one wave).

@@ -230,6 +230,49 @@ def test_kron_grid_graph(P, ctx):
     assert np.abs(R.to_dense() - Ro.to_dense()).max() <= 1e-9 * np.abs(Ro.to_dense()).max()
 
 
+def _stencil_laplacian(h, w, offsets):
+    ti, tj = [], []
+    for r in range(h):
+        for c in range(w):
+            for dr, dc in offsets:
+                r2, c2 = r + dr, c + dc
+                if 0 <= r2 < h and 0 <= c2 < w:
+                    a, b = r * w + c, r2 * w + c2
+                    ti += [a, b]
+                    tj += [b, a]
+    return O.graph_from_adjacency(O.Csr.from_triplets(h * w, h * w, ti, tj, [1.0] * len(ti))).laplacian
+
+
+@pytest.mark.parametrize("shape,offsets,keep", [
+    ((41, 37), [(0, 1), (1, -1), (1, 0), (1, 1)], 150),                    # rows of <= 9 entries
+    ((33, 29), [(0, 1), (0, 2), (1, -1), (1, 0), (1, 1), (2, 0)], 90),     # rows of <= 13 entries
+])
+def test_kron_shared_memory_pcg(P, ctx, shape, offsets, keep):
+    """Interiors whose PCG vectors fit one CTA's shared memory run one
+    right-hand side per CTA (pcg_smem_k); same recurrence, <= 1e-9."""
+    Lo = _stencil_laplacian(*shape, offsets)
+    n = shape[0] * shape[1]
+    kp = O.draw_plan(n, 1, keep, 1, seed=7).omega_r
+    R = P.kron_reduce(to_device(ctx, Lo), kp, 1e-11, 1e-12, ctx=ctx)
+    Ro = O.kron_reduce(Lo, kp, 1e-11, 1e-12)
+    assert np.abs(R.to_dense() - Ro.to_dense()).max() <= 1e-9 * np.abs(Ro.to_dense()).max()
+
+
+def test_kron_config1_rows_matches_oracle(P, ctx):
+    """Config 1's row reduction at full size: the 112 x 92 pixel grid,
+    1 031 kept pixels, 9 273 interior nodes per PCG (graph.cpp:170-235)."""
+    from paper_1602_02070_b200 import workloads
+
+    W = workloads.grid_adjacency(112, 92)
+    Lo = O.graph_from_adjacency(O.Csr.from_scipy(W)).laplacian
+    kp = O.draw_plan(112 * 92, 1000, 1031, 100, seed=1603).omega_r
+    R = P.kron_reduce(to_device(ctx, Lo), kp, 1e-11, 1e-12, ctx=ctx)
+    Ro = O.kron_reduce(Lo, kp, 1e-11, 1e-12)
+    Rd, Rod = R.to_dense(), Ro.to_dense()
+    assert np.abs(Rd - Rod).max() <= 1e-9 * np.abs(Rod).max()
+    assert np.array_equal(Rd, Rd.T)
+
+
 # ------------------------------------------------------------------ pipeline
 def test_pipeline_small_matches_oracle_stages(P, ctx):
     from paper_1602_02070_b200.workloads import config0
