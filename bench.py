@@ -197,6 +197,14 @@ def clock_sampler(device: int):
 
 
 # ------------------------------------------------------------------ workload
+def y_sha(wl):
+    """First 16 hex digits of SHA-256 over Y's fp32 bytes (column-major): the
+    generator gives the same input on every machine, and both arms say so."""
+    import hashlib
+
+    return hashlib.sha256(np.asfortranarray(wl.Y, dtype=np.float32).tobytes(order="F")).hexdigest()[:16]
+
+
 def make_workload():
     from paper_1602_02070_b200 import workloads
 
@@ -447,7 +455,7 @@ def run_ours(args, rank, local_rank, world):
                                "(rho 1031x100), FRPCAG 300 it, alternate CG decoder 200 it",
                    "global_batch": 1, "parallelism": "replicas" if world > 1 else "single",
                    "l2": "flushed between steps (512 MiB write outside the events)",
-                   "gamma": wl.gamma, "lambda_k1": [wl.lambda_k1_r, wl.lambda_k1_c]},
+                   "gamma": wl.gamma, "lambda_k1": [wl.lambda_k1_r, wl.lambda_k1_c], "y_sha256": y_sha(wl)},
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": int(launches),
         "clocks": clk, "stage_ms": {k: round(v, 3) for k, v in stages.items()}, "iters": iters,
         "cg_iteration": {"bytes_B_iter": cg_iter_bytes,
@@ -581,7 +589,8 @@ def run_reference(args, rank, world):
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded config-1 generator",
            "config": {"workload": "cfg1: CPCA 10304x1000, pixel-grid W_r + kNN(K=10) L_c, a=b=10 "
                                   "(rho 1031x100), FRPCAG 300 it, alternate CG decoder 200 it",
-                      "parallelism": "cpu threads"},
+                      "parallelism": "cpu threads", "lambda_k1": [wl.lambda_k1_r, wl.lambda_k1_c],
+                      "y_sha256": y_sha(wl)},
            "impl": "reference",
            "cpu_baseline": {"value": round(v, 3), "unit": "s", "cores": O.get_threads(), "kind": "port",
                             "sample": sample, "last_step_stage_s": {k: round(x, 3) for k, x in stages.items()},

@@ -1098,11 +1098,16 @@ Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg
   for (i64 j = 0; j < m; ++j)
     if (rp_ba[j + 1] > rp_ba[j]) active.push_back(j);
 
-  // Columns per slice: 6 dense |int| x b fp64 vectors within ~40% of free HBM.
-  size_t free_b = 0, total_b = 0;
-  CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+  // Columns per slice: 6 dense |int| x b fp64 vectors within ~40% of free HBM
+  // (cudaMemGetInfo only for reductions above 1 GB: the query itself was
+  // measured stalling the stream by up to tens of ms).
   const double per_col = 6.0 * 8.0 * static_cast<double>(ni) + 64.0;
-  i64 slice = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
+  i64 slice = static_cast<i64>(active.size());
+  if (per_col * static_cast<double>(active.size()) > 1e9) {
+    size_t free_b = 0, total_b = 0;
+    CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+    slice = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
+  }
   slice = std::max<i64>(1, std::min<i64>(slice, static_cast<i64>(active.size())));
   const i64 max_iter = 20 * ni + 100;
 

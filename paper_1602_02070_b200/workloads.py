@@ -11,10 +11,13 @@ stand in with the configs' shapes, ranks and corruption levels
             8-neighbour pixel grid and a latent 1 000-node circle kNN graph,
             10 % additive outliers U(-255, 255), X0 scaled to max|X0| = 255,
             a = b = 10.
+  (configs 0/1: the rank-k factors are graph-smooth bases -- low-pass
+  filtered Gaussian vectors, smooth_basis -- so the data is the same bits on
+  every machine; the spectral gaps are rounded to 10 digits.)
   config 3  decoder only: kNN graphs (K=10) over N(0, I_64) points, p = 4 096,
             n = 200 000, rank 20 low-pass basis, 1/8 x 1/8 sampling.
 
-Generation uses numpy/scipy only (LAPACK for the small eigenproblems); it is
+Generation uses numpy/scipy only (LAPACK only for eigenvalues); it is
 harness code, never timed.
 """
 from __future__ import annotations
@@ -36,7 +39,12 @@ def knn_laplacian_dense(pts: np.ndarray, K: int) -> np.ndarray:
     for small generator graphs: union symmetrisation, sigma2 = mean of the
     per-point mean squared kNN distance, w = exp(-d2 / sigma2)."""
     P = pts.T
-    g = P @ P.T
+    if P.shape[1] <= 16:  # the generators' 3-D latent points: elementwise (no BLAS), the same bits everywhere
+        g = np.zeros((P.shape[0], P.shape[0]))
+        for d in range(P.shape[1]):
+            g += P[:, d][:, None] * P[:, d][None, :]
+    else:  # CPU-only fallback of _lambda_k1_of_knn
+        g = P @ P.T
     sq = np.diag(g)
     d2 = np.maximum(0.0, sq[:, None] + sq[None, :] - 2.0 * g)
     n = d2.shape[0]
@@ -73,6 +81,44 @@ def grid_adjacency(h: int, w: int):
     W.sum_duplicates()
     W.sort_indices()
     return W
+
+
+def smooth_basis(L, k: int, rs: np.random.Generator, sweeps: int = 300) -> np.ndarray:
+    """Orthonormal n x k basis of graph-smooth vectors: Gaussian vectors
+    low-pass filtered by `sweeps` steps B <- B - L B / (2 max L_ii) (the
+    Gershgorin bound of a Laplacian's spectrum), then modified Gram-Schmidt.
+    Only sparse products and numpy's pairwise sums: the same bits on every
+    machine, unlike LAPACK eigenvectors (arbitrary signs and rotations in
+    degenerate eigenspaces, thread-count dependent)."""
+    import scipy.sparse as sp
+
+    L = sp.csr_matrix(L)
+    s = 1.0 / (2.0 * float(L.diagonal().max()))
+    B = rs.standard_normal((L.shape[0], k))
+    for _ in range(sweeps):
+        B = B - s * (L @ B)
+    for j in range(k):
+        for i in range(j):
+            B[:, j] -= np.sum(B[:, i] * B[:, j]) * B[:, i]
+        B[:, j] /= math.sqrt(np.sum(B[:, j] * B[:, j]))
+    return B
+
+
+def low_rank(U: np.ndarray, A: np.ndarray, V: np.ndarray) -> np.ndarray:
+    """U A V^T as sums of outer products in a fixed order (elementwise numpy,
+    no BLAS, so no FMA/blocking differences between machines)."""
+    M = np.zeros((U.shape[0], A.shape[1]))
+    for j in range(A.shape[0]):
+        M += U[:, j][:, None] * A[j, :][None, :]
+    X = np.zeros((U.shape[0], V.shape[0]), order="F")
+    for j in range(A.shape[1]):
+        X += M[:, j][:, None] * V[:, j][None, :]
+    return X
+
+
+def _round_sig(x: float, digits: int = 10) -> float:
+    """Rounds a generator constant so every machine prints and uses the same value."""
+    return float(f"{x:.{digits}g}")
 
 
 def smallest_eigvecs_dense(L: np.ndarray, k: int):
@@ -126,10 +172,10 @@ def config0(seed: int = 1602, small: bool = False) -> tuple[np.ndarray, np.ndarr
     p, n, k = (60, 80, 5) if small else (200, 300, 10)
     Lr = knn_laplacian_dense(circle_points(p, rs), 10)
     Lc = knn_laplacian_dense(circle_points(n, rs), 10)
-    _, U = smallest_eigvecs_dense(Lr, k)
-    _, V = smallest_eigvecs_dense(Lc, k)
+    U = smooth_basis(Lr, k, rs)
+    V = smooth_basis(Lc, k, rs)
     A = rs.standard_normal((k, k))
-    X0 = np.asfortranarray(U @ A @ V.T)
+    X0 = np.asfortranarray(low_rank(U, A, V))
     Y = add_outliers(X0, 0.05, rs, amp=5.0 * np.abs(X0).max())
     return np.asfortranarray(Y), X0
 
@@ -165,7 +211,7 @@ def _lambda_k1_of_knn(Y, axis_rows, K, k):
         pts = Y if axis_rows else Y.T
         L = knn_laplacian_dense(np.ascontiguousarray(pts.T), K)
     ev = np.linalg.eigvalsh(0.5 * (L + L.T))
-    return float(max(ev[k], 1e-12))
+    return _round_sig(max(ev[k], 1e-12))
 
 
 def config1(seed: int = 1603) -> Workload:
@@ -177,17 +223,18 @@ def config1(seed: int = 1603) -> Workload:
     import scipy.sparse as sp
 
     Lr = sp.diags(deg) - Wr
-    ev_r, U = smallest_eigvecs_sparse(Lr, k + 1)
+    ev_r, _ = smallest_eigvecs_sparse(Lr, k + 1)  # lambda_{k+1} only (eigenvalues are well defined)
+    U = smooth_basis(Lr, k, rs)
     Lc_lat = knn_laplacian_dense(circle_points(n, rs), 10)
-    _, V = smallest_eigvecs_dense(Lc_lat, k)
+    V = smooth_basis(Lc_lat, k, rs)
     A = rs.standard_normal((k, k))
-    X0 = U[:, :k] @ A @ V.T
+    X0 = low_rank(U, A, V)
     X0 *= 255.0 / np.abs(X0).max()
     Y = add_outliers(np.asfortranarray(X0), 0.10, rs, symmetric_uniform=255.0)
     p = h * w
     lc = _lambda_k1_of_knn(Y, False, 10, k)
     return Workload("cfg1 CPCA 10304x1000 fp32", np.asfortranarray(Y), np.asfortranarray(X0), 10, 10,
-                    math.sqrt(max(p, n)), 300, 200, 1e-8, float(ev_r[k]), lc, Wr, k)
+                    math.sqrt(max(p, n)), 300, 200, 1e-8, _round_sig(float(ev_r[k])), lc, Wr, k)
 
 
 def config2_points(seed: int = 1604, n: int = 100_000, d: int = 512, clusters: int = 20) -> np.ndarray:

@@ -15,8 +15,12 @@ from oracle import pyoracle as O  # noqa: E402
 from paper_1602_02070_b200.workloads import config0  # noqa: E402
 
 
-def stages():
-    Y, _ = config0(seed=1602, small=True)  # 60 x 80, rank 5 on circle-manifold kNN graphs + 5 % outliers
+def stages(Y=None):
+    """Every stage from Y (default: the config-0 generator's 60 x 80 input;
+    the committed fixture keeps its own Y, so it does not depend on the
+    generator)."""
+    if Y is None:
+        Y, _ = config0(seed=1602, small=True)  # 60 x 80, rank 5 on circle-manifold kNN graphs + 5 % outliers
     p, n = Y.shape
     gr = O.build_knn_graph(Y, True, 10)
     gc = O.build_knn_graph(Y, False, 10)
