@@ -626,9 +626,13 @@ __global__ void csr_to_ell_k(i64 n, int E, const i64* __restrict__ rp, const int
 
 constexpr int kPcgSmemThreads = 512;
 
+// E > 0: the matrix as ELL with E entries a row, read from global memory;
+// E == 0: the CSR (rp, ci, v of nnz entries) staged in shared memory after
+// the three vectors (small interiors, e.g. config 1's 900-node column graph).
 template <int RPT, int E>
 __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, const double* __restrict__ ev,
                                                                  const int* __restrict__ ec,
+                                                                 const i64* __restrict__ crp,
                                                                  const double* __restrict__ inv,
                                                                  const double* __restrict__ B, double* __restrict__ X,
                                                                  double tol, i64 max_iter, ColState* st) {
@@ -637,6 +641,11 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
   double* Ps = smd;
   double* Xs = smd + n;
   double* Is = smd + 2 * n;
+  // E == 0: CSR in shared memory (values, row pointers as int, columns)
+  const int nnz = E == 0 ? static_cast<int>(crp[n]) : 0;
+  double* Sv = smd + 3 * n;
+  int* Srp = reinterpret_cast<int*>(Sv + nnz);
+  int* Sci = Srp + n + 1;
   __shared__ double red[2 * 3 * NW];
   const i64 col = blockIdx.x;
   const int t = threadIdx.x;
@@ -644,12 +653,24 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
     Is[i] = inv[i];
     Xs[i] = X[slab_at(n, i, col)];
   }
+  if constexpr (E == 0) {
+    for (int k = t; k < nnz; k += NT) {
+      Sv[k] = ev[k];
+      Sci[k] = ec[k];
+    }
+    for (int i = t; i <= n; i += NT) Srp[i] = static_cast<int>(crp[i]);
+  }
   __syncthreads();
   int par = 0;
   auto spmv = [&](const double* src, int i) {
     double a = 0.0;
+    if constexpr (E == 0) {
+      for (int k = Srp[i]; k < Srp[i + 1]; ++k) a = __dadd_rn(a, __dmul_rn(Sv[k], src[Sci[k]]));
+    } else {
 #pragma unroll
-    for (int k = 0; k < E; ++k) a = __dadd_rn(a, __dmul_rn(ev[static_cast<i64>(k) * n + i], src[ec[static_cast<i64>(k) * n + i]]));
+      for (int k = 0; k < E; ++k)
+        a = __dadd_rn(a, __dmul_rn(ev[static_cast<i64>(k) * n + i], src[ec[static_cast<i64>(k) * n + i]]));
+    }
     return a;
   };
   double R[RPT], AP[RPT];
@@ -747,30 +768,45 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
   }
 }
 
-// Runs pcg_smem_k when it applies (3 n fp64 within a CTA's shared memory,
-// rows of <= 16 entries, n <= 20 x 512); returns false otherwise.
+// Runs pcg_smem_k when it applies: 3 n fp64 within a CTA's shared memory,
+// n <= 20 x 512, and the matrix either staged in shared memory too (CSR) or
+// read as ELL (rows of <= 16 entries).  Returns false otherwise.
 template <int RPT>
-bool pcg_smem_rpt(Ctx* c, int E, const double* ev, const int* ec, const double* inv, const double* B, double* X,
-                  i64 n, i64 nb, double tol, i64 max_iter, ColState* st) {
-  const size_t smem = static_cast<size_t>(3 * n) * sizeof(double);
+void pcg_smem_rpt(Ctx* c, int E, size_t smem, const double* ev, const int* ec, const i64* crp, const double* inv,
+                  const double* B, double* X, i64 n, i64 nb, double tol, i64 max_iter, ColState* st) {
   auto launch = [&](auto k) {
     ensure_smem(k, smem);
     KScope ks_(c, "pcg_persistent");
-    k<<<static_cast<unsigned>(nb), kPcgSmemThreads, smem, c->stream>>>(static_cast<int>(n), nb, ev, ec, inv, B, X, tol,
-                                                                      max_iter, st);
+    k<<<static_cast<unsigned>(nb), kPcgSmemThreads, smem, c->stream>>>(static_cast<int>(n), nb, ev, ec, crp, inv, B, X,
+                                                                      tol, max_iter, st);
     launched(c);
   };
-  if (E <= 9)
+  if (E == 0)
+    launch(pcg_smem_k<RPT, 0>);
+  else if (E <= 9)
     launch(pcg_smem_k<RPT, 9>);
   else
     launch(pcg_smem_k<RPT, 16>);
-  return true;
 }
 
 bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb, double tol,
               i64 max_iter, ColState* st) {
-  const size_t smem = static_cast<size_t>(3 * n) * sizeof(double) + 2 * 3 * 16 * sizeof(double);
-  if (n <= 0 || n > 20 * kPcgSmemThreads || smem > 227 * 1024 || A->nnz == 0) return false;
+  constexpr size_t kMax = 227 * 1024 - 2 * 3 * 16 * sizeof(double);
+  const size_t vec = static_cast<size_t>(3 * n) * sizeof(double);
+  if (n <= 0 || n > 20 * kPcgSmemThreads || vec > kMax || A->nnz == 0) return false;
+  const size_t csr = static_cast<size_t>(A->nnz) * 12 + static_cast<size_t>(n + 1) * 4 + 16;
+  const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
+  auto run = [&](int E, size_t smem, const double* ev, const int* ec, const i64* crp) {
+    if (rpt <= 4) return pcg_smem_rpt<4>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 8) return pcg_smem_rpt<8>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 12) return pcg_smem_rpt<12>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 16) return pcg_smem_rpt<16>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    return pcg_smem_rpt<20>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+  };
+  if (vec + csr <= kMax && A->nnz < (i64{1} << 30)) {  // the whole operator in shared memory
+    run(0, vec + csr, A->v, A->ci, A->rp);
+    return true;
+  }
   // longest row (E): one small reduction on the host copy of the row pointers
   std::vector<i64> rp(static_cast<size_t>(n) + 1);
   CUDA_OK(cudaMemcpyAsync(rp.data(), A->rp, sizeof(i64) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
@@ -783,12 +819,8 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   DevBuf<int> ec(c, static_cast<size_t>(Ep) * n);
   csr_to_ell_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ev.p, ec.p);
   launched(c);
-  const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
-  if (rpt <= 4) return pcg_smem_rpt<4>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
-  if (rpt <= 8) return pcg_smem_rpt<8>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
-  if (rpt <= 12) return pcg_smem_rpt<12>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
-  if (rpt <= 16) return pcg_smem_rpt<16>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
-  return pcg_smem_rpt<20>(c, Ep, ev.p, ec.p, inv, B, X, n, nb, tol, max_iter, st);
+  run(Ep, vec, ev.p, ec.p, nullptr);
+  return true;
 }
 
 struct PcgBatchOut {
