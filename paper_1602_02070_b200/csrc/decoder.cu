@@ -63,6 +63,8 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
   DevBuf<CgState> st(c, 1);
   st.zero(c);
   const unsigned nbv = stride_blocks(c, std::max<i64>(N, 1));
+  // the CG vector kernels: one wave of 8 x 256 threads per SM (4 vectors in flight per thread)
+  const unsigned nbw = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(c->num_sms * 8, (N + 1023) / 1024)));
   size_t nparts = std::max<size_t>({static_cast<size_t>(nbv), lr_blocks(apK), lr_blocks(apR)});
   DevBuf<double> part(c, std::max<size_t>(nparts, 1));
   cg_init_k<TK, TX, TX><<<nbv, kBlock, 0, c->stream>>>(p, n, 0, pl, Xt, X, R.p, P.p, part.p, st.p);
@@ -91,7 +93,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
       {
         KScope ks_(c, "cg_residual");
         if (vecK)
-          cg_residual_k<TK, true><<<nbv, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+          cg_residual_k<TK, true><<<nbw, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
         else
           cg_residual_k<TK, false><<<nbv, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
         launched(c);
@@ -99,7 +101,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
       {
         KScope ks_(c, "cg_update");
         if (vecU)
-          cg_update_k<TK, TX, true><<<nbv, kBlock, 0, c->stream>>>(N, X, P.p, R.p, st.p);
+          cg_update_k<TK, TX, true><<<nbw, kBlock, 0, c->stream>>>(N, X, P.p, R.p, st.p);
         else
           cg_update_k<TK, TX, false><<<nbv, kBlock, 0, c->stream>>>(N, X, P.p, R.p, st.p);
         launched(c);

@@ -1007,7 +1007,26 @@ __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ 
     const i64 nv = N / W;
     V* Rv = reinterpret_cast<V*>(R);
     const V* Av = reinterpret_cast<const V*>(AP);
-    for (i64 q = t0; q < nv; q += ts) {
+    i64 q = t0;
+    for (; q + 3 * ts < nv; q += 4 * ts) {  // four 16-byte pairs in flight per thread
+      V r[4], a[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        r[u] = Rv[q + u * ts];
+        a[u] = Av[q + u * ts];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          TK& x = lane_of<TK>(r[u], k);
+          x = sub_rn(x, mul_rn(alpha, reinterpret_cast<const TK*>(&a[u])[k]));
+          s[0] += static_cast<double>(x) * static_cast<double>(x);
+        }
+        Rv[q + u * ts] = r[u];
+      }
+    }
+    for (; q < nv; q += ts) {
       V r = Rv[q];
       const V a = Av[q];
 #pragma unroll
@@ -1045,15 +1064,33 @@ __global__ void cg_update_k(i64 N, TX* __restrict__ X, TK* __restrict__ P, const
     V* Xv = reinterpret_cast<V*>(X);
     V* Pv = reinterpret_cast<V*>(P);
     const V* Rv = reinterpret_cast<const V*>(R);
-    for (i64 q = t0; q < nv; q += ts) {
-      V x = Xv[q], pv = Pv[q];
-      const V r = Rv[q];
-      V pn;
+    auto one = [&](V& x, const V& pv, const V& r, V& pn) {
 #pragma unroll
       for (int k = 0; k < W; ++k) {
-        lane_of<TK>(x, k) = add_rn(lane_of<TK>(x, k), mul_rn(alpha, lane_of<TK>(pv, k)));
-        lane_of<TK>(pn, k) = add_rn(reinterpret_cast<const TK*>(&r)[k], mul_rn(beta, lane_of<TK>(pv, k)));
+        lane_of<TK>(x, k) = add_rn(lane_of<TK>(x, k), mul_rn(alpha, reinterpret_cast<const TK*>(&pv)[k]));
+        lane_of<TK>(pn, k) = add_rn(reinterpret_cast<const TK*>(&r)[k], mul_rn(beta, reinterpret_cast<const TK*>(&pv)[k]));
       }
+    };
+    i64 q = t0;
+    for (; q + 3 * ts < nv; q += 4 * ts) {  // four 16-byte triples in flight per thread
+      V x[4], pv[4], r[4], pn[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x[u] = Xv[q + u * ts];
+        pv[u] = Pv[q + u * ts];
+        r[u] = Rv[q + u * ts];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        one(x[u], pv[u], r[u], pn[u]);
+        Xv[q + u * ts] = x[u];
+        Pv[q + u * ts] = pn[u];
+      }
+    }
+    for (; q < nv; q += ts) {
+      V x = Xv[q], pv = Pv[q], pn;
+      const V r = Rv[q];
+      one(x, pv, r, pn);
       Xv[q] = x;
       Pv[q] = pn;
     }
