@@ -84,6 +84,9 @@ int cpcag_ctx_synchronize(cpcag_ctx ctx);
  * passes, 2 = fused whenever its shared-memory slice fits, 3 = slab whenever
  * it applies. */
 int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path);
+/* Test hook: the persistent FISTA kernel's tile GEMM, 0 = automatic (fp64
+ * tensor cores, DMMA, when the tiling fits), 1 = SIMT fp64 multiply-adds. */
+int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path);
 /* The path (1, 2 or 3 as above) the most recently planned decoder operator
  * took; 0 before any. */
 int cpcag_ctx_last_apply_path(cpcag_ctx ctx);

@@ -174,6 +174,10 @@ class Context:
         """Decoder operator path: "auto", "split" (two passes), "fused" or "slab"."""
         N.check(N.lib().cpcag_ctx_set_apply_path(self.handle, {"auto": 0, "split": 1, "fused": 2, "slab": 3}[path]))
 
+    def set_fista_path(self, path: str):
+        """Persistent FISTA tile GEMM: "auto" (DMMA tensor cores) or "simt" (tests)."""
+        N.check(N.lib().cpcag_ctx_set_fista_path(self.handle, {"auto": 0, "simt": 1}[path]))
+
     def last_apply_path(self) -> str:
         """The path the most recently planned decoder operator took."""
         return {0: "none", 1: "split", 2: "fused", 3: "slab"}[N.lib().cpcag_ctx_last_apply_path(self.handle)]

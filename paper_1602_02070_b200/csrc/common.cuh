@@ -84,6 +84,7 @@ struct Ctx {
   std::string timing_filter;  // comma-separated tags; empty = all
   int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused, 3 slab (tests)
   int last_apply_path = 0;    // the path the last planned operator took (1, 2 or 3; tests)
+  int fista_simt = 0;         // 1: the persistent FISTA kernel's SIMT tile GEMM instead of DMMA (tests)
   cudaStream_t side = nullptr;  // second stream for independent work (lazily created)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   KernelTimes kt;

@@ -942,6 +942,13 @@ int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path) {
   });
 }
 
+int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path) {
+  return guard([&] {
+    if (path < 0 || path > 1) invalid("fista path must be 0 or 1");
+    as_ctx(ctx)->fista_simt = path;
+  });
+}
+
 int cpcag_ctx_last_apply_path(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->last_apply_path : -1; }
 
 int cpcag_ctx_synchronize(cpcag_ctx ctx) {

@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "fista_persist.cuh"
@@ -44,6 +45,7 @@ namespace {
 constexpr int kPT = 256;      // threads per CTA
 constexpr int kMaxGrid = 160;      // CTAs (one per SM)
 constexpr int kPsm = 4 * kMaxGrid;  // doubles of the partial-sum staging area
+constexpr int kNst1 = 4;            // MODE 1 ring stages (A and S chunks)
 
 template <typename T>
 struct PersistArgs {
@@ -51,12 +53,12 @@ struct PersistArgs {
   int TM, TN, C, KS, KC;
   int ldA, ldB;  // shared-memory row strides of the k-major A (TM) and B (TN) panels
   int use_r, use_c, loss;
-  int dbg;  // diagnostics (CPCAG_FISTA_PERSIST_DBG): 1 = no B chunk loads, 2 = no chunk FMAs
   T step;
   double tol;
   i64 max_iter;
   double gamma_r, gamma_c;
   const T* Dr;  // rr x rr dense, exactly symmetric
+  const T* Drs;  // MODE 1: g_r L~_r k-major with ldS rows per k (A panels streamed from it), padding rows 0
   const T* Dc;  // rc x rc dense, exactly symmetric
   const T* Y;   // rr x rc column-major
   T* Sg[2];     // S_j column-major, ldS rows (padding rows stay 0)
@@ -84,7 +86,6 @@ __device__ __forceinline__ unsigned long long gtimer_ns() {
   return t;
 }
 
-__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
 // four consecutive values (16-byte aligned) of either precision
 __device__ __forceinline__ void ld4v(const float* p, float (&v)[4]) {
@@ -127,48 +128,84 @@ __device__ __forceinline__ void strip_gemm(double (&acc)[4][4], const T* ap, int
   }
 }
 
-// acc[x 8 + y] += a[x] b[y] for one k (8-float strips of A and B).
-__device__ __forceinline__ void fma88(float (&acc)[64], const float* ap, const float* bp) {
-  const float4 a0 = lds4(ap), a1 = lds4(ap + 4), b0 = lds4(bp), b1 = lds4(bp + 4);
-  const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-  const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-  for (int x = 0; x < 8; ++x)
-#pragma unroll
-    for (int y = 0; y < 8; ++y) acc[x * 8 + y] = fmaf(av[x], bv[y], acc[x * 8 + y]);
+// fp64 tensor-core multiply-add (DMMA): D(8 x 8) += A(8 x 4) B(4 x 8), lane
+// (g, t) = (lane / 4, lane % 4) supplies A(g, t) and B(t, g) and holds
+// D(g, 2t), D(g, 2t + 1) (layout checked against a scalar product in
+// tools/micro/dmma_peak.cu; 37 TFLOP/s measured vs 34 for DFMA).
+__device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
 }
 
-// Sum of the 64 partial entries over the 32 lanes, scattered: after five
-// halving rounds (partner lane ^ 16, 8, 4, 2, 1; the lane with the bit set
-// keeps the upper half) lane l holds entries 2 l and 2 l + 1 in acc[0..1].
-// The summation tree is fixed, so the result is deterministic.
-__device__ __forceinline__ void reduce_scatter64(float (&acc)[64], int lane) {
-#pragma unroll
-  for (int r = 0; r < 5; ++r) {
-    const int o = 16 >> r, half = 32 >> r;
-    const bool up = (lane & o) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float send = up ? acc[i] : acc[i + half];
-      const float keep = up ? acc[i + half] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
+// Swizzled k-major panel index for MODE 1: row k, column i.  Columns are
+// XOR-ed by multiples of 8 elements per k (4 k-rows for fp32, 2 for fp64), so
+// a DMMA operand load (8 columns x 4 k-rows) hits distinct banks; 16-byte
+// groups stay contiguous (cp.async copies keep working).
+template <typename T>
+__device__ __forceinline__ int swz(int k, int i, int ld) {
+  constexpr int W = sizeof(T) == 4 ? 3 : 1;
+  return k * ld + (i ^ ((k & W) << 3));
+}
+
+// MODE 1 k-loop: acc (a 16 x 16 block at (m0, n0) as 2 x 2 DMMA tiles) +=
+// A(m0.., k) B(k, n0..) for the k4 steps q = s, s + KS, ... < nk4 (k-split
+// s).  A and B are shared byte addresses of swizzled k-major panels whose rows
+// past the data are zero up to a multiple of 4, so the loop needs no bounds:
+// lane (g, t) reads row 4 q + t, whose swizzle (t << 3) is loop-invariant.
+template <typename T>
+__device__ __forceinline__ T lds_t(unsigned a) {
+  if constexpr (sizeof(T) == 4) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+  } else {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
   }
 }
 
-// MODE 0: 4 x 4 micro-tiles, the k range split across thread groups (KS),
-//         partial tiles summed through shared memory.
-// MODE 1: 8 x 8 micro-tiles, one warp per micro-tile with the k range split
-//         across its lanes, lanes reduced by a fixed shuffle reduce-scatter
-//         (twice the multiply-adds per shared-memory wavefront of MODE 0).
+template <typename T>
+__device__ __forceinline__ void dmma_block(double (&acc)[2][2][2], unsigned A, int lda, unsigned B, int ldb, int nk4,
+                                           int m0, int n0, int s, int KS, int lane) {
+  constexpr unsigned E = sizeof(T);
+  const int g = lane >> 2, t = lane & 3;
+  const int sw = (t & (E == 4 ? 3 : 1)) << 3;
+  const int k = 4 * s + t;
+  unsigned a0 = A + static_cast<unsigned>(k * lda + ((m0 + g) ^ sw)) * E;
+  unsigned a1 = A + static_cast<unsigned>(k * lda + ((m0 + 8 + g) ^ sw)) * E;
+  unsigned b0 = B + static_cast<unsigned>(k * ldb + ((n0 + g) ^ sw)) * E;
+  unsigned b1 = B + static_cast<unsigned>(k * ldb + ((n0 + 8 + g) ^ sw)) * E;
+  const unsigned da = static_cast<unsigned>(4 * KS * lda) * E, db = static_cast<unsigned>(4 * KS * ldb) * E;
+#pragma unroll 2
+  for (int q = s; q < nk4; q += KS) {
+    const double x0 = static_cast<double>(lds_t<T>(a0)), x1 = static_cast<double>(lds_t<T>(a1));
+    const double y0 = static_cast<double>(lds_t<T>(b0)), y1 = static_cast<double>(lds_t<T>(b1));
+    dmma884(acc[0][0], x0, y0);
+    dmma884(acc[0][1], x0, y1);
+    dmma884(acc[1][0], x1, y0);
+    dmma884(acc[1][1], x1, y1);
+    a0 += da;
+    a1 += da;
+    b0 += db;
+    b1 += db;
+  }
+}
+
+// MODE 0: 4 x 4 SIMT micro-tiles (fp64 DFMA on widened operands), the k range
+//         split across thread groups (KS), partial tiles summed through shared
+//         memory.
+// MODE 1: fp64 tensor cores (DMMA m8n8k4): one warp per 16 x 16 block and
+//         k-split s, operands widened once per load, k-major panels swizzled
+//         (swz); partial tiles summed through shared memory as MODE 0.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(const PersistArgs<T> a) {
-  static_assert(MODE == 0 || sizeof(T) == 4, "MODE 1 is fp32 only");
   constexpr int EPC = 16 / static_cast<int>(sizeof(T));  // values per 16-byte cp.async
   const int kPT = blockDim.x;
   // stages of the S-panel ring (MODE 0: 2 x 128-row chunks measured 16.1 us
   // per iteration vs 19.2 us for 4 x 64)
-  constexpr int NST = MODE == 0 ? 2 : 4;
+  constexpr int NST = MODE == 0 ? 2 : kNst1;
   extern __shared__ __align__(16) double smd[];
   double* psm = smd;  // [kPsm] partial sums of the previous iteration (4 per CTA)
   double* red = smd + kPsm;  // [KS][TE] split-k partial tiles (fp64; MODE 1: KS = 1)
@@ -180,11 +217,14 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   const int r0 = rb * TM, c0 = cb * TN;
   const int rn = min(TM, rr - r0), cn = min(TN, rc - c0);
   const int ldA = a.ldA, ldB = a.ldB;
-  T* As = sm;                                      // [rr][ldA]  g_r L~_r(r0 + i, k)
-  T* Bc = As + static_cast<size_t>(rr) * ldA;      // [rc][ldB]  g_c L~_c(k, c0 + j)
-  T* A2 = Bc + static_cast<size_t>(rc) * ldB;      // [rc][ldA]  S(r0 + i, k)
-  T* Bb = A2 + static_cast<size_t>(rc) * ldA;      // [2][KC][ldB]  S(k, c0 + j)
-  T* Yt = Bb + NST * static_cast<size_t>(KC) * ldB;  // tile state, e = i + TM j
+  // MODE 0 keeps g_r L~_r resident (As); MODE 1 streams it chunk by chunk (Ab)
+  T* As = sm;                                                        // [rr][ldA]  g_r L~_r(r0 + i, k)
+  T* Bc = As + (MODE == 0 ? static_cast<size_t>(rr) * ldA : 0);      // [rc4][ldB]  g_c L~_c(k, c0 + j)
+  const int rc4 = (rc + 3) / 4 * 4;                                  // MODE 1: zero rows up to a multiple of 4
+  T* A2 = Bc + static_cast<size_t>(rc4) * ldB;                       // [rc4][ldA]  S(r0 + i, k)
+  T* Bb = A2 + static_cast<size_t>(rc4) * ldA;                       // [NST][KC][ldB]  S(k, c0 + j)
+  T* Ab = Bb + NST * static_cast<size_t>(KC) * ldB;                  // MODE 1: [NST][KC][ldA]  g_r L~_r(r0 + i, k)
+  T* Yt = Ab + (MODE == 1 ? NST * static_cast<size_t>(KC) * ldA : 0);  // tile state, e = i + TM j
   T* Zt = Yt + TE;                                // Z_j
   T* HZ = Zt + TE;                                // H(Z_j)
   T* Sp = HZ + TE;                                // S_{j-1}
@@ -192,18 +232,25 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   T* Sc = Hp + TE;                                // S_j
 
   // ---- one-time staging of the pre-scaled operators and the tile of Y
-  if (a.use_r)
+  auto pidx = [&](int k, int i, int ld) { return MODE == 1 ? swz<T>(k, i, ld) : k * ld + i; };
+  auto sh = [](const T* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); };
+  if (MODE == 0 && a.use_r)
     for (int t = tid; t < rr * TM; t += kPT) {
       const int k = t / TM, i = t - k * TM;
       // L~_r(r0 + i, k) from the column-major dense copy (contiguous in i)
-      As[k * ldA + i] = i < rn ? static_cast<T>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr]))
-                     : T(0);
+      As[pidx(k, i, ldA)] =
+          i < rn ? static_cast<T>(a.gamma_r * static_cast<double>(a.Dr[(r0 + i) + static_cast<i64>(k) * rr])) : T(0);
     }
+  for (int t = tid; t < (rc4 - rc) * (TM > TN ? TM : TN); t += kPT) {  // padding rows of A2 and Bc
+    const int k = rc + t / (TM > TN ? TM : TN), i = t % (TM > TN ? TM : TN);
+    if (i < TM) A2[k * ldA + i] = T(0);
+    if (i < TN) Bc[k * ldB + i] = T(0);
+  }
   if (a.use_c)
     for (int t = tid; t < rc * TN; t += kPT) {
       const int k = t / TN, j = t - k * TN;
-      Bc[k * ldB + j] = j < cn ? static_cast<T>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc]))
-                     : T(0);
+      Bc[pidx(k, j, ldB)] =
+          j < cn ? static_cast<T>(a.gamma_c * static_cast<double>(a.Dc[(c0 + j) + static_cast<i64>(k) * rc])) : T(0);
     }
   for (int e = tid; e < TE; e += kPT) {
     const int j = e / TM, i = e - j * TM;
@@ -223,63 +270,83 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   const int nmi = TM / 4, NMT = nmi * (TN / 4);
   const bool gthr = tid < NMT * KS;
   const int mt = tid % NMT, s = tid / NMT, mi = mt % nmi, ni = mt / nmi;
-  const int mi8 = warp % max(TM / 8, 1), ni8 = warp / max(TM / 8, 1);
-  const bool w8 = MODE == 1 && warp < (TM / 8) * (TN / 8);
+  // MODE 1: warp -> (16 x 16 block, k-split)
+  const int nbm = TM / 16, nblk = nbm * (TN / 16);
+  const bool wd = MODE == 1 && warp < nblk * KS;
+  const int wb = warp % max(nblk, 1), ws = warp / max(nblk, 1);
+  const int m16 = 16 * (wb % max(nbm, 1)), n16 = 16 * (wb / max(nbm, 1));
   auto tile_gemm = [&](const T* Sbuf, const T* SbufT) {
     double acc[4][4];
-    float acc8[MODE == 1 ? 64 : 1];
+    double accd[2][2][2];
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
 #pragma unroll
-    for (int q = 0; q < (MODE == 1 ? 64 : 1); ++q) acc8[q] = 0.f;
-    const int q4m = TM / EPC, q4n = TN / EPC;
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y) accd[x][y][0] = accd[x][y][1] = 0.0;
+    const int q4m = TM / EPC;
     if (a.use_c)  // S(r0.., k) for every k: TM contiguous floats per column k
       for (int t = tid; t < rc * q4m; t += kPT) {
         const int k = t / q4m, q = t - k * q4m;
-        cp_async16(A2 + k * ldA + EPC * q, Sbuf + (r0 + EPC * q) + static_cast<i64>(k) * a.ldS);
+        cp_async16(A2 + pidx(k, EPC * q, ldA), Sbuf + (r0 + EPC * q) + static_cast<i64>(k) * a.ldS);
       }
     cp_async_commit();  // group 0: A2 (and the caller's partial sums)
     const int nch = a.use_r ? (rr + KC - 1) / KC : 0;
+    const int q4n = TN / EPC;
     auto issue_chunk = [&](int ch) {
       const int k0 = ch * KC, kl = min(KC, rr - k0);
       T* dst = Bb + (ch % NST) * KC * ldB;
       for (int t = tid; t < kl * q4n; t += kPT) {
         const int k = t / q4n, q = t - k * q4n;
-        cp_async16(dst + k * ldB + EPC * q, SbufT + (c0 + EPC * q) + static_cast<i64>(k0 + k) * a.ldT);
+        cp_async16(dst + pidx(k, EPC * q, ldB), SbufT + (c0 + EPC * q) + static_cast<i64>(k0 + k) * a.ldT);
+      }
+      if constexpr (MODE == 1) {
+        T* dsa = Ab + (ch % NST) * KC * ldA;
+        for (int t = tid; t < kl * q4m; t += kPT) {
+          const int k = t / q4m, q = t - k * q4m;
+          cp_async16(dsa + pidx(k, EPC * q, ldA), a.Drs + (r0 + EPC * q) + static_cast<i64>(k0 + k) * a.ldS);
+        }
+        const int kl4 = (kl + 3) / 4 * 4;  // rows past the data up to a multiple of 4: zeros
+        for (int t = tid; t < (kl4 - kl) * (TM > TN ? TM : TN); t += kPT) {
+          const int k = kl + t / (TM > TN ? TM : TN), i = t % (TM > TN ? TM : TN);
+          if (i < TM) dsa[k * ldA + i] = T(0);
+          if (i < TN) dst[k * ldB + i] = T(0);
+        }
       }
     };
-    // NST-stage ring: chunks 0 .. NST-2 in flight before the first one is used
+    // NST-stage ring: chunks 0 .. NST-2 in flight before the first one is used;
+    // one CTA barrier per chunk: after it, every warp is done with chunk
+    // ch - 1, whose slot the chunk issued next (ch + NST - 1) reuses
 #pragma unroll
     for (int q = 0; q < NST - 1; ++q) {
-      if (q < nch && !(a.dbg & 1)) issue_chunk(q);
+      if (q < nch) issue_chunk(q);
       cp_async_commit();
     }
     for (int ch = 0; ch < nch; ++ch) {
-      if (ch + NST - 1 < nch && !(a.dbg & 1)) issue_chunk(ch + NST - 1);
-      cp_async_commit();
-      cp_async_wait<NST - 1>();  // A2 and chunk ch have landed
+      cp_async_wait<NST - 2>();  // A2 and chunk ch have landed
       __syncthreads();
+      if (ch + NST - 1 < nch) issue_chunk(ch + NST - 1);
+      cp_async_commit();
       if constexpr (MODE == 0) {
-        if (gthr && !(a.dbg & 2)) {
+        if (gthr) {
           const int k0 = ch * KC, kl = min(KC, rr - k0);
           const int cnt = s < kl ? (kl - 1 - s) / KS + 1 : 0;
           strip_gemm(acc, As + static_cast<size_t>(k0 + s) * ldA + 4 * mi, KS * ldA,
                      Bb + (ch % NST) * KC * ldB + s * ldB + 4 * ni, KS * ldB, cnt);
         }
       } else {
-        if (w8) {
+        if (wd) {
           if (ch == 0 && a.use_c)  // the resident S L~_c part overlaps the chunks in flight
-            for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
+            dmma_block<T>(accd, sh(A2), ldA, sh(Bc), ldB, rc4 / 4, m16, n16, ws, KS, lane);
           const int k0 = ch * KC, kl = min(KC, rr - k0);
-          const float* ab = As + static_cast<size_t>(k0) * ldA + 8 * mi8;
-          const float* bb = Bb + (ch % NST) * KC * ldB + 8 * ni8;
-          for (int k = lane; k < kl; k += 32) fma88(acc8, ab + k * ldA, bb + k * ldB);
+          dmma_block<T>(accd, sh(Ab + (ch % NST) * KC * ldA), ldA, sh(Bb + (ch % NST) * KC * ldB), ldB, (kl + 3) / 4,
+                        m16, n16, ws, KS, lane);
         }
       }
-      __syncthreads();
     }
+    __syncthreads();
     if (nch == 0) {
       cp_async_wait<0>();
       __syncthreads();
@@ -297,14 +364,16 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
           for (int y = 0; y < 4; ++y) o[(4 * mi + x) + TM * (4 * ni + y)] = acc[x][y];
       }
     } else {
-      if (w8) {
-        if (a.use_c && nch == 0)
-          for (int k = lane; k < rc; k += 32) fma88(acc8, A2 + k * ldA + 8 * mi8, Bc + k * ldB + 8 * ni8);
-        reduce_scatter64(acc8, lane);  // lane now holds entries 2 lane, 2 lane + 1 of the micro-tile
-        const int x = lane >> 2, y = (2 * lane) & 7;
-        double* o = red + (8 * mi8 + x) + TM * (8 * ni8 + y);
-        o[0] = acc8[0];
-        o[TM] = acc8[1];
+      if (wd) {
+        if (a.use_c && nch == 0) dmma_block<T>(accd, sh(A2), ldA, sh(Bc), ldB, rc4 / 4, m16, n16, ws, KS, lane);
+        const int g = lane >> 2, t = lane & 3;
+        double* o = red + static_cast<size_t>(ws) * TE;
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < 2; ++y)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) o[(m16 + 8 * x + g) + TM * (n16 + 8 * y + 2 * t + q)] = accd[x][y][q];
       }
     }
     __syncthreads();
@@ -459,54 +528,67 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
   }
 }
 
+// Drs[k ldS + i] = g_r Dr(i, k) rounded to T (the value MODE 0 stages), 0 for i >= rr.
+template <typename T>
+__global__ void scale_panel_k(i64 rr, i64 ldS, double g, const T* __restrict__ Dr, T* __restrict__ Drs) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= ldS) return;
+  for (i64 k = blockIdx.y; k < rr; k += gridDim.y)
+    Drs[k * ldS + i] = i < rr ? static_cast<T>(g * static_cast<double>(Dr[i + k * rr])) : T(0);
+}
+
 struct Geom {
   int mode, TM, TN, R, C, KS, KC, ldA, ldB, threads;
   size_t smem;
 };
 
-size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst, size_t w = 4) {
+size_t geom_smem(i64 rr, i64 rc, int TM, int TN, int ldA, int ldB, int KS, int KC, int nst, size_t w = 4,
+                 int mode = 0) {
   const size_t TE = static_cast<size_t>(TM) * TN;
+  const size_t rc4 = static_cast<size_t>((rc + 3) / 4 * 4);
+  const size_t a_panel = mode == 0 ? static_cast<size_t>(rr) * ldA : static_cast<size_t>(nst) * KC * ldA;
   return 8 * kPsm + 8 * static_cast<size_t>(KS) * TE +
-         w * (static_cast<size_t>(rr) * ldA + static_cast<size_t>(rc) * ldB + static_cast<size_t>(rc) * ldA +
-              static_cast<size_t>(nst) * KC * ldB + 6 * TE);
+         w * (a_panel + rc4 * ldB + rc4 * ldA + static_cast<size_t>(nst) * KC * ldB + 6 * TE);
 }
 
-// MODE 1 (preferred): TM, TN multiples of 8, one warp per 8 x 8 micro-tile
-// (at most 16 warps), k-major panels padded by 4 floats so that lanes at
-// different k hit distinct 16-byte bank groups; minimises the per-scheduler
-// multiply-add work max(warps, 4) (rr + rc) within the shared-memory budget.
-bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out) {
+// MODE 1 (DMMA): TM a multiple of 32 (fp32; 16 for fp64) and TN of 32 (16),
+// so the swizzled panels stay in range; one warp per 16 x 16 block and
+// k-split (at most 16 warps).  The tensor pipe is shared per SM, so the
+// per-CTA time follows TM TN (rr + rc): take the smallest tile area the SM
+// count allows, then the most k-splits (latency hiding) and the longest S
+// chunks the shared memory holds.
+bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out, size_t w) {
+  const i64 mq = w == 4 ? 32 : 16, nq = w == 4 ? 32 : 16;
   bool found = false;
   double best = 0.0;
   const i64 sms = c->num_sms;
-  const int fix_m = 0, fix_n = 0;
-  for (i64 TM = 8; TM <= std::max<i64>(8, (rr + 7) / 8 * 8); TM += 8)
-    for (i64 TN = 8; TN <= std::max<i64>(8, (rc + 7) / 8 * 8); TN += 8) {
+  for (i64 TM = mq; TM <= std::max<i64>(mq, (rr + mq - 1) / mq * mq); TM += mq)
+    for (i64 TN = nq; TN <= std::max<i64>(nq, (rc + nq - 1) / nq * nq); TN += nq) {
       const i64 R = (rr + TM - 1) / TM, C = (rc + TN - 1) / TN;
-      const i64 warps = (TM / 8) * (TN / 8);
-      if (R * C > sms || warps > 16) continue;
-      if (fix_m && (TM != fix_m || TN != fix_n)) continue;
-      const int ldA = static_cast<int>(TM + 4), ldB = static_cast<int>(TN + 4);
-      int KC = 64;
-      size_t sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), ldA, ldB, 1, KC, 4);
-      if (sm > budget) {
-        KC = 32;
-        sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), ldA, ldB, 1, KC, 4);
-      }
-      if (sm > budget) continue;
-      // per-scheduler multiply-add work, plus the exposed latency of the S
-      // panel ring: each of the ceil(rr / KC) chunks must cover ~1 us of L2
-      // latency spread over the 3 chunks in flight (measured: a 8 x 104 tile
-      // with 2 k-steps per lane per chunk ran latency-bound)
-      const double work = static_cast<double>(std::max<i64>(warps, 4)) * static_cast<double>(rr + rc) * 64.0 / 4.0;
-      const double chunk_work = static_cast<double>(std::max<i64>(warps, 4)) * KC * 64.0 / 4.0 / 32.0;
-      const double cost = work + static_cast<double>((rr + KC - 1) / KC) * std::max(0.0, 700.0 - chunk_work) +
-                          1e-3 * static_cast<double>(sm);
-      if (!found || cost < best) {
-        found = true;
-        best = cost;
-        *out = Geom{1, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), 1, KC,
-                    ldA, ldB, static_cast<int>(std::max<i64>(warps, 4) * 32), sm};
+      if (R * C > sms) continue;
+      const i64 blocks = (TM / 16) * (TN / 16);
+      if (blocks > 16) continue;
+      for (int KS = static_cast<int>(std::min<i64>(4, 16 / blocks)); KS >= 1; KS /= 2) {
+        int KC = 0;
+        size_t sm = 0;
+        for (int kc : {128, 64, 32}) {
+          sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM), static_cast<int>(TN),
+                         KS, kc, kNst1, w, 1);
+          if (sm <= budget) {
+            KC = kc;
+            break;
+          }
+        }
+        if (!KC) continue;
+        const double cost = static_cast<double>(TM * TN) * static_cast<double>(rr + rc) * (1.0 + 0.25 / KS) +
+                            64.0 * static_cast<double>(rr) / KC;
+        if (!found || cost < best) {
+          found = true;
+          best = cost;
+          *out = Geom{1, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(R), static_cast<int>(C), KS, KC,
+                      static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(blocks * KS * 32), sm};
+        }
+        break;  // the most k-splits that fit
       }
     }
   return found;
@@ -568,22 +650,16 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
   CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
   const size_t budget = static_cast<size_t>(optin) > 4096 ? static_cast<size_t>(optin) - 4096 : 0;
   Geom g;
-  // MODE 0 (wide row panels); the MODE 1 micro-tile variant measured no
-  // faster at config 1 (16.6 vs 16.1 us per tile GEMM) and is not selected.
-  const bool want1 = false;
-  if (!(want1 && plan_mode1(c, rr, rc, budget, &g)) && !plan_mode0(c, rr, rc, budget, &g, sizeof(T))) return false;
-  const void* kfn;
-  if constexpr (sizeof(T) == 4) {
-    kfn = g.mode == 1 ? reinterpret_cast<const void*>(fista_persist_k<T, 1>)
-                      : reinterpret_cast<const void*>(fista_persist_k<T, 0>);
-    if (g.mode == 1)
-      ensure_smem(fista_persist_k<T, 1>, g.smem);
-    else
-      ensure_smem(fista_persist_k<T, 0>, g.smem);
-  } else {
-    kfn = reinterpret_cast<const void*>(fista_persist_k<T, 0>);
+  // MODE 1 (fp64 tensor cores) when its tiling fits, else MODE 0 (SIMT DFMA)
+  const bool simt = c->fista_simt != 0;  // test hook: force the SIMT tile GEMM
+  if (!(!simt && plan_mode1(c, rr, rc, budget, &g, sizeof(T))) && !plan_mode0(c, rr, rc, budget, &g, sizeof(T)))
+    return false;
+  const void* kfn = g.mode == 1 ? reinterpret_cast<const void*>(fista_persist_k<T, 1>)
+                                : reinterpret_cast<const void*>(fista_persist_k<T, 0>);
+  if (g.mode == 1)
+    ensure_smem(fista_persist_k<T, 1>, g.smem);
+  else
     ensure_smem(fista_persist_k<T, 0>, g.smem);
-  }
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, g.threads, g.smem));
   const i64 grid = static_cast<i64>(g.R) * g.C;
@@ -591,6 +667,12 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
 
   const i64 ldS = static_cast<i64>(g.R) * g.TM, ldT = static_cast<i64>(g.C) * g.TN;
   const size_t sz = static_cast<size_t>(ldS * ldT);
+  DevBuf<T> drs(c, g.mode == 1 ? static_cast<size_t>(rr) * ldS : 1);
+  if (g.mode == 1 && cfg.gamma_r != 0.0) {
+    dim3 gs(static_cast<unsigned>((ldS + 255) / 256), static_cast<unsigned>(std::min<i64>(rr, 65535)));
+    scale_panel_k<T><<<gs, 256, 0, c->stream>>>(rr, ldS, cfg.gamma_r, Dr, drs.p);
+    launched(c);
+  }
   DevBuf<T> sbuf(c, 4 * sz);
   sbuf.zero(c);
   DevBuf<double> part(c, 2 * 4 * static_cast<size_t>(grid));
@@ -619,6 +701,7 @@ bool fista_persist_run(Ctx* c, const T* Y, i64 rr, i64 rc, const T* Dr, const T*
   a.gamma_r = cfg.gamma_r;
   a.gamma_c = cfg.gamma_c;
   a.Dr = Dr;
+  a.Drs = drs.p;
   a.Dc = Dc;
   a.Y = Y;
   a.Sg[0] = sbuf.p;

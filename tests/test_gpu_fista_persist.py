@@ -26,6 +26,15 @@ def ctx(P):
     return P.Context(0)
 
 
+@pytest.fixture(params=["auto", "simt"])
+def gemm(request, ctx):
+    """Both tile GEMMs of the persistent kernel: fp64 tensor cores (DMMA,
+    the default) and SIMT DFMA."""
+    ctx.set_fista_path(request.param)
+    yield request.param
+    ctx.set_fista_path("auto")
+
+
 def _reduced(p, n, rr, rc, seed):
     Lr_full, Lc_full = knn_laplacian(p, 3, 10, seed), knn_laplacian(n, 3, 10, seed + 1)
     plan = O.draw_plan(p, n, rr, rc, seed=seed)
@@ -48,7 +57,7 @@ def _run(P, ctx, Y, Lr, Lc, gr, gc, loss, tol, its, timed=True):
     ((200, 160, 50, 40), 0.0, 5.0, "l2"),     # row term off, l2 prox
     ((160, 120, 9, 7), 2.0, 2.0, "l1"),       # tiny, single tile
 ])
-def test_persistent_fista_matches_oracle(P, ctx, shape, gr, gc, loss):
+def test_persistent_fista_matches_oracle(P, ctx, shape, gr, gc, loss, gemm):
     p, n, rr, rc = shape
     Lr, Lc = _reduced(p, n, rr, rc, 40 + rr)
     Y = np.random.default_rng(rr).standard_normal((rr, rc)) * 4.0
@@ -115,3 +124,30 @@ def test_persistent_fista_divergence_error(P, ctx):
     cfg = P.FrpcagConfig(gamma_r=1.0, gamma_c=1.0, step=10.0, tol=1e-300, max_iter=30)
     with pytest.raises(RuntimeError, match=r"diverged \(non-finite objective at iteration \d+\); step too large"):
         P.fista_solve(Y, to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+
+
+@pytest.mark.parametrize("prec", [np.float32, np.float64])
+def test_persistent_fista_tensor_core_gemm_matches_simt(P, ctx, prec):
+    """DMMA and SIMT tile GEMMs both accumulate H = g L~ S in fp64 from the
+    same operands; only the summation order differs (fp64 rounding), so the
+    solves agree far inside the fp32 bar, and fp64 runs stay within the
+    fp64 parity bar of each other and of the oracle (1e-9)."""
+    Lr, Lc = _reduced(400, 300, 101, 60, 21)
+    Y = (np.random.default_rng(8).standard_normal((101, 60)) * 4.0).astype(prec)
+    cfg = P.FrpcagConfig(gamma_r=3.0, gamma_c=3.0, tol=1e-300, max_iter=120)
+    out = {}
+    try:
+        for path in ("auto", "simt"):
+            ctx.set_fista_path(path)
+            out[path] = P.fista_solve(Y, to_device(ctx, Lr), to_device(ctx, Lc), cfg, ctx=ctx)
+    finally:
+        ctx.set_fista_path("auto")
+    (Xd, trd), (Xs, trs) = out["auto"], out["simt"]
+    assert Xd.dtype == prec
+    Xo, tro = O.fista_solve(Y.astype(np.float64), Lr, Lc, O.FrpcagConfig(3.0, 3.0, "l1", 1e-300, 120))
+    if prec == np.float64:
+        assert rel(Xd, Xs) <= 1e-12
+        assert rel(Xd, Xo) <= 1e-9
+    else:
+        assert rel(Xd, Xs) <= 1e-5
+        assert rel(Xd, Xo) <= 1e-4
