@@ -418,7 +418,6 @@ struct PowerState {
   double est;
   i64 iterations;
   unsigned bar_count, bar_gen;
-  int prof;  // CPCAG_POWER_PROF: CTA 0 prints its phase times
 };
 
 __device__ __forceinline__ double warp_row_dot(i64 k0, i64 k1, const int* __restrict__ ci,
@@ -525,16 +524,6 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   const double* vsrc = v_in_smem ? vs : v0;
   double est = 0.0;
   i64 it = 0;
-  unsigned long long pt[4] = {0, 0, 0, 0}, tq = 0;  // CTA 0 phase timers (CPCAG_POWER_PROF)
-  auto mark = [&](int ph) {
-    if (st->prof && blockIdx.x == 0 && threadIdx.x == 0) {
-      unsigned long long now;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
-      if (ph >= 0) pt[ph] += now - tq;
-      tq = now;
-    }
-  };
-  mark(-1);
   for (; it < max_iter; ++it) {
     double* w = wbuf + (it & 1) * n;
     for (i64 r = r0 + wid; r < r1; r += nw) {
@@ -547,9 +536,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       acc = warp_sum(acc);
       if (lane == 0) w[r] = acc;
     }
-    mark(0);
     grid_barrier(&st->bar_count, &st->bar_gen);
-    mark(1);
     // ||w||^2 straight from w, which every CTA reads anyway: one L2 round
     // trip per iteration instead of two (partials, then w).  Same data and
     // the same fixed-order block reduction in every CTA, so every CTA gets
@@ -561,7 +548,6 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       t[0] += x * x;
     }
     block_sum<1>(t);
-    mark(2);
     const double nrm = sqrt(t[0]);
     if (nrm == 0.0) {
       est = 0.0;
@@ -578,17 +564,12 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       double* vg = v0;
       for (i64 i = r0 + threadIdx.x; i < r1; i += blockDim.x) vg[i] = __ddiv_rn(__ldcg(w + i), nrm);
     }
-    mark(3);
     if (it > 0 && fabs(est - prev) <= tol * est) {
       ++it;
       break;
     }
     if (!v_in_smem) grid_barrier(&st->bar_count, &st->bar_gen);
   }
-  if (st->prof && blockIdx.x == 0 && threadIdx.x == 0)
-    printf("[power_iter] grid %d n %lld its %lld: spmv %.1f barrier %.1f read+norm %.1f scale %.1f us\n", gridDim.x,
-           static_cast<long long>(n), static_cast<long long>(it), pt[0] * 1e-3, pt[1] * 1e-3, pt[2] * 1e-3,
-           pt[3] * 1e-3);
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->est = est;
     st->iterations = it;

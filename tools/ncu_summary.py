@@ -9,9 +9,9 @@ import subprocess
 import sys
 
 TAGS = {
-    "cg_apply": "cg_apply", "cg_residual": "cg_residual", "cg_update": "cg_update",
-    "fista_splitk_partial": "fista_objective", "pcg_persistent": "pcg_persistent",
-    "cg_apply_band": "cg_apply_band", "cg_apply_col": "cg_apply_col",
+    "slab_k": "cg_apply", "fused_k": "cg_apply", "cg_residual": "cg_residual", "cg_update": "cg_update",
+    "lc_k": "cg_apply_lc", "lc_smem_k": "cg_apply_lc", "lr_reg_k": "cg_apply_lr",
+    "pcg_smem_k": "pcg_persistent", "pcg_persistent": "pcg_persistent",
     "knn_tile": "knn_tile", "knn_tc_filter": "knn_tc_filter", "power_iter": "power_iter",
     "fista_persist": "fista_persist",
 }
