@@ -354,6 +354,150 @@ cpcag_spectral_gap spectral_gap_host(const double* evals, i64 order, i64 k) {
 }
 
 // eigs.cpp:59-64.
+// ---------------------------------------------------------------- rank job
+// The pipeline's detected rank (pipeline.cpp:319-321): singular values of the
+// compressed solution Xt = sqrt of the eigenvalues of its Gram matrix.  The
+// eigenvalues come from a parallel cyclic Jacobi in ONE CTA (the Gram matrix
+// of config 1 is 100 x 100: 80 KB in shared memory), so the whole job runs
+// on the side stream beside the decoder and the host reads the result after
+// the decode; no library solver on the timed path.
+constexpr int kJacobiThreads = 1024;
+
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_eigvals_k(int n, const double* __restrict__ G,
+                                                                    double* __restrict__ lam, int max_sweeps) {
+  extern __shared__ double A[];  // m x m, m = n rounded up to even (padding index: zero row/column)
+  const int m = n + (n & 1);
+  double* cs = A + static_cast<size_t>(m) * m;  // [m/2][2] rotation (c, s) per pair
+  int* pr = reinterpret_cast<int*>(cs + m);      // [m] pair members of the current step
+  __shared__ double red[2][32];
+  __shared__ int stop;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const int i = e % m, j = e / m;
+    A[e] = (i < n && j < n) ? G[i + static_cast<i64>(j) * n] : 0.0;
+  }
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  const int half = m / 2, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    // convergence: off-diagonal vs diagonal Frobenius norms (fixed-order sums)
+    double off = 0.0, dia = 0.0;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = e % m, j = e / m;
+      const double x = A[e];
+      if (i == j)
+        dia += x * x;
+      else
+        off += x * x;
+    }
+    off = warp_sum(off);
+    dia = warp_sum(dia);
+    if (lane == 0) {
+      red[0][wid] = off;
+      red[1][wid] = dia;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double o = 0.0, d = 0.0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) o += red[0][w], d += red[1][w];
+      stop = !(o > 1e-30 * d) || o == 0.0;
+    }
+    __syncthreads();
+    if (stop) break;
+    for (int step = 0; step < m - 1; ++step) {
+      // round-robin pairing: index 0 fixed, the others rotate
+      for (int k = threadIdx.x; k < half; k += blockDim.x) {
+        const int a = k == 0 ? 0 : 1 + (k - 1 + step) % (m - 1);
+        const int b = 1 + (m - 2 - k + step) % (m - 1);
+        const int p = a < b ? a : b, q = a < b ? b : a;
+        pr[2 * k] = p;
+        pr[2 * k + 1] = q;
+        const double apq = A[p + q * m], app = A[p + p * m], aqq = A[q + q * m];
+        double c = 1.0, s = 0.0;
+        if (apq != 0.0) {
+          const double th = (aqq - app) / (2.0 * apq);
+          const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+          c = 1.0 / sqrt(t * t + 1.0);
+          s = t * c;
+        }
+        cs[2 * k] = c;
+        cs[2 * k + 1] = s;
+      }
+      __syncthreads();
+      // rows p, q <- rotated (disjoint across pairs)
+      for (int e = threadIdx.x; e < half * m; e += blockDim.x) {
+        const int k = e / m, col = e % m;
+        const int p = pr[2 * k], q = pr[2 * k + 1];
+        const double c = cs[2 * k], s = cs[2 * k + 1];
+        const double xp = A[p + col * m], xq = A[q + col * m];
+        A[p + col * m] = c * xp - s * xq;
+        A[q + col * m] = s * xp + c * xq;
+      }
+      __syncthreads();
+      // columns p, q <- rotated
+      for (int e = threadIdx.x; e < half * m; e += blockDim.x) {
+        const int k = e / m, row = e % m;
+        const int p = pr[2 * k], q = pr[2 * k + 1];
+        const double c = cs[2 * k], s = cs[2 * k + 1];
+        const double xp = A[row + p * m], xq = A[row + q * m];
+        A[row + p * m] = c * xp - s * xq;
+        A[row + q * m] = s * xp + c * xq;
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lam[i] = A[i + i * m];
+}
+
+void rank_job_start(Ctx* c, RankJob& job, const double* Xt64, i64 m, i64 n, cudaStream_t s) {
+  job.q = std::min(m, n);
+  if (job.q == 0) return;
+  if (job.q > 110) invalid("rank job: Gram order above 110");
+  const bool tall = m >= n;
+  job.G.alloc(c, job.q * job.q);
+  job.lam.alloc(c, job.q);
+  job.flag.alloc(c, 1);
+  job.flag.zero(c);
+  if (!job.host) CUDA_OK(cudaMallocHost(&job.host, sizeof(double) * 128));
+  CUDA_OK(cudaEventRecord(c->fork_ev, c->stream));
+  CUDA_OK(cudaStreamWaitEvent(s, c->fork_ev, 0));
+  nonfinite_k<<<stride_blocks(c, m * n), kBlock, 0, s>>>(m * n, Xt64, job.flag.p);
+  launched(c);
+  gram_k<<<dim3(blocks_for(job.q), static_cast<unsigned>(job.q)), kBlock, 0, s>>>(m, n, tall, Xt64, job.G.p);
+  launched(c);
+  const int mm = static_cast<int>(job.q + (job.q & 1));
+  const size_t smem = sizeof(double) * (static_cast<size_t>(mm) * mm + mm) + sizeof(int) * mm;
+  ensure_smem(jacobi_eigvals_k, smem);
+  jacobi_eigvals_k<<<1, kJacobiThreads, smem, s>>>(static_cast<int>(job.q), job.G.p, job.lam.p, 60);
+  launched(c);
+  CUDA_OK(cudaMemcpyAsync(job.host, job.lam.p, sizeof(double) * job.q, cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaMemcpyAsync(reinterpret_cast<int*>(reinterpret_cast<double*>(job.host) + 120), job.flag.p, sizeof(int),
+                          cudaMemcpyDeviceToHost, s));
+  CUDA_OK(cudaEventRecord(c->join_ev, s));
+  job.side = s;
+  job.running = true;
+}
+
+// Joins the job (the main stream waits for the side stream) and returns the
+// singular values, descending.
+std::vector<double> rank_job_finish(Ctx* c, RankJob& job) {
+  std::vector<double> sv;
+  if (!job.running) return sv;
+  CUDA_OK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+  CUDA_OK(cudaEventSynchronize(c->join_ev));
+  job.running = false;
+  const double* h = reinterpret_cast<const double*>(job.host);
+  if (*reinterpret_cast<const int*>(h + 120)) invalid("thin_svd: non-finite input");
+  sv.resize(static_cast<size_t>(job.q));
+  for (i64 i = 0; i < job.q; ++i) sv[i] = std::sqrt(std::max(h[i], 0.0));
+  std::sort(sv.begin(), sv.end(), [](double a, double b) { return a > b; });
+  return sv;
+}
+
+RankJob::~RankJob() {
+  if (running && side) cudaStreamSynchronize(side);  // an exception left the job in flight
+  if (host) cudaFreeHost(host);
+}
+
 i64 detect_rank_host(const std::vector<double>& s, double thr) {
   if (s.empty() || !(s[0] > 0.0)) return 0;
   i64 k = 0;

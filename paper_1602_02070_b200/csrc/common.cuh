@@ -420,6 +420,19 @@ struct HostRng {
 
 // Internal entry points shared between translation units.
 double power_norm(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_iter);
+// Singular values of a small fp64 matrix (Gram + one-CTA Jacobi) on stream s,
+// read back by rank_job_finish (approx.cu).
+struct RankJob {
+  DevBuf<double> G, lam;
+  DevBuf<int> flag;
+  void* host = nullptr;  // pinned: eigenvalues [0, 110), non-finite flag at double index 120
+  i64 q = 0;
+  bool running = false;
+  cudaStream_t side = nullptr;
+  ~RankJob();
+};
+void rank_job_start(Ctx* c, RankJob& job, const double* Xt64, i64 m, i64 n, cudaStream_t s);
+std::vector<double> rank_job_finish(Ctx* c, RankJob& job);
 void power_norm_pair(Ctx* c, Csr* A1, Csr* A2, double tol, uint64_t seed, i64 max_iter, double* out1,
                      double* out2);
 // kmeans / decode_labels on the device (cluster.cu).

@@ -122,16 +122,29 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
 
   // pipeline.cpp:319-320: the detected rank of the compressed solution (its
   // singular values only), outside the stage timers as in the reference.
+  // Gram matrices of order <= 110 (config 1: 100) go through the one-CTA
+  // Jacobi job on the side stream; when nothing downstream needs the rank
+  // (alternate decoder, both spectral gaps given, no clustering) the job runs
+  // beside the decoder and is read after it.
   trace_mark(c, "pipeline: stages to solve");
-  {
-    const i64 q = std::min(rho_r, rho_c);
-    DevBuf<double> A(c, std::max<i64>(rho_r * rho_c, 1)), sv(c, std::max<i64>(q, 1));
+  const i64 q_rank = std::min(rho_r, rho_c);
+  DevBuf<double> A_rank(c, std::max<i64>(rho_r * rho_c, 1));
+  RankJob rank_job;
+  const bool rank_small = q_rank > 0 && q_rank <= 110;
+  const bool rank_later = rank_small && cfg.decoder_variant == CPCAG_DECODER_ALTERNATE && cfg.lambda_k1_r > 0.0 &&
+                          cfg.lambda_k1_c > 0.0 && cfg.task == CPCAG_TASK_LOWRANK;
+  if (rank_small) {
+    to_f64_device(c, Xt_out, rho_r * rho_c, A_rank.p);
+    rank_job_start(c, rank_job, A_rank.p, rho_r, rho_c, side_stream(c));
+    if (!rank_later) rep->detected_rank = detect_rank_host(rank_job_finish(c, rank_job), cfg.approx.rank_threshold);
+  } else {
+    DevBuf<double> sv(c, std::max<i64>(q_rank, 1));
     if (rho_r * rho_c) {
-      to_f64_device(c, Xt_out, rho_r * rho_c, A.p);
-      gram_svd_device(c, A.p, rho_r, rho_c, 0, sv.p, nullptr, nullptr);
+      to_f64_device(c, Xt_out, rho_r * rho_c, A_rank.p);
+      gram_svd_device(c, A_rank.p, rho_r, rho_c, 0, sv.p, nullptr, nullptr);
     }
-    std::vector<double> hs(static_cast<size_t>(q));
-    if (q) CUDA_OK(cudaMemcpyAsync(hs.data(), sv.p, sizeof(double) * q, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> hs(static_cast<size_t>(q_rank));
+    if (q_rank) CUDA_OK(cudaMemcpyAsync(hs.data(), sv.p, sizeof(double) * q_rank, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     rep->detected_rank = detect_rank_host(hs, cfg.approx.rank_threshold);
   }
@@ -216,6 +229,7 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
       rep->n_clusters = k;
     });
   }
+  if (rank_later) rep->detected_rank = detect_rank_host(rank_job_finish(c, rank_job), cfg.approx.rank_threshold);
   if (om_r_out) std::copy(om_r.begin(), om_r.end(), om_r_out);
   if (om_c_out) std::copy(om_c.begin(), om_c.end(), om_c_out);
 }

@@ -335,6 +335,35 @@ def test_pipeline_approx_decoder_matches_oracle(P, ctx):
     assert rel(rep.factors.U, dec.U) <= 1e-6 and np.allclose(rep.factors.sigma, dec.sigma, rtol=1e-7)
 
 
+@pytest.mark.parametrize("a,b", [(4, 4), (2, 2)])
+def test_pipeline_detected_rank_beside_the_decoder(P, ctx, a, b):
+    """With the alternate decoder, both spectral gaps given and no clustering,
+    the detected rank (pipeline.cpp:319-321) runs on the side stream beside
+    the decode (Gram + one-CTA Jacobi eigenvalues when min(rho_r, rho_c) <=
+    110; a = b = 2 gives 30 x 40, a = b = 4 gives 15 x 20) and must equal the
+    oracle's SVD-based rank."""
+    from paper_1602_02070_b200.workloads import config0
+
+    Y, _ = config0(seed=1602, small=True)
+    p, n = Y.shape
+    g = math.sqrt(max(p, n))
+    cfg = P.PipelineConfig(knn=10, a=a, b=b, frpcag=P.FrpcagConfig(gamma_r=g, gamma_c=g, tol=1e-300, max_iter=60),
+                           decoder=P.DecoderConfig(pcg_tol=1e-10, pcg_max_iter=300, variant="alternate",
+                                                   rank_threshold=0.05),
+                           lambda_k1_r=0.05, lambda_k1_c=0.07, seed=1602)
+    rep = P.run_pipeline(Y, cfg, ctx=ctx)
+    gr = O.build_knn_graph(Y, True, 10)
+    gc = O.build_knn_graph(Y, False, 10)
+    plan = O.draw_plan(p, n, -(-p // b), -(-n // a), seed=1602)
+    Lr_t = O.kron_reduce(gr.laplacian, plan.omega_r, 1e-11)
+    Lc_t = O.kron_reduce(gc.laplacian, plan.omega_c, 1e-11)
+    Xt, _ = O.fista_solve(O.subsample(Y, plan), Lr_t, Lc_t, O.FrpcagConfig(g, g, "l1", 1e-300, 60))
+    sv = O.thin_svd(Xt)[1]
+    assert rep.detected_rank == O.detect_rank(sv, 0.05)
+    dec = O.alternate_decode(Xt, plan, gr.laplacian, gc.laplacian, 0.05, 0.07, 1.0, 1e-10, 300)
+    assert rel(rep.X, dec.X) <= 1e-8
+
+
 def test_pipeline_stage_error_is_tagged(P, ctx):
     Y = np.random.default_rng(0).standard_normal((20, 30))
     cfg = P.PipelineConfig(knn=50, a=2, b=2)
