@@ -45,7 +45,7 @@ namespace {
 constexpr int kPT = 256;      // threads per CTA
 constexpr int kMaxGrid = 160;      // CTAs (one per SM)
 constexpr int kPsm = 4 * kMaxGrid;  // doubles of the partial-sum staging area
-constexpr int kNst1 = 4;            // MODE 1 ring stages (A and S chunks)
+constexpr int kNst1 = 2;            // MODE 1 ring stages (A and S chunks)
 
 template <typename T>
 struct PersistArgs {
@@ -571,7 +571,7 @@ bool plan_mode1(Ctx* c, i64 rr, i64 rc, size_t budget, Geom* out, size_t w) {
       for (int KS = static_cast<int>(std::min<i64>(4, 16 / blocks)); KS >= 1; KS /= 2) {
         int KC = 0;
         size_t sm = 0;
-        for (int kc : {128, 64, 32}) {
+        for (int kc : {256, 128, 64, 32}) {
           sm = geom_smem(rr, rc, static_cast<int>(TM), static_cast<int>(TN), static_cast<int>(TM), static_cast<int>(TN),
                          KS, kc, kNst1, w, 1);
           if (sm <= budget) {
