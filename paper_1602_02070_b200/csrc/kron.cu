@@ -959,29 +959,61 @@ __global__ void schur_update_k(i64 m, i64 ni, i64 nb, const i64* __restrict__ co
 }
 
 // Symmetrise (0.5 (S + S^T)) and prune (v != 0 and |v| > tol) row by row.
-__global__ void sym_count_k(i64 m, const double* __restrict__ S, double prune, bool symmetrize, i64* cnt) {
-  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  i64 k = 0;
-  for (i64 j = 0; j < m; ++j) {
-    const double x = symmetrize ? __dmul_rn(0.5, __dadd_rn(S[i + j * m], S[j + i * m])) : S[i + j * m];
-    k += (x != 0.0 && fabs(x) > prune);
+// Row-contiguous copy of the dense result: T[j + i m] = x(i, j), x = 0.5 (S(i, j) +
+// S(j, i)) (symmetrize; commutative, so T is exactly symmetric) or S(i, j),
+// through 32 x 32 shared-memory tiles so both reads and the write coalesce.
+// Rows [r0, r1) only (T row-local), so large m works in blocks.
+__global__ void row_major_k(i64 m, i64 r0, i64 r1, const double* __restrict__ S, bool symmetrize,
+                            double* __restrict__ T) {
+  __shared__ double a[32][33], b[32][33];
+  const i64 bi = r0 + static_cast<i64>(blockIdx.x) * 32, bj = static_cast<i64>(blockIdx.y) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  for (int r = ty; r < 32; r += 8) {
+    const i64 i = bi + tx, j = bj + r;  // S(i, j), i contiguous
+    a[r][tx] = (i < r1 && j < m) ? S[i + j * m] : 0.0;
+    const i64 i2 = bj + tx, j2 = bi + r;  // S(j, i) as (row bj + tx, column bi + r)
+    b[r][tx] = (i2 < m && j2 < r1) ? S[i2 + j2 * m] : 0.0;
   }
-  cnt[i] = k;
+  __syncthreads();
+  // write T[j + i m] for i = bi + r, j = bj + tx: x(i, j) = S(i, j) [= a[tx][r]] (+ S(j, i) [= b[r][tx]])
+  for (int r = ty; r < 32; r += 8) {
+    const i64 i = bi + r, j = bj + tx;
+    if (i < r1 && j < m) T[j + (i - r0) * m] = symmetrize ? __dmul_rn(0.5, __dadd_rn(a[tx][r], b[r][tx])) : a[tx][r];
+  }
 }
 
-__global__ void sym_fill_k(i64 m, const double* __restrict__ S, double prune, bool symmetrize,
+// Warp per row over the row-contiguous copy: counts, then compacted (column,
+// value) pairs in increasing column order (ballot prefix).
+__global__ void row_count_k(i64 m, i64 r0, i64 r1, const double* __restrict__ T, double prune, i64* cnt) {
+  const i64 il = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, i = r0 + il;
+  const int lane = threadIdx.x & 31;
+  if (i >= r1) return;
+  i64 k = 0;
+  for (i64 j0 = 0; j0 < m; j0 += 32) {
+    const i64 j = j0 + lane;
+    const double x = j < m ? T[j + il * m] : 0.0;
+    k += __popc(__ballot_sync(0xffffffffu, x != 0.0 && fabs(x) > prune));
+  }
+  if (lane == 0) cnt[i] = k;
+}
+
+__global__ void row_fill_k(i64 m, i64 r0, i64 r1, const double* __restrict__ T, double prune,
                            const i64* __restrict__ rp, int* __restrict__ ci, double* __restrict__ v) {
-  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
-  if (i >= m) return;
+  const i64 il = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5, i = r0 + il;
+  const int lane = threadIdx.x & 31;
+  if (i >= r1) return;
   i64 o = rp[i];
-  for (i64 j = 0; j < m; ++j) {
-    const double x = symmetrize ? __dmul_rn(0.5, __dadd_rn(S[i + j * m], S[j + i * m])) : S[i + j * m];
-    if (x != 0.0 && fabs(x) > prune) {
-      ci[o] = static_cast<int>(j);
-      v[o] = x;
-      ++o;
+  for (i64 j0 = 0; j0 < m; j0 += 32) {
+    const i64 j = j0 + lane;
+    const double x = j < m ? T[j + il * m] : 0.0;
+    const bool keep = x != 0.0 && fabs(x) > prune;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const i64 at = o + __popc(bal & ((1u << lane) - 1u));
+      ci[at] = static_cast<int>(j);
+      v[at] = x;
     }
+    o += __popc(bal);
   }
 }
 
@@ -1004,8 +1036,19 @@ i64 scan_counts(Ctx* c, const i64* cnt, i64 rows, i64* rp) {
 Csr* dense_to_csr(Ctx* c, const double* S, i64 m, double prune, bool symmetrize) {
   DevBuf<i64> cnt(c, std::max<i64>(m, 1));
   Csr* out = csr_alloc(c, m, m, 0);
-  if (m) {
-    sym_count_k<<<blocks_for(m, 128), 128, 0, c->stream>>>(m, S, prune, symmetrize, cnt.p);
+  // row blocks of the row-contiguous copy, <= 256 MB each
+  const i64 rb = std::max<i64>(32, std::min<i64>(m, ((i64{32} << 20) / std::max<i64>(m, 1)) / 32 * 32));
+  DevBuf<double> T(c, std::max<i64>(std::min(rb, m) * m, 1));
+  auto to_rows = [&](i64 r0, i64 r1) {
+    row_major_k<<<dim3(static_cast<unsigned>((r1 - r0 + 31) / 32), static_cast<unsigned>((m + 31) / 32)), 256, 0,
+                  c->stream>>>(m, r0, r1, S, symmetrize, T.p);
+    launched(c);
+  };
+  for (i64 r0 = 0; r0 < m; r0 += rb) {
+    const i64 r1 = std::min(m, r0 + rb);
+    to_rows(r0, r1);
+    row_count_k<<<static_cast<unsigned>(((r1 - r0) * 32 + 255) / 256), 256, 0, c->stream>>>(m, r0, r1, T.p, prune,
+                                                                                           cnt.p);
     launched(c);
   }
   const i64 nnz = scan_counts(c, cnt.p, m, out->rp);
@@ -1013,8 +1056,13 @@ Csr* dense_to_csr(Ctx* c, const double* S, i64 m, double prune, bool symmetrize)
   if (nnz) {
     out->ci = static_cast<int*>(csr_malloc(c, sizeof(int) * nnz));
     out->v = static_cast<double*>(csr_malloc(c, sizeof(double) * nnz));
-    sym_fill_k<<<blocks_for(m, 128), 128, 0, c->stream>>>(m, S, prune, symmetrize, out->rp, out->ci, out->v);
-    launched(c);
+    for (i64 r0 = 0; r0 < m; r0 += rb) {
+      const i64 r1 = std::min(m, r0 + rb);
+      if (rb < m) to_rows(r0, r1);  // one block: the copy from the counting pass is still there
+      row_fill_k<<<static_cast<unsigned>(((r1 - r0) * 32 + 255) / 256), 256, 0, c->stream>>>(m, r0, r1, T.p, prune,
+                                                                                            out->rp, out->ci, out->v);
+      launched(c);
+    }
   }
   return out;
 }
