@@ -50,24 +50,28 @@ __global__ void gather_points_k(const T* __restrict__ X, i64 x_rows, i64 n, i64 
 // points; each 32-wide k slab is loaded coalesced (one point row per load)
 // and transposed through shared memory so lane r accumulates point r's slab
 // in k order.
-__global__ void __launch_bounds__(32) sqnorm_k(const double* __restrict__ Pm, i64 n, i64 d,
-                                               double* __restrict__ sq) {
-  // one thread per point, its row streamed with 8 loads in flight; the sum
-  // runs over k in order with separate rounding (the canonical g_ii)
-  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) sqnorm_k(const double* __restrict__ Pm, i64 n, i64 d,
+                                                double* __restrict__ sq) {
+  // one warp per point: 32-value chunks of its row read coalesced one chunk
+  // ahead, the sum over k in order with separate rounding (the canonical
+  // g_ii) run redundantly by every lane on shuffled values
+  const i64 i = (blockIdx.x * (i64)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= n) return;
   const double* r = Pm + i * d;
   double s = 0.0;
-  i64 k = 0;
-  for (; k + 8 <= d; k += 8) {
-    double x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = r[k + u];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(x[u], x[u]));
+  double cur = lane < d ? r[lane] : 0.0;
+  for (i64 k0 = 0; k0 < d; k0 += 32) {
+    const double nxt = k0 + 32 + lane < d ? r[k0 + 32 + lane] : 0.0;
+    const int cnt = static_cast<int>(min(static_cast<i64>(32), d - k0));
+#pragma unroll 8
+    for (int u = 0; u < cnt; ++u) {
+      const double x = __shfl_sync(0xffffffffu, cur, u);
+      s = __dadd_rn(s, __dmul_rn(x, x));
+    }
+    cur = nxt;
   }
-  for (; k < d; ++k) s = __dadd_rn(s, __dmul_rn(r[k], r[k]));
-  sq[i] = s;
+  if (lane == 0) sq[i] = s;
 }
 
 __device__ __forceinline__ bool lex_less(double da, int ja, double db, int jb) {
@@ -599,7 +603,7 @@ void knn_lists(Ctx* c, const T* X, i64 x_rows, i64 x_cols, bool axis_rows, i64 K
   } else {
     out->Pm.zero(c);
   }
-  sqnorm_k<<<static_cast<unsigned>((n + 31) / 32), 32, 0, c->stream>>>(out->Pm.p, n, d, sq.p);
+  sqnorm_k<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, c->stream>>>(out->Pm.p, n, d, sq.p);
   launched(c);
   out->nbr.alloc(c, n * K);
   out->d2.alloc(c, n * K);
