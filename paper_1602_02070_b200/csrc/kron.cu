@@ -624,12 +624,29 @@ __global__ void csr_to_ell_k(i64 n, int E, const i64* __restrict__ rp, const int
   }
 }
 
+// Packed ELL when every value is exact in fp32: one 8-byte word per entry
+// (fp32 value bits, column), two thirds of the bytes of (fp64, int32); the
+// flag reports a value that fp32 cannot hold.
+__global__ void csr_to_ell_packed_k(i64 n, int E, const i64* __restrict__ rp, const int* __restrict__ ci,
+                                    const double* __restrict__ v, uint2* __restrict__ ep, int* flag) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const i64 k0 = rp[i], d = rp[i + 1] - k0;
+  for (int k = 0; k < E; ++k) {
+    const double x = k < d ? v[k0 + k] : 0.0;
+    const float f = static_cast<float>(x);
+    if (static_cast<double>(f) != x) *flag = 1;
+    ep[k * n + i] = make_uint2(__float_as_uint(f), static_cast<unsigned>(k < d ? ci[k0 + k] : static_cast<int>(i)));
+  }
+}
+
 constexpr int kPcgSmemThreads = 512;
 
 // E > 0: the matrix as ELL with E entries a row, read from global memory;
 // E == 0: the CSR (rp, ci, v of nnz entries) staged in shared memory after
 // the three vectors (small interiors, e.g. config 1's 900-node column graph).
-template <int RPT, int E>
+// PK: the ELL packed as (fp32 value, column) words (ev is then a uint2 array).
+template <int RPT, int E, bool PK = false>
 __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, const double* __restrict__ ev,
                                                                  const int* __restrict__ ec,
                                                                  const i64* __restrict__ crp,
@@ -666,6 +683,13 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
     double a = 0.0;
     if constexpr (E == 0) {
       for (int k = Srp[i]; k < Srp[i + 1]; ++k) a = __dadd_rn(a, __dmul_rn(Sv[k], src[Sci[k]]));
+    } else if constexpr (PK) {
+      const uint2* ep = reinterpret_cast<const uint2*>(ev);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const uint2 w = ep[static_cast<i64>(k) * n + i];
+        a = __dadd_rn(a, __dmul_rn(static_cast<double>(__uint_as_float(w.x)), src[w.y]));
+      }
     } else {
 #pragma unroll
       for (int k = 0; k < E; ++k)
@@ -772,8 +796,9 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
 // n <= 20 x 512, and the matrix either staged in shared memory too (CSR) or
 // read as ELL (rows of <= 16 entries).  Returns false otherwise.
 template <int RPT>
-void pcg_smem_rpt(Ctx* c, int E, size_t smem, const double* ev, const int* ec, const i64* crp, const double* inv,
-                  const double* B, double* X, i64 n, i64 nb, double tol, i64 max_iter, ColState* st) {
+void pcg_smem_rpt(Ctx* c, int E, bool packed, size_t smem, const double* ev, const int* ec, const i64* crp,
+                  const double* inv, const double* B, double* X, i64 n, i64 nb, double tol, i64 max_iter,
+                  ColState* st) {
   auto launch = [&](auto k) {
     ensure_smem(k, smem);
     KScope ks_(c, "pcg_persistent");
@@ -784,9 +809,9 @@ void pcg_smem_rpt(Ctx* c, int E, size_t smem, const double* ev, const int* ec, c
   if (E == 0)
     launch(pcg_smem_k<RPT, 0>);
   else if (E <= 9)
-    launch(pcg_smem_k<RPT, 9>);
+    packed ? launch(pcg_smem_k<RPT, 9, true>) : launch(pcg_smem_k<RPT, 9>);
   else
-    launch(pcg_smem_k<RPT, 16>);
+    packed ? launch(pcg_smem_k<RPT, 16, true>) : launch(pcg_smem_k<RPT, 16>);
 }
 
 bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb, double tol,
@@ -796,15 +821,15 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   if (n <= 0 || n > 20 * kPcgSmemThreads || vec > kMax || A->nnz == 0) return false;
   const size_t csr = static_cast<size_t>(A->nnz) * 12 + static_cast<size_t>(n + 1) * 4 + 16;
   const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
-  auto run = [&](int E, size_t smem, const double* ev, const int* ec, const i64* crp) {
-    if (rpt <= 4) return pcg_smem_rpt<4>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 8) return pcg_smem_rpt<8>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 12) return pcg_smem_rpt<12>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 16) return pcg_smem_rpt<16>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    return pcg_smem_rpt<20>(c, E, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+  auto run = [&](int E, bool pk, size_t smem, const double* ev, const int* ec, const i64* crp) {
+    if (rpt <= 4) return pcg_smem_rpt<4>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 8) return pcg_smem_rpt<8>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 12) return pcg_smem_rpt<12>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 16) return pcg_smem_rpt<16>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    return pcg_smem_rpt<20>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
   };
   if (vec + csr <= kMax && A->nnz < (i64{1} << 30)) {  // the whole operator in shared memory
-    run(0, vec + csr, A->v, A->ci, A->rp);
+    run(0, false, vec + csr, A->v, A->ci, A->rp);
     return true;
   }
   // longest row (E): one small reduction on the host copy of the row pointers
@@ -815,11 +840,22 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   for (i64 i = 0; i < n; ++i) E = std::max(E, rp[i + 1] - rp[i]);
   if (E > 16) return false;
   const int Ep = E <= 9 ? 9 : 16;
+  // packed (fp32 value, column) words when every value is exact in fp32
+  // (unit-weight grids: the interior's values are small integers)
+  DevBuf<uint2> ep(c, static_cast<size_t>(Ep) * n);
+  DevBuf<int> flag(c, 1);
+  flag.zero(c);
+  csr_to_ell_packed_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ep.p, flag.p);
+  launched(c);
+  if (!read_back(c, flag.p)) {
+    run(Ep, true, vec, reinterpret_cast<const double*>(ep.p), nullptr, nullptr);
+    return true;
+  }
   DevBuf<double> ev(c, static_cast<size_t>(Ep) * n);
   DevBuf<int> ec(c, static_cast<size_t>(Ep) * n);
   csr_to_ell_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ev.p, ec.p);
   launched(c);
-  run(Ep, vec, ev.p, ec.p, nullptr);
+  run(Ep, false, vec, ev.p, ec.p, nullptr);
   return true;
 }
 

@@ -230,27 +230,34 @@ def test_kron_grid_graph(P, ctx):
     assert np.abs(R.to_dense() - Ro.to_dense()).max() <= 1e-9 * np.abs(Ro.to_dense()).max()
 
 
-def _stencil_laplacian(h, w, offsets):
-    ti, tj = [], []
+def _stencil_laplacian(h, w, offsets, weighted=False):
+    ti, tj, tv = [], [], []
+    rs = np.random.default_rng(h * w)
     for r in range(h):
         for c in range(w):
             for dr, dc in offsets:
                 r2, c2 = r + dr, c + dc
                 if 0 <= r2 < h and 0 <= c2 < w:
                     a, b = r * w + c, r2 * w + c2
+                    x = float(rs.uniform(0.5, 2.0)) if weighted else 1.0
                     ti += [a, b]
                     tj += [b, a]
-    return O.graph_from_adjacency(O.Csr.from_triplets(h * w, h * w, ti, tj, [1.0] * len(ti))).laplacian
+                    tv += [x, x]
+    return O.graph_from_adjacency(O.Csr.from_triplets(h * w, h * w, ti, tj, tv)).laplacian
 
 
-@pytest.mark.parametrize("shape,offsets,keep", [
-    ((41, 37), [(0, 1), (1, -1), (1, 0), (1, 1)], 150),                    # rows of <= 9 entries
-    ((33, 29), [(0, 1), (0, 2), (1, -1), (1, 0), (1, 1), (2, 0)], 90),     # rows of <= 13 entries
+@pytest.mark.parametrize("shape,offsets,keep,weighted", [
+    ((41, 37), [(0, 1), (1, -1), (1, 0), (1, 1)], 150, False),                # CSR staged in shared memory
+    ((33, 29), [(0, 1), (0, 2), (1, -1), (1, 0), (1, 1), (2, 0)], 90, False),  # rows of <= 13 entries
+    ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, False),                # ELL from L2, packed fp32 words
+    ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, True),                 # ELL from L2, fp64 values
 ])
-def test_kron_shared_memory_pcg(P, ctx, shape, offsets, keep):
+def test_kron_shared_memory_pcg(P, ctx, shape, offsets, keep, weighted):
     """Interiors whose PCG vectors fit one CTA's shared memory run one
-    right-hand side per CTA (pcg_smem_k); same recurrence, <= 1e-9."""
-    Lo = _stencil_laplacian(*shape, offsets)
+    right-hand side per CTA (pcg_smem_k): the operator staged in shared
+    memory when it fits, else ELL from L2 (packed (fp32, column) words when
+    every value is exact in fp32); same recurrence, <= 1e-9."""
+    Lo = _stencil_laplacian(*shape, offsets, weighted)
     n = shape[0] * shape[1]
     kp = O.draw_plan(n, 1, keep, 1, seed=7).omega_r
     R = P.kron_reduce(to_device(ctx, Lo), kp, 1e-11, 1e-12, ctx=ctx)
