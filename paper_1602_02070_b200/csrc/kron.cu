@@ -23,6 +23,8 @@
 #include <memory>
 #include <numeric>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "frpcag.cuh"
 
@@ -635,8 +637,21 @@ __global__ void csr_to_ell_packed_k(i64 n, int E, const i64* __restrict__ rp, co
   for (int k = 0; k < E; ++k) {
     const double x = k < d ? v[k0 + k] : 0.0;
     const float f = static_cast<float>(x);
-    if (static_cast<double>(f) != x) *flag = 1;
+    if (static_cast<double>(f) != x) atomicOr(flag, 1);
+    if (static_cast<double>(__half2float(__float2half_rn(f))) != x) atomicOr(flag, 2);
     ep[k * n + i] = make_uint2(__float_as_uint(f), static_cast<unsigned>(k < d ? ci[k0 + k] : static_cast<int>(i)));
+  }
+}
+
+// Narrowest packing: (fp16 value, u16 column) in one 4-byte word, when every
+// value is exact in fp16 (unit-weight grids: small integers) and n < 65536.
+__global__ void ell_pack16_k(i64 n, int E, const uint2* __restrict__ ep, unsigned* __restrict__ eh) {
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = 0; k < E; ++k) {
+    const uint2 w = ep[k * n + i];
+    const unsigned short h = __half_as_ushort(__float2half_rn(__uint_as_float(w.x)));
+    eh[k * n + i] = static_cast<unsigned>(h) | (w.y << 16);
   }
 }
 
@@ -645,8 +660,9 @@ constexpr int kPcgSmemThreads = 512;
 // E > 0: the matrix as ELL with E entries a row, read from global memory;
 // E == 0: the CSR (rp, ci, v of nnz entries) staged in shared memory after
 // the three vectors (small interiors, e.g. config 1's 900-node column graph).
-// PK: the ELL packed as (fp32 value, column) words (ev is then a uint2 array).
-template <int RPT, int E, bool PK = false>
+// PK: the ELL packed as (fp32 value, column) 8-byte words (ev is then a uint2
+// array, PK == 1) or (fp16 value, u16 column) 4-byte words (PK == 2).
+template <int RPT, int E, int PK = 0>
 __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, const double* __restrict__ ev,
                                                                  const int* __restrict__ ec,
                                                                  const i64* __restrict__ crp,
@@ -683,7 +699,15 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
     double a = 0.0;
     if constexpr (E == 0) {
       for (int k = Srp[i]; k < Srp[i + 1]; ++k) a = __dadd_rn(a, __dmul_rn(Sv[k], src[Sci[k]]));
-    } else if constexpr (PK) {
+    } else if constexpr (PK == 2) {
+      const unsigned* eh = reinterpret_cast<const unsigned*>(ev);
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const unsigned w = eh[static_cast<i64>(k) * n + i];
+        a = __dadd_rn(a, __dmul_rn(static_cast<double>(__half2float(__ushort_as_half(static_cast<unsigned short>(w & 0xffffu)))),
+                                   src[w >> 16]));
+      }
+    } else if constexpr (PK == 1) {
       const uint2* ep = reinterpret_cast<const uint2*>(ev);
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -796,7 +820,7 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
 // n <= 20 x 512, and the matrix either staged in shared memory too (CSR) or
 // read as ELL (rows of <= 16 entries).  Returns false otherwise.
 template <int RPT>
-void pcg_smem_rpt(Ctx* c, int E, bool packed, size_t smem, const double* ev, const int* ec, const i64* crp,
+void pcg_smem_rpt(Ctx* c, int E, int packed, size_t smem, const double* ev, const int* ec, const i64* crp,
                   const double* inv, const double* B, double* X, i64 n, i64 nb, double tol, i64 max_iter,
                   ColState* st) {
   auto launch = [&](auto k) {
@@ -809,9 +833,10 @@ void pcg_smem_rpt(Ctx* c, int E, bool packed, size_t smem, const double* ev, con
   if (E == 0)
     launch(pcg_smem_k<RPT, 0>);
   else if (E <= 9)
-    packed ? launch(pcg_smem_k<RPT, 9, true>) : launch(pcg_smem_k<RPT, 9>);
+    packed == 2 ? launch(pcg_smem_k<RPT, 9, 2>) : packed == 1 ? launch(pcg_smem_k<RPT, 9, 1>) : launch(pcg_smem_k<RPT, 9>);
   else
-    packed ? launch(pcg_smem_k<RPT, 16, true>) : launch(pcg_smem_k<RPT, 16>);
+    packed == 2 ? launch(pcg_smem_k<RPT, 16, 2>)
+                : packed == 1 ? launch(pcg_smem_k<RPT, 16, 1>) : launch(pcg_smem_k<RPT, 16>);
 }
 
 bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64 n, i64 nb, double tol,
@@ -821,7 +846,7 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   if (n <= 0 || n > 20 * kPcgSmemThreads || vec > kMax || A->nnz == 0) return false;
   const size_t csr = static_cast<size_t>(A->nnz) * 12 + static_cast<size_t>(n + 1) * 4 + 16;
   const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
-  auto run = [&](int E, bool pk, size_t smem, const double* ev, const int* ec, const i64* crp) {
+  auto run = [&](int E, int pk, size_t smem, const double* ev, const int* ec, const i64* crp) {
     if (rpt <= 4) return pcg_smem_rpt<4>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
     if (rpt <= 8) return pcg_smem_rpt<8>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
     if (rpt <= 12) return pcg_smem_rpt<12>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
@@ -829,7 +854,7 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
     return pcg_smem_rpt<20>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
   };
   if (vec + csr <= kMax && A->nnz < (i64{1} << 30)) {  // the whole operator in shared memory
-    run(0, false, vec + csr, A->v, A->ci, A->rp);
+    run(0, 0, vec + csr, A->v, A->ci, A->rp);
     return true;
   }
   // longest row (E): one small reduction on the host copy of the row pointers
@@ -847,15 +872,23 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   flag.zero(c);
   csr_to_ell_packed_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ep.p, flag.p);
   launched(c);
-  if (!read_back(c, flag.p)) {
-    run(Ep, true, vec, reinterpret_cast<const double*>(ep.p), nullptr, nullptr);
+  const int fl = read_back(c, flag.p);
+  if (!(fl & 2) && n < 65536) {
+    DevBuf<unsigned> eh(c, static_cast<size_t>(Ep) * n);
+    ell_pack16_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, ep.p, eh.p);
+    launched(c);
+    run(Ep, 2, vec, reinterpret_cast<const double*>(eh.p), nullptr, nullptr);
+    return true;
+  }
+  if (!(fl & 1)) {
+    run(Ep, 1, vec, reinterpret_cast<const double*>(ep.p), nullptr, nullptr);
     return true;
   }
   DevBuf<double> ev(c, static_cast<size_t>(Ep) * n);
   DevBuf<int> ec(c, static_cast<size_t>(Ep) * n);
   csr_to_ell_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ev.p, ec.p);
   launched(c);
-  run(Ep, false, vec, ev.p, ec.p, nullptr);
+  run(Ep, 0, vec, ev.p, ec.p, nullptr);
   return true;
 }
 

@@ -239,7 +239,8 @@ def _stencil_laplacian(h, w, offsets, weighted=False):
                 r2, c2 = r + dr, c + dc
                 if 0 <= r2 < h and 0 <= c2 < w:
                     a, b = r * w + c, r2 * w + c2
-                    x = float(rs.uniform(0.5, 2.0)) if weighted else 1.0
+                    x = {False: 1.0, "fp32": 1.0 + 2.0 ** -12, True: None}[weighted]
+                    x = float(rs.uniform(0.5, 2.0)) if x is None else x
                     ti += [a, b]
                     tj += [b, a]
                     tv += [x, x]
@@ -249,14 +250,16 @@ def _stencil_laplacian(h, w, offsets, weighted=False):
 @pytest.mark.parametrize("shape,offsets,keep,weighted", [
     ((41, 37), [(0, 1), (1, -1), (1, 0), (1, 1)], 150, False),                # CSR staged in shared memory
     ((33, 29), [(0, 1), (0, 2), (1, -1), (1, 0), (1, 1), (2, 0)], 90, False),  # rows of <= 13 entries
-    ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, False),                # ELL from L2, packed fp32 words
+    ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, False),                # ELL from L2, (fp16, u16) words
+    ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, "fp32"),               # ELL from L2, (fp32, int) words
     ((95, 90), [(0, 1), (1, -1), (1, 0), (1, 1)], 700, True),                 # ELL from L2, fp64 values
 ])
 def test_kron_shared_memory_pcg(P, ctx, shape, offsets, keep, weighted):
     """Interiors whose PCG vectors fit one CTA's shared memory run one
     right-hand side per CTA (pcg_smem_k): the operator staged in shared
-    memory when it fits, else ELL from L2 (packed (fp32, column) words when
-    every value is exact in fp32); same recurrence, <= 1e-9."""
+    memory when it fits, else ELL from L2 (packed (fp16, u16) or (fp32,
+    int32) words when every value is exact in that format); same
+    recurrence, <= 1e-9."""
     Lo = _stencil_laplacian(*shape, offsets, weighted)
     n = shape[0] * shape[1]
     kp = O.draw_plan(n, 1, keep, 1, seed=7).omega_r
