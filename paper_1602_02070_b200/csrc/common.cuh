@@ -374,6 +374,28 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
   __syncthreads();
 }
 
+// The same barrier with the generation tracked in a register: `g` counts the
+// barriers this CTA has passed (0 at kernel start, *gen zeroed before the
+// launch), so thread 0 skips the initial load of *gen -- one L2 round trip
+// less per barrier.  Every CTA must pass the same sequence of barriers.
+__device__ __forceinline__ void grid_barrier_local(unsigned* count, unsigned* gen, unsigned& g) {
+  __syncthreads();
+  ++g;
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(count) : "memory");
+    if (old == nb - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(count) : "memory");
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(g) : "memory");
+    } else {
+      while (static_cast<int>(ld_acquire_gpu(gen) - g) < 0) {
+      }
+    }
+  }
+  __syncthreads();
+}
+
 inline unsigned blocks_for(i64 n, int block = kBlock) {
   i64 b = (n + block - 1) / block;
   if (b < 1) b = 1;

@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   const double* vsrc = v_in_smem ? vs : v0;
   double est = 0.0;
   i64 it = 0;
+  unsigned bar_g = 0;  // barriers passed (PowerState is zeroed before the launch)
   for (; it < max_iter; ++it) {
     double* w = wbuf + (it & 1) * n;
     for (i64 r = r0 + wid; r < r1; r += nw) {
@@ -536,7 +537,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       acc = warp_sum(acc);
       if (lane == 0) w[r] = acc;
     }
-    grid_barrier(&st->bar_count, &st->bar_gen);
+    grid_barrier_local(&st->bar_count, &st->bar_gen, bar_g);
     // ||w||^2 straight from w, which every CTA reads anyway: one L2 round
     // trip per iteration instead of two (partials, then w).  Same data and
     // the same fixed-order block reduction in every CTA, so every CTA gets
@@ -568,7 +569,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       ++it;
       break;
     }
-    if (!v_in_smem) grid_barrier(&st->bar_count, &st->bar_gen);
+    if (!v_in_smem) grid_barrier_local(&st->bar_count, &st->bar_gen, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->est = est;
