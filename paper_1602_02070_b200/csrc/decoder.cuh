@@ -983,22 +983,11 @@ __device__ __forceinline__ T& lane_of(V& v, int k) {
 }
 
 // alpha = rho / <P, AP> (breakdown check, solvers.hpp:53-57); R -= alpha AP;
-// rho_next = ||R||^2.
+// rho_next = ||R||^2.  The element loops are device functions shared by the
+// separate kernels (sharded solver) and the fused cooperative kernel below.
 template <typename TK, bool kVec>
-__global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ AP, double* partials,
-                              CgState* st) {
-  if (st->done) return;
-  const double curv = st->curv;
-  if (!isfinite(curv) || curv <= 0.0) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->err = 1;
-      st->err_it = st->it;
-      st->done = 1;
-    }
-    return;
-  }
-  const TK alpha = static_cast<TK>(st->rho / curv);
-  double s[1] = {0.0};
+__device__ __forceinline__ double residual_loop(i64 N, TK* __restrict__ R, const TK* __restrict__ AP, TK alpha) {
+  double s = 0.0;
   const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, ts = (i64)gridDim.x * blockDim.x;
   i64 from = 0;
   if constexpr (kVec) {
@@ -1021,7 +1010,7 @@ __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ 
         for (int k = 0; k < W; ++k) {
           TK& x = lane_of<TK>(r[u], k);
           x = sub_rn(x, mul_rn(alpha, reinterpret_cast<const TK*>(&a[u])[k]));
-          s[0] += static_cast<double>(x) * static_cast<double>(x);
+          s += static_cast<double>(x) * static_cast<double>(x);
         }
         Rv[q + u * ts] = r[u];
       }
@@ -1033,7 +1022,7 @@ __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ 
       for (int k = 0; k < W; ++k) {
         TK& x = lane_of<TK>(r, k);
         x = sub_rn(x, mul_rn(alpha, reinterpret_cast<const TK*>(&a)[k]));
-        s[0] += static_cast<double>(x) * static_cast<double>(x);
+        s += static_cast<double>(x) * static_cast<double>(x);
       }
       Rv[q] = r;
     }
@@ -1042,19 +1031,15 @@ __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ 
   for (i64 q = from + t0; q < N; q += ts) {
     const TK r = sub_rn(R[q], mul_rn(alpha, AP[q]));
     R[q] = r;
-    s[0] += static_cast<double>(r) * static_cast<double>(r);
+    s += static_cast<double>(r) * static_cast<double>(r);
   }
-  double tot[1];
-  if (grid_sum_last<1>(s, partials, &st->cnt[2], tot) && threadIdx.x == 0) st->rho_next = tot[0];
+  return s;
 }
 
-// X += alpha P, P = R + beta P (beta = rho_next / rho); the last block
-// advances the iteration and applies the loop-top stop test.
+// X += alpha P, P = R + beta P.
 template <typename TK, typename TX, bool kVec>
-__global__ void cg_update_k(i64 N, TX* __restrict__ X, TK* __restrict__ P, const TK* __restrict__ R, CgState* st) {
-  if (st->done) return;
-  const TK alpha = static_cast<TK>(st->rho / st->curv);
-  const TK beta = static_cast<TK>(st->rho_next / st->rho);
+__device__ __forceinline__ void update_loop(i64 N, TX* __restrict__ X, TK* __restrict__ P, const TK* __restrict__ R,
+                                            TK alpha, TK beta) {
   const i64 t0 = blockIdx.x * (i64)blockDim.x + threadIdx.x, ts = (i64)gridDim.x * blockDim.x;
   i64 from = 0;
   if constexpr (kVec && sizeof(TX) == sizeof(TK)) {
@@ -1124,6 +1109,41 @@ __global__ void cg_update_k(i64 N, TX* __restrict__ X, TK* __restrict__ P, const
     X[q] = static_cast<TX>(add_rn(static_cast<TK>(X[q]), mul_rn(alpha, pv)));
     P[q] = add_rn(R[q], mul_rn(beta, pv));
   }
+}
+
+// breakdown check (solvers.hpp:53-57), uniform over the grid; true when the
+// iteration stops here
+__device__ __forceinline__ bool cg_breakdown(CgState* st) {
+  const double curv = st->curv;
+  if (!isfinite(curv) || curv <= 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->err = 1;
+      st->err_it = st->it;
+      st->done = 1;
+    }
+    return true;
+  }
+  return false;
+}
+
+template <typename TK, bool kVec>
+__global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ AP, double* partials,
+                              CgState* st) {
+  if (st->done || cg_breakdown(st)) return;
+  const TK alpha = static_cast<TK>(st->rho / st->curv);
+  double s[1] = {residual_loop<TK, kVec>(N, R, AP, alpha)};
+  double tot[1];
+  if (grid_sum_last<1>(s, partials, &st->cnt[2], tot) && threadIdx.x == 0) st->rho_next = tot[0];
+}
+
+// X += alpha P, P = R + beta P (beta = rho_next / rho); the last block
+// advances the iteration and applies the loop-top stop test.
+template <typename TK, typename TX, bool kVec>
+__global__ void cg_update_k(i64 N, TX* __restrict__ X, TK* __restrict__ P, const TK* __restrict__ R, CgState* st) {
+  if (st->done) return;
+  const TK alpha = static_cast<TK>(st->rho / st->curv);
+  const TK beta = static_cast<TK>(st->rho_next / st->rho);
+  update_loop<TK, TX, kVec>(N, X, P, R, alpha, beta);
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
