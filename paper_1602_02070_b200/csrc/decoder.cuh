@@ -265,10 +265,17 @@ __device__ __forceinline__ int4 lds_i128(unsigned a) {
   return v;
 }
 
-template <typename TK, int EVR, bool kResid, typename TB>
+// O32: p n < 2^31, element offsets in 32 bits (no 64-bit multiplies per column).
+template <typename TK, int EVR, bool kResid, typename TB, bool O32 = false>
 __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int parts, SlabPlan sp,
                                                            const float* __restrict__ P, Combine<TK, TB> cb) {
   if (cb.st && cb.st->done) return;
+  auto colp = [p](int c) -> i64 {
+    if constexpr (O32)
+      return static_cast<i64>(static_cast<unsigned>(c) * static_cast<unsigned>(p));
+    else
+      return static_cast<i64>(c) * p;
+  };
   extern __shared__ __align__(16) unsigned char smraw[];
   const int slab = blockIdx.x / parts, part = blockIdx.x % parts;
   const int i0 = slab * 32, rows = min(32, p - i0);
@@ -323,7 +330,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int part
     auto window = [&](const SlabStep& q) {  // the quad's L_r windows (one commit group)
       if (wcopy)
 #pragma unroll
-        for (int g = 0; g < 4; ++g) cp_async16(hbase + g * 512 + lane * 16, wsrc + static_cast<i64>(q.col[g]) * p);
+        for (int g = 0; g < 4; ++g) cp_async16(hbase + g * 512 + lane * 16, wsrc + colp(q.col[g]));
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     window(S[st0]);
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int part
                                   : 0.0;
             s += d * d;
           } else {
-            if (real) APi[static_cast<i64>(cur.col[g]) * p] = out;
+            if (real) APi[colp(cur.col[g])] = out;
             s += real ? static_cast<double>(pv) * static_cast<double>(out) : 0.0;
           }
         }
@@ -1712,8 +1719,11 @@ void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const T
   if constexpr (sizeof(TI) == 4 && sizeof(TV) == 4) {
     if (ap.slab) {
       KScope ks_(c, "cg_apply");
-      auto k = cb.Xt ? (ap.s_evr == 9 ? slab_k<TK, 9, true, TB> : slab_k<TK, 16, true, TB>)
-                     : (ap.s_evr == 9 ? slab_k<TK, 9, false, TB> : slab_k<TK, 16, false, TB>);
+      const bool o32 = ap.p * ap.ncols < (i64{1} << 31);
+      auto k = cb.Xt ? (ap.s_evr == 9 ? (o32 ? slab_k<TK, 9, true, TB, true> : slab_k<TK, 9, true, TB>)
+                                      : (o32 ? slab_k<TK, 16, true, TB, true> : slab_k<TK, 16, true, TB>))
+                     : (ap.s_evr == 9 ? (o32 ? slab_k<TK, 9, false, TB, true> : slab_k<TK, 9, false, TB>)
+                                      : (o32 ? slab_k<TK, 16, false, TB, true> : slab_k<TK, 16, false, TB>));
       ensure_smem(k, ap.s_smem);
       const SlabPlan sp{ap.s_rec.p,  reinterpret_cast<const SlabStep*>(ap.s_steps.p), ap.s_wsteps.p, ap.s_max_steps,
                         ap.s_win.p, ap.s_lv.p, ap.s_lo.p};
