@@ -277,53 +277,67 @@ __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int part
       return static_cast<i64>(c) * p;
   };
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int slab = blockIdx.x / parts, part = blockIdx.x % parts;
-  const int i0 = slab * 32, rows = min(32, p - i0);
   float* Pb = reinterpret_cast<float*>(smraw);  // [n][32]
   const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(Pb));
-  if (rows == 32) {
-    for (int q = threadIdx.x; q < n * 8; q += kSlabThreads)
-      cp_async16(sbase + static_cast<unsigned>(q) * 16u, P + static_cast<i64>(q >> 3) * p + i0 + (q & 7) * 4);
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  } else {
-    for (int q = threadIdx.x; q < n * 32; q += kSlabThreads) {
-      const int c = q >> 5, r = q & 31;
-      Pb[q] = r < rows ? P[static_cast<i64>(c) * p + i0 + r] : 0.f;
-    }
-  }
-  // the part's step list next to the slab (copied with it)
-  const int pst0 = sp.wsteps[part * (kSlabWarps + 1)], pst1 = sp.wsteps[part * (kSlabWarps + 1) + kSlabWarps];
   const unsigned stbase = sbase + static_cast<unsigned>(static_cast<size_t>(n) * 128);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g4 = lane >> 3, s4 = lane & 7;  // quad layout: column g4, rows 4 s4 .. 4 s4 + 3
+  const unsigned wbase = stbase + static_cast<unsigned>(sp.max_steps) * 32u +
+                         static_cast<unsigned>(warp) * static_cast<unsigned>(kSlabWarpBytes);
+  const unsigned rbase = wbase, hbase = wbase + kSlabRing * 512, xbase = hbase + 4 * 512;
+  // persistent: this CTA's contiguous range of (slab, column part) items; the
+  // slab is copied again only when the slab changes
+  const int items = ((p + 31) / 32) * parts;
+  const int ia = static_cast<int>(static_cast<i64>(items) * blockIdx.x / gridDim.x);
+  const int ib = static_cast<int>(static_cast<i64>(items) * (blockIdx.x + 1) / gridDim.x);
+  double s = 0.0;
+  int cur_slab = -1, i0 = 0, rows = 0, i = 0;
+  bool vrow = false, wcopy = false, rs = false;
+  float lv[EVR];
+  unsigned lo[EVR];  // shared address of the entry's row in window 0
+  const float* wsrc = P;
+  TK* APi = nullptr;
+  for (int item = ia; item < ib; ++item) {
+  const int slab = item / parts, part = item % parts;
+  __syncthreads();  // the previous item is done with the slab, steps, rings and windows
+  if (slab != cur_slab) {
+    cur_slab = slab;
+    i0 = slab * 32;
+    rows = min(32, p - i0);
+    if (rows == 32) {
+      for (int q = threadIdx.x; q < n * 8; q += kSlabThreads)
+        cp_async16(sbase + static_cast<unsigned>(q) * 16u, P + colp(q >> 3) + i0 + (q & 7) * 4);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    } else {
+      for (int q = threadIdx.x; q < n * 32; q += kSlabThreads) {
+        const int c = q >> 5, r = q & 31;
+        Pb[q] = r < rows ? P[colp(c) + i0 + r] : 0.f;
+      }
+    }
+    vrow = lane < rows;
+    i = i0 + (vrow ? lane : 0);
+#pragma unroll
+    for (int e = 0; e < EVR; ++e) {
+      lv[e] = vrow ? sp.lv[static_cast<i64>(e) * p + i] : 0.f;
+      lo[e] = hbase + (vrow ? static_cast<unsigned>(sp.lo[static_cast<i64>(e) * p + i]) : 0u);
+    }
+    const int wrow = sp.win[slab * 32 + lane];  // this lane's window chunk (rows wrow .. wrow + 3)
+    wcopy = wrow != kNoChunk;
+    wsrc = P + i0 + (wcopy ? wrow : 0);
+    rs = vrow && cb.pl.rsel[i] >= 0;
+    if constexpr (!kResid) APi = cb.AP + i;
+  }
+  // the part's step list next to the slab
+  const int pst0 = sp.wsteps[part * (kSlabWarps + 1)], pst1 = sp.wsteps[part * (kSlabWarps + 1) + kSlabWarps];
   {
     const unsigned char* src = reinterpret_cast<const unsigned char*>(sp.steps + pst0);
     for (int q = threadIdx.x; q < (pst1 - pst0) * 2; q += kSlabThreads) cp_async16(stbase + q * 16u, src + q * 16);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
   const SlabStep* S = reinterpret_cast<const SlabStep*>(smraw + (stbase - sbase)) - pst0;  // indexed by step
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g4 = lane >> 3, s4 = lane & 7;  // quad layout: column g4, rows 4 s4 .. 4 s4 + 3
-  const bool vrow = lane < rows;
-  const int i = i0 + (vrow ? lane : 0);
-  const unsigned wbase = stbase + static_cast<unsigned>(sp.max_steps) * 32u +
-                         static_cast<unsigned>(warp) * static_cast<unsigned>(kSlabWarpBytes);
-  const unsigned rbase = wbase, hbase = wbase + kSlabRing * 512, xbase = hbase + 4 * 512;
-  float lv[EVR];
-  unsigned lo[EVR];  // shared address of the entry's row in window 0
-#pragma unroll
-  for (int e = 0; e < EVR; ++e) {
-    lv[e] = vrow ? sp.lv[static_cast<i64>(e) * p + i] : 0.f;
-    lo[e] = hbase + (vrow ? static_cast<unsigned>(sp.lo[static_cast<i64>(e) * p + i]) : 0u);
-  }
-  const int wrow = sp.win[slab * 32 + lane];  // this lane's window chunk (rows wrow .. wrow + 3)
-  const bool wcopy = wrow != kNoChunk;
-  const float* wsrc = P + i0 + (wcopy ? wrow : 0);
-  const bool rs = vrow && cb.pl.rsel[i] >= 0;
-  TK* const APi = kResid ? nullptr : cb.AP + i;
   const int st0 = sp.wsteps[part * (kSlabWarps + 1) + warp], st1 = sp.wsteps[part * (kSlabWarps + 1) + warp + 1];
-  (void)st0;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  double s = 0.0;
   if (st0 < st1) {
     unsigned issued = static_cast<unsigned>(S[st0].rec) / 512u;
     const unsigned char* gsrc = sp.rec + lane * 16;
@@ -431,6 +445,7 @@ __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int part
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   }
+  }  // items
   finish_reduction(s, cb);
 }
 
@@ -1183,7 +1198,7 @@ struct ApplyPlan {
   i64 p = 0, ncols = 0, n_local = 0, col_base = 0;
   // slab apply (slab_k): fp32 iterates, a 32-row slab of all columns in shared memory
   bool slab = false;
-  int s_parts = 1, s_evr = 9, s_max_steps = 0;
+  int s_parts = 1, s_evr = 9, s_max_steps = 0, s_grid = 1;
   size_t s_smem = 0;
   DevBuf<unsigned char> s_rec, s_steps;  // interleaved L_c records, SlabStep list
   DevBuf<int> s_wsteps, s_win, s_lo;
@@ -1299,16 +1314,10 @@ bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr,
       }
     }
     trace_mark(c, "slab plan: windows");
-    // column ranges per slab: minimise waves x (slab copy + columns), the copy
-    // costing ~0.1 of a whole slab's compute
-    const i64 per_sm = smem <= 113 * 1024 ? 2 : 1;
-    int best = 1;
-    double best_t = 1e300;
-    for (int parts = 1; parts <= 4; ++parts) {
-      const i64 waves = (slabs * parts + c->num_sms * per_sm - 1) / (c->num_sms * per_sm);
-      const double t = static_cast<double>(waves) * (0.1 + 1.0 / parts);
-      if (t < best_t - 1e-9) best_t = t, best = parts;
-    }
+    // column parts per slab: the persistent CTAs take contiguous runs of
+    // (slab, part) items, so finer parts balance the SMs; each part keeps
+    // >= ~4 quads per warp for the warps' own balance
+    const int best = n >= 768 ? 4 : n >= 384 ? 2 : 1;
     // L_c quads: per part, columns sorted by degree, 4 at a time, dealt to the
     // warps round-robin; each warp's steps (<= (kSlabRing - 1) chunks of
     // records) laid out contiguously
@@ -1402,6 +1411,7 @@ bool plan_slab(Ctx* c, ApplyPlan& ap, i64 p, i64 n, const std::vector<i64>& rpr,
     rec.resize(((rec.size() + 31) / 32 + 1) * 32, int4{0, 0, 0, 0});  // whole 512-byte chunks, one spare
     ap.slab = true;
     ap.s_parts = best;
+    ap.s_grid = static_cast<int>(std::min<i64>(c->num_sms, slabs * best));
     ap.s_evr = EVR;
     ap.s_smem = smem_all;
     ap.s_max_steps = max_steps;
@@ -1634,7 +1644,7 @@ inline size_t lc_blocks(const ApplyPlan& ap, int S) {
                     : static_cast<size_t>((ap.p + 31) / 32) * ap.lc_chunks;
 }
 inline size_t lr_blocks(const ApplyPlan& ap) {
-  if (ap.slab) return static_cast<size_t>((ap.p + 31) / 32) * ap.s_parts;
+  if (ap.slab) return static_cast<size_t>(ap.s_grid);
   if (ap.fused) return static_cast<size_t>(ap.f_grid.x) * ap.f_grid.y;
   return ap.lr_reg ? static_cast<size_t>(ap.lr_groups) * ap.lr_stripes
                    : static_cast<size_t>(ap.n_ranges) * ((ap.ncols + ap.gen_C - 1) / ap.gen_C);
@@ -1727,7 +1737,7 @@ void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const T
       ensure_smem(k, ap.s_smem);
       const SlabPlan sp{ap.s_rec.p,  reinterpret_cast<const SlabStep*>(ap.s_steps.p), ap.s_wsteps.p, ap.s_max_steps,
                         ap.s_win.p, ap.s_lv.p, ap.s_lo.p};
-      const unsigned grid = static_cast<unsigned>(((ap.p + 31) / 32) * ap.s_parts);
+      const unsigned grid = static_cast<unsigned>(ap.s_grid);  // persistent, one CTA per SM
       k<<<grid, kSlabThreads, ap.s_smem, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols), ap.s_parts,
                                                      sp, P, cb);
       launched(c);
