@@ -202,6 +202,172 @@ __global__ void __launch_bounds__(256) knn_tile_k(const double* __restrict__ Pm,
   }
 }
 
+// All-points search over the upper triangle of 64-point tile pairs: g_ij and
+// g_ji are the same bits (products commute, same k order), so one CTA per
+// pair (it <= jt) forms the 64 x 64 d2 tile once and feeds both top-K
+// lists: queries of `it` over candidates of `jt` (threads 0-63) and, off the
+// diagonal, queries of `jt` over candidates of `it` (threads 64-127, reading
+// the tile transposed).  Half the Gram work of knn_tile_k.  Output list
+// (source tile s, query i) goes to cand[(s n + i) K]: every (s, i) is written
+// by exactly one CTA.  The k-chunks are double-buffered through registers
+// (one barrier per chunk): the 166 KB of shared memory leaves one CTA per SM.
+constexpr int kKcS = 64;  // k-chunk of the symmetric kernel (one barrier per 64 k)
+constexpr size_t kKnnSymStage = 4 * kKcS * (kTile + 1) * sizeof(double);
+constexpr size_t kKnnSymTail = kTile * (kTile + 1) * sizeof(double) +
+                               2 * kTile * (kMaxK + 1) * (sizeof(double) + sizeof(int));
+constexpr size_t kKnnSymSmem = kKnnSymStage > kKnnSymTail ? kKnnSymStage : kKnnSymTail;
+
+__device__ __forceinline__ void topk_insert(double* bd, int* bj, int K, double v, int j) {
+  if (!lex_less(v, j, bd[K - 1], bj[K - 1])) return;
+  int q = K - 1;
+  while (q > 0 && lex_less(v, j, bd[q - 1], bj[q - 1])) {
+    bd[q] = bd[q - 1];
+    bj[q] = bj[q - 1];
+    --q;
+  }
+  bd[q] = v;
+  bj[q] = j;
+}
+
+// coincident candidate j < i of query i (d2 == 0): exact coordinate test (graph.cpp:68-84)
+__device__ __forceinline__ void dup_check(const double* __restrict__ Pm, i64 d, i64 i, i64 j, int* dup) {
+  if (dup[i]) return;
+  const double* a = Pm + i * d;
+  const double* b = Pm + j * d;
+  bool same = true;
+  for (i64 k = 0; k < d && same; ++k) same = a[k] == b[k];
+  if (same) dup[i] = 1;
+}
+
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) knn_sym_k(const double* __restrict__ Pm, const double* __restrict__ sq,
+                                                 i64 n, i64 d, int K, int T, double* __restrict__ cand_d,
+                                                 int* __restrict__ cand_j, int* __restrict__ dup) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using Row = double[kTile + 1];
+  Row* As = reinterpret_cast<Row*>(smem);  // [2][kKcS]
+  Row* Bs = As + 2 * kKcS;                 // [2][kKcS]
+  Row* Dt = reinterpret_cast<Row*>(smem);  // [kTile], over the staging buffers once the Gram is done
+  double(*best_d)[kMaxK + 1] = reinterpret_cast<double(*)[kMaxK + 1]>(Dt + kTile);  // [2 kTile]
+  int(*best_j)[kMaxK + 1] = reinterpret_cast<int(*)[kMaxK + 1]>(best_d + 2 * kTile);
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  int pr = blockIdx.x, it = 0;
+  while (pr >= T - it) {
+    pr -= T - it;
+    ++it;
+  }
+  const int jt = it + pr;
+  const i64 i0 = static_cast<i64>(it) * kTile, j0 = static_cast<i64>(jt) * kTile;
+
+  constexpr int kPer = (kTile * kKcS) / kThreads;
+  constexpr int kRows = kTile / (kThreads / 16);  // accumulator rows per thread (16 column groups of 4)
+  constexpr int kRs = kThreads / 16;              // row stride
+  double ra[kPer], rb[kPer];
+  auto load = [&](i64 k0) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int idx = tid + kThreads * q, pt = idx / kKcS;
+      const i64 k = k0 + idx % kKcS;
+      ra[q] = (i0 + pt < n && k < d) ? Pm[(i0 + pt) * d + k] : 0.0;
+      rb[q] = (j0 + pt < n && k < d) ? Pm[(j0 + pt) * d + k] : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int idx = tid + kThreads * q, pt = idx / kKcS, kk = idx % kKcS;
+      As[buf * kKcS + kk][pt] = ra[q];
+      Bs[buf * kKcS + kk][pt] = rb[q];
+    }
+  };
+  double acc[kRows][4];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
+  const i64 nch = (d + kKcS - 1) / kKcS;
+  load(0);
+  store(0);
+  __syncthreads();
+  for (i64 ch = 0; ch < nch; ++ch) {
+    const int buf = static_cast<int>(ch & 1);
+    if (ch + 1 < nch) load((ch + 1) * kKcS);  // next chunk in flight during this one's products
+    const Row* A = As + buf * kKcS;
+    const Row* B = Bs + buf * kKcS;
+#pragma unroll
+    for (int kk = 0; kk < kKcS; ++kk) {
+      double a[kRows], b[4];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) a[r] = A[kk][ty + kRs * r];
+#pragma unroll
+      for (int s = 0; s < 4; ++s) b[s] = B[kk][tx + 16 * s];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc[r][s] = __dadd_rn(acc[r][s], __dmul_rn(a[r], b[s]));
+    }
+    if (ch + 1 < nch) store(buf ^ 1);
+    __syncthreads();
+  }
+  // d2 tile (graph.cpp:63), masked outside the matrix and on the diagonal
+  // (the loop's last barrier retired every read of the staging buffers)
+  if (tid < 2 * kTile)
+    for (int q = 0; q < K; ++q) {
+      best_d[tid][q] = CUDART_INF;
+      best_j[tid][q] = INT32_MAX;
+    }
+#pragma unroll
+  for (int r = 0; r < kRows; ++r)
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int li = ty + kRs * r, lj = tx + 16 * s;
+      const i64 gi = i0 + li, gj = j0 + lj;
+      double v = CUDART_INF;
+      if (gi < n && gj < n && gi != gj) {
+        const double t = __dsub_rn(__dadd_rn(sq[gi], sq[gj]), __dmul_rn(2.0, acc[r][s]));
+        v = t > 0.0 ? t : 0.0;
+      }
+      Dt[li][lj] = v;
+    }
+  __syncthreads();
+  if (tid < kTile) {  // queries of tile it, candidates of tile jt
+    const i64 gi = i0 + tid;
+    if (gi < n) {
+      for (int lj = 0; lj < kTile; ++lj) {
+        const double v = Dt[tid][lj];
+        const i64 gj = j0 + lj;
+        if (v == 0.0 && gj < gi && gj < n) dup_check(Pm, d, gi, gj, dup);
+        topk_insert(best_d[tid], best_j[tid], K, v, static_cast<int>(gj < n ? gj : INT32_MAX));
+      }
+      double* od = cand_d + (static_cast<i64>(jt) * n + gi) * K;
+      int* oj = cand_j + (static_cast<i64>(jt) * n + gi) * K;
+      for (int q = 0; q < K; ++q) {
+        od[q] = best_d[tid][q];
+        oj[q] = best_j[tid][q];
+      }
+    }
+  } else if (tid < 2 * kTile && it != jt) {  // queries of tile jt, candidates of tile it
+    const int q0 = tid - kTile;
+    const i64 gq = j0 + q0;
+    if (gq < n) {
+      for (int li = 0; li < kTile; ++li) {
+        const double v = Dt[li][q0];
+        const i64 gc = i0 + li;
+        if (v == 0.0 && gc < gq && gc < n) dup_check(Pm, d, gq, gc, dup);
+        topk_insert(best_d[tid], best_j[tid], K, v, static_cast<int>(gc < n ? gc : INT32_MAX));
+      }
+      double* od = cand_d + (static_cast<i64>(it) * n + gq) * K;
+      int* oj = cand_j + (static_cast<i64>(it) * n + gq) * K;
+      for (int q = 0; q < K; ++q) {
+        od[q] = best_d[tid][q];
+        oj[q] = best_j[tid][q];
+      }
+    }
+  }
+}
+
 // Merge the per-split sorted lists of each point; mean d2 in ascending order.
 __global__ void knn_merge_k(i64 n, int K, int splits, const double* __restrict__ cand_d,
                             const int* __restrict__ cand_j, int64_t* __restrict__ nbr,
@@ -557,6 +723,22 @@ void knn_exact_rows(Ctx* c, const double* Pm, const double* sq, i64 n, i64 d, i6
   if (nq == 0) return;
   const i64 q_tiles = (nq + kTile - 1) / kTile;
   const i64 n_tiles = (n + kTile - 1) / kTile;
+  if (!qidx && nq == n && n_tiles <= 64) {  // all points: the upper triangle of tile pairs
+    DevBuf<double> cand_d(c, n_tiles * n * K);
+    DevBuf<int> cand_j(c, n_tiles * n * K);
+    constexpr int kSymThreads = 256;
+    ensure_smem(knn_sym_k<kSymThreads>, kKnnSymSmem);
+    {
+      KScope ks_(c, "knn_tile");
+      knn_sym_k<kSymThreads><<<static_cast<unsigned>(n_tiles * (n_tiles + 1) / 2), kSymThreads, kKnnSymSmem, c->stream>>>(
+          Pm, sq, n, d, static_cast<int>(K), static_cast<int>(n_tiles), cand_d.p, cand_j.p, dup);
+      launched(c);
+    }
+    knn_merge_k<<<blocks_for(n, 128), 128, 0, c->stream>>>(n, static_cast<int>(K), static_cast<int>(n_tiles),
+                                                           cand_d.p, cand_j.p, nbr, nbr_d2, mean, nullptr);
+    launched(c);
+    return;
+  }
   i64 splits = std::max<i64>(1, (2 * static_cast<i64>(c->num_sms) + q_tiles - 1) / q_tiles);
   splits = std::min<i64>({splits, n_tiles, 64});
   const i64 tps = (n_tiles + splits - 1) / splits;

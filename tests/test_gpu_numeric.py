@@ -85,7 +85,9 @@ def test_power_iteration_known_answers(P, ctx):
 
 
 def test_power_iteration_matches_oracle(P, ctx):
-    for seed, n in [(1, 50), (2, 700), (3, 3000)]:
+    # 50, 700: one CTA; 3000: cooperative grid, v in shared memory;
+    # 20000: cooperative grid, v renormalised in global memory
+    for seed, n in [(1, 50), (2, 700), (3, 3000), (4, 20000)]:
         L = knn_laplacian(n, 4, 8, seed)
         got = P.power_iteration_norm(to_device(ctx, L), 1e-7, 42, ctx=ctx)
         want = O.power_iteration_norm(L, 1e-7, 42)
