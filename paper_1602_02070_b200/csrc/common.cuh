@@ -11,6 +11,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -87,7 +89,23 @@ struct Ctx {
   int fista_simt = 0;         // 1: the persistent FISTA kernel's SIMT tile GEMM instead of DMMA (tests)
   cudaStream_t side = nullptr;  // second stream for independent work (lazily created)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // Host work deferred to the next long device wait (run_idle_work): it runs
+  // with `stream` switched to `aux`, and the context stream then waits on it.
+  std::function<void()> idle_work;
+  cudaStream_t aux = nullptr;
+  cudaEvent_t aux_ev = nullptr;
   KernelTimes kt;
+};
+
+// Runs (and clears) c->idle_work on the aux stream while the device works
+// through what the context stream already holds; no-op when none is pending.
+void run_idle_work(Ctx* c);
+
+// Clears c->idle_work when the scope that set it ends (its captures die there).
+struct IdleWorkScope {
+  Ctx* c;
+  explicit IdleWorkScope(Ctx* ctx) : c(ctx) {}
+  ~IdleWorkScope() { c->idle_work = nullptr; }
 };
 
 // The context's side stream (non-blocking, created on first use) and its
@@ -479,11 +497,20 @@ void fista_device(Ctx* c, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
                   const cpcag_frpcag_config& cfg, T* X, double* objective_host,
                   cpcag_solve_trace* trace);
 
+// The alternate decoder's operator plans, built ahead of the decode (host
+// planning that can overlap device work; see run_idle_work).
+struct DecodePrepBase {
+  virtual ~DecodePrepBase() = default;
+};
+template <typename T>
+std::unique_ptr<DecodePrepBase> alternate_decode_prepare(Ctx* c, i64 p, i64 n, Csr* Lr, Csr* Lc,
+                                                         const cpcag_decoder_config& cfg);
+
 template <typename T>
 void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i64* om_r_host,
                              const i64* om_c_host, i64 p, i64 n, Csr* Lr, Csr* Lc, double lk1_r,
                              double lk1_c, const cpcag_decoder_config& cfg, T* X, int* converged,
-                             i64* iterations);
+                             i64* iterations, DecodePrepBase* prep = nullptr);
 
 Csr* kron_reduce_device(Ctx* c, Csr* L, const std::vector<i64>& keep, double pcg_tol,
                         double prune_tol);

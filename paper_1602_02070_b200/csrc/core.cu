@@ -63,6 +63,27 @@ void ensure_smem_impl(const void* func, size_t bytes) {
   seen.push_back({func, bytes});
 }
 
+void run_idle_work(Ctx* c) {
+  if (!c->idle_work) return;
+  std::function<void()> work = std::move(c->idle_work);
+  c->idle_work = nullptr;
+  if (!c->aux) {
+    CUDA_OK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&c->aux_ev, cudaEventDisableTiming));
+  }
+  cudaStream_t main_stream = c->stream;
+  c->stream = c->aux;
+  try {
+    work();
+  } catch (...) {
+    c->stream = main_stream;
+    throw;
+  }
+  c->stream = main_stream;
+  CUDA_OK(cudaEventRecord(c->aux_ev, c->aux));
+  CUDA_OK(cudaStreamWaitEvent(main_stream, c->aux_ev, 0));
+}
+
 void trace_mark(Ctx* c, const char* what) {
   static const bool on = std::getenv("CPCAG_TRACE") != nullptr;
   if (!on) return;
@@ -697,6 +718,7 @@ void power_norm_pair(Ctx* c, Csr* A1, Csr* A2, double tol, uint64_t seed, i64 ma
   power_prepare(c, A2, tol, seed, max_iter, j2, c->stream, true);
   CUDA_OK(cudaEventRecord(c->join_ev, side));
   CUDA_OK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
+  run_idle_work(c);  // host work beside the iterations (the pipeline's decoder planning)
   *out1 = power_result(c, j1);
   *out2 = power_result(c, j2);
 }
@@ -902,6 +924,11 @@ int cpcag_ctx_destroy(cpcag_ctx ctx) {
       cudaStreamDestroy(c->side);
       cudaEventDestroy(c->fork_ev);
       cudaEventDestroy(c->join_ev);
+    }
+    if (c->aux) {
+      cudaStreamSynchronize(c->aux);
+      cudaStreamDestroy(c->aux);
+      cudaEventDestroy(c->aux_ev);
     }
     cudaStreamDestroy(c->own);
     delete c;

@@ -38,27 +38,55 @@
 namespace cpcag_cuda {
 
 // ------------------------------------------------------------------ the solver
+// The operator plans of one decode: pulls of L_r / L_c in the value type
+// and the apply plans of the CG (TK iterates) and of the true residual (TX).
 template <typename TX, typename TK, typename TV>
-void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* Lr, Csr* Lc, double gbar_r,
-                 double gbar_c, const Plan& pl, const cpcag_decoder_config& cfg, TX* X, int* converged,
-                 i64* iterations) {
-  const i64 N = p * n;
-  const Pull<TV> pr = make_pull<TV>(c, Lr, false), pc = make_pull<TV>(c, Lc, true);
+struct DecodePrep : DecodePrepBase {
+  Pull<TV> pr{}, pc{};
+  ApplyPlan apK, apX;
+  i64 p = 0, n = 0;
+  const Csr* Lr = nullptr;
+  const Csr* Lc = nullptr;
+};
+
+template <typename TX, typename TK, typename TV>
+void decode_prepare(Ctx* c, i64 p, i64 n, Csr* Lr, Csr* Lc, DecodePrep<TX, TK, TV>& d) {
+  d.pr = make_pull<TV>(c, Lr, false);
+  d.pc = make_pull<TV>(c, Lc, true);
   std::vector<i64> rpr;
   std::vector<int> cir;
   std::vector<TV> vr;
-  host_pull<TV>(c, pr, p, Lr->nnz, rpr, cir, &vr);
-  ApplyPlan apK, apX;
+  host_pull<TV>(c, d.pr, p, Lr->nnz, rpr, cir, &vr);
   const bool exact = sizeof(TX) == 8;
   HostPull<TV> lcp;
-  host_pull<TV>(c, pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
+  host_pull<TV>(c, d.pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
   trace_mark(c, "decode: operator copies");
-  plan_apply<TK, TK, TV>(c, apK, p, n, n, 0, rpr, cir, vr, exact, &lcp);
+  plan_apply<TK, TK, TV>(c, d.apK, p, n, n, 0, rpr, cir, vr, exact, &lcp);
   trace_mark(c, "decode: plan K");
-  constexpr bool same_plan = std::is_same<TX, TK>::value;  // the true residual reuses the CG's operator plan
-  if constexpr (!same_plan) plan_apply<TX, TK, TV>(c, apX, p, n, n, 0, rpr, cir, vr, exact, &lcp);
-  const ApplyPlan& apR = same_plan ? apK : apX;
+  // the true residual reuses the CG's operator plan when X and the iterates share a type
+  if constexpr (!std::is_same<TX, TK>::value) plan_apply<TX, TK, TV>(c, d.apX, p, n, n, 0, rpr, cir, vr, exact, &lcp);
   trace_mark(c, "decode: plans");
+  d.p = p;
+  d.n = n;
+  d.Lr = Lr;
+  d.Lc = Lc;
+}
+
+template <typename TX, typename TK, typename TV>
+void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* Lr, Csr* Lc, double gbar_r,
+                 double gbar_c, const Plan& pl, const cpcag_decoder_config& cfg, TX* X, int* converged,
+                 i64* iterations, DecodePrepBase* prep_in) {
+  const i64 N = p * n;
+  auto* prep = dynamic_cast<DecodePrep<TX, TK, TV>*>(prep_in);
+  DecodePrep<TX, TK, TV> local;
+  if (!prep || prep->p != p || prep->n != n || prep->Lr != Lr || prep->Lc != Lc) {
+    decode_prepare<TX, TK, TV>(c, p, n, Lr, Lc, local);
+    prep = &local;
+  }
+  const Pull<TV> pr = prep->pr, pc = prep->pc;
+  constexpr bool same_plan = std::is_same<TX, TK>::value;
+  const ApplyPlan& apK = prep->apK;
+  const ApplyPlan& apR = same_plan ? prep->apK : prep->apX;
   DevBuf<TK> R(c, N), P(c, N), AP(c, N), U(c, N);
   DevBuf<CgState> st(c, 1);
   st.zero(c);
@@ -129,7 +157,7 @@ template <typename T>
 void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i64* om_r_host,
                              const i64* om_c_host, i64 p, i64 n, Csr* Lr, Csr* Lc, double lk1_r,
                              double lk1_c, const cpcag_decoder_config& cfg, T* X, int* converged,
-                             i64* iterations) {
+                             i64* iterations, DecodePrepBase* prep) {
   if (Lr->rows != p || Lc->rows != n || Lr->cols != p || Lc->cols != n)
     invalid("alternate decoder: Laplacians do not match plan");
   if (cfg.gamma <= 0.0) invalid("alternate decoder: gamma must be positive");
@@ -173,23 +201,48 @@ void alternate_decode_device(Ctx* c, const T* Xt, i64 rho_r, i64 rho_c, const i6
   const Plan pl{rsel.p, csel.p, rho_r};
   if constexpr (sizeof(T) == 8) {
     decode_impl<double, double, double>(c, Xt, rho_r, rho_c, p, n, Lr, Lc, gbar_r, gbar_c, pl, cfg, X, converged,
-                                        iterations);
+                                        iterations, prep);
   } else {
     if (cfg.krylov_precision == CPCAG_F32)
       decode_impl<float, float, float>(c, Xt, rho_r, rho_c, p, n, Lr, Lc, gbar_r, gbar_c, pl, cfg, X, converged,
-                                       iterations);
+                                       iterations, prep);
     else
       decode_impl<float, double, float>(c, Xt, rho_r, rho_c, p, n, Lr, Lc, gbar_r, gbar_c, pl, cfg, X, converged,
-                                        iterations);
+                                        iterations, prep);
   }
 }
 
 template void alternate_decode_device<double>(Ctx*, const double*, i64, i64, const i64*, const i64*, i64, i64,
                                               Csr*, Csr*, double, double, const cpcag_decoder_config&,
-                                              double*, int*, i64*);
+                                              double*, int*, i64*, DecodePrepBase*);
 template void alternate_decode_device<float>(Ctx*, const float*, i64, i64, const i64*, const i64*, i64, i64,
                                              Csr*, Csr*, double, double, const cpcag_decoder_config&,
-                                             float*, int*, i64*);
+                                             float*, int*, i64*, DecodePrepBase*);
+
+// The plans alternate_decode_device<T> will use, built now (same type
+// selection); null when the shapes leave nothing to plan.
+template <typename T>
+std::unique_ptr<DecodePrepBase> alternate_decode_prepare(Ctx* c, i64 p, i64 n, Csr* Lr, Csr* Lc,
+                                                         const cpcag_decoder_config& cfg) {
+  if (Lr->rows != p || Lc->rows != n || Lr->cols != p || Lc->cols != n || p * n == 0) return nullptr;
+  if (p > INT32_MAX / 2 || n > INT32_MAX / 2) return nullptr;
+  auto make = [&](auto* tag) -> std::unique_ptr<DecodePrepBase> {
+    using D = std::remove_pointer_t<decltype(tag)>;
+    auto d = std::make_unique<D>();
+    decode_prepare(c, p, n, Lr, Lc, *d);
+    return d;
+  };
+  if constexpr (sizeof(T) == 8) {
+    return make(static_cast<DecodePrep<double, double, double>*>(nullptr));
+  } else {
+    if (cfg.krylov_precision == CPCAG_F32) return make(static_cast<DecodePrep<float, float, float>*>(nullptr));
+    return make(static_cast<DecodePrep<float, double, float>*>(nullptr));
+  }
+}
+template std::unique_ptr<DecodePrepBase> alternate_decode_prepare<double>(Ctx*, i64, i64, Csr*, Csr*,
+                                                                          const cpcag_decoder_config&);
+template std::unique_ptr<DecodePrepBase> alternate_decode_prepare<float>(Ctx*, i64, i64, Csr*, Csr*,
+                                                                         const cpcag_decoder_config&);
 
 }  // namespace cpcag_cuda
 

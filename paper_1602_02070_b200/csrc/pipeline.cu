@@ -116,6 +116,22 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     Lc_s->sym = 1;
   });
 
+  // The decoder's operator planning (host work, ~1 ms at config 1) runs
+  // while the device iterates the spectral norms of the solve stage; the
+  // decode stage builds the plans itself if that did not happen.
+  const bool want_x = cfg.task != CPCAG_TASK_CLUSTER;
+  std::unique_ptr<DecodePrepBase> dprep;
+  IdleWorkScope idle_scope(c);
+  if (want_x && !full && cfg.decoder_variant == CPCAG_DECODER_ALTERNATE)
+    c->idle_work = [&] {
+      try {
+        dprep = alternate_decode_prepare<T>(c, p, n, Lr.get(), Lc.get(), cfg.decoder);
+      } catch (const Error& e) {
+        if (e.status == CPCAG_ERR_CUDA) throw;
+        dprep.reset();  // the decode stage plans again and reports the error there
+      }
+    };
+
   rep->stage_ms[4] = tm.run("solve", [&] {
     fista_device<T>(c, Yt.p, rho_r, rho_c, Lr_s.get(), Lc_s.get(), cfg.frpcag, Xt_out, objective, &rep->trace);
   });
@@ -152,8 +168,8 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
   rep->has_factors = 0;
   rep->factors_k = 0;
 
-  const bool want_x = cfg.task != CPCAG_TASK_CLUSTER;
   if (want_x) rep->stage_ms[5] = tm.run("decode", [&] {
+    run_idle_work(c);
     if (full) {
       // pipeline.cpp:327-337: no compression, scatter back through the plan.
       dim3 g(blocks_for(rho_r), static_cast<unsigned>(std::min<i64>(rho_c, 65535)));
@@ -209,7 +225,7 @@ void run_pipeline_device(Ctx* c, const T* Y, i64 p, i64 n, Csr* Wr, Csr* Wc, con
     int conv = 0;
     i64 it = 0;
     alternate_decode_device<T>(c, Xt_out, rho_r, rho_c, om_r.data(), om_c.data(), p, n, Lr.get(), Lc.get(), lk1_r,
-                               lk1_c, cfg.decoder, X_out, &conv, &it);
+                               lk1_c, cfg.decoder, X_out, &conv, &it, dprep.get());
     rep->decoder_converged = conv;
     rep->decoder_iterations = it;
   });
