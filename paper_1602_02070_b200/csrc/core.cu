@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       acc = warp_sum(acc);
       if (lane == 0) w[r] = acc;
     }
-    grid_barrier_local(&st->bar_count, &st->bar_gen, bar_g);
+    grid_barrier_mono(&st->bar_count, bar_g);
     // ||w||^2 straight from w, which every CTA reads anyway: one L2 round
     // trip per iteration instead of two (partials, then w).  Same data and
     // the same fixed-order block reduction in every CTA, so every CTA gets
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
       ++it;
       break;
     }
-    if (!v_in_smem) grid_barrier_local(&st->bar_count, &st->bar_gen, bar_g);
+    if (!v_in_smem) grid_barrier_mono(&st->bar_count, bar_g);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     st->est = est;

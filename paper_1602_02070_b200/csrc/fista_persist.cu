@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
 
   unsigned bar_g = 0;  // grid barriers passed (a.bar is zeroed before the launch)
   // ---- H(Y): Z_1 = S_0 = Y, so H(Z_1) = H(S_0)
-  grid_barrier_local(&a.bar[0], &a.bar[1], bar_g);
+  grid_barrier_mono(&a.bar[0], bar_g);
   tile_gemm(a.Sg[0], a.SgT[0]);
   for (int e = tid; e < TE; e += kPT) {
     const float h = tile_h(e);
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(MODE == 0 ? 256 : 512, 1) fista_persist_k(cons
       }
     }
     mark(0);
-    grid_barrier_local(&a.bar[0], &a.bar[1], bar_g);
+    grid_barrier_mono(&a.bar[0], bar_g);
     mark(1);
     // partial sums of iteration j-1: cp.async (L2 -> shared, bypassing L1)
     // issued now, joining the GEMM's first copy group, consumed after the
