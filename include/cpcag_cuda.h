@@ -87,6 +87,13 @@ int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path);
 /* Test hook: the persistent FISTA kernel's tile GEMM, 0 = automatic (fp64
  * tensor cores, DMMA, when the tiling fits), 1 = SIMT fp64 multiply-adds. */
 int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path);
+/* Test hook: the cooperative power iteration (operators too large for one
+ * CTA), 0 = automatic (two products per grid barrier through the dense square
+ * of the operator when a CTA's rows of it fit in shared memory), 1 = always
+ * one product per barrier.  last_power_path: 2 / 1 as above for the most
+ * recent power iteration, 0 when it ran in the single-CTA kernel. */
+int cpcag_ctx_set_power_path(cpcag_ctx ctx, int path);
+int cpcag_ctx_last_power_path(cpcag_ctx ctx);
 /* The path (1, 2 or 3 as above) the most recently planned decoder operator
  * took; 0 before any. */
 int cpcag_ctx_last_apply_path(cpcag_ctx ctx);

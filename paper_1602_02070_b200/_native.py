@@ -120,6 +120,8 @@ SIGNATURES = {
     "cpcag_ctx_set_apply_path": (C.c_int, [vp, C.c_int]),
     "cpcag_ctx_last_apply_path": (C.c_int, [vp]),
     "cpcag_ctx_set_fista_path": (C.c_int, [vp, C.c_int]),
+    "cpcag_ctx_set_power_path": (C.c_int, [vp, C.c_int]),
+    "cpcag_ctx_last_power_path": (C.c_int, [vp]),
     "cpcag_cuda_thin_svd": (C.c_int, [vp, vp, i64, i64, vp, vp, vp]),
     "cpcag_cuda_sym_eig": (C.c_int, [vp, vp, i64, vp, vp]),
     "cpcag_cuda_sym_eigvals_lanczos": (C.c_int, [vp, vp, i64, C.c_double, i64, C.c_uint64, vp, vp]),

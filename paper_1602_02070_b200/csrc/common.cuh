@@ -87,6 +87,8 @@ struct Ctx {
   int apply_path = 0;         // decoder operator: 0 auto, 1 two passes, 2 fused, 3 slab (tests)
   int last_apply_path = 0;    // the path the last planned operator took (1, 2 or 3; tests)
   int fista_simt = 0;         // 1: the persistent FISTA kernel's SIMT tile GEMM instead of DMMA (tests)
+  int power_path = 0;         // cooperative power iteration: 0 auto, 1 one product per barrier (tests)
+  int last_power_path = 0;    // 1 one product, 2 two products per barrier; 0 single-CTA kernel or none (tests)
   cudaStream_t side = nullptr;  // second stream for independent work (lazily created)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
   // Host work deferred to the next long device wait (run_idle_work): it runs

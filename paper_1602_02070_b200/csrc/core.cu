@@ -598,12 +598,174 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   }
 }
 
+// Two products per grid barrier for operators whose square fits beside them:
+// with A2 = A A (dense, built once), one round forms w1 = A v and w2 = A2 v
+// from the same v.  ||w1|| is the reference's estimate of this iteration; the
+// next iterate would be v' = w1 / ||w1||, so A v' = w2 / ||w1|| and the next
+// estimate is ||w2|| / ||w1||, the iterate after it w2 / ||w2||
+// (solvers.cpp:43-51 twice, both stop tests in order).  The barrier and the
+// L2 round trip of w are paid once per two reference iterations; estimates
+// agree with the one-product form to rounding (~1e-15 relative).
+__global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __restrict__ rp,
+                                                          const int* __restrict__ ci,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ A2, i64 ld,
+                                                          const double* __restrict__ v0, double* wbuf, double tol,
+                                                          i64 max_iter, PowerState* st) {
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned nb = gridDim.x;
+  const i64 r0 = (n * blockIdx.x) / nb, r1 = (n * (blockIdx.x + 1)) / nb;
+  const int nr = static_cast<int>(r1 - r0);
+  const i64 k0 = rp[r0], k1 = rp[r1];
+  double* vs = sm;                     // n
+  double* a2s = vs + n;                // nr x n, the CTA's rows of A2
+  double* sval = a2s + static_cast<i64>(nr) * n;
+  int* sci = reinterpret_cast<int*>(sval + (k1 - k0));
+  for (i64 k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+    sval[k - k0] = val[k];
+    sci[k - k0] = ci[k];
+  }
+  for (i64 q = threadIdx.x; q < static_cast<i64>(nr) * n; q += blockDim.x) {
+    const i64 r = q / n, j = q - r * n;
+    a2s[q] = A2[(r0 + r) * ld + j];
+  }
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
+  __syncthreads();
+  double est = 0.0;
+  i64 it = 0;
+  unsigned bar_g = 0, round = 0;
+  while (it < max_iter) {
+    double* w1 = wbuf + (round & 1) * 2 * n;
+    double* w2 = w1 + n;
+    ++round;
+    for (int task = wid; task < 2 * nr; task += nw) {
+      double a0 = 0.0, a1 = 0.0;
+      if (task < nr) {
+        const i64 ra = rp[r0 + task] - k0, rb = rp[r0 + task + 1] - k0;
+        i64 k = ra + lane;
+        for (; k + 32 < rb; k += 64) {
+          a0 += sval[k] * vs[sci[k]];
+          a1 += sval[k + 32] * vs[sci[k + 32]];
+        }
+        if (k < rb) a0 += sval[k] * vs[sci[k]];
+        a0 = warp_sum(a0 + a1);
+        if (lane == 0) w1[r0 + task] = a0;
+      } else {
+        const double* row = a2s + static_cast<i64>(task - nr) * n;
+        i64 j = lane;
+        for (; j + 32 < n; j += 64) {
+          a0 += row[j] * vs[j];
+          a1 += row[j + 32] * vs[j + 32];
+        }
+        if (j < n) a0 += row[j] * vs[j];
+        a0 = warp_sum(a0 + a1);
+        if (lane == 0) w2[r0 + task - nr] = a0;
+      }
+    }
+    grid_barrier_mono(&st->bar_count, bar_g);
+    // every CTA reads all of w1 and w2 and reduces in the same fixed order
+    double t[2] = {0.0, 0.0};
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
+      const double x1 = __ldcg(w1 + i), x2 = __ldcg(w2 + i);
+      vs[i] = x2;
+      t[0] += x1 * x1;
+      t[1] += x2 * x2;
+    }
+    block_sum<2>(t);
+    const double n1 = sqrt(t[0]);
+    if (n1 == 0.0) {
+      est = 0.0;
+      break;
+    }
+    double prev = est;
+    est = n1;
+    ++it;
+    if ((it > 1 && fabs(est - prev) <= tol * est) || it >= max_iter) break;
+    const double n2 = sqrt(t[1]);
+    if (n2 == 0.0) {  // A v' = 0: the reference returns 0
+      est = 0.0;
+      ++it;
+      break;
+    }
+    prev = est;
+    est = __ddiv_rn(n2, n1);
+    ++it;
+    if (fabs(est - prev) <= tol * est) break;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(vs[i], n2);
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->est = est;
+    st->iterations = it;
+  }
+}
+
+// Dense copy of a CSR matrix into a zeroed ld x ld row-major array.
+__global__ void csr_to_dense_k(i64 n, const i64* __restrict__ rp, const int* __restrict__ ci,
+                               const double* __restrict__ val, i64 ld, double* __restrict__ D) {
+  const int lane = threadIdx.x & 31;
+  const i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  if (r >= n) return;
+  for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) D[r * ld + ci[k]] = val[k];
+}
+
+// C = A A for a dense row-major ld x ld array (ld a multiple of 64, zero
+// padded): 64 x 64 tile per CTA, 4 x 4 per thread, k ascending (each entry of
+// C is one fixed-order fp64 FMA chain).
+__global__ void __launch_bounds__(256) dense_square_k(int ld, const double* __restrict__ A, double* __restrict__ C) {
+  __shared__ double As[16][64 + 4];
+  __shared__ __align__(16) double Bs[16][64];
+  const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) acc[u][w] = 0.0;
+  const int ai = t >> 2, ak = (t & 3) * 4;   // A tile: 64 rows x 16 k
+  const int bk = t >> 4, bj = (t & 15) * 4;  // B tile: 16 k x 64 columns
+  for (int kk = 0; kk < ld; kk += 16) {
+    const double2 x0 = *reinterpret_cast<const double2*>(A + static_cast<i64>(i0 + ai) * ld + kk + ak);
+    const double2 x1 = *reinterpret_cast<const double2*>(A + static_cast<i64>(i0 + ai) * ld + kk + ak + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(A + static_cast<i64>(kk + bk) * ld + j0 + bj);
+    const double2 y1 = *reinterpret_cast<const double2*>(A + static_cast<i64>(kk + bk) * ld + j0 + bj + 2);
+    __syncthreads();
+    As[ak][ai] = x0.x;
+    As[ak + 1][ai] = x0.y;
+    As[ak + 2][ai] = x1.x;
+    As[ak + 3][ai] = x1.y;
+    *reinterpret_cast<double2*>(&Bs[bk][bj]) = y0;
+    *reinterpret_cast<double2*>(&Bs[bk][bj + 2]) = y1;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a[u] = As[k][ty * 4 + u];
+      const double2 b0 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4]);
+      const double2 b1 = *reinterpret_cast<const double2*>(&Bs[k][tx * 4 + 2]);
+      b[0] = b0.x, b[1] = b0.y, b[2] = b1.x, b[3] = b1.y;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[u][w] = fma(a[u], b[w], acc[u][w]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    double* out = C + static_cast<i64>(i0 + ty * 4 + u) * ld + j0 + tx * 4;
+    *reinterpret_cast<double2*>(out) = make_double2(acc[u][0], acc[u][1]);
+    *reinterpret_cast<double2*>(out + 2) = make_double2(acc[u][2], acc[u][3]);
+  }
+}
+
 // One power iteration, set up and launched on `s` (the host work -- start
 // vector, geometry -- happens now; the result lands in st->est).  Returns
 // false when there is nothing to launch (st->est is then set on the host:
 // n == 0, ||v0|| == 0 or max_iter <= 0 give 0).
 struct PowerJob {
-  DevBuf<double> v, w, part;
+  DevBuf<double> v, w, part, dense, sq;
   DevBuf<PowerState> st;
   double host_est = 0.0;
   bool launched = false;
@@ -614,6 +776,7 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
                           bool timed) {
   if (A->rows != A->cols) invalid("power iteration: square matrix required");
   const i64 n = A->rows;
+  c->last_power_path = 0;
   if (n == 0) return;
   HostRng rng(HostRng::mix(seed ^ 0x5ca1ab1eULL));
   std::vector<double> v0(static_cast<size_t>(n));
@@ -668,6 +831,50 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
   size_t smem = v_in_smem ? static_cast<size_t>(n) * 8 : 0;
   int slice_in_smem = smem + static_cast<size_t>(max_slice) * 12 + 16 <= budget ? 1 : 0;
   if (slice_in_smem) smem += static_cast<size_t>(max_slice) * 12 + 16;
+  // two products per barrier when the CTA's rows of A A fit beside its slice
+  if (s == c->stream && v_in_smem && slice_in_smem && c->power_path != 1) {
+    const i64 rows_max = (n + nb - 1) / nb;
+    const i64 ld = ((n + 63) / 64) * 64;
+    const size_t smem2 = static_cast<size_t>(n) * 8 + static_cast<size_t>(rows_max) * n * 8 +
+                         static_cast<size_t>(max_slice) * 12 + 16;
+    if (smem2 <= budget && ld * ld * 8 <= (i64{64} << 20) && max_iter >= 2) {
+      job.dense.alloc(c, static_cast<size_t>(ld * ld));
+      job.sq.alloc(c, static_cast<size_t>(ld * ld));
+      job.dense.zero(c);
+      job.w.alloc(c, 4 * n);
+      ensure_smem(power_iter_coop2_k, smem2);
+      int fit = 0;
+      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coop2_k, 512, smem2));
+      if (fit < 1) invalid("power iteration: kernel does not fit on an SM");
+      const i64* rp = A->rp;
+      const int* ci = A->ci;
+      const double* val = A->v;
+      const double* a2 = job.sq.p;
+      const double* vp = job.v.p;
+      double* wp = job.w.p;
+      PowerState* sp = job.st.p;
+      i64 nn = n, ldd = ld;
+      void* args[] = {(void*)&nn, (void*)&rp, (void*)&ci, (void*)&val, (void*)&a2, (void*)&ldd, (void*)&vp,
+                      (void*)&wp, (void*)&tol, (void*)&max_iter, (void*)&sp};
+      job.launched = true;
+      auto go = [&] {
+        csr_to_dense_k<<<blocks_for(n * 32), kBlock, 0, s>>>(n, rp, ci, val, ld, job.dense.p);
+        const unsigned gt = static_cast<unsigned>(ld / 64);
+        dense_square_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.dense.p, job.sq.p);
+        CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop2_k, dim3(nb), dim3(512), args, smem2, s));
+      };
+      if (timed) {
+        KScope ks_(c, "power_iter");
+        go();
+      } else {
+        go();
+      }
+      launched(c);
+      c->last_power_path = 2;
+      return;
+    }
+  }
+  c->last_power_path = 1;
   ensure_smem(power_iter_coop_k, smem);
   int per_sm = 0;
   CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, power_iter_coop_k, 512, smem));
@@ -957,6 +1164,15 @@ int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path) {
     as_ctx(ctx)->fista_simt = path;
   });
 }
+
+int cpcag_ctx_set_power_path(cpcag_ctx ctx, int path) {
+  return guard([&] {
+    if (path < 0 || path > 1) invalid("power path must be 0 or 1");
+    as_ctx(ctx)->power_path = path;
+  });
+}
+
+int cpcag_ctx_last_power_path(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->last_power_path : -1; }
 
 int cpcag_ctx_last_apply_path(cpcag_ctx ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->last_apply_path : -1; }
 

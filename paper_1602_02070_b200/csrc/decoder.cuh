@@ -1024,7 +1024,7 @@ __device__ __forceinline__ double residual_loop(i64 N, TK* __restrict__ R, const
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         r[u] = Rv[q + u * ts];
-        a[u] = Av[q + u * ts];
+        a[u] = __ldcs(Av + q + u * ts);  // AP is dead after this pass: evict-first
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1039,7 +1039,7 @@ __device__ __forceinline__ double residual_loop(i64 N, TK* __restrict__ R, const
     }
     for (; q < nv; q += ts) {
       V r = Rv[q];
-      const V a = Av[q];
+      const V a = __ldcs(Av + q);
 #pragma unroll
       for (int k = 0; k < W; ++k) {
         TK& x = lane_of<TK>(r, k);
@@ -1079,26 +1079,31 @@ __device__ __forceinline__ void update_loop(i64 N, TX* __restrict__ X, TK* __res
       }
     };
     i64 q = t0;
+    // X is touched by this pass only: streamed (evict-first) loads and stores,
+    // so the L2 keeps R, P and AP for the passes that share them (config 1:
+    // 3 x 41 MB of Krylov vectors against 126 MB of L2)
+    auto ldx = [&](i64 k) { return __ldcs(Xv + k); };
+    auto stx = [&](i64 k, const V& v) { __stcs(Xv + k, v); };
     for (; q + 3 * ts < nv; q += 4 * ts) {  // four 16-byte triples in flight per thread
       V x[4], pv[4], r[4], pn[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        x[u] = Xv[q + u * ts];
+        x[u] = ldx(q + u * ts);
         pv[u] = Pv[q + u * ts];
         r[u] = Rv[q + u * ts];
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         one(x[u], pv[u], r[u], pn[u]);
-        Xv[q + u * ts] = x[u];
+        stx(q + u * ts, x[u]);
         Pv[q + u * ts] = pn[u];
       }
     }
     for (; q < nv; q += ts) {
-      V x = Xv[q], pv = Pv[q], pn;
+      V x = ldx(q), pv = Pv[q], pn;
       const V r = Rv[q];
       one(x, pv, r, pn);
-      Xv[q] = x;
+      stx(q, x);
       Pv[q] = pn;
     }
     from = nv * W;
@@ -1472,7 +1477,9 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
   const size_t band_bytes = static_cast<size_t>(n_local) * 128;
   ap.lc_smem = band_bytes + lc_smem_ent_bytes<TI, TV>() <= 220 * 1024;
   ap.lc_smem_bytes = std::max<size_t>(band_bytes, 16);
-  ap.lc_cpc = 8 * 32;  // L2 mode: 8 warps x 32 columns (one row-pointer load per warp)
+  // L2 mode: a band's chunks fill one wave of resident CTAs (4 per SM), so the
+  // CTAs in flight gather from one band (<= 51 MB) rather than straddling two
+  ap.lc_cpc = static_cast<int>(std::max<i64>(64, (ncols + static_cast<i64>(c->num_sms) * 4 - 1) / (static_cast<i64>(c->num_sms) * 4)));
   ap.lc_chunks = static_cast<int>(std::max<i64>(1, (ncols + ap.lc_cpc - 1) / ap.lc_cpc));
   // row order: degree-sorted when natural warps would pad the rows > 30 %
   std::vector<int> deg(static_cast<size_t>(p));
@@ -1569,6 +1576,64 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
             }
           }
         }
+      // Bank-aware entry order (fp32 data; fp64 data keeps the CSR order for
+      // bit parity).  Step e of a warp is one shared-memory gather: the lanes
+      // of a phase (128 bytes of requests: 8 lanes of 16-byte records, 16 of
+      // 8-byte) read records of unrelated rows, and every extra distinct
+      // record in one bank group is another wavefront (measured ~2.8 per
+      // ideal one with the entries in CSR order).  The entries of a vrow may
+      // be summed in any order here, so each lane's entries are dealt to the
+      // steps greedily -- at every step a lane takes, among the entries it
+      // has left, the one whose bank group is least loaded in its phase.
+      if (!exact) {
+        const int rb = C * static_cast<int>(sizeof(TI));       // record bytes
+        const int aw = std::min(rb, 16);                        // bytes per shared load
+        const int phase = 128 / aw;                             // lanes served by one wavefront
+        const int ngr = 128 / aw;                               // bank groups
+        auto group_of = [&](int j) { return ((static_cast<i64>(j) * rb) % 128) / aw; };
+        std::vector<int> load(static_cast<size_t>(ngr));
+        std::vector<std::vector<int>> seen(static_cast<size_t>(ngr));
+        std::vector<unsigned char> used(static_cast<size_t>(32) * EV);
+        for (size_t g = 0; g < grp.size(); ++g)
+          for (int w0 = 0; w0 < T; w0 += 32) {
+            std::fill(used.begin(), used.end(), 0);
+            // the warp's entries, before reordering
+            std::vector<TV> ov(static_cast<size_t>(32) * EV);
+            std::vector<int> oj(static_cast<size_t>(32) * EV);
+            for (int l = 0; l < 32; ++l)
+              for (int e = 0; e < EV; ++e) {
+                const size_t at = (g * EV + e) * static_cast<size_t>(T) + w0 + l;
+                ov[l * EV + e] = hv[at];
+                oj[l * EV + e] = hj[at];
+              }
+            for (int e = 0; e < EV; ++e)
+              for (int ph = 0; ph < 32; ph += phase) {
+                std::fill(load.begin(), load.end(), 0);
+                for (auto& sj : seen) sj.clear();
+                for (int l = ph; l < ph + phase; ++l) {
+                  int best = -1, best_cost = INT32_MAX;
+                  for (int x = 0; x < EV; ++x) {
+                    if (used[l * EV + x]) continue;
+                    const int j = oj[l * EV + x];
+                    const int gq = static_cast<int>(group_of(j));
+                    const bool dup = std::find(seen[gq].begin(), seen[gq].end(), j) != seen[gq].end();
+                    const int cost = dup ? -1 : load[gq];
+                    if (cost < best_cost) best_cost = cost, best = x;
+                  }
+                  used[l * EV + best] = 1;
+                  const int j = oj[l * EV + best];
+                  const int gq = static_cast<int>(group_of(j));
+                  if (std::find(seen[gq].begin(), seen[gq].end(), j) == seen[gq].end()) {
+                    seen[gq].push_back(j);
+                    ++load[gq];
+                  }
+                  const size_t at = (g * EV + e) * static_cast<size_t>(T) + w0 + l;
+                  hv[at] = ov[l * EV + best];
+                  hj[at] = j;
+                }
+              }
+          }
+      }
       ap.groups.alloc(c, grp.size());
       ap.vrow_row.alloc(c, vrow_row.size());
       ap.vrow_np.alloc(c, vrow_np.size());

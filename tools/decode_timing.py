@@ -45,15 +45,21 @@ if "cfg3" in which:
     Xt = workloads.config3_rhs(P, gr.laplacian, gc.laplacian, plan, ctx)
     g1 = P.SpectralGap(lambda_k1=1.0)
     out = {}
-    for name, xt, kp in [("f32/krylov64", Xt.float().t().contiguous().t(), "fp64"),
-                         ("f32/krylov32", Xt.float().t().contiguous().t(), "fp32"),
-                         ("f64", Xt, "fp64")]:
+    variants = [("f32/krylov64", Xt.float().t().contiguous().t(), "fp64"),
+                ("f32/krylov32", Xt.float().t().contiguous().t(), "fp32"),
+                ("f64", Xt, "fp64")]
+    only = os.environ.get("VARIANTS")
+    if only:
+        variants = [v for v in variants if v[0] in only.split(",")]
+    for name, xt, kp in variants:
         cfg = P.DecoderConfig(1.0, 1e-30, 100, krylov_precision=kp)
         ms, kt, r = timed(lambda: P.alternate_decode(xt, plan, gr.laplacian, gc.laplacian, g1, g1, cfg, ctx=ctx))
         out[name] = r.X.double()
         print(f"cfg3 {name}: {ms:.1f} ms ({ms / 100:.2f} ms/it) kernels {kt}", flush=True)
         del r
     for k in ("f32/krylov64", "f32/krylov32"):
+        if k not in out or "f64" not in out:
+            continue
         d = float(torch.linalg.norm(out[k] - out["f64"]) / torch.linalg.norm(out["f64"]))
         print(f"cfg3 {k} vs f64: {d:.3e}", flush=True)
     del out, gr, gc, Xt
