@@ -141,6 +141,32 @@ inline void launched(Ctx* c) {
   CUDA_OK(cudaGetLastError());
 }
 
+// Programmatic dependent launch.  A kernel launched with launch_pdl may be
+// scheduled while its predecessor on the stream still runs (once every CTA of
+// the predecessor has called pdl_trigger or exited); it must call pdl_wait
+// before touching anything the predecessor writes -- the wait returns when the
+// predecessor has completed and its writes are visible.  Back-to-back short
+// kernels (the decoder's three per CG iteration) overlap their launch latency
+// and CTA ramp-up with the predecessor's tail this way.  Both calls are no-ops
+// in a kernel launched the ordinary way.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CUDA_OK(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
+
 // Stream-ordered device buffer.
 template <typename T>
 struct DevBuf {

@@ -212,7 +212,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
       {
         KScope ks_(c, "cg_residual");
         if (vecK)
-          cg_residual_k<TK, true><<<nbw, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
+          launch_pdl(cg_residual_k<TK, true>, dim3(nbw), dim3(kBlock), 0, c->stream, N, R.p, AP.p, part.p, st.p);
         else
           cg_residual_k<TK, false><<<nbv, kBlock, 0, c->stream>>>(N, R.p, AP.p, part.p, st.p);
         launched(c);
@@ -220,7 +220,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
       {
         KScope ks_(c, "cg_update");
         if (vecU)
-          cg_update_k<TK, TX, true><<<nbw, kBlock, 0, c->stream>>>(N, X, P.p, R.p, st.p);
+          launch_pdl(cg_update_k<TK, TX, true>, dim3(nbw), dim3(kBlock), 0, c->stream, N, X, P.p, R.p, st.p);
         else
           cg_update_k<TK, TX, false><<<nbv, kBlock, 0, c->stream>>>(N, X, P.p, R.p, st.p);
         launched(c);

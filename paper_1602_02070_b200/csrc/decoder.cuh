@@ -269,6 +269,8 @@ __device__ __forceinline__ int4 lds_i128(unsigned a) {
 template <typename TK, int EVR, bool kResid, typename TB, bool O32 = false>
 __global__ void __launch_bounds__(kSlabThreads, 1) slab_k(int p, int n, int parts, SlabPlan sp,
                                                            const float* __restrict__ P, Combine<TK, TB> cb) {
+  pdl_wait();  // P and the solver state come from the previous kernel on the stream
+  pdl_trigger();
   if (cb.st && cb.st->done) return;
   auto colp = [p](int c) -> i64 {
     if constexpr (O32)
@@ -1156,6 +1158,8 @@ __device__ __forceinline__ bool cg_breakdown(CgState* st) {
 template <typename TK, bool kVec>
 __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ AP, double* partials,
                               CgState* st) {
+  pdl_wait();
+  pdl_trigger();
   if (st->done || cg_breakdown(st)) return;
   const TK alpha = static_cast<TK>(st->rho / st->curv);
   double s[1] = {residual_loop<TK, kVec>(N, R, AP, alpha)};
@@ -1167,6 +1171,8 @@ __global__ void cg_residual_k(i64 N, TK* __restrict__ R, const TK* __restrict__ 
 // advances the iteration and applies the loop-top stop test.
 template <typename TK, typename TX, bool kVec>
 __global__ void cg_update_k(i64 N, TX* __restrict__ X, TK* __restrict__ P, const TK* __restrict__ R, CgState* st) {
+  pdl_wait();
+  pdl_trigger();
   if (st->done) return;
   const TK alpha = static_cast<TK>(st->rho / st->curv);
   const TK beta = static_cast<TK>(st->rho_next / st->rho);
@@ -1477,9 +1483,7 @@ void plan_apply(Ctx* c, ApplyPlan& ap, i64 p, i64 ncols, i64 n_local, i64 col_ba
   const size_t band_bytes = static_cast<size_t>(n_local) * 128;
   ap.lc_smem = band_bytes + lc_smem_ent_bytes<TI, TV>() <= 220 * 1024;
   ap.lc_smem_bytes = std::max<size_t>(band_bytes, 16);
-  // L2 mode: a band's chunks fill one wave of resident CTAs (4 per SM), so the
-  // CTAs in flight gather from one band (<= 51 MB) rather than straddling two
-  ap.lc_cpc = static_cast<int>(std::max<i64>(64, (ncols + static_cast<i64>(c->num_sms) * 4 - 1) / (static_cast<i64>(c->num_sms) * 4)));
+  ap.lc_cpc = 8 * 32;  // L2 mode: 8 warps x 32 columns (one row-pointer load per warp)
   ap.lc_chunks = static_cast<int>(std::max<i64>(1, (ncols + ap.lc_cpc - 1) / ap.lc_cpc));
   // row order: degree-sorted when natural warps would pad the rows > 30 %
   std::vector<int> deg(static_cast<size_t>(p));
@@ -1803,8 +1807,8 @@ void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const T
       const SlabPlan sp{ap.s_rec.p,  reinterpret_cast<const SlabStep*>(ap.s_steps.p), ap.s_wsteps.p, ap.s_max_steps,
                         ap.s_win.p, ap.s_lv.p, ap.s_lo.p};
       const unsigned grid = static_cast<unsigned>(ap.s_grid);  // persistent, one CTA per SM
-      k<<<grid, kSlabThreads, ap.s_smem, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols), ap.s_parts,
-                                                     sp, P, cb);
+      launch_pdl(k, dim3(grid), dim3(kSlabThreads), ap.s_smem, c->stream, static_cast<int>(ap.p),
+                 static_cast<int>(ap.ncols), ap.s_parts, sp, P, cb);
       launched(c);
       return;
     }
