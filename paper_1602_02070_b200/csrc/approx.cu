@@ -475,6 +475,7 @@ void rank_job_start(Ctx* c, RankJob& job, const double* Xt64, i64 m, i64 n, cuda
   CUDA_OK(cudaEventRecord(c->join_ev, s));
   job.side = s;
   job.running = true;
+  c->side_job_running = true;
 }
 
 // Joins the job (the main stream waits for the side stream) and returns the
@@ -485,6 +486,8 @@ std::vector<double> rank_job_finish(Ctx* c, RankJob& job) {
   CUDA_OK(cudaStreamWaitEvent(c->stream, c->join_ev, 0));
   CUDA_OK(cudaEventSynchronize(c->join_ev));
   job.running = false;
+  c->side_job_running = false;
+  c->sm_reserve = 0;
   const double* h = reinterpret_cast<const double*>(job.host);
   if (*reinterpret_cast<const int*>(h + 120)) invalid("thin_svd: non-finite input");
   sv.resize(static_cast<size_t>(job.q));

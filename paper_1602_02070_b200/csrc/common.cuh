@@ -91,6 +91,11 @@ struct Ctx {
   int last_power_path = 0;    // 1 one product, 2 two products per barrier; 0 single-CTA kernel or none (tests)
   cudaStream_t side = nullptr;  // second stream for independent work (lazily created)
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  // A one-CTA job on the side stream that fills an SM (the detected-rank
+  // Jacobi kernel): while it runs, persistent one-CTA-per-SM grids on the main
+  // stream size themselves to the SMs that are left (join_ev marks its end).
+  bool side_job_running = false;
+  int sm_reserve = 0;
   // Host work deferred to the next long device wait (run_idle_work): it runs
   // with `stream` switched to `aux`, and the context stream then waits on it.
   std::function<void()> idle_work;

@@ -666,6 +666,7 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
     grid_barrier_mono(&st->bar_count, bar_g);
     // every CTA reads all of w1 and w2 and reduces in the same fixed order
     double t[2] = {0.0, 0.0};
+#pragma unroll 4
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
       const double x1 = __ldcg(w1 + i), x2 = __ldcg(w2 + i);
       vs[i] = x2;

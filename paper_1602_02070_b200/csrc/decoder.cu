@@ -207,6 +207,13 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
   while (!host.done && launched_it < cfg.pcg_max_iter) {
     // exactly the iterations that can still run (no launch past max_iter)
     const i64 todo = std::min<i64>(chunk, cfg.pcg_max_iter - launched_it);
+    // a side-stream job holding an SM: the persistent slab grid leaves it out
+    // (its 148th CTA would otherwise queue behind another and double the pass)
+    if (c->side_job_running) {
+      const bool busy = cudaEventQuery(c->join_ev) == cudaErrorNotReady;
+      (void)cudaGetLastError();
+      c->sm_reserve = busy ? 1 : 0;
+    }
     for (i64 k = 0; k < todo; ++k) {
       launch_apply<TK, TK, TV, TX>(c, apK, pr, pc, P.p, U.p, cbK);
       {

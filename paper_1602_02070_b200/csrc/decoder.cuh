@@ -1806,7 +1806,8 @@ void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const T
       ensure_smem(k, ap.s_smem);
       const SlabPlan sp{ap.s_rec.p,  reinterpret_cast<const SlabStep*>(ap.s_steps.p), ap.s_wsteps.p, ap.s_max_steps,
                         ap.s_win.p, ap.s_lv.p, ap.s_lo.p};
-      const unsigned grid = static_cast<unsigned>(ap.s_grid);  // persistent, one CTA per SM
+      // persistent, one CTA per SM (less the SMs a side-stream job holds)
+      const unsigned grid = static_cast<unsigned>(std::max(1, std::min(ap.s_grid, c->num_sms - c->sm_reserve)));
       launch_pdl(k, dim3(grid), dim3(kSlabThreads), ap.s_smem, c->stream, static_cast<int>(ap.p),
                  static_cast<int>(ap.ncols), ap.s_parts, sp, P, cb);
       launched(c);
