@@ -634,6 +634,10 @@ __global__ void csr_to_ell_packed_k(i64 n, int E, const i64* __restrict__ rp, co
   const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const i64 k0 = rp[i], d = rp[i + 1] - k0;
+  // flag[1]: the half bandwidth max |column - row| (the reach of one product)
+  int bw = 0;
+  for (i64 k = 0; k < d; ++k) bw = max(bw, abs(ci[k0 + k] - static_cast<int>(i)));
+  if (bw > 0) atomicMax(flag + 1, bw);
   for (int k = 0; k < E; ++k) {
     const double x = k < d ? v[k0 + k] : 0.0;
     const float f = static_cast<float>(x);
@@ -668,8 +672,21 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
                                                                  const i64* __restrict__ crp,
                                                                  const double* __restrict__ inv,
                                                                  const double* __restrict__ B, double* __restrict__ X,
-                                                                 double tol, i64 max_iter, ColState* st) {
+                                                                 double tol, i64 max_iter, ColState* st,
+                                                                 const int* __restrict__ bwp) {
   constexpr int NT = kPcgSmemThreads, NW = NT / 32;
+  // Support window.  With half bandwidth bw = max |column - row|, one product
+  // widens the rows where p, r and A p can be nonzero by bw on each side; a
+  // Kron right-hand side (one kept node's few interior neighbours) starts
+  // narrow, so most rows are exact zeros for the first n / (2 bw) iterations.
+  // Rows outside the window are skipped -- they would compute 0 = 0 + v * 0
+  // and x += alpha * 0, so every value is bit-identical to the full sweep.
+  const int bw = bwp ? *bwp : n;
+  __shared__ int s_lo, s_hi;
+  if (threadIdx.x == 0) {
+    s_lo = n;
+    s_hi = -1;
+  }
   extern __shared__ __align__(16) double smd[];
   double* Ps = smd;
   double* Xs = smd + n;
@@ -724,6 +741,7 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
   double R[RPT], AP[RPT];
   // r = b - A x, z = inv o r, p = z
   double s3[3] = {0.0, 0.0, 0.0};
+  int my_lo = n, my_hi = -1;
 #pragma unroll
   for (int r = 0; r < RPT; ++r) {
     const int i = t + r * NT;
@@ -737,7 +755,15 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
       s3[0] += b * b;
       s3[1] += rr * z;
       s3[2] += rr * rr;
+      if (rr != 0.0 || z != 0.0) {
+        my_lo = min(my_lo, i);
+        my_hi = max(my_hi, i);
+      }
     }
+  }
+  if (my_hi >= 0) {
+    atomicMin(&s_lo, my_lo);
+    atomicMax(&s_hi, my_hi);
   }
   cta_sum<3, NW>(s3, red, par);
   const double norm_b = sqrt(s3[0]), target = tol * norm_b;
@@ -746,14 +772,16 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
   int err = 0;
   double curv = 0.0;
   i64 it = 0;
-  __syncthreads();  // p complete
+  __syncthreads();  // p and the support window complete
+  int lo = s_lo, hi = s_hi + 1;  // rows [lo, hi) hold every nonzero of p and r
   while (done == 0) {
+    const int alo = max(0, lo - bw), ahi = static_cast<int>(min(static_cast<i64>(n), static_cast<i64>(hi) + bw));
     double cv[1] = {0.0};
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int i = t + r * NT;
       AP[r] = 0.0;
-      if (i < n) {
+      if (i >= alo && i < ahi) {
         AP[r] = spmv(Ps, i);
         cv[0] += Ps[i] * AP[r];
       }
@@ -770,7 +798,7 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int i = t + r * NT;
-      if (i < n) {
+      if (i >= alo && i < ahi) {
         Xs[i] = __dadd_rn(Xs[i], __dmul_rn(alpha, Ps[i]));
         const double rr = __dsub_rn(R[r], __dmul_rn(alpha, AP[r]));
         R[r] = rr;
@@ -784,8 +812,10 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
       const int i = t + r * NT;
-      if (i < n) Ps[i] = __dadd_rn(__dmul_rn(Is[i], R[r]), __dmul_rn(beta, Ps[i]));
+      if (i >= alo && i < ahi) Ps[i] = __dadd_rn(__dmul_rn(Is[i], R[r]), __dmul_rn(beta, Ps[i]));
     }
+    lo = alo;
+    hi = ahi;
     rho = s2[0];
     it += 1;
     if (sqrt(s2[1]) <= target || it >= max_iter) done = 1;
@@ -822,12 +852,12 @@ __global__ void __launch_bounds__(kPcgSmemThreads, 1) pcg_smem_k(int n, i64 nb, 
 template <int RPT>
 void pcg_smem_rpt(Ctx* c, int E, int packed, size_t smem, const double* ev, const int* ec, const i64* crp,
                   const double* inv, const double* B, double* X, i64 n, i64 nb, double tol, i64 max_iter,
-                  ColState* st) {
+                  ColState* st, const int* bwp) {
   auto launch = [&](auto k) {
     ensure_smem(k, smem);
     KScope ks_(c, "pcg_persistent");
     k<<<static_cast<unsigned>(nb), kPcgSmemThreads, smem, c->stream>>>(static_cast<int>(n), nb, ev, ec, crp, inv, B, X,
-                                                                      tol, max_iter, st);
+                                                                      tol, max_iter, st, bwp);
     launched(c);
   };
   if (E == 0)
@@ -846,12 +876,13 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   if (n <= 0 || n > 20 * kPcgSmemThreads || vec > kMax || A->nnz == 0) return false;
   const size_t csr = static_cast<size_t>(A->nnz) * 12 + static_cast<size_t>(n + 1) * 4 + 16;
   const i64 rpt = (n + kPcgSmemThreads - 1) / kPcgSmemThreads;
+  const int* bwp = nullptr;  // device half bandwidth (ELL paths); null: no window
   auto run = [&](int E, int pk, size_t smem, const double* ev, const int* ec, const i64* crp) {
-    if (rpt <= 4) return pcg_smem_rpt<4>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 8) return pcg_smem_rpt<8>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 12) return pcg_smem_rpt<12>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    if (rpt <= 16) return pcg_smem_rpt<16>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
-    return pcg_smem_rpt<20>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st);
+    if (rpt <= 4) return pcg_smem_rpt<4>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st, bwp);
+    if (rpt <= 8) return pcg_smem_rpt<8>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st, bwp);
+    if (rpt <= 12) return pcg_smem_rpt<12>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st, bwp);
+    if (rpt <= 16) return pcg_smem_rpt<16>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st, bwp);
+    return pcg_smem_rpt<20>(c, E, pk, smem, ev, ec, crp, inv, B, X, n, nb, tol, max_iter, st, bwp);
   };
   if (vec + csr <= kMax && A->nnz < (i64{1} << 30)) {  // the whole operator in shared memory
     run(0, 0, vec + csr, A->v, A->ci, A->rp);
@@ -868,11 +899,12 @@ bool pcg_smem(Ctx* c, Csr* A, const double* inv, const double* B, double* X, i64
   // packed (fp32 value, column) words when every value is exact in fp32
   // (unit-weight grids: the interior's values are small integers)
   DevBuf<uint2> ep(c, static_cast<size_t>(Ep) * n);
-  DevBuf<int> flag(c, 1);
+  DevBuf<int> flag(c, 2);  // [0] packing flags, [1] half bandwidth
   flag.zero(c);
   csr_to_ell_packed_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, A->rp, A->ci, A->v, ep.p, flag.p);
   launched(c);
   const int fl = read_back(c, flag.p);
+  bwp = flag.p + 1;
   if (!(fl & 2) && n < 65536) {
     DevBuf<unsigned> eh(c, static_cast<size_t>(Ep) * n);
     ell_pack16_k<<<blocks_for(n), kBlock, 0, c->stream>>>(n, Ep, ep.p, eh.p);
