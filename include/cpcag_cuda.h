@@ -87,6 +87,13 @@ int cpcag_ctx_set_apply_path(cpcag_ctx ctx, int path);
 /* Test hook: the persistent FISTA kernel's tile GEMM, 0 = automatic (fp64
  * tensor cores, DMMA, when the tiling fits), 1 = SIMT fp64 multiply-adds. */
 int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path);
+/* Environment test hooks (read by the library; results are the same on
+ * either side of each, the tests compare them): CPCAG_FISTA_PERSIST=0 runs
+ * dense FRPCAG through the per-kernel path instead of the one persistent
+ * kernel; CPCAG_KNN=tc|simt forces the kNN tile path; CPCAG_KNN_PASS2=0 sends
+ * every uncertified row of the tensor-core kNN to the exact fp64 kernel;
+ * CPCAG_GAP_LANCZOS=1 takes the Lanczos spectral gap inside run_pipeline at
+ * any size; CPCAG_TRACE=1 prints stage marks to stderr. */
 /* Test hook: the cooperative power iteration (operators too large for one
  * CTA), 0 = automatic (two products per grid barrier through the dense square
  * of the operator when a CTA's rows of it fit in shared memory), 1 = always
