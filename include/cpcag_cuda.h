@@ -3,7 +3,7 @@
  * path (Compressive PCA on graphs, arXiv 1602.02070).
  *
  * This is the drop-in boundary: every entry point replaces one public
- * function of the reference library `cpcag` (proj/core/include/cpcag/*.hpp,
+ * function of the reference library `cpcag` (the headers under proj/core/include/cpcag,
  * cited per function) with the same argument meaning, the same defaults
  * (documented per argument) and the same error behaviour: a nonzero status
  * maps back to the reference exception type and cpcag_cuda_last_error()

@@ -116,6 +116,8 @@ struct alignas(sizeof(TV) == 8 ? 16 : 8) OffEnt {
 template <typename TI, typename TK, typename TV, typename TB>
 __global__ void __launch_bounds__(256, 4) fused_k(int p, int n, Pull<TV> Lr, Pull<TV> Lc, int cols_per_cta,
                                                  const TI* __restrict__ P, Combine<TK, TB> cb) {
+  pdl_wait();  // P and the solver state come from the previous kernel on the stream
+  pdl_trigger();
   if (cb.st && cb.st->done) return;
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int RB = 512;
@@ -1818,8 +1820,8 @@ void launch_apply(Ctx* c, const ApplyPlan& ap, Pull<TV> Lr, Pull<TV> Lc, const T
     KScope ks_(c, "cg_apply");
     auto k = fused_k<TI, TK, TV, TB>;
     ensure_smem(k, ap.f_smem);
-    k<<<ap.f_grid, 256, ap.f_smem, c->stream>>>(static_cast<int>(ap.p), static_cast<int>(ap.ncols), Lr, Lc, ap.f_cpc,
-                                               P, cb);
+    launch_pdl(k, ap.f_grid, dim3(256), ap.f_smem, c->stream, static_cast<int>(ap.p), static_cast<int>(ap.ncols), Lr,
+               Lc, ap.f_cpc, P, cb);
     launched(c);
     return;
   }
