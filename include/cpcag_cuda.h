@@ -95,10 +95,11 @@ int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path);
  * CPCAG_GAP_LANCZOS=1 takes the Lanczos spectral gap inside run_pipeline at
  * any size; CPCAG_TRACE=1 prints stage marks to stderr. */
 /* Test hook: the cooperative power iteration (operators too large for one
- * CTA), 0 = automatic (two products per grid barrier through the dense square
- * of the operator when a CTA's rows of it fit in shared memory), 1 = always
- * one product per barrier.  last_power_path: 2 / 1 as above for the most
- * recent power iteration, 0 when it ran in the single-CTA kernel. */
+ * CTA), 0 = automatic (three, else two products per grid barrier through the
+ * dense powers of the operator when a CTA's rows of them fit in shared
+ * memory), 1 = always one product per barrier, 2 = at most two.
+ * last_power_path: 3 / 2 / 1 products per barrier for the most recent power
+ * iteration, 0 when it ran in the single-CTA kernel. */
 int cpcag_ctx_set_power_path(cpcag_ctx ctx, int path);
 int cpcag_ctx_last_power_path(cpcag_ctx ctx);
 /* The path (1, 2 or 3 as above) the most recently planned decoder operator

@@ -179,12 +179,13 @@ class Context:
         N.check(N.lib().cpcag_ctx_set_fista_path(self.handle, {"auto": 0, "simt": 1}[path]))
 
     def set_power_path(self, path: str):
-        """Cooperative power iteration: "auto" (two products per barrier when A A fits) or "single" (tests)."""
-        N.check(N.lib().cpcag_ctx_set_power_path(self.handle, {"auto": 0, "single": 1}[path]))
+        """Cooperative power iteration: "auto" (three or two products per barrier when the dense powers
+        of the operator fit), "single" or "double" (tests)."""
+        N.check(N.lib().cpcag_ctx_set_power_path(self.handle, {"auto": 0, "single": 1, "double": 2}[path]))
 
     def last_power_path(self) -> str:
         """How the most recent power iteration ran."""
-        return {0: "cta", 1: "single", 2: "double"}[N.lib().cpcag_ctx_last_power_path(self.handle)]
+        return {0: "cta", 1: "single", 2: "double", 3: "triple"}[N.lib().cpcag_ctx_last_power_path(self.handle)]
 
     def last_apply_path(self) -> str:
         """The path the most recently planned decoder operator took."""

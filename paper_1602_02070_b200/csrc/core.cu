@@ -598,18 +598,21 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
   }
 }
 
-// Two products per grid barrier for operators whose square fits beside them:
-// with A2 = A A (dense, built once), one round forms w1 = A v and w2 = A2 v
-// from the same v.  ||w1|| is the reference's estimate of this iteration; the
-// next iterate would be v' = w1 / ||w1||, so A v' = w2 / ||w1|| and the next
-// estimate is ||w2|| / ||w1||, the iterate after it w2 / ||w2||
-// (solvers.cpp:43-51 twice, both stop tests in order).  The barrier and the
-// L2 round trip of w are paid once per two reference iterations; estimates
+// K products per grid barrier for operators whose powers fit beside them:
+// with A2 = A A (and A3 = A2 A), dense and built once, one round forms
+// w_m = A^m v, m = 1..K, from the same v.  ||w_1|| is the reference's estimate
+// of this iteration; the next iterate would be v' = w_1 / ||w_1||, so
+// A v' = w_2 / ||w_1|| and the next estimate is ||w_2|| / ||w_1||, the one
+// after it ||w_3|| / ||w_2||, and the iterate after the round w_K / ||w_K||
+// (solvers.cpp:43-51 K times, every stop test in order).  The barrier and the
+// L2 round trip of w are paid once per K reference iterations; estimates
 // agree with the one-product form to rounding (~1e-15 relative).
-__global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __restrict__ rp,
+template <int K>
+__global__ void __launch_bounds__(512) power_iter_coopk_k(i64 n, const i64* __restrict__ rp,
                                                           const int* __restrict__ ci,
                                                           const double* __restrict__ val,
-                                                          const double* __restrict__ A2, i64 ld,
+                                                          const double* __restrict__ A2,
+                                                          const double* __restrict__ A3, i64 ld,
                                                           const double* __restrict__ v0, double* wbuf, double tol,
                                                           i64 max_iter, PowerState* st) {
   extern __shared__ double sm[];
@@ -619,8 +622,8 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
   const int nr = static_cast<int>(r1 - r0);
   const i64 k0 = rp[r0], k1 = rp[r1];
   double* vs = sm;                     // n
-  double* a2s = vs + n;                // nr x n, the CTA's rows of A2
-  double* sval = a2s + static_cast<i64>(nr) * n;
+  double* pws = vs + n;                // (K - 1) x nr x n: the CTA's rows of A2 (, A3)
+  double* sval = pws + static_cast<i64>(K - 1) * nr * n;
   int* sci = reinterpret_cast<int*>(sval + (k1 - k0));
   for (i64 k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
     sval[k - k0] = val[k];
@@ -628,7 +631,8 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
   }
   for (i64 q = threadIdx.x; q < static_cast<i64>(nr) * n; q += blockDim.x) {
     const i64 r = q / n, j = q - r * n;
-    a2s[q] = A2[(r0 + r) * ld + j];
+    pws[q] = A2[(r0 + r) * ld + j];
+    if constexpr (K == 3) pws[static_cast<i64>(nr) * n + q] = A3[(r0 + r) * ld + j];
   }
   for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v0[i];
   __syncthreads();
@@ -636,10 +640,9 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
   i64 it = 0;
   unsigned bar_g = 0, round = 0;
   while (it < max_iter) {
-    double* w1 = wbuf + (round & 1) * 2 * n;
-    double* w2 = w1 + n;
+    double* w = wbuf + (round & 1) * K * n;  // w_1 | w_2 (| w_3)
     ++round;
-    for (int task = wid; task < 2 * nr; task += nw) {
+    for (int task = wid; task < K * nr; task += nw) {
       double a0 = 0.0, a1 = 0.0;
       if (task < nr) {
         const i64 ra = rp[r0 + task] - k0, rb = rp[r0 + task + 1] - k0;
@@ -650,9 +653,10 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
         }
         if (k < rb) a0 += sval[k] * vs[sci[k]];
         a0 = warp_sum(a0 + a1);
-        if (lane == 0) w1[r0 + task] = a0;
+        if (lane == 0) w[r0 + task] = a0;
       } else {
-        const double* row = a2s + static_cast<i64>(task - nr) * n;
+        const int m = task / nr, rr = task - m * nr;  // power m + 1, row rr
+        const double* row = pws + (static_cast<i64>(m - 1) * nr + rr) * n;
         i64 j = lane;
         for (; j + 32 < n; j += 64) {
           a0 += row[j] * vs[j];
@@ -660,40 +664,47 @@ __global__ void __launch_bounds__(512) power_iter_coop2_k(i64 n, const i64* __re
         }
         if (j < n) a0 += row[j] * vs[j];
         a0 = warp_sum(a0 + a1);
-        if (lane == 0) w2[r0 + task - nr] = a0;
+        if (lane == 0) w[m * n + r0 + rr] = a0;
       }
     }
     grid_barrier_mono(&st->bar_count, bar_g);
-    // every CTA reads all of w1 and w2 and reduces in the same fixed order
-    double t[2] = {0.0, 0.0};
+    // every CTA reads all of w and reduces the K norms in the same fixed order
+    double t[K];
+#pragma unroll
+    for (int m = 0; m < K; ++m) t[m] = 0.0;
 #pragma unroll 4
     for (i64 i = threadIdx.x; i < n; i += blockDim.x) {
-      const double x1 = __ldcg(w1 + i), x2 = __ldcg(w2 + i);
-      vs[i] = x2;
-      t[0] += x1 * x1;
-      t[1] += x2 * x2;
+      double x[K];
+#pragma unroll
+      for (int m = 0; m < K; ++m) x[m] = __ldcg(w + m * n + i);
+      vs[i] = x[K - 1];
+#pragma unroll
+      for (int m = 0; m < K; ++m) t[m] += x[m] * x[m];
     }
-    block_sum<2>(t);
-    const double n1 = sqrt(t[0]);
-    if (n1 == 0.0) {
-      est = 0.0;
-      break;
-    }
-    double prev = est;
-    est = n1;
-    ++it;
-    if ((it > 1 && fabs(est - prev) <= tol * est) || it >= max_iter) break;
-    const double n2 = sqrt(t[1]);
-    if (n2 == 0.0) {  // A v' = 0: the reference returns 0
-      est = 0.0;
+    block_sum<K>(t);
+    bool stop = false;
+    double nprev = 1.0, nlast = 1.0;
+#pragma unroll
+    for (int m = 0; m < K; ++m) {
+      const double nm = sqrt(t[m]);
+      if (nm == 0.0) {  // A v = 0 for the current iterate: the reference returns 0
+        est = 0.0;
+        if (m > 0) ++it;
+        stop = true;
+        break;
+      }
+      const double prev = est;
+      est = m == 0 ? nm : __ddiv_rn(nm, nprev);
       ++it;
-      break;
+      nprev = nm;
+      nlast = nm;
+      if ((it > 1 && fabs(est - prev) <= tol * est) || it >= max_iter) {
+        stop = true;
+        break;
+      }
     }
-    prev = est;
-    est = __ddiv_rn(n2, n1);
-    ++it;
-    if (fabs(est - prev) <= tol * est) break;
-    for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(vs[i], n2);
+    if (stop) break;
+    for (i64 i = threadIdx.x; i < n; i += blockDim.x) vs[i] = __ddiv_rn(vs[i], nlast);
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -711,10 +722,11 @@ __global__ void csr_to_dense_k(i64 n, const i64* __restrict__ rp, const int* __r
   for (i64 k = rp[r] + lane; k < rp[r + 1]; k += 32) D[r * ld + ci[k]] = val[k];
 }
 
-// C = A A for a dense row-major ld x ld array (ld a multiple of 64, zero
+// C = A B for dense row-major ld x ld arrays (ld a multiple of 64, zero
 // padded): 64 x 64 tile per CTA, 4 x 4 per thread, k ascending (each entry of
 // C is one fixed-order fp64 FMA chain).
-__global__ void __launch_bounds__(256) dense_square_k(int ld, const double* __restrict__ A, double* __restrict__ C) {
+__global__ void __launch_bounds__(256) dense_mm_k(int ld, const double* __restrict__ A, const double* __restrict__ B,
+                                                  double* __restrict__ C) {
   __shared__ double As[16][64 + 4];
   __shared__ __align__(16) double Bs[16][64];
   const int t = threadIdx.x, ty = t >> 4, tx = t & 15;
@@ -729,8 +741,8 @@ __global__ void __launch_bounds__(256) dense_square_k(int ld, const double* __re
   for (int kk = 0; kk < ld; kk += 16) {
     const double2 x0 = *reinterpret_cast<const double2*>(A + static_cast<i64>(i0 + ai) * ld + kk + ak);
     const double2 x1 = *reinterpret_cast<const double2*>(A + static_cast<i64>(i0 + ai) * ld + kk + ak + 2);
-    const double2 y0 = *reinterpret_cast<const double2*>(A + static_cast<i64>(kk + bk) * ld + j0 + bj);
-    const double2 y1 = *reinterpret_cast<const double2*>(A + static_cast<i64>(kk + bk) * ld + j0 + bj + 2);
+    const double2 y0 = *reinterpret_cast<const double2*>(B + static_cast<i64>(kk + bk) * ld + j0 + bj);
+    const double2 y1 = *reinterpret_cast<const double2*>(B + static_cast<i64>(kk + bk) * ld + j0 + bj + 2);
     __syncthreads();
     As[ak][ai] = x0.x;
     As[ak + 1][ai] = x0.y;
@@ -766,7 +778,7 @@ __global__ void __launch_bounds__(256) dense_square_k(int ld, const double* __re
 // false when there is nothing to launch (st->est is then set on the host:
 // n == 0, ||v0|| == 0 or max_iter <= 0 give 0).
 struct PowerJob {
-  DevBuf<double> v, w, part, dense, sq;
+  DevBuf<double> v, w, part, dense, sq, cube;
   DevBuf<PowerState> st;
   double host_est = 0.0;
   bool launched = false;
@@ -832,37 +844,52 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
   size_t smem = v_in_smem ? static_cast<size_t>(n) * 8 : 0;
   int slice_in_smem = smem + static_cast<size_t>(max_slice) * 12 + 16 <= budget ? 1 : 0;
   if (slice_in_smem) smem += static_cast<size_t>(max_slice) * 12 + 16;
-  // two products per barrier when the CTA's rows of A A fit beside its slice
+  // K = 3 or 2 products per barrier when the CTA's rows of A^2 (and A^3) fit beside its slice
   if (s == c->stream && v_in_smem && slice_in_smem && c->power_path != 1) {
     const i64 rows_max = (n + nb - 1) / nb;
     const i64 ld = ((n + 63) / 64) * 64;
-    const size_t smem2 = static_cast<size_t>(n) * 8 + static_cast<size_t>(rows_max) * n * 8 +
-                         static_cast<size_t>(max_slice) * 12 + 16;
-    if (smem2 <= budget && ld * ld * 8 <= (i64{64} << 20) && max_iter >= 2) {
+    auto smem_k = [&](int K) {
+      return static_cast<size_t>(n) * 8 + static_cast<size_t>(K - 1) * rows_max * n * 8 +
+             static_cast<size_t>(max_slice) * 12 + 16;
+    };
+    int K = 0;
+    if (ld * ld * 8 <= (i64{64} << 20)) {
+      if (smem_k(3) <= budget && max_iter >= 3 && c->power_path != 2) K = 3;
+      else if (smem_k(2) <= budget && max_iter >= 2) K = 2;
+    }
+    if (K) {
+      const size_t smemk = smem_k(K);
       job.dense.alloc(c, static_cast<size_t>(ld * ld));
       job.sq.alloc(c, static_cast<size_t>(ld * ld));
+      if (K == 3) job.cube.alloc(c, static_cast<size_t>(ld * ld));
       job.dense.zero(c);
-      job.w.alloc(c, 4 * n);
-      ensure_smem(power_iter_coop2_k, smem2);
+      job.w.alloc(c, 2 * K * n);
+      void* kern = K == 3 ? (void*)power_iter_coopk_k<3> : (void*)power_iter_coopk_k<2>;
+      ensure_smem_impl(kern, smemk);
       int fit = 0;
-      CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coop2_k, 512, smem2));
+      if (K == 3)
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<3>, 512, smemk));
+      else
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<2>, 512, smemk));
       if (fit < 1) invalid("power iteration: kernel does not fit on an SM");
       const i64* rp = A->rp;
       const int* ci = A->ci;
       const double* val = A->v;
       const double* a2 = job.sq.p;
+      const double* a3 = job.cube.p;
       const double* vp = job.v.p;
       double* wp = job.w.p;
       PowerState* sp = job.st.p;
       i64 nn = n, ldd = ld;
-      void* args[] = {(void*)&nn, (void*)&rp, (void*)&ci, (void*)&val, (void*)&a2, (void*)&ldd, (void*)&vp,
-                      (void*)&wp, (void*)&tol, (void*)&max_iter, (void*)&sp};
+      void* args[] = {(void*)&nn, (void*)&rp, (void*)&ci, (void*)&val, (void*)&a2, (void*)&a3, (void*)&ldd,
+                      (void*)&vp, (void*)&wp, (void*)&tol, (void*)&max_iter, (void*)&sp};
       job.launched = true;
       auto go = [&] {
         csr_to_dense_k<<<blocks_for(n * 32), kBlock, 0, s>>>(n, rp, ci, val, ld, job.dense.p);
         const unsigned gt = static_cast<unsigned>(ld / 64);
-        dense_square_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.dense.p, job.sq.p);
-        CUDA_OK(cudaLaunchCooperativeKernel((void*)power_iter_coop2_k, dim3(nb), dim3(512), args, smem2, s));
+        dense_mm_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.dense.p, job.dense.p, job.sq.p);
+        if (K == 3) dense_mm_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.sq.p, job.dense.p, job.cube.p);
+        CUDA_OK(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(512), args, smemk, s));
       };
       if (timed) {
         KScope ks_(c, "power_iter");
@@ -871,7 +898,7 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
         go();
       }
       launched(c);
-      c->last_power_path = 2;
+      c->last_power_path = K;
       return;
     }
   }
@@ -1168,7 +1195,7 @@ int cpcag_ctx_set_fista_path(cpcag_ctx ctx, int path) {
 
 int cpcag_ctx_set_power_path(cpcag_ctx ctx, int path) {
   return guard([&] {
-    if (path < 0 || path > 1) invalid("power path must be 0 or 1");
+    if (path < 0 || path > 2) invalid("power path must be 0, 1 or 2");
     as_ctx(ctx)->power_path = path;
   });
 }

@@ -94,35 +94,37 @@ def test_power_iteration_matches_oracle(P, ctx):
         assert got == pytest.approx(want, rel=1e-6)
 
 
-def test_power_iteration_two_products_per_barrier(P, ctx):
-    # operators whose rows of A A fit a CTA's shared memory iterate twice per
-    # grid barrier (w1 = A v, w2 = A A v): same estimates and stop iteration
-    # as solvers.cpp:43-51, also against the one-product kernel
+def test_power_iteration_several_products_per_barrier(P, ctx):
+    # operators whose rows of A A (and A A A) fit a CTA's shared memory iterate
+    # two or three times per grid barrier (w_m = A^m v): same estimates and stop
+    # iteration as solvers.cpp:43-51, also against the one-product kernel
     rs = np.random.default_rng(17)
     W = np.abs(rs.standard_normal((900, 900))) * (rs.random((900, 900)) < 0.6)
     W = np.triu(W, 1)
     W = W + W.T
     Ld = np.diag(W.sum(1)) - W  # dense-ish Laplacian, the shape of a Kron-reduced graph
     ii, jj = np.nonzero(Ld)
-    cases = [O.Csr.from_triplets(900, 900, ii, jj, Ld[ii, jj]), knn_laplacian(1400, 4, 8, 5)]
-    for L in cases:
+    # 900 rows: 7 rows of A^2 and A^3 per CTA fit; 1400 rows: only A^2's 10 rows do
+    cases = [(O.Csr.from_triplets(900, 900, ii, jj, Ld[ii, jj]), "triple"), (knn_laplacian(1400, 4, 8, 5), "double")]
+    for L, auto in cases:
         A = to_device(ctx, L)
-        got = P.power_iteration_norm(A, 1e-7, 42, ctx=ctx)
-        assert ctx.last_power_path() == "double"
         want = O.power_iteration_norm(L, 1e-7, 42)
-        assert got == pytest.approx(want, rel=1e-9)
-        ctx.set_power_path("single")
+        got = {}
         try:
-            one = P.power_iteration_norm(A, 1e-7, 42, ctx=ctx)
-            assert ctx.last_power_path() == "single"
+            for path, ran in (("auto", auto), ("double", "double"), ("single", "single")):
+                ctx.set_power_path(path)
+                got[path] = P.power_iteration_norm(A, 1e-7, 42, ctx=ctx)
+                assert ctx.last_power_path() == ran
+                assert got[path] == pytest.approx(want, rel=1e-9)
+                # iteration caps of every residue stop where the reference stops
+                for cap in (1, 2, 3, 4, 5, 6, 7):
+                    g = P.power_iteration_norm(A, 1e-30, 42, cap, ctx=ctx)
+                    w = O.power_iteration_norm(L, 1e-30, 42, cap)
+                    assert g == pytest.approx(w, rel=1e-9)
         finally:
             ctx.set_power_path("auto")
-        assert got == pytest.approx(one, rel=1e-12)
-        # odd and even iteration caps stop where the reference stops
-        for cap in (1, 2, 5, 6):
-            g = P.power_iteration_norm(A, 1e-30, 42, cap, ctx=ctx)
-            w = O.power_iteration_norm(L, 1e-30, 42, cap)
-            assert g == pytest.approx(w, rel=1e-9)
+        assert got["auto"] == pytest.approx(got["single"], rel=1e-12)
+        assert got["double"] == pytest.approx(got["single"], rel=1e-12)
 
 
 def test_plan_and_subsample_bit_exact(P, ctx):
