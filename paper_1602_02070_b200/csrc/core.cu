@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(512) power_iter_coop_k(i64 n, const i64* __res
 // L2 round trip of w are paid once per K reference iterations; estimates
 // agree with the one-product form to rounding (~1e-15 relative).
 template <int K>
-__global__ void __launch_bounds__(512) power_iter_coopk_k(i64 n, const i64* __restrict__ rp,
+__global__ void __launch_bounds__(K == 3 ? 768 : 512) power_iter_coopk_k(i64 n, const i64* __restrict__ rp,
                                                           const int* __restrict__ ci,
                                                           const double* __restrict__ val,
                                                           const double* __restrict__ A2,
@@ -867,10 +867,11 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
       void* kern = K == 3 ? (void*)power_iter_coopk_k<3> : (void*)power_iter_coopk_k<2>;
       ensure_smem_impl(kern, smemk);
       int fit = 0;
+      const int threads = K == 3 ? 768 : 512;  // one warp per row task (K x ~7 rows at config 1)
       if (K == 3)
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<3>, 512, smemk));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<3>, threads, smemk));
       else
-        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<2>, 512, smemk));
+        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, power_iter_coopk_k<2>, threads, smemk));
       if (fit < 1) invalid("power iteration: kernel does not fit on an SM");
       const i64* rp = A->rp;
       const int* ci = A->ci;
@@ -889,7 +890,7 @@ static void power_prepare(Ctx* c, Csr* A, double tol, uint64_t seed, i64 max_ite
         const unsigned gt = static_cast<unsigned>(ld / 64);
         dense_mm_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.dense.p, job.dense.p, job.sq.p);
         if (K == 3) dense_mm_k<<<dim3(gt, gt), 256, 0, s>>>(static_cast<int>(ld), job.sq.p, job.dense.p, job.cube.p);
-        CUDA_OK(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(512), args, smemk, s));
+        CUDA_OK(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(threads), args, smemk, s));
       };
       if (timed) {
         KScope ks_(c, "power_iter");

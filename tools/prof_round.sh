@@ -19,7 +19,7 @@ timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none --
 echo "launch list rc=$?"; python tools/launch_summary.py $O/launches_cfg1.csv > $O/launches_cfg1_summary.txt
 # full captures of the cfg1 step's top kernels
 python tools/profile_step.py > $O/plain_step.log 2>&1 && \
-for k in slab_k pcg_smem_k fista_persist_k power_iter_coop2_k cg_update_k cg_residual_k; do
+for k in slab_k pcg_smem_k fista_persist_k power_iter_coopk_k cg_update_k cg_residual_k; do
   timeout -s KILL 600 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:"^$k" -c 1 \
     -o $O/full_cfg1_$k -f python tools/profile_step.py > $O/ncu_full_cfg1_$k.log 2>&1; echo "ncu $k rc=$?"
 done

@@ -32,7 +32,7 @@ def rows(path):
     return lines[:2], lines[2:]
 
 
-order = ["slab_k", "pcg_smem_k", "fista_persist_k", "power_iter_coop2_k", "cg_update_k", "cg_residual_k"]
+order = ["slab_k", "pcg_smem_k", "fista_persist_k", "power_iter_coopk_k", "cg_update_k", "cg_residual_k"]
 out = [f"# Round 2 ncu --set full summaries (one B200, --clock-control none; HEAD {head})", "",
        "Config 1 step kernels (tools/profile_step.py, one launch each):", ""]
 hdr = None
