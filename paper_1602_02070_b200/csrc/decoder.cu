@@ -38,25 +38,6 @@
 
 namespace cpcag_cuda {
 
-static __global__ void gather_int_k(i64 len, const int* __restrict__ src, const int* __restrict__ idx, int* dst) {
-  const i64 k = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (k < len) dst[k] = src[idx[k]];
-}
-
-// X(i, c) <- X(pos[i], c) for every column, in place through shared memory.
-template <typename TX>
-__global__ void __launch_bounds__(1024) unpermute_rows_k(i64 p, i64 n, const int* __restrict__ pos, TX* X) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  TX* s = reinterpret_cast<TX*>(smraw);
-  for (i64 col = blockIdx.x; col < n; col += gridDim.x) {
-    TX* x = X + col * p;
-    for (i64 i = threadIdx.x; i < p; i += blockDim.x) s[i] = x[i];
-    __syncthreads();
-    for (i64 i = threadIdx.x; i < p; i += blockDim.x) x[i] = s[pos[i]];
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ the solver
 // The operator plans of one decode: pulls of L_r / L_c in the value type
 // and the apply plans of the CG (TK iterates) and of the true residual (TX).
@@ -65,14 +46,7 @@ struct DecodePrep : DecodePrepBase {
   Pull<TV> pr{}, pc{};
   ApplyPlan apK, apX;
   i64 p = 0, n = 0;
-  // Row permutation of the two-pass path (hub-heavy row graphs): the CG runs
-  // on rows sorted by degree, L_r renamed into that order on the device
-  // (perm_*), `ord` new -> old row, `pos` old -> new.
-  bool permuted = false;
-  DevBuf<int> ord, pos;
-  DevBuf<i64> perm_rp;
-  DevBuf<int> perm_ci;
-  DevBuf<TV> perm_v;
+  RowOrder<TV> ro;  // the solve's row order (two-pass path, hub-heavy row graphs)
   const Csr* Lr = nullptr;
   const Csr* Lc = nullptr;
 };
@@ -86,59 +60,10 @@ void decode_prepare(Ctx* c, i64 p, i64 n, Csr* Lr, Csr* Lc, DecodePrep<TX, TK, T
   std::vector<TV> vr;
   host_pull<TV>(c, d.pr, p, Lr->nnz, rpr, cir, &vr);
   const bool exact = sizeof(TX) == 8;
-  // Hub-heavy row graphs on the two-pass path: the row-group pass wants rows
-  // of similar degree side by side (32 natural rows would pad the entries by
-  // > 30 %).  Rather than indirecting every row access through a sorted order
-  // (scattered 8-byte reads of U and writes of AP: 4x their bytes in 32-byte
-  // sectors), the whole system is solved in the sorted row order -- L_r's rows
-  // and column indices renamed (each row's entries keep their order, so every
-  // sum is the same chain), rsel permuted, X put back at the end.
   {
     const bool two_pass = c->apply_path == 1 ||
                           (c->apply_path == 0 && p * n * static_cast<i64>(sizeof(TK)) > (i64{96} << 20));
-    i64 tot = 0, pad_nat = 0;
-    for (i64 w = 0; w < p; w += 32) {
-      i64 mx = 0;
-      for (i64 i = w; i < std::min<i64>(p, w + 32); ++i) {
-        mx = std::max(mx, rpr[i + 1] - rpr[i]);
-        tot += rpr[i + 1] - rpr[i];
-      }
-      pad_nat += mx * std::min<i64>(32, p - w);
-    }
-    if (two_pass && tot > 0 && pad_nat > tot + tot / 3 && p * static_cast<i64>(sizeof(TX)) <= 160 * 1024) {
-      std::vector<int> ord(static_cast<size_t>(p)), pos(static_cast<size_t>(p));
-      std::iota(ord.begin(), ord.end(), 0);
-      std::stable_sort(ord.begin(), ord.end(),
-                       [&](int a, int b) { return rpr[a + 1] - rpr[a] > rpr[b + 1] - rpr[b]; });
-      for (i64 t = 0; t < p; ++t) pos[ord[t]] = static_cast<int>(t);
-      std::vector<i64> rp2(static_cast<size_t>(p) + 1, 0);
-      std::vector<int> ci2(cir.size());
-      std::vector<TV> v2(vr.size());
-      for (i64 t = 0; t < p; ++t) {
-        const i64 a = rpr[ord[t]], b = rpr[ord[t] + 1];
-        rp2[t + 1] = rp2[t] + (b - a);
-        for (i64 k = a; k < b; ++k) {
-          ci2[rp2[t] + (k - a)] = pos[cir[k]];
-          v2[rp2[t] + (k - a)] = vr[k];
-        }
-      }
-      d.ord.alloc(c, static_cast<size_t>(p));
-      d.pos.alloc(c, static_cast<size_t>(p));
-      d.perm_rp.alloc(c, rp2.size());
-      d.perm_ci.alloc(c, std::max<size_t>(ci2.size(), 1));
-      d.perm_v.alloc(c, std::max<size_t>(v2.size(), 1));
-      CUDA_OK(cudaMemcpyAsync(d.ord.p, ord.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
-      CUDA_OK(cudaMemcpyAsync(d.pos.p, pos.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
-      CUDA_OK(cudaMemcpyAsync(d.perm_rp.p, rp2.data(), sizeof(i64) * rp2.size(), cudaMemcpyHostToDevice, c->stream));
-      CUDA_OK(cudaMemcpyAsync(d.perm_ci.p, ci2.data(), sizeof(int) * ci2.size(), cudaMemcpyHostToDevice, c->stream));
-      CUDA_OK(cudaMemcpyAsync(d.perm_v.p, v2.data(), sizeof(TV) * v2.size(), cudaMemcpyHostToDevice, c->stream));
-      sync(c);  // the host arrays go out of scope below
-      d.pr = Pull<TV>{d.perm_rp.p, d.perm_ci.p, d.perm_v.p};
-      rpr.swap(rp2);
-      cir.swap(ci2);
-      vr.swap(v2);
-      d.permuted = true;
-    }
+    if (d.ro.build(c, p, two_pass, sizeof(TX), rpr, cir, vr)) d.pr = d.ro.pull;
   }
   HostPull<TV> lcp;
   host_pull<TV>(c, d.pc, n, Lc->nnz, lcp.rp, lcp.ci, &lcp.v);
@@ -175,12 +100,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
   // the solve runs in the prepared row order
   DevBuf<int> rsel_perm;
   Plan pl = pl_in;
-  if (prep->permuted) {
-    rsel_perm.alloc(c, static_cast<size_t>(p));
-    gather_int_k<<<blocks_for(p), kBlock, 0, c->stream>>>(p, pl_in.rsel, prep->ord.p, rsel_perm.p);
-    launched(c);
-    pl.rsel = rsel_perm.p;
-  }
+  if (prep->ro.on) pl.rsel = prep->ro.permute_rsel(c, pl_in.rsel, rsel_perm);
   const unsigned nbv = stride_blocks(c, std::max<i64>(N, 1));
   // the CG vector kernels: one wave of 8 x 256 threads per SM (4 vectors in flight per thread)
   const unsigned nbw = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(c->num_sms * 8, (N + 1023) / 1024)));
@@ -245,13 +165,7 @@ void decode_impl(Ctx* c, const TX* Xt, i64 rho_r, i64 rho_c, i64 p, i64 n, Csr* 
     const Combine<TK, TX> cbR{U.p, nullptr, gr, gc, pl, Xt, part.p, st.p};
     launch_apply<TX, TK, TV, TX>(c, apR, pr, pc, X, U.p, cbR);
   }
-  if (prep->permuted) {  // rows of X back to the caller's order, column by column in place
-    const size_t bytes = static_cast<size_t>(p) * sizeof(TX);
-    ensure_smem(unpermute_rows_k<TX>, bytes);
-    const unsigned g = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(n, static_cast<i64>(c->num_sms) * 2)));
-    unpermute_rows_k<TX><<<g, 1024, bytes, c->stream>>>(p, n, prep->pos.p, X);
-    launched(c);
-  }
+  if (prep->ro.on) prep->ro.restore_rows(c, X, n);  // rows of X back to the caller's order
   host = read_back(c, st.p);
   const double rel = host.norm_b > 0.0 ? std::sqrt(host.curv) / host.norm_b : 0.0;
   *converged = rel <= cfg.pcg_tol ? 1 : 0;

@@ -1203,6 +1203,111 @@ static __global__ void scatter_sel_k(const i64* __restrict__ om, i64 rho, int* s
   if (k < rho) sel[om[k]] = static_cast<int>(k);
 }
 
+static __global__ void gather_int_k(i64 len, const int* __restrict__ src, const int* __restrict__ idx, int* dst) {
+  const i64 k = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (k < len) dst[k] = src[idx[k]];
+}
+
+// X(i, c) <- X(pos[i], c) for every column, in place through shared memory.
+template <typename TX>
+__global__ void __launch_bounds__(1024) unpermute_rows_k(i64 p, i64 n, const int* __restrict__ pos, TX* X) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  TX* s = reinterpret_cast<TX*>(smraw);
+  for (i64 col = blockIdx.x; col < n; col += gridDim.x) {
+    TX* x = X + col * p;
+    for (i64 i = threadIdx.x; i < p; i += blockDim.x) s[i] = x[i];
+    __syncthreads();
+    for (i64 i = threadIdx.x; i < p; i += blockDim.x) x[i] = s[pos[i]];
+    __syncthreads();
+  }
+}
+
+
+// The solve's row order.  Hub-heavy row graphs on the two-pass path: the
+// row-group pass wants rows of similar degree side by side (32 natural rows
+// would pad the entries by > 30 %).  Rather than indirecting every row access
+// through a sorted order (scattered 8-byte reads of U and writes of AP: 4x
+// their bytes in 32-byte sectors), the whole system is solved in the sorted
+// row order -- L_r's rows and column indices renamed (each row's entries keep
+// their order, so every sum is the same chain), rsel permuted, X put back at
+// the end.  `ord` new -> old row, `pos` old -> new.
+template <typename TV>
+struct RowOrder {
+  bool on = false;
+  i64 p = 0;
+  DevBuf<int> ord, pos;
+  DevBuf<i64> rp;
+  DevBuf<int> ci;
+  DevBuf<TV> v;
+  Pull<TV> pull{};
+
+  // Decides (two-pass path, padding > 30 %, a column of X fits shared memory)
+  // and, when on, renames the host CSR in place and uploads it (`pull`).
+  bool build(Ctx* c, i64 p_, bool two_pass, size_t x_bytes, std::vector<i64>& rpr, std::vector<int>& cir,
+             std::vector<TV>& vr) {
+    p = p_;
+    i64 tot = 0, pad_nat = 0;
+    for (i64 w = 0; w < p; w += 32) {
+      i64 mx = 0;
+      for (i64 i = w; i < std::min<i64>(p, w + 32); ++i) {
+        mx = std::max(mx, rpr[i + 1] - rpr[i]);
+        tot += rpr[i + 1] - rpr[i];
+      }
+      pad_nat += mx * std::min<i64>(32, p - w);
+    }
+    if (!(two_pass && tot > 0 && pad_nat > tot + tot / 3 && p * static_cast<i64>(x_bytes) <= 160 * 1024)) return false;
+    std::vector<int> o(static_cast<size_t>(p)), q(static_cast<size_t>(p));
+    std::iota(o.begin(), o.end(), 0);
+    std::stable_sort(o.begin(), o.end(), [&](int a, int b) { return rpr[a + 1] - rpr[a] > rpr[b + 1] - rpr[b]; });
+    for (i64 t = 0; t < p; ++t) q[o[t]] = static_cast<int>(t);
+    std::vector<i64> rp2(static_cast<size_t>(p) + 1, 0);
+    std::vector<int> ci2(cir.size());
+    std::vector<TV> v2(vr.size());
+    for (i64 t = 0; t < p; ++t) {
+      const i64 a = rpr[o[t]], b = rpr[o[t] + 1];
+      rp2[t + 1] = rp2[t] + (b - a);
+      for (i64 k = a; k < b; ++k) {
+        ci2[rp2[t] + (k - a)] = q[cir[k]];
+        v2[rp2[t] + (k - a)] = vr[k];
+      }
+    }
+    ord.alloc(c, static_cast<size_t>(p));
+    pos.alloc(c, static_cast<size_t>(p));
+    rp.alloc(c, rp2.size());
+    ci.alloc(c, std::max<size_t>(ci2.size(), 1));
+    v.alloc(c, std::max<size_t>(v2.size(), 1));
+    CUDA_OK(cudaMemcpyAsync(ord.p, o.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(pos.p, q.data(), sizeof(int) * p, cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(rp.p, rp2.data(), sizeof(i64) * rp2.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(ci.p, ci2.data(), sizeof(int) * ci2.size(), cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(v.p, v2.data(), sizeof(TV) * v2.size(), cudaMemcpyHostToDevice, c->stream));
+    sync(c);  // the host arrays go out of scope below
+    pull = Pull<TV>{rp.p, ci.p, v.p};
+    rpr.swap(rp2);
+    cir.swap(ci2);
+    vr.swap(v2);
+    on = true;
+    return true;
+  }
+  // rsel in the solve's order (out owns the storage)
+  const int* permute_rsel(Ctx* c, const int* rsel, DevBuf<int>& out) const {
+    out.alloc(c, static_cast<size_t>(p));
+    gather_int_k<<<blocks_for(p), kBlock, 0, c->stream>>>(p, rsel, ord.p, out.p);
+    launched(c);
+    return out.p;
+  }
+  // rows of X (p x ncols) back to the caller's order, column by column in place
+  template <typename TX>
+  void restore_rows(Ctx* c, TX* X, i64 ncols) const {
+    if (ncols <= 0) return;
+    const size_t bytes = static_cast<size_t>(p) * sizeof(TX);
+    ensure_smem(unpermute_rows_k<TX>, bytes);
+    const unsigned g = static_cast<unsigned>(std::max<i64>(1, std::min<i64>(ncols, static_cast<i64>(c->num_sms) * 2)));
+    unpermute_rows_k<TX><<<g, 1024, bytes, c->stream>>>(p, ncols, pos.p, X);
+    launched(c);
+  }
+};
+
 // ------------------------------------------------------------------ the apply engine
 // Geometry of both passes for one operator pair, built once per decode.  The
 // lc pass works on a local column space of n_local columns ([own | halo] for

@@ -174,6 +174,8 @@ struct Shard {
   DevBuf<TV> lv;
   DevBuf<int> send_idx;
   ApplyPlan apK, apX;
+  RowOrder<TV> ro;
+  DevBuf<int> rsel_perm;
   DevBuf<TK> Ploc, R, AP, U, sendK;
   DevBuf<TX> Xloc, sendX;
   DevBuf<CgState> st;
@@ -225,8 +227,17 @@ struct Shard {
     std::vector<int> sidx(h.send_cols.begin(), h.send_cols.end());
     send_idx.alloc(c, std::max<i64>(nsend, 1));
     if (nsend) CUDA_OK(cudaMemcpyAsync(send_idx.p, sidx.data(), sizeof(int) * nsend, cudaMemcpyHostToDevice, c->stream));
-    plan_apply<TK, TK, TV>(c, apK, p, nb, nb + nh, h.c0, rpr, cir, vr, sizeof(TX) == 8);
-    plan_apply<TX, TK, TV>(c, apX, p, nb, nb + nh, h.c0, rpr, cir, vr, sizeof(TX) == 8);
+    // the solve's row order (every rank derives the same one from L_r, so
+    // exchanged columns agree): hub-heavy row graphs run in degree-sorted rows
+    std::vector<i64> rpr2(rpr);
+    std::vector<int> cir2(cir);
+    std::vector<TV> vr2(vr);
+    if (ro.build(c, p, true, sizeof(TX), rpr2, cir2, vr2)) {
+      pr = ro.pull;
+      pl.rsel = ro.permute_rsel(c, plan.rsel, rsel_perm);
+    }
+    plan_apply<TK, TK, TV>(c, apK, p, nb, nb + nh, h.c0, rpr2, cir2, vr2, sizeof(TX) == 8);
+    plan_apply<TX, TK, TV>(c, apX, p, nb, nb + nh, h.c0, rpr2, cir2, vr2, sizeof(TX) == 8);
     const i64 N = p * nb;
     Ploc.alloc(c, static_cast<size_t>(std::max<i64>(p * (nb + nh), 1)));
     R.alloc(c, std::max<i64>(N, 1));
@@ -244,6 +255,9 @@ struct Shard {
 
   i64 N() const { return p * nb; }
   unsigned nbv() const { return stride_blocks(c, std::max<i64>(N(), 1)); }
+  void finish() {  // the block's rows of X back to the caller's order
+    if (ro.on) ro.restore_rows(c, X, nb);
+  }
 
   void init_partial() {  // X = 0, R = P_own = b, st->rho = ||b_block||^2
     cg_init_k<TK, TX, TX><<<nbv(), kBlock, 0, c->stream>>>(p, nb, hp.c0, pl, Xt, X, R.p, Ploc.p, part.p, st.p);
@@ -271,14 +285,25 @@ struct Shard {
     const Combine<TK, TX> cb{U.p, AP.p, gr, gc, pl, nullptr, part.p, st.p};
     launch_lc<TK, TK, TV, TX>(c, apK, pcl, Ploc.p, nullptr, cb, true);
   }
+  // the CG vector kernels: one wave of 8 x 256 threads per SM, 16-byte vectors when the buffers allow
+  unsigned nbw() const {
+    return static_cast<unsigned>(std::max<i64>(1, std::min<i64>(c->num_sms * 8, (N() + 1023) / 1024)));
+  }
+  static bool al16(const void* q) { return reinterpret_cast<uintptr_t>(q) % 16 == 0; }
   void residual() {
     KScope ks_(c, "cg_residual");
-    cg_residual_k<TK, false><<<nbv(), kBlock, 0, c->stream>>>(N(), R.p, AP.p, part.p, st.p);
+    if (al16(R.p) && al16(AP.p))
+      cg_residual_k<TK, true><<<nbw(), kBlock, 0, c->stream>>>(N(), R.p, AP.p, part.p, st.p);
+    else
+      cg_residual_k<TK, false><<<nbv(), kBlock, 0, c->stream>>>(N(), R.p, AP.p, part.p, st.p);
     launched(c);
   }
   void update() {
     KScope ks_(c, "cg_update");
-    cg_update_k<TK, TX, false><<<nbv(), kBlock, 0, c->stream>>>(N(), X, Ploc.p, R.p, st.p);
+    if (al16(R.p) && al16(X) && al16(Ploc.p))
+      cg_update_k<TK, TX, true><<<nbw(), kBlock, 0, c->stream>>>(N(), X, Ploc.p, R.p, st.p);
+    else
+      cg_update_k<TK, TX, false><<<nbv(), kBlock, 0, c->stream>>>(N(), X, Ploc.p, R.p, st.p);
     launched(c);
   }
   // true residual: X halo first (Xloc = [X own | X halo]), then x1 -> U and the combine in residual mode
@@ -436,6 +461,7 @@ void decode_sharded_nccl(Ctx* c, Comm* cm, const TX* Xt, const std::vector<i64>&
   if (sh.nsend || sh.nh) nccl_exchange<TX>(cm, hp, p, sh.sendX.p, sh.Xloc.p + sh.nb * p, c->stream);
   sh.true_residual_partial(gr, gc);
   NCCL_OK(nccl().AllReduce(curv, curv, 1, ncclDouble, ncclSum, cm->nc, c->stream));
+  sh.finish();
   host = read_back(c, sh.st.p);
   const double rel = host.norm_b > 0.0 ? std::sqrt(host.curv) / host.norm_b : 0.0;
   *converged = rel <= cfg.pcg_tol ? 1 : 0;
@@ -527,6 +553,7 @@ void decode_sharded_emulated(Ctx* c, int G, const TX* Xt, const std::vector<i64>
   exchange(true);
   for (auto& s : sh) s->true_residual_partial(gr, gc);
   allreduce(1);
+  for (auto& s : sh) s->finish();
   host = read_back(c, sh[0]->st.p);
   const double rel = host.norm_b > 0.0 ? std::sqrt(host.curv) / host.norm_b : 0.0;
   *converged = rel <= cfg.pcg_tol ? 1 : 0;
