@@ -365,6 +365,28 @@ int cpcag_cuda_alternate_decode_sharded_emulated(cpcag_ctx ctx, int nranks, int 
                                                  cpcag_csr Lc, double lambda_k1_r, double lambda_k1_c,
                                                  const cpcag_decoder_config* cfg, const int64_t* bounds, void* X,
                                                  int* converged, int64_t* iterations, cpcag_shard_stats* stats);
+/* fista_solve (frpcag.hpp:46-47, frpcag.cpp:62-112) with the compressed
+ * matrix split into contiguous column blocks, one per rank (SURVEY.md 8e:
+ * "FISTA scalars all-reduced, X~ all-gathered").  Y (rows x cols), Lr, Lc and
+ * cfg are the same on every rank; bounds has nranks + 1 ascending entries
+ * 0 ... cols.  Each iteration a rank forms its block of S from the full Z,
+ * the blocks are all-gathered (grouped NCCL send/recv), the five scalars of
+ * the objective and the stopping rule are all-reduced on the device, and
+ * every rank forms the full Z_next locally.  X_block receives this rank's
+ * rows x (bounds[rank + 1] - bounds[rank]) block; objective and trace as
+ * cpcag_cuda_fista (identical on every rank).  S matches the single-GPU CSR
+ * path bit for bit per iteration; the scalars are summed in another order.
+ * Errors: the reference's fista messages, plus "sharded fista: ..." for a
+ * bad partition. */
+int cpcag_cuda_fista_sharded(cpcag_ctx ctx, cpcag_comm comm, int precision, const void* Y, int64_t rows,
+                             int64_t cols, cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg,
+                             const int64_t* bounds, void* X_block, double* objective, cpcag_solve_trace* trace);
+/* The same for `nranks` ranks emulated in one process on one GPU (device
+ * copies for the all-gather, a rank-ordered sum for the all-reduce, ranks run
+ * phase by phase).  X receives the whole rows x cols solution. */
+int cpcag_cuda_fista_sharded_emulated(cpcag_ctx ctx, int nranks, int precision, const void* Y, int64_t rows,
+                                      int64_t cols, cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg,
+                                      const int64_t* bounds, void* X, double* objective, cpcag_solve_trace* trace);
 /* Host only (no device): the halo plan of `rank` for L_c's CSR structure
  * (row_ptr n + 1, col_idx).  recv_counts[q] / send_counts[q]: columns this
  * rank receives from / sends to rank q; recv_cols (capacity n): their global

@@ -149,6 +149,10 @@ SIGNATURES = {
     "cpcag_cuda_alternate_decode_sharded_emulated": (C.c_int, [vp, C.c_int, C.c_int, vp, i64, i64, vp, vp, i64, i64,
                                                                vp, vp, dbl, dbl, C.POINTER(DecoderConfigC), vp, vp,
                                                                C.POINTER(C.c_int), ip, C.POINTER(ShardStatsC)]),
+    "cpcag_cuda_fista_sharded": (C.c_int, [vp, vp, C.c_int, vp, i64, i64, vp, vp, C.POINTER(FrpcagConfigC), vp, vp,
+                                           vp, C.POINTER(SolveTraceC)]),
+    "cpcag_cuda_fista_sharded_emulated": (C.c_int, [vp, C.c_int, C.c_int, vp, i64, i64, vp, vp,
+                                                    C.POINTER(FrpcagConfigC), vp, vp, vp, C.POINTER(SolveTraceC)]),
     "cpcag_cuda_gram_tf32x3": (C.c_int, [vp, vp, i64, i64, vp]),
     "cpcag_cuda_run_pipeline": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp,
                                           C.POINTER(PipelineConfigC), vp, vp, vp, vp, vp,

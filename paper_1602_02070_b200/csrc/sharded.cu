@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "decoder.cuh"
+#include "frpcag.cuh"
 
 namespace cpcag_cuda {
 
@@ -602,6 +603,306 @@ std::vector<i64> fetch_list(const int64_t* src, i64 k) {
   return v;
 }
 
+
+// ------------------------------------------------------------------ column-sharded FISTA (frpcag.cpp:62-112)
+// the compressed problem (rows x cols) split into contiguous
+// column blocks, one per rank.  Per iteration a rank
+//   1. forms its block of S = prox(Z - step grad g(Z)) from the full Z
+//      (the Z L_c term reads every column of Z: the Kron-reduced L_c is dense),
+//   2. all-gathers S (grouped send/recv of the blocks, ragged blocks allowed),
+//   3. sums its block's share of the objective's three terms and of
+//      ||Z||^2, ||Z_next - Z||^2 (one kernel, fixed order),
+//   4. all-reduces those five scalars on the device,
+//   5. decides (one thread: trace, t, coef, stop) and forms the full
+//      Z_next = S + coef (S - S_prev) locally (elementwise, no exchange).
+// The state lives on the device; the host polls it every kShfPoll iterations.
+// S is bit-identical to the single-GPU CSR path (same element formulas); only
+// the five scalars are summed in another order.
+struct ShfState {
+  double t, coef, frc;
+  i64 j, iterations;
+  int done, converged, err, pad;
+  i64 err_j;
+  unsigned cnt[2];
+};
+constexpr int kShfPoll = 16;
+
+template <typename T>
+__global__ void shf_grad_prox_k(i64 rows, i64 c0, i64 c1, Pull<T> Lr, Pull<T> Lc, T s_r, T s_c, int use_r,
+                                int use_c, int loss, T step, const T* __restrict__ Z, const T* __restrict__ Y,
+                                T* __restrict__ S, const ShfState* st) {
+  if (st->done) return;
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (i64 c = c0 + blockIdx.y; c < c1; c += gridDim.y) {
+    const i64 at = i + c * rows;
+    const T g = grad_elem(Lr, Lc, s_r, s_c, use_r, use_c, Z, rows, i, c);
+    const T arg = sub_rn(Z[at], mul_rn(step, g));
+    S[at] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[at], step) : prox_l1_elem(arg, Y[at], step);
+  }
+}
+
+// scal[0..4] = this block's {data term, <S, S L_c>, <S, L_r S>, ||Z||^2, ||Z_next - Z||^2}.
+template <typename T>
+__global__ void shf_block_sums_k(i64 rows, i64 c0, i64 c1, Pull<T> Lr, Pull<T> Lc, int use_r, int use_c, int loss,
+                                 const T* __restrict__ S, const T* __restrict__ Sp, const T* __restrict__ Z,
+                                 const T* __restrict__ Y, double* partials, double* scal, ShfState* st) {
+  if (st->done) return;
+  const double t = st->t;
+  const T coef = static_cast<T>((t - 1.0) / (0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t))));
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x;
+  if (i < rows) {
+    for (i64 c = c0 + blockIdx.y; c < c1; c += gridDim.y) {
+      const i64 at = i + c * rows;
+      const T sv = S[at];
+      const double x = static_cast<double>(sv);
+      const double e = static_cast<double>(Y[at]) - x;
+      s[0] += loss == CPCAG_LOSS_L2 ? e * e : fabs(e);
+      if (use_c) s[1] += static_cast<double>(pull_right(Lc.rp[c], Lc.rp[c + 1], Lc.ci, Lc.v, S, rows, i)) * x;
+      if (use_r) s[2] += static_cast<double>(pull_left(Lr.rp[i], Lr.rp[i + 1], Lr.ci, Lr.v, S + c * rows)) * x;
+      const T zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[at])));
+      const T z = Z[at];
+      const double zd = static_cast<double>(z);
+      const double dd = static_cast<double>(sub_rn(zn, z));
+      s[3] += zd * zd;
+      s[4] += dd * dd;
+    }
+  }
+  double tot[5];
+  if (grid_sum_last<5>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) scal[q] = tot[q];
+  }
+}
+
+// frpcag.cpp:84-110 on the all-reduced scalars (identical on every rank).
+__global__ void shf_decide_k(const double* scal, double gamma_r, double gamma_c, double tol, i64 max_iter,
+                             double* trace, ShfState* st) {
+  if (st->done) return;
+  double val = scal[0];
+  if (gamma_c != 0.0) val += gamma_c * scal[1];
+  if (gamma_r != 0.0) val += gamma_r * scal[2];
+  const i64 j = st->j;
+  if (!isfinite(val)) {
+    st->err = 1;
+    st->err_j = j;
+    st->done = 1;
+    return;
+  }
+  trace[j - 1] = val;
+  st->iterations = j;
+  const double t = st->t;
+  const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+  st->coef = (t - 1.0) / tn;
+  const double denom = scal[3], change = scal[4];
+  st->frc = denom > 0.0 ? change / denom : change;
+  if (change < tol * denom) {
+    st->converged = 1;
+    st->done = 1;
+    return;
+  }
+  st->t = tn;
+  st->j = j + 1;
+  if (st->j > max_iter) st->done = 1;
+}
+
+template <typename T>
+__global__ void shf_update_k(i64 N, const T* __restrict__ S, const T* __restrict__ Sp, T* __restrict__ Z,
+                             const ShfState* st) {
+  if (st->done) return;
+  const T coef = static_cast<T>(st->coef);
+  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < N; q += (i64)gridDim.x * blockDim.x) {
+    const T sv = S[q];
+    Z[q] = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[q])));
+  }
+}
+
+// Emulated all-reduce: rank-ordered sum of the G five-scalar records, written to all.
+__global__ void shf_emu_allreduce_k(double* scal_all, int G) {
+  const int q = threadIdx.x;
+  if (q >= 5) return;
+  double s = 0.0;
+  for (int g = 0; g < G; ++g) s += scal_all[5 * g + q];
+  for (int g = 0; g < G; ++g) scal_all[5 * g + q] = s;
+}
+
+double shf_step(Ctx* c, Csr* Lr, Csr* Lc, const cpcag_frpcag_config& cfg) {
+  if (cfg.step > 0.0) return cfg.step;
+  // frpcag.cpp:70-75, computed by every rank on the whole (replicated) Laplacians.
+  double nc = 0.0, nr = 0.0;
+  if (cfg.gamma_c != 0.0 && cfg.gamma_r != 0.0)
+    power_norm_pair(c, Lc, Lr, 1e-7, 42, 50000, &nc, &nr);
+  else if (cfg.gamma_c != 0.0)
+    nc = power_norm(c, Lc, 1e-7, 42, 50000);
+  else if (cfg.gamma_r != 0.0)
+    nr = power_norm(c, Lr, 1e-7, 42, 50000);
+  const double beta = 2.0 * cfg.gamma_c * nc + 2.0 * cfg.gamma_r * nr;
+  return beta > 0.0 ? 1.0 / beta : 1.0;
+}
+
+void shf_check(i64 rows, i64 cols, Csr* Lr, Csr* Lc, const cpcag_frpcag_config* cfg, const i64* bd, int G) {
+  if (!cfg) invalid("null argument");
+  frpcag_check_dims(rows, cols, Lr, Lc);
+  if (cfg->gamma_r < 0.0 || cfg->gamma_c < 0.0) invalid("fista: negative regularization weight");
+  if (cfg->tol <= 0.0) invalid("fista: stopping tolerance must be positive");
+  if (cfg->max_iter < 1) invalid("fista: max_iter must be >= 1");
+  if (G < 1) invalid("sharded fista: at least one rank");
+  if (bd[0] != 0 || bd[G] != cols) invalid("sharded fista: bounds must run from 0 to cols");
+  for (int g = 0; g < G; ++g)
+    if (bd[g + 1] < bd[g]) invalid("sharded fista: bounds must ascend");
+}
+
+// One rank's buffers and the three block-local launches of an iteration.
+template <typename T>
+struct ShfRank {
+  i64 rows = 0, cols = 0, c0 = 0, c1 = 0;
+  DevBuf<T> S[2], Z;
+  DevBuf<double> part, trace;
+  DevBuf<ShfState> st;
+  double* scal = nullptr;
+  dim3 grid;
+  unsigned nb1 = 1;
+
+  void init(Ctx* c, const T* Y, i64 r, i64 cl, i64 b0, i64 b1, i64 max_iter, double* scal_dev) {
+    rows = r, cols = cl, c0 = b0, c1 = b1, scal = scal_dev;
+    const i64 N = rows * cols;
+    S[0].alloc(c, N), S[1].alloc(c, N), Z.alloc(c, N);
+    CUDA_OK(cudaMemcpyAsync(S[0].p, Y, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OK(cudaMemcpyAsync(Z.p, Y, sizeof(T) * N, cudaMemcpyDeviceToDevice, c->stream));
+    trace.alloc(c, max_iter);
+    ShfState init{};
+    init.t = 1.0;
+    init.j = 1;
+    st.alloc(c, 1);
+    CUDA_OK(cudaMemcpyAsync(st.p, &init, sizeof(init), cudaMemcpyHostToDevice, c->stream));
+    const unsigned gx = blocks_for(std::max<i64>(rows, 1));
+    const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx);
+    grid = dim3(gx, static_cast<unsigned>(std::max<i64>(1, std::min<i64>({c1 - c0, ycap, 65535}))));
+    nb1 = stride_blocks(c, N);
+    part.alloc(c, 5 * static_cast<size_t>(grid.x) * grid.y);
+  }
+  void grad_prox(Ctx* c, const Pull<T>& pr, const Pull<T>& pc, const cpcag_frpcag_config& cfg, T step, const T* Y,
+                 i64 j) {
+    if (c1 == c0) return;
+    KScope ks_(c, "shf_grad_prox");
+    shf_grad_prox_k<T><<<grid, kBlock, 0, c->stream>>>(
+        rows, c0, c1, pr, pc, static_cast<T>(2.0 * cfg.gamma_r), static_cast<T>(2.0 * cfg.gamma_c),
+        cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, cfg.loss, step, Z.p, Y, S[j & 1].p, st.p);
+    launched(c);
+  }
+  void block_sums(Ctx* c, const Pull<T>& pr, const Pull<T>& pc, const cpcag_frpcag_config& cfg, const T* Y, i64 j) {
+    KScope ks_(c, "shf_block_sums");
+    shf_block_sums_k<T><<<grid, kBlock, 0, c->stream>>>(rows, c0, c1, pr, pc, cfg.gamma_r != 0.0, cfg.gamma_c != 0.0,
+                                                        cfg.loss, S[j & 1].p, S[(j - 1) & 1].p, Z.p, Y, part.p, scal,
+                                                        st.p);
+    launched(c);
+  }
+  void decide_update(Ctx* c, const cpcag_frpcag_config& cfg, i64 j) {
+    KScope ks_(c, "shf_update");
+    shf_decide_k<<<1, 1, 0, c->stream>>>(scal, cfg.gamma_r, cfg.gamma_c, cfg.tol, cfg.max_iter, trace.p, st.p);
+    launched(c);
+    shf_update_k<T><<<nb1, kBlock, 0, c->stream>>>(rows * cols, S[j & 1].p, S[(j - 1) & 1].p, Z.p, st.p);
+    launched(c);
+  }
+};
+
+template <typename T>
+void shf_finish(Ctx* c, ShfRank<T>& R, const ShfState& host, double step, T* X, i64 col0, i64 col1,
+                double* objective_host, cpcag_solve_trace* trace) {
+  if (host.err)
+    runtime("fista: diverged (non-finite objective at iteration " + std::to_string(host.err_j) +
+            "); step too large");
+  const i64 J = host.iterations;
+  if (col1 > col0)
+    CUDA_OK(cudaMemcpyAsync(X, R.S[J & 1].p + col0 * R.rows, sizeof(T) * R.rows * (col1 - col0),
+                            cudaMemcpyDeviceToDevice, c->stream));
+  if (objective_host && J > 0)
+    CUDA_OK(cudaMemcpyAsync(objective_host, R.trace.p, sizeof(double) * J, cudaMemcpyDefault, c->stream));
+  sync(c);
+  trace->iterations = J;
+  trace->converged = host.converged;
+  trace->final_rel_change = host.frc;
+  trace->step = step;
+}
+
+void shf_empty(const cpcag_frpcag_config& cfg, double step, double* objective_host, cpcag_solve_trace* trace) {
+  // As the single-GPU path: every norm is zero, 0 < 0 is false, max_iter zero objectives.
+  if (objective_host) std::fill(objective_host, objective_host + cfg.max_iter, 0.0);
+  trace->iterations = cfg.max_iter;
+  trace->converged = 0;
+  trace->final_rel_change = 0.0;
+  trace->step = step;
+}
+
+template <typename T>
+void fista_sharded_nccl(Ctx* c, Comm* cm, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
+                        const cpcag_frpcag_config& cfg, const i64* bd, T* X_block, double* objective_host,
+                        cpcag_solve_trace* trace) {
+  const double step = shf_step(c, Lr, Lc, cfg);
+  if (rows * cols == 0) return shf_empty(cfg, step, objective_host, trace);
+  const int G = cm->size, me = cm->rank;
+  DevBuf<double> scal(c, 5);
+  ShfRank<T> R;
+  R.init(c, Y, rows, cols, bd[me], bd[me + 1], cfg.max_iter, scal.p);
+  const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
+  ShfState host{};
+  for (i64 j0 = 1; j0 <= cfg.max_iter; j0 += kShfPoll) {
+    const i64 j1 = std::min<i64>(cfg.max_iter, j0 + kShfPoll - 1);
+    for (i64 j = j0; j <= j1; ++j) {
+      R.grad_prox(c, pr, pc, cfg, static_cast<T>(step), Y, j);
+      if (G > 1) {  // all-gather of the S blocks
+        T* S = R.S[j & 1].p;
+        NCCL_OK(nccl().GroupStart());
+        for (int q = 0; q < G; ++q) {
+          if (q == me) continue;
+          const i64 mine = (bd[me + 1] - bd[me]) * rows, theirs = (bd[q + 1] - bd[q]) * rows;
+          if (mine) NCCL_OK(nccl().Send(S + bd[me] * rows, static_cast<size_t>(mine), nccl_type<T>(), q, cm->nc, c->stream));
+          if (theirs) NCCL_OK(nccl().Recv(S + bd[q] * rows, static_cast<size_t>(theirs), nccl_type<T>(), q, cm->nc, c->stream));
+        }
+        NCCL_OK(nccl().GroupEnd());
+      }
+      R.block_sums(c, pr, pc, cfg, Y, j);
+      if (G > 1) NCCL_OK(nccl().AllReduce(scal.p, scal.p, 5, ncclDouble, ncclSum, cm->nc, c->stream));
+      R.decide_update(c, cfg, j);
+    }
+    host = read_back(c, R.st.p);
+    if (host.done) break;
+  }
+  shf_finish(c, R, host, step, X_block, bd[me], bd[me + 1], objective_host, trace);
+}
+
+template <typename T>
+void fista_sharded_emulated(Ctx* c, int G, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
+                            const cpcag_frpcag_config& cfg, const i64* bd, T* X, double* objective_host,
+                            cpcag_solve_trace* trace) {
+  const double step = shf_step(c, Lr, Lc, cfg);
+  if (rows * cols == 0) return shf_empty(cfg, step, objective_host, trace);
+  DevBuf<double> scal(c, 5 * static_cast<size_t>(G));
+  std::vector<ShfRank<T>> R(static_cast<size_t>(G));
+  for (int g = 0; g < G; ++g) R[g].init(c, Y, rows, cols, bd[g], bd[g + 1], cfg.max_iter, scal.p + 5 * g);
+  const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
+  ShfState host{};
+  for (i64 j0 = 1; j0 <= cfg.max_iter; j0 += kShfPoll) {
+    const i64 j1 = std::min<i64>(cfg.max_iter, j0 + kShfPoll - 1);
+    for (i64 j = j0; j <= j1; ++j) {
+      for (int g = 0; g < G; ++g) R[g].grad_prox(c, pr, pc, cfg, static_cast<T>(step), Y, j);
+      for (int g = 0; g < G; ++g)  // the all-gather as device copies of rank g's block to every other rank
+        for (int q = 0; q < G; ++q)
+          if (q != g && bd[g + 1] > bd[g])
+            CUDA_OK(cudaMemcpyAsync(R[q].S[j & 1].p + bd[g] * rows, R[g].S[j & 1].p + bd[g] * rows,
+                                    sizeof(T) * rows * (bd[g + 1] - bd[g]), cudaMemcpyDeviceToDevice, c->stream));
+      for (int g = 0; g < G; ++g) R[g].block_sums(c, pr, pc, cfg, Y, j);
+      shf_emu_allreduce_k<<<1, 32, 0, c->stream>>>(scal.p, G);
+      launched(c);
+      for (int g = 0; g < G; ++g) R[g].decide_update(c, cfg, j);
+    }
+    host = read_back(c, R[0].st.p);
+    if (host.done) break;
+  }
+  shf_finish(c, R[G - 1], host, step, X, 0, cols, objective_host, trace);
+}
+
 }  // namespace cpcag_cuda
 
 using namespace cpcag_cuda;
@@ -712,6 +1013,70 @@ extern "C" int cpcag_cuda_alternate_decode_sharded_emulated(cpcag_ctx ctx, int n
                                           stats);
       x.flush(c);
       sync(c);
+    });
+  });
+}
+
+template <typename F>
+static int shf_dispatch(int precision, F&& f) {
+  if (precision == CPCAG_F64) return f(double{});
+  if (precision == CPCAG_F32) return f(float{});
+  set_last_error("unknown precision flag");
+  return CPCAG_ERR_INVALID_ARGUMENT;
+}
+
+template <typename T, typename Body>
+static void shf_call(Ctx* c, const void* Y, int64_t rows, int64_t cols, const cpcag_frpcag_config* cfg, void* X,
+                     int64_t x_elems, double* objective, cpcag_solve_trace* trace, Body&& body) {
+  InView<T> y(c, static_cast<const T*>(Y), static_cast<size_t>(rows * cols));
+  OutView<T> x(c, static_cast<T*>(X), static_cast<size_t>(x_elems));
+  std::vector<double> obj_host;
+  double* obj_dst = objective;
+  if (objective && is_device_ptr(objective)) {
+    obj_host.resize(static_cast<size_t>(std::max<int64_t>(cfg->max_iter, 1)));
+    obj_dst = obj_host.data();
+  }
+  body(y.d, x.d, obj_dst);
+  x.flush(c);
+  if (!obj_host.empty() && trace->iterations > 0)
+    CUDA_OK(cudaMemcpyAsync(objective, obj_host.data(), sizeof(double) * trace->iterations, cudaMemcpyHostToDevice,
+                            c->stream));
+  sync(c);
+}
+
+extern "C" int cpcag_cuda_fista_sharded(cpcag_ctx ctx, cpcag_comm comm, int precision, const void* Y, int64_t rows,
+                                        int64_t cols, cpcag_csr Lr, cpcag_csr Lc, const cpcag_frpcag_config* cfg,
+                                        const int64_t* bounds, void* X_block, double* objective,
+                                        cpcag_solve_trace* trace) {
+  return shf_dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      Comm* cm = reinterpret_cast<Comm*>(comm);
+      if (!cm || !bounds || !trace) invalid("null argument");
+      shf_check(rows, cols, as_csr(Lr), as_csr(Lc), cfg, bounds, cm->size);
+      const int64_t nb = bounds[cm->rank + 1] - bounds[cm->rank];
+      shf_call<T>(c, Y, rows, cols, cfg, X_block, rows * nb, objective, trace, [&](const T* y, T* x, double* obj) {
+        fista_sharded_nccl<T>(c, cm, y, rows, cols, as_csr(Lr), as_csr(Lc), *cfg, bounds, x, obj, trace);
+      });
+    });
+  });
+}
+
+extern "C" int cpcag_cuda_fista_sharded_emulated(cpcag_ctx ctx, int nranks, int precision, const void* Y, int64_t rows,
+                                                 int64_t cols, cpcag_csr Lr, cpcag_csr Lc,
+                                                 const cpcag_frpcag_config* cfg, const int64_t* bounds, void* X,
+                                                 double* objective, cpcag_solve_trace* trace) {
+  return shf_dispatch(precision, [&](auto tag) {
+    using T = decltype(tag);
+    return guard([&] {
+      Ctx* c = as_ctx(ctx);
+      if (!bounds || !trace) invalid("null argument");
+      if (nranks < 1) invalid("sharded fista: at least one rank");
+      shf_check(rows, cols, as_csr(Lr), as_csr(Lc), cfg, bounds, nranks);
+      shf_call<T>(c, Y, rows, cols, cfg, X, rows * cols, objective, trace, [&](const T* y, T* x, double* obj) {
+        fista_sharded_emulated<T>(c, nranks, y, rows, cols, as_csr(Lr), as_csr(Lc), *cfg, bounds, x, obj, trace);
+      });
     });
   });
 }

@@ -16,7 +16,10 @@ per 32 iterations.  This module holds the Python side of that C-ABI:
     torch.distributed (rank 0's ncclUniqueId is broadcast);
   * `alternate_decode_sharded`: this rank's block of the solution;
   * `alternate_decode_sharded_emulated`: all ranks in one process on one GPU
-    (device copies for the exchange), for tests of the multi-rank logic.
+    (device copies for the exchange), for tests of the multi-rank logic;
+  * `fista_solve_sharded` / `fista_solve_sharded_emulated`: FRPCAG's FISTA on
+    column blocks of the compressed matrix (S blocks all-gathered, the five
+    objective / stopping scalars all-reduced on the device).
 """
 from __future__ import annotations
 
@@ -173,3 +176,60 @@ def alternate_decode_sharded_emulated(Xt, plan, Lr, Lc, gap_r, gap_c, cfg, nrank
         om_c.ctypes.data if om_c.size else None, plan.p, plan.n, Lr.handle, Lc.handle, float(gap_r.lambda_k1),
         float(gap_c.lambda_k1), C.byref(dc), bd.ctypes.data, op, C.byref(cv), C.byref(it), C.byref(st)))
     return AlternateDecodeResult(res, bool(cv.value), int(it.value)), _stats(st)
+
+
+@dataclass
+class ShardedFistaResult:
+    X_block: object      # rows x (c1 - c0) block of this rank
+    c0: int
+    c1: int
+    trace: object        # SolveTrace, identical on every rank
+
+
+def fista_solve_sharded(Y, Lr, Lc, cfg, comm: ShardComm, bounds=None, precision=None, ctx=None) -> ShardedFistaResult:
+    """frpcag.cpp:62-112 for this rank's column block of the compressed
+    matrix.  Y, Lr, Lc and cfg are the same on every rank."""
+    from .cpcag import SolveTrace, _ctx, _In, _is_cuda, _out, _precision, _torch_device
+
+    prec = _precision(Y, precision)
+    y = _In(Y, prec)
+    if len(y.shape) != 2:
+        raise ValueError("fista: Y must be a matrix")
+    rows, cols = y.shape
+    bd = np.ascontiguousarray(bounds_of(cols, comm.world) if bounds is None else bounds, np.int64)
+    if bd.size != comm.world + 1:
+        raise ValueError("sharded fista: bounds must hold world + 1 entries")
+    c0, c1 = int(bd[comm.rank]), int(bd[comm.rank + 1])
+    out, op = _out(_is_cuda(Y), _torch_device(Y), (rows, max(c1 - c0, 0)), prec)
+    obj = np.zeros(max(int(cfg.max_iter), 1))
+    tr = N.SolveTraceC()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_fista_sharded(_ctx(ctx), comm.h, prec, y.ptr, rows, cols, Lr.handle, Lc.handle,
+                                             C.byref(c), bd.ctypes.data, op, obj.ctypes.data, C.byref(tr)))
+    n = int(tr.iterations)
+    return ShardedFistaResult(out, c0, c1, SolveTrace(list(obj[:n]), n, bool(tr.converged),
+                                                      float(tr.final_rel_change), float(tr.step)))
+
+
+def fista_solve_sharded_emulated(Y, Lr, Lc, cfg, nranks: int, bounds=None, precision=None, ctx=None):
+    """All `nranks` ranks of the sharded FISTA in this process on one GPU
+    (tests).  Returns (X, SolveTrace) like fista_solve."""
+    from .cpcag import SolveTrace, _ctx, _In, _is_cuda, _out, _precision, _torch_device
+
+    prec = _precision(Y, precision)
+    y = _In(Y, prec)
+    if len(y.shape) != 2:
+        raise ValueError("fista: Y must be a matrix")
+    rows, cols = y.shape
+    bd = np.ascontiguousarray(bounds_of(cols, nranks) if bounds is None else bounds, np.int64)
+    if bd.size != nranks + 1:
+        raise ValueError("sharded fista: bounds must hold world + 1 entries")
+    out, op = _out(_is_cuda(Y), _torch_device(Y), (rows, cols), prec)
+    obj = np.zeros(max(int(cfg.max_iter), 1))
+    tr = N.SolveTraceC()
+    c = cfg.c()
+    N.check(N.lib().cpcag_cuda_fista_sharded_emulated(_ctx(ctx), int(nranks), prec, y.ptr, rows, cols, Lr.handle,
+                                                      Lc.handle, C.byref(c), bd.ctypes.data, op, obj.ctypes.data,
+                                                      C.byref(tr)))
+    n = int(tr.iterations)
+    return out, SolveTrace(list(obj[:n]), n, bool(tr.converged), float(tr.final_rel_change), float(tr.step))
