@@ -34,6 +34,7 @@
 
 #include "decoder.cuh"
 #include "frpcag.cuh"
+#include "fista_dense.cuh"
 
 namespace cpcag_cuda {
 
@@ -676,6 +677,78 @@ __global__ void shf_block_sums_k(i64 rows, i64 c0, i64 c1, Pull<T> Lr, Pull<T> L
   }
 }
 
+// Dense-operator forms of the two block kernels (Kron-reduced Laplacians are
+// near dense; fista_dense.cuh): one 32 x 32 output tile per CTA, tiles of the
+// block's columns only; fp64 sums run over k in ascending order with explicit
+// multiply then add, i.e. the CSR-order sums plus exact zeros.
+template <typename T>
+__global__ void __launch_bounds__(256) shf_dense_grad_prox_k(i64 rr, i64 rc, i64 b0, i64 b1, const T* __restrict__ Lr,
+                                                             const T* __restrict__ Lc, T s_r, T s_c, int use_r,
+                                                             int use_c, int loss, T step, const T* __restrict__ Z,
+                                                             const T* __restrict__ Y, T* __restrict__ S,
+                                                             const ShfState* st) {
+  if (st->done) return;
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = b0 + static_cast<i64>(blockIdx.y) * kDT;
+  T acc1[2][2], acc2[2][2];
+  dual_gemm_tile(Lr, Lc, Z, rr, rc, use_r, use_c, i0, c0, acc1, acc2);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      if (i >= rr || c >= b1) continue;
+      const i64 at = i + c * rr;
+      T g = T(0);
+      if (use_c) g = add_rn(g, mul_rn(s_c, acc2[a][b]));
+      if (use_r) g = add_rn(g, mul_rn(s_r, acc1[a][b]));
+      const T arg = sub_rn(Z[at], mul_rn(step, g));
+      S[at] = loss == CPCAG_LOSS_L2 ? prox_l2_elem(arg, Y[at], step) : prox_l1_elem(arg, Y[at], step);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) shf_dense_block_sums_k(i64 rr, i64 rc, i64 b0, i64 b1,
+                                                              const T* __restrict__ Lr, const T* __restrict__ Lc,
+                                                              int use_r, int use_c, int loss, const T* __restrict__ S,
+                                                              const T* __restrict__ Sp, const T* __restrict__ Z,
+                                                              const T* __restrict__ Y, double* partials, double* scal,
+                                                              ShfState* st) {
+  if (st->done) return;
+  const double t = st->t;
+  const T coef = static_cast<T>((t - 1.0) / (0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t))));
+  const i64 i0 = static_cast<i64>(blockIdx.x) * kDT, c0 = b0 + static_cast<i64>(blockIdx.y) * kDT;
+  T acc1[2][2], acc2[2][2];
+  dual_gemm_tile(Lr, Lc, S, rr, rc, use_r, use_c, i0, c0, acc1, acc2);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double s[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const i64 i = i0 + ty + 16 * a, c = c0 + tx + 16 * b;
+      if (i >= rr || c >= b1) continue;
+      const i64 at = i + c * rr;
+      const T sv = S[at];
+      const double x = static_cast<double>(sv);
+      const double e = static_cast<double>(Y[at]) - x;
+      s[0] += loss == CPCAG_LOSS_L2 ? e * e : fabs(e);
+      s[1] += static_cast<double>(acc2[a][b]) * x;
+      s[2] += static_cast<double>(acc1[a][b]) * x;
+      const T zn = add_rn(sv, mul_rn(coef, sub_rn(sv, Sp[at])));
+      const T z = Z[at];
+      const double zd = static_cast<double>(z);
+      const double dd = static_cast<double>(sub_rn(zn, z));
+      s[3] += zd * zd;
+      s[4] += dd * dd;
+    }
+  double tot[5];
+  if (grid_sum_last<5>(s, partials, &st->cnt[0], tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) scal[q] = tot[q];
+  }
+}
+
 // frpcag.cpp:84-110 on the all-reduced scalars (identical on every rank).
 __global__ void shf_decide_k(const double* scal, double gamma_r, double gamma_c, double tol, i64 max_iter,
                              double* trace, ShfState* st) {
@@ -761,8 +834,9 @@ struct ShfRank {
   DevBuf<double> part, trace;
   DevBuf<ShfState> st;
   double* scal = nullptr;
-  dim3 grid;
+  dim3 grid, gd;
   unsigned nb1 = 1;
+  const T *Dr = nullptr, *Dc = nullptr;  // dense images of Lr, Lc (null: CSR pulls)
 
   void init(Ctx* c, const T* Y, i64 r, i64 cl, i64 b0, i64 b1, i64 max_iter, double* scal_dev) {
     rows = r, cols = cl, c0 = b0, c1 = b1, scal = scal_dev;
@@ -780,12 +854,21 @@ struct ShfRank {
     const i64 ycap = std::max<i64>(1, (static_cast<i64>(c->num_sms) * 16) / gx);
     grid = dim3(gx, static_cast<unsigned>(std::max<i64>(1, std::min<i64>({c1 - c0, ycap, 65535}))));
     nb1 = stride_blocks(c, N);
-    part.alloc(c, 5 * static_cast<size_t>(grid.x) * grid.y);
+    gd = dim3(static_cast<unsigned>((rows + kDT - 1) / kDT),
+              static_cast<unsigned>(std::max<i64>(1, (c1 - c0 + kDT - 1) / kDT)));
+    part.alloc(c, 5 * std::max(static_cast<size_t>(grid.x) * grid.y, static_cast<size_t>(gd.x) * gd.y));
   }
   void grad_prox(Ctx* c, const Pull<T>& pr, const Pull<T>& pc, const cpcag_frpcag_config& cfg, T step, const T* Y,
                  i64 j) {
     if (c1 == c0) return;
     KScope ks_(c, "shf_grad_prox");
+    if (Dr) {
+      shf_dense_grad_prox_k<T><<<gd, 256, 0, c->stream>>>(
+          rows, cols, c0, c1, Dr, Dc, static_cast<T>(2.0 * cfg.gamma_r), static_cast<T>(2.0 * cfg.gamma_c),
+          cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, cfg.loss, step, Z.p, Y, S[j & 1].p, st.p);
+      launched(c);
+      return;
+    }
     shf_grad_prox_k<T><<<grid, kBlock, 0, c->stream>>>(
         rows, c0, c1, pr, pc, static_cast<T>(2.0 * cfg.gamma_r), static_cast<T>(2.0 * cfg.gamma_c),
         cfg.gamma_r != 0.0, cfg.gamma_c != 0.0, cfg.loss, step, Z.p, Y, S[j & 1].p, st.p);
@@ -793,6 +876,13 @@ struct ShfRank {
   }
   void block_sums(Ctx* c, const Pull<T>& pr, const Pull<T>& pc, const cpcag_frpcag_config& cfg, const T* Y, i64 j) {
     KScope ks_(c, "shf_block_sums");
+    if (Dr) {
+      shf_dense_block_sums_k<T><<<gd, 256, 0, c->stream>>>(rows, cols, c0, c1, Dr, Dc, cfg.gamma_r != 0.0,
+                                                           cfg.gamma_c != 0.0, cfg.loss, S[j & 1].p,
+                                                           S[(j - 1) & 1].p, Z.p, Y, part.p, scal, st.p);
+      launched(c);
+      return;
+    }
     shf_block_sums_k<T><<<grid, kBlock, 0, c->stream>>>(rows, c0, c1, pr, pc, cfg.gamma_r != 0.0, cfg.gamma_c != 0.0,
                                                         cfg.loss, S[j & 1].p, S[(j - 1) & 1].p, Z.p, Y, part.p, scal,
                                                         st.p);
@@ -835,6 +925,16 @@ void shf_empty(const cpcag_frpcag_config& cfg, double step, double* objective_ho
   trace->step = step;
 }
 
+// Dense images when both Laplacians are >= 25 % full and exactly symmetric
+// (the one-GPU path's rule, fista.cu).
+template <typename T>
+bool shf_densify(Ctx* c, Csr* Lr, Csr* Lc, DevBuf<T>& Dr, DevBuf<T>& Dc) {
+  if (!(dense_worthwhile(Lr) && dense_worthwhile(Lc) && csr_symmetric(c, Lr) && csr_symmetric(c, Lc))) return false;
+  densify<T>(c, Lr, Dr);
+  densify<T>(c, Lc, Dc);
+  return true;
+}
+
 template <typename T>
 void fista_sharded_nccl(Ctx* c, Comm* cm, const T* Y, i64 rows, i64 cols, Csr* Lr, Csr* Lc,
                         const cpcag_frpcag_config& cfg, const i64* bd, T* X_block, double* objective_host,
@@ -845,6 +945,8 @@ void fista_sharded_nccl(Ctx* c, Comm* cm, const T* Y, i64 rows, i64 cols, Csr* L
   DevBuf<double> scal(c, 5);
   ShfRank<T> R;
   R.init(c, Y, rows, cols, bd[me], bd[me + 1], cfg.max_iter, scal.p);
+  DevBuf<T> Dr, Dc;
+  if (shf_densify<T>(c, Lr, Lc, Dr, Dc)) R.Dr = Dr.p, R.Dc = Dc.p;
   const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
   ShfState host{};
   for (i64 j0 = 1; j0 <= cfg.max_iter; j0 += kShfPoll) {
@@ -881,6 +983,9 @@ void fista_sharded_emulated(Ctx* c, int G, const T* Y, i64 rows, i64 cols, Csr* 
   DevBuf<double> scal(c, 5 * static_cast<size_t>(G));
   std::vector<ShfRank<T>> R(static_cast<size_t>(G));
   for (int g = 0; g < G; ++g) R[g].init(c, Y, rows, cols, bd[g], bd[g + 1], cfg.max_iter, scal.p + 5 * g);
+  DevBuf<T> Dr, Dc;
+  if (shf_densify<T>(c, Lr, Lc, Dr, Dc))
+    for (int g = 0; g < G; ++g) R[g].Dr = Dr.p, R[g].Dc = Dc.p;
   const Pull<T> pr = make_pull<T>(c, Lr, false), pc = make_pull<T>(c, Lc, true);
   ShfState host{};
   for (i64 j0 = 1; j0 <= cfg.max_iter; j0 += kShfPoll) {

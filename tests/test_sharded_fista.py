@@ -203,6 +203,34 @@ def test_sharded_fista_errors():
                                      ctx=ctx)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("world", [1, 3])
+def test_sharded_fista_dense_operator_path(world, prec):
+    """Kron-reduced (near dense) Laplacians: the block kernels' tiled dense
+    form, 32-column tiles that straddle ragged block ends."""
+    import paper_1602_02070_b200 as P
+    from paper_1602_02070_b200.sharded import fista_solve_sharded_emulated
+
+    ctx = P.Context(0)
+    Lr_full, Lc_full = knn_laplacian(300, 3, 10, 31), knn_laplacian(240, 3, 10, 32)
+    plan = O.draw_plan(300, 240, 75, 60, seed=5)
+    Lr, Lc = O.kron_reduce(Lr_full, plan.omega_r, 1e-11), O.kron_reduce(Lc_full, plan.omega_c, 1e-11)
+    assert Lr.nnz >= 0.25 * 75 * 75 and Lc.nnz >= 0.25 * 60 * 60
+    dt = np.float64 if prec == "f64" else np.float32
+    Y = (np.random.default_rng(4).standard_normal((75, 60)) * 3.0).astype(dt)
+    cfg = P.FrpcagConfig(gamma_r=8.0, gamma_c=8.0, tol=1e-300, max_iter=150)
+    bd = np.array([0, 60]) if world == 1 else np.array([0, 7, 41, 60])
+    dLr, dLc = to_device(ctx, Lr), to_device(ctx, Lc)
+    X, tr = fista_solve_sharded_emulated(Y, dLr, dLc, cfg, world, bounds=bd, ctx=ctx)
+    Xo, tro = O.fista_solve(Y.astype(np.float64), Lr, Lc, O.FrpcagConfig(8.0, 8.0, "l1", 1e-300, 150))
+    assert tr.iterations == 150
+    assert rel(X, Xo) <= (1e-9 if prec == "f64" else 1e-4)
+    assert np.allclose(tr.objective, tro.objective, rtol=1e-9 if prec == "f64" else 1e-4)
+    X1, _ = P.fista_solve(Y, dLr, dLc, cfg, ctx=ctx)  # the one-GPU (persistent) solve sums in another order
+    assert rel(X, X1) <= (1e-8 if prec == "f64" else 1e-4)
+
+
 def _nccl_worker(port, out):
     import torch
     import torch.distributed as dist
