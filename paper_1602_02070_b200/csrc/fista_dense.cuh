@@ -31,18 +31,30 @@ __device__ __forceinline__ void dual_gemm_tile(const T* __restrict__ Lr, const T
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b) acc1[a][b] = acc2[a][b] = T(0);
+  // The next chunk's eight operands are loaded into registers while the
+  // current chunk is multiplied (the k-loop is serial per CTA; the sums keep
+  // their ascending-k order).
+  const int lo = tid & 31, hi = tid >> 5;
+  T ra[4], rb[4];
   if (use_r) {
+    auto fetch = [&](i64 k0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const i64 gi = i0 + lo, gk = k0 + hi + 8 * q;
+        ra[q] = (gi < rr && gk < rr) ? Lr[gk * rr + gi] : T(0);
+        const i64 gk2 = k0 + lo, gc = c0 + hi + 8 * q;
+        rb[q] = (gk2 < rr && gc < rc) ? Z[gc * rr + gk2] : T(0);
+      }
+    };
+    fetch(0);
     for (i64 k0 = 0; k0 < rr; k0 += kDK) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
-        const i64 gi = i0 + ii, gk = k0 + kk;
-        As[kk][ii] = (gi < rr && gk < rr) ? Lr[gk * rr + gi] : T(0);
-        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
-        const i64 gk2 = k0 + kk2, gc = c0 + cc;
-        Bs[kk2][cc] = (gk2 < rr && gc < rc) ? Z[gc * rr + gk2] : T(0);
+        As[hi + 8 * q][lo] = ra[q];
+        Bs[lo][hi + 8 * q] = rb[q];
       }
       __syncthreads();
+      if (k0 + kDK < rr) fetch(k0 + kDK);
 #pragma unroll 8
       for (int kk = 0; kk < kDK; ++kk) {
         const T a0 = As[kk][ty], a1 = As[kk][ty + 16];
@@ -56,17 +68,24 @@ __device__ __forceinline__ void dual_gemm_tile(const T* __restrict__ Lr, const T
     }
   }
   if (use_c) {
+    auto fetch = [&](i64 k0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const i64 gi = i0 + lo, gk = k0 + hi + 8 * q;
+        ra[q] = (gi < rr && gk < rc) ? Z[gk * rr + gi] : T(0);
+        const i64 gk2 = k0 + lo, gc = c0 + hi + 8 * q;
+        rb[q] = (gk2 < rc && gc < rc) ? Lc[gc * rc + gk2] : T(0);
+      }
+    };
+    fetch(0);
     for (i64 k0 = 0; k0 < rc; k0 += kDK) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int ii = tid & 31, kk = (tid >> 5) + 8 * q;
-        const i64 gi = i0 + ii, gk = k0 + kk;
-        As[kk][ii] = (gi < rr && gk < rc) ? Z[gk * rr + gi] : T(0);
-        const int kk2 = tid & 31, cc = (tid >> 5) + 8 * q;
-        const i64 gk2 = k0 + kk2, gc = c0 + cc;
-        Bs[kk2][cc] = (gk2 < rc && gc < rc) ? Lc[gc * rc + gk2] : T(0);
+        As[hi + 8 * q][lo] = ra[q];
+        Bs[lo][hi + 8 * q] = rb[q];
       }
       __syncthreads();
+      if (k0 + kDK < rc) fetch(k0 + kDK);
 #pragma unroll 8
       for (int kk = 0; kk < kDK; ++kk) {
         const T a0 = As[kk][ty], a1 = As[kk][ty + 16];
